@@ -1,0 +1,502 @@
+"""AdamW-GS optimizer-step benchmark (BASELINE.json metric).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+                    [--workload c3] [--mask bernoulli|coherent] [--vis P]
+
+A *step* is one pass of the hot path over one batch of synthetic input:
+visibility compaction (K1) + the fused AdamW-GS step (K2, with the per-step
+statistics) + the Re-State Regularization scatter on RSR boundaries (K3),
+exactly as ``run_training`` composes them (pipeline.py:316-370).
+
+Default workload (N=1): BASELINE.json configs[2] — 6M Gaussians, SH-3,
+30% i.i.d. visibility, full AdamW-GS (DAR lambda_o=1e-3, lambda_s=1e-5,
+N_I=1e6) with RSR (ratio 0.25, alpha 0.2/0.04, interval 100).  Multi-GPU
+runs shard rows by contiguous index; each rank owns the workload's N rows
+(weak scaling) and the per-step statistics are summed over ranks with one
+NCCL all-reduce.
+
+``value``  visible Gaussians updated / s, inputs resident in HBM, device time
+           (CUDA events on the launching stream, max over ranks).
+``e2e``    the same metric through the public API with host buffers: per
+           step the mask and dense gradients are copied H2D from pinned
+           memory and the step statistics are read back D2H.
+``roofline`` the fused step kernel (K2): algorithmic bytes per launch /
+           its CUDA-event duration vs the measured HBM copy peak.
+``cpu_baseline`` the reference algorithm (oracle float64 port of
+           optimizer.py:241-298) on a bounded sample, rank 0 at N=1.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+WORKLOADS = {
+    # name: (n rows per GPU, p_vis, mode, lambda_o, lambda_s, rsr, resets, description)
+    "c1": dict(n=100_000, p=0.5, mode="adamw-gs", lo=1e-3, ls=1e-5, rsr=False, reset=0.0,
+               desc="100k SH3 Gaussians, 50% visibility, adamw-gs (DAR)"),
+    "c2": dict(n=1_000_000, p=0.3, mode="sparse-adam", lo=0.01, ls=0.0, rsr=False, reset=0.0,
+               desc="1M SH3 Gaussians, 30% visibility, sparse Adam + coupled opacity decay 0.01"),
+    "c3": dict(n=6_000_000, p=0.3, mode="adamw-gs", lo=1e-3, ls=1e-5, rsr=True, reset=0.0,
+               desc="6M SH3 Gaussians, 30% visibility, adamw-gs DAR + RSR(0.25, a=0.2/0.04, "
+                    "every 100)"),
+    "c4": dict(n=3_000_000, p=0.3, mode="adamw-gs", lo=0.01, ls=0.01, rsr=True, reset=0.02,
+               desc="3M-cap MCMC cloud, 30% visibility, adamw-gs + RSR + 2% relocation resets "
+                    "every 100"),
+    "c5": dict(n=50_000_000, p=0.3, mode="adamw-gs", lo=1e-3, ls=1e-5, rsr=False, reset=0.0,
+               desc="50M SH3 Gaussians index-sharded, adamw-gs"),
+}
+RSR_INTERVAL = 100
+RSR_RATIO = 0.25
+ALPHA1, ALPHA2 = 0.2, 0.04
+FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c3", choices=sorted(WORKLOADS))
+    ap.add_argument("--mask", default="bernoulli", choices=["bernoulli", "coherent"])
+    ap.add_argument("--vis", type=float, default=None, help="override visibility fraction")
+    ap.add_argument("--n", type=int, default=None, help="override rows per GPU")
+    ap.add_argument("--strong", action="store_true", help="split --n across ranks (strong)")
+    ap.add_argument("--check", default="fused", choices=["fused", "strict"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--ref-seconds", type=float, default=150.0,
+                    help="budget of the whole --impl reference run")
+    ap.add_argument("--seed", type=int, default=0)
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------- helpers
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def measured_hbm_peak():
+    p = ROOT / "MEASURED_PEAKS.json"
+    try:
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def traffic_from_profiles(workload, mask, p_vis):
+    p = ROOT / "profiles" / "traffic.json"
+    try:
+        d = json.loads(p.read_text())
+        return d.get(f"{workload}/{mask}/{p_vis:g}")
+    except Exception:
+        return None
+
+
+REASON_BITS = {
+    0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+    0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+    0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.samples = []
+        self.proc = None
+        self.thread = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 3:
+                try:
+                    self.samples.append((float(parts[0]), float(parts[1]), int(parts[2], 16)))
+                except ValueError:
+                    pass
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        busy = [s for s in self.samples if not (s[2] & 0x1)] or self.samples
+        reasons = set()
+        for _, _, r in busy:
+            for bit, name in REASON_BITS.items():
+                if r & bit and name != "gpu_idle":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(s[0] for s in busy),
+                "sm_max_mhz": max(s[1] for s in busy), "reasons": sorted(reasons),
+                "samples": len(busy)}
+
+
+# ------------------------------------------------------------ CPU baseline
+def cpu_reference_rate(wl: dict, p_vis: float, mask: str, budget_s: float, steps=None, warmup=1,
+                       seed=0):
+    """Time the reference algorithm (float64 oracle port of dar_step /
+    sparse_adam_step, optimizer.py:231-298) on a bounded sample of the
+    workload: the same layout, distributions, visibility fraction and mode,
+    on fewer rows.  Returns (visible/s, sample description, per-step rows)."""
+    import numpy as np
+
+    from oracle import adamw_gs_oracle as O
+    from paper_2601_16736_b200 import synthetic as S
+
+    def run(n_rows, n_steps):
+        cfg = S.WorkloadConfig(n=n_rows, p_vis=p_vis, mask_family=mask, seed=seed)
+        lay = O.LAYOUT_SH3
+        host = S.make_params(cfg)
+        p = {k: v.astype(np.float64) for k, v in host.items()}
+        m = {g.name: np.zeros((n_rows, g.width)) for g in lay}
+        v = {g.name: np.zeros((n_rows, g.width)) for g in lay}
+        t = np.zeros(n_rows, np.int64)
+        hp = O.Hyper(lr=S.LR_SH3, lambda_o=wl["lo"], lambda_s=wl["ls"])
+        grad_sets = []
+        for s in range(min(n_steps, 3)):
+            vis = S.visibility(cfg, s)
+            grad_sets.append({k: x.astype(np.float64)
+                              for k, x in S.step_grads(cfg, s, vis).items()})
+        times, nv = [], []
+        for s in range(n_steps):
+            vis = S.visibility(cfg, s)
+            g = {k: x.copy() for k, x in grad_sets[s % len(grad_sets)].items()}
+            t0 = time.perf_counter()
+            if wl["mode"] == "adamw-gs":
+                O.dar_step_f64(lay, p, g, m, v, t, vis, hp, cfg.n_pixels)
+            else:
+                reg = O.coupled_reg_grad_f64(lay, p, vis, wl["lo"], wl["ls"])
+                for k, r in reg.items():
+                    g[k] = g[k] + r
+                O.sparse_adam_step_f64(lay, p, g, m, v, t, vis, hp)
+            times.append(time.perf_counter() - t0)
+            nv.append(int(vis.sum()))
+        return times, nv
+
+    # calibrate on a small sample, then size the sample to the budget
+    n0 = 20_000
+    tt, nv = run(n0, 2)
+    rate = nv[-1] / max(tt[-1], 1e-9)
+    n_steps = steps if steps is not None else 4
+    rows = int(min(wl["n"], max(n0, rate * budget_s / max(n_steps + warmup, 1) / p_vis)))
+    tt, nv = run(rows, n_steps + warmup)
+    tt, nv = tt[warmup:], nv[warmup:]
+    value = sum(nv) / sum(tt)
+    sample = (f"{rows} of {wl['n']} rows, {n_steps} timed steps after {warmup} warm-up, float64 "
+              f"NumPy port of the reference step (oracle/adamw_gs_oracle.py), 1 thread")
+    return value, sample, rows, tt
+
+
+def reference_arm(args, wl, p_vis):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    budget = args.ref_seconds
+    import numpy as np  # noqa: F401
+    value, sample, rows, tt = cpu_reference_rate(
+        wl, p_vis, args.mask, budget_s=budget * 0.8, steps=args.steps, warmup=args.warmup,
+        seed=args.seed)
+    cores = 1
+    line = {
+        "metric": "visible Gaussians updated/sec per optimizer step",
+        "value": value, "unit": "visible Gaussians/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1000.0 * statistics.mean(tt),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "impl": "reference",
+        "config": workload_config(args, wl, p_vis, world),
+        "cpu_baseline": {"value": value, "unit": "visible Gaussians/s", "cores": cores,
+                         "kind": "port", "sample": sample,
+                         "host_cpus": os.cpu_count(),
+                         "affinity_cpus": len(os.sched_getaffinity(0))},
+        "e2e": {"value": value, "unit": "visible Gaussians/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(args, wl, p_vis, world):
+    n = args.n if args.n is not None else wl["n"]
+    return {"workload": f"{args.workload}: {wl['desc']}", "n_per_gpu": n // world if args.strong
+            else n, "n_total": n if args.strong else n * world, "p_visible": p_vis,
+            "mask": args.mask, "mode": wl["mode"], "layout": "SH3 (59 fp32 / Gaussian)",
+            "lambda_o": wl["lo"], "lambda_s": wl["ls"], "n_pixels": 1_000_000,
+            "rsr": {"ratio": RSR_RATIO, "alpha1": ALPHA1, "alpha2": ALPHA2,
+                    "interval": RSR_INTERVAL} if wl["rsr"] else None,
+            "reset_fraction": wl["reset"] or None, "check": args.check,
+            "l2": "inputs larger than L2 (working set >> 126 MB)" if n >= 1_000_000 else
+                  "L2 flushed between timed steps",
+            "parallelism": f"index-sharded x{world}"}
+
+
+# --------------------------------------------------------------- our arm
+def ours(args, wl, p_vis):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2601_16736_b200 import synthetic as S
+    from paper_2601_16736_b200.optimizer import AdamWGS
+    from paper_2601_16736_b200.sampling import StSSchedule, shard_rows, stream, stss_sample
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    n_total = args.n if args.n is not None else wl["n"]
+    n = n_total // world if args.strong else n_total
+    base = rank * n
+    cfg = S.WorkloadConfig(n=n, p_vis=p_vis, mask_family=args.mask, seed=args.seed * 1000 + rank,
+                           lambda_o=wl["lo"], lambda_s=wl["ls"])
+    params = S.make_params_device(cfg, dev)
+    opt = AdamWGS(S.param_groups(params), mode=wl["mode"], lambda_o=wl["lo"], lambda_s=wl["ls"],
+                  check=args.check, errors="defer")
+    total_steps = args.warmup + args.steps
+    masks = [S.visibility_device(cfg, s, dev) for s in range(total_steps)]
+    n_vis = torch.stack([m.sum() for m in masks]).cpu().numpy().astype(np.int64)
+    grad_sets = [S.grads_device(cfg, s, dev) for s in range(2)]
+    # RSR / relocation samples are host-drawn with the reference RNG contract
+    # (optimizer.py:379-386, rng.py:17-30) and uploaded before timing.
+    events = {}
+    sched = StSSchedule(milestones=((0, RSR_RATIO),), interval=RSR_INTERVAL)
+    n_global = n * world
+    for it in range(total_steps):
+        boundary = it + 1
+        if boundary % RSR_INTERVAL:
+            continue
+        ev = {}
+        if wl["rsr"]:
+            picked = stss_sample(sched, boundary, n_global, stream(args.seed, "stss", boundary))
+            ev["rsr"] = torch.from_numpy(shard_rows(picked, base, base + n).astype(np.int32)).to(dev)
+        if wl["reset"]:
+            rng = stream(args.seed, "relocate", boundary)
+            k = int(wl["reset"] * n_global)
+            dead = np.sort(rng.choice(n_global, k, replace=False))
+            ev["reset"] = torch.from_numpy(shard_rows(dead, base, base + n).astype(np.int32)).to(dev)
+        events[it] = ev
+    stats_sum = torch.zeros(10, dtype=torch.float64, device=dev)
+    launches = [0]
+
+    k2_events = []
+
+    def one_step(it, timed):
+        g = grad_sets[it % 2]
+        if timed:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        eng = opt.engine
+        # K1 + K2 through the optimizer, K2 bracketed by events
+        rows, count = eng.compact(masks[it])
+        if timed:
+            e0.record()
+        _step_k2(opt, g, rows, count, wl)
+        if timed:
+            e1.record()
+            k2_events.append((e0, e1))
+        launches[0] += 2 + (1 if args.check == "strict" else 0)
+        ev = events.get(it)
+        if ev:
+            if "rsr" in ev:
+                opt.rsr_apply(ev["rsr"], ALPHA1, ALPHA2)
+                launches[0] += 1
+            if "reset" in ev:
+                opt.reset_rows(ev["reset"])
+                launches[0] += 1
+        if world > 1:
+            stats_sum.copy_(opt.engine.stats)
+            dist.all_reduce(stats_sum)
+
+    for it in range(args.warmup):
+        one_step(it, False)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches[0] = 0
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        start.record()
+        for it in range(args.warmup, total_steps):
+            one_step(it, True)
+        end.record()
+        torch.cuda.synchronize()
+    ms = start.elapsed_time(end)
+    k2_ms = [a.elapsed_time(b) for a, b in k2_events]
+    opt.check_errors()
+    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    vis_t = torch.tensor([float(n_vis[args.warmup:].sum())], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(vis_t)
+    ms_max = float(ms_t.item())
+    total_visible = float(vis_t.item())
+    value = total_visible / (ms_max / 1000.0)
+
+    # roofline of K2 (this rank's launches)
+    width = S.SH3_WIDTH
+    k2_bytes = [int(nv) * (28 * width + 12) for nv in n_vis[args.warmup:]]
+    k2_avg_ms = statistics.mean(k2_ms)
+    achieved = (sum(k2_bytes) / len(k2_bytes)) / (k2_avg_ms / 1000.0) / 1e9
+    peak, peak_src = measured_hbm_peak()
+    step_bytes = [S.algorithmic_bytes(n, int(nv)) for nv in n_vis[args.warmup:]]
+    step_gbs = sum(step_bytes) / (ms / 1000.0) / 1e9
+
+    # e2e through the public API with host buffers (rank-local, then max)
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, opt, cfg, dev, world, masks, n_vis)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        v, sample, _, _ = cpu_reference_rate(wl, p_vis, args.mask, budget_s=args.cpu_seconds,
+                                              seed=args.seed)
+        cpu = {"value": v, "unit": "visible Gaussians/s", "cores": 1, "kind": "port",
+               "sample": sample, "host_cpus": os.cpu_count()}
+
+    if rank == 0:
+        line = {
+            "metric": "visible Gaussians updated/sec per optimizer step",
+            "value": value, "unit": "visible Gaussians/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "strong" if args.strong else "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded Gaussian cloud, SURVEY §8(d) distributions)",
+            "config": workload_config(args, wl, p_vis, world),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak,
+                         "traffic": traffic_from_profiles(args.workload, args.mask, p_vis),
+                         "kernel": "gs::step_kernel (K2)", "peak_source": peak_src,
+                         "k2_ms_avg": k2_avg_ms,
+                         "k2_bytes_per_launch": sum(k2_bytes) / len(k2_bytes),
+                         "bytes_per_visible": 28 * width + 12,
+                         "step_gbs_algorithmic": step_gbs,
+                         "step_frac": step_gbs / peak},
+            "e2e": e2e, "gpu_launches": launches[0], "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+            "visible_per_step": float(n_vis[args.warmup:].mean()),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def _step_k2(opt, grads, rows, count, wl):
+    """The optimizer's K2 launch for an already-compacted index list
+    (AdamWGS.step does K1 + K2; the bench splits them to time K2 alone)."""
+    b = opt._bindings(grads)
+    eng = opt.engine
+    from paper_2601_16736_b200.engine import round_pixel_count
+    if wl["mode"] == "adamw-gs":
+        eng.step(b, "adamw-gs", opt.state.clock, rows=rows, count=count, eps=opt.eps,
+                 lambda_opacity=wl["lo"], lambda_scale=wl["ls"], clip_opacity=opt.ct_opacity,
+                 clip_scale=opt.ct_scale, n_pixels_rounded=round_pixel_count(1_000_000),
+                 check=opt.check)
+    else:
+        eng.step(b, wl["mode"], opt.state.clock, rows=rows, count=count, eps=opt.eps,
+                 lambda_opacity=wl["lo"], lambda_scale=wl["ls"], n_visible_dev=count,
+                 check=opt.check)
+    opt._last_ctx = (b, rows, count, wl["lo"], wl["ls"], wl["mode"])
+    opt._after_step(eng.stats)
+
+
+def run_e2e(args, opt, cfg, dev, world, masks, n_vis):
+    """Public-API step with host buffers: H2D mask + gradients from pinned
+    memory, opt.step(), D2H of the step statistics, every step."""
+    import torch
+    import torch.distributed as dist
+
+    host_grads = {k: torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+                  for k, t in opt_grads_like(opt).items()}
+    dev_grads = {k: torch.empty_like(t) for k, t in opt_grads_like(opt).items()}
+    for k, t in host_grads.items():
+        t.copy_(torch.randn(t.shape) * 1e-4)
+    host_mask = torch.empty(masks[0].shape, dtype=torch.bool, pin_memory=True)
+    host_mask.copy_(masks[0].cpu())
+    dev_mask = torch.empty_like(masks[0])
+    stats_host = torch.empty(10, dtype=torch.float64, pin_memory=True)
+    h2d = host_mask.numel() + sum(t.numel() * 4 for t in host_grads.values())
+    d2h = stats_host.numel() * 8
+    nv = float(host_mask.sum())
+
+    def one():
+        dev_mask.copy_(host_mask, non_blocking=True)
+        for k in dev_grads:
+            dev_grads[k].copy_(host_grads[k], non_blocking=True)
+        opt.step(dev_mask, 1_000_000, grads=dev_grads)
+        stats_host.copy_(opt.engine.stats, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+
+    for _ in range(2):
+        one()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        one()
+    ms = (time.perf_counter() - t0) * 1000.0 / args.e2e_steps
+    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms = float(ms_t.item())
+    return {"value": nv * world / (ms / 1000.0), "unit": "visible Gaussians/s",
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": ms,
+            "steps": args.e2e_steps, "timing": "host wall clock around H2D + step + D2H + sync"}
+
+
+def opt_grads_like(opt):
+    return {g["name"]: g["params"][0] for g in opt.param_groups}
+
+
+def main():
+    args = parse()
+    wl = dict(WORKLOADS[args.workload])
+    if args.n is not None:
+        wl["n"] = args.n
+    p_vis = args.vis if args.vis is not None else wl["p"]
+    if args.impl == "reference":
+        reference_arm(args, wl, p_vis)
+        return
+    ours(args, wl, p_vis)
+
+
+if __name__ == "__main__":
+    main()

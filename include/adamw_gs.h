@@ -1,0 +1,168 @@
+/*
+ * adamw_gs.h — C ABI of the B200-native AdamW-GS optimizer step.
+ *
+ * Drop-in boundary for the reference optimizer's step family
+ * (/root/reference/pkg/src/splatlab/optimizer.py).  Every entry point is
+ * stream-ordered, never allocates, never synchronises the host, and takes
+ * plain device pointers + sizes.  Buffers belong to the caller.
+ *
+ * Status: every function returns GS_OK (0) or a negative GS_ERR_* code;
+ * gs_last_error() describes the last failure of the calling thread.
+ * Data errors (non-finite gradients, tau/kappa outside the activation
+ * domain) are not status codes: they are counted in the step statistics
+ * (fused check) or raised in a device flag (strict check), so the host can
+ * raise GradientError / DomainError without a per-step sync.
+ *
+ * Reference interface each entry point replaces (file:line under
+ * /root/reference/pkg/src/splatlab/):
+ *   gs_compact_u8 / gs_compact_i32  np.flatnonzero(vis)            optimizer.py:235,249
+ *   gs_step                         adam_step_sync / sparse_adam_step /
+ *                                   dar_step (_decoupled_reg_step) /
+ *                                   adamw_const_step (+ coupled_reg_grad
+ *                                   folded in for the coupled modes)
+ *                                   optimizer.py:222-324, loss.py:177-198
+ *   gs_check_grads                  ParamGrads.finite_check / _check_grads
+ *                                   gradients.py:50-58, optimizer.py:181-184
+ *   gs_rsr_apply                    rsr_apply                       optimizer.py:327-340
+ *   gs_reset_rows                   reset_rows                      optimizer.py:159-165
+ *   gs_stats_all                    classify_active + moment_stats  primitives.py:228-238,
+ *                                                                   optimizer.py:489-506
+ */
+#ifndef ADAMW_GS_H
+#define ADAMW_GS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GS_ABI_VERSION 1
+#define GS_MAX_GROUPS 8
+
+/* status codes */
+#define GS_OK 0
+#define GS_ERR_ARG (-1)
+#define GS_ERR_LAUNCH (-2)
+#define GS_ERR_WORKSPACE (-3)
+#define GS_ERR_ALIGN (-4)
+
+/* attribute-group roles (optimizer.py:217,259-263) */
+#define GS_ROLE_PLAIN 0
+#define GS_ROLE_POSITION 1 /* takes mu_lr_scale (already folded into lr) */
+#define GS_ROLE_OPACITY 2  /* tau: sigma'(tau) penalty */
+#define GS_ROLE_SCALE 3    /* kappa: exp(kappa) penalty, kappa <= 80 */
+
+/* step modes (optimizer.py:55 MODES) */
+#define GS_MODE_COUPLED_ADAM 0     /* dense sync Adam, global clock (+ coupled reg) */
+#define GS_MODE_SPARSE_ADAM 1      /* masked Adam (+ coupled reg / N_v) */
+#define GS_MODE_ADAMW_CONST 2      /* decoupled + lambda*R'(theta) */
+#define GS_MODE_ADAMW_CONST_CLIP 3 /* decoupled + min(lambda*R'(theta), clip) */
+#define GS_MODE_ADAMW_GS 4         /* decoupled + DAR min(lambda*(R'/N_I')/(sqrt(v^)+eps), C_t) */
+
+/* error-check policies */
+#define GS_CHECK_FUSED 0  /* rows with bad gradients / domain are skipped and counted */
+#define GS_CHECK_STRICT 1 /* step is a no-op when *abort_flag != 0 (from gs_check_grads) */
+
+/* indices of the per-step statistics written by gs_step (doubles) */
+#define GS_STAT_N_VISIBLE 0      /* rows in the index list */
+#define GS_STAT_N_STEPPED 1      /* rows updated */
+#define GS_STAT_N_BAD_GRAD 2     /* rows skipped: non-finite gradient */
+#define GS_STAT_N_BAD_DOMAIN 3   /* rows skipped: tau non-finite / kappa > 80 */
+#define GS_STAT_N_ACTIVE_PRE 4   /* stepped rows with sigma(tau) > 1/255 before */
+#define GS_STAT_N_ACTIVE_POST 5  /* ... after */
+#define GS_STAT_N_CLIP_OPACITY 6 /* opacity penalty terms that hit C_t / clip */
+#define GS_STAT_N_CLIP_SCALE 7   /* scale penalty terms that hit C_t / clip */
+#define GS_STAT_SUM_EXTRA_OPACITY 8
+#define GS_STAT_SUM_EXTRA_SCALE 9
+#define GS_STEP_STATS 10
+
+/* One attribute group: row-major [n_rows, width] fp32, contiguous rows. */
+typedef struct gs_group {
+  float* param;
+  const float* grad;
+  float* exp_avg;    /* first moment m  */
+  float* exp_avg_sq; /* second moment v */
+  int64_t width;
+  int32_t role; /* GS_ROLE_* */
+  float lr;     /* effective learning rate of this step */
+} gs_group;
+
+typedef struct gs_step_cfg {
+  int32_t mode;  /* GS_MODE_* */
+  int32_t check; /* GS_CHECK_* */
+  float one_minus_beta1;
+  float one_minus_beta2;
+  float eps;
+  float active_logit; /* tau > active_logit  <=>  sigmoid(tau) > 1/255 (f64) */
+  double lambda_opacity; /* DAR / const / coupled lambda for the opacity group */
+  double lambda_scale;
+  double clip_opacity; /* C_t (adamw-gs) or clip (adamw-const-clip) */
+  double clip_scale;
+  double n_pixels_rounded; /* N_I' (optimizer.py:168-178), adamw-gs only */
+  const float* bias_lut;   /* device float2 per clock t: 1/(1-b1^t), 1/(1-b2^t) */
+  int32_t lut_len;
+  int32_t global_t;     /* coupled-adam: the incremented global clock */
+  double beta1, beta2;  /* bias correction beyond the LUT */
+  const int32_t* n_visible_norm; /* device N_v for the coupled modes (may be NULL) */
+  double n_visible_host;         /* used when n_visible_norm == NULL */
+  const int32_t* abort_flag;    /* strict mode: device flag written by gs_check_grads */
+} gs_step_cfg;
+
+int32_t gs_abi_version(void);
+const char* gs_last_error(void);
+int32_t gs_device_sm_count(void);
+
+/* K1 — visibility compaction: ascending int32 indices of nonzero mask bytes
+ * (or radii > 0), count written to *count_out (device).  Bit-exact with
+ * np.flatnonzero.  ws: gs_compact_workspace_bytes(n) bytes, zero-filled once
+ * at allocation and then reused untouched between calls (single-pass
+ * decoupled look-back with epoch-tagged tile status; graph-capturable). */
+size_t gs_compact_workspace_bytes(int64_t n);
+int gs_compact_u8(const uint8_t* mask, int64_t n, int32_t* idx_out, int32_t* count_out,
+                  void* ws, size_t ws_bytes, void* stream);
+int gs_compact_i32(const int32_t* radii, int64_t n, int32_t* idx_out, int32_t* count_out,
+                   void* ws, size_t ws_bytes, void* stream);
+
+/* K2 — the fused step over the rows listed in rows[0 .. *n_rows_dev) (or all
+ * max_rows rows in coupled-adam mode, rows == NULL).  clock: int32 per row.
+ * stats_out: GS_STEP_STATS doubles (overwritten).  ws: gs_step_workspace_bytes(),
+ * zero-filled once at allocation. */
+size_t gs_step_workspace_bytes(void);
+int gs_step(const gs_group* groups, int32_t n_groups, const gs_step_cfg* cfg,
+            const int32_t* rows, const int32_t* n_rows_dev, int64_t max_rows,
+            int32_t* clock, double* stats_out, void* ws, size_t ws_bytes, void* stream);
+
+/* Strict pre-check: non-finite gradients over ALL n_rows rows (bit 0), and
+ * over the listed visible rows rows[0 .. *n_list_dev) tau non-finite when
+ * lambda_opacity != 0 or kappa non-finite / > 80 when lambda_scale != 0
+ * (bit 1).  *abort_flag is reset then OR-ed; bad_rows_out (nullable, 4-byte
+ * aligned, n_rows bytes) gets the per-row bits.  rows may be NULL (no domain
+ * check). */
+int gs_check_grads(const gs_group* groups, int32_t n_groups, int64_t n_rows,
+                   const int32_t* rows, const int32_t* n_list_dev, double lambda_opacity,
+                   double lambda_scale, uint8_t* bad_rows_out, int32_t* abort_flag,
+                   void* stream);
+
+/* K3 — re-state regularisation m *= alpha1, v *= alpha2 on the k rows
+ * (clock untouched), and relocation resets m = v = 0, clock = 0. */
+int gs_rsr_apply(const gs_group* groups, int32_t n_groups, const int32_t* rows, int64_t k,
+                 double alpha1, double alpha2, void* stream);
+int gs_reset_rows(const gs_group* groups, int32_t n_groups, int32_t* clock,
+                  const int32_t* rows, int64_t k, void* stream);
+
+/* K4 — all-row statistics.  out (device doubles, 2 + 5*n_groups):
+ *   [0] n_alive, [1] n_active (opacity group tau > active_logit, alive rows),
+ *   then per group g at 2+5g: sum sqrt(v), max sqrt(v), n(v>0),
+ *   sum |m|/sqrt(v) over v>0, max |m|/sqrt(v).
+ * alive may be NULL (all rows alive).  ws: gs_stats_workspace_bytes(). */
+size_t gs_stats_workspace_bytes(int32_t n_groups);
+int gs_stats_all(const gs_group* groups, int32_t n_groups, int64_t n_rows,
+                 const uint8_t* alive, float active_logit, double* out, void* ws,
+                 size_t ws_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ADAMW_GS_H */

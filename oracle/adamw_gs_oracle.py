@@ -1,0 +1,550 @@
+"""CPU oracle for the AdamW-GS optimizer step — TEST INFRASTRUCTURE ONLY.
+
+Not part of the product: only ``tests/``, ``__graft_entry__.smoke()`` and
+``bench.py``'s CPU legs may import this module (see ``oracle/__init__.py``).
+
+Two restatements of the reference step, both over an arbitrary ordered
+group layout (the reference's 2D ``mu/kappa/rot/tau/color`` testbed or the
+3DGS SH-3 ``xyz/f_dc/f_rest/opacity/scaling/rotation`` layout):
+
+``*_f64``
+    The reference algorithm of ``/root/reference/pkg/src/splatlab/optimizer.py``
+    restated in NumPy float64 with the reference's own association order, so
+    that it reproduces the reference bit for bit.  Pinned against golden
+    vectors written by the UNMODIFIED reference (``tests/golden/make_golden.py``
+    imports ``splatlab`` and drives it through the SH-3 adapter of SURVEY §8(c)).
+
+``step_fp32``
+    The exact fp32 operation order of the CUDA kernel
+    (``paper_2601_16736_b200/csrc/gs_step.cu``): every fp32 op correctly
+    rounded, no FMA contraction, transcendental / DAR terms in float64 rounded
+    once.  The GPU path must agree with it elementwise (bit-exact up to the
+    last-ulp behaviour of ``exp`` in float64).
+
+Every function cites the reference file:line it follows.  Rows are 2-D
+``(N, W)`` arrays for every group (width-1 groups are ``(N, 1)``).
+"""
+
+from __future__ import annotations
+
+import hashlib
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+F32 = np.float32
+F64 = np.float64
+
+MODES = ("coupled-adam", "sparse-adam", "adamw-const", "adamw-const-clip", "adamw-gs")
+ACTIVE_OPACITY_THRESHOLD = 1.0 / 255.0          # primitives.py:33
+MAX_LOG_SCALE = 80.0                            # primitives.py:37
+
+
+class OracleDomainError(ValueError):
+    """primitives.py:40 DomainError."""
+
+
+class OracleGradientError(RuntimeError):
+    """optimizer.py:62-67 GradientError (carries ``ids``)."""
+
+    def __init__(self, ids):
+        self.ids = np.asarray(ids)
+        super().__init__(f"non-finite gradient on primitives {self.ids.tolist()[:16]}")
+
+
+class OracleConfigError(ValueError):
+    """optimizer.py:58 ConfigError."""
+
+
+@dataclass(frozen=True)
+class Group:
+    """One attribute group: name, row width and role.
+
+    ``role`` is ``"position"`` (takes ``mu_lr_scale``, optimizer.py:217,263),
+    ``"opacity"`` (tau DAR, optimizer.py:259-260), ``"scale"`` (kappa DAR,
+    optimizer.py:261-262) or ``"plain"``.
+    """
+
+    name: str
+    width: int
+    role: str = "plain"
+
+
+LAYOUT_REF2D = (Group("mu", 2, "position"), Group("kappa", 2, "scale"), Group("rot", 1),
+                Group("tau", 1, "opacity"), Group("color", 3))          # gradients.py:15
+LAYOUT_SH3 = (Group("xyz", 3, "position"), Group("f_dc", 3), Group("f_rest", 45),
+              Group("opacity", 1, "opacity"), Group("scaling", 3, "scale"), Group("rotation", 4))
+
+
+@dataclass
+class Hyper:
+    """The OptimizerConfig fields the step reads (optimizer.py:70-100)."""
+
+    lr: dict
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps: float = 1e-8
+    lambda_o: float = 0.0
+    lambda_s: float = 0.0
+    ct_opacity: float = 10.0
+    ct_scale: float = 10.0
+    round_n_pixels: bool = True
+
+
+# --------------------------------------------------------------------------
+# scalar helpers
+# --------------------------------------------------------------------------
+
+def round_pixel_count(n_pixels: int, enabled: bool = True) -> float:
+    """optimizer.py:168-178 — keep the leading digit of N_I, divide by ten."""
+    if n_pixels <= 0:
+        raise OracleConfigError("pixel count must be positive")
+    if not enabled:
+        return float(n_pixels)
+    p = 10 ** math.floor(math.log10(n_pixels))
+    return (n_pixels // p) * p / 10.0
+
+
+def _finite_or_raise(name, x):
+    a = np.asarray(x, dtype=F64)
+    if not np.all(np.isfinite(a)):
+        raise OracleDomainError(f"{name} must be finite")
+    return a
+
+
+def sigmoid_f64(tau):
+    """primitives.py:51-59 — stable two-branch sigmoid in float64."""
+    t = _finite_or_raise("tau", tau)
+    out = np.empty_like(t)
+    pos = t >= 0
+    out[pos] = 1.0 / (1.0 + np.exp(-t[pos]))
+    e = np.exp(t[~pos])
+    out[~pos] = e / (1.0 + e)
+    return out
+
+
+def opacity_derivative_f64(tau):
+    """primitives.py:62-66 — sigma * (1 - sigma)."""
+    o = sigmoid_f64(tau)
+    return o * (1.0 - o)
+
+
+def activate_scale_f64(kappa):
+    """primitives.py:78-84 — exp with the kappa > 80 guard."""
+    k = _finite_or_raise("kappa", kappa)
+    if np.any(k > MAX_LOG_SCALE):
+        raise OracleDomainError(f"log-scale above {MAX_LOG_SCALE} would overflow")
+    return np.exp(k)
+
+
+def active_logit_threshold_f32() -> np.float32:
+    """Largest fp32 tau with sigmoid_f64(tau) <= 1/255.
+
+    ``classify_active`` (primitives.py:228-238) tests ``sigmoid(tau) > 1/255``
+    in float64; on fp32 inputs that is exactly ``tau > T`` for this T because
+    the float64 sigmoid is monotone at fp32 spacing near the threshold.
+    """
+    t = F32(math.log(ACTIVE_OPACITY_THRESHOLD / (1.0 - ACTIVE_OPACITY_THRESHOLD)))
+    for _ in range(64):
+        if sigmoid_f64(np.array([t], F64))[0] > ACTIVE_OPACITY_THRESHOLD:
+            t = np.nextafter(t, F32(-np.inf))
+        else:
+            break
+    while sigmoid_f64(np.array([np.nextafter(t, F32(np.inf))], F64))[0] <= ACTIVE_OPACITY_THRESHOLD:
+        t = np.nextafter(t, F32(np.inf))
+    return F32(t)
+
+
+def bias_lut_f32(beta1: float, beta2: float, t_max: int) -> np.ndarray:
+    """fp32 bias-correction factors 1/(1-beta^t), t in [0, t_max], from float64.
+
+    The denominators are the reference's ``1 - np.power(beta, t)``
+    (optimizer.py:202-203); entry 0 is unused (set to 1).
+    """
+    t = np.arange(t_max + 1, dtype=F64)
+    with np.errstate(divide="ignore"):
+        c1 = 1.0 / (1.0 - np.power(beta1, t))
+        c2 = 1.0 / (1.0 - np.power(beta2, t))
+    c1[0] = c2[0] = 1.0
+    return np.stack([c1.astype(F32), c2.astype(F32)], axis=1)
+
+
+# --------------------------------------------------------------------------
+# float64 restatement of the reference (bit-exact with splatlab)
+# --------------------------------------------------------------------------
+
+def finite_check_f64(layout, grads):
+    """gradients.py:50-58 — ids of rows with any non-finite gradient, or None."""
+    n = grads[layout[0].name].shape[0]
+    bad = np.zeros(n, dtype=bool)
+    for g in layout:
+        bad |= ~np.isfinite(grads[g.name]).all(axis=1)
+    ids = np.flatnonzero(bad)
+    return ids if ids.size else None
+
+
+def _corrected_f64(m, v, t_rows, beta1, beta2, global_t=None):
+    """optimizer.py:187-204 — bias correction with per-row (async) or global clock."""
+    if global_t is not None:
+        t = float(global_t)
+    else:
+        t = t_rows.astype(F64)[:, None]
+    return m / (1.0 - np.power(beta1, t)), v / (1.0 - np.power(beta2, t))
+
+
+def _lr_of(g: Group, hp: Hyper, mu_lr_scale: float) -> float:
+    """optimizer.py:217,263 — per-group lr, position group scaled."""
+    return hp.lr[g.name] * (mu_lr_scale if g.role == "position" else 1.0)
+
+
+def _update_rows_f64(layout, params, grads, m, v, t, rows, hp, mu_lr_scale, global_t=None):
+    """optimizer.py:207-219 — plain Adam on selected rows (association lr*m_hat/(...))."""
+    t[rows] += 1                       # one clock for all groups
+    for g in layout:
+        gr = grads[g.name][rows]
+        m[g.name][rows] = hp.beta1 * m[g.name][rows] + (1.0 - hp.beta1) * gr
+        v[g.name][rows] = hp.beta2 * v[g.name][rows] + (1.0 - hp.beta2) * (gr * gr)
+        mh, vh = _corrected_f64(m[g.name][rows], v[g.name][rows], t[rows], hp.beta1, hp.beta2,
+                                global_t)
+        lr = _lr_of(g, hp, mu_lr_scale)
+        params[g.name][rows] = params[g.name][rows] - lr * mh / (np.sqrt(vh) + hp.eps)
+
+
+def adam_step_sync_f64(layout, params, grads, m, v, t, state_global_t, hp, mu_lr_scale=1.0):
+    """optimizer.py:222-228.  Returns the new global_t."""
+    ids = finite_check_f64(layout, grads)
+    if ids is not None:
+        raise OracleGradientError(ids)
+    gt = state_global_t + 1
+    _update_rows_f64(layout, params, grads, m, v, t, slice(None), hp, mu_lr_scale, gt)
+    return gt
+
+
+def sparse_adam_step_f64(layout, params, grads, m, v, t, vis, hp, mu_lr_scale=1.0):
+    """optimizer.py:231-238."""
+    ids = finite_check_f64(layout, grads)
+    if ids is not None:
+        raise OracleGradientError(ids)
+    rows = np.flatnonzero(np.asarray(vis, dtype=bool))
+    if rows.size:
+        _update_rows_f64(layout, params, grads, m, v, t, rows, hp, mu_lr_scale)
+
+
+def _decoupled_reg_step_f64(layout, params, grads, m, v, t, vis, hp, mu_lr_scale,
+                            extra_opacity, extra_scale):
+    """optimizer.py:241-266 (association lr*(m_hat/(...) + extra))."""
+    ids = finite_check_f64(layout, grads)
+    if ids is not None:
+        raise OracleGradientError(ids)
+    rows = np.flatnonzero(np.asarray(vis, dtype=bool))
+    if rows.size == 0:
+        return
+    t[rows] += 1
+    for g in layout:
+        gr = grads[g.name][rows]
+        m[g.name][rows] = hp.beta1 * m[g.name][rows] + (1.0 - hp.beta1) * gr
+        v[g.name][rows] = hp.beta2 * v[g.name][rows] + (1.0 - hp.beta2) * (gr * gr)
+        mh, vh = _corrected_f64(m[g.name][rows], v[g.name][rows], t[rows], hp.beta1, hp.beta2)
+        step = mh / (np.sqrt(vh) + hp.eps)
+        if g.role == "opacity" and extra_opacity is not None:
+            step = step + extra_opacity(params[g.name][rows], vh)
+        elif g.role == "scale" and extra_scale is not None:
+            step = step + extra_scale(params[g.name][rows], vh)
+        lr = _lr_of(g, hp, mu_lr_scale)
+        params[g.name][rows] = params[g.name][rows] - lr * step
+
+
+def dar_step_f64(layout, params, grads, m, v, t, vis, hp, n_pixels, mu_lr_scale=1.0,
+                 lambda_o=None, lambda_s=None):
+    """optimizer.py:269-298 — DAR: min(lambda*(R'/N_I')/(sqrt(v_hat)+eps), C_t)."""
+    lo = hp.lambda_o if lambda_o is None else lambda_o
+    ls = hp.lambda_s if lambda_s is None else lambda_s
+    if hp.ct_opacity <= 0.0 or hp.ct_scale <= 0.0:
+        raise OracleConfigError("clip bounds C_t must be positive")
+    n_i = round_pixel_count(n_pixels, hp.round_n_pixels)
+
+    def extra_tau(tau, vh):
+        if lo == 0.0:
+            return 0.0
+        reg = opacity_derivative_f64(tau) / n_i
+        return np.minimum(lo * reg / (np.sqrt(vh) + hp.eps), hp.ct_opacity)
+
+    def extra_kappa(kappa, vh):
+        if ls == 0.0:
+            return 0.0
+        reg = activate_scale_f64(kappa) / n_i
+        return np.minimum(ls * reg / (np.sqrt(vh) + hp.eps), hp.ct_scale)
+
+    _decoupled_reg_step_f64(layout, params, grads, m, v, t, vis, hp, mu_lr_scale,
+                            extra_tau, extra_kappa)
+
+
+def adamw_const_step_f64(layout, params, grads, m, v, t, vis, hp, clip=None, mu_lr_scale=1.0):
+    """optimizer.py:301-324 — constant penalty lambda*R'(theta), optional clamp."""
+
+    def extra_tau(tau, vh):
+        if hp.lambda_o == 0.0:
+            return 0.0
+        term = hp.lambda_o * opacity_derivative_f64(tau)
+        return np.minimum(term, clip) if clip is not None else term
+
+    def extra_kappa(kappa, vh):
+        if hp.lambda_s == 0.0:
+            return 0.0
+        term = hp.lambda_s * activate_scale_f64(kappa)
+        return np.minimum(term, clip) if clip is not None else term
+
+    _decoupled_reg_step_f64(layout, params, grads, m, v, t, vis, hp, mu_lr_scale,
+                            extra_tau, extra_kappa)
+
+
+def coupled_reg_grad_f64(layout, params, vis, lambda_o, lambda_s, alive=None, apply_to_all=False):
+    """loss.py:177-198 — coupled L1 gradients lambda*R'(theta)/N_v.
+
+    Returns ``{group_name: grad}`` for the opacity and scale groups.
+    """
+    n = params[layout[0].name].shape[0]
+    out = {g.name: np.zeros((n, g.width)) for g in layout if g.role in ("opacity", "scale")}
+    n_vis = int(np.asarray(vis).sum())
+    if n_vis == 0 or (lambda_o == 0.0 and lambda_s == 0.0):
+        return out
+    if apply_to_all:
+        rows = np.ones(n, bool) if alive is None else np.asarray(alive, bool)
+    else:
+        rows = np.asarray(vis, dtype=bool)
+    for g in layout:
+        if g.role == "opacity" and lambda_o != 0.0:
+            out[g.name][rows] = lambda_o * opacity_derivative_f64(params[g.name][rows]) / n_vis
+        elif g.role == "scale" and lambda_s != 0.0:
+            out[g.name][rows] = lambda_s * activate_scale_f64(params[g.name][rows]) / n_vis
+    return out
+
+
+def rsr_apply_f64(layout, m, v, indices, alpha1, alpha2):
+    """optimizer.py:327-340 — m *= alpha1, v *= alpha2 on the rows; clock untouched."""
+    if not (0.0 <= alpha1 < 1.0 and 0.0 <= alpha2 < 1.0):
+        raise OracleConfigError("RSR factors must lie in [0, 1)")
+    for g in layout:
+        m[g.name][indices] *= alpha1
+        v[g.name][indices] *= alpha2
+
+
+def reset_rows_f64(layout, m, v, t, indices):
+    """optimizer.py:159-165 — m = v = 0, t = 0 on the rows."""
+    for g in layout:
+        m[g.name][indices] = 0.0
+        v[g.name][indices] = 0.0
+    t[indices] = 0
+
+
+def classify_active_f64(tau, alive=None, threshold=ACTIVE_OPACITY_THRESHOLD):
+    """primitives.py:228-238 — (n_active, n_dead) over alive rows."""
+    tau = np.asarray(tau, F64).reshape(-1)
+    alive = np.ones(tau.shape[0], bool) if alive is None else np.asarray(alive, bool)
+    active = alive & (sigmoid_f64(tau) > threshold)
+    n_active = int(active.sum())
+    return n_active, int(alive.sum()) - n_active
+
+
+def moment_stats_f64(layout, m, v, alive=None):
+    """optimizer.py:489-506 — per-group mean/max sqrt(v) and |m|/sqrt(v) over alive rows."""
+    out = {}
+    for g in layout:
+        n = m[g.name].shape[0]
+        al = np.ones(n, bool) if alive is None else np.asarray(alive, bool)
+        vv = np.asarray(v[g.name], F64)[al].reshape(-1)
+        mm = np.asarray(m[g.name], F64)[al].reshape(-1)
+        sq = np.sqrt(vv)
+        pos = sq > 0.0
+        ratio = np.abs(mm[pos]) / sq[pos]
+        out[g.name] = {
+            "mean_sqrt_v": float(sq.mean()) if sq.size else 0.0,
+            "max_sqrt_v": float(sq.max()) if sq.size else 0.0,
+            "mean_abs_m_over_sqrt_v": float(ratio.mean()) if ratio.size else 0.0,
+            "max_abs_m_over_sqrt_v": float(ratio.max()) if ratio.size else 0.0,
+        }
+    return out
+
+
+def flatnonzero(mask) -> np.ndarray:
+    """optimizer.py:235,249 — the visibility compaction, ascending indices."""
+    return np.flatnonzero(np.asarray(mask, dtype=bool))
+
+
+# --------------------------------------------------------------------------
+# host RNG restatement for the RSR sample (rng.py:17-30, optimizer.py:379-386)
+# --------------------------------------------------------------------------
+
+def rng_stream(seed: int, label: str, *indices: int) -> np.random.Generator:
+    """rng.py:17-30 — Philox keyed by (seed, blake2b-4(label), indices)."""
+    key = (int.from_bytes(hashlib.blake2b(label.encode("utf-8"), digest_size=4).digest(), "little"),
+           *(int(i) & 0xFFFFFFFF for i in indices))
+    ss = np.random.SeedSequence(entropy=int(seed), spawn_key=key)
+    return np.random.Generator(np.random.Philox(ss))
+
+
+def stss_sample(milestones, iteration: int, n_p: int, rng: np.random.Generator) -> np.ndarray:
+    """optimizer.py:359-364,379-386 — floor(ratio*N) sorted distinct rows."""
+    ratio = 0.0
+    for it, r in milestones:
+        if iteration >= it:
+            ratio = r
+    k = int(math.floor(ratio * n_p))
+    if k <= 0:
+        return np.empty(0, dtype=np.int64)
+    return np.sort(rng.choice(n_p, size=k, replace=False).astype(np.int64))
+
+
+# --------------------------------------------------------------------------
+# fp32 restatement in the CUDA kernel's exact op order
+# --------------------------------------------------------------------------
+
+STAT_FIELDS = ("n_visible", "n_stepped", "n_bad_grad", "n_bad_domain", "n_active_pre",
+               "n_active_post", "n_clip_opacity", "n_clip_scale", "sum_extra_opacity",
+               "sum_extra_scale")
+
+
+def _reg_deriv_f64(role, theta32):
+    """R'(theta) in float64 from fp32 theta: sigma' for opacity, exp for scale."""
+    th = theta32.astype(F64)
+    if role == "opacity":
+        return opacity_derivative_f64(th)
+    return np.exp(th)
+
+
+def _domain_bad(role, theta32):
+    th = theta32.astype(F64)
+    bad = ~np.isfinite(th)
+    if role == "scale":
+        bad |= th > MAX_LOG_SCALE
+    return bad.any(axis=1)
+
+
+def step_fp32(mode, layout, params, grads, m, v, clock, rows, hp, *, n_pixels=None,
+              mu_lr_scale=1.0, lambda_o=None, lambda_s=None, clip=None, n_visible_norm=None,
+              global_t=None, lut=None, alive=None, skip_bad_rows=True):
+    """One fused step in the kernel's fp32 op order; mutates the fp32 arrays in place.
+
+    ``rows`` is the ascending visible index list (dense ``coupled-adam`` passes
+    all rows).  ``n_visible_norm`` is N_v for the coupled regularization
+    (``sparse-adam`` / ``coupled-adam`` with lambda != 0).  Returns the
+    per-step statistics dict (STAT_FIELDS).  Bad rows (non-finite gradient,
+    or tau/kappa out of the activation domain where a penalty is active) are
+    skipped and counted, as the kernel does in fused-check mode.
+    """
+    assert mode in MODES
+    rows = np.asarray(rows, dtype=np.int64)
+    dense = mode == "coupled-adam"
+    coupled = mode in ("sparse-adam", "coupled-adam")
+    if coupled:
+        # the pipeline's coupled composite (pipeline.py:305-315): lambdas are
+        # explicit, absent means plain sparse / sync Adam
+        lo = 0.0 if lambda_o is None else lambda_o
+        ls = 0.0 if lambda_s is None else lambda_s
+    elif mode == "adamw-gs":
+        lo = hp.lambda_o if lambda_o is None else lambda_o        # optimizer.py:279-280
+        ls = hp.lambda_s if lambda_s is None else lambda_s
+    else:
+        lo, ls = hp.lambda_o, hp.lambda_s                         # optimizer.py:312,318
+    n_i = round_pixel_count(n_pixels, hp.round_n_pixels) if mode == "adamw-gs" else None
+    a1 = F32(1.0 - hp.beta1)
+    a2 = F32(1.0 - hp.beta2)
+    eps = F32(hp.eps)
+    if lut is None:
+        tmax = int(clock.max(initial=0)) + 2 if not dense else int(global_t) + 1
+        lut = bias_lut_f32(hp.beta1, hp.beta2, max(tmax, 2))
+    thr = active_logit_threshold_f32()
+
+    stats = {k: 0 for k in STAT_FIELDS}
+    stats["sum_extra_opacity"] = 0.0
+    stats["sum_extra_scale"] = 0.0
+    stats["n_visible"] = int(rows.size)
+    if rows.size == 0:
+        return stats
+    if coupled and (n_visible_norm is None or n_visible_norm == 0):
+        lo_c = ls_c = 0.0
+    else:
+        lo_c, ls_c = lo, ls
+
+    # ---- pass A: per-row validity --------------------------------------
+    bad_grad = np.zeros(rows.size, bool)
+    bad_dom = np.zeros(rows.size, bool)
+    for g in layout:
+        bad_grad |= ~np.isfinite(grads[g.name][rows]).all(axis=1)
+        lam = lo if g.role == "opacity" else ls if g.role == "scale" else 0.0
+        if coupled:
+            lam = lo_c if g.role == "opacity" else ls_c if g.role == "scale" else 0.0
+        if g.role in ("opacity", "scale") and lam != 0.0:
+            bad_dom |= _domain_bad(g.role, params[g.name][rows])
+    if coupled:
+        # coupled reg is added to the gradient first; a domain error makes it
+        # non-computable, a non-finite sum is a gradient error
+        pass
+    bad_dom &= ~bad_grad
+    ok = ~(bad_grad | bad_dom) if skip_bad_rows else np.ones(rows.size, bool)
+    stats["n_bad_grad"] = int(bad_grad.sum())
+    stats["n_bad_domain"] = int(bad_dom.sum())
+    r = rows[ok]
+    stats["n_stepped"] = int(r.size)
+    if r.size == 0:
+        return stats
+
+    # ---- clocks and bias correction --------------------------------------
+    clock[r] += 1
+    tb = np.full(r.size, int(global_t)) if dense else clock[r].astype(np.int64)
+    tb = np.minimum(tb, lut.shape[0] - 1)
+    c1 = lut[tb, 0][:, None]
+    c2 = lut[tb, 1][:, None]
+
+    for g in layout:
+        th = params[g.name][r]
+        gr = grads[g.name][r]
+        mm = m[g.name][r]
+        vv = v[g.name][r]
+        if coupled and g.role in ("opacity", "scale"):
+            lam = lo_c if g.role == "opacity" else ls_c
+            if lam != 0.0:
+                regc = lam * _reg_deriv_f64(g.role, th) / float(n_visible_norm)
+                gr = (gr.astype(F64) + regc).astype(F32)
+        d = gr - mm
+        m_new = mm + a1 * d
+        g2 = gr * gr
+        e = g2 - vv
+        v_new = vv + a2 * e
+        mh = m_new * c1
+        vh = v_new * c2
+        den = np.sqrt(vh) + eps
+        step = mh / den
+        if g.role in ("opacity", "scale") and not coupled:
+            lam = lo if g.role == "opacity" else ls
+            if lam != 0.0:
+                deriv = _reg_deriv_f64(g.role, th)
+                if mode == "adamw-gs":
+                    cap = hp.ct_opacity if g.role == "opacity" else hp.ct_scale
+                    x = lam * (deriv / n_i) / den.astype(F64)
+                    clipped = x >= cap
+                    ex64 = np.minimum(x, cap)
+                else:
+                    x = lam * deriv
+                    if mode == "adamw-const-clip" or clip is not None:
+                        cap = clip if clip is not None else hp.ct_opacity
+                        clipped = x >= cap
+                        ex64 = np.minimum(x, cap)
+                    else:
+                        clipped = np.zeros(x.shape, bool)
+                        ex64 = x
+                ex = ex64.astype(F32)
+                step = step + ex
+                key = "opacity" if g.role == "opacity" else "scale"
+                stats["n_clip_" + key] += int(clipped.sum())
+                stats["sum_extra_" + key] += float(ex.astype(F64).sum())
+        lr = F32(hp.lr[g.name] * (mu_lr_scale if g.role == "position" else 1.0))
+        th_new = th - lr * step
+        if g.role == "opacity":
+            stats["n_active_pre"] += int((th[:, 0] > thr).sum())
+            stats["n_active_post"] += int((th_new[:, 0] > thr).sum())
+        params[g.name][r] = th_new
+        m[g.name][r] = m_new
+        v[g.name][r] = v_new
+    return stats

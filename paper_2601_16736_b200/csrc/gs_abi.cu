@@ -1,0 +1,40 @@
+// ABI plumbing: version, thread-local last error, device properties.
+#include <stdarg.h>
+#include <stdio.h>
+
+#include "gs_common.cuh"
+
+static thread_local char g_err[512] = "";
+
+void gs_set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int gs_check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    gs_set_error("%s: %s", what, cudaGetErrorString(e));
+    return GS_ERR_LAUNCH;
+  }
+  return GS_OK;
+}
+
+int gs_sm_count() {
+  static thread_local int dev_cached = -1;
+  static thread_local int sms = 0;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  if (dev != dev_cached) {
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0)
+      sms = 148;
+    dev_cached = dev;
+  }
+  return sms;
+}
+
+extern "C" int32_t gs_abi_version(void) { return GS_ABI_VERSION; }
+extern "C" const char* gs_last_error(void) { return g_err; }
+extern "C" int32_t gs_device_sm_count(void) { return gs_sm_count(); }

@@ -1,0 +1,309 @@
+// State kernels around the step:
+//   gs_check_grads  strict all-row finite check (gradients.py:50-58,
+//                   optimizer.py:181-184) + visible-row activation domain
+//                   (primitives.py:44-48,78-84)
+//   gs_rsr_apply    re-state regularisation (optimizer.py:327-340)
+//   gs_reset_rows   relocation reset (optimizer.py:159-165)
+//   gs_stats_all    classify_active + moment_stats (primitives.py:228-238,
+//                   optimizer.py:489-506)
+#include "gs_common.cuh"
+
+namespace gs {
+
+struct GroupPtrs {
+  float* param;
+  const float* grad;
+  float* m;
+  float* v;
+  int width;
+  int role;
+};
+
+struct GroupSet {
+  GroupPtrs g[GS_MAX_GROUPS];
+  int n;
+};
+
+static int fill_groups(const gs_group* groups, int32_t n_groups, GroupSet& S, const char* who,
+                       bool need_grad) {
+  if (!groups || n_groups < 1 || n_groups > GS_MAX_GROUPS) {
+    gs_set_error("%s: bad group list", who);
+    return GS_ERR_ARG;
+  }
+  S.n = n_groups;
+  for (int i = 0; i < n_groups; ++i) {
+    const gs_group& g = groups[i];
+    if (!g.exp_avg || !g.exp_avg_sq || (need_grad && !g.grad) || g.width < 1 || g.width > 4096) {
+      gs_set_error("%s: group %d invalid", who, i);
+      return GS_ERR_ARG;
+    }
+    S.g[i] = GroupPtrs{g.param, g.grad, g.exp_avg, g.exp_avg_sq, (int)g.width, g.role};
+  }
+  return GS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// strict check: one flat pass per group over all n_rows * width gradients
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void mark_row(uint8_t* bad_rows, int64_t row, int bad) {
+  atomicOr(reinterpret_cast<unsigned int*>(bad_rows + (row & ~3ll)),
+           (unsigned int)bad << (8 * (row & 3)));
+}
+
+__global__ void __launch_bounds__(kThreads)
+    check_grads_kernel(const GroupSet S, int64_t n_rows, const int32_t* __restrict__ rows,
+                       const int32_t* __restrict__ n_list_dev, double lam_op, double lam_sc,
+                       uint8_t* __restrict__ bad_rows, int32_t* __restrict__ abort_flag) {
+  int flag = 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t tid0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t n_list = rows ? (int64_t)(*n_list_dev) : 0;
+  for (int gi = 0; gi < S.n; ++gi) {
+    const GroupPtrs G = S.g[gi];
+    const int W = G.width;
+    const int64_t total = n_rows * W;
+    for (int64_t e = tid0; e < total; e += stride) {
+      if (!isfinite(__ldg(G.grad + e))) {
+        flag |= 1;
+        if (bad_rows) mark_row(bad_rows, e / W, 1);
+      }
+    }
+    const double lam = G.role == GS_ROLE_OPACITY ? lam_op : G.role == GS_ROLE_SCALE ? lam_sc : 0.0;
+    if (lam != 0.0 && G.param != nullptr) {
+      const int64_t tot = n_list * W;
+      for (int64_t e = tid0; e < tot; e += stride) {
+        const int64_t row = __ldg(rows + e / W);
+        if (domain_bad(G.role, G.param[row * W + e % W])) {
+          flag |= 2;
+          if (bad_rows) mark_row(bad_rows, row, 2);
+        }
+      }
+    }
+  }
+  flag = __reduce_or_sync(0xffffffffu, flag);
+  if ((threadIdx.x & 31) == 0 && flag) atomicOr(abort_flag, flag);
+}
+
+// ---------------------------------------------------------------------------
+// RSR / reset: chunk of kThreads rows per CTA, flattened (row, col) per group
+// ---------------------------------------------------------------------------
+template <bool RESET>
+__global__ void __launch_bounds__(kThreads)
+    scatter_state_kernel(const GroupSet S, const int32_t* __restrict__ rows, int64_t k,
+                         double a1, double a2, int32_t* __restrict__ clock) {
+  __shared__ int32_t s_row[kThreads];
+  const int tid = threadIdx.x;
+  const int64_t n_chunks = (k + kThreads - 1) / kThreads;
+  for (int64_t chunk = blockIdx.x; chunk < n_chunks; chunk += gridDim.x) {
+    const int64_t base = chunk * kThreads;
+    const int nvalid = (int)(k - base < kThreads ? k - base : kThreads);
+    if (tid < nvalid) {
+      const int32_t r = __ldg(rows + base + tid);
+      s_row[tid] = r;
+      if (RESET && clock) clock[r] = 0;
+    }
+    __syncthreads();
+    for (int gi = 0; gi < S.n; ++gi) {
+      const GroupPtrs G = S.g[gi];
+      const int W = G.width;
+      const int E = nvalid * W;
+      const int dq = kThreads / W, dr = kThreads % W;
+      int lr = tid / W, lc = tid % W;
+      for (int e = tid; e < E; e += kThreads) {
+        const int64_t off = (int64_t)s_row[lr] * W + lc;
+        if (RESET) {
+          G.m[off] = 0.0f;
+          G.v[off] = 0.0f;
+        } else {
+          // m *= alpha1 in float64, rounded once (optimizer.py:338-339)
+          G.m[off] = __double2float_rn(__dmul_rn((double)G.m[off], a1));
+          G.v[off] = __double2float_rn(__dmul_rn((double)G.v[off], a2));
+        }
+        lc += dr;
+        lr += dq;
+        if (lc >= W) { lc -= W; ++lr; }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// all-row statistics
+// ---------------------------------------------------------------------------
+constexpr int kStatsFields = 2 + 5 * GS_MAX_GROUPS;
+
+struct StatsWorkspace {
+  unsigned int counter;
+  unsigned int pad[15];
+};
+
+__global__ void __launch_bounds__(kThreads)
+    stats_all_kernel(const GroupSet S, int64_t n_rows, const uint8_t* __restrict__ alive,
+                     float active_logit, double* __restrict__ out, double* partials,
+                     unsigned int* counter) {
+  __shared__ double s_red[kStatsFields * (kThreads / 32)];
+  double acc[kStatsFields];
+  bool is_max[kStatsFields];
+#pragma unroll
+  for (int f = 0; f < kStatsFields; ++f) {
+    acc[f] = 0.0;
+    is_max[f] = f >= 2 && (((f - 2) % 5) == 1 || ((f - 2) % 5) == 4);
+  }
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t tid0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (int64_t r = tid0; r < n_rows; r += stride) {
+    const bool al = alive == nullptr || alive[r] != 0;
+    acc[0] += al;
+  }
+#pragma unroll
+  for (int gi = 0; gi < GS_MAX_GROUPS; ++gi) {
+    if (gi >= S.n) break;
+    const GroupPtrs G = S.g[gi];
+    const int64_t total = n_rows * G.width;
+    double s_sq = 0.0, m_sq = 0.0, n_pos = 0.0, s_rt = 0.0, m_rt = 0.0;
+    for (int64_t e = tid0; e < total; e += stride) {
+      if (alive != nullptr && alive[e / G.width] == 0) continue;
+      const double vv = (double)__ldg(G.v + e);
+      const double sq = sqrt(vv);
+      s_sq += sq;
+      m_sq = fmax(m_sq, sq);
+      if (sq > 0.0) {
+        const double rt = __ddiv_rn(fabs((double)__ldg(G.m + e)), sq);
+        n_pos += 1.0;
+        s_rt += rt;
+        m_rt = fmax(m_rt, rt);
+      }
+      if (G.role == GS_ROLE_OPACITY && G.width == 1 && G.param != nullptr)
+        acc[1] += __ldg(G.param + e) > active_logit;
+    }
+    acc[2 + 5 * gi + 0] = s_sq;
+    acc[2 + 5 * gi + 1] = m_sq;
+    acc[2 + 5 * gi + 2] = n_pos;
+    acc[2 + 5 * gi + 3] = s_rt;
+    acc[2 + 5 * gi + 4] = m_rt;
+  }
+  block_reduce<kStatsFields>(acc, is_max, s_red);
+  if (threadIdx.x == 0) {
+    for (int f = 0; f < kStatsFields; ++f) partials[(size_t)blockIdx.x * kStatsFields + f] = acc[f];
+  }
+  if (last_block_arrive(counter)) {
+    const int nf = 2 + 5 * S.n;
+    for (int f = threadIdx.x; f < nf; f += blockDim.x) {
+      const bool mx = f >= 2 && (((f - 2) % 5) == 1 || ((f - 2) % 5) == 4);
+      double a = partials[f];
+      for (unsigned b = 1; b < gridDim.x; ++b) {
+        const double x = partials[(size_t)b * kStatsFields + f];
+        a = mx ? fmax(a, x) : a + x;
+      }
+      out[f] = a;
+    }
+  }
+}
+
+int stats_blocks() { return gs_sm_count() * 2; }
+
+}  // namespace gs
+
+extern "C" int gs_check_grads(const gs_group* groups, int32_t n_groups, int64_t n_rows,
+                              const int32_t* rows, const int32_t* n_list_dev,
+                              double lambda_opacity, double lambda_scale, uint8_t* bad_rows_out,
+                              int32_t* abort_flag, void* stream) {
+  using namespace gs;
+  GroupSet S{};
+  int rc = fill_groups(groups, n_groups, S, "gs_check_grads", true);
+  if (rc) return rc;
+  if (!abort_flag || n_rows < 0) {
+    gs_set_error("gs_check_grads: abort_flag required");
+    return GS_ERR_ARG;
+  }
+  if (bad_rows_out && (reinterpret_cast<uintptr_t>(bad_rows_out) & 3u)) {
+    gs_set_error("gs_check_grads: bad_rows_out must be 4-byte aligned");
+    return GS_ERR_ALIGN;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  if (cudaMemsetAsync(abort_flag, 0, sizeof(int32_t), s) != cudaSuccess)
+    return gs_check_launch("gs_check_grads memset");
+  if (bad_rows_out && n_rows > 0 &&
+      cudaMemsetAsync(bad_rows_out, 0, (size_t)n_rows, s) != cudaSuccess)
+    return gs_check_launch("gs_check_grads memset");
+  if (n_rows == 0) return GS_OK;
+  int grid = gs_sm_count() * 8;
+  if (rows && !n_list_dev) {
+    gs_set_error("gs_check_grads: rows given without their device count");
+    return GS_ERR_ARG;
+  }
+  check_grads_kernel<<<grid, kThreads, 0, s>>>(S, n_rows, rows, n_list_dev, lambda_opacity,
+                                               lambda_scale, bad_rows_out, abort_flag);
+  return gs_check_launch("gs_check_grads");
+}
+
+extern "C" int gs_rsr_apply(const gs_group* groups, int32_t n_groups, const int32_t* rows,
+                            int64_t k, double alpha1, double alpha2, void* stream) {
+  using namespace gs;
+  GroupSet S{};
+  int rc = fill_groups(groups, n_groups, S, "gs_rsr_apply", false);
+  if (rc) return rc;
+  if (!(alpha1 >= 0.0 && alpha1 < 1.0 && alpha2 >= 0.0 && alpha2 < 1.0)) {
+    gs_set_error("gs_rsr_apply: RSR factors must lie in [0, 1)");
+    return GS_ERR_ARG;
+  }
+  if (k < 0 || (k > 0 && !rows)) {
+    gs_set_error("gs_rsr_apply: bad index list");
+    return GS_ERR_ARG;
+  }
+  if (k == 0) return GS_OK;
+  const int64_t chunks = (k + kThreads - 1) / kThreads;
+  int grid = (int)std::min<int64_t>(chunks, (int64_t)gs_sm_count() * 8);
+  scatter_state_kernel<false><<<grid, kThreads, 0, (cudaStream_t)stream>>>(S, rows, k, alpha1,
+                                                                           alpha2, nullptr);
+  return gs_check_launch("gs_rsr_apply");
+}
+
+extern "C" int gs_reset_rows(const gs_group* groups, int32_t n_groups, int32_t* clock,
+                             const int32_t* rows, int64_t k, void* stream) {
+  using namespace gs;
+  GroupSet S{};
+  int rc = fill_groups(groups, n_groups, S, "gs_reset_rows", false);
+  if (rc) return rc;
+  if (k < 0 || (k > 0 && !rows)) {
+    gs_set_error("gs_reset_rows: bad index list");
+    return GS_ERR_ARG;
+  }
+  if (k == 0) return GS_OK;
+  const int64_t chunks = (k + kThreads - 1) / kThreads;
+  int grid = (int)std::min<int64_t>(chunks, (int64_t)gs_sm_count() * 8);
+  scatter_state_kernel<true><<<grid, kThreads, 0, (cudaStream_t)stream>>>(S, rows, k, 0.0, 0.0,
+                                                                          clock);
+  return gs_check_launch("gs_reset_rows");
+}
+
+extern "C" size_t gs_stats_workspace_bytes(int32_t n_groups) {
+  (void)n_groups;
+  return sizeof(gs::StatsWorkspace) +
+         (size_t)gs::stats_blocks() * gs::kStatsFields * sizeof(double);
+}
+
+extern "C" int gs_stats_all(const gs_group* groups, int32_t n_groups, int64_t n_rows,
+                            const uint8_t* alive, float active_logit, double* out, void* ws,
+                            size_t ws_bytes, void* stream) {
+  using namespace gs;
+  GroupSet S{};
+  int rc = fill_groups(groups, n_groups, S, "gs_stats_all", false);
+  if (rc) return rc;
+  if (!out || n_rows < 0) {
+    gs_set_error("gs_stats_all: bad arguments");
+    return GS_ERR_ARG;
+  }
+  if (!ws || ws_bytes < gs_stats_workspace_bytes(n_groups)) {
+    gs_set_error("gs_stats_all: workspace too small");
+    return GS_ERR_WORKSPACE;
+  }
+  auto* hdr = reinterpret_cast<StatsWorkspace*>(ws);
+  auto* partials = reinterpret_cast<double*>(reinterpret_cast<char*>(ws) + sizeof(StatsWorkspace));
+  const int64_t need = (n_rows * 4 + kThreads - 1) / kThreads;
+  int grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, stats_blocks()));
+  stats_all_kernel<<<grid, kThreads, 0, (cudaStream_t)stream>>>(S, n_rows, alive, active_logit,
+                                                                out, partials, &hdr->counter);
+  return gs_check_launch("gs_stats_all");
+}

@@ -1,0 +1,327 @@
+"""Device-side step engine: owns the scratch buffers of one row range and
+drives the C ABI (include/adamw_gs.h) on the current CUDA stream.
+
+Everything here is plumbing around the four kernel families; no arithmetic
+of the optimizer runs in Python or PyTorch.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib as L
+
+ACTIVE_OPACITY_THRESHOLD = 1.0 / 255.0   # primitives.py:33
+
+
+class ConfigError(ValueError):
+    """Invalid optimizer configuration (optimizer.py:58)."""
+
+
+class GradientError(RuntimeError):
+    """A step hit a non-finite gradient (optimizer.py:62-67); ``ids`` lists the rows."""
+
+    def __init__(self, ids):
+        self.ids = np.asarray(ids)
+        super().__init__(f"non-finite gradient on primitives {self.ids.tolist()[:16]}")
+
+
+class DomainError(ValueError):
+    """tau non-finite or kappa > 80 on a visible row (primitives.py:40-48,78-84)."""
+
+    def __init__(self, msg, ids=()):
+        self.ids = np.asarray(ids)
+        super().__init__(msg)
+
+
+def round_pixel_count(n_pixels: int, enabled: bool = True) -> float:
+    """N_I' — keep the most significant digit of N_I, divide by ten (optimizer.py:168-178)."""
+    if n_pixels <= 0:
+        raise ConfigError("pixel count must be positive")
+    if not enabled:
+        return float(n_pixels)
+    p = 10 ** math.floor(math.log10(n_pixels))
+    return (n_pixels // p) * p / 10.0
+
+
+def _sigmoid_f64(t: float) -> float:
+    """primitives.py:51-59 on one float64."""
+    if t >= 0:
+        return 1.0 / (1.0 + math.exp(-t))
+    e = math.exp(t)
+    return e / (1.0 + e)
+
+
+def active_logit_threshold() -> float:
+    """Largest fp32 tau with float64 sigmoid(tau) <= 1/255.
+
+    ``classify_active`` (primitives.py:228-238) compares the float64 sigmoid
+    with 1/255; for fp32 tau this is exactly ``tau > T`` with this T, so the
+    kernels count active rows with one fp32 compare.
+    """
+    t = np.float32(math.log(ACTIVE_OPACITY_THRESHOLD / (1.0 - ACTIVE_OPACITY_THRESHOLD)))
+    up, down = np.float32(np.inf), np.float32(-np.inf)
+    while _sigmoid_f64(float(t)) > ACTIVE_OPACITY_THRESHOLD:
+        t = np.nextafter(t, down)
+    while _sigmoid_f64(float(np.nextafter(t, up))) <= ACTIVE_OPACITY_THRESHOLD:
+        t = np.nextafter(t, up)
+    return float(t)
+
+
+def bias_lut(beta1: float, beta2: float, cap: int = 1 << 22) -> np.ndarray:
+    """fp32 factors 1/(1-beta^t) from float64, t in [0, L); beyond L both are 1.0f.
+
+    Denominators as in ``_corrected`` (optimizer.py:202-203).  The table is
+    extended until both factors round to exactly 1.0f, so clamping the clock
+    to the last entry is exact; otherwise the kernel evaluates the float64
+    formula for clocks past the table.
+    """
+    b = max(beta1, beta2)
+    if b <= 0.0:
+        n = 2
+    else:
+        n = int(min(cap, math.ceil(math.log(2.0 ** -26) / math.log(b)) + 2))
+    n = max(n, 2)
+    t = np.arange(n, dtype=np.float64)
+    with np.errstate(divide="ignore"):
+        c1 = 1.0 / (1.0 - np.power(beta1, t))
+        c2 = 1.0 / (1.0 - np.power(beta2, t))
+    c1[0] = c2[0] = 1.0
+    return np.ascontiguousarray(np.stack([c1.astype(np.float32), c2.astype(np.float32)], axis=1))
+
+
+def _ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _stream_handle(device: torch.device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+@dataclass
+class GroupBinding:
+    """One attribute group as the kernels see it: [rows, width] fp32 views."""
+
+    name: str
+    role: int
+    lr: float
+    param: torch.Tensor
+    grad: torch.Tensor | None
+    exp_avg: torch.Tensor
+    exp_avg_sq: torch.Tensor
+
+    @property
+    def width(self) -> int:
+        n = self.param.shape[0]
+        return self.param.numel() // max(n, 1) if n else max(1, int(np.prod(self.param.shape[1:])))
+
+
+def _check_tensor(name, t: torch.Tensor, n_rows: int, width: int, device, dtype=torch.float32):
+    if t.device != device:
+        raise ConfigError(f"{name} is on {t.device}, expected {device}")
+    if t.dtype != dtype:
+        raise ConfigError(f"{name} has dtype {t.dtype}, expected {dtype}")
+    if not t.is_contiguous():
+        raise ConfigError(f"{name} must be contiguous")
+    if t.shape[0] != n_rows or t.numel() != n_rows * width:
+        raise ConfigError(f"{name} has shape {tuple(t.shape)}, expected {n_rows} rows x {width}")
+
+
+class StepEngine:
+    """Scratch buffers + C-ABI launches for one optimizer of ``n_rows`` rows."""
+
+    def __init__(self, n_rows: int, device: torch.device, beta1: float, beta2: float):
+        if not torch.cuda.is_available():
+            raise L.ExtensionMissing("CUDA device required: the step has no CPU fallback")
+        self.lib = L.load()
+        self.device = torch.device(device)
+        self.n_rows = int(n_rows)
+        self.beta1, self.beta2 = float(beta1), float(beta2)
+        dev = self.device
+        with torch.cuda.device(dev):
+            n = max(self.n_rows, 1)
+            self.idx = torch.empty(n, dtype=torch.int32, device=dev)
+            self.count = torch.zeros(1, dtype=torch.int32, device=dev)
+            self.compact_ws = torch.zeros(int(self.lib.gs_compact_workspace_bytes(n)),
+                                          dtype=torch.uint8, device=dev)
+            self.step_ws = torch.zeros(int(self.lib.gs_step_workspace_bytes()), dtype=torch.uint8,
+                                       device=dev)
+            self.stats = torch.zeros(L.GS_STEP_STATS, dtype=torch.float64, device=dev)
+            self.abort = torch.zeros(1, dtype=torch.int32, device=dev)
+            lut = bias_lut(self.beta1, self.beta2)
+            self.lut = torch.from_numpy(lut).to(dev)
+            self.stats_ws = torch.zeros(int(self.lib.gs_stats_workspace_bytes(L.GS_MAX_GROUPS)),
+                                        dtype=torch.uint8, device=dev)
+            self.stats_all_out = torch.zeros(2 + 5 * L.GS_MAX_GROUPS, dtype=torch.float64,
+                                             device=dev)
+            self._bad_rows = None
+            self._rows_tmp = None
+        self.active_logit = active_logit_threshold()
+        self._group_cache_key = None
+        self._group_cache = None
+
+    # ------------------------------------------------------------------ groups
+    def group_array(self, groups: list[GroupBinding], need_grad: bool = True):
+        key = tuple((g.role, float(g.lr), _ptr(g.param), _ptr(g.grad), _ptr(g.exp_avg),
+                     _ptr(g.exp_avg_sq)) for g in groups)
+        if key == self._group_cache_key:
+            return self._group_cache
+        if not 1 <= len(groups) <= L.GS_MAX_GROUPS:
+            raise ConfigError(f"between 1 and {L.GS_MAX_GROUPS} attribute groups are supported")
+        arr = (L.GsGroup * len(groups))()
+        for i, g in enumerate(groups):
+            w = g.width
+            _check_tensor(f"{g.name}.param", g.param, self.n_rows, w, self.device)
+            _check_tensor(f"{g.name}.exp_avg", g.exp_avg, self.n_rows, w, self.device)
+            _check_tensor(f"{g.name}.exp_avg_sq", g.exp_avg_sq, self.n_rows, w, self.device)
+            if need_grad:
+                if g.grad is None:
+                    raise ConfigError(f"group {g.name} has no gradient")
+                _check_tensor(f"{g.name}.grad", g.grad, self.n_rows, w, self.device)
+            arr[i] = L.GsGroup(_ptr(g.param), _ptr(g.grad), _ptr(g.exp_avg), _ptr(g.exp_avg_sq),
+                               w, g.role, float(np.float32(g.lr)))
+        self._group_cache_key, self._group_cache = key, arr
+        return arr
+
+    # ------------------------------------------------------------- compaction
+    def compact(self, vis: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor]:
+        """K1: visibility mask (bool/uint8) or radii (int32 > 0) -> (idx, count)."""
+        if vis.device != self.device:
+            raise ConfigError(f"visibility is on {vis.device}, expected {self.device}")
+        if vis.dim() != 1 or vis.shape[0] != self.n_rows:
+            raise ConfigError(f"visibility must have shape ({self.n_rows},), got {tuple(vis.shape)}")
+        if not vis.is_contiguous():
+            raise ConfigError("visibility must be contiguous")
+        s = _stream_handle(self.device)
+        ws, wsb = self.compact_ws.data_ptr(), self.compact_ws.numel()
+        if vis.dtype in (torch.bool, torch.uint8):
+            rc = self.lib.gs_compact_u8(vis.data_ptr(), self.n_rows, self.idx.data_ptr(),
+                                        self.count.data_ptr(), ws, wsb, s)
+        elif vis.dtype == torch.int32:
+            rc = self.lib.gs_compact_i32(vis.data_ptr(), self.n_rows, self.idx.data_ptr(),
+                                         self.count.data_ptr(), ws, wsb, s)
+        else:
+            raise ConfigError(f"visibility dtype {vis.dtype} not supported (bool/uint8 mask or "
+                              "int32 radii)")
+        L.check(rc, "gs_compact")
+        return self.idx, self.count
+
+    # ------------------------------------------------------------------ step
+    def step(self, groups: list[GroupBinding], mode: str, clock: torch.Tensor, *,
+             rows: torch.Tensor | None, count: torch.Tensor | None, eps: float,
+             lambda_opacity: float = 0.0, lambda_scale: float = 0.0, clip_opacity: float = 10.0,
+             clip_scale: float = 10.0, n_pixels_rounded: float = 0.0, global_t: int = 0,
+             n_visible_dev: torch.Tensor | None = None, n_visible_host: float = 0.0,
+             check: str = "fused") -> torch.Tensor:
+        """K2 (plus the strict pre-check when ``check == "strict"``)."""
+        if mode not in L.MODE_IDS:
+            raise ConfigError(f"unknown mode {mode!r}; expected one of {tuple(L.MODE_IDS)}")
+        _check_tensor("clock", clock, self.n_rows, 1, self.device, torch.int32)
+        garr = self.group_array(groups)
+        s = _stream_handle(self.device)
+        cfg = L.GsStepCfg()
+        cfg.mode = L.MODE_IDS[mode]
+        cfg.check = L.CHECK_STRICT if check == "strict" else L.CHECK_FUSED
+        cfg.one_minus_beta1 = float(np.float32(1.0 - self.beta1))
+        cfg.one_minus_beta2 = float(np.float32(1.0 - self.beta2))
+        cfg.eps = float(np.float32(eps))
+        cfg.active_logit = self.active_logit
+        cfg.lambda_opacity = float(lambda_opacity)
+        cfg.lambda_scale = float(lambda_scale)
+        cfg.clip_opacity = float(clip_opacity)
+        cfg.clip_scale = float(clip_scale)
+        cfg.n_pixels_rounded = float(n_pixels_rounded)
+        cfg.bias_lut = self.lut.data_ptr()
+        cfg.lut_len = self.lut.shape[0]
+        cfg.global_t = int(global_t)
+        cfg.beta1, cfg.beta2 = self.beta1, self.beta2
+        cfg.n_visible_norm = _ptr(n_visible_dev)
+        cfg.n_visible_host = float(n_visible_host)
+        cfg.abort_flag = self.abort.data_ptr()
+        if check == "strict":
+            # the penalty's activation domain is checked where the penalty
+            # applies: listed rows, or every row for the dense coupled mode
+            drows, dcount = (self.all_rows() if mode == "coupled-adam" else (rows, count))
+            rc = self.lib.gs_check_grads(garr, len(groups), self.n_rows, _ptr(drows),
+                                         _ptr(dcount), float(lambda_opacity),
+                                         float(lambda_scale), None, self.abort.data_ptr(), s)
+            L.check(rc, "gs_check_grads")
+        rc = self.lib.gs_step(garr, len(groups), C.byref(cfg), _ptr(rows), _ptr(count),
+                              self.n_rows, clock.data_ptr(), self.stats.data_ptr(),
+                              self.step_ws.data_ptr(), self.step_ws.numel(), s)
+        L.check(rc, "gs_step")
+        return self.stats
+
+    def all_rows(self) -> tuple[torch.Tensor, torch.Tensor]:
+        """Identity index list (dense mode domain checks, error ids)."""
+        if getattr(self, "_all_rows", None) is None:
+            self._all_rows = torch.arange(self.n_rows, dtype=torch.int32, device=self.device)
+            self._all_count = torch.tensor([self.n_rows], dtype=torch.int32, device=self.device)
+        return self._all_rows, self._all_count
+
+    # ----------------------------------------------------------- error ids
+    def bad_rows(self, groups: list[GroupBinding], rows=None, count=None, lambda_opacity=0.0,
+                 lambda_scale=0.0) -> tuple[np.ndarray, np.ndarray]:
+        """Row ids with a non-finite gradient (all rows, gradients.py:50-58) and
+        visible row ids outside the activation domain (error path only)."""
+        garr = self.group_array(groups)
+        if self._bad_rows is None:
+            self._bad_rows = torch.zeros((self.n_rows + 3) // 4 * 4, dtype=torch.uint8,
+                                         device=self.device)
+        flag = torch.zeros(1, dtype=torch.int32, device=self.device)
+        rc = self.lib.gs_check_grads(garr, len(groups), self.n_rows, _ptr(rows), _ptr(count),
+                                     float(lambda_opacity), float(lambda_scale),
+                                     self._bad_rows.data_ptr(), flag.data_ptr(),
+                                     _stream_handle(self.device))
+        L.check(rc, "gs_check_grads")
+        bits = self._bad_rows[: self.n_rows].cpu().numpy()
+        return np.flatnonzero(bits & 1), np.flatnonzero(bits & 2)
+
+    # --------------------------------------------------------- RSR / reset
+    def _rows_device(self, indices) -> tuple[torch.Tensor, int]:
+        if isinstance(indices, torch.Tensor):
+            t = indices.to(device=self.device, dtype=torch.int32).contiguous()
+        else:
+            arr = np.asarray(indices, dtype=np.int64).reshape(-1)
+            if arr.size and (arr.min() < 0 or arr.max() >= self.n_rows):
+                raise IndexError("row index out of range")
+            t = torch.from_numpy(arr.astype(np.int32)).to(self.device, non_blocking=False)
+        return t, int(t.numel())
+
+    def rsr_apply(self, groups: list[GroupBinding], indices, alpha1: float, alpha2: float):
+        if not (0.0 <= alpha1 < 1.0 and 0.0 <= alpha2 < 1.0):
+            raise ConfigError("RSR factors must lie in [0, 1)")
+        rows, k = self._rows_device(indices)
+        garr = self.group_array(groups, need_grad=False)
+        rc = self.lib.gs_rsr_apply(garr, len(groups), rows.data_ptr() if k else None, k,
+                                   float(alpha1), float(alpha2), _stream_handle(self.device))
+        L.check(rc, "gs_rsr_apply")
+        self._rows_tmp = rows  # keep alive until the kernel has consumed it
+
+    def reset_rows(self, groups: list[GroupBinding], clock: torch.Tensor, indices):
+        rows, k = self._rows_device(indices)
+        garr = self.group_array(groups, need_grad=False)
+        rc = self.lib.gs_reset_rows(garr, len(groups), clock.data_ptr(),
+                                    rows.data_ptr() if k else None, k,
+                                    _stream_handle(self.device))
+        L.check(rc, "gs_reset_rows")
+        self._rows_tmp = rows
+
+    # ---------------------------------------------------------- statistics
+    def stats_all(self, groups: list[GroupBinding], alive: torch.Tensor | None = None):
+        garr = self.group_array(groups, need_grad=False)
+        if alive is not None:
+            if alive.dtype not in (torch.bool, torch.uint8) or alive.numel() != self.n_rows:
+                raise ConfigError("alive must be a bool/uint8 mask over the rows")
+            alive = alive.contiguous()
+        rc = self.lib.gs_stats_all(garr, len(groups), self.n_rows, _ptr(alive),
+                                   float(self.active_logit), self.stats_all_out.data_ptr(),
+                                   self.stats_ws.data_ptr(), self.stats_ws.numel(),
+                                   _stream_handle(self.device))
+        L.check(rc, "gs_stats_all")
+        return self.stats_all_out[: 2 + 5 * len(groups)]

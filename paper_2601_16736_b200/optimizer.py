@@ -1,0 +1,407 @@
+"""AdamW-GS optimizer: the reference's optimizer API over CUDA tensors.
+
+Drop-in for the reference step family (/root/reference/pkg/src/splatlab/
+optimizer.py) on the 3DGS parameter groups ``xyz / f_dc / f_rest / opacity /
+scaling / rotation`` (or the reference's own ``mu / kappa / rot / tau /
+color``).  Construction takes torch-style param groups, ``step()`` takes the
+per-view visibility mask (or the rasterizer's int32 radii), and the state is
+the reference's ``MomentState`` layout: per-group ``m`` and ``v`` shaped like
+the parameters plus the per-primitive step clock.
+
+All arithmetic runs in the sm_100a kernels behind ``include/adamw_gs.h``;
+this module is host plumbing.  There is no CPU path.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from .engine import (ConfigError, DomainError, GradientError, GroupBinding, StepEngine,
+                     round_pixel_count)
+
+MODES = ("coupled-adam", "sparse-adam", "adamw-const", "adamw-const-clip", "adamw-gs")
+CHECKS = ("fused", "strict")
+ERRORS = ("raise", "defer", "ignore")
+
+# group name -> role (optimizer.py:217,259-263 key on mu / tau / kappa)
+ROLE_BY_NAME = {
+    "xyz": L.ROLE_POSITION, "mu": L.ROLE_POSITION, "means": L.ROLE_POSITION,
+    "opacity": L.ROLE_OPACITY, "tau": L.ROLE_OPACITY, "opacities": L.ROLE_OPACITY,
+    "scaling": L.ROLE_SCALE, "kappa": L.ROLE_SCALE, "scales": L.ROLE_SCALE,
+}
+ROLE_NAMES = {"plain": L.ROLE_PLAIN, "position": L.ROLE_POSITION, "opacity": L.ROLE_OPACITY,
+              "scale": L.ROLE_SCALE}
+# reference attribute <-> 3DGS group
+SH3_ALIASES = {"xyz": "mu", "f_dc": "color", "opacity": "tau", "scaling": "kappa",
+               "rotation": "rot"}
+
+
+def role_of(name: str, role=None) -> int:
+    if role is None:
+        return ROLE_BY_NAME.get(name, L.ROLE_PLAIN)
+    if isinstance(role, str):
+        return ROLE_NAMES[role]
+    return int(role)
+
+
+@dataclass
+class OptimizerConfig:
+    """optimizer.py:70-100, plus learning rates for groups the reference lacks."""
+
+    mode: str = "coupled-adam"
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps: float = 1e-8
+    lr_mu: float = 0.029
+    lr_tau: float = 0.05
+    lr_kappa: float = 5e-3
+    lr_rot: float = 1e-3
+    lr_color: float = 2.5e-3
+    lambda_o: float = 0.0
+    lambda_s: float = 0.0
+    ct_opacity: float = 10.0
+    ct_scale: float = 10.0
+    round_n_pixels: bool = True
+    lr_extra: dict = field(default_factory=dict)
+
+    def __post_init__(self):
+        validate_hyper(self.mode, self.beta1, self.beta2, self.eps, self.ct_opacity, self.ct_scale)
+
+    def lr(self, attr: str) -> float:
+        if attr in self.lr_extra:
+            return float(self.lr_extra[attr])
+        name = SH3_ALIASES.get(attr, attr)
+        if hasattr(self, f"lr_{name}"):
+            return float(getattr(self, f"lr_{name}"))
+        raise ConfigError(f"no learning rate for attribute group {attr!r}")
+
+
+def validate_hyper(mode, beta1, beta2, eps, ct_opacity, ct_scale):
+    if mode not in MODES:
+        raise ConfigError(f"unknown mode {mode!r}; expected one of {MODES}")
+    for name, b in (("beta1", beta1), ("beta2", beta2)):
+        if not (0.0 <= b < 1.0):
+            raise ConfigError(f"{name} must lie in [0, 1)")
+    if not (eps > 0.0):
+        raise ConfigError("eps must be positive")
+    if not (ct_opacity > 0.0 and ct_scale > 0.0):
+        raise ConfigError("clip bounds C_t must be positive")
+
+
+@dataclass
+class MomentState:
+    """optimizer.py:103-156 — m, v per group (param-shaped) + the step clock.
+
+    The reference keeps one int64 clock per group; every code path moves them
+    together, so one int32 clock per primitive is stored
+    and ``t[group]`` returns that shared tensor.
+    """
+
+    m: dict
+    v: dict
+    clock: torch.Tensor
+    global_t: int = 0
+
+    @property
+    def t(self) -> dict:
+        return {k: self.clock for k in self.m}
+
+    def __len__(self) -> int:
+        return int(self.clock.numel())
+
+    @staticmethod
+    def zeros_like(params: dict) -> "MomentState":
+        first = next(iter(params.values()))
+        return MomentState(
+            m={k: torch.zeros_like(p, dtype=torch.float32, memory_format=torch.contiguous_format)
+               for k, p in params.items()},
+            v={k: torch.zeros_like(p, dtype=torch.float32, memory_format=torch.contiguous_format)
+               for k, p in params.items()},
+            clock=torch.zeros(first.shape[0], dtype=torch.int32, device=first.device))
+
+    def copy(self) -> "MomentState":
+        return MomentState({k: t.clone() for k, t in self.m.items()},
+                           {k: t.clone() for k, t in self.v.items()}, self.clock.clone(),
+                           self.global_t)
+
+    def select(self, index) -> "MomentState":
+        """Rows ``index`` (prune/clone bookkeeping, optimizer.py:141-147)."""
+        return MomentState({k: t[index].contiguous() for k, t in self.m.items()},
+                           {k: t[index].contiguous() for k, t in self.v.items()},
+                           self.clock[index].contiguous(), self.global_t)
+
+    @staticmethod
+    def concatenate(a: "MomentState", b: "MomentState") -> "MomentState":
+        """optimizer.py:149-156."""
+        return MomentState({k: torch.cat([a.m[k], b.m[k]]) for k in a.m},
+                           {k: torch.cat([a.v[k], b.v[k]]) for k in a.v},
+                           torch.cat([a.clock, b.clock]), a.global_t)
+
+
+def _stats_dict(arr) -> dict:
+    vals = [float(x) for x in arr]
+    out = {}
+    for k, x in zip(L.STAT_FIELDS, vals):
+        out[k] = x if k.startswith("sum_") else int(x)
+    return out
+
+
+class AdamWGS:
+    """Fused sparse Adam + DAR + RSR optimizer over 3DGS parameter groups.
+
+    ``params``: list of dicts ``{"params": [tensor], "lr": float, "name": str}``
+    (optionally ``"role"``: plain / position / opacity / scale), one tensor per
+    group, all with the same leading row count N, fp32, contiguous, on one
+    CUDA device.  Gradients are read from ``tensor.grad`` or from the
+    ``grads`` mapping passed to :meth:`step`.
+    """
+
+    def __init__(self, params, *, mode: str = "adamw-gs", betas=(0.9, 0.999), eps: float = 1e-8,
+                 lambda_o: float = 0.0, lambda_s: float = 0.0, ct_opacity: float = 10.0,
+                 ct_scale: float = 10.0, round_n_pixels: bool = True, check: str = "fused",
+                 errors: str = "raise"):
+        validate_hyper(mode, betas[0], betas[1], eps, ct_opacity, ct_scale)
+        if check not in CHECKS:
+            raise ConfigError(f"check must be one of {CHECKS}")
+        if errors not in ERRORS:
+            raise ConfigError(f"errors must be one of {ERRORS}")
+        self.mode = mode
+        self.beta1, self.beta2 = float(betas[0]), float(betas[1])
+        self.eps = float(eps)
+        self.lambda_o, self.lambda_s = float(lambda_o), float(lambda_s)
+        self.ct_opacity, self.ct_scale = float(ct_opacity), float(ct_scale)
+        self.round_n_pixels = bool(round_n_pixels)
+        self.check, self.errors = check, errors
+
+        self.param_groups = []
+        for i, g in enumerate(params):
+            ps = g["params"]
+            ps = [ps] if isinstance(ps, torch.Tensor) else list(ps)
+            if len(ps) != 1:
+                raise ConfigError("each attribute group holds exactly one tensor")
+            name = g.get("name", f"group{i}")
+            self.param_groups.append({"params": ps, "lr": float(g["lr"]), "name": name,
+                                      "role": role_of(name, g.get("role"))})
+        if not self.param_groups:
+            raise ConfigError("no parameter groups")
+        first = self.param_groups[0]["params"][0]
+        self.device = first.device
+        self.n_rows = int(first.shape[0])
+        for g in self.param_groups:
+            p = g["params"][0]
+            if p.device != self.device or p.shape[0] != self.n_rows:
+                raise ConfigError(f"group {g['name']}: all groups must share device and row count")
+            if p.dtype != torch.float32 or not p.is_contiguous():
+                raise ConfigError(f"group {g['name']}: parameters must be contiguous fp32")
+        self.state = MomentState.zeros_like({g["name"]: g["params"][0] for g in self.param_groups})
+        self.engine = StepEngine(self.n_rows, self.device, self.beta1, self.beta2)
+        self._stats_host = torch.zeros(L.GS_STEP_STATS, dtype=torch.float64, pin_memory=True)
+        self._pending = None
+        self._last_ctx = None
+
+    # ------------------------------------------------------------------ helpers
+    def _bindings(self, grads=None, mu_lr_scale: float = 1.0) -> list[GroupBinding]:
+        out = []
+        for g in self.param_groups:
+            p = g["params"][0]
+            name = g["name"]
+            gr = None
+            if grads is not None:
+                gr = grads[name]
+            elif p.grad is not None:
+                gr = p.grad
+            lr = g["lr"] * (mu_lr_scale if g["role"] == L.ROLE_POSITION else 1.0)
+            out.append(GroupBinding(name, g["role"], lr, p.data, gr, self.state.m[name],
+                                    self.state.v[name]))
+        return out
+
+    def _state_bindings(self) -> list[GroupBinding]:
+        return [GroupBinding(g["name"], g["role"], g["lr"], g["params"][0].data, None,
+                             self.state.m[g["name"]], self.state.v[g["name"]])
+                for g in self.param_groups]
+
+    # --------------------------------------------------------------------- step
+    @torch.no_grad()
+    def step(self, visibility: torch.Tensor | None = None, n_pixels: int | None = None, *,
+             mu_lr_scale: float = 1.0, lambda_o: float | None = None,
+             lambda_s: float | None = None, clip: float | None = None, grads=None,
+             n_visible: torch.Tensor | None = None):
+        """One optimizer step over the visible primitives.
+
+        adamw-gs            dar_step (optimizer.py:269-298): ``n_pixels`` = N_I,
+                            ``lambda_o`` / ``lambda_s`` override the configured
+                            lambdas (the pipeline's DAR gating, pipeline.py:316-320).
+        adamw-const[-clip]  adamw_const_step (optimizer.py:301-324); the clip
+                            defaults to C_t(opacity) as the pipeline passes it.
+        sparse-adam         sparse_adam_step with the pipeline's coupled
+                            L1 gradients lambda*R'(theta)/N_v folded in
+                            (pipeline.py:311-315); lambda 0 is plain Sparse Adam.
+        coupled-adam        adam_step_sync over every row, coupled terms on
+                            every row (pipeline.py:305-310).
+        ``n_visible``: device int32 [1] global N_v (index-sharded multi-GPU).
+        """
+        self._raise_pending()
+        mode = self.mode
+        b = self._bindings(grads, mu_lr_scale)
+        eng = self.engine
+        lo = self.lambda_o if lambda_o is None else float(lambda_o)
+        ls = self.lambda_s if lambda_s is None else float(lambda_s)
+        kw = dict(eps=self.eps, check=self.check)
+        if mode == "coupled-adam":
+            self.state.global_t += 1
+            nv = None
+            if (lo != 0.0 or ls != 0.0):
+                if n_visible is None:
+                    if visibility is None:
+                        raise ConfigError("coupled-adam regularization needs the visibility mask")
+                    _, nv = eng.compact(visibility)
+                else:
+                    nv = n_visible
+            stats = eng.step(b, mode, self.state.clock, rows=None, count=None,
+                             lambda_opacity=lo, lambda_scale=ls, global_t=self.state.global_t,
+                             n_visible_dev=nv, **kw)
+            rows = count = None
+        else:
+            if visibility is None:
+                raise ConfigError(f"{mode} needs the visibility mask")
+            rows, count = eng.compact(visibility)
+            if mode == "adamw-gs":
+                if n_pixels is None:
+                    raise ConfigError("adamw-gs needs n_pixels (N_I)")
+                n_i = round_pixel_count(int(n_pixels), self.round_n_pixels)
+                stats = eng.step(b, mode, self.state.clock, rows=rows, count=count,
+                                 lambda_opacity=lo, lambda_scale=ls, clip_opacity=self.ct_opacity,
+                                 clip_scale=self.ct_scale, n_pixels_rounded=n_i, **kw)
+            elif mode in ("adamw-const", "adamw-const-clip"):
+                lo, ls = self.lambda_o, self.lambda_s
+                c = clip if clip is not None else (self.ct_opacity if mode == "adamw-const-clip"
+                                                   else None)
+                m = "adamw-const-clip" if c is not None else "adamw-const"
+                cv = float(c) if c is not None else 0.0
+                stats = eng.step(b, m, self.state.clock, rows=rows, count=count,
+                                 lambda_opacity=lo, lambda_scale=ls, clip_opacity=cv,
+                                 clip_scale=cv, **kw)
+            else:  # sparse-adam (+ coupled)
+                stats = eng.step(b, mode, self.state.clock, rows=rows, count=count,
+                                 lambda_opacity=lo, lambda_scale=ls,
+                                 n_visible_dev=count if n_visible is None else n_visible, **kw)
+        self._last_ctx = (b, rows, count, lo, ls, mode)
+        self._after_step(stats)
+
+    # ---------------------------------------------------------------- errors
+    def _after_step(self, stats: torch.Tensor):
+        if self.errors == "ignore":
+            return
+        self._stats_host.copy_(stats, non_blocking=True)
+        abort = None
+        if self.check == "strict":
+            abort = self.engine.abort.to("cpu", non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(self.device))
+        self._pending = (ev, abort)
+        if self.errors == "raise":
+            self._raise_pending()
+
+    def _raise_pending(self):
+        if self._pending is None:
+            return
+        ev, abort = self._pending
+        self._pending = None
+        ev.synchronize()
+        st = _stats_dict(self._stats_host.tolist())
+        flag = int(abort.item()) if abort is not None else 0
+        bad_g = st["n_bad_grad"] > 0 or (flag & 1)
+        bad_d = st["n_bad_domain"] > 0 or (flag & 2)
+        if not (bad_g or bad_d):
+            return
+        b, rows, count, lo, ls, mode = self._last_ctx
+        if mode == "coupled-adam":
+            rows, count = self.engine.all_rows()
+        g_ids, d_ids = self.engine.bad_rows(b, rows, count, lo, ls)
+        if bad_g:
+            raise GradientError(g_ids)
+        raise DomainError("tau must be finite / log-scale above 80.0 would overflow", d_ids)
+
+    def check_errors(self):
+        """Raise a deferred GradientError / DomainError of the last step, if any."""
+        self._raise_pending()
+
+    def last_stats(self) -> dict:
+        """Per-step statistics of the last step (host sync)."""
+        return _stats_dict(self.engine.stats.tolist())
+
+    # ----------------------------------------------------------- state ops
+    @torch.no_grad()
+    def rsr_apply(self, indices, alpha1: float, alpha2: float):
+        """Re-State Regularization (optimizer.py:327-340): m*=a1, v*=a2, clock kept."""
+        self.engine.rsr_apply(self._state_bindings(), indices, alpha1, alpha2)
+
+    @torch.no_grad()
+    def reset_rows(self, indices):
+        """Fresh state on the rows (optimizer.py:159-165): m = v = 0, t = 0."""
+        self.engine.reset_rows(self._state_bindings(), self.state.clock, indices)
+
+    @torch.no_grad()
+    def moment_stats(self, alive: torch.Tensor | None = None) -> dict:
+        """optimizer.py:489-506 over alive rows."""
+        return _moment_stats(self.engine, self._state_bindings(), alive)
+
+    @torch.no_grad()
+    def classify_active(self, alive: torch.Tensor | None = None) -> tuple[int, int]:
+        """(N_a, N_d) of primitives.py:228-238 (opacity group)."""
+        out = self.engine.stats_all(self._state_bindings(), alive).tolist()
+        return int(out[1]), int(out[0]) - int(out[1])
+
+    def moment_state(self) -> MomentState:
+        return self.state
+
+    def zero_grad(self, set_to_none: bool = True):
+        for g in self.param_groups:
+            p = g["params"][0]
+            if p.grad is not None:
+                if set_to_none:
+                    p.grad = None
+                else:
+                    p.grad.zero_()
+
+    def state_dict(self) -> dict:
+        """Optimizer-state checkpoint (the reference persists none)."""
+        return {"format": "adamw-gs-b200/1", "mode": self.mode, "global_t": self.state.global_t,
+                "clock": self.state.clock.detach().cpu(),
+                "m": {k: t.detach().cpu() for k, t in self.state.m.items()},
+                "v": {k: t.detach().cpu() for k, t in self.state.v.items()},
+                "hyper": {"betas": (self.beta1, self.beta2), "eps": self.eps,
+                          "lambda_o": self.lambda_o, "lambda_s": self.lambda_s,
+                          "ct_opacity": self.ct_opacity, "ct_scale": self.ct_scale,
+                          "lr": {g["name"]: g["lr"] for g in self.param_groups}}}
+
+    def load_state_dict(self, sd: dict):
+        if sd.get("format") != "adamw-gs-b200/1":
+            raise ConfigError("unknown optimizer-state format")
+        with torch.no_grad():
+            self.state.clock.copy_(sd["clock"])
+            for k in self.state.m:
+                self.state.m[k].copy_(sd["m"][k])
+                self.state.v[k].copy_(sd["v"][k])
+        self.state.global_t = int(sd["global_t"])
+
+
+def _moment_stats(engine: StepEngine, bindings, alive) -> dict:
+    out = engine.stats_all(bindings, alive).tolist()
+    n_alive = out[0]
+    res = {}
+    for i, b in enumerate(bindings):
+        s_sq, m_sq, n_pos, s_rt, m_rt = out[2 + 5 * i: 7 + 5 * i]
+        cnt = n_alive * b.width
+        res[b.name] = {
+            "mean_sqrt_v": s_sq / cnt if cnt else 0.0,
+            "max_sqrt_v": m_sq if cnt else 0.0,
+            "mean_abs_m_over_sqrt_v": s_rt / n_pos if n_pos else 0.0,
+            "max_abs_m_over_sqrt_v": m_rt if n_pos else 0.0,
+        }
+    return res

@@ -1,0 +1,98 @@
+"""Host-side state sampling for Re-State Regularization (RSR).
+
+The sampled row set must be bit-identical to the reference's, so it is drawn
+on the host with the reference's counter-based stream contract — Philox
+keyed by (seed, blake2b-4(label), indices) (rng.py:17-30) — and uploaded to
+the GPU as a sorted int32 index list for ``gs_rsr_apply``.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .engine import ConfigError
+
+
+def _label_key(label: str) -> int:
+    """rng.py:12-14 — 32-bit little-endian blake2b digest of the label."""
+    return int.from_bytes(hashlib.blake2b(label.encode("utf-8"), digest_size=4).digest(), "little")
+
+
+def stream(seed: int, label: str, *indices: int) -> np.random.Generator:
+    """rng.py:17-30 — the same (seed, label, indices) always yield the same draws."""
+    key = (_label_key(label), *(int(i) & 0xFFFFFFFF for i in indices))
+    ss = np.random.SeedSequence(entropy=int(seed), spawn_key=key)
+    return np.random.Generator(np.random.Philox(ss))
+
+
+class RngHub:
+    """rng.py:33-43 — stream factory bound to one experiment seed."""
+
+    def __init__(self, seed: int):
+        self.seed = int(seed)
+
+    def stream(self, label: str, *indices: int) -> np.random.Generator:
+        return stream(self.seed, label, *indices)
+
+
+@dataclass(frozen=True)
+class StSSchedule:
+    """Milestone sampling ratios (optimizer.py:343-364); ratio 0 before the first."""
+
+    milestones: tuple = ()
+    interval: int = 10
+
+    def __post_init__(self):
+        iters = [it for it, _ in self.milestones]
+        if any(b <= a for a, b in zip(iters, iters[1:])):
+            raise ConfigError("milestones must be strictly increasing")
+        if any(not (0.0 <= r <= 1.0) for _, r in self.milestones):
+            raise ConfigError("sampling ratios must lie in [0, 1]")
+        if self.interval < 1:
+            raise ConfigError("interval must be >= 1")
+
+    def ratio_at(self, iteration: int) -> float:
+        out = 0.0
+        for it, ratio in self.milestones:
+            if iteration >= it:
+                out = ratio
+        return out
+
+
+@dataclass(frozen=True)
+class RsrConfig:
+    """optimizer.py:367-376."""
+
+    alpha1: float = 0.2
+    alpha2: float = 0.04
+    schedule: StSSchedule = field(default_factory=StSSchedule)
+    enabled: bool = False
+
+    def __post_init__(self):
+        if not (0.0 <= self.alpha1 < 1.0 and 0.0 <= self.alpha2 < 1.0):
+            raise ConfigError("RSR factors must lie in [0, 1)")
+
+
+def stss_sample(schedule: StSSchedule, iteration: int, n_p: int,
+                rng: np.random.Generator) -> np.ndarray:
+    """optimizer.py:379-386 — floor(ratio*N_p) distinct rows, sorted, int64."""
+    ratio = schedule.ratio_at(iteration)
+    k = int(math.floor(ratio * n_p))
+    if k <= 0:
+        return np.empty(0, dtype=np.int64)
+    return np.sort(rng.choice(n_p, size=k, replace=False).astype(np.int64))
+
+
+def shard_rows(indices: np.ndarray, lo: int, hi: int) -> np.ndarray:
+    """Rows of a sorted global sample that fall in the shard [lo, hi), made local.
+
+    Every rank draws the same global sample (same seed/label/boundary) and
+    keeps its slice — no communication.
+    """
+    a = np.searchsorted(indices, lo, side="left")
+    b = np.searchsorted(indices, hi, side="left")
+    return indices[a:b] - lo

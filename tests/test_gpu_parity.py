@@ -1,0 +1,213 @@
+"""GPU parity: the CUDA path through the C ABI vs the oracle (marked gpu).
+
+Tiers:
+  * indices / counts / clocks: bit-exact;
+  * vs the fp32 kernel-order restatement (oracle.step_fp32): elementwise,
+    allowing at most ULP_TOL ulps (float64 ``exp`` may differ in its last
+    bit between libdevice and NumPy, which can flip one fp32 rounding);
+  * vs the float64 reference (golden vectors from the unmodified reference):
+    normwise max|d|/max|ref| <= 1e-6 per tensor.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from _golden import STEP_CASES, Case, normwise
+from oracle import adamw_gs_oracle as O
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda:0"
+ULP_TOL = 2
+NORM_TOL = 1e-6
+
+
+def ulp_diff(a, b):
+    a = np.ascontiguousarray(a, np.float32).view(np.int32).astype(np.int64)
+    b = np.ascontiguousarray(b, np.float32).view(np.int32).astype(np.int64)
+    a = np.where(a < 0, np.int64(-2**31) - a, a)
+    b = np.where(b < 0, np.int64(-2**31) - b, b)
+    return np.abs(a - b)
+
+
+def assert_close_ulp(got, want, what, tol=ULP_TOL):
+    d = ulp_diff(got, want)
+    assert d.max(initial=0) <= tol, f"{what}: max ulp diff {d.max()} (at {np.argmax(d)})"
+
+
+# --------------------------------------------------------------------------
+# K1 compaction
+# --------------------------------------------------------------------------
+
+@pytest.mark.parametrize("n", [0, 1, 15, 16, 17, 4095, 4096, 4097, 100_003, 1_000_000, 6_000_000])
+@pytest.mark.parametrize("p", [0.0, 0.01, 0.3, 1.0])
+def test_compaction_bit_exact(n, p):
+    from paper_2601_16736_b200.engine import StepEngine
+    rng = np.random.default_rng(n + int(p * 100))
+    mask = rng.random(n) < p
+    eng = StepEngine(n, torch.device(DEV), 0.9, 0.999)
+    vis = torch.from_numpy(mask).to(DEV)
+    for _ in range(2):  # second call exercises the epoch-tagged workspace reuse
+        idx, cnt = eng.compact(vis)
+        c = int(cnt.item())
+        ref = np.flatnonzero(mask)
+        assert c == ref.size
+        assert np.array_equal(idx[:c].cpu().numpy(), ref)
+
+
+def test_compaction_coherent_misaligned_and_radii():
+    from paper_2601_16736_b200.engine import StepEngine
+    rng = np.random.default_rng(3)
+    n = 300_001
+    blocks = rng.random((n + 63) // 64) < 0.3
+    mask = np.repeat(blocks, 64)[:n]
+    eng = StepEngine(n, torch.device(DEV), 0.9, 0.999)
+    big = torch.zeros(n + 1, dtype=torch.bool, device=DEV)
+    big[1:] = torch.from_numpy(mask).to(DEV)
+    idx, cnt = eng.compact(big[1:])  # pointer not 16-byte aligned -> scalar path
+    assert np.array_equal(idx[: int(cnt.item())].cpu().numpy(), np.flatnonzero(mask))
+    radii = rng.integers(-3, 4, n).astype(np.int32)
+    idx, cnt = eng.compact(torch.from_numpy(radii).to(DEV))
+    assert np.array_equal(idx[: int(cnt.item())].cpu().numpy(), np.flatnonzero(radii > 0))
+
+
+def test_compaction_many_launches_same_workspace():
+    from paper_2601_16736_b200.engine import StepEngine
+    rng = np.random.default_rng(5)
+    n = 50_000
+    eng = StepEngine(n, torch.device(DEV), 0.9, 0.999)
+    for i in range(50):
+        mask = rng.random(n) < rng.random()
+        idx, cnt = eng.compact(torch.from_numpy(mask).to(DEV))
+        ref = np.flatnonzero(mask)
+        assert int(cnt.item()) == ref.size
+        assert np.array_equal(idx[: ref.size].cpu().numpy(), ref)
+
+
+# --------------------------------------------------------------------------
+# K2 step on the golden cases
+# --------------------------------------------------------------------------
+
+def _gpu_case_run(case: Case, check="fused"):
+    from paper_2601_16736_b200.optimizer import AdamWGS
+    hp = case.hyper()
+    meta = case.meta
+    init = case.init(np.float32)
+    params = {g.name: torch.from_numpy(init[g.name]).to(DEV) for g in case.layout}
+    coupled = case.layout is O.LAYOUT_REF2D
+    opt = AdamWGS([{"params": [params[g.name]], "lr": hp.lr[g.name], "name": g.name}
+                   for g in case.layout], mode=case.mode, betas=(hp.beta1, hp.beta2), eps=hp.eps,
+                  lambda_o=hp.lambda_o if (coupled or case.mode != "sparse-adam") else 0.0,
+                  lambda_s=hp.lambda_s if (coupled or case.mode != "sparse-adam") else 0.0,
+                  ct_opacity=hp.ct_opacity, ct_scale=hp.ct_scale, check=check)
+    stats = []
+    for s in range(case.steps):
+        gr = case.grads(s, np.float32)
+        grads = {k: torch.from_numpy(v).to(DEV) for k, v in gr.items()}
+        vis = torch.from_numpy(case.vis[s]).to(DEV)
+        opt.step(vis, meta.get("n_pixels"), mu_lr_scale=meta["mu_lr_scale"],
+                 clip=meta.get("clip"), grads=grads)
+        stats.append(opt.last_stats())
+    out = {k: p.cpu().numpy() for k, p in params.items()}
+    m = {k: t.cpu().numpy() for k, t in opt.state.m.items()}
+    v = {k: t.cpu().numpy() for k, t in opt.state.v.items()}
+    return out, m, v, opt.state.clock.cpu().numpy(), stats
+
+
+def _oracle_fp32(case: Case):
+    from test_oracle import coupled_lambdas
+    hp = case.hyper()
+    p = case.init(np.float32)
+    m = {g.name: np.zeros((case.n, g.width), np.float32) for g in case.layout}
+    v = {g.name: np.zeros((case.n, g.width), np.float32) for g in case.layout}
+    clock = np.zeros(case.n, np.int32)
+    lut = O.bias_lut_f32(hp.beta1, hp.beta2, 20000)
+    stats = []
+    for s in range(case.steps):
+        g = case.grads(s, np.float32)
+        vis = case.vis[s]
+        rows = np.flatnonzero(vis) if case.mode != "coupled-adam" else np.arange(case.n)
+        stats.append(O.step_fp32(case.mode, case.layout, p, g, m, v, clock, rows, hp,
+                                 n_pixels=case.meta.get("n_pixels"),
+                                 mu_lr_scale=case.meta["mu_lr_scale"], clip=case.meta.get("clip"),
+                                 n_visible_norm=int(vis.sum()), global_t=s + 1, lut=lut,
+                                 **coupled_lambdas(case)))
+    return p, m, v, clock, stats
+
+
+@pytest.mark.parametrize("name", STEP_CASES)
+@pytest.mark.parametrize("check", ["fused", "strict"])
+def test_golden_step_parity(name, check):
+    case = Case(name)
+    out, m, v, clock, stats = _gpu_case_run(case, check)
+    # tier (i): vs the float64 reference
+    eo, em, ev, et = case.expected()
+    assert np.array_equal(clock, et)
+    for g in case.layout:
+        assert normwise(out[g.name], eo[g.name]) <= NORM_TOL, g.name
+        assert normwise(m[g.name], em[g.name]) <= NORM_TOL, g.name
+        assert normwise(v[g.name], ev[g.name]) <= NORM_TOL, g.name
+    # tier (ii): vs the fp32 restatement of the kernel
+    po, mo, vo, co, so = _oracle_fp32(case)
+    assert np.array_equal(clock, co)
+    for g in case.layout:
+        assert_close_ulp(out[g.name], po[g.name], f"{name}/{g.name}/param")
+        assert_close_ulp(m[g.name], mo[g.name], f"{name}/{g.name}/m")
+        assert_close_ulp(v[g.name], vo[g.name], f"{name}/{g.name}/v")
+    if check == "fused":
+        for s_gpu, s_ref in zip(stats, so):
+            for k, want in s_ref.items():
+                if k.startswith("sum_"):
+                    assert s_gpu[k] == pytest.approx(want, rel=1e-6, abs=1e-30), k
+                else:
+                    assert s_gpu[k] == want, k
+
+
+# --------------------------------------------------------------------------
+# C1: 100k SH3, 50% visibility, 100 steps (BASELINE.json configs[0])
+# --------------------------------------------------------------------------
+
+@pytest.mark.parametrize("family", ["bernoulli", "coherent"])
+def test_c1_100_steps_vs_oracles(family):
+    from paper_2601_16736_b200 import synthetic as S
+    from paper_2601_16736_b200.optimizer import AdamWGS
+    n, steps = 100_000, 100
+    cfg = S.WorkloadConfig(n=n, p_vis=0.5, mask_family=family, seed=1)
+    host = S.make_params(cfg)
+    params = {k: torch.from_numpy(v).to(DEV) for k, v in host.items()}
+    opt = AdamWGS(S.param_groups(params, cfg), mode="adamw-gs", lambda_o=cfg.lambda_o,
+                  lambda_s=cfg.lambda_s)
+    # oracles
+    lay = O.LAYOUT_SH3
+    hp = O.Hyper(lr=S.LR_SH3, lambda_o=cfg.lambda_o, lambda_s=cfg.lambda_s)
+    p32 = {k: v.copy() for k, v in host.items()}
+    m32 = {g.name: np.zeros((n, g.width), np.float32) for g in lay}
+    v32 = {g.name: np.zeros((n, g.width), np.float32) for g in lay}
+    c32 = np.zeros(n, np.int32)
+    p64 = {k: v.astype(np.float64) for k, v in host.items()}
+    m64 = {g.name: np.zeros((n, g.width)) for g in lay}
+    v64 = {g.name: np.zeros((n, g.width)) for g in lay}
+    t64 = np.zeros(n, np.int64)
+    lut = O.bias_lut_f32(0.9, 0.999, steps + 2)
+    for s in range(steps):
+        vis = S.visibility(cfg, s)
+        g = S.step_grads(cfg, s, vis)
+        opt.step(torch.from_numpy(vis).to(DEV), cfg.n_pixels,
+                 grads={k: torch.from_numpy(x).to(DEV) for k, x in g.items()})
+        O.step_fp32("adamw-gs", lay, p32, g, m32, v32, c32, np.flatnonzero(vis), hp,
+                    n_pixels=cfg.n_pixels, lut=lut)
+        O.dar_step_f64(lay, p64, {k: x.astype(np.float64) for k, x in g.items()}, m64, v64, t64,
+                       vis, hp, cfg.n_pixels)
+    clock = opt.state.clock.cpu().numpy()
+    assert np.array_equal(clock, c32)
+    assert np.array_equal(clock, t64)
+    for gname in host:
+        got_p = params[gname].cpu().numpy()
+        got_m = opt.state.m[gname].cpu().numpy()
+        got_v = opt.state.v[gname].cpu().numpy()
+        assert_close_ulp(got_p, p32[gname], f"{gname}/param")
+        assert_close_ulp(got_m, m32[gname], f"{gname}/m")
+        assert_close_ulp(got_v, v32[gname], f"{gname}/v")
+        assert normwise(got_p, p64[gname]) <= NORM_TOL, gname
+        assert normwise(got_m, m64[gname]) <= NORM_TOL, gname
+        assert normwise(got_v, v64[gname]) <= NORM_TOL, gname
