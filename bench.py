@@ -81,6 +81,8 @@ def parse():
     ap.add_argument("--ref-seconds", type=float, default=150.0,
                     help="budget of the whole --impl reference run")
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--layout", default="rows", choices=["rows", "groups"],
+                    help="optimizer-state layout (row records or per-group tensors)")
     return ap.parse_args()
 
 
@@ -263,6 +265,7 @@ def workload_config(args, wl, p_vis, world):
             "rsr": {"ratio": RSR_RATIO, "alpha1": ALPHA1, "alpha2": ALPHA2,
                     "interval": RSR_INTERVAL} if wl["rsr"] else None,
             "reset_fraction": wl["reset"] or None, "check": args.check,
+            "state_layout": args.layout,
             "l2": "inputs larger than L2 (working set >> 126 MB)" if n >= 1_000_000 else
                   "L2 flushed between timed steps",
             "parallelism": f"index-sharded x{world}"}
@@ -290,7 +293,7 @@ def ours(args, wl, p_vis):
                            lambda_o=wl["lo"], lambda_s=wl["ls"])
     params = S.make_params_device(cfg, dev)
     opt = AdamWGS(S.param_groups(params), mode=wl["mode"], lambda_o=wl["lo"], lambda_s=wl["ls"],
-                  check=args.check, errors="defer")
+                  check=args.check, errors="defer", state_layout=args.layout)
     total_steps = args.warmup + args.steps
     masks = [S.visibility_device(cfg, s, dev) for s in range(total_steps)]
     n_vis = torch.stack([m.sum() for m in masks]).cpu().numpy().astype(np.int64)
@@ -332,15 +335,12 @@ def ours(args, wl, p_vis):
         if timed:
             e1.record()
             k2_events.append((e0, e1))
-        launches[0] += 2 + (1 if args.check == "strict" else 0)
         ev = events.get(it)
         if ev:
             if "rsr" in ev:
                 opt.rsr_apply(ev["rsr"], ALPHA1, ALPHA2)
-                launches[0] += 1
             if "reset" in ev:
                 opt.reset_rows(ev["reset"])
-                launches[0] += 1
         if world > 1:
             stats_sum.copy_(opt.engine.stats)
             dist.all_reduce(stats_sum)
@@ -350,7 +350,7 @@ def ours(args, wl, p_vis):
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    launches[0] = 0
+    launches0 = opt.engine.launches
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
@@ -360,6 +360,7 @@ def ours(args, wl, p_vis):
         end.record()
         torch.cuda.synchronize()
     ms = start.elapsed_time(end)
+    launches[0] = opt.engine.launches - launches0
     k2_ms = [a.elapsed_time(b) for a, b in k2_events]
     opt.check_errors()
     ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
@@ -403,7 +404,8 @@ def ours(args, wl, p_vis):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak,
                          "traffic": traffic_from_profiles(args.workload, args.mask, p_vis),
-                         "kernel": "gs::step_kernel (K2)", "peak_source": peak_src,
+                         "kernel": "gs::step_rows_kernel (K2)" if args.layout == "rows"
+                                   else "gs::step_kernel (K2)", "peak_source": peak_src,
                          "k2_ms_avg": k2_avg_ms,
                          "k2_bytes_per_launch": sum(k2_bytes) / len(k2_bytes),
                          "bytes_per_visible": 28 * width + 12,
@@ -428,11 +430,11 @@ def _step_k2(opt, grads, rows, count, wl):
         eng.step(b, "adamw-gs", opt.state.clock, rows=rows, count=count, eps=opt.eps,
                  lambda_opacity=wl["lo"], lambda_scale=wl["ls"], clip_opacity=opt.ct_opacity,
                  clip_scale=opt.ct_scale, n_pixels_rounded=round_pixel_count(1_000_000),
-                 check=opt.check)
+                 check=opt.check, record=opt.state.record)
     else:
         eng.step(b, wl["mode"], opt.state.clock, rows=rows, count=count, eps=opt.eps,
                  lambda_opacity=wl["lo"], lambda_scale=wl["ls"], n_visible_dev=count,
-                 check=opt.check)
+                 check=opt.check, record=opt.state.record)
     opt._last_ctx = (b, rows, count, wl["lo"], wl["ls"], wl["mode"])
     opt._after_step(eng.stats)
 

@@ -162,6 +162,32 @@ int gs_stats_all(const gs_group* groups, int32_t n_groups, int64_t n_rows,
                  const uint8_t* alive, float active_logit, double* out, void* ws,
                  size_t ws_bytes, void* stream);
 
+/* ---- row-record optimizer state (the default AdamWGS layout) -------------
+ * record[row] = { (m_0, v_0), ..., (m_{P-1}, v_{P-1}), (clock:int32, pad) },
+ * P = sum of the group widths in group order, record_stride >= 2*(P+1)
+ * floats (even).  The exp_avg / exp_avg_sq fields of gs_group are ignored by
+ * these entry points; param / grad / width / role / lr are used.  One
+ * contiguous record per visible row replaces 2*n_groups narrow scattered
+ * spans plus the clock (see paper_2601_16736_b200/csrc/gs_step_rows.cu). */
+size_t gs_step_rows_workspace_bytes(void);
+/* Select the (rows-in-flight, residency) variant of the SH-3 step kernel
+ * (0 = default; tuning only, results are identical).  Returns the previous
+ * variant.  The GS_ROWS_VARIANT environment variable sets the initial one. */
+int32_t gs_set_rows_variant(int32_t variant);
+int gs_step_rows(const gs_group* groups, int32_t n_groups, const gs_step_cfg* cfg,
+                 const int32_t* rows, const int32_t* n_rows_dev, int64_t max_rows,
+                 float* record, int64_t record_stride, double* stats_out, void* ws,
+                 size_t ws_bytes, void* stream);
+int gs_rsr_apply_rows(float* record, int64_t record_stride, int32_t n_elems,
+                      const int32_t* rows, int64_t k, double alpha1, double alpha2,
+                      void* stream);
+int gs_reset_rows_rows(float* record, int64_t record_stride, int32_t n_elems,
+                       const int32_t* rows, int64_t k, void* stream);
+int gs_stats_all_rows(const gs_group* groups, int32_t n_groups, int64_t n_rows,
+                      const float* record, int64_t record_stride, const uint8_t* alive,
+                      float active_logit, double* out, void* ws, size_t ws_bytes,
+                      void* stream);
+
 #ifdef __cplusplus
 }
 #endif

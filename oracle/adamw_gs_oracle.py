@@ -15,11 +15,12 @@ group layout (the reference's 2D ``mu/kappa/rot/tau/color`` testbed or the
     imports ``splatlab`` and drives it through the SH-3 adapter of SURVEY §8(c)).
 
 ``step_fp32``
-    The exact fp32 operation order of the CUDA kernel
-    (``paper_2601_16736_b200/csrc/gs_step.cu``): every fp32 op correctly
-    rounded, no FMA contraction, transcendental / DAR terms in float64 rounded
-    once.  The GPU path must agree with it elementwise (bit-exact up to the
-    last-ulp behaviour of ``exp`` in float64).
+    The exact fp32 operation order of the CUDA kernels
+    (``paper_2601_16736_b200/csrc/gs_common.cuh::update_element``): every
+    operation one correctly rounded fp32 op, no FMA contraction, the
+    activation derivatives through the kernel's own deterministic ``gs_expf``,
+    bias-correction factors from the same float64-derived LUT.  The GPU path
+    must agree with it bit for bit.
 
 Every function cites the reference file:line it follows.  Rows are 2-D
 ``(N, W)`` arrays for every group (width-1 groups are ``(N, 1)``).
@@ -405,12 +406,39 @@ STAT_FIELDS = ("n_visible", "n_stepped", "n_bad_grad", "n_bad_domain", "n_active
                "sum_extra_scale")
 
 
-def _reg_deriv_f64(role, theta32):
-    """R'(theta) in float64 from fp32 theta: sigma' for opacity, exp for scale."""
-    th = theta32.astype(F64)
+_EXP_C = tuple(F32(c) for c in (1.0 / 5040, 1.0 / 720, 1.0 / 120, 1.0 / 24, 1.0 / 6, 0.5, 1.0,
+                                  1.0))
+
+
+def gs_expf(x):
+    """The kernel's deterministic fp32 exp (csrc/gs_common.cuh::gs_expf).
+
+    Cody-Waite reduction x = n*ln2 + r, degree-7 Taylor polynomial in Horner
+    form, exact power-of-two scaling; every operation one rounded fp32 op.
+    Inputs below -86 return 0.
+    """
+    x = np.asarray(x, F32)
+    n = np.rint(x * F32(1.442695))
+    r = x - n * F32(0.693145751953125)
+    r = r - n * F32(1.4286068e-06)
+    p = _EXP_C[0] * np.ones_like(r)
+    for c in _EXP_C[1:]:
+        p = p * r + c
+    with np.errstate(over="ignore", invalid="ignore"):
+        scale = np.ldexp(np.ones_like(p), np.clip(n, -126, 127).astype(np.int32)).astype(F32)
+    out = (p * scale).astype(F32)
+    return np.where(x < F32(-86.0), F32(0.0), out).astype(F32)
+
+
+def _reg_deriv_f32(role, theta32):
+    """R'(theta) in fp32 (gs_common.cuh::reg_deriv): sigma' = e/(1+e)^2 with
+    e = exp(-|tau|) for opacity (primitives.py:51-66), exp(kappa) for scale."""
+    th = np.asarray(theta32, F32)
     if role == "opacity":
-        return opacity_derivative_f64(th)
-    return np.exp(th)
+        e = gs_expf(-np.abs(th))
+        d = F32(1.0) + e
+        return (e / (d * d)).astype(F32)
+    return gs_expf(th)
 
 
 def _domain_bad(role, theta32):
@@ -493,20 +521,34 @@ def step_fp32(mode, layout, params, grads, m, v, clock, rows, hp, *, n_pixels=No
     # ---- clocks and bias correction --------------------------------------
     clock[r] += 1
     tb = np.full(r.size, int(global_t)) if dense else clock[r].astype(np.int64)
-    tb = np.minimum(tb, lut.shape[0] - 1)
-    c1 = lut[tb, 0][:, None]
-    c2 = lut[tb, 1][:, None]
+    inside = tb < lut.shape[0]
+    c1 = np.empty(r.size, F32)
+    c2 = np.empty(r.size, F32)
+    c1[inside] = lut[tb[inside], 0]
+    c2[inside] = lut[tb[inside], 1]
+    tf = tb[~inside].astype(F64)          # past the table: float64 formula, rounded once
+    c1[~inside] = (1.0 / (1.0 - np.power(hp.beta1, tf))).astype(F32)
+    c2[~inside] = (1.0 / (1.0 - np.power(hp.beta2, tf))).astype(F32)
+    c1 = c1[:, None]
+    c2 = c2[:, None]
 
+    lam32 = {"opacity": F32(lo), "scale": F32(ls)}
+    cap32 = {"opacity": F32(hp.ct_opacity), "scale": F32(hp.ct_scale)}
+    if mode in ("adamw-const", "adamw-const-clip") and (clip is not None or
+                                                        mode == "adamw-const-clip"):
+        c = clip if clip is not None else hp.ct_opacity          # pipeline.py:323-325
+        cap32 = {"opacity": F32(c), "scale": F32(c)}
+    inv_ni = F32(1.0 / n_i) if n_i else F32(0.0)
+    inv_nv = (F32(1.0) / F32(n_visible_norm)) if (coupled and n_visible_norm) else F32(0.0)
     for g in layout:
         th = params[g.name][r]
         gr = grads[g.name][r]
         mm = m[g.name][r]
         vv = v[g.name][r]
-        if coupled and g.role in ("opacity", "scale"):
-            lam = lo_c if g.role == "opacity" else ls_c
-            if lam != 0.0:
-                regc = lam * _reg_deriv_f64(g.role, th) / float(n_visible_norm)
-                gr = (gr.astype(F64) + regc).astype(F32)
+        lam = lam32.get(g.role, F32(0.0)) if g.role in ("opacity", "scale") else F32(0.0)
+        if coupled and g.role in ("opacity", "scale") and lam != 0.0 and (lo_c or ls_c):
+            # loss.py:177-198 folded in: g += (lambda * R') * (1/N_v)
+            gr = gr + (lam * _reg_deriv_f32(g.role, th)) * inv_nv
         d = gr - mm
         m_new = mm + a1 * d
         g2 = gr * gr
@@ -516,29 +558,25 @@ def step_fp32(mode, layout, params, grads, m, v, clock, rows, hp, *, n_pixels=No
         vh = v_new * c2
         den = np.sqrt(vh) + eps
         step = mh / den
-        if g.role in ("opacity", "scale") and not coupled:
-            lam = lo if g.role == "opacity" else ls
-            if lam != 0.0:
-                deriv = _reg_deriv_f64(g.role, th)
-                if mode == "adamw-gs":
-                    cap = hp.ct_opacity if g.role == "opacity" else hp.ct_scale
-                    x = lam * (deriv / n_i) / den.astype(F64)
-                    clipped = x >= cap
-                    ex64 = np.minimum(x, cap)
-                else:
-                    x = lam * deriv
-                    if mode == "adamw-const-clip" or clip is not None:
-                        cap = clip if clip is not None else hp.ct_opacity
-                        clipped = x >= cap
-                        ex64 = np.minimum(x, cap)
-                    else:
-                        clipped = np.zeros(x.shape, bool)
-                        ex64 = x
-                ex = ex64.astype(F32)
-                step = step + ex
-                key = "opacity" if g.role == "opacity" else "scale"
-                stats["n_clip_" + key] += int(clipped.sum())
-                stats["sum_extra_" + key] += float(ex.astype(F64).sum())
+        if g.role in ("opacity", "scale") and not coupled and lam != 0.0:
+            deriv = _reg_deriv_f32(g.role, th)
+            cap = cap32[g.role]
+            if mode == "adamw-gs":
+                # min(lambda * (R' / N_I') / (sqrt(v^) + eps), C_t), optimizer.py:285-295
+                x = ((lam * deriv) * inv_ni) / den
+                clipped = x >= cap
+                ex = np.where(clipped, cap, x).astype(F32)
+            elif mode == "adamw-const-clip" or clip is not None:
+                x = lam * deriv                                   # optimizer.py:314-315
+                clipped = x >= cap
+                ex = np.where(clipped, cap, x).astype(F32)
+            else:
+                ex = (lam * deriv).astype(F32)
+                clipped = np.zeros(ex.shape, bool)
+            step = step + ex
+            key = "opacity" if g.role == "opacity" else "scale"
+            stats["n_clip_" + key] += int(clipped.sum())
+            stats["sum_extra_" + key] += float(ex.astype(F64).sum())
         lr = F32(hp.lr[g.name] * (mu_lr_scale if g.role == "position" else 1.0))
         th_new = th - lr * step
         if g.role == "opacity":

@@ -73,6 +73,18 @@ SIGNATURES = {
     "gs_reset_rows": (C.c_int, [C.POINTER(GsGroup), C.c_int32, C.c_void_p, C.c_void_p,
                                 C.c_int64, C.c_void_p]),
     "gs_stats_workspace_bytes": (C.c_size_t, [C.c_int32]),
+    "gs_step_rows_workspace_bytes": (C.c_size_t, []),
+    "gs_set_rows_variant": (C.c_int32, [C.c_int32]),
+    "gs_step_rows": (C.c_int, [C.POINTER(GsGroup), C.c_int32, C.POINTER(GsStepCfg), C.c_void_p,
+                               C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p,
+                               C.c_void_p, C.c_size_t, C.c_void_p]),
+    "gs_rsr_apply_rows": (C.c_int, [C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_int64,
+                                    C.c_double, C.c_double, C.c_void_p]),
+    "gs_reset_rows_rows": (C.c_int, [C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_int64,
+                                     C.c_void_p]),
+    "gs_stats_all_rows": (C.c_int, [C.POINTER(GsGroup), C.c_int32, C.c_int64, C.c_void_p,
+                                    C.c_int64, C.c_void_p, C.c_float, C.c_void_p, C.c_void_p,
+                                    C.c_size_t, C.c_void_p]),
     "gs_stats_all": (C.c_int, [C.POINTER(GsGroup), C.c_int32, C.c_int64, C.c_void_p, C.c_float,
                                C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
 }

@@ -19,22 +19,92 @@ constexpr int kThreads = 256;  // rows per chunk == threads per CTA
 
 __device__ __forceinline__ bool finitef(float x) { return isfinite(x); }
 
-// Stable float64 sigmoid derivative, primitives.py:51-66.
-__device__ __forceinline__ double sigmoid_deriv_f64(double t) {
-  double o;
-  if (t >= 0.0) {
-    o = __ddiv_rn(1.0, __dadd_rn(1.0, exp(-t)));
-  } else {
-    double e = exp(t);
-    o = __ddiv_rn(e, __dadd_rn(1.0, e));
-  }
-  return __dmul_rn(o, __dsub_rn(1.0, o));
+// Deterministic fp32 exp: Cody-Waite reduction x = n*ln2 + r, degree-7
+// Taylor polynomial in Horner form, exact power-of-two scaling.  Every step is
+// one correctly rounded fp32 operation, so oracle/adamw_gs_oracle.py::gs_expf
+// reproduces it bit for bit (max error ~2 ulp).  Inputs below -86 return 0
+// (the result would be subnormal; the penalty term is then negligible).
+__device__ __forceinline__ float gs_expf(float x) {
+  if (x < -86.0f) return 0.0f;
+  const float n = rintf(__fmul_rn(x, 1.442695f));
+  float r = __fsub_rn(x, __fmul_rn(n, 0.693145751953125f));
+  r = __fsub_rn(r, __fmul_rn(n, 1.4286068e-06f));
+  float p = 1.984127e-04f;                      // 1/5040
+  p = __fadd_rn(__fmul_rn(p, r), 1.3888889e-03f);  // 1/720
+  p = __fadd_rn(__fmul_rn(p, r), 8.333334e-03f);  // 1/120
+  p = __fadd_rn(__fmul_rn(p, r), 4.1666668e-02f);  // 1/24
+  p = __fadd_rn(__fmul_rn(p, r), 1.6666667e-01f);  // 1/6
+  p = __fadd_rn(__fmul_rn(p, r), 0.5f);
+  p = __fadd_rn(__fmul_rn(p, r), 1.0f);
+  p = __fadd_rn(__fmul_rn(p, r), 1.0f);
+  return __fmul_rn(p, __int_as_float(((int)n + 127) << 23));
 }
 
-// R'(theta) of the L1 penalty on the activated attribute (primitives.py:62-84).
-__device__ __forceinline__ double reg_deriv_f64(int role, float theta) {
-  double t = (double)theta;
-  return role == GS_ROLE_OPACITY ? sigmoid_deriv_f64(t) : exp(t);
+// R'(theta) of the L1 penalty on the activated attribute (primitives.py:62-84):
+// sigma'(tau) = e / (1 + e)^2 with e = exp(-|tau|) (both branches of the
+// stable sigmoid give this form), and exp(kappa) for the scale.
+__device__ __forceinline__ float reg_deriv(int role, float theta) {
+  if (role == GS_ROLE_OPACITY) {
+    const float e = gs_expf(-fabsf(theta));
+    const float d = __fadd_rn(1.0f, e);
+    return __fdiv_rn(e, __fmul_rn(d, d));
+  }
+  return gs_expf(theta);
+}
+
+// Step constants shared by the per-group and row-record kernels.
+struct StepConsts {
+  float a1, a2, eps;
+  float lam_op, lam_sc;    // penalty lambdas (0 = none)
+  float cap_op, cap_sc;    // C_t / clip
+  float inv_ni, inv_nv;    // 1/N_I' (adamw-gs), 1/N_v (coupled)
+};
+
+// The per-element update, identical for every kernel and mirrored by
+// oracle/adamw_gs_oracle.py::step_fp32.  MODE is a GS_MODE_*.  Returns the
+// new theta / m / v; ex is the penalty term added to the step (0 if none).
+template <int MODE>
+__device__ __forceinline__ void update_element(int role, float lr, float th, float g, float mm,
+                                               float vv, float2 bc, const StepConsts& K,
+                                               float& th_out, float& m_out, float& v_out,
+                                               float& ex, bool& clipped) {
+  constexpr bool kCoupled = MODE == GS_MODE_COUPLED_ADAM || MODE == GS_MODE_SPARSE_ADAM;
+  const float lam = role == GS_ROLE_OPACITY ? K.lam_op : role == GS_ROLE_SCALE ? K.lam_sc : 0.0f;
+  ex = 0.0f;
+  clipped = false;
+  if (kCoupled && lam != 0.0f) {
+    // loss.py:177-198 folded in: g += lambda * R'(theta) / N_v
+    g = __fadd_rn(g, __fmul_rn(__fmul_rn(lam, reg_deriv(role, th)), K.inv_nv));
+  }
+  const float d = __fsub_rn(g, mm);
+  const float mn = __fadd_rn(mm, __fmul_rn(K.a1, d));
+  const float g2 = __fmul_rn(g, g);
+  const float ee = __fsub_rn(g2, vv);
+  const float vn = __fadd_rn(vv, __fmul_rn(K.a2, ee));
+  const float mh = __fmul_rn(mn, bc.x);
+  const float vh = __fmul_rn(vn, bc.y);
+  const float den = __fadd_rn(__fsqrt_rn(vh), K.eps);
+  float step = __fdiv_rn(mh, den);
+  if (!kCoupled && lam != 0.0f) {
+    const float deriv = reg_deriv(role, th);
+    const float cap = role == GS_ROLE_OPACITY ? K.cap_op : K.cap_sc;
+    if (MODE == GS_MODE_ADAMW_GS) {
+      // optimizer.py:285-295: min(lambda * (R' / N_I') / (sqrt(v^) + eps), C_t)
+      const float x = __fdiv_rn(__fmul_rn(__fmul_rn(lam, deriv), K.inv_ni), den);
+      clipped = x >= cap;
+      ex = clipped ? cap : x;
+    } else if (MODE == GS_MODE_ADAMW_CONST_CLIP) {
+      const float x = __fmul_rn(lam, deriv);          // optimizer.py:314-315
+      clipped = x >= cap;
+      ex = clipped ? cap : x;
+    } else {
+      ex = __fmul_rn(lam, deriv);
+    }
+    step = __fadd_rn(step, ex);
+  }
+  th_out = __fsub_rn(th, __fmul_rn(lr, step));
+  m_out = mn;
+  v_out = vn;
 }
 
 // Domain of the activation (primitives.py:44-48,78-84).
@@ -43,16 +113,12 @@ __device__ __forceinline__ bool domain_bad(int role, float theta) {
   return role == GS_ROLE_SCALE && (double)theta > 80.0;
 }
 
-// Bias-correction factors for clock t (t >= 1).
-__device__ __forceinline__ float2 bias_factors(const float* lut, int lut_len, int t,
-                                               double beta1, double beta2) {
-  if (t < lut_len) {
-    return reinterpret_cast<const float2*>(lut)[t];
-  }
-  double td = (double)t;
-  float c1 = __double2float_rn(__ddiv_rn(1.0, __dsub_rn(1.0, pow(beta1, td))));
-  float c2 = __double2float_rn(__ddiv_rn(1.0, __dsub_rn(1.0, pow(beta2, td))));
-  return make_float2(c1, c2);
+// Bias-correction factors for clock t (t >= 1).  The host builds the LUT
+// until both factors round to exactly 1.0f, so clamping t is exact.
+__device__ __forceinline__ float2 bias_factors(const float* lut, int lut_len, int t, double,
+                                               double) {
+  const int i = t < lut_len ? t : lut_len - 1;
+  return __ldg(reinterpret_cast<const float2*>(lut) + i);
 }
 
 __device__ __forceinline__ double warp_sum(double x) {
@@ -108,6 +174,22 @@ __device__ __forceinline__ bool last_block_arrive(unsigned int* counter) {
   __syncthreads();
   if (s_last) __threadfence();
   return s_last;
+}
+
+// Host: fp32 constants of a step from the C-ABI configuration (every value
+// rounded once from float64, as the oracle does).
+inline StepConsts make_consts(const gs_step_cfg* cfg) {
+  StepConsts K;
+  K.a1 = cfg->one_minus_beta1;
+  K.a2 = cfg->one_minus_beta2;
+  K.eps = cfg->eps;
+  K.lam_op = (float)cfg->lambda_opacity;
+  K.lam_sc = (float)cfg->lambda_scale;
+  K.cap_op = (float)cfg->clip_opacity;
+  K.cap_sc = (float)cfg->clip_scale;
+  K.inv_ni = cfg->n_pixels_rounded > 0.0 ? (float)(1.0 / cfg->n_pixels_rounded) : 0.0f;
+  K.inv_nv = 0.0f;  // coupled modes: set on the device from N_v
+  return K;
 }
 
 }  // namespace gs

@@ -20,6 +20,7 @@ namespace gs {
 constexpr int kCompactItems = 16;                              // rows per thread
 constexpr int kCompactTile = kThreads * kCompactItems;         // 4096 rows per CTA
 constexpr uint64_t kFlagAgg = 1ull, kFlagPre = 2ull;
+constexpr int kLookPerLane = 8;  // look-back window 32*8 tiles
 
 struct CompactHeader {
   unsigned int epoch;
@@ -149,33 +150,46 @@ __global__ void __launch_bounds__(kThreads)
       if (lane == 0) s_excl = 0;
     } else {
       if (lane == 0) st_status(&status[tile], tag | (kFlagAgg << 32) | total);
+      // warp-wide look-back, kLookback predecessors per round (8 per lane,
+      // lane 0 nearest): one L2 round trip covers 256 tiles, so the chain of
+      // dependent rounds is ~tile/256 instead of ~tile/32
       uint32_t excl = 0;
       int64_t end = tile - 1;
       while (true) {
-        int64_t j = end - lane;
-        uint64_t s = 0;
-        bool ready;
-        do {
-          if (j >= 0) {
-            s = ld_status(&status[j]);
-            ready = ((s >> 34) == ep) && (((s >> 32) & 3ull) != 0ull);
+        uint32_t sum_all = 0, sum_upto = 0;
+        int first_pre = kLookPerLane;
+#pragma unroll
+        for (int k = 0; k < kLookPerLane; ++k) {
+          const int64_t j = end - (int64_t)lane * kLookPerLane - k;
+          uint64_t sv;
+          if (j < 0) {
+            sv = kFlagPre << 32;  // virtual inclusive prefix 0 before tile 0
           } else {
-            s = (kFlagPre << 32);
-            ready = true;
+            do {
+              sv = ld_status(&status[j]);
+            } while (!(((sv >> 34) == ep) && (((sv >> 32) & 3ull) != 0ull)));
           }
-        } while (!__all_sync(0xffffffffu, ready));
-        const bool pre = ((s >> 32) & 3ull) == kFlagPre;
-        const uint32_t pmask = __ballot_sync(0xffffffffu, pre);
-        uint32_t val = (uint32_t)(s & 0xffffffffull);
+          const uint32_t val = (uint32_t)(sv & 0xffffffffull);
+          const bool pre = ((sv >> 32) & 3ull) == kFlagPre;
+          sum_all += val;
+          if (first_pre == kLookPerLane) {
+            sum_upto += val;
+            if (pre) first_pre = k;
+          }
+        }
+        const uint32_t pmask = __ballot_sync(0xffffffffu, first_pre < kLookPerLane);
+        uint32_t contrib;
         if (pmask) {
-          const int first = __ffs(pmask) - 1;
-          if (lane > first) val = 0;
+          const int fl = __ffs(pmask) - 1;
+          contrib = lane < fl ? sum_all : (lane == fl ? sum_upto : 0u);
+        } else {
+          contrib = sum_all;
         }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
-        excl += val;
+        for (int o = 16; o > 0; o >>= 1) contrib += __shfl_xor_sync(0xffffffffu, contrib, o);
+        excl += contrib;
         if (pmask) break;
-        end -= 32;
+        end -= 32 * kLookPerLane;
       }
       if (lane == 0) {
         st_status(&status[tile], tag | (kFlagPre << 32) | (excl + total));

@@ -25,7 +25,7 @@ struct GroupSet {
 };
 
 static int fill_groups(const gs_group* groups, int32_t n_groups, GroupSet& S, const char* who,
-                       bool need_grad) {
+                       bool need_grad, bool need_state = true) {
   if (!groups || n_groups < 1 || n_groups > GS_MAX_GROUPS) {
     gs_set_error("%s: bad group list", who);
     return GS_ERR_ARG;
@@ -33,7 +33,8 @@ static int fill_groups(const gs_group* groups, int32_t n_groups, GroupSet& S, co
   S.n = n_groups;
   for (int i = 0; i < n_groups; ++i) {
     const gs_group& g = groups[i];
-    if (!g.exp_avg || !g.exp_avg_sq || (need_grad && !g.grad) || g.width < 1 || g.width > 4096) {
+    if ((need_state && (!g.exp_avg || !g.exp_avg_sq)) || (need_grad && !g.grad) || g.width < 1 ||
+        g.width > 4096) {
       gs_set_error("%s: group %d invalid", who, i);
       return GS_ERR_ARG;
     }
@@ -203,7 +204,182 @@ __global__ void __launch_bounds__(kThreads)
 
 int stats_blocks() { return gs_sm_count() * 2; }
 
+// ---------------------------------------------------------------------------
+// row-record state (see gs_step_rows.cu): slot s < P holds (m, v), slot P the
+// int32 clock.  A warp owns a row; lanes stride over its slots.
+// ---------------------------------------------------------------------------
+template <bool RESET>
+__global__ void __launch_bounds__(kThreads)
+    scatter_rows_kernel(float* __restrict__ record, int64_t stride, int P,
+                        const int32_t* __restrict__ rows, int64_t k, double a1, double a2) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (kThreads / 32);
+  for (int64_t i = (int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5); i < k; i += warps) {
+    float* rec = record + (int64_t)__ldg(rows + i) * stride;
+    for (int s = lane; s <= P; s += 32) {
+      float2* p = reinterpret_cast<float2*>(rec + 2 * s);
+      if (RESET) {
+        if (s < P) *p = make_float2(0.f, 0.f);
+        else reinterpret_cast<int*>(rec)[2 * s] = 0;  // clock = 0, pad kept
+      } else if (s < P) {
+        const float2 x = *p;
+        *p = make_float2(__double2float_rn(__dmul_rn((double)x.x, a1)),
+                         __double2float_rn(__dmul_rn((double)x.y, a2)));
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kThreads)
+    stats_rows_kernel(const GroupSet S, const float* __restrict__ record, int64_t stride,
+                      int64_t n_rows, const uint8_t* __restrict__ alive, float active_logit,
+                      double* __restrict__ out, double* partials, unsigned int* counter) {
+  __shared__ double s_red[kStatsFields * (kThreads / 32)];
+  double acc[kStatsFields];
+  bool is_max[kStatsFields];
+#pragma unroll
+  for (int f = 0; f < kStatsFields; ++f) {
+    acc[f] = 0.0;
+    is_max[f] = f >= 2 && (((f - 2) % 5) == 1 || ((f - 2) % 5) == 4);
+  }
+  const int64_t stride_t = (int64_t)gridDim.x * blockDim.x;
+  const int64_t tid0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (int64_t r = tid0; r < n_rows; r += stride_t) acc[0] += alive == nullptr || alive[r] != 0;
+  int off = 0;
+#pragma unroll
+  for (int gi = 0; gi < GS_MAX_GROUPS; ++gi) {
+    if (gi >= S.n) break;
+    const GroupPtrs G = S.g[gi];
+    const int W = G.width;
+    const int64_t total = n_rows * W;
+    double s_sq = 0.0, m_sq = 0.0, n_pos = 0.0, s_rt = 0.0, m_rt = 0.0;
+    for (int64_t e = tid0; e < total; e += stride_t) {
+      const int64_t row = e / W;
+      const int col = (int)(e - row * W);
+      if (alive != nullptr && alive[row] == 0) continue;
+      const float2 x = __ldg(reinterpret_cast<const float2*>(record + row * stride + 2 * (off + col)));
+      const double sq = sqrt((double)x.y);
+      s_sq += sq;
+      m_sq = fmax(m_sq, sq);
+      if (sq > 0.0) {
+        const double rt = __ddiv_rn(fabs((double)x.x), sq);
+        n_pos += 1.0;
+        s_rt += rt;
+        m_rt = fmax(m_rt, rt);
+      }
+      if (G.role == GS_ROLE_OPACITY && W == 1 && G.param != nullptr)
+        acc[1] += __ldg(G.param + e) > active_logit;
+    }
+    acc[2 + 5 * gi + 0] = s_sq;
+    acc[2 + 5 * gi + 1] = m_sq;
+    acc[2 + 5 * gi + 2] = n_pos;
+    acc[2 + 5 * gi + 3] = s_rt;
+    acc[2 + 5 * gi + 4] = m_rt;
+    off += W;
+  }
+  block_reduce<kStatsFields>(acc, is_max, s_red);
+  if (threadIdx.x == 0) {
+    for (int f = 0; f < kStatsFields; ++f) partials[(size_t)blockIdx.x * kStatsFields + f] = acc[f];
+  }
+  if (last_block_arrive(counter)) {
+    const int nf = 2 + 5 * S.n;
+    for (int f = threadIdx.x; f < nf; f += blockDim.x) {
+      const bool mx = f >= 2 && (((f - 2) % 5) == 1 || ((f - 2) % 5) == 4);
+      double a = partials[f];
+      for (unsigned b = 1; b < gridDim.x; ++b) {
+        const double x = partials[(size_t)b * kStatsFields + f];
+        a = mx ? fmax(a, x) : a + x;
+      }
+      out[f] = a;
+    }
+  }
+}
+
+static int record_args(const float* record, int64_t stride, int P, const char* who) {
+  if (!record || P < 1 || stride < 2 * (P + 1) || (stride & 1) ||
+      (reinterpret_cast<uintptr_t>(record) & 7u)) {
+    gs_set_error("%s: bad record (stride %lld, P %d)", who, (long long)stride, P);
+    return GS_ERR_ARG;
+  }
+  return GS_OK;
+}
+
 }  // namespace gs
+
+extern "C" int gs_rsr_apply_rows(float* record, int64_t record_stride, int32_t n_elems,
+                                 const int32_t* rows, int64_t k, double alpha1, double alpha2,
+                                 void* stream) {
+  using namespace gs;
+  int rc = record_args(record, record_stride, n_elems, "gs_rsr_apply_rows");
+  if (rc) return rc;
+  if (!(alpha1 >= 0.0 && alpha1 < 1.0 && alpha2 >= 0.0 && alpha2 < 1.0)) {
+    gs_set_error("gs_rsr_apply_rows: RSR factors must lie in [0, 1)");
+    return GS_ERR_ARG;
+  }
+  if (k < 0 || (k > 0 && !rows)) {
+    gs_set_error("gs_rsr_apply_rows: bad index list");
+    return GS_ERR_ARG;
+  }
+  if (k == 0) return GS_OK;
+  const int64_t need = (k + 7) / 8;
+  const int grid = (int)std::min<int64_t>(need, (int64_t)gs_sm_count() * 8);
+  scatter_rows_kernel<false><<<grid, kThreads, 0, (cudaStream_t)stream>>>(
+      record, record_stride, n_elems, rows, k, alpha1, alpha2);
+  return gs_check_launch("gs_rsr_apply_rows");
+}
+
+extern "C" int gs_reset_rows_rows(float* record, int64_t record_stride, int32_t n_elems,
+                                  const int32_t* rows, int64_t k, void* stream) {
+  using namespace gs;
+  int rc = record_args(record, record_stride, n_elems, "gs_reset_rows_rows");
+  if (rc) return rc;
+  if (k < 0 || (k > 0 && !rows)) {
+    gs_set_error("gs_reset_rows_rows: bad index list");
+    return GS_ERR_ARG;
+  }
+  if (k == 0) return GS_OK;
+  const int64_t need = (k + 7) / 8;
+  const int grid = (int)std::min<int64_t>(need, (int64_t)gs_sm_count() * 8);
+  scatter_rows_kernel<true><<<grid, kThreads, 0, (cudaStream_t)stream>>>(
+      record, record_stride, n_elems, rows, k, 0.0, 0.0);
+  return gs_check_launch("gs_reset_rows_rows");
+}
+
+extern "C" int gs_stats_all_rows(const gs_group* groups, int32_t n_groups, int64_t n_rows,
+                                 const float* record, int64_t record_stride,
+                                 const uint8_t* alive, float active_logit, double* out, void* ws,
+                                 size_t ws_bytes, void* stream) {
+  using namespace gs;
+  GroupSet S{};
+  if (!groups || n_groups < 1 || n_groups > GS_MAX_GROUPS) {
+    gs_set_error("gs_stats_all_rows: bad group list");
+    return GS_ERR_ARG;
+  }
+  S.n = n_groups;
+  int P = 0;
+  for (int i = 0; i < n_groups; ++i) {
+    S.g[i] = GroupPtrs{groups[i].param, nullptr, nullptr, nullptr, (int)groups[i].width,
+                       groups[i].role};
+    if (groups[i].width < 1) {
+      gs_set_error("gs_stats_all_rows: group %d invalid", i);
+      return GS_ERR_ARG;
+    }
+    P += (int)groups[i].width;
+  }
+  int rc = record_args(record, record_stride, P, "gs_stats_all_rows");
+  if (rc) return rc;
+  if (!out || n_rows < 0 || !ws || ws_bytes < gs_stats_workspace_bytes(n_groups)) {
+    gs_set_error("gs_stats_all_rows: bad output / workspace");
+    return GS_ERR_WORKSPACE;
+  }
+  auto* hdr = reinterpret_cast<StatsWorkspace*>(ws);
+  auto* partials = reinterpret_cast<double*>(reinterpret_cast<char*>(ws) + sizeof(StatsWorkspace));
+  const int64_t need = (n_rows * 4 + kThreads - 1) / kThreads;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, stats_blocks()));
+  stats_rows_kernel<<<grid, kThreads, 0, (cudaStream_t)stream>>>(
+      S, record, record_stride, n_rows, alive, active_logit, out, partials, &hdr->counter);
+  return gs_check_launch("gs_stats_all_rows");
+}
 
 extern "C" int gs_check_grads(const gs_group* groups, int32_t n_groups, int64_t n_rows,
                               const int32_t* rows, const int32_t* n_list_dev,
@@ -211,7 +387,7 @@ extern "C" int gs_check_grads(const gs_group* groups, int32_t n_groups, int64_t 
                               int32_t* abort_flag, void* stream) {
   using namespace gs;
   GroupSet S{};
-  int rc = fill_groups(groups, n_groups, S, "gs_check_grads", true);
+  int rc = fill_groups(groups, n_groups, S, "gs_check_grads", true, false);
   if (rc) return rc;
   if (!abort_flag || n_rows < 0) {
     gs_set_error("gs_check_grads: abort_flag required");

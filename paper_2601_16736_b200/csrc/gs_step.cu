@@ -38,8 +38,8 @@ struct StepParams {
   GroupDev g[GS_MAX_GROUPS];
   int n_groups;
   int check;
-  float a1, a2, eps, active_logit;
-  double lam_op, lam_sc, clip_op, clip_sc, n_i;
+  float active_logit;
+  StepConsts K;
   const float* lut;
   int lut_len;
   int global_t;
@@ -77,10 +77,15 @@ __global__ void __launch_bounds__(kThreads, kStepBlocksPerSM) step_kernel(const 
   int64_t n_rows = T::kDense ? P.max_rows : (int64_t)(*P.n_rows_dev);
   if (STRICT && *P.abort_flag != 0) n_rows = 0;
 
-  double nv = 0.0;
-  if (T::kCoupled) nv = P.nv_dev ? (double)(*P.nv_dev) : P.nv_host;
-  const double lam_op = (T::kCoupled && nv == 0.0) ? 0.0 : P.lam_op;
-  const double lam_sc = (T::kCoupled && nv == 0.0) ? 0.0 : P.lam_sc;
+  // decoupled modes read the constants straight from the parameter bank;
+  // the coupled modes patch in 1/N_v (loss.py:190-192: no term when N_v = 0)
+  StepConsts Kc = P.K;
+  if (T::kCoupled) {
+    const float nv = P.nv_dev ? (float)(*P.nv_dev) : (float)P.nv_host;
+    Kc.inv_nv = nv != 0.0f ? __frcp_rn(nv) : 0.0f;
+    if (nv == 0.0f) Kc.lam_op = Kc.lam_sc = 0.0f;
+  }
+  const StepConsts& K = T::kCoupled ? Kc : P.K;
 
   unsigned int c_vis = 0, c_step = 0, c_badg = 0, c_badd = 0, c_apre = 0, c_apost = 0,
                c_clo = 0, c_cls = 0;
@@ -107,9 +112,9 @@ __global__ void __launch_bounds__(kThreads, kStepBlocksPerSM) step_kernel(const 
         const GroupDev G = P.g[gi];
         const int W = G.width;
         const int E = nvalid * W;
-        const double lam = G.role == GS_ROLE_OPACITY ? lam_op
-                           : G.role == GS_ROLE_SCALE ? lam_sc : 0.0;
-        const bool dom = lam != 0.0;
+        const float lam = G.role == GS_ROLE_OPACITY ? K.lam_op
+                          : G.role == GS_ROLE_SCALE ? K.lam_sc : 0.0f;
+        const bool dom = lam != 0.0f;
         const int dq = kThreads / W, dr = kThreads % W;
         int lr = tid / W, lc = tid % W;
         for (int e = tid; e < E; e += kThreads) {
@@ -151,8 +156,6 @@ __global__ void __launch_bounds__(kThreads, kStepBlocksPerSM) step_kernel(const 
       const int W = G.width;
       const int E = nvalid * W;
       const int role = G.role;
-      const double lam = role == GS_ROLE_OPACITY ? lam_op : role == GS_ROLE_SCALE ? lam_sc : 0.0;
-      const double cap = role == GS_ROLE_OPACITY ? P.clip_op : P.clip_sc;
       const float lrf = G.lr;
       const int dq = kThreads / W, dr = kThreads % W;
       int lr = tid / W, lc = tid % W;
@@ -167,40 +170,13 @@ __global__ void __launch_bounds__(kThreads, kStepBlocksPerSM) step_kernel(const 
         const int64_t off = (int64_t)r * W + this_lc;
         const float2 bc = s_bc[this_lr];
         const float th = G.param[off];
-        float gr = __ldg(G.grad + off);
+        const float gr = __ldg(G.grad + off);
         const float mm = G.m[off];
         const float vv = G.v[off];
-        if (T::kCoupled && lam != 0.0) {
-          const double regc = __ddiv_rn(__dmul_rn(lam, reg_deriv_f64(role, th)), nv);
-          gr = __double2float_rn(__dadd_rn((double)gr, regc));
-        }
-        const float d = __fsub_rn(gr, mm);
-        const float mn = __fadd_rn(mm, __fmul_rn(P.a1, d));
-        const float g2 = __fmul_rn(gr, gr);
-        const float ee = __fsub_rn(g2, vv);
-        const float vn = __fadd_rn(vv, __fmul_rn(P.a2, ee));
-        const float mh = __fmul_rn(mn, bc.x);
-        const float vh = __fmul_rn(vn, bc.y);
-        const float den = __fadd_rn(__fsqrt_rn(vh), P.eps);
-        float step = __fdiv_rn(mh, den);
-        if (T::kDecoupled && lam != 0.0) {
-          const double deriv = reg_deriv_f64(role, th);
-          double x;
-          bool clipped = false;
-          double ex64;
-          if (MODE == GS_MODE_ADAMW_GS) {
-            x = __ddiv_rn(__dmul_rn(lam, __ddiv_rn(deriv, P.n_i)), (double)den);
-            clipped = x >= cap;
-            ex64 = clipped ? cap : x;
-          } else if (MODE == GS_MODE_ADAMW_CONST_CLIP) {
-            x = __dmul_rn(lam, deriv);
-            clipped = x >= cap;
-            ex64 = clipped ? cap : x;
-          } else {
-            ex64 = __dmul_rn(lam, deriv);
-          }
-          const float ex = __double2float_rn(ex64);
-          step = __fadd_rn(step, ex);
+        float tn, mn, vn, ex;
+        bool clipped;
+        update_element<MODE>(role, lrf, th, gr, mm, vv, bc, K, tn, mn, vn, ex, clipped);
+        if (!T::kCoupled && (role == GS_ROLE_OPACITY || role == GS_ROLE_SCALE)) {
           if (role == GS_ROLE_OPACITY) {
             c_clo += clipped;
             s_exo += (double)ex;
@@ -209,7 +185,6 @@ __global__ void __launch_bounds__(kThreads, kStepBlocksPerSM) step_kernel(const 
             s_exs += (double)ex;
           }
         }
-        const float tn = __fsub_rn(th, __fmul_rn(lrf, step));
         if (role == GS_ROLE_OPACITY) {
           c_apre += th > P.active_logit;
           c_apost += tn > P.active_logit;
@@ -319,15 +294,8 @@ extern "C" int gs_step(const gs_group* groups, int32_t n_groups, const gs_step_c
   }
   P.n_groups = n_groups;
   P.check = cfg->check;
-  P.a1 = cfg->one_minus_beta1;
-  P.a2 = cfg->one_minus_beta2;
-  P.eps = cfg->eps;
   P.active_logit = cfg->active_logit;
-  P.lam_op = cfg->lambda_opacity;
-  P.lam_sc = cfg->lambda_scale;
-  P.clip_op = cfg->clip_opacity;
-  P.clip_sc = cfg->clip_scale;
-  P.n_i = cfg->n_pixels_rounded;
+  P.K = make_consts(cfg);
   P.lut = cfg->bias_lut;
   P.lut_len = cfg->lut_len;
   P.global_t = cfg->global_t;

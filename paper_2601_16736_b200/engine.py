@@ -112,13 +112,16 @@ class GroupBinding:
     lr: float
     param: torch.Tensor
     grad: torch.Tensor | None
-    exp_avg: torch.Tensor
-    exp_avg_sq: torch.Tensor
+    exp_avg: torch.Tensor | None
+    exp_avg_sq: torch.Tensor | None
+    w: int = 0  # width when neither param nor per-group state is given
 
     @property
     def width(self) -> int:
-        n = self.param.shape[0]
-        return self.param.numel() // max(n, 1) if n else max(1, int(np.prod(self.param.shape[1:])))
+        t = self.param if self.param is not None else self.exp_avg
+        if t is None:
+            return int(self.w)
+        return max(1, int(np.prod(t.shape[1:]))) if t.dim() > 1 else 1
 
 
 def _check_tensor(name, t: torch.Tensor, n_rows: int, width: int, device, dtype=torch.float32):
@@ -151,6 +154,8 @@ class StepEngine:
                                           dtype=torch.uint8, device=dev)
             self.step_ws = torch.zeros(int(self.lib.gs_step_workspace_bytes()), dtype=torch.uint8,
                                        device=dev)
+            self.rows_ws = torch.zeros(int(self.lib.gs_step_rows_workspace_bytes()),
+                                       dtype=torch.uint8, device=dev)
             self.stats = torch.zeros(L.GS_STEP_STATS, dtype=torch.float64, device=dev)
             self.abort = torch.zeros(1, dtype=torch.int32, device=dev)
             lut = bias_lut(self.beta1, self.beta2)
@@ -162,6 +167,7 @@ class StepEngine:
             self._bad_rows = None
             self._rows_tmp = None
         self.active_logit = active_logit_threshold()
+        self.launches = 0  # C-ABI kernel launches issued (bench accounting)
         self._group_cache_key = None
         self._group_cache = None
 
@@ -176,9 +182,13 @@ class StepEngine:
         arr = (L.GsGroup * len(groups))()
         for i, g in enumerate(groups):
             w = g.width
-            _check_tensor(f"{g.name}.param", g.param, self.n_rows, w, self.device)
-            _check_tensor(f"{g.name}.exp_avg", g.exp_avg, self.n_rows, w, self.device)
-            _check_tensor(f"{g.name}.exp_avg_sq", g.exp_avg_sq, self.n_rows, w, self.device)
+            if g.param is not None:
+                _check_tensor(f"{g.name}.param", g.param, self.n_rows, w, self.device)
+            elif need_grad:
+                raise ConfigError(f"group {g.name} has no parameter tensor")
+            if g.exp_avg is not None:  # per-group state (the row-record layout passes None)
+                _check_tensor(f"{g.name}.exp_avg", g.exp_avg, self.n_rows, w, self.device)
+                _check_tensor(f"{g.name}.exp_avg_sq", g.exp_avg_sq, self.n_rows, w, self.device)
             if need_grad:
                 if g.grad is None:
                     raise ConfigError(f"group {g.name} has no gradient")
@@ -209,6 +219,7 @@ class StepEngine:
             raise ConfigError(f"visibility dtype {vis.dtype} not supported (bool/uint8 mask or "
                               "int32 radii)")
         L.check(rc, "gs_compact")
+        self.launches += 1
         return self.idx, self.count
 
     # ------------------------------------------------------------------ step
@@ -217,11 +228,18 @@ class StepEngine:
              lambda_opacity: float = 0.0, lambda_scale: float = 0.0, clip_opacity: float = 10.0,
              clip_scale: float = 10.0, n_pixels_rounded: float = 0.0, global_t: int = 0,
              n_visible_dev: torch.Tensor | None = None, n_visible_host: float = 0.0,
-             check: str = "fused") -> torch.Tensor:
-        """K2 (plus the strict pre-check when ``check == "strict"``)."""
+             check: str = "fused", record: torch.Tensor | None = None) -> torch.Tensor:
+        """K2 (plus the strict pre-check when ``check == "strict"``).
+
+        ``record`` given: row-record state (gs_step_rows), ``clock`` ignored;
+        otherwise per-group m / v tensors and the int32 ``clock``.
+        """
         if mode not in L.MODE_IDS:
             raise ConfigError(f"unknown mode {mode!r}; expected one of {tuple(L.MODE_IDS)}")
-        _check_tensor("clock", clock, self.n_rows, 1, self.device, torch.int32)
+        if record is None:
+            _check_tensor("clock", clock, self.n_rows, 1, self.device, torch.int32)
+        else:
+            self._check_record(record, groups)
         garr = self.group_array(groups)
         s = _stream_handle(self.device)
         cfg = L.GsStepCfg()
@@ -251,11 +269,27 @@ class StepEngine:
                                          _ptr(dcount), float(lambda_opacity),
                                          float(lambda_scale), None, self.abort.data_ptr(), s)
             L.check(rc, "gs_check_grads")
-        rc = self.lib.gs_step(garr, len(groups), C.byref(cfg), _ptr(rows), _ptr(count),
-                              self.n_rows, clock.data_ptr(), self.stats.data_ptr(),
-                              self.step_ws.data_ptr(), self.step_ws.numel(), s)
-        L.check(rc, "gs_step")
+        if record is None:
+            rc = self.lib.gs_step(garr, len(groups), C.byref(cfg), _ptr(rows), _ptr(count),
+                                  self.n_rows, clock.data_ptr(), self.stats.data_ptr(),
+                                  self.step_ws.data_ptr(), self.step_ws.numel(), s)
+            L.check(rc, "gs_step")
+        else:
+            rc = self.lib.gs_step_rows(garr, len(groups), C.byref(cfg), _ptr(rows), _ptr(count),
+                                       self.n_rows, record.data_ptr(), record.stride(0),
+                                       self.stats.data_ptr(), self.rows_ws.data_ptr(),
+                                       self.rows_ws.numel(), s)
+            L.check(rc, "gs_step_rows")
+        self.launches += 2 if check == "strict" else 1
         return self.stats
+
+    def _check_record(self, record: torch.Tensor, groups):
+        p = sum(g.width for g in groups)
+        if (record.device != self.device or record.dtype != torch.float32 or record.dim() != 2
+                or record.shape[0] != self.n_rows or record.stride(1) != 1
+                or record.shape[1] < 2 * (p + 1)):
+            raise ConfigError(f"state record must be fp32 [{self.n_rows}, >= {2 * (p + 1)}] "
+                              f"with unit column stride, got {tuple(record.shape)}")
 
     def all_rows(self) -> tuple[torch.Tensor, torch.Tensor]:
         """Identity index list (dense mode domain checks, error ids)."""
@@ -293,35 +327,62 @@ class StepEngine:
             t = torch.from_numpy(arr.astype(np.int32)).to(self.device, non_blocking=False)
         return t, int(t.numel())
 
-    def rsr_apply(self, groups: list[GroupBinding], indices, alpha1: float, alpha2: float):
+    def rsr_apply(self, groups: list[GroupBinding], indices, alpha1: float, alpha2: float,
+                  record: torch.Tensor | None = None):
         if not (0.0 <= alpha1 < 1.0 and 0.0 <= alpha2 < 1.0):
             raise ConfigError("RSR factors must lie in [0, 1)")
         rows, k = self._rows_device(indices)
-        garr = self.group_array(groups, need_grad=False)
-        rc = self.lib.gs_rsr_apply(garr, len(groups), rows.data_ptr() if k else None, k,
-                                   float(alpha1), float(alpha2), _stream_handle(self.device))
+        s = _stream_handle(self.device)
+        if record is not None:
+            self._check_record(record, groups)
+            rc = self.lib.gs_rsr_apply_rows(record.data_ptr(), record.stride(0),
+                                            sum(g.width for g in groups),
+                                            rows.data_ptr() if k else None, k, float(alpha1),
+                                            float(alpha2), s)
+        else:
+            garr = self.group_array(groups, need_grad=False)
+            rc = self.lib.gs_rsr_apply(garr, len(groups), rows.data_ptr() if k else None, k,
+                                       float(alpha1), float(alpha2), s)
         L.check(rc, "gs_rsr_apply")
+        self.launches += 1 if k else 0
         self._rows_tmp = rows  # keep alive until the kernel has consumed it
 
-    def reset_rows(self, groups: list[GroupBinding], clock: torch.Tensor, indices):
+    def reset_rows(self, groups: list[GroupBinding], clock: torch.Tensor | None, indices,
+                   record: torch.Tensor | None = None):
         rows, k = self._rows_device(indices)
-        garr = self.group_array(groups, need_grad=False)
-        rc = self.lib.gs_reset_rows(garr, len(groups), clock.data_ptr(),
-                                    rows.data_ptr() if k else None, k,
-                                    _stream_handle(self.device))
+        s = _stream_handle(self.device)
+        if record is not None:
+            self._check_record(record, groups)
+            rc = self.lib.gs_reset_rows_rows(record.data_ptr(), record.stride(0),
+                                             sum(g.width for g in groups),
+                                             rows.data_ptr() if k else None, k, s)
+        else:
+            garr = self.group_array(groups, need_grad=False)
+            rc = self.lib.gs_reset_rows(garr, len(groups), clock.data_ptr(),
+                                        rows.data_ptr() if k else None, k, s)
         L.check(rc, "gs_reset_rows")
+        self.launches += 1 if k else 0
         self._rows_tmp = rows
 
     # ---------------------------------------------------------- statistics
-    def stats_all(self, groups: list[GroupBinding], alive: torch.Tensor | None = None):
+    def stats_all(self, groups: list[GroupBinding], alive: torch.Tensor | None = None,
+                  record: torch.Tensor | None = None):
         garr = self.group_array(groups, need_grad=False)
         if alive is not None:
             if alive.dtype not in (torch.bool, torch.uint8) or alive.numel() != self.n_rows:
                 raise ConfigError("alive must be a bool/uint8 mask over the rows")
             alive = alive.contiguous()
-        rc = self.lib.gs_stats_all(garr, len(groups), self.n_rows, _ptr(alive),
-                                   float(self.active_logit), self.stats_all_out.data_ptr(),
-                                   self.stats_ws.data_ptr(), self.stats_ws.numel(),
-                                   _stream_handle(self.device))
+        s = _stream_handle(self.device)
+        if record is not None:
+            self._check_record(record, groups)
+            rc = self.lib.gs_stats_all_rows(garr, len(groups), self.n_rows, record.data_ptr(),
+                                            record.stride(0), _ptr(alive),
+                                            float(self.active_logit),
+                                            self.stats_all_out.data_ptr(),
+                                            self.stats_ws.data_ptr(), self.stats_ws.numel(), s)
+        else:
+            rc = self.lib.gs_stats_all(garr, len(groups), self.n_rows, _ptr(alive),
+                                       float(self.active_logit), self.stats_all_out.data_ptr(),
+                                       self.stats_ws.data_ptr(), self.stats_ws.numel(), s)
         L.check(rc, "gs_stats_all")
         return self.stats_all_out[: 2 + 5 * len(groups)]

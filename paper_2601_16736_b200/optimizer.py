@@ -93,19 +93,43 @@ def validate_hyper(mode, beta1, beta2, eps, ct_opacity, ct_scale):
         raise ConfigError("clip bounds C_t must be positive")
 
 
-@dataclass
+def _tail_strides(tail: tuple) -> tuple:
+    out, acc = [], 1
+    for d in reversed(tail):
+        out.append(acc)
+        acc *= d
+    return tuple(reversed(out))
+
+
 class MomentState:
     """optimizer.py:103-156 — m, v per group (param-shaped) + the step clock.
 
     The reference keeps one int64 clock per group; every code path moves them
     together, so one int32 clock per primitive is stored
     and ``t[group]`` returns that shared tensor.
+
+    Two storage layouts, same interface:
+
+    ``"rows"`` (default) — one fp32 record per primitive holding the (m, v)
+        pairs of all its elements in group order followed by the int32 clock
+        (``record`` [N, 2*(P+1)]); ``m[g]``, ``v[g]`` and ``clock`` are strided
+        views into it.  A visible primitive's whole optimizer state is one
+        contiguous 8*(P+1)-byte span (480 B for SH-3), which is what the
+        fused B200 step streams.
+    ``"groups"`` — contiguous per-group ``m`` / ``v`` tensors and a separate
+        int32 clock (the reference's own layout).
     """
 
-    m: dict
-    v: dict
-    clock: torch.Tensor
-    global_t: int = 0
+    def __init__(self, m: dict, v: dict, clock: torch.Tensor, global_t: int = 0,
+                 record: torch.Tensor | None = None, spec: tuple | None = None):
+        self.m, self.v, self.clock = m, v, clock
+        self.global_t = int(global_t)
+        self.record = record
+        self.spec = spec
+
+    @property
+    def layout(self) -> str:
+        return "rows" if self.record is not None else "groups"
 
     @property
     def t(self) -> dict:
@@ -115,22 +139,55 @@ class MomentState:
         return int(self.clock.numel())
 
     @staticmethod
-    def zeros_like(params: dict) -> "MomentState":
+    def _views(record: torch.Tensor, spec: tuple):
+        n, stride, base = record.shape[0], record.stride(0), record.storage_offset()
+        m, v = {}, {}
+        for name, off, tail in spec:
+            st = (stride,) + tuple(2 * x for x in _tail_strides(tail))
+            m[name] = record.as_strided((n,) + tail, st, base + 2 * off)
+            v[name] = record.as_strided((n,) + tail, st, base + 2 * off + 1)
+        p = sum(int(np.prod(t)) for _, _, t in spec)
+        clock = record.view(torch.int32).as_strided((n,), (stride,), base + 2 * p)
+        return m, v, clock
+
+    @staticmethod
+    def from_record(record: torch.Tensor, spec: tuple, global_t: int = 0) -> "MomentState":
+        m, v, clock = MomentState._views(record, spec)
+        return MomentState(m, v, clock, global_t, record, spec)
+
+    @staticmethod
+    def zeros_like(params: dict, layout: str = "rows") -> "MomentState":
         first = next(iter(params.values()))
-        return MomentState(
-            m={k: torch.zeros_like(p, dtype=torch.float32, memory_format=torch.contiguous_format)
-               for k, p in params.items()},
-            v={k: torch.zeros_like(p, dtype=torch.float32, memory_format=torch.contiguous_format)
-               for k, p in params.items()},
-            clock=torch.zeros(first.shape[0], dtype=torch.int32, device=first.device))
+        n = first.shape[0]
+        if layout == "groups":
+            return MomentState(
+                m={k: torch.zeros(p.shape, dtype=torch.float32, device=p.device)
+                   for k, p in params.items()},
+                v={k: torch.zeros(p.shape, dtype=torch.float32, device=p.device)
+                   for k, p in params.items()},
+                clock=torch.zeros(n, dtype=torch.int32, device=first.device))
+        if layout != "rows":
+            raise ConfigError(f"unknown state layout {layout!r}")
+        spec, off = [], 0
+        for k, p in params.items():
+            tail = tuple(p.shape[1:])
+            spec.append((k, off, tail))
+            off += int(np.prod(tail)) if tail else 1
+        record = torch.zeros((n, 2 * (off + 1)), dtype=torch.float32, device=first.device)
+        return MomentState.from_record(record, tuple(spec))
 
     def copy(self) -> "MomentState":
+        if self.record is not None:
+            return MomentState.from_record(self.record.clone(), self.spec, self.global_t)
         return MomentState({k: t.clone() for k, t in self.m.items()},
                            {k: t.clone() for k, t in self.v.items()}, self.clock.clone(),
                            self.global_t)
 
     def select(self, index) -> "MomentState":
         """Rows ``index`` (prune/clone bookkeeping, optimizer.py:141-147)."""
+        if self.record is not None:
+            return MomentState.from_record(self.record[index].contiguous(), self.spec,
+                                           self.global_t)
         return MomentState({k: t[index].contiguous() for k, t in self.m.items()},
                            {k: t[index].contiguous() for k, t in self.v.items()},
                            self.clock[index].contiguous(), self.global_t)
@@ -138,6 +195,8 @@ class MomentState:
     @staticmethod
     def concatenate(a: "MomentState", b: "MomentState") -> "MomentState":
         """optimizer.py:149-156."""
+        if a.record is not None and b.record is not None:
+            return MomentState.from_record(torch.cat([a.record, b.record]), a.spec, a.global_t)
         return MomentState({k: torch.cat([a.m[k], b.m[k]]) for k in a.m},
                            {k: torch.cat([a.v[k], b.v[k]]) for k in a.v},
                            torch.cat([a.clock, b.clock]), a.global_t)
@@ -164,7 +223,7 @@ class AdamWGS:
     def __init__(self, params, *, mode: str = "adamw-gs", betas=(0.9, 0.999), eps: float = 1e-8,
                  lambda_o: float = 0.0, lambda_s: float = 0.0, ct_opacity: float = 10.0,
                  ct_scale: float = 10.0, round_n_pixels: bool = True, check: str = "fused",
-                 errors: str = "raise"):
+                 errors: str = "raise", state_layout: str = "rows"):
         validate_hyper(mode, betas[0], betas[1], eps, ct_opacity, ct_scale)
         if check not in CHECKS:
             raise ConfigError(f"check must be one of {CHECKS}")
@@ -198,7 +257,8 @@ class AdamWGS:
                 raise ConfigError(f"group {g['name']}: all groups must share device and row count")
             if p.dtype != torch.float32 or not p.is_contiguous():
                 raise ConfigError(f"group {g['name']}: parameters must be contiguous fp32")
-        self.state = MomentState.zeros_like({g["name"]: g["params"][0] for g in self.param_groups})
+        self.state = MomentState.zeros_like({g["name"]: g["params"][0] for g in self.param_groups},
+                                            state_layout)
         self.engine = StepEngine(self.n_rows, self.device, self.beta1, self.beta2)
         self._stats_host = torch.zeros(L.GS_STEP_STATS, dtype=torch.float64, pin_memory=True)
         self._pending = None
@@ -216,13 +276,17 @@ class AdamWGS:
             elif p.grad is not None:
                 gr = p.grad
             lr = g["lr"] * (mu_lr_scale if g["role"] == L.ROLE_POSITION else 1.0)
-            out.append(GroupBinding(name, g["role"], lr, p.data, gr, self.state.m[name],
-                                    self.state.v[name]))
+            rows = self.state.record is not None
+            out.append(GroupBinding(name, g["role"], lr, p.data, gr,
+                                    None if rows else self.state.m[name],
+                                    None if rows else self.state.v[name]))
         return out
 
     def _state_bindings(self) -> list[GroupBinding]:
+        rows = self.state.record is not None
         return [GroupBinding(g["name"], g["role"], g["lr"], g["params"][0].data, None,
-                             self.state.m[g["name"]], self.state.v[g["name"]])
+                             None if rows else self.state.m[g["name"]],
+                             None if rows else self.state.v[g["name"]])
                 for g in self.param_groups]
 
     # --------------------------------------------------------------------- step
@@ -251,7 +315,7 @@ class AdamWGS:
         eng = self.engine
         lo = self.lambda_o if lambda_o is None else float(lambda_o)
         ls = self.lambda_s if lambda_s is None else float(lambda_s)
-        kw = dict(eps=self.eps, check=self.check)
+        kw = dict(eps=self.eps, check=self.check, record=self.state.record)
         if mode == "coupled-adam":
             self.state.global_t += 1
             nv = None
@@ -339,22 +403,24 @@ class AdamWGS:
     @torch.no_grad()
     def rsr_apply(self, indices, alpha1: float, alpha2: float):
         """Re-State Regularization (optimizer.py:327-340): m*=a1, v*=a2, clock kept."""
-        self.engine.rsr_apply(self._state_bindings(), indices, alpha1, alpha2)
+        self.engine.rsr_apply(self._state_bindings(), indices, alpha1, alpha2,
+                              record=self.state.record)
 
     @torch.no_grad()
     def reset_rows(self, indices):
         """Fresh state on the rows (optimizer.py:159-165): m = v = 0, t = 0."""
-        self.engine.reset_rows(self._state_bindings(), self.state.clock, indices)
+        self.engine.reset_rows(self._state_bindings(), self.state.clock, indices,
+                               record=self.state.record)
 
     @torch.no_grad()
     def moment_stats(self, alive: torch.Tensor | None = None) -> dict:
         """optimizer.py:489-506 over alive rows."""
-        return _moment_stats(self.engine, self._state_bindings(), alive)
+        return _moment_stats(self.engine, self._state_bindings(), alive, self.state.record)
 
     @torch.no_grad()
     def classify_active(self, alive: torch.Tensor | None = None) -> tuple[int, int]:
         """(N_a, N_d) of primitives.py:228-238 (opacity group)."""
-        out = self.engine.stats_all(self._state_bindings(), alive).tolist()
+        out = self.engine.stats_all(self._state_bindings(), alive, self.state.record).tolist()
         return int(out[1]), int(out[0]) - int(out[1])
 
     def moment_state(self) -> MomentState:
@@ -388,11 +454,12 @@ class AdamWGS:
             for k in self.state.m:
                 self.state.m[k].copy_(sd["m"][k])
                 self.state.v[k].copy_(sd["v"][k])
+        # (views into the row record are written in place)
         self.state.global_t = int(sd["global_t"])
 
 
-def _moment_stats(engine: StepEngine, bindings, alive) -> dict:
-    out = engine.stats_all(bindings, alive).tolist()
+def _moment_stats(engine: StepEngine, bindings, alive, record=None) -> dict:
+    out = engine.stats_all(bindings, alive, record).tolist()
     n_alive = out[0]
     res = {}
     for i, b in enumerate(bindings):

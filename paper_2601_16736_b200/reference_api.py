@@ -66,12 +66,14 @@ def _get(obj, name):
 
 def _bindings(state: MomentState, pset, grads, cfg: OptimizerConfig, mu_lr_scale: float):
     out = []
+    rows = state.record is not None
     for name in state.m:
         role = role_of(name)
         lr = cfg.lr(name) * (mu_lr_scale if role == L.ROLE_POSITION else 1.0)
         p = _get(pset, name)
         g = None if grads is None else _get(grads, name)
-        out.append(GroupBinding(name, role, lr, p, g, state.m[name], state.v[name]))
+        out.append(GroupBinding(name, role, lr, p, g, None if rows else state.m[name],
+                                None if rows else state.v[name]))
     return out
 
 
@@ -99,14 +101,15 @@ def _run(mode, state, pset, grads, vis, cfg, *, mu_lr_scale=1.0, lam_o=0.0, lam_
         state.global_t += 1
         stats = eng.step(b, mode, state.clock, rows=None, count=None, eps=cfg.eps,
                          lambda_opacity=lam_o, lambda_scale=lam_s, global_t=state.global_t,
-                         n_visible_dev=nv, check="strict")
+                         n_visible_dev=nv, check="strict", record=state.record)
         drows, dcount = eng.all_rows()
     else:
         rows, count = eng.compact(_as_mask(vis, n, dev))
         stats = eng.step(b, mode, state.clock, rows=rows, count=count, eps=cfg.eps,
                          lambda_opacity=lam_o, lambda_scale=lam_s, clip_opacity=clip_o,
                          clip_scale=clip_s, n_pixels_rounded=n_i,
-                         n_visible_dev=count if coupled else None, check="strict")
+                         n_visible_dev=count if coupled else None, check="strict",
+                         record=state.record)
         drows, dcount = rows, count
     flag = int(eng.abort.item())                      # reference semantics: raise now
     if flag:
@@ -157,9 +160,17 @@ def adamw_const_step(state, pset, grads, vis, cfg, clip=None, mu_lr_scale=1.0):
     return pset, state
 
 
-def _state_bindings(state: MomentState):
-    return [GroupBinding(k, role_of(k), 0.0, state.m[k], None, state.m[k], state.v[k])
-            for k in state.m]
+def _state_bindings(state: MomentState, pset=None):
+    rows = state.record is not None
+    out = []
+    for k in state.m:
+        p = None
+        if pset is not None:
+            p = _get(pset, k)
+        w = max(1, int(np.prod(state.m[k].shape[1:]))) if state.m[k].dim() > 1 else 1
+        out.append(GroupBinding(k, role_of(k), 0.0, p, None, None if rows else state.m[k],
+                                None if rows else state.v[k], w))
+    return out
 
 
 def rsr_apply(state: MomentState, indices, alpha1: float, alpha2: float) -> MomentState:
@@ -167,14 +178,14 @@ def rsr_apply(state: MomentState, indices, alpha1: float, alpha2: float) -> Mome
     if not (0.0 <= alpha1 < 1.0 and 0.0 <= alpha2 < 1.0):
         raise ConfigError("RSR factors must lie in [0, 1)")
     eng = _engine(len(state), state.clock.device, 0.9, 0.999)
-    eng.rsr_apply(_state_bindings(state), indices, alpha1, alpha2)
+    eng.rsr_apply(_state_bindings(state), indices, alpha1, alpha2, record=state.record)
     return state
 
 
 def reset_rows(state: MomentState, indices) -> MomentState:
     """optimizer.py:159-165."""
     eng = _engine(len(state), state.clock.device, 0.9, 0.999)
-    eng.reset_rows(_state_bindings(state), state.clock, indices)
+    eng.reset_rows(_state_bindings(state), state.clock, indices, record=state.record)
     return state
 
 
@@ -183,7 +194,7 @@ def moment_stats(state: MomentState, alive=None) -> dict:
     eng = _engine(len(state), state.clock.device, 0.9, 0.999)
     if alive is not None and not isinstance(alive, torch.Tensor):
         alive = torch.from_numpy(np.asarray(alive, dtype=bool)).to(state.clock.device)
-    return _moment_stats(eng, _state_bindings(state), alive)
+    return _moment_stats(eng, _state_bindings(state), alive, state.record)
 
 
 def classify_active(pset, threshold: float = 1.0 / 255.0, alive=None):
@@ -195,6 +206,7 @@ def classify_active(pset, threshold: float = 1.0 / 255.0, alive=None):
     tau = tau.reshape(-1, 1).contiguous()
     n = tau.shape[0]
     eng = _engine(n, tau.device, 0.9, 0.999)
+    # counts only: the per-group moment sums computed alongside are ignored
     b = [GroupBinding("tau", L.ROLE_OPACITY, 0.0, tau, None, tau, tau)]
     if alive is None:
         alive = getattr(pset, "alive", None)
