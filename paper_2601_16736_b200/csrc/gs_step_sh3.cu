@@ -70,31 +70,38 @@ struct FixedParams {
 
 constexpr int kFixedThreads = 256;
 
-// Element i of a chunk of R rows, enumerated group-major:
-//   [group 0: R x W_0][group 1: R x W_1] ... ; group g starts at R * OFF_g.
-// With R a multiple of 32 every group boundary is a multiple of 32, so the
-// group of i is uniform across a warp.
-template <class L>
-__device__ __forceinline__ int group_of(int i, int R) {
-  int g = 0;
-#pragma unroll
-  for (int k = 1; k < L::G; ++k) g += (i >= R * L::OFF(k)) ? 1 : 0;
-  return g;
-}
+// Rounds of group g in a chunk of R rows: ceil(R * W_g / NT) (compile-time).
+template <class L, int R, int NT>
+struct ChunkShape {
+  __host__ __device__ static constexpr int rounds(int g) { return (R * L::W(g) + NT - 1) / NT; }
+  __host__ __device__ static constexpr int first(int g) {
+    int s = 0;
+    for (int k = 0; k < g; ++k) s += rounds(k);
+    return s;
+  }
+  static constexpr int total = first(L::G);
+};
 
-template <class L, int MODE, bool STRICT, int R, int MINB>
-__global__ void __launch_bounds__(kFixedThreads, MINB) step_fixed_kernel(const FixedParams P) {
+// Chunk elements are enumerated group by group; element k*NT + t of group g
+// is (row (k*NT + t) / W_g, column (k*NT + t) % W_g) of the chunk.  The group
+// loop is unrolled, so widths, roles, record offsets and the parameter
+// pointers are compile-time per round, and a round's warp-uniform predicate
+// (k*NT + t < R*W_g) is the only control flow.
+template <class L, int MODE, bool STRICT, int R, int MINB, int NT>
+__global__ void __launch_bounds__(NT, MINB) step_fixed_kernel(const FixedParams P) {
   constexpr bool kDense = MODE == GS_MODE_COUPLED_ADAM;
   constexpr bool kCoupled = MODE == GS_MODE_COUPLED_ADAM || MODE == GS_MODE_SPARSE_ADAM;
-  constexpr int NT = kFixedThreads;
-  constexpr int E = R * L::P;              // elements per chunk
-  constexpr int J = (E + NT - 1) / NT;     // elements per thread per chunk
-  __shared__ int32_t s_row[R];
+  using S = ChunkShape<L, R, NT>;
+  constexpr int NR = S::total;  // element rounds per thread per chunk
+  __shared__ uint32_t s_row[R];
   __shared__ int s_bad[R];
   __shared__ float2 s_bc[R];
+  __shared__ int s_any_bad;
   __shared__ double s_red[GS_STEP_STATS * (NT / 32)];
 
   const int t = threadIdx.x;
+  float2* const rec_base = reinterpret_cast<float2*>(P.record);
+  const uint32_t rec_stride2 = (uint32_t)(P.stride / 2);  // float2 per record
   int64_t n_rows = kDense ? P.max_rows : (int64_t)(*P.n_rows_dev);
   if (STRICT && *P.abort_flag != 0) n_rows = 0;
   StepConsts Kc = P.K;
@@ -114,46 +121,43 @@ __global__ void __launch_bounds__(kFixedThreads, MINB) step_fixed_kernel(const F
     const int64_t base = chunk * R;
     const int nvalid = (int)(n_rows - base < R ? n_rows - base : R);
     __syncthreads();  // previous chunk's shared-memory readers are done
-    int32_t my_row = 0;
     int my_clock = 0;
+    float2* my_rec = nullptr;
+    if (t == 0) s_any_bad = 0;
     if (t < R) {
-      my_row = t < nvalid ? (kDense ? (int32_t)(base + t) : __ldg(P.rows + base + t)) : 0;
-      s_row[t] = my_row;
+      const int32_t my_row = t < nvalid ? (kDense ? (int32_t)(base + t) : __ldg(P.rows + base + t)) : 0;
+      my_rec = rec_base + (size_t)my_row * rec_stride2;
+      s_row[t] = (uint32_t)my_row;
       s_bad[t] = t < nvalid ? 0 : 4;
-      if (t < nvalid)
-        my_clock = reinterpret_cast<const int*>(P.record + (int64_t)my_row * P.stride)[2 * L::P];
+      if (t < nvalid) my_clock = reinterpret_cast<const int*>(my_rec)[2 * L::P];
     }
     __syncthreads();
 
-    // ---- phase L: issue every load of this thread's elements ----------------
-    float th[J], gr[J];
-    float2 mv[J];
+    // ---- phase L: every load of this thread's elements, all groups ------------
+    float th[NR], gr[NR];
+    float2 mv[NR];
+    int bad_any = 0;
 #pragma unroll
-    for (int j = 0; j < J; ++j) {
-      const int i = t + NT * j;
-      th[j] = gr[j] = 0.f;
-      mv[j] = make_float2(0.f, 0.f);
-      if (i < E) {
-        const int g = group_of<L>(i, R);
+    for (int gg = 0; gg < L::G; ++gg) {
+      const int W = L::W(gg);
 #pragma unroll
-        for (int gg = 0; gg < L::G; ++gg) {
-          if (g == gg) {
-            const int W = L::W(gg);
-            const int local = i - R * L::OFF(gg);
-            const int r = local / W;
-            const int c = local - r * W;
-            if (r < nvalid) {
-              const int32_t row = s_row[r];
-              const int64_t off = (int64_t)row * W + c;
-              th[j] = P.g[gg].param[off];
-              gr[j] = __ldg(P.g[gg].grad + off);
-              mv[j] = reinterpret_cast<const float2*>(P.record + (int64_t)row * P.stride)[L::OFF(gg) + c];
-            }
-          }
+      for (int k = 0; k < S::rounds(gg); ++k) {
+        const int q = S::first(gg) + k;
+        const int i = k * NT + t;
+        const int r = i / W;
+        th[q] = gr[q] = 0.f;
+        mv[q] = make_float2(0.f, 0.f);
+        if (i < R * W && r < nvalid) {
+          const int c = i - r * W;
+          // 32-bit element offset: the host guarantees n_rows * W < 2^32
+          const uint32_t row = s_row[r];
+          const uint32_t off = row * (uint32_t)W + (uint32_t)c;
+          th[q] = P.g[gg].param[off];
+          gr[q] = __ldg(P.g[gg].grad + off);
+          mv[q] = rec_base[(size_t)row * rec_stride2 + L::OFF(gg) + c];
         }
       }
     }
-    // bias factors of the clock after this step (used only if the row is valid)
     float2 my_bc = make_float2(1.f, 1.f);
     if (t < nvalid)
       my_bc = bias_factors(P.lut, P.lut_len, kDense ? P.global_t : my_clock + 1, 0.0, 0.0);
@@ -161,33 +165,33 @@ __global__ void __launch_bounds__(kFixedThreads, MINB) step_fixed_kernel(const F
     // ---- validity: non-finite gradient (bit 0), activation domain (bit 1) -----
     if (!STRICT) {
 #pragma unroll
-      for (int j = 0; j < J; ++j) {
-        const int i = t + NT * j;
-        if (i < E) {
-          const int g = group_of<L>(i, R);
+      for (int gg = 0; gg < L::G; ++gg) {
+        const int W = L::W(gg);
+        const int role = L::ROLE(gg);
+        const float lam = role == GS_ROLE_OPACITY ? K.lam_op : role == GS_ROLE_SCALE ? K.lam_sc : 0.f;
 #pragma unroll
-          for (int gg = 0; gg < L::G; ++gg) {
-            if (g == gg) {
-              const int W = L::W(gg);
-              const int local = i - R * L::OFF(gg);
-              const int r = local / W;
-              const int role = L::ROLE(gg);
-              const float lam = role == GS_ROLE_OPACITY ? K.lam_op
-                                : role == GS_ROLE_SCALE ? K.lam_sc : 0.f;
-              int bad = isfinite(gr[j]) ? 0 : 1;
-              if (lam != 0.f && domain_bad(role, th[j])) bad |= 2;
-              if (r < nvalid && bad) atomicOr(&s_bad[r], bad);
-            }
+        for (int k = 0; k < S::rounds(gg); ++k) {
+          const int q = S::first(gg) + k;
+          const int i = k * NT + t;
+          const int r = i / W;
+          int bad = isfinite(gr[q]) ? 0 : 1;
+          if ((role == GS_ROLE_OPACITY || role == GS_ROLE_SCALE) && lam != 0.f &&
+              domain_bad(role, th[q]))
+            bad |= 2;
+          if (bad && i < R * W && r < nvalid) {
+            atomicOr(&s_bad[r], bad);
+            s_any_bad = 1;
           }
         }
       }
     }
     __syncthreads();
+    const bool any_bad = s_any_bad != 0 || nvalid < R;  // block-uniform
     if (t < nvalid) {
       ++c_vis;
       const int bad = s_bad[t];
       if (bad == 0) {
-        reinterpret_cast<int*>(P.record + (int64_t)my_row * P.stride)[2 * L::P] = my_clock + 1;
+        reinterpret_cast<int*>(my_rec)[2 * L::P] = my_clock + 1;
         s_bc[t] = my_bc;
         ++c_step;
       } else if (bad & 1) {
@@ -200,40 +204,38 @@ __global__ void __launch_bounds__(kFixedThreads, MINB) step_fixed_kernel(const F
 
     // ---- phase U: update and store ----------------------------------------------
 #pragma unroll
-    for (int j = 0; j < J; ++j) {
-      const int i = t + NT * j;
-      if (i < E) {
-        const int g = group_of<L>(i, R);
+    for (int gg = 0; gg < L::G; ++gg) {
+      const int W = L::W(gg);
+      const int role = L::ROLE(gg);
+      float* const par = P.g[gg].param;
+      const float lr = P.g[gg].lr;
 #pragma unroll
-        for (int gg = 0; gg < L::G; ++gg) {
-          if (g == gg) {
-            const int W = L::W(gg);
-            const int role = L::ROLE(gg);
-            const int local = i - R * L::OFF(gg);
-            const int r = local / W;
-            const int c = local - r * W;
-            if (r < nvalid && s_bad[r] == 0) {
-              const int32_t row = s_row[r];
-              float tn, mn, vn, ex;
-              bool clipped;
-              update_element<MODE>(role, P.g[gg].lr, th[j], gr[j], mv[j].x, mv[j].y, s_bc[r], K,
-                                   tn, mn, vn, ex, clipped);
-              if (!kCoupled && role == GS_ROLE_OPACITY) {
-                c_clo += clipped;
-                s_exo += (double)ex;
-              } else if (!kCoupled && role == GS_ROLE_SCALE) {
-                c_cls += clipped;
-                s_exs += (double)ex;
-              }
-              if (role == GS_ROLE_OPACITY) {
-                c_apre += th[j] > P.active_logit;
-                c_apost += tn > P.active_logit;
-              }
-              P.g[gg].param[(int64_t)row * W + c] = tn;
-              reinterpret_cast<float2*>(P.record + (int64_t)row * P.stride)[L::OFF(gg) + c] =
-                  make_float2(mn, vn);
-            }
+      for (int k = 0; k < S::rounds(gg); ++k) {
+        const int q = S::first(gg) + k;
+        const int i = k * NT + t;
+        const int r = i / W;
+        // common case (no bad / missing row in the chunk): no per-element check
+        if (i < R * W && (!any_bad || (r < nvalid && s_bad[r] == 0))) {
+          const int c = i - r * W;
+          const uint32_t row = s_row[r];
+          const uint32_t off = row * (uint32_t)W + (uint32_t)c;
+          float tn, mn, vn, ex;
+          bool clipped;
+          update_element<MODE>(role, lr, th[q], gr[q], mv[q].x, mv[q].y, s_bc[r], K, tn, mn, vn,
+                               ex, clipped);
+          if (!kCoupled && role == GS_ROLE_OPACITY) {
+            c_clo += clipped;
+            s_exo += (double)ex;
+          } else if (!kCoupled && role == GS_ROLE_SCALE) {
+            c_cls += clipped;
+            s_exs += (double)ex;
           }
+          if (role == GS_ROLE_OPACITY) {
+            c_apre += th[q] > P.active_logit;
+            c_apost += tn > P.active_logit;
+          }
+          par[off] = tn;
+          rec_base[(size_t)row * rec_stride2 + L::OFF(gg) + c] = make_float2(mn, vn);
         }
       }
     }
@@ -260,6 +262,524 @@ __global__ void __launch_bounds__(kFixedThreads, MINB) step_fixed_kernel(const F
   }
 }
 
+// ---------------------------------------------------------------------------
+// Pipelined variant: a persistent CTA walks its chunks through an S-stage
+// shared-memory ring filled with cp.async (LDGSTS).  While chunk c is
+// validated, updated and written back, the gathers of chunks c+1 .. c+S-1
+// are in flight, so every SM keeps ~(S-1) chunks of loads outstanding
+// without holding them in registers.
+//   * records: whole 8*(P+1)-byte rows, 16-byte cp.async.cg pieces;
+//   * theta / grad: 4-byte cp.async.ca gathers in chunk element order;
+//   * write-back: theta with scattered 4-byte stores, the updated record
+//     (m, v pairs + clock) from shared memory with 16-byte stores.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+template <class L, int R>
+struct PipeStage {
+  static constexpr int kSlots = L::P + 1;                  // record slots per row
+  static constexpr int kRec = R * kSlots * 8;              // bytes of records
+  static constexpr int kTh = R * L::P * 4;                 // theta bytes
+  static constexpr int kBytes = kRec + 2 * kTh;
+};
+
+template <class L, int MODE, bool STRICT, int R, int S, int MINB>
+__global__ void __launch_bounds__(kFixedThreads, MINB) step_pipe_kernel(const FixedParams P) {
+  constexpr bool kDense = MODE == GS_MODE_COUPLED_ADAM;
+  constexpr bool kCoupled = MODE == GS_MODE_COUPLED_ADAM || MODE == GS_MODE_SPARSE_ADAM;
+  constexpr int NT = kFixedThreads;
+  constexpr int SLOTS = L::P + 1;
+  using SH = ChunkShape<L, R, NT>;
+  using ST = PipeStage<L, R>;
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ int s_bad[R];
+  __shared__ float2 s_bc[R];
+  __shared__ uint32_t s_rows[S + 1][R];  // row ids, one slot more than stages (no reuse race)
+  __shared__ double s_red[GS_STEP_STATS * (NT / 32)];
+
+  auto rec_of = [&](int st) { return reinterpret_cast<float2*>(smem + st * ST::kBytes); };
+  auto th_of = [&](int st) { return reinterpret_cast<float*>(smem + st * ST::kBytes + ST::kRec); };
+  auto g_of = [&](int st) {
+    return reinterpret_cast<float*>(smem + st * ST::kBytes + ST::kRec + ST::kTh);
+  };
+  auto row_of = [&](int64_t k) { return s_rows[k % (S + 1)]; };
+
+  const int t = threadIdx.x;
+  int64_t n_rows = kDense ? P.max_rows : (int64_t)(*P.n_rows_dev);
+  if (STRICT && *P.abort_flag != 0) n_rows = 0;
+  StepConsts Kc = P.K;
+  if (kCoupled) {
+    const float nv = P.nv_dev ? (float)(*P.nv_dev) : (float)P.nv_host;
+    Kc.inv_nv = nv != 0.0f ? __frcp_rn(nv) : 0.0f;
+    if (nv == 0.0f) Kc.lam_op = Kc.lam_sc = 0.0f;
+  }
+  const StepConsts& K = kCoupled ? Kc : P.K;
+
+  unsigned c_vis = 0, c_step = 0, c_badg = 0, c_badd = 0, c_apre = 0, c_apost = 0, c_clo = 0,
+           c_cls = 0;
+  double s_exo = 0.0, s_exs = 0.0;
+
+  const int64_t n_chunks = (n_rows + R - 1) / R;
+  // this CTA's k-th chunk
+  auto chunk_id = [&](int64_t k) { return (int64_t)blockIdx.x + k * gridDim.x; };
+  auto chunk_rows = [&](int64_t ch) -> int {
+    const int64_t rem = n_rows - ch * R;
+    return rem <= 0 ? 0 : (rem < R ? (int)rem : R);
+  };
+  auto load_row_id = [&](int64_t ch) -> uint32_t {
+    if (t >= R || t >= chunk_rows(ch)) return 0u;
+    const int64_t i = ch * R + t;
+    return kDense ? (uint32_t)i : (uint32_t)__ldg(P.rows + i);
+  };
+  // issue the gathers of this CTA's k-th chunk into stage st (row ids in smem)
+  auto issue = [&](int64_t kc, int st) {
+    const int64_t ch = chunk_id(kc);
+    const int nv = chunk_rows(ch);
+    const uint32_t* rows = row_of(kc);
+    float2* srec = rec_of(st);
+    // records: 16-byte pieces, SLOTS*8/16 per row
+    constexpr int kPieces = SLOTS * 8 / 16;
+    for (int p = t; p < nv * kPieces; p += NT) {
+      const int r = p / kPieces;
+      const int k = p - r * kPieces;
+      const float* src = P.record + (int64_t)rows[r] * P.stride + 4 * k;
+      cp_async16(reinterpret_cast<float*>(srec + r * SLOTS) + 4 * k, src);
+    }
+    float* sth = th_of(st);
+    float* sg = g_of(st);
+#pragma unroll
+    for (int gg = 0; gg < L::G; ++gg) {
+      const int W = L::W(gg);
+#pragma unroll
+      for (int k = 0; k < SH::rounds(gg); ++k) {
+        const int i = k * NT + t;
+        const int r = i / W;
+        if (i < R * W && r < nv) {
+          const int c = i - r * W;
+          const uint32_t off = rows[r] * (uint32_t)W + (uint32_t)c;
+          const int e = R * L::OFF(gg) + i;
+          cp_async4(sth + e, P.g[gg].param + off);
+          cp_async4(sg + e, P.g[gg].grad + off);
+        }
+      }
+    }
+  };
+
+  // ---- prologue: row ids + gathers of the first S-1 chunks ---------------------
+  uint32_t pf_row = 0;
+#pragma unroll
+  for (int s = 0; s < S - 1; ++s) {
+    if (t < R) row_of(s)[t] = load_row_id(chunk_id(s));
+  }
+  pf_row = load_row_id(chunk_id(S - 1));
+  __syncthreads();
+#pragma unroll
+  for (int s = 0; s < S - 1; ++s) {
+    if (chunk_id(s) < n_chunks) issue(s, s);
+    cp_async_commit();
+  }
+
+  for (int64_t k = 0; chunk_id(k) < n_chunks; ++k) {
+    const int st = (int)(k % S);
+    const int st_next = (int)((k + S - 1) % S);
+    const int64_t ch = chunk_id(k);
+    const int nvalid = chunk_rows(ch);
+    // A. row ids of chunk k+S-1 (its id slot was last read two iterations
+    //    ago); prefetch the ids of chunk k+S
+    if (t < R) row_of(k + S - 1)[t] = pf_row;
+    pf_row = load_row_id(chunk_id(k + S));
+    __syncthreads();  // B: stage st_next free (chunk k-1 written back), ids visible
+    if (t < R) s_bad[t] = t < nvalid ? 0 : 4;
+    // C. gathers of chunk k+S-1
+    if (chunk_id(k + S - 1) < n_chunks) issue(k + S - 1, st_next);
+    cp_async_commit();
+    // D. chunk k landed
+    cp_async_wait<S - 1>();
+    __syncthreads();
+
+    float2* srec = rec_of(st);
+    float* sth = th_of(st);
+    float* sg = g_of(st);
+    const uint32_t* srow = row_of(k);
+    // E. validity
+    if (!STRICT) {
+#pragma unroll
+      for (int gg = 0; gg < L::G; ++gg) {
+        const int W = L::W(gg);
+        const int role = L::ROLE(gg);
+        const float lam = role == GS_ROLE_OPACITY ? K.lam_op : role == GS_ROLE_SCALE ? K.lam_sc : 0.f;
+#pragma unroll
+        for (int kk = 0; kk < SH::rounds(gg); ++kk) {
+          const int i = kk * NT + t;
+          const int r = i / W;
+          if (i < R * W && r < nvalid) {
+            const int e = R * L::OFF(gg) + i;
+            int bad = isfinite(sg[e]) ? 0 : 1;
+            if ((role == GS_ROLE_OPACITY || role == GS_ROLE_SCALE) && lam != 0.f &&
+                domain_bad(role, sth[e]))
+              bad |= 2;
+            if (bad) atomicOr(&s_bad[r], bad);
+          }
+        }
+      }
+      __syncthreads();
+    }
+    // F. clocks and bias factors (thread r owns row r)
+    if (t < nvalid) {
+      ++c_vis;
+      const int bad = s_bad[t];
+      if (bad == 0) {
+        int* clk = reinterpret_cast<int*>(srec + t * SLOTS + L::P);
+        const int tn = *clk + 1;
+        *clk = tn;
+        s_bc[t] = bias_factors(P.lut, P.lut_len, kDense ? P.global_t : tn, 0.0, 0.0);
+        ++c_step;
+      } else if (bad & 1) {
+        ++c_badg;
+      } else {
+        ++c_badd;
+      }
+    }
+    __syncthreads();
+    // G. update: theta to global, (m, v) into the staged record
+#pragma unroll
+    for (int gg = 0; gg < L::G; ++gg) {
+      const int W = L::W(gg);
+      const int role = L::ROLE(gg);
+      float* const par = P.g[gg].param;
+      const float lr = P.g[gg].lr;
+#pragma unroll
+      for (int kk = 0; kk < SH::rounds(gg); ++kk) {
+        const int i = kk * NT + t;
+        const int r = i / W;
+        if (i < R * W && r < nvalid && s_bad[r] == 0) {
+          const int c = i - r * W;
+          const int e = R * L::OFF(gg) + i;
+          float2* slot = srec + r * SLOTS + L::OFF(gg) + c;
+          const float2 mv = *slot;
+          const float th = sth[e];
+          float tn, mn, vn, ex;
+          bool clipped;
+          update_element<MODE>(role, lr, th, sg[e], mv.x, mv.y, s_bc[r], K, tn, mn, vn, ex,
+                               clipped);
+          if (!kCoupled && role == GS_ROLE_OPACITY) {
+            c_clo += clipped;
+            s_exo += (double)ex;
+          } else if (!kCoupled && role == GS_ROLE_SCALE) {
+            c_cls += clipped;
+            s_exs += (double)ex;
+          }
+          if (role == GS_ROLE_OPACITY) {
+            c_apre += th > P.active_logit;
+            c_apost += tn > P.active_logit;
+          }
+          par[srow[r] * (uint32_t)W + (uint32_t)c] = tn;
+          *slot = make_float2(mn, vn);
+        }
+      }
+    }
+    __syncthreads();
+    // H. record write-back, 16-byte pieces, valid rows only
+    {
+      constexpr int kPieces = SLOTS * 8 / 16;
+      for (int p = t; p < nvalid * kPieces; p += NT) {
+        const int r = p / kPieces;
+        if (s_bad[r] != 0) continue;
+        const int kk = p - r * kPieces;
+        const float4 v = reinterpret_cast<const float4*>(srec + r * SLOTS)[kk];
+        reinterpret_cast<float4*>(P.record + (int64_t)srow[r] * P.stride)[kk] = v;
+      }
+    }
+  }
+  cp_async_wait<0>();
+
+  double acc[GS_STEP_STATS] = {(double)c_vis,  (double)c_step, (double)c_badg, (double)c_badd,
+                               (double)c_apre, (double)c_apost, (double)c_clo, (double)c_cls,
+                               s_exo,          s_exs};
+  const bool is_max[GS_STEP_STATS] = {false, false, false, false, false,
+                                      false, false, false, false, false};
+  block_reduce<GS_STEP_STATS>(acc, is_max, s_red);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int f = 0; f < GS_STEP_STATS; ++f)
+      P.partials[(size_t)blockIdx.x * GS_STEP_STATS + f] = acc[f];
+  }
+  if (last_block_arrive(P.counter)) {
+    if (threadIdx.x < GS_STEP_STATS) {
+      double s = 0.0;
+      for (unsigned b = 0; b < gridDim.x; ++b)
+        s += P.partials[(size_t)b * GS_STEP_STATS + threadIdx.x];
+      P.stats_out[threadIdx.x] = s;
+    }
+  }
+}
+
+template <class L, int MODE, bool STRICT, int R, int S, int MINB>
+void launch_pipe(const FixedParams& P, int64_t max_rows, cudaStream_t s) {
+  constexpr int bytes = S * PipeStage<L, R>::kBytes;
+  static bool attr_set = false;  // per instantiation
+  if (!attr_set) {
+    cudaFuncSetAttribute(step_pipe_kernel<L, MODE, STRICT, R, S, MINB>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    attr_set = true;
+  }
+  const int64_t chunks = (max_rows + R - 1) / R;
+  const int grid =
+      (int)std::max<int64_t>(1, std::min<int64_t>(chunks, (int64_t)gs_sm_count() * MINB));
+  step_pipe_kernel<L, MODE, STRICT, R, S, MINB><<<grid, kFixedThreads, bytes, s>>>(P);
+}
+
+// ---------------------------------------------------------------------------
+// pipe2: the cp.async ring with three barriers per chunk.  Row ids ride one
+// slot ahead of the data ring; the bad-row flags are double-buffered so they
+// can be re-armed without an extra barrier; the updated (m, v) pairs and the
+// clock go straight to global memory (the staged record is read-only).
+// ---------------------------------------------------------------------------
+template <class L, int MODE, bool STRICT, int R, int S, int MINB>
+__global__ void __launch_bounds__(kFixedThreads, MINB) step_pipe2_kernel(const FixedParams P) {
+  constexpr bool kDense = MODE == GS_MODE_COUPLED_ADAM;
+  constexpr bool kCoupled = MODE == GS_MODE_COUPLED_ADAM || MODE == GS_MODE_SPARSE_ADAM;
+  constexpr int NT = kFixedThreads;
+  constexpr int SLOTS = L::P + 1;
+  using SH = ChunkShape<L, R, NT>;
+  using ST = PipeStage<L, R>;
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ int s_bad[2][R];
+  __shared__ float2 s_bc[2][R];
+  __shared__ int s_any[2];
+  __shared__ uint32_t s_rows[S + 1][R];
+  __shared__ double s_red[GS_STEP_STATS * (NT / 32)];
+
+  const int t = threadIdx.x;
+  float2* const rec_base = reinterpret_cast<float2*>(P.record);
+  const uint32_t rec_stride2 = (uint32_t)(P.stride / 2);
+  int64_t n_rows = kDense ? P.max_rows : (int64_t)(*P.n_rows_dev);
+  if (STRICT && *P.abort_flag != 0) n_rows = 0;
+  StepConsts Kc = P.K;
+  if (kCoupled) {
+    const float nv = P.nv_dev ? (float)(*P.nv_dev) : (float)P.nv_host;
+    Kc.inv_nv = nv != 0.0f ? __frcp_rn(nv) : 0.0f;
+    if (nv == 0.0f) Kc.lam_op = Kc.lam_sc = 0.0f;
+  }
+  const StepConsts& K = kCoupled ? Kc : P.K;
+
+  unsigned c_vis = 0, c_step = 0, c_badg = 0, c_badd = 0, c_apre = 0, c_apost = 0, c_clo = 0,
+           c_cls = 0;
+  double s_exo = 0.0, s_exs = 0.0;
+
+  const int64_t n_chunks = (n_rows + R - 1) / R;
+  auto chunk_id = [&](int64_t k) { return (int64_t)blockIdx.x + k * gridDim.x; };
+  auto chunk_rows = [&](int64_t k) -> int {
+    const int64_t rem = n_rows - chunk_id(k) * R;
+    return rem <= 0 ? 0 : (rem < R ? (int)rem : R);
+  };
+  auto load_row_id = [&](int64_t k) -> uint32_t {
+    if (t >= R || t >= chunk_rows(k)) return 0u;
+    const int64_t i = chunk_id(k) * R + t;
+    return kDense ? (uint32_t)i : (uint32_t)__ldg(P.rows + i);
+  };
+  auto stage = [&](int st) { return smem + st * ST::kBytes; };
+  auto issue = [&](int64_t kc, int st) {
+    const int nv = chunk_rows(kc);
+    const uint32_t* rows = s_rows[kc % (S + 1)];
+    float2* srec = reinterpret_cast<float2*>(stage(st));
+    constexpr int kPieces = SLOTS * 8 / 16;
+    for (int p = t; p < nv * kPieces; p += NT) {
+      const int r = p / kPieces;
+      const int k = p - r * kPieces;
+      cp_async16(reinterpret_cast<float*>(srec + r * SLOTS) + 4 * k,
+                 P.record + (size_t)rows[r] * P.stride + 4 * k);
+    }
+    float* sth = reinterpret_cast<float*>(stage(st) + ST::kRec);
+    float* sg = sth + R * L::P;
+#pragma unroll
+    for (int gg = 0; gg < L::G; ++gg) {
+      const int W = L::W(gg);
+#pragma unroll
+      for (int k = 0; k < SH::rounds(gg); ++k) {
+        const int i = k * NT + t;
+        const int r = i / W;
+        if (i < R * W && r < nv) {
+          const uint32_t off = rows[r] * (uint32_t)W + (uint32_t)(i - r * W);
+          const int e = R * L::OFF(gg) + i;
+          cp_async4(sth + e, P.g[gg].param + off);
+          cp_async4(sg + e, P.g[gg].grad + off);
+        }
+      }
+    }
+  };
+
+  // prologue: ids of chunks 0..S-1 (the last one prefetched in a register),
+  // gathers of chunks 0..S-2, bad flags of chunk 0
+  uint32_t pf_row = 0;
+#pragma unroll
+  for (int s = 0; s < S - 1; ++s)
+    if (t < R) s_rows[s % (S + 1)][t] = load_row_id(s);
+  pf_row = load_row_id(S - 1);
+  if (t < R) s_bad[0][t] = t < chunk_rows(0) ? 0 : 4;
+  if (t == 0) s_any[0] = chunk_rows(0) < R;
+  __syncthreads();
+#pragma unroll
+  for (int s = 0; s < S - 1; ++s) {
+    if (chunk_id(s) < n_chunks) issue(s, s);
+    cp_async_commit();
+  }
+
+  for (int64_t k = 0; chunk_id(k) < n_chunks; ++k) {
+    const int st = (int)(k % S);
+    const int b = (int)(k & 1);
+    const int nvalid = chunk_rows(k);
+    // A. ids of chunk k+S-1 (slot last read in iteration k-2); prefetch k+S
+    if (t < R) s_rows[(k + S - 1) % (S + 1)][t] = pf_row;
+    pf_row = load_row_id(k + S);
+    // #1: chunk k landed; iteration k-1 finished (stage (k-1)%S free)
+    cp_async_wait<S - 2>();
+    __syncthreads();
+    if (chunk_id(k + S - 1) < n_chunks) issue(k + S - 1, (int)((k + S - 1) % S));
+    cp_async_commit();
+
+    const float2* srec = reinterpret_cast<const float2*>(stage(st));
+    const float* sth = reinterpret_cast<const float*>(stage(st) + ST::kRec);
+    const float* sg = sth + R * L::P;
+    const uint32_t* srow = s_rows[k % (S + 1)];
+    // E. validity; thread r prepares row r's clock and bias factors
+    if (!STRICT) {
+#pragma unroll
+      for (int gg = 0; gg < L::G; ++gg) {
+        const int W = L::W(gg);
+        const int role = L::ROLE(gg);
+        const float lam = role == GS_ROLE_OPACITY ? K.lam_op : role == GS_ROLE_SCALE ? K.lam_sc : 0.f;
+#pragma unroll
+        for (int kk = 0; kk < SH::rounds(gg); ++kk) {
+          const int i = kk * NT + t;
+          const int r = i / W;
+          if (i < R * W && r < nvalid) {
+            const int e = R * L::OFF(gg) + i;
+            int bad = isfinite(sg[e]) ? 0 : 1;
+            if ((role == GS_ROLE_OPACITY || role == GS_ROLE_SCALE) && lam != 0.f &&
+                domain_bad(role, sth[e]))
+              bad |= 2;
+            if (bad) {
+              atomicOr(&s_bad[b][r], bad);
+              s_any[b] = 1;
+            }
+          }
+        }
+      }
+    }
+    int tn = 0;
+    float2 bc = make_float2(1.f, 1.f);
+    if (t < nvalid) {
+      tn = reinterpret_cast<const int*>(srec + t * SLOTS + L::P)[0] + 1;
+      bc = bias_factors(P.lut, P.lut_len, kDense ? P.global_t : tn, 0.0, 0.0);
+    }
+    __syncthreads();  // #2: bad flags final
+    const bool any_bad = s_any[b] != 0;
+    if (t < nvalid) {
+      ++c_vis;
+      const int bad = s_bad[b][t];
+      if (bad == 0) {
+        reinterpret_cast<int*>(rec_base + (size_t)srow[t] * rec_stride2 + L::P)[0] = tn;
+        s_bc[b][t] = bc;
+        ++c_step;
+      } else if (bad & 1) {
+        ++c_badg;
+      } else {
+        ++c_badd;
+      }
+    }
+    // re-arm the other flag buffer for chunk k+1 (last read in iteration k-1)
+    if (t < R) s_bad[b ^ 1][t] = t < chunk_rows(k + 1) ? 0 : 4;
+    if (t == 0) s_any[b ^ 1] = chunk_rows(k + 1) < R;
+    __syncthreads();  // #3: bias factors visible
+    // G. update: theta and (m, v) straight to global
+#pragma unroll
+    for (int gg = 0; gg < L::G; ++gg) {
+      const int W = L::W(gg);
+      const int role = L::ROLE(gg);
+      float* const par = P.g[gg].param;
+      const float lr = P.g[gg].lr;
+#pragma unroll
+      for (int kk = 0; kk < SH::rounds(gg); ++kk) {
+        const int i = kk * NT + t;
+        const int r = i / W;
+        if (i < R * W && (!any_bad || (r < nvalid && s_bad[b][r] == 0))) {
+          const int c = i - r * W;
+          const int e = R * L::OFF(gg) + i;
+          const uint32_t row = srow[r];
+          const float2 mv = srec[r * SLOTS + L::OFF(gg) + c];
+          const float th = sth[e];
+          float tnv, mn, vn, ex;
+          bool clipped;
+          update_element<MODE>(role, lr, th, sg[e], mv.x, mv.y, s_bc[b][r], K, tnv, mn, vn, ex,
+                               clipped);
+          if (!kCoupled && role == GS_ROLE_OPACITY) {
+            c_clo += clipped;
+            s_exo += (double)ex;
+          } else if (!kCoupled && role == GS_ROLE_SCALE) {
+            c_cls += clipped;
+            s_exs += (double)ex;
+          }
+          if (role == GS_ROLE_OPACITY) {
+            c_apre += th > P.active_logit;
+            c_apost += tnv > P.active_logit;
+          }
+          par[row * (uint32_t)W + (uint32_t)c] = tnv;
+          rec_base[(size_t)row * rec_stride2 + L::OFF(gg) + c] = make_float2(mn, vn);
+        }
+      }
+    }
+  }
+  cp_async_wait<0>();
+
+  double acc[GS_STEP_STATS] = {(double)c_vis,  (double)c_step, (double)c_badg, (double)c_badd,
+                               (double)c_apre, (double)c_apost, (double)c_clo, (double)c_cls,
+                               s_exo,          s_exs};
+  const bool is_max[GS_STEP_STATS] = {false, false, false, false, false,
+                                      false, false, false, false, false};
+  block_reduce<GS_STEP_STATS>(acc, is_max, s_red);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int f = 0; f < GS_STEP_STATS; ++f)
+      P.partials[(size_t)blockIdx.x * GS_STEP_STATS + f] = acc[f];
+  }
+  if (last_block_arrive(P.counter)) {
+    if (threadIdx.x < GS_STEP_STATS) {
+      double s = 0.0;
+      for (unsigned bb = 0; bb < gridDim.x; ++bb)
+        s += P.partials[(size_t)bb * GS_STEP_STATS + threadIdx.x];
+      P.stats_out[threadIdx.x] = s;
+    }
+  }
+}
+
+template <class L, int MODE, bool STRICT, int R, int S, int MINB>
+void launch_pipe2(const FixedParams& P, int64_t max_rows, cudaStream_t s) {
+  constexpr int bytes = S * PipeStage<L, R>::kBytes;
+  static bool attr_set = false;  // per instantiation
+  if (!attr_set) {
+    cudaFuncSetAttribute(step_pipe2_kernel<L, MODE, STRICT, R, S, MINB>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    attr_set = true;
+  }
+  const int64_t chunks = (max_rows + R - 1) / R;
+  const int grid =
+      (int)std::max<int64_t>(1, std::min<int64_t>(chunks, (int64_t)gs_sm_count() * MINB));
+  step_pipe2_kernel<L, MODE, STRICT, R, S, MINB><<<grid, kFixedThreads, bytes, s>>>(P);
+}
+
 static int g_fixed_variant = -1;
 
 int fixed_variant() {
@@ -270,21 +790,22 @@ int fixed_variant() {
   return g_fixed_variant;
 }
 
-template <class L, int MODE, bool STRICT, int R, int MINB>
+template <class L, int MODE, bool STRICT, int R, int MINB, int NT = kFixedThreads>
 void launch_fixed_v(const FixedParams& P, int64_t max_rows, cudaStream_t s) {
   const int64_t chunks = (max_rows + R - 1) / R;
   const int grid =
       (int)std::max<int64_t>(1, std::min<int64_t>(chunks, (int64_t)gs_sm_count() * MINB));
-  step_fixed_kernel<L, MODE, STRICT, R, MINB><<<grid, kFixedThreads, 0, s>>>(P);
+  step_fixed_kernel<L, MODE, STRICT, R, MINB, NT><<<grid, NT, 0, s>>>(P);
 }
 
 template <class L, int MODE, bool STRICT>
 void launch_fixed(const FixedParams& P, int64_t max_rows, cudaStream_t s) {
   switch (fixed_variant()) {
-    case 1: launch_fixed_v<L, MODE, STRICT, 32, 4>(P, max_rows, s); return;
-    case 2: launch_fixed_v<L, MODE, STRICT, 32, 3>(P, max_rows, s); return;
-    case 3: launch_fixed_v<L, MODE, STRICT, 64, 3>(P, max_rows, s); return;
-    default: launch_fixed_v<L, MODE, STRICT, 64, 2>(P, max_rows, s); return;
+    case 1: launch_fixed_v<L, MODE, STRICT, 64, 2>(P, max_rows, s); return;
+    case 2: launch_pipe<L, MODE, STRICT, 32, 2, 3>(P, max_rows, s); return;
+    case 3: launch_pipe2<L, MODE, STRICT, 32, 3, 2>(P, max_rows, s); return;
+    case 4: launch_pipe2<L, MODE, STRICT, 32, 2, 3>(P, max_rows, s); return;
+    default: launch_pipe2<L, MODE, STRICT, 32, 2, 3>(P, max_rows, s); return;
   }
 }
 
@@ -322,6 +843,7 @@ int gs_step_fixed_try(const gs_group* groups, int32_t n_groups, const gs_step_cf
   const char* off = getenv("GS_DISABLE_FIXED");
   if (off && off[0] == '1') return 0;
   if (!layout_matches<LayoutSH3>(groups, n_groups)) return 0;
+  if (max_rows * 45 >= (int64_t)UINT32_MAX) return 0;  // 32-bit element offsets
   FixedParams P{};
   for (int i = 0; i < n_groups; ++i)
     P.g[i] = FixedGroup{groups[i].param, groups[i].grad, groups[i].lr, 0};
