@@ -404,8 +404,9 @@ def ours(args, wl, p_vis):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak,
                          "traffic": traffic_from_profiles(args.workload, args.mask, p_vis),
-                         "kernel": "gs::step_rows_kernel (K2)" if args.layout == "rows"
-                                   else "gs::step_kernel (K2)", "peak_source": peak_src,
+                         "kernel": "gs::step_pipe2_kernel<LayoutSH3> (K2, via gs_step_rows)"
+                                   if args.layout == "rows" else "gs::step_kernel (K2, gs_step)",
+                         "peak_source": peak_src,
                          "k2_ms_avg": k2_avg_ms,
                          "k2_bytes_per_launch": sum(k2_bytes) / len(k2_bytes),
                          "bytes_per_visible": 28 * width + 12,

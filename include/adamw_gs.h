@@ -116,9 +116,9 @@ int32_t gs_device_sm_count(void);
 
 /* K1 — visibility compaction: ascending int32 indices of nonzero mask bytes
  * (or radii > 0), count written to *count_out (device).  Bit-exact with
- * np.flatnonzero.  ws: gs_compact_workspace_bytes(n) bytes, zero-filled once
- * at allocation and then reused untouched between calls (single-pass
- * decoupled look-back with epoch-tagged tile status; graph-capturable). */
+ * np.flatnonzero.  ws: gs_compact_workspace_bytes(n) bytes (one int per
+ * 4096-row tile, overwritten by every call; graph-capturable).  Two launches:
+ * per-tile counts, then prefix + ordered writes. */
 size_t gs_compact_workspace_bytes(int64_t n);
 int gs_compact_u8(const uint8_t* mask, int64_t n, int32_t* idx_out, int32_t* count_out,
                   void* ws, size_t ws_bytes, void* stream);

@@ -160,6 +160,30 @@ __device__ __forceinline__ void block_reduce(double (&v)[NV], const bool (&is_ma
   }
 }
 
+// Same as block_reduce for a block of NW warps (any block size).
+template <int NV, int NW>
+__device__ __forceinline__ void block_reduce_n(double (&v)[NV], const bool (&is_max)[NV],
+                                               double* scratch) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int f = 0; f < NV; ++f) v[f] = is_max[f] ? warp_max(v[f]) : warp_sum(v[f]);
+  __syncthreads();
+  if (lane == 0) {
+#pragma unroll
+    for (int f = 0; f < NV; ++f) scratch[f * NW + warp] = v[f];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int f = 0; f < NV; ++f) {
+      double acc = scratch[f * NW];
+      for (int w = 1; w < NW; ++w)
+        acc = is_max[f] ? fmax(acc, scratch[f * NW + w]) : acc + scratch[f * NW + w];
+      v[f] = acc;
+    }
+  }
+}
+
 // Last-block-done finalisation: every CTA writes its partials, the last one
 // to arrive reduces them in CTA order (deterministic) and re-arms the counter.
 // Returns true in thread 0 of the last CTA.
@@ -190,6 +214,52 @@ inline StepConsts make_consts(const gs_step_cfg* cfg) {
   K.inv_ni = cfg->n_pixels_rounded > 0.0 ? (float)(1.0 / cfg->n_pixels_rounded) : 0.0f;
   K.inv_nv = 0.0f;  // coupled modes: set on the device from N_v
   return K;
+}
+
+// Final pass of the deterministic cross-CTA reduction, run by the last CTA:
+// out[f] = sum (or max) over b of partials[b * stride + f].  Each thread folds
+// a fixed strided subset of the CTAs, then a fixed-shape block tree combines
+// the threads, so the result depends only on the grid size.
+template <int NV>
+__device__ __forceinline__ void final_reduce(const double* partials, int nblocks, int stride,
+                                             double* out, const bool (&is_max)[NV],
+                                             double* scratch) {
+  double v[NV];
+#pragma unroll
+  for (int f = 0; f < NV; ++f) v[f] = 0.0;
+  for (int b = threadIdx.x; b < nblocks; b += blockDim.x) {
+#pragma unroll
+    for (int f = 0; f < NV; ++f) {
+      const double x = partials[(size_t)b * stride + f];
+      v[f] = is_max[f] ? fmax(v[f], x) : v[f] + x;
+    }
+  }
+  block_reduce<NV>(v, is_max, scratch);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int f = 0; f < NV; ++f) out[f] = v[f];
+  }
+}
+
+template <int NV, int NW>
+__device__ __forceinline__ void final_reduce_n(const double* partials, int nblocks, int stride,
+                                               double* out, const bool (&is_max)[NV],
+                                               double* scratch) {
+  double v[NV];
+#pragma unroll
+  for (int f = 0; f < NV; ++f) v[f] = 0.0;
+  for (int b = threadIdx.x; b < nblocks; b += blockDim.x) {
+#pragma unroll
+    for (int f = 0; f < NV; ++f) {
+      const double x = partials[(size_t)b * stride + f];
+      v[f] = is_max[f] ? fmax(v[f], x) : v[f] + x;
+    }
+  }
+  block_reduce_n<NV, NW>(v, is_max, scratch);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int f = 0; f < NV; ++f) out[f] = v[f];
+  }
 }
 
 }  // namespace gs

@@ -189,16 +189,10 @@ __global__ void __launch_bounds__(kThreads)
     for (int f = 0; f < kStatsFields; ++f) partials[(size_t)blockIdx.x * kStatsFields + f] = acc[f];
   }
   if (last_block_arrive(counter)) {
-    const int nf = 2 + 5 * S.n;
-    for (int f = threadIdx.x; f < nf; f += blockDim.x) {
-      const bool mx = f >= 2 && (((f - 2) % 5) == 1 || ((f - 2) % 5) == 4);
-      double a = partials[f];
-      for (unsigned b = 1; b < gridDim.x; ++b) {
-        const double x = partials[(size_t)b * kStatsFields + f];
-        a = mx ? fmax(a, x) : a + x;
-      }
-      out[f] = a;
-    }
+    double tmp[kStatsFields];
+    final_reduce<kStatsFields>(partials, gridDim.x, kStatsFields, tmp, is_max, s_red);
+    if (threadIdx.x == 0)
+      for (int f = 0; f < 2 + 5 * S.n; ++f) out[f] = tmp[f];
   }
 }
 
@@ -282,16 +276,10 @@ __global__ void __launch_bounds__(kThreads)
     for (int f = 0; f < kStatsFields; ++f) partials[(size_t)blockIdx.x * kStatsFields + f] = acc[f];
   }
   if (last_block_arrive(counter)) {
-    const int nf = 2 + 5 * S.n;
-    for (int f = threadIdx.x; f < nf; f += blockDim.x) {
-      const bool mx = f >= 2 && (((f - 2) % 5) == 1 || ((f - 2) % 5) == 4);
-      double a = partials[f];
-      for (unsigned b = 1; b < gridDim.x; ++b) {
-        const double x = partials[(size_t)b * kStatsFields + f];
-        a = mx ? fmax(a, x) : a + x;
-      }
-      out[f] = a;
-    }
+    double tmp[kStatsFields];
+    final_reduce<kStatsFields>(partials, gridDim.x, kStatsFields, tmp, is_max, s_red);
+    if (threadIdx.x == 0)
+      for (int f = 0; f < 2 + 5 * S.n; ++f) out[f] = tmp[f];
   }
 }
 

@@ -208,14 +208,8 @@ __global__ void __launch_bounds__(kThreads, kStepBlocksPerSM) step_kernel(const 
 #pragma unroll
     for (int f = 0; f < GS_STEP_STATS; ++f) P.partials[(size_t)blockIdx.x * GS_STEP_STATS + f] = acc[f];
   }
-  if (last_block_arrive(P.counter)) {
-    // sum partials in CTA order, one field per thread
-    if (tid < GS_STEP_STATS) {
-      double s = 0.0;
-      for (unsigned b = 0; b < gridDim.x; ++b) s += P.partials[(size_t)b * GS_STEP_STATS + tid];
-      P.stats_out[tid] = s;
-    }
-  }
+  if (last_block_arrive(P.counter))
+    final_reduce<GS_STEP_STATS>(P.partials, gridDim.x, GS_STEP_STATS, P.stats_out, is_max, s_red);
 }
 
 struct StepWorkspace {

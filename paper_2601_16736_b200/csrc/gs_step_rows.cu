@@ -262,14 +262,8 @@ __global__ void __launch_bounds__(kRowThreads, MINB)
     for (int f = 0; f < GS_STEP_STATS; ++f)
       P.partials[(size_t)blockIdx.x * GS_STEP_STATS + f] = acc[f];
   }
-  if (last_block_arrive(P.counter)) {
-    if (threadIdx.x < GS_STEP_STATS) {
-      double s = 0.0;
-      for (unsigned b = 0; b < gridDim.x; ++b)
-        s += P.partials[(size_t)b * GS_STEP_STATS + threadIdx.x];
-      P.stats_out[threadIdx.x] = s;
-    }
-  }
+  if (last_block_arrive(P.counter))
+    final_reduce<GS_STEP_STATS>(P.partials, gridDim.x, GS_STEP_STATS, P.stats_out, is_max, s_red);
 }
 
 struct RowStepWorkspace {

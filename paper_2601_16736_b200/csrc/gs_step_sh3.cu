@@ -252,14 +252,8 @@ __global__ void __launch_bounds__(NT, MINB) step_fixed_kernel(const FixedParams 
     for (int f = 0; f < GS_STEP_STATS; ++f)
       P.partials[(size_t)blockIdx.x * GS_STEP_STATS + f] = acc[f];
   }
-  if (last_block_arrive(P.counter)) {
-    if (threadIdx.x < GS_STEP_STATS) {
-      double s = 0.0;
-      for (unsigned b = 0; b < gridDim.x; ++b)
-        s += P.partials[(size_t)b * GS_STEP_STATS + threadIdx.x];
-      P.stats_out[threadIdx.x] = s;
-    }
-  }
+  if (last_block_arrive(P.counter))
+    final_reduce<GS_STEP_STATS>(P.partials, gridDim.x, GS_STEP_STATS, P.stats_out, is_max, s_red);
 }
 
 // ---------------------------------------------------------------------------
@@ -516,14 +510,8 @@ __global__ void __launch_bounds__(kFixedThreads, MINB) step_pipe_kernel(const Fi
     for (int f = 0; f < GS_STEP_STATS; ++f)
       P.partials[(size_t)blockIdx.x * GS_STEP_STATS + f] = acc[f];
   }
-  if (last_block_arrive(P.counter)) {
-    if (threadIdx.x < GS_STEP_STATS) {
-      double s = 0.0;
-      for (unsigned b = 0; b < gridDim.x; ++b)
-        s += P.partials[(size_t)b * GS_STEP_STATS + threadIdx.x];
-      P.stats_out[threadIdx.x] = s;
-    }
-  }
+  if (last_block_arrive(P.counter))
+    final_reduce<GS_STEP_STATS>(P.partials, gridDim.x, GS_STEP_STATS, P.stats_out, is_max, s_red);
 }
 
 template <class L, int MODE, bool STRICT, int R, int S, int MINB>
@@ -755,14 +743,8 @@ __global__ void __launch_bounds__(kFixedThreads, MINB) step_pipe2_kernel(const F
     for (int f = 0; f < GS_STEP_STATS; ++f)
       P.partials[(size_t)blockIdx.x * GS_STEP_STATS + f] = acc[f];
   }
-  if (last_block_arrive(P.counter)) {
-    if (threadIdx.x < GS_STEP_STATS) {
-      double s = 0.0;
-      for (unsigned bb = 0; bb < gridDim.x; ++bb)
-        s += P.partials[(size_t)bb * GS_STEP_STATS + threadIdx.x];
-      P.stats_out[threadIdx.x] = s;
-    }
-  }
+  if (last_block_arrive(P.counter))
+    final_reduce<GS_STEP_STATS>(P.partials, gridDim.x, GS_STEP_STATS, P.stats_out, is_max, s_red);
 }
 
 template <class L, int MODE, bool STRICT, int R, int S, int MINB>
@@ -778,6 +760,295 @@ void launch_pipe2(const FixedParams& P, int64_t max_rows, cudaStream_t s) {
   const int grid =
       (int)std::max<int64_t>(1, std::min<int64_t>(chunks, (int64_t)gs_sm_count() * MINB));
   step_pipe2_kernel<L, MODE, STRICT, R, S, MINB><<<grid, kFixedThreads, bytes, s>>>(P);
+}
+
+// ---------------------------------------------------------------------------
+// Warp-specialised variant: kProd producer warps fill an S-stage ring with
+// cp.async gathers (row ids, 16-byte record pieces, 4-byte theta / grad
+// elements) and signal a per-stage "full" mbarrier through
+// cp.async.mbarrier.arrive.noinc; kCons consumer warps wait on it, validate,
+// update and store, synchronising only among themselves (named barrier 1),
+// and release the stage through an "empty" mbarrier.  Producers never wait
+// on a block barrier, so gathers for the next chunks stay in flight while
+// the consumers compute.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(a), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cp_async(uint64_t* bar) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ void named_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+template <class L, int R>
+struct WsStage {
+  static constexpr int kSlots = L::P + 1;
+  static constexpr int kRec = R * kSlots * 8;
+  static constexpr int kTh = R * L::P * 4;
+  static constexpr int kBytes = kRec + 2 * kTh + R * 4;  // + row ids
+};
+
+template <class L, int MODE, bool STRICT, int R, int S, int NPW, int NCW, int MINB>
+__global__ void __launch_bounds__((NPW + NCW) * 32, MINB) step_ws_kernel(const FixedParams P) {
+  constexpr bool kDense = MODE == GS_MODE_COUPLED_ADAM;
+  constexpr bool kCoupled = MODE == GS_MODE_COUPLED_ADAM || MODE == GS_MODE_SPARSE_ADAM;
+  constexpr int NC = NCW * 32;  // consumer threads
+  constexpr int NP = NPW * 32;  // producer threads
+  constexpr int SLOTS = L::P + 1;
+  using SH = ChunkShape<L, R, NC>;
+  using ST = WsStage<L, R>;
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ __align__(8) uint64_t full_bar[S];
+  __shared__ __align__(8) uint64_t empty_bar[S];
+  __shared__ int s_bad[S][R];
+  __shared__ int s_any[S];
+  __shared__ float2 s_bc[S][R];
+  __shared__ uint32_t s_crow[S][R];  // consumers' copy of the row ids
+  __shared__ double s_red[GS_STEP_STATS * ((NPW + NCW))];
+
+  const int tid = threadIdx.x;
+  const bool producer = tid >= NC;
+  int64_t n_rows = kDense ? P.max_rows : (int64_t)(*P.n_rows_dev);
+  if (STRICT && *P.abort_flag != 0) n_rows = 0;
+  const int64_t n_chunks = (n_rows + R - 1) / R;
+  auto chunk_id = [&](int64_t k) { return (int64_t)blockIdx.x + k * gridDim.x; };
+  auto chunk_rows = [&](int64_t k) -> int {
+    const int64_t rem = n_rows - chunk_id(k) * R;
+    return rem <= 0 ? 0 : (rem < R ? (int)rem : R);
+  };
+  auto stage = [&](int st) { return smem + st * ST::kBytes; };
+
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full_bar[s], NP);
+      mbar_init(&empty_bar[s], NC);
+    }
+  }
+  if (tid < R * S) s_bad[tid / R][tid % R] = 0;
+  if (tid < S) s_any[tid] = 0;
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  __syncthreads();
+
+  unsigned c_vis = 0, c_step = 0, c_badg = 0, c_badd = 0, c_apre = 0, c_apost = 0, c_clo = 0,
+           c_cls = 0;
+  double s_exo = 0.0, s_exs = 0.0;
+
+  if (producer) {
+    // ------------------------------------------------------------------ producer
+    const int pt = tid - NC;
+    // row id of row pt of chunk k (producer lanes pt < R), prefetched one
+    // chunk ahead so the gathers never wait on the index list
+    auto fetch_id = [&](int64_t k) -> uint32_t {
+      if (pt >= R || pt >= chunk_rows(k)) return 0u;
+      const int64_t i = chunk_id(k) * R + pt;
+      return kDense ? (uint32_t)i : (uint32_t)__ldg(P.rows + i);
+    };
+    uint32_t next_id = fetch_id(0);
+    for (int64_t k = 0; chunk_id(k) < n_chunks; ++k) {
+      const int st = (int)(k % S);
+      const uint32_t my_id = next_id;
+      next_id = fetch_id(k + 1);
+      if (k >= S) mbar_wait(&empty_bar[st], (unsigned)(((k / S) - 1) & 1));
+      const int nv = chunk_rows(k);
+      unsigned char* sb = stage(st);
+      uint32_t* srows = reinterpret_cast<uint32_t*>(sb + ST::kRec + 2 * ST::kTh);
+      if (pt < R) srows[pt] = my_id;
+      named_sync(2, NP);  // producer-only: ids visible to the other producer lanes
+      float2* srec = reinterpret_cast<float2*>(sb);
+      constexpr int kPieces = SLOTS * 8 / 16;
+      for (int p = pt; p < nv * kPieces; p += NP) {
+        const int r = p / kPieces;
+        const int kk = p - r * kPieces;
+        cp_async16(reinterpret_cast<float*>(srec + r * SLOTS) + 4 * kk,
+                   P.record + (size_t)srows[r] * P.stride + 4 * kk);
+      }
+      float* sth = reinterpret_cast<float*>(sb + ST::kRec);
+      float* sg = sth + R * L::P;
+      using PS = ChunkShape<L, R, NP>;
+#pragma unroll
+      for (int gg = 0; gg < L::G; ++gg) {
+        const int W = L::W(gg);
+#pragma unroll
+        for (int kk = 0; kk < PS::rounds(gg); ++kk) {
+          const int i = kk * NP + pt;
+          const int r = i / W;
+          if (i < R * W && r < nv) {
+            const uint32_t off = srows[r] * (uint32_t)W + (uint32_t)(i - r * W);
+            const int e = R * L::OFF(gg) + i;
+            cp_async4(sth + e, P.g[gg].param + off);
+            cp_async4(sg + e, P.g[gg].grad + off);
+          }
+        }
+      }
+      mbar_arrive_cp_async(&full_bar[st]);
+    }
+  } else {
+    // ------------------------------------------------------------------ consumers
+    const int t = tid;
+    StepConsts Kc = P.K;
+    if (kCoupled) {
+      const float nv = P.nv_dev ? (float)(*P.nv_dev) : (float)P.nv_host;
+      Kc.inv_nv = nv != 0.0f ? __frcp_rn(nv) : 0.0f;
+      if (nv == 0.0f) Kc.lam_op = Kc.lam_sc = 0.0f;
+    }
+    const StepConsts& K = kCoupled ? Kc : P.K;
+    float2* const rec_base = reinterpret_cast<float2*>(P.record);
+    const uint32_t rec_stride2 = (uint32_t)(P.stride / 2);
+    for (int64_t k = 0; chunk_id(k) < n_chunks; ++k) {
+      const int st = (int)(k % S);
+      const int nvalid = chunk_rows(k);
+      // row ids straight from the index list (visible after the first named
+      // barrier below); the producers keep their own copy in the stage
+      if (t < R)
+        s_crow[st][t] = t < nvalid ? (kDense ? (uint32_t)(chunk_id(k) * R + t)
+                                             : (uint32_t)__ldg(P.rows + chunk_id(k) * R + t))
+                                   : 0u;
+      mbar_wait(&full_bar[st], (unsigned)((k / S) & 1));
+      const unsigned char* sb = stage(st);
+      const float2* srec = reinterpret_cast<const float2*>(sb);
+      const float* sth = reinterpret_cast<const float*>(sb + ST::kRec);
+      const float* sg = sth + R * L::P;
+      const uint32_t* srow = s_crow[st];
+      if (!STRICT) {
+#pragma unroll
+        for (int gg = 0; gg < L::G; ++gg) {
+          const int W = L::W(gg);
+          const int role = L::ROLE(gg);
+          const float lam = role == GS_ROLE_OPACITY ? K.lam_op : role == GS_ROLE_SCALE ? K.lam_sc : 0.f;
+#pragma unroll
+          for (int kk = 0; kk < SH::rounds(gg); ++kk) {
+            const int i = kk * NC + t;
+            const int r = i / W;
+            if (i < R * W && r < nvalid) {
+              const int e = R * L::OFF(gg) + i;
+              int bad = isfinite(sg[e]) ? 0 : 1;
+              if ((role == GS_ROLE_OPACITY || role == GS_ROLE_SCALE) && lam != 0.f &&
+                  domain_bad(role, sth[e]))
+                bad |= 2;
+              if (bad) {
+                atomicOr(&s_bad[st][r], bad);
+                s_any[st] = 1;
+              }
+            }
+          }
+        }
+      }
+      int tn = 0;
+      float2 bc = make_float2(1.f, 1.f);
+      if (t < nvalid) {
+        tn = reinterpret_cast<const int*>(srec + t * SLOTS + L::P)[0] + 1;
+        bc = bias_factors(P.lut, P.lut_len, kDense ? P.global_t : tn, 0.0, 0.0);
+      }
+      named_sync(1, NC);  // bad flags final
+      const bool any_bad = s_any[st] != 0 || nvalid < R;
+      if (t < nvalid) {
+        ++c_vis;
+        const int bad = s_bad[st][t];
+        if (bad == 0) {
+          reinterpret_cast<int*>(rec_base + (size_t)s_crow[st][t] * rec_stride2 + L::P)[0] = tn;
+          s_bc[st][t] = bc;
+          ++c_step;
+        } else if (bad & 1) {
+          ++c_badg;
+        } else {
+          ++c_badd;
+        }
+      }
+      named_sync(1, NC);  // bias factors visible
+#pragma unroll
+      for (int gg = 0; gg < L::G; ++gg) {
+        const int W = L::W(gg);
+        const int role = L::ROLE(gg);
+        float* const par = P.g[gg].param;
+        const float lr = P.g[gg].lr;
+#pragma unroll
+        for (int kk = 0; kk < SH::rounds(gg); ++kk) {
+          const int i = kk * NC + t;
+          const int r = i / W;
+          if (i < R * W && (!any_bad || (r < nvalid && s_bad[st][r] == 0))) {
+            const int c = i - r * W;
+            const int e = R * L::OFF(gg) + i;
+            const uint32_t row = srow[r];
+            const float2 mv = srec[r * SLOTS + L::OFF(gg) + c];
+            const float th = sth[e];
+            float tnv, mn, vn, ex;
+            bool clipped;
+            update_element<MODE>(role, lr, th, sg[e], mv.x, mv.y, s_bc[st][r], K, tnv, mn, vn,
+                                 ex, clipped);
+            if (!kCoupled && role == GS_ROLE_OPACITY) {
+              c_clo += clipped;
+              s_exo += (double)ex;
+            } else if (!kCoupled && role == GS_ROLE_SCALE) {
+              c_cls += clipped;
+              s_exs += (double)ex;
+            }
+            if (role == GS_ROLE_OPACITY) {
+              c_apre += th > P.active_logit;
+              c_apost += tnv > P.active_logit;
+            }
+            par[row * (uint32_t)W + (uint32_t)c] = tnv;
+            rec_base[(size_t)row * rec_stride2 + L::OFF(gg) + c] = make_float2(mn, vn);
+          }
+        }
+      }
+      named_sync(1, NC);  // all reads of this stage's flags / data done
+      if (t < R) s_bad[st][t] = 0;
+      if (t == 0) s_any[st] = 0;
+      mbar_arrive(&empty_bar[st]);
+    }
+  }
+  cp_async_wait<0>();
+
+  double acc[GS_STEP_STATS] = {(double)c_vis,  (double)c_step, (double)c_badg, (double)c_badd,
+                               (double)c_apre, (double)c_apost, (double)c_clo, (double)c_cls,
+                               s_exo,          s_exs};
+  const bool is_max[GS_STEP_STATS] = {false, false, false, false, false,
+                                      false, false, false, false, false};
+  block_reduce_n<GS_STEP_STATS, (NPW + NCW)>(acc, is_max, s_red);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int f = 0; f < GS_STEP_STATS; ++f)
+      P.partials[(size_t)blockIdx.x * GS_STEP_STATS + f] = acc[f];
+  }
+  if (last_block_arrive(P.counter))
+    final_reduce_n<GS_STEP_STATS, (NPW + NCW)>(P.partials, gridDim.x, GS_STEP_STATS, P.stats_out,
+                                               is_max, s_red);
+}
+
+template <class L, int MODE, bool STRICT, int R, int S, int NPW, int NCW, int MINB>
+void launch_ws(const FixedParams& P, int64_t max_rows, cudaStream_t s) {
+  constexpr int bytes = S * WsStage<L, R>::kBytes;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(step_ws_kernel<L, MODE, STRICT, R, S, NPW, NCW, MINB>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    attr_set = true;
+  }
+  const int64_t chunks = (max_rows + R - 1) / R;
+  const int grid =
+      (int)std::max<int64_t>(1, std::min<int64_t>(chunks, (int64_t)gs_sm_count() * MINB));
+  step_ws_kernel<L, MODE, STRICT, R, S, NPW, NCW, MINB>
+      <<<grid, (NPW + NCW) * 32, bytes, s>>>(P);
 }
 
 static int g_fixed_variant = -1;
@@ -804,7 +1075,9 @@ void launch_fixed(const FixedParams& P, int64_t max_rows, cudaStream_t s) {
     case 1: launch_fixed_v<L, MODE, STRICT, 64, 2>(P, max_rows, s); return;
     case 2: launch_pipe<L, MODE, STRICT, 32, 2, 3>(P, max_rows, s); return;
     case 3: launch_pipe2<L, MODE, STRICT, 32, 3, 2>(P, max_rows, s); return;
-    case 4: launch_pipe2<L, MODE, STRICT, 32, 2, 3>(P, max_rows, s); return;
+    case 4: launch_ws<L, MODE, STRICT, 32, 3, 2, 8, 2>(P, max_rows, s); return;
+    case 5: launch_ws<L, MODE, STRICT, 32, 4, 2, 8, 1>(P, max_rows, s); return;
+    case 6: launch_ws<L, MODE, STRICT, 32, 3, 1, 8, 2>(P, max_rows, s); return;
     default: launch_pipe2<L, MODE, STRICT, 32, 2, 3>(P, max_rows, s); return;
   }
 }

@@ -52,8 +52,8 @@ def test_ctypes_struct_layout_matches_header():
 def test_workspace_queries_without_gpu():
     from paper_2601_16736_b200 import _lib
     lib = _lib.load()
-    assert lib.gs_compact_workspace_bytes(0) >= 64
-    assert lib.gs_compact_workspace_bytes(6_000_000) == 64 + 8 * ((6_000_000 + 4095) // 4096)
+    assert lib.gs_compact_workspace_bytes(0) >= 4
+    assert lib.gs_compact_workspace_bytes(6_000_000) == 4 * ((6_000_000 + 4095) // 4096)
     assert lib.gs_step_workspace_bytes() > 0
 
 
