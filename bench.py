@@ -81,6 +81,8 @@ def parse():
     ap.add_argument("--ref-seconds", type=float, default=150.0,
                     help="budget of the whole --impl reference run")
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-graph", dest="graph", action="store_false",
+                    help="launch the timed steps eagerly instead of as one CUDA graph")
     ap.add_argument("--layout", default="rows", choices=["rows", "groups"],
                     help="optimizer-state layout (row records or per-group tensors)")
     return ap.parse_args()
@@ -268,7 +270,8 @@ def workload_config(args, wl, p_vis, world):
             "state_layout": args.layout,
             "l2": "inputs larger than L2 (working set >> 126 MB)" if n >= 1_000_000 else
                   "L2 flushed between timed steps",
-            "parallelism": f"index-sharded x{world}"}
+            "parallelism": f"index-sharded x{world}",
+            "launch": "CUDA graph of the K timed steps" if (args.graph and world == 1) else "eager"}
 
 
 # --------------------------------------------------------------- our arm
@@ -320,21 +323,11 @@ def ours(args, wl, p_vis):
     stats_sum = torch.zeros(10, dtype=torch.float64, device=dev)
     launches = [0]
 
-    k2_events = []
-
-    def one_step(it, timed):
-        g = grad_sets[it % 2]
-        if timed:
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    def one_step(it):
+        """K1 + K2 (+ K3 on RSR / relocation boundaries) for step it."""
         eng = opt.engine
-        # K1 + K2 through the optimizer, K2 bracketed by events
         rows, count = eng.compact(masks[it])
-        if timed:
-            e0.record()
-        _step_k2(opt, g, rows, count, wl)
-        if timed:
-            e1.record()
-            k2_events.append((e0, e1))
+        _step_k2(opt, grad_sets[it % 2], rows, count, wl)
         ev = events.get(it)
         if ev:
             if "rsr" in ev:
@@ -346,23 +339,42 @@ def ours(args, wl, p_vis):
             dist.all_reduce(stats_sum)
 
     for it in range(args.warmup):
-        one_step(it, False)
+        one_step(it)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    timed_steps = range(args.warmup, total_steps)
+    # CUDA graph: the K timed steps are captured once and replayed as one
+    # launch, so host launch latency never shows up in device time (the
+    # small clouds are otherwise host-bound).  Multi-rank runs stay eager
+    # (the per-step NCCL all-reduce is issued from the host).
+    use_graph = args.graph and world == 1
     launches0 = opt.engine.launches
+    graph = None
+    if use_graph:
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            for it in timed_steps:
+                one_step(it)
+    launches[0] = opt.engine.launches - launches0
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
         start.record()
-        for it in range(args.warmup, total_steps):
-            one_step(it, True)
+        if graph is not None:
+            graph.replay()
+        else:
+            for it in timed_steps:
+                one_step(it)
         end.record()
         torch.cuda.synchronize()
     ms = start.elapsed_time(end)
-    launches[0] = opt.engine.launches - launches0
-    k2_ms = [a.elapsed_time(b) for a, b in k2_events]
-    opt.check_errors()
+    if graph is None:
+        launches[0] = opt.engine.launches - launches0
+    del graph
+    st = opt.last_stats()  # the last timed step's statistics (host read, after timing)
+    if st["n_bad_grad"] or st["n_bad_domain"] or st["n_stepped"] != st["n_visible"]:
+        raise RuntimeError(f"step statistics report skipped rows: {st}")
     ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
     vis_t = torch.tensor([float(n_vis[args.warmup:].sum())], dtype=torch.float64, device=dev)
     if world > 1:
@@ -371,6 +383,36 @@ def ours(args, wl, p_vis):
     ms_max = float(ms_t.item())
     total_visible = float(vis_t.item())
     value = total_visible / (ms_max / 1000.0)
+
+    # K2 alone, for the roofline: the timed steps' index lists are compacted
+    # up front, then K2 is launched K times back to back (as a graph on one
+    # rank) between two CUDA events on the launching stream
+    idx_lists = []
+    for it in timed_steps:
+        rows, count = opt.engine.compact(masks[it])
+        idx_lists.append((rows.clone(), count.clone()))
+
+    def k2_only():
+        for j, it in enumerate(timed_steps):
+            _step_k2(opt, grad_sets[it % 2], idx_lists[j][0], idx_lists[j][1], wl)
+
+    k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if use_graph:
+        g2 = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g2):
+            k2_only()
+        torch.cuda.synchronize()
+        k0.record()
+        g2.replay()
+        k1.record()
+    else:
+        torch.cuda.synchronize()
+        k0.record()
+        k2_only()
+        k1.record()
+    torch.cuda.synchronize()
+    k2_ms = [k0.elapsed_time(k1) / len(idx_lists)]
+    del idx_lists
 
     # roofline of K2 (this rank's launches)
     width = S.SH3_WIDTH
@@ -423,7 +465,8 @@ def ours(args, wl, p_vis):
 
 def _step_k2(opt, grads, rows, count, wl):
     """The optimizer's K2 launch for an already-compacted index list
-    (AdamWGS.step does K1 + K2; the bench splits them to time K2 alone)."""
+    (AdamWGS.step does K1 + K2; the bench splits them to time K2 alone).
+    Graph-capturable: no host synchronisation, no error readback."""
     b = opt._bindings(grads)
     eng = opt.engine
     from paper_2601_16736_b200.engine import round_pixel_count
@@ -437,7 +480,6 @@ def _step_k2(opt, grads, rows, count, wl):
                  lambda_opacity=wl["lo"], lambda_scale=wl["ls"], n_visible_dev=count,
                  check=opt.check, record=opt.state.record)
     opt._last_ctx = (b, rows, count, wl["lo"], wl["ls"], wl["mode"])
-    opt._after_step(eng.stats)
 
 
 def run_e2e(args, opt, cfg, dev, world, masks, n_vis):

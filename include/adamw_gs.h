@@ -174,6 +174,12 @@ size_t gs_step_rows_workspace_bytes(void);
  * (0 = default; tuning only, results are identical).  Returns the previous
  * variant.  The GS_ROWS_VARIANT environment variable sets the initial one. */
 int32_t gs_set_rows_variant(int32_t variant);
+/* Select the variant of the compile-time-layout (3DGS SH-3) step kernel that
+ * gs_step_rows dispatches to for that layout: 0 = default, > 0 tuning
+ * variants (identical results), -1 = disable the fixed-layout path (the
+ * generic row kernel runs).  Returns the previous value.  GS_FIXED_VARIANT
+ * sets the initial one. */
+int32_t gs_set_fixed_variant(int32_t variant);
 int gs_step_rows(const gs_group* groups, int32_t n_groups, const gs_step_cfg* cfg,
                  const int32_t* rows, const int32_t* n_rows_dev, int64_t max_rows,
                  float* record, int64_t record_stride, double* stats_out, void* ws,

@@ -1053,10 +1053,13 @@ void launch_ws(const FixedParams& P, int64_t max_rows, cudaStream_t s) {
 
 static int g_fixed_variant = -1;
 
+static bool g_fixed_variant_set = false;
+
 int fixed_variant() {
-  if (g_fixed_variant < 0) {
+  if (!g_fixed_variant_set) {
     const char* e = getenv("GS_FIXED_VARIANT");
     g_fixed_variant = e ? atoi(e) : 0;
+    g_fixed_variant_set = true;
   }
   return g_fixed_variant;
 }
@@ -1106,6 +1109,12 @@ bool layout_matches(const gs_group* groups, int n_groups) {
 
 }  // namespace gs
 
+extern "C" int32_t gs_set_fixed_variant(int32_t variant) {
+  const int32_t prev = gs::fixed_variant();
+  gs::g_fixed_variant = variant;
+  return prev;
+}
+
 // Called by gs_step_rows (gs_step_rows.cu) after argument validation; returns
 // 1 if a compiled fixed layout handled the launch, 0 otherwise.
 int gs_step_fixed_try(const gs_group* groups, int32_t n_groups, const gs_step_cfg* cfg,
@@ -1113,8 +1122,7 @@ int gs_step_fixed_try(const gs_group* groups, int32_t n_groups, const gs_step_cf
                       float* record, int64_t record_stride, double* stats_out, double* partials,
                       unsigned int* counter, void* stream) {
   using namespace gs;
-  const char* off = getenv("GS_DISABLE_FIXED");
-  if (off && off[0] == '1') return 0;
+  if (fixed_variant() < 0) return 0;  // fixed-layout path disabled
   if (!layout_matches<LayoutSH3>(groups, n_groups)) return 0;
   if (max_rows * 45 >= (int64_t)UINT32_MAX) return 0;  // 32-bit element offsets
   FixedParams P{};

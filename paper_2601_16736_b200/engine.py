@@ -219,7 +219,7 @@ class StepEngine:
             raise ConfigError(f"visibility dtype {vis.dtype} not supported (bool/uint8 mask or "
                               "int32 radii)")
         L.check(rc, "gs_compact")
-        self.launches += 1
+        self.launches += 2 if self.n_rows > 0 else 0  # count + write passes
         return self.idx, self.count
 
     # ------------------------------------------------------------------ step

@@ -466,8 +466,12 @@ def test_optimizer_error_semantics(check):
         assert st["n_bad_grad"] == 1 and st["n_stepped"] == int(vis.sum()) - 1
 
 
-def test_rows_kernel_variants_identical():
-    """Every tuning variant of the SH-3 row kernel gives the same bits."""
+@pytest.mark.parametrize("mode", ["adamw-gs", "sparse-adam", "adamw-const-clip",
+                                  "coupled-adam"])
+def test_step_kernels_all_identical(mode):
+    """Every K2 implementation and tuning variant gives the same bits: the
+    fixed-layout SH-3 kernels (variants 0..6), the generic row-record kernel
+    (variants 0..6) and the per-group-state kernel."""
     from paper_2601_16736_b200 import _lib
     from paper_2601_16736_b200 import synthetic as S
     from paper_2601_16736_b200.optimizer import AdamWGS
@@ -475,25 +479,39 @@ def test_rows_kernel_variants_identical():
     cfg = S.WorkloadConfig(n=20_011, p_vis=0.4, seed=9)
     host = S.make_params(cfg)
     results = []
-    prev = lib.gs_set_rows_variant(0)
+    runs = [("fixed", v) for v in range(7)] + [("rows", v) for v in range(7)] + [("groups", 0)]
+    prev_f = lib.gs_set_fixed_variant(0)
+    prev_r = lib.gs_set_rows_variant(0)
     try:
-        for variant in range(7):
-            lib.gs_set_rows_variant(variant)
+        for kind, variant in runs:
+            lib.gs_set_fixed_variant(variant if kind == "fixed" else -1)
+            lib.gs_set_rows_variant(variant if kind == "rows" else 0)
             params = {k: torch.from_numpy(v).to(DEV) for k, v in host.items()}
-            opt = AdamWGS(S.param_groups(params), mode="adamw-gs", lambda_o=1e-3, lambda_s=1e-5)
+            layout = "groups" if kind == "groups" else "rows"
+            opt = AdamWGS(S.param_groups(params), mode=mode, lambda_o=1e-3, lambda_s=1e-5,
+                          state_layout=layout)
             for s in range(3):
                 vis = S.visibility(cfg, s)
                 g = {k: torch.from_numpy(x).to(DEV) for k, x in S.step_grads(cfg, s, vis).items()}
                 opt.step(torch.from_numpy(vis).to(DEV), cfg.n_pixels, grads=g)
             results.append(({k: p.cpu().numpy() for k, p in params.items()},
-                            opt.state.record.cpu().numpy(), opt.last_stats()))
+                            {k: t.contiguous().cpu().numpy() for k, t in opt.state.m.items()},
+                            {k: t.contiguous().cpu().numpy() for k, t in opt.state.v.items()},
+                            opt.state.clock.contiguous().cpu().numpy(), opt.last_stats()))
     finally:
-        lib.gs_set_rows_variant(prev)
-    for p, rec, st in results[1:]:
-        assert np.array_equal(rec, results[0][1])
-        for k in p:
-            assert np.array_equal(p[k], results[0][0][k])
-        assert st == results[0][2]
+        lib.gs_set_fixed_variant(prev_f)
+        lib.gs_set_rows_variant(prev_r)
+    ref = results[0]
+    for (kind, variant), res in zip(runs[1:], results[1:]):
+        for i in range(3):
+            for k in ref[i]:
+                assert np.array_equal(res[i][k], ref[i][k]), (kind, variant, i, k)
+        assert np.array_equal(res[3], ref[3]), (kind, variant)
+        for f, x in ref[4].items():
+            if f.startswith("sum_"):
+                assert res[4][f] == pytest.approx(x, rel=1e-12), (kind, variant, f)
+            else:
+                assert res[4][f] == x, (kind, variant, f)
 
 
 def test_state_views_and_checkpoint_roundtrip():
