@@ -543,6 +543,11 @@ __global__ void __launch_bounds__(kFixedThreads, MINB) step_pipe2_kernel(const F
   constexpr int SLOTS = L::P + 1;
   using SH = ChunkShape<L, R, NT>;
   using ST = PipeStage<L, R>;
+  static_assert(NT % 32 == 0 && (R * 1) % 32 == 0, "warp-uniform group boundaries");
+  // Each group's elements start at thread (R * OFF_g) mod NT instead of 0, so
+  // the small groups land on different warps and every warp gets the same
+  // number of 32-element pieces per chunk (balanced barriers).
+  auto rot_of = [](int gg) { return (R * L::OFF(gg)) & (NT - 1); };
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ int s_bad[2][R];
   __shared__ float2 s_bc[2][R];
@@ -597,7 +602,7 @@ __global__ void __launch_bounds__(kFixedThreads, MINB) step_pipe2_kernel(const F
       const int W = L::W(gg);
 #pragma unroll
       for (int k = 0; k < SH::rounds(gg); ++k) {
-        const int i = k * NT + t;
+        const int i = k * NT + ((t - rot_of(gg)) & (NT - 1));
         const int r = i / W;
         if (i < R * W && r < nv) {
           const uint32_t off = rows[r] * (uint32_t)W + (uint32_t)(i - r * W);
@@ -651,7 +656,7 @@ __global__ void __launch_bounds__(kFixedThreads, MINB) step_pipe2_kernel(const F
         const float lam = role == GS_ROLE_OPACITY ? K.lam_op : role == GS_ROLE_SCALE ? K.lam_sc : 0.f;
 #pragma unroll
         for (int kk = 0; kk < SH::rounds(gg); ++kk) {
-          const int i = kk * NT + t;
+          const int i = kk * NT + ((t - rot_of(gg)) & (NT - 1));
           const int r = i / W;
           if (i < R * W && r < nvalid) {
             const int e = R * L::OFF(gg) + i;
@@ -692,40 +697,53 @@ __global__ void __launch_bounds__(kFixedThreads, MINB) step_pipe2_kernel(const F
     if (t < R) s_bad[b ^ 1][t] = t < chunk_rows(k + 1) ? 0 : 4;
     if (t == 0) s_any[b ^ 1] = chunk_rows(k + 1) < R;
     __syncthreads();  // #3: bias factors visible
-    // G. update: theta and (m, v) straight to global
-#pragma unroll
-    for (int gg = 0; gg < L::G; ++gg) {
+    // G. update: theta and (m, v) straight to global.  The common case (a
+    //    full chunk without bad rows) runs without any per-element predicate
+    //    on the full rounds; otherwise every element checks its row.
+    auto update = [&](int gg, int i, int r) {
       const int W = L::W(gg);
       const int role = L::ROLE(gg);
-      float* const par = P.g[gg].param;
-      const float lr = P.g[gg].lr;
+      const int c = i - r * W;
+      const int e = R * L::OFF(gg) + i;
+      const uint32_t row = srow[r];
+      const float2 mv = srec[r * SLOTS + L::OFF(gg) + c];
+      const float th = sth[e];
+      float tnv, mn, vn, ex;
+      bool clipped;
+      update_element<MODE>(role, P.g[gg].lr, th, sg[e], mv.x, mv.y, s_bc[b][r], K, tnv, mn, vn,
+                           ex, clipped);
+      if (!kCoupled && role == GS_ROLE_OPACITY) {
+        c_clo += clipped;
+        s_exo += (double)ex;
+      } else if (!kCoupled && role == GS_ROLE_SCALE) {
+        c_cls += clipped;
+        s_exs += (double)ex;
+      }
+      if (role == GS_ROLE_OPACITY) {
+        c_apre += th > P.active_logit;
+        c_apost += tnv > P.active_logit;
+      }
+      P.g[gg].param[row * (uint32_t)W + (uint32_t)c] = tnv;
+      rec_base[(size_t)row * rec_stride2 + L::OFF(gg) + c] = make_float2(mn, vn);
+    };
+    if (!any_bad) {
 #pragma unroll
-      for (int kk = 0; kk < SH::rounds(gg); ++kk) {
-        const int i = kk * NT + t;
-        const int r = i / W;
-        if (i < R * W && (!any_bad || (r < nvalid && s_bad[b][r] == 0))) {
-          const int c = i - r * W;
-          const int e = R * L::OFF(gg) + i;
-          const uint32_t row = srow[r];
-          const float2 mv = srec[r * SLOTS + L::OFF(gg) + c];
-          const float th = sth[e];
-          float tnv, mn, vn, ex;
-          bool clipped;
-          update_element<MODE>(role, lr, th, sg[e], mv.x, mv.y, s_bc[b][r], K, tnv, mn, vn, ex,
-                               clipped);
-          if (!kCoupled && role == GS_ROLE_OPACITY) {
-            c_clo += clipped;
-            s_exo += (double)ex;
-          } else if (!kCoupled && role == GS_ROLE_SCALE) {
-            c_cls += clipped;
-            s_exs += (double)ex;
-          }
-          if (role == GS_ROLE_OPACITY) {
-            c_apre += th > P.active_logit;
-            c_apost += tnv > P.active_logit;
-          }
-          par[row * (uint32_t)W + (uint32_t)c] = tnv;
-          rec_base[(size_t)row * rec_stride2 + L::OFF(gg) + c] = make_float2(mn, vn);
+      for (int gg = 0; gg < L::G; ++gg) {
+#pragma unroll
+        for (int kk = 0; kk < SH::rounds(gg); ++kk) {
+          const int i = kk * NT + ((t - rot_of(gg)) & (NT - 1));
+          const bool full = (kk + 1) * NT <= R * L::W(gg);  // compile-time
+          if (full || i < R * L::W(gg)) update(gg, i, i / L::W(gg));
+        }
+      }
+    } else {
+#pragma unroll
+      for (int gg = 0; gg < L::G; ++gg) {
+#pragma unroll
+        for (int kk = 0; kk < SH::rounds(gg); ++kk) {
+          const int i = kk * NT + ((t - rot_of(gg)) & (NT - 1));
+          const int r = i / L::W(gg);
+          if (i < R * L::W(gg) && r < nvalid && s_bad[b][r] == 0) update(gg, i, r);
         }
       }
     }
