@@ -446,7 +446,7 @@ def ours(args, wl, p_vis):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak,
                          "traffic": traffic_from_profiles(args.workload, args.mask, p_vis),
-                         "kernel": "gs::step_pipe2_kernel<LayoutSH3> (K2, via gs_step_rows)"
+                         "kernel": "gs::step_ws_kernel<LayoutSH3> (K2, warp-specialised, via gs_step_rows)"
                                    if args.layout == "rows" else "gs::step_kernel (K2, gs_step)",
                          "peak_source": peak_src,
                          "k2_ms_avg": k2_avg_ms,

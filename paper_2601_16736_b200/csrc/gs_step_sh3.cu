@@ -908,7 +908,7 @@ __global__ void __launch_bounds__((NPW + NCW) * 32, MINB) step_ws_kernel(const F
         const int W = L::W(gg);
 #pragma unroll
         for (int kk = 0; kk < PS::rounds(gg); ++kk) {
-          const int i = kk * NP + pt;
+          const int i = kk * NP + ((pt + NP - (R * L::OFF(gg)) % NP) % NP);
           const int r = i / W;
           if (i < R * W && r < nv) {
             const uint32_t off = srows[r] * (uint32_t)W + (uint32_t)(i - r * W);
@@ -955,7 +955,7 @@ __global__ void __launch_bounds__((NPW + NCW) * 32, MINB) step_ws_kernel(const F
           const float lam = role == GS_ROLE_OPACITY ? K.lam_op : role == GS_ROLE_SCALE ? K.lam_sc : 0.f;
 #pragma unroll
           for (int kk = 0; kk < SH::rounds(gg); ++kk) {
-            const int i = kk * NC + t;
+            const int i = kk * NC + ((t + NC - (R * L::OFF(gg)) % NC) % NC);
             const int r = i / W;
             if (i < R * W && r < nvalid) {
               const int e = R * L::OFF(gg) + i;
@@ -993,39 +993,50 @@ __global__ void __launch_bounds__((NPW + NCW) * 32, MINB) step_ws_kernel(const F
         }
       }
       named_sync(1, NC);  // bias factors visible
-#pragma unroll
-      for (int gg = 0; gg < L::G; ++gg) {
+      auto update = [&](int gg, int i, int r) {
         const int W = L::W(gg);
         const int role = L::ROLE(gg);
-        float* const par = P.g[gg].param;
-        const float lr = P.g[gg].lr;
+        const int c = i - r * W;
+        const int e = R * L::OFF(gg) + i;
+        const uint32_t row = srow[r];
+        const float2 mv = srec[r * SLOTS + L::OFF(gg) + c];
+        const float th = sth[e];
+        float tnv, mn, vn, ex;
+        bool clipped;
+        update_element<MODE>(role, P.g[gg].lr, th, sg[e], mv.x, mv.y, s_bc[st][r], K, tnv, mn,
+                             vn, ex, clipped);
+        if (!kCoupled && role == GS_ROLE_OPACITY) {
+          c_clo += clipped;
+          s_exo += (double)ex;
+        } else if (!kCoupled && role == GS_ROLE_SCALE) {
+          c_cls += clipped;
+          s_exs += (double)ex;
+        }
+        if (role == GS_ROLE_OPACITY) {
+          c_apre += th > P.active_logit;
+          c_apost += tnv > P.active_logit;
+        }
+        P.g[gg].param[row * (uint32_t)W + (uint32_t)c] = tnv;
+        rec_base[(size_t)row * rec_stride2 + L::OFF(gg) + c] = make_float2(mn, vn);
+      };
+      if (!any_bad) {
 #pragma unroll
-        for (int kk = 0; kk < SH::rounds(gg); ++kk) {
-          const int i = kk * NC + t;
-          const int r = i / W;
-          if (i < R * W && (!any_bad || (r < nvalid && s_bad[st][r] == 0))) {
-            const int c = i - r * W;
-            const int e = R * L::OFF(gg) + i;
-            const uint32_t row = srow[r];
-            const float2 mv = srec[r * SLOTS + L::OFF(gg) + c];
-            const float th = sth[e];
-            float tnv, mn, vn, ex;
-            bool clipped;
-            update_element<MODE>(role, lr, th, sg[e], mv.x, mv.y, s_bc[st][r], K, tnv, mn, vn,
-                                 ex, clipped);
-            if (!kCoupled && role == GS_ROLE_OPACITY) {
-              c_clo += clipped;
-              s_exo += (double)ex;
-            } else if (!kCoupled && role == GS_ROLE_SCALE) {
-              c_cls += clipped;
-              s_exs += (double)ex;
-            }
-            if (role == GS_ROLE_OPACITY) {
-              c_apre += th > P.active_logit;
-              c_apost += tnv > P.active_logit;
-            }
-            par[row * (uint32_t)W + (uint32_t)c] = tnv;
-            rec_base[(size_t)row * rec_stride2 + L::OFF(gg) + c] = make_float2(mn, vn);
+        for (int gg = 0; gg < L::G; ++gg) {
+#pragma unroll
+          for (int kk = 0; kk < SH::rounds(gg); ++kk) {
+            const int i = kk * NC + ((t + NC - (R * L::OFF(gg)) % NC) % NC);
+            const bool full = (kk + 1) * NC <= R * L::W(gg);  // compile-time
+            if (full || i < R * L::W(gg)) update(gg, i, i / L::W(gg));
+          }
+        }
+      } else {
+#pragma unroll
+        for (int gg = 0; gg < L::G; ++gg) {
+#pragma unroll
+          for (int kk = 0; kk < SH::rounds(gg); ++kk) {
+            const int i = kk * NC + ((t + NC - (R * L::OFF(gg)) % NC) % NC);
+            const int r = i / L::W(gg);
+            if (i < R * L::W(gg) && r < nvalid && s_bad[st][r] == 0) update(gg, i, r);
           }
         }
       }
@@ -1095,11 +1106,11 @@ void launch_fixed(const FixedParams& P, int64_t max_rows, cudaStream_t s) {
   switch (fixed_variant()) {
     case 1: launch_fixed_v<L, MODE, STRICT, 64, 2>(P, max_rows, s); return;
     case 2: launch_pipe<L, MODE, STRICT, 32, 2, 3>(P, max_rows, s); return;
-    case 3: launch_pipe2<L, MODE, STRICT, 32, 3, 2>(P, max_rows, s); return;
+    case 3: launch_pipe2<L, MODE, STRICT, 32, 2, 3>(P, max_rows, s); return;
     case 4: launch_ws<L, MODE, STRICT, 32, 3, 2, 8, 2>(P, max_rows, s); return;
-    case 5: launch_ws<L, MODE, STRICT, 32, 4, 2, 8, 1>(P, max_rows, s); return;
-    case 6: launch_ws<L, MODE, STRICT, 32, 3, 1, 8, 2>(P, max_rows, s); return;
-    default: launch_pipe2<L, MODE, STRICT, 32, 2, 3>(P, max_rows, s); return;
+    case 5: launch_pipe2<L, MODE, STRICT, 32, 3, 2>(P, max_rows, s); return;
+    case 6: launch_ws<L, MODE, STRICT, 32, 3, 2, 6, 2>(P, max_rows, s); return;
+    default: launch_ws<L, MODE, STRICT, 32, 3, 3, 8, 2>(P, max_rows, s); return;
   }
 }
 
