@@ -108,6 +108,13 @@ typedef struct gs_step_cfg {
   const int32_t* n_visible_norm; /* device N_v for the coupled modes (may be NULL) */
   double n_visible_host;         /* used when n_visible_norm == NULL */
   const int32_t* abort_flag;    /* strict mode: device flag written by gs_check_grads */
+  /* fused densification statistics (DensifyStats.observe, pipeline.py:67-91):
+   * for every stepped row, accum[row] += ||grad[group densify_group][row]||_2
+   * * densify_scale and count[row] += 1.  densify_group < 0 disables. */
+  float* densify_accum;
+  int32_t* densify_count;
+  float densify_scale;
+  int32_t densify_group;
 } gs_step_cfg;
 
 int32_t gs_abi_version(void);
@@ -124,6 +131,13 @@ int gs_compact_u8(const uint8_t* mask, int64_t n, int32_t* idx_out, int32_t* cou
                   void* ws, size_t ws_bytes, void* stream);
 int gs_compact_i32(const int32_t* radii, int64_t n, int32_t* idx_out, int32_t* count_out,
                    void* ws, size_t ws_bytes, void* stream);
+/* Generalised selection: rows with mask != 0 (invert = 0) or mask == 0
+ * (invert != 0), restricted to alive[row] != 0 when alive is not NULL — e.g.
+ * the invisible alive rows of aiu_apply, np.flatnonzero(alive & ~vis)
+ * (optimizer.py:437). */
+int gs_compact_select_u8(const uint8_t* mask, const uint8_t* alive, int32_t invert, int64_t n,
+                         int32_t* idx_out, int32_t* count_out, void* ws, size_t ws_bytes,
+                         void* stream);
 
 /* K2 — the fused step over the rows listed in rows[0 .. *n_rows_dev) (or all
  * max_rows rows in coupled-adam mode, rows == NULL).  clock: int32 per row.
@@ -169,6 +183,30 @@ int gs_stats_all(const gs_group* groups, int32_t n_groups, int64_t n_rows,
  * these entry points; param / grad / width / role / lr are used.  One
  * contiguous record per visible row replaces 2*n_groups narrow scattered
  * spans plus the clock (see paper_2601_16736_b200/csrc/gs_step_rows.cu). */
+/* AIU — artificial implicit updates (optimizer.py:425-450): picked row i is
+ * inv_idx[jlist[i]] for i < *k_dev (<= max_k); each picked row with clock > 0
+ * steps theta -= (lr_eta * m^) / (sqrt(v^) + eps) with its frozen record
+ * state; m, v, clock untouched.  groups[g].lr carries fl32(lr_g * eta).
+ * picked_out (nullable) receives the picked rows in order. */
+int gs_aiu_apply_rows(const gs_group* groups, int32_t n_groups, float* record,
+                      int64_t record_stride, const int32_t* inv_idx, const int32_t* jlist,
+                      const int32_t* k_dev, int64_t max_k, const float* bias_lut,
+                      int32_t lut_len, float eps, int32_t* picked_out, void* stream);
+
+/* Opacity-gated position noise (optimizer.py:453-486): for every alive row,
+ * delta = -eta_ratio * lr_position * sigmoid(-lambda_mu (sigmoid(tau) -
+ * lambda_t)) * Sigma gamma, Sigma = R diag(exp(2 log_scale)) R^T, gamma from a
+ * Philox4x32-10 stream keyed by seed, counted by (row, iteration).  dims 2:
+ * position [n,2], log_scale [n,2], rotation = angle [n]; dims 3 (3DGS):
+ * position [n,3], log_scale [n,3], rotation = quaternion (w,x,y,z) [n,4].
+ * delta_out (nullable, [n,dims]) receives delta; add_in_place adds it to
+ * position.  Statistical parity with the reference (host RNG not reproduced). */
+int gs_noise_perturb(float* position, const float* log_scale, const float* rotation,
+                     const float* opacity_logit, const uint8_t* alive, int64_t n, int32_t dims,
+                     float lr_position, float eta_ratio, float lambda_mu, float lambda_t,
+                     uint64_t seed, uint32_t iteration, float* delta_out, int32_t add_in_place,
+                     void* stream);
+
 size_t gs_step_rows_workspace_bytes(void);
 /* Select the (rows-in-flight, residency) variant of the SH-3 step kernel
  * (0 = default; tuning only, results are identical).  Returns the previous

@@ -586,3 +586,57 @@ def step_fp32(mode, layout, params, grads, m, v, clock, rows, hp, *, n_pixels=No
         m[g.name][r] = m_new
         v[g.name][r] = v_new
     return stats
+
+
+def densify_observe_fp32(grad_pos, rows, accum, count, scale):
+    """DensifyStats.observe (pipeline.py:77-82) in the kernels' fp32 order:
+    accum[r] += sqrt(sum_c g_c^2) * scale (sequential fp32 sum), count[r] += 1."""
+    g = np.asarray(grad_pos, F32)[rows]
+    s2 = np.zeros(g.shape[0], F32)
+    for c in range(g.shape[1]):
+        s2 = s2 + g[:, c] * g[:, c]
+    accum[rows] = accum[rows] + np.sqrt(s2) * F32(scale)
+    count[rows] += 1
+
+
+def densify_observe_f64(grad_pos, vis, accum, count, view_scale):
+    """pipeline.py:77-82 restated (float64): the reference's DensifyStats.observe."""
+    rows = np.flatnonzero(vis)
+    if rows.size:
+        norms = np.linalg.norm(np.asarray(grad_pos, F64)[rows], axis=1) * view_scale
+        accum[rows] += norms
+        count[rows] += 1
+
+
+def aiu_apply_f64(layout, params, m, v, t, vis, alive, lr, beta1, beta2, eps, prob, eta, rng):
+    """optimizer.py:425-450 restated: extra steps on sampled invisible rows with
+    frozen moments and clocks; returns the picked rows (int64)."""
+    invisible = np.flatnonzero(np.asarray(alive, bool) & ~np.asarray(vis, bool))
+    if invisible.size == 0 or prob <= 0.0 or eta == 0.0:
+        return np.empty(0, dtype=np.int64)
+    picked = invisible[rng.random(invisible.size) < prob]
+    if picked.size == 0:
+        return picked
+    for g in layout:
+        started = picked[t[picked] > 0]
+        if started.size == 0:
+            continue
+        mh, vh = _corrected_f64(m[g.name][started], v[g.name][started], t[started], beta1, beta2)
+        params[g.name][started] = params[g.name][started] - lr[g.name] * eta * mh / (
+            np.sqrt(vh) + eps)
+    return picked
+
+
+def aiu_apply_fp32(layout, params, m, v, t, picked, lr, eta, eps, lut):
+    """The AIU kernel's fp32 order (gs_state.cu::aiu_rows_kernel):
+    theta -= (fl32(lr*eta) * m^) / (sqrt(v^) + eps), rows with clock 0 skipped."""
+    rows = np.asarray(picked, np.int64)
+    rows = rows[t[rows] > 0]
+    tb = np.minimum(t[rows], lut.shape[0] - 1)
+    c1 = lut[tb, 0][:, None]
+    c2 = lut[tb, 1][:, None]
+    for g in layout:
+        mh = m[g.name][rows] * c1
+        vh = v[g.name][rows] * c2
+        den = np.sqrt(vh) + F32(eps)
+        params[g.name][rows] = params[g.name][rows] - (F32(lr[g.name] * eta) * mh) / den

@@ -17,7 +17,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libadamw_gs_b200.so"
-SOURCES = ("gs_abi.cu", "gs_compact.cu", "gs_step.cu", "gs_step_rows.cu", "gs_step_sh3.cu", "gs_state.cu")
+SOURCES = ("gs_abi.cu", "gs_compact.cu", "gs_step.cu", "gs_step_rows.cu", "gs_step_sh3.cu", "gs_state.cu", "gs_noise.cu")
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -48,7 +48,9 @@ class GsStepCfg(C.Structure):
                 ("n_pixels_rounded", C.c_double), ("bias_lut", C.c_void_p),
                 ("lut_len", C.c_int32), ("global_t", C.c_int32), ("beta1", C.c_double),
                 ("beta2", C.c_double), ("n_visible_norm", C.c_void_p),
-                ("n_visible_host", C.c_double), ("abort_flag", C.c_void_p)]
+                ("n_visible_host", C.c_double), ("abort_flag", C.c_void_p),
+                ("densify_accum", C.c_void_p), ("densify_count", C.c_void_p),
+                ("densify_scale", C.c_float), ("densify_group", C.c_int32)]
 
 
 # name -> (restype, argtypes); exactly the symbols declared in include/adamw_gs.h
@@ -73,6 +75,15 @@ SIGNATURES = {
     "gs_reset_rows": (C.c_int, [C.POINTER(GsGroup), C.c_int32, C.c_void_p, C.c_void_p,
                                 C.c_int64, C.c_void_p]),
     "gs_stats_workspace_bytes": (C.c_size_t, [C.c_int32]),
+    "gs_compact_select_u8": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int64, C.c_void_p,
+                                       C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
+    "gs_aiu_apply_rows": (C.c_int, [C.POINTER(GsGroup), C.c_int32, C.c_void_p, C.c_int64,
+                                    C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
+                                    C.c_int32, C.c_float, C.c_void_p, C.c_void_p]),
+    "gs_noise_perturb": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                   C.c_int64, C.c_int32, C.c_float, C.c_float, C.c_float,
+                                   C.c_float, C.c_uint64, C.c_uint32, C.c_void_p, C.c_int32,
+                                   C.c_void_p]),
     "gs_step_rows_workspace_bytes": (C.c_size_t, []),
     "gs_set_rows_variant": (C.c_int32, [C.c_int32]),
     "gs_set_fixed_variant": (C.c_int32, [C.c_int32]),

@@ -200,6 +200,25 @@ __device__ __forceinline__ bool last_block_arrive(unsigned int* counter) {
   return s_last;
 }
 
+// Densification statistics of one row from its position-group gradient
+// (pipeline.py:77-82): accum += sqrt(sum_c g_c^2) * scale, count += 1, in a
+// fixed fp32 order (oracle: densify_observe_fp32).
+struct DensifyArgs {
+  float* accum;
+  int32_t* count;
+  float scale;
+  int group;  // < 0: off
+};
+
+__device__ __forceinline__ void densify_row(const DensifyArgs& D, uint32_t row, const float* g,
+                                            int w, int stride) {
+  float s2 = 0.0f;
+  for (int c = 0; c < w; ++c) s2 = __fadd_rn(s2, __fmul_rn(g[c * stride], g[c * stride]));
+  const float v = __fmul_rn(__fsqrt_rn(s2), D.scale);
+  D.accum[row] = __fadd_rn(D.accum[row], v);
+  D.count[row] += 1;
+}
+
 // Host: fp32 constants of a step from the C-ABI configuration (every value
 // rounded once from float64, as the oracle does).
 inline StepConsts make_consts(const gs_step_cfg* cfg) {

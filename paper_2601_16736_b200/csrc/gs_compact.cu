@@ -72,6 +72,23 @@ __device__ __forceinline__ uint32_t load_bits<int32_t>(const int32_t* __restrict
   return bits;
 }
 
+// Selection bits of the thread's rows: the mask bits, or their complement
+// (invisible rows), restricted to alive rows when an alive mask is given.
+template <typename T>
+__device__ __forceinline__ uint32_t select_bits(const T* __restrict__ mask,
+                                                const uint8_t* __restrict__ alive, bool invert,
+                                                int64_t row0, int64_t n, bool vec_ok) {
+  uint32_t bits = load_bits<T>(mask, row0, n, vec_ok);
+  if (invert || alive) {
+    const int64_t left = n - row0;
+    const uint32_t in_range =
+        left >= kCompactItems ? 0xffffu : (left <= 0 ? 0u : ((1u << left) - 1u));
+    if (invert) bits = ~bits & in_range;
+    if (alive) bits &= load_bits<uint8_t>(alive, row0, n, vec_ok);
+  }
+  return bits;
+}
+
 __device__ __forceinline__ int block_exclusive_scan(int cnt, int* s_warp, int* total) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int incl = cnt;
@@ -99,11 +116,11 @@ __device__ __forceinline__ int block_exclusive_scan(int cnt, int* s_warp, int* t
 
 template <typename T>
 __global__ void __launch_bounds__(kThreads)
-    compact_count_kernel(const T* __restrict__ mask, int64_t n, int32_t* __restrict__ counts,
-                         bool vec_ok) {
+    compact_count_kernel(const T* __restrict__ mask, const uint8_t* __restrict__ alive,
+                         bool invert, int64_t n, int32_t* __restrict__ counts, bool vec_ok) {
   __shared__ int s_sum[kThreads / 32];
   const int64_t row0 = (int64_t)blockIdx.x * kCompactTile + (int64_t)threadIdx.x * kCompactItems;
-  int c = __popc(load_bits<T>(mask, row0, n, vec_ok));
+  int c = __popc(select_bits<T>(mask, alive, invert, row0, n, vec_ok));
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
   if ((threadIdx.x & 31) == 0) s_sum[threadIdx.x >> 5] = c;
@@ -118,7 +135,8 @@ __global__ void __launch_bounds__(kThreads)
 
 template <typename T>
 __global__ void __launch_bounds__(kThreads)
-    compact_write_kernel(const T* __restrict__ mask, int64_t n,
+    compact_write_kernel(const T* __restrict__ mask, const uint8_t* __restrict__ alive,
+                         bool invert, int64_t n,
                          const int32_t* __restrict__ counts, int32_t* __restrict__ idx_out,
                          int32_t* __restrict__ count_out, bool vec_ok) {
   __shared__ int32_t s_out[kCompactTile];
@@ -134,7 +152,7 @@ __global__ void __launch_bounds__(kThreads)
   for (int o = 16; o > 0; o >>= 1) pre += __shfl_xor_sync(0xffffffffu, pre, o);
   if ((tid & 31) == 0) s_red[tid >> 5] = pre;
   const int64_t row0 = tile * kCompactTile + (int64_t)tid * kCompactItems;
-  const uint32_t bits = load_bits<T>(mask, row0, n, vec_ok);
+  const uint32_t bits = select_bits<T>(mask, alive, invert, row0, n, vec_ok);
   const int local_off = block_exclusive_scan(__popc(bits), s_warp, &s_total);
   long long excl = 0;
 #pragma unroll
@@ -156,7 +174,8 @@ __global__ void __launch_bounds__(kThreads)
 
 template <typename T>
 int compact_launch(const T* mask, int64_t n, int32_t* idx_out, int32_t* count_out, void* ws,
-                   size_t ws_bytes, void* stream) {
+                   size_t ws_bytes, void* stream, const uint8_t* alive = nullptr,
+                   bool invert = false) {
   if (n < 0 || (n > 0 && (!mask || !idx_out)) || !count_out || n >= (int64_t)INT32_MAX) {
     gs_set_error("gs_compact: invalid arguments (n=%lld)", (long long)n);
     return GS_ERR_ARG;
@@ -174,10 +193,12 @@ int compact_launch(const T* mask, int64_t n, int32_t* idx_out, int32_t* count_ou
   }
   const int64_t tiles = (n + kCompactTile - 1) / kCompactTile;
   auto* counts = reinterpret_cast<int32_t*>(ws);
-  const bool vec_ok = (reinterpret_cast<uintptr_t>(mask) & 15u) == 0;
-  compact_count_kernel<T><<<(unsigned)tiles, kThreads, 0, s>>>(mask, n, counts, vec_ok);
-  compact_write_kernel<T><<<(unsigned)tiles, kThreads, 0, s>>>(mask, n, counts, idx_out,
-                                                               count_out, vec_ok);
+  const bool vec_ok = (reinterpret_cast<uintptr_t>(mask) & 15u) == 0 &&
+                      (reinterpret_cast<uintptr_t>(alive) & 15u) == 0;
+  compact_count_kernel<T><<<(unsigned)tiles, kThreads, 0, s>>>(mask, alive, invert, n, counts,
+                                                               vec_ok);
+  compact_write_kernel<T><<<(unsigned)tiles, kThreads, 0, s>>>(mask, alive, invert, n, counts,
+                                                               idx_out, count_out, vec_ok);
   return gs_check_launch("gs_compact");
 }
 
@@ -197,4 +218,11 @@ extern "C" int gs_compact_u8(const uint8_t* mask, int64_t n, int32_t* idx_out,
 extern "C" int gs_compact_i32(const int32_t* radii, int64_t n, int32_t* idx_out,
                               int32_t* count_out, void* ws, size_t ws_bytes, void* stream) {
   return gs::compact_launch<int32_t>(radii, n, idx_out, count_out, ws, ws_bytes, stream);
+}
+
+extern "C" int gs_compact_select_u8(const uint8_t* mask, const uint8_t* alive, int32_t invert,
+                                    int64_t n, int32_t* idx_out, int32_t* count_out, void* ws,
+                                    size_t ws_bytes, void* stream) {
+  return gs::compact_launch<uint8_t>(mask, n, idx_out, count_out, ws, ws_bytes, stream, alive,
+                                     invert != 0);
 }

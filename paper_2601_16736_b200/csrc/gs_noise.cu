@@ -1,0 +1,134 @@
+// Opacity-gated position noise (optimizer.py:453-486; applied to every
+// alive row after the step, pipeline.py:334-336):
+//
+//     delta = -eta_ratio * lr_position * gate(o) * Sigma @ gamma,
+//     gate(o) = sigmoid(-lambda_mu * (o - lambda_t)),  o = sigmoid(tau),
+//     Sigma = R diag(exp(2 kappa)) R^T,  gamma ~ N(0, I),  dead rows: 0.
+//
+// 2-D form (the reference testbed): R = rotation by the angle rot.  3-D form
+// (3DGS): R from the normalised quaternion (w, x, y, z) as in 3DGS
+// build_rotation, kappa = the 3 log-scales.  gamma comes from a counter-based
+// Philox4x32-10 stream keyed by the seed and counted by (row, iteration), so
+// the draws are reproducible and independent of the launch shape; the
+// reference's own host Generator draws are not reproduced (statistical parity
+// only).  One thread per row, all rows, HBM-bound:
+// 2-D 37 B/row, 3-D 57 B/row.
+#include "gs_common.cuh"
+
+namespace gs {
+
+__device__ __forceinline__ uint4 philox4x32_10(uint4 ctr, uint2 key) {
+  constexpr uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u, W0 = 0x9E3779B9u, W1 = 0xBB67AE85u;
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t hi0 = __umulhi(M0, ctr.x), lo0 = M0 * ctr.x;
+    const uint32_t hi1 = __umulhi(M1, ctr.z), lo1 = M1 * ctr.z;
+    ctr = make_uint4(hi1 ^ ctr.y ^ key.x, lo1, hi0 ^ ctr.w ^ key.y, lo0);
+    key.x += W0;
+    key.y += W1;
+  }
+  return ctr;
+}
+
+// two standard normals from two uniforms (Box-Muller)
+__device__ __forceinline__ float2 box_muller(uint32_t a, uint32_t b) {
+  const float u1 = ((float)(a >> 8) + 0.5f) * (1.0f / 16777216.0f);  // (0, 1)
+  const float u2 = (float)(b >> 8) * (1.0f / 16777216.0f);           // [0, 1)
+  const float r = sqrtf(-2.0f * logf(u1));
+  float s, c;
+  sincospif(2.0f * u2, &s, &c);
+  return make_float2(r * c, r * s);
+}
+
+__device__ __forceinline__ float sigmoidf_stable(float x) {
+  if (x >= 0.f) return 1.0f / (1.0f + expf(-x));
+  const float e = expf(x);
+  return e / (1.0f + e);
+}
+
+template <int D>
+__global__ void __launch_bounds__(256)
+    noise_kernel(float* __restrict__ pos, const float* __restrict__ kappa,
+                 const float* __restrict__ rot, const float* __restrict__ tau,
+                 const uint8_t* __restrict__ alive, int64_t n, float coef, float lambda_mu,
+                 float lambda_t, uint2 key, uint32_t iteration, float* __restrict__ delta_out,
+                 int add) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float d[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) d[k] = 0.f;
+    if (alive == nullptr || alive[i]) {
+      const uint4 rnd = philox4x32_10(
+          make_uint4((uint32_t)i, (uint32_t)(i >> 32), iteration, 0x6e6f6973u /* "nois" */), key);
+      const float2 g01 = box_muller(rnd.x, rnd.y);
+      const float2 g23 = box_muller(rnd.z, rnd.w);
+      const float o = sigmoidf_stable(tau[i]);
+      const float gate = sigmoidf_stable(-lambda_mu * (o - lambda_t));
+      const float a = -coef * gate;
+      if (D == 2) {
+        const float e0 = expf(2.0f * kappa[2 * i]), e1 = expf(2.0f * kappa[2 * i + 1]);
+        float s, c;
+        sincosf(rot[i], &s, &c);
+        const float sxx = c * c * e0 + s * s * e1;
+        const float syy = s * s * e0 + c * c * e1;
+        const float sxy = c * s * (e0 - e1);
+        d[0] = a * (sxx * g01.x + sxy * g01.y);
+        d[1] = a * (sxy * g01.x + syy * g01.y);
+      } else {
+        const float4 q4 = reinterpret_cast<const float4*>(rot)[i];
+        const float qn = rsqrtf(q4.x * q4.x + q4.y * q4.y + q4.z * q4.z + q4.w * q4.w);
+        const float w = q4.x * qn, x = q4.y * qn, y = q4.z * qn, z = q4.w * qn;
+        const float Rm[3][3] = {{1.f - 2.f * (y * y + z * z), 2.f * (x * y - w * z), 2.f * (x * z + w * y)},
+                                {2.f * (x * y + w * z), 1.f - 2.f * (x * x + z * z), 2.f * (y * z - w * x)},
+                                {2.f * (x * z - w * y), 2.f * (y * z + w * x), 1.f - 2.f * (x * x + y * y)}};
+        const float g[3] = {g01.x, g01.y, g23.x};
+        float u[3];
+#pragma unroll
+        for (int r = 0; r < 3; ++r)  // u = S^2 R^T gamma
+          u[r] = expf(2.0f * kappa[3 * i + r]) * (Rm[0][r] * g[0] + Rm[1][r] * g[1] + Rm[2][r] * g[2]);
+#pragma unroll
+        for (int r = 0; r < 3; ++r) d[r] = a * (Rm[r][0] * u[0] + Rm[r][1] * u[1] + Rm[r][2] * u[2]);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      if (delta_out) delta_out[D * i + k] = d[k];
+      if (add) pos[D * i + k] += d[k];
+    }
+  }
+}
+
+}  // namespace gs
+
+extern "C" int gs_noise_perturb(float* position, const float* log_scale, const float* rotation,
+                                const float* opacity_logit, const uint8_t* alive, int64_t n,
+                                int32_t dims, float lr_position, float eta_ratio,
+                                float lambda_mu, float lambda_t, uint64_t seed,
+                                uint32_t iteration, float* delta_out, int32_t add_in_place,
+                                void* stream) {
+  using namespace gs;
+  if (n < 0 || !position || !log_scale || !rotation || !opacity_logit ||
+      (dims != 2 && dims != 3) || (!delta_out && !add_in_place)) {
+    gs_set_error("gs_noise_perturb: invalid arguments");
+    return GS_ERR_ARG;
+  }
+  if (dims == 3 && (reinterpret_cast<uintptr_t>(rotation) & 15u)) {
+    gs_set_error("gs_noise_perturb: quaternions must be 16-byte aligned");
+    return GS_ERR_ALIGN;
+  }
+  if (n == 0) return GS_OK;
+  const uint2 key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
+  const float coef = eta_ratio * lr_position;
+  const int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)gs_sm_count() * 8);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dims == 2)
+    noise_kernel<2><<<grid, 256, 0, s>>>(position, log_scale, rotation, opacity_logit, alive, n,
+                                         coef, lambda_mu, lambda_t, key, iteration, delta_out,
+                                         add_in_place);
+  else
+    noise_kernel<3><<<grid, 256, 0, s>>>(position, log_scale, rotation, opacity_logit, alive, n,
+                                         coef, lambda_mu, lambda_t, key, iteration, delta_out,
+                                         add_in_place);
+  return gs_check_launch("gs_noise_perturb");
+}

@@ -17,6 +17,7 @@ struct GroupPtrs {
   float* v;
   int width;
   int role;
+  float lr;
 };
 
 struct GroupSet {
@@ -38,7 +39,7 @@ static int fill_groups(const gs_group* groups, int32_t n_groups, GroupSet& S, co
       gs_set_error("%s: group %d invalid", who, i);
       return GS_ERR_ARG;
     }
-    S.g[i] = GroupPtrs{g.param, g.grad, g.exp_avg, g.exp_avg_sq, (int)g.width, g.role};
+    S.g[i] = GroupPtrs{g.param, g.grad, g.exp_avg, g.exp_avg_sq, (int)g.width, g.role, g.lr};
   }
   return GS_OK;
 }
@@ -283,6 +284,45 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
+// AIU (optimizer.py:425-450): picked invisible rows take one extra step with
+// their frozen moments and clock, state untouched.  picked row i is
+// inv_idx[jlist[i]]; lr_eta is fl32(lr * eta) per group (the reference does
+// not apply mu_lr_scale here, optimizer.py:449).  Rows with clock 0 are
+// skipped (:444).  A warp owns a row; lanes stride over its elements.
+__global__ void __launch_bounds__(kThreads)
+    aiu_rows_kernel(const GroupSet S, int P, float* __restrict__ record, int64_t stride,
+                    const int32_t* __restrict__ inv_idx, const int32_t* __restrict__ jlist,
+                    const int32_t* __restrict__ k_dev, const float* __restrict__ lut,
+                    int lut_len, float eps, int32_t* __restrict__ picked_out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t k = *k_dev;
+  const int64_t warps = (int64_t)gridDim.x * (kThreads / 32);
+  for (int64_t i = (int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5); i < k; i += warps) {
+    const int32_t row = __ldg(inv_idx + __ldg(jlist + i));
+    if (lane == 0 && picked_out) picked_out[i] = row;
+    const float* rec = record + (int64_t)row * stride;
+    const int t = reinterpret_cast<const int*>(rec)[2 * P];
+    if (t <= 0) continue;
+    const float2 bc = bias_factors(lut, lut_len, t, 0.0, 0.0);
+    for (int sl = lane; sl < P; sl += 32) {
+      int off = 0, gi = 0;
+      for (; gi < S.n; ++gi) {
+        if (sl < off + S.g[gi].width) break;
+        off += S.g[gi].width;
+      }
+      const int W = S.g[gi].width;
+      const int c = sl - off;
+      const float2 mv = reinterpret_cast<const float2*>(rec)[sl];
+      const float mh = __fmul_rn(mv.x, bc.x);
+      const float vh = __fmul_rn(mv.y, bc.y);
+      const float den = __fadd_rn(__fsqrt_rn(vh), eps);
+      const float upd = __fdiv_rn(__fmul_rn(S.g[gi].lr, mh), den);
+      float* p = S.g[gi].param + (int64_t)row * W + c;
+      *p = __fsub_rn(*p, upd);
+    }
+  }
+}
+
 static int record_args(const float* record, int64_t stride, int P, const char* who) {
   if (!record || P < 1 || stride < 2 * (P + 1) || (stride & 1) ||
       (reinterpret_cast<uintptr_t>(record) & 7u)) {
@@ -347,7 +387,7 @@ extern "C" int gs_stats_all_rows(const gs_group* groups, int32_t n_groups, int64
   int P = 0;
   for (int i = 0; i < n_groups; ++i) {
     S.g[i] = GroupPtrs{groups[i].param, nullptr, nullptr, nullptr, (int)groups[i].width,
-                       groups[i].role};
+                       groups[i].role, 0.f};
     if (groups[i].width < 1) {
       gs_set_error("gs_stats_all_rows: group %d invalid", i);
       return GS_ERR_ARG;
@@ -470,4 +510,41 @@ extern "C" int gs_stats_all(const gs_group* groups, int32_t n_groups, int64_t n_
   stats_all_kernel<<<grid, kThreads, 0, (cudaStream_t)stream>>>(S, n_rows, alive, active_logit,
                                                                 out, partials, &hdr->counter);
   return gs_check_launch("gs_stats_all");
+}
+
+extern "C" int gs_aiu_apply_rows(const gs_group* groups, int32_t n_groups, float* record,
+                                 int64_t record_stride, const int32_t* inv_idx,
+                                 const int32_t* jlist, const int32_t* k_dev, int64_t max_k,
+                                 const float* bias_lut, int32_t lut_len, float eps,
+                                 int32_t* picked_out, void* stream) {
+  using namespace gs;
+  GroupSet S{};
+  if (!groups || n_groups < 1 || n_groups > GS_MAX_GROUPS) {
+    gs_set_error("gs_aiu_apply_rows: bad group list");
+    return GS_ERR_ARG;
+  }
+  S.n = n_groups;
+  int P = 0;
+  for (int i = 0; i < n_groups; ++i) {
+    if (!groups[i].param || groups[i].width < 1) {
+      gs_set_error("gs_aiu_apply_rows: group %d invalid", i);
+      return GS_ERR_ARG;
+    }
+    // lr carries fl32(lr * eta), set by the caller
+    S.g[i] = GroupPtrs{groups[i].param, nullptr, nullptr, nullptr, (int)groups[i].width,
+                       groups[i].role, groups[i].lr};
+    P += (int)groups[i].width;
+  }
+  int rc = record_args(record, record_stride, P, "gs_aiu_apply_rows");
+  if (rc) return rc;
+  if (!inv_idx || !jlist || !k_dev || !bias_lut || lut_len < 2 || max_k < 0) {
+    gs_set_error("gs_aiu_apply_rows: bad index / LUT arguments");
+    return GS_ERR_ARG;
+  }
+  if (max_k == 0) return GS_OK;
+  const int64_t need = (max_k + 7) / 8;
+  const int grid = (int)std::min<int64_t>(need, (int64_t)gs_sm_count() * 8);
+  aiu_rows_kernel<<<grid, kThreads, 0, (cudaStream_t)stream>>>(
+      S, P, record, record_stride, inv_idx, jlist, k_dev, bias_lut, lut_len, eps, picked_out);
+  return gs_check_launch("gs_aiu_apply_rows");
 }

@@ -47,6 +47,7 @@ struct StepParams {
   const int32_t* nv_dev;
   double nv_host;
   const int32_t* abort_flag;
+  DensifyArgs D;
   const int32_t* rows;
   const int32_t* n_rows_dev;
   int64_t max_rows;
@@ -139,6 +140,10 @@ __global__ void __launch_bounds__(kThreads, kStepBlocksPerSM) step_kernel(const 
       if (bad == 0) {
         const int tn = t + 1;
         P.clock[row] = tn;
+        if (P.D.group >= 0) {
+          const GroupDev& DG = P.g[P.D.group];
+          densify_row(P.D, (uint32_t)row, DG.grad + (int64_t)row * DG.width, DG.width, 1);
+        }
         const int tb = T::kDense ? P.global_t : tn;
         s_bc[tid] = bias_factors(P.lut, P.lut_len, tb, P.beta1, P.beta2);
         ++c_step;
@@ -298,6 +303,12 @@ extern "C" int gs_step(const gs_group* groups, int32_t n_groups, const gs_step_c
   P.nv_dev = cfg->n_visible_norm;
   P.nv_host = cfg->n_visible_host;
   P.abort_flag = cfg->abort_flag;
+  P.D = DensifyArgs{cfg->densify_accum, cfg->densify_count, cfg->densify_scale,
+                    cfg->densify_group};
+  if (P.D.group >= n_groups || (P.D.group >= 0 && (!P.D.accum || !P.D.count))) {
+    gs_set_error("gs_step: bad densification-statistics arguments");
+    return GS_ERR_ARG;
+  }
   P.rows = rows;
   P.n_rows_dev = n_rows_dev;
   P.max_rows = max_rows;

@@ -58,6 +58,7 @@ struct RowParams {
   const int32_t* nv_dev;
   double nv_host;
   const int32_t* abort_flag;
+  DensifyArgs D;
   const int32_t* rows;
   const int32_t* n_rows_dev;
   int64_t max_rows;
@@ -211,6 +212,10 @@ __global__ void __launch_bounds__(kRowThreads, MINB)
       if (!valid[r]) continue;  // uniform within the sub-warp
       if (q == clock_lane) {
         ++c_vis;
+        if (!row_bad && P.D.group >= 0) {
+          const RowGroup& DG = P.g[P.D.group];
+          densify_row(P.D, (uint32_t)row[r], DG.grad + (int64_t)row[r] * DG.width, DG.width, 1);
+        }
         if (!row_bad) ++c_step;
         else if (b1) ++c_badg;
         else ++c_badd;
@@ -412,6 +417,12 @@ extern "C" int gs_step_rows(const gs_group* groups, int32_t n_groups, const gs_s
   P.nv_dev = cfg->n_visible_norm;
   P.nv_host = cfg->n_visible_host;
   P.abort_flag = cfg->abort_flag;
+  P.D = DensifyArgs{cfg->densify_accum, cfg->densify_count, cfg->densify_scale,
+                    cfg->densify_group};
+  if (P.D.group >= n_groups || (P.D.group >= 0 && (!P.D.accum || !P.D.count))) {
+    gs_set_error("gs_step_rows: bad densification-statistics arguments");
+    return GS_ERR_ARG;
+  }
   P.rows = rows;
   P.n_rows_dev = n_rows_dev;
   P.max_rows = max_rows;

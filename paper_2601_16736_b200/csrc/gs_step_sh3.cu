@@ -58,6 +58,7 @@ struct FixedParams {
   const int32_t* nv_dev;
   double nv_host;
   const int32_t* abort_flag;
+  DensifyArgs D;
   const int32_t* rows;
   const int32_t* n_rows_dev;
   int64_t max_rows;
@@ -985,6 +986,12 @@ __global__ void __launch_bounds__((NPW + NCW) * 32, MINB) step_ws_kernel(const F
         if (bad == 0) {
           reinterpret_cast<int*>(rec_base + (size_t)s_crow[st][t] * rec_stride2 + L::P)[0] = tn;
           s_bc[st][t] = bc;
+          if (P.D.group >= 0) {
+#pragma unroll
+            for (int gg = 0; gg < L::G; ++gg)
+              if (gg == P.D.group)
+                densify_row(P.D, s_crow[st][t], sg + R * L::OFF(gg) + t * L::W(gg), L::W(gg), 1);
+          }
           ++c_step;
         } else if (bad & 1) {
           ++c_badg;
@@ -1103,7 +1110,9 @@ void launch_fixed_v(const FixedParams& P, int64_t max_rows, cudaStream_t s) {
 
 template <class L, int MODE, bool STRICT>
 void launch_fixed(const FixedParams& P, int64_t max_rows, cudaStream_t s) {
-  switch (fixed_variant()) {
+  // the densification statistics are fused into the warp-specialised kernel only
+  const int variant = P.D.group >= 0 ? 0 : fixed_variant();
+  switch (variant) {
     case 1: launch_fixed_v<L, MODE, STRICT, 64, 2>(P, max_rows, s); return;
     case 2: launch_pipe<L, MODE, STRICT, 32, 2, 3>(P, max_rows, s); return;
     case 3: launch_pipe2<L, MODE, STRICT, 32, 2, 3>(P, max_rows, s); return;
@@ -1165,6 +1174,8 @@ int gs_step_fixed_try(const gs_group* groups, int32_t n_groups, const gs_step_cf
   P.nv_dev = cfg->n_visible_norm;
   P.nv_host = cfg->n_visible_host;
   P.abort_flag = cfg->abort_flag;
+  P.D = DensifyArgs{cfg->densify_accum, cfg->densify_count, cfg->densify_scale,
+                    cfg->densify_group};
   P.rows = rows;
   P.n_rows_dev = n_rows_dev;
   P.max_rows = max_rows;

@@ -166,6 +166,7 @@ class StepEngine:
                                              device=dev)
             self._bad_rows = None
             self._rows_tmp = None
+            self._sel = None  # secondary compaction buffers (AIU), lazily
         self.active_logit = active_logit_threshold()
         self.launches = 0  # C-ABI kernel launches issued (bench accounting)
         self._group_cache_key = None
@@ -222,13 +223,79 @@ class StepEngine:
         self.launches += 2 if self.n_rows > 0 else 0  # count + write passes
         return self.idx, self.count
 
+    def compact_select(self, mask: torch.Tensor, alive: torch.Tensor | None = None,
+                       invert: bool = False) -> tuple[torch.Tensor, torch.Tensor]:
+        """Rows with mask != 0 (or == 0 when ``invert``), alive only; into a
+        second index buffer so the step's visible list is not clobbered."""
+        if mask.dtype not in (torch.bool, torch.uint8) or mask.numel() != self.n_rows:
+            raise ConfigError("selection mask must be a bool/uint8 row mask")
+        if alive is not None and (alive.dtype not in (torch.bool, torch.uint8)
+                                  or alive.numel() != self.n_rows):
+            raise ConfigError("alive must be a bool/uint8 row mask")
+        if self._sel is None:
+            n = max(self.n_rows, 1)
+            self._sel = (torch.empty(n, dtype=torch.int32, device=self.device),
+                         torch.zeros(1, dtype=torch.int32, device=self.device),
+                         torch.zeros(int(self.lib.gs_compact_workspace_bytes(n)),
+                                     dtype=torch.uint8, device=self.device))
+        idx, cnt, ws = self._sel
+        mask = mask.contiguous()
+        alive = alive.contiguous() if alive is not None else None
+        rc = self.lib.gs_compact_select_u8(mask.data_ptr(), _ptr(alive), int(bool(invert)),
+                                           self.n_rows, idx.data_ptr(), cnt.data_ptr(),
+                                           ws.data_ptr(), ws.numel(), _stream_handle(self.device))
+        L.check(rc, "gs_compact_select_u8")
+        self.launches += 2 if self.n_rows > 0 else 0
+        return idx, cnt
+
+    def compact_positions(self, mask: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor]:
+        """K1 on an arbitrary-length uint8 mask (scratch buffers sized on demand)."""
+        n = int(mask.numel())
+        buf = getattr(self, "_pos", None)
+        if buf is None or buf[0].numel() < n:
+            cap = max(n, 1)
+            buf = (torch.empty(cap, dtype=torch.int32, device=self.device),
+                   torch.zeros(1, dtype=torch.int32, device=self.device),
+                   torch.zeros(int(self.lib.gs_compact_workspace_bytes(cap)), dtype=torch.uint8,
+                               device=self.device))
+            self._pos = buf
+        idx, cnt, ws = buf
+        rc = self.lib.gs_compact_u8(mask.contiguous().data_ptr(), n, idx.data_ptr(),
+                                    cnt.data_ptr(), ws.data_ptr(), ws.numel(),
+                                    _stream_handle(self.device))
+        L.check(rc, "gs_compact_u8")
+        self.launches += 2 if n > 0 else 0
+        return idx, cnt
+
+    def aiu(self, groups: list[GroupBinding], record: torch.Tensor, inv_idx: torch.Tensor,
+            jlist: torch.Tensor, k_dev: torch.Tensor, max_k: int, eta: float, eps: float):
+        """Artificial implicit updates on picked rows (optimizer.py:425-450);
+        returns the picked rows (device int32 [max_k])."""
+        self._check_record(record, groups)
+        arr = (L.GsGroup * len(groups))()
+        for i, g in enumerate(groups):
+            _check_tensor(f"{g.name}.param", g.param, self.n_rows, g.width, self.device)
+            # optimizer.py:449: lr * eta (no mu_lr_scale), rounded once
+            arr[i] = L.GsGroup(_ptr(g.param), None, None, None, g.width, g.role,
+                               float(np.float32(g.lr * eta)))
+        picked = torch.empty(max(max_k, 1), dtype=torch.int32, device=self.device)
+        rc = self.lib.gs_aiu_apply_rows(arr, len(groups), record.data_ptr(), record.stride(0),
+                                        inv_idx.data_ptr(), jlist.data_ptr(), k_dev.data_ptr(),
+                                        int(max_k), self.lut.data_ptr(), self.lut.shape[0],
+                                        float(np.float32(eps)), picked.data_ptr(),
+                                        _stream_handle(self.device))
+        L.check(rc, "gs_aiu_apply_rows")
+        self.launches += 1 if max_k else 0
+        return picked[:max_k]
+
     # ------------------------------------------------------------------ step
     def step(self, groups: list[GroupBinding], mode: str, clock: torch.Tensor, *,
              rows: torch.Tensor | None, count: torch.Tensor | None, eps: float,
              lambda_opacity: float = 0.0, lambda_scale: float = 0.0, clip_opacity: float = 10.0,
              clip_scale: float = 10.0, n_pixels_rounded: float = 0.0, global_t: int = 0,
              n_visible_dev: torch.Tensor | None = None, n_visible_host: float = 0.0,
-             check: str = "fused", record: torch.Tensor | None = None) -> torch.Tensor:
+             check: str = "fused", record: torch.Tensor | None = None,
+             densify: tuple | None = None) -> torch.Tensor:
         """K2 (plus the strict pre-check when ``check == "strict"``).
 
         ``record`` given: row-record state (gs_step_rows), ``clock`` ignored;
@@ -261,6 +328,15 @@ class StepEngine:
         cfg.n_visible_norm = _ptr(n_visible_dev)
         cfg.n_visible_host = float(n_visible_host)
         cfg.abort_flag = self.abort.data_ptr()
+        cfg.densify_group = -1
+        if densify is not None:
+            accum, dcount, dscale, dgroup = densify
+            _check_tensor("densify accum", accum, self.n_rows, 1, self.device, torch.float32)
+            _check_tensor("densify count", dcount, self.n_rows, 1, self.device, torch.int32)
+            cfg.densify_accum = accum.data_ptr()
+            cfg.densify_count = dcount.data_ptr()
+            cfg.densify_scale = float(np.float32(dscale))
+            cfg.densify_group = int(dgroup)
         if check == "strict":
             # the penalty's activation domain is checked where the penalty
             # applies: listed rows, or every row for the dense coupled mode

@@ -263,6 +263,7 @@ class AdamWGS:
         self._stats_host = torch.zeros(L.GS_STEP_STATS, dtype=torch.float64, pin_memory=True)
         self._pending = None
         self._last_ctx = None
+        self._densify = None  # (accum, count, group index) when enabled
 
     # ------------------------------------------------------------------ helpers
     def _bindings(self, grads=None, mu_lr_scale: float = 1.0) -> list[GroupBinding]:
@@ -294,7 +295,7 @@ class AdamWGS:
     def step(self, visibility: torch.Tensor | None = None, n_pixels: int | None = None, *,
              mu_lr_scale: float = 1.0, lambda_o: float | None = None,
              lambda_s: float | None = None, clip: float | None = None, grads=None,
-             n_visible: torch.Tensor | None = None):
+             n_visible: torch.Tensor | None = None, densify_scale: float | None = None):
         """One optimizer step over the visible primitives.
 
         adamw-gs            dar_step (optimizer.py:269-298): ``n_pixels`` = N_I,
@@ -308,6 +309,9 @@ class AdamWGS:
         coupled-adam        adam_step_sync over every row, coupled terms on
                             every row (pipeline.py:305-310).
         ``n_visible``: device int32 [1] global N_v (index-sharded multi-GPU).
+        ``densify_scale``: with :meth:`enable_densify_stats`, accumulate
+        ||grad_position|| * densify_scale and a count per stepped row, fused
+        into the step (DensifyStats.observe, pipeline.py:67-91).
         """
         self._raise_pending()
         mode = self.mode
@@ -316,6 +320,11 @@ class AdamWGS:
         lo = self.lambda_o if lambda_o is None else float(lambda_o)
         ls = self.lambda_s if lambda_s is None else float(lambda_s)
         kw = dict(eps=self.eps, check=self.check, record=self.state.record)
+        if densify_scale is not None:
+            if self._densify is None:
+                raise ConfigError("call enable_densify_stats() first")
+            acc, cnt, gidx = self._densify
+            kw["densify"] = (acc, cnt, float(densify_scale), gidx)
         if mode == "coupled-adam":
             self.state.global_t += 1
             nv = None
@@ -399,6 +408,32 @@ class AdamWGS:
         """Per-step statistics of the last step (host sync)."""
         return _stats_dict(self.engine.stats.tolist())
 
+    # ----------------------------------------------- densification statistics
+    def enable_densify_stats(self, group: str | None = None):
+        """Allocate the per-row gradient-norm accumulator and count
+        (DensifyStats, pipeline.py:67-91) for the position group (or ``group``)."""
+        names = [g["name"] for g in self.param_groups]
+        if group is None:
+            pos = [g["name"] for g in self.param_groups if g["role"] == L.ROLE_POSITION]
+            if not pos:
+                raise ConfigError("no position group; pass group=")
+            group = pos[0]
+        gidx = names.index(group)
+        acc = torch.zeros(self.n_rows, dtype=torch.float32, device=self.device)
+        cnt = torch.zeros(self.n_rows, dtype=torch.int32, device=self.device)
+        self._densify = (acc, cnt, gidx)
+
+    def densify_stats(self):
+        """(accum, count) device tensors; mean = accum / max(count, 1)."""
+        if self._densify is None:
+            raise ConfigError("densification statistics are not enabled")
+        return self._densify[0], self._densify[1]
+
+    def reset_densify_stats(self):
+        if self._densify is not None:
+            self._densify[0].zero_()
+            self._densify[1].zero_()
+
     # ----------------------------------------------------------- state ops
     @torch.no_grad()
     def rsr_apply(self, indices, alpha1: float, alpha2: float):
@@ -411,6 +446,56 @@ class AdamWGS:
         """Fresh state on the rows (optimizer.py:159-165): m = v = 0, t = 0."""
         self.engine.reset_rows(self._state_bindings(), self.state.clock, indices,
                                record=self.state.record)
+
+    @torch.no_grad()
+    def aiu_apply(self, visibility: torch.Tensor, aiu, rng: np.random.Generator, iteration: int,
+                  alive: torch.Tensor | None = None) -> np.ndarray:
+        """Artificial implicit updates (optimizer.py:425-450).
+
+        The invisible alive rows are compacted on the GPU; the Bernoulli picks
+        are drawn on the host from ``rng`` exactly as the reference does
+        (``rng.random(invisible.size) < prob``), so the picked set is
+        bit-identical; the frozen-moment update runs on the GPU.  Returns the
+        picked rows (int64, ascending).
+        """
+        empty = np.empty(0, dtype=np.int64)
+        if not aiu.active(iteration):
+            return empty
+        if self.state.record is None:
+            raise ConfigError("aiu_apply needs the row-record state layout")
+        prob, eta = aiu.prob_at(iteration), aiu.eta_at(iteration)
+        eng = self.engine
+        vis = visibility if visibility.dtype in (torch.bool, torch.uint8) else visibility > 0
+        inv_idx, inv_cnt = eng.compact_select(vis, alive, invert=True)
+        n_inv = int(inv_cnt.item())
+        if n_inv == 0 or prob <= 0.0 or eta == 0.0:
+            return empty
+        sel = rng.random(n_inv) < prob
+        k = int(sel.sum())
+        if k == 0:
+            return empty
+        jmask = torch.from_numpy(sel.view(np.uint8)).to(self.device)
+        # positions of the picks inside the invisible list (bit-exact order)
+        jlist, jcnt = eng.compact_positions(jmask)
+        picked = eng.aiu(self._state_bindings(), self.state.record, inv_idx, jlist, jcnt, k, eta,
+                         self.eps)
+        return picked.cpu().numpy().astype(np.int64)
+
+    @torch.no_grad()
+    def noise_perturb(self, lr_position: float, cfg, seed: int, iteration: int,
+                      alive: torch.Tensor | None = None, add: bool = True) -> torch.Tensor:
+        """Opacity-gated position noise (optimizer.py:453-486) over the
+        position / scale / rotation / opacity groups; added in place by default
+        (pipeline.py:334-336)."""
+        from .noise import noise_perturb
+        by_role = {g["role"]: g["params"][0] for g in self.param_groups}
+        rot = [g["params"][0] for g in self.param_groups if g["name"] in ("rotation", "rot")]
+        if L.ROLE_POSITION not in by_role or L.ROLE_SCALE not in by_role or \
+                L.ROLE_OPACITY not in by_role or not rot:
+            raise ConfigError("noise needs position, scaling, rotation and opacity groups")
+        return noise_perturb(by_role[L.ROLE_POSITION].data, by_role[L.ROLE_SCALE].data,
+                             rot[0].data, by_role[L.ROLE_OPACITY].data, lr_position, cfg, seed,
+                             iteration, alive=alive, add=add)
 
     @torch.no_grad()
     def moment_stats(self, alive: torch.Tensor | None = None) -> dict:

@@ -37,9 +37,11 @@ from . import _lib as L
 from .engine import (ConfigError, DomainError, GradientError, GroupBinding, StepEngine,
                      round_pixel_count)
 from .optimizer import MomentState, OptimizerConfig, _moment_stats, role_of
-from .sampling import RsrConfig, StSSchedule, stss_sample
+from .noise import NoiseConfig, seed_from_generator
+from .noise import noise_perturb as _noise_perturb
+from .sampling import AiuConfig, RsrConfig, StSSchedule, stss_sample
 
-__all__ = ["MODES", "ConfigError", "GradientError", "DomainError", "OptimizerConfig",
+__all__ = ["noise_perturb", "aiu_apply", "NoiseConfig", "AiuConfig", "MODES", "ConfigError", "GradientError", "DomainError", "OptimizerConfig",
            "MomentState", "StSSchedule", "RsrConfig", "round_pixel_count", "adam_step_sync",
            "sparse_adam_step", "dar_step", "adamw_const_step", "rsr_apply", "stss_sample",
            "reset_rows", "moment_stats", "classify_active"]
@@ -214,3 +216,54 @@ def classify_active(pset, threshold: float = 1.0 / 255.0, alive=None):
         alive = torch.from_numpy(np.asarray(alive, dtype=bool)).to(tau.device)
     out = eng.stats_all(b, alive).tolist()
     return int(out[1]), int(out[0]) - int(out[1]), None
+
+
+def noise_perturb(pset, state, lr_position: float, cfg, rng) -> torch.Tensor:
+    """optimizer.py:463-486 — the additive position perturbation of every alive
+    row (the caller adds it, pipeline.py:335).  ``pset`` holds ``mu``, ``kappa``,
+    ``rot`` (2-D) or ``xyz``, ``scaling``, ``rotation`` (3DGS) and the opacity
+    logit ``tau`` / ``opacity``; ``rng`` seeds the on-device Philox stream."""
+    def pick(*names):
+        for nm in names:
+            if (isinstance(pset, dict) and nm in pset) or hasattr(pset, nm):
+                return _get(pset, nm)
+        raise ConfigError(f"primitive set lacks {names}")
+    pos = pick("mu", "xyz")
+    alive = pset.get("alive") if isinstance(pset, dict) else getattr(pset, "alive", None)
+    if alive is not None and not isinstance(alive, torch.Tensor):
+        alive = torch.from_numpy(np.asarray(alive, dtype=bool)).to(pos.device)
+    return _noise_perturb(pos, pick("kappa", "scaling"), pick("rot", "rotation"),
+                          pick("tau", "opacity"), lr_position, cfg, seed_from_generator(rng), 0,
+                          alive=alive)
+
+
+def aiu_apply(state, pset, vis, cfg, aiu, rng, iteration: int, alive=None) -> np.ndarray:
+    """optimizer.py:425-450 over a row-record MomentState (picked rows bit-exact)."""
+    from .optimizer import AdamWGS  # noqa: F401  (engine plumbing below)
+    if state.record is None:
+        raise ConfigError("aiu_apply needs the row-record state layout")
+    if not aiu.active(iteration):
+        return np.empty(0, dtype=np.int64)
+    n = len(state)
+    eng = _engine(n, state.clock.device, cfg.beta1, cfg.beta2)
+    vis_t = _as_mask(vis, n, state.clock.device)
+    if vis_t.dtype == torch.int32:
+        vis_t = vis_t > 0
+    if alive is None:
+        alive = getattr(pset, "alive", None) if not isinstance(pset, dict) else pset.get("alive")
+    if alive is not None and not isinstance(alive, torch.Tensor):
+        alive = torch.from_numpy(np.asarray(alive, dtype=bool)).to(state.clock.device)
+    prob, eta = aiu.prob_at(iteration), aiu.eta_at(iteration)
+    inv_idx, inv_cnt = eng.compact_select(vis_t, alive, invert=True)
+    n_inv = int(inv_cnt.item())
+    if n_inv == 0 or prob <= 0.0 or eta == 0.0:
+        return np.empty(0, dtype=np.int64)
+    sel = rng.random(n_inv) < prob
+    k = int(sel.sum())
+    if k == 0:
+        return np.empty(0, dtype=np.int64)
+    jlist, jcnt = eng.compact_positions(torch.from_numpy(sel.view(np.uint8)).to(inv_idx.device))
+    groups = [GroupBinding(k_, role_of(k_), cfg.lr(k_), _get(pset, k_), None, None, None)
+              for k_ in state.m]
+    picked = eng.aiu(groups, state.record, inv_idx, jlist, jcnt, k, eta, cfg.eps)
+    return picked.cpu().numpy().astype(np.int64)

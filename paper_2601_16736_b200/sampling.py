@@ -77,6 +77,43 @@ class RsrConfig:
             raise ConfigError("RSR factors must lie in [0, 1)")
 
 
+@dataclass(frozen=True)
+class AiuConfig:
+    """Artificial implicit updates for sampled invisible primitives
+    (optimizer.py:389-422)."""
+
+    start: int = 0
+    end: int = -1  # inclusive; -1 disables
+    prob_schedule: tuple = ()  # ((iteration, probability), ...)
+    eta_schedule: tuple = ()  # ((iteration, step scale), ...)
+    enabled: bool = False
+
+    def __post_init__(self):
+        for sched in (self.prob_schedule, self.eta_schedule):
+            iters = [it for it, _ in sched]
+            if any(b <= a for a, b in zip(iters, iters[1:])):
+                raise ConfigError("schedule milestones must be strictly increasing")
+        if any(not (0.0 <= p <= 1.0) for _, p in self.prob_schedule):
+            raise ConfigError("sampling probabilities must lie in [0, 1]")
+
+    def active(self, iteration: int) -> bool:
+        return self.enabled and self.start <= iteration <= self.end
+
+    @staticmethod
+    def _at(schedule, iteration: int) -> float:
+        out = 0.0
+        for it, val in schedule:
+            if iteration >= it:
+                out = val
+        return out
+
+    def prob_at(self, iteration: int) -> float:
+        return self._at(self.prob_schedule, iteration)
+
+    def eta_at(self, iteration: int) -> float:
+        return self._at(self.eta_schedule, iteration)
+
+
 def stss_sample(schedule: StSSchedule, iteration: int, n_p: int,
                 rng: np.random.Generator) -> np.ndarray:
     """optimizer.py:379-386 — floor(ratio*N_p) distinct rows, sorted, int64."""

@@ -280,6 +280,46 @@ def run_rsr_stats(name="rsr_stats", n=64, seed=11):
     save(name, meta, arrays)
 
 
+def run_aiu(name="aiu", n=200, seed=21):
+    """aiu_apply (optimizer.py:425-450) on the native 2-D layout."""
+    gradients, optimizer, primitives, loss = _import_reference()
+    rng = np.random.default_rng(seed)
+    p0 = {"mu": f32(rng.normal(0, 5, (n, 2))),
+          "kappa": f32(rng.uniform(math.log(1e-3), math.log(0.5), (n, 2))),
+          "rot": f32(rng.normal(0, 1, (n, 1))), "tau": f32(rng.normal(-1, 2, (n, 1))),
+          "color": f32(rng.normal(0, 0.5, (n, 3)))}
+    alive = rng.random(n) < 0.9
+    ps = primitives.PrimitiveSet(mu=p0["mu"], kappa=p0["kappa"], rot=p0["rot"][:, 0],
+                                 tau=p0["tau"][:, 0], color=p0["color"], depth=np.zeros(n),
+                                 alive=alive)
+    st = optimizer.MomentState.zeros_like(ps)
+    t = rng.integers(0, 40, n)                  # some rows never stepped (t = 0)
+    m0, v0 = {}, {}
+    for a, w in REF2D:
+        m0[a] = f32(rng.standard_normal((n, w)) * 1e-3)
+        v0[a] = f32(rng.random((n, w)) * 1e-6)
+        st.m[a][:] = m0[a].reshape(st.m[a].shape)
+        st.v[a][:] = v0[a].reshape(st.v[a].shape)
+        st.t[a][:] = t
+    vis = rng.random(n) < 0.4
+    cfg = optimizer.OptimizerConfig()
+    aiu = optimizer.AiuConfig(start=0, end=100, prob_schedule=((0, 0.3),),
+                              eta_schedule=((0, 0.1),), enabled=True)
+    draw_seed = 777
+    picked = optimizer.aiu_apply(st, ps, vis, cfg, aiu, np.random.default_rng(draw_seed), 10)
+    arrays = {"vis": vis, "alive": alive, "t": t.astype(np.int64), "picked": picked}
+    for a, w in REF2D:
+        arrays[f"init_{a}"] = p0[a]
+        arrays[f"m_{a}"] = m0[a]
+        arrays[f"v_{a}"] = v0[a]
+        arrays[f"out_{a}"] = np.asarray(getattr(ps, a), np.float64).reshape(n, w)
+    meta = dict(layout="ref2d", n=n, seed=seed, draw_seed=draw_seed, prob=0.3, eta=0.1,
+                iteration=10, lr={"mu": cfg.lr_mu, "kappa": cfg.lr_kappa, "rot": cfg.lr_rot,
+                                  "tau": cfg.lr_tau, "color": cfg.lr_color},
+                beta1=cfg.beta1, beta2=cfg.beta2, eps=cfg.eps)
+    save(name, meta, arrays)
+
+
 if __name__ == "__main__":
     run_sh3_case("sh3_dar", "adamw-gs")
     run_sh3_case("sh3_dar_clip", "adamw-gs", seed=1, lambda_o=0.1, lambda_s=0.05, n_pixels=1024,
@@ -291,3 +331,4 @@ if __name__ == "__main__":
     run_ref2d_coupled("ref2d_sparse_coupled", "sparse-adam")
     run_ref2d_coupled("ref2d_sync_coupled", "coupled-adam", seed=6, p_vis=0.7)
     run_rsr_stats()
+    run_aiu()

@@ -42,11 +42,28 @@ def test_library_is_sm100a():
     assert "sm_100a" in out
 
 
-def test_ctypes_struct_layout_matches_header():
+def test_ctypes_struct_layout_matches_header(tmp_path):
+    """Compile the header with gcc and compare every field offset and the
+    struct sizes with the ctypes mirror."""
+    import subprocess
     from paper_2601_16736_b200 import _lib
-    assert ctypes.sizeof(_lib.GsGroup) == 48
-    # gs_step_cfg: 2 int + 4 float + 5 double + ptr + 2 int + 2 double + ptr + double + ptr
-    assert ctypes.sizeof(_lib.GsStepCfg) == 8 + 16 + 40 + 8 + 8 + 16 + 8 + 8 + 8
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "adamw_gs.h"',
+             'int main(void) {']
+    for cname, py in (("gs_group", _lib.GsGroup), ("gs_step_cfg", _lib.GsStepCfg)):
+        lines.append(f'printf("{cname} size %zu\\n", sizeof({cname}));')
+        for f, _ in py._fields_:
+            lines.append(f'printf("{cname} {f} %zu\\n", offsetof({cname}, {f}));')
+    lines += ["return 0;", "}"]
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", str(HEADER.parent), str(src), "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split("\n")
+    got = {tuple(l.split()[:2]): int(l.split()[2]) for l in out if l.strip()}
+    for cname, py in (("gs_group", _lib.GsGroup), ("gs_step_cfg", _lib.GsStepCfg)):
+        assert got[(cname, "size")] == ctypes.sizeof(py), cname
+        for f, _ in py._fields_:
+            assert got[(cname, f)] == getattr(py, f).offset, (cname, f)
 
 
 def test_workspace_queries_without_gpu():

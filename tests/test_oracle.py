@@ -159,3 +159,19 @@ def test_sigmoid_threshold_is_exact_boundary():
     s = O.sigmoid_f64(np.array([thr, np.nextafter(thr, np.float32(1))], np.float64))
     assert s[0] <= O.ACTIVE_OPACITY_THRESHOLD < s[1]
     assert abs(float(thr) - math.log(1 / 254)) < 1e-6
+
+
+def test_aiu_f64_restatement_is_bitwise_reference():
+    import json
+    z = np.load(Case.__init__.__globals__["GOLDEN"] / "aiu.npz")
+    meta = json.loads(str(z["meta"]))
+    lay = O.LAYOUT_REF2D
+    p = {g.name: z[f"init_{g.name}"].astype(np.float64) for g in lay}
+    m = {g.name: z[f"m_{g.name}"].astype(np.float64) for g in lay}
+    v = {g.name: z[f"v_{g.name}"].astype(np.float64) for g in lay}
+    picked = O.aiu_apply_f64(lay, p, m, v, z["t"], z["vis"], z["alive"], meta["lr"],
+                             meta["beta1"], meta["beta2"], meta["eps"], meta["prob"],
+                             meta["eta"], np.random.default_rng(meta["draw_seed"]))
+    assert np.array_equal(picked, z["picked"])
+    for g in lay:
+        assert np.array_equal(p[g.name], z[f"out_{g.name}"]), g.name
