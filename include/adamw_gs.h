@@ -121,6 +121,13 @@ int32_t gs_abi_version(void);
 const char* gs_last_error(void);
 int32_t gs_device_sm_count(void);
 
+/* Device address of page-locked (pinned, mapped) host memory.  Gradient
+ * pointers in gs_group may be such addresses: the step then gathers only the
+ * visible rows' gradients over PCIe instead of a dense host->device copy
+ * (zero-copy; the reference's gradients come from the host renderer,
+ * pipeline.py:299-304). */
+int gs_host_device_pointer(const void* host_ptr, void** dev_ptr);
+
 /* K1 — visibility compaction: ascending int32 indices of nonzero mask bytes
  * (or radii > 0), count written to *count_out (device).  Bit-exact with
  * np.flatnonzero.  ws: gs_compact_workspace_bytes(n) bytes (one int per

@@ -58,6 +58,7 @@ SIGNATURES = {
     "gs_abi_version": (C.c_int32, []),
     "gs_last_error": (C.c_char_p, []),
     "gs_device_sm_count": (C.c_int32, []),
+    "gs_host_device_pointer": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
     "gs_compact_workspace_bytes": (C.c_size_t, [C.c_int64]),
     "gs_compact_u8": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p,
                                 C.c_size_t, C.c_void_p]),

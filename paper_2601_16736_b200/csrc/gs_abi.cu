@@ -38,3 +38,19 @@ int gs_sm_count() {
 extern "C" int32_t gs_abi_version(void) { return GS_ABI_VERSION; }
 extern "C" const char* gs_last_error(void) { return g_err; }
 extern "C" int32_t gs_device_sm_count(void) { return gs_sm_count(); }
+
+extern "C" int gs_host_device_pointer(const void* host_ptr, void** dev_ptr) {
+  if (!host_ptr || !dev_ptr) {
+    gs_set_error("gs_host_device_pointer: null pointer");
+    return GS_ERR_ARG;
+  }
+  void* d = nullptr;
+  const cudaError_t e = cudaHostGetDevicePointer(&d, const_cast<void*>(host_ptr), 0);
+  if (e != cudaSuccess) {
+    (void)cudaGetLastError();
+    gs_set_error("gs_host_device_pointer: not page-locked mapped host memory");
+    return GS_ERR_ARG;
+  }
+  *dev_ptr = d;
+  return GS_OK;
+}

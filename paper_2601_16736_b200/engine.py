@@ -190,14 +190,30 @@ class StepEngine:
             if g.exp_avg is not None:  # per-group state (the row-record layout passes None)
                 _check_tensor(f"{g.name}.exp_avg", g.exp_avg, self.n_rows, w, self.device)
                 _check_tensor(f"{g.name}.exp_avg_sq", g.exp_avg_sq, self.n_rows, w, self.device)
+            grad_ptr = _ptr(g.grad)
             if need_grad:
                 if g.grad is None:
                     raise ConfigError(f"group {g.name} has no gradient")
-                _check_tensor(f"{g.name}.grad", g.grad, self.n_rows, w, self.device)
-            arr[i] = L.GsGroup(_ptr(g.param), _ptr(g.grad), _ptr(g.exp_avg), _ptr(g.exp_avg_sq),
+                if g.grad.device.type == "cpu":
+                    grad_ptr = self._host_mapped(f"{g.name}.grad", g.grad, w)
+                else:
+                    _check_tensor(f"{g.name}.grad", g.grad, self.n_rows, w, self.device)
+            arr[i] = L.GsGroup(_ptr(g.param), grad_ptr, _ptr(g.exp_avg), _ptr(g.exp_avg_sq),
                                w, g.role, float(np.float32(g.lr)))
         self._group_cache_key, self._group_cache = key, arr
         return arr
+
+    def _host_mapped(self, name: str, t: torch.Tensor, width: int) -> int:
+        """Pinned host gradients are read zero-copy by the step kernel: only
+        the visible rows' bytes cross PCIe (``gs_host_device_pointer``)."""
+        if not t.is_pinned():
+            raise ConfigError(f"{name} is in pageable host memory; pass a CUDA tensor or a "
+                              "pinned (page-locked) host tensor")
+        _check_tensor(name, t, self.n_rows, width, t.device)
+        dptr = L.C.c_void_p()
+        L.check(self.lib.gs_host_device_pointer(t.data_ptr(), L.C.byref(dptr)),
+                "gs_host_device_pointer")
+        return int(dptr.value)
 
     # ------------------------------------------------------------- compaction
     def compact(self, vis: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor]:

@@ -308,6 +308,9 @@ class AdamWGS:
                             (pipeline.py:311-315); lambda 0 is plain Sparse Adam.
         coupled-adam        adam_step_sync over every row, coupled terms on
                             every row (pipeline.py:305-310).
+        ``grads``: name -> gradient tensor, on the device or in pinned host
+        memory; pinned host gradients are gathered zero-copy by the step
+        kernel, so only the visible rows cross PCIe.
         ``n_visible``: device int32 [1] global N_v (index-sharded multi-GPU).
         ``densify_scale``: with :meth:`enable_densify_stats`, accumulate
         ||grad_position|| * densify_scale and a count per stepped row, fused

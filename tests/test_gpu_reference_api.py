@@ -536,3 +536,36 @@ def test_state_views_and_checkpoint_roundtrip():
     opt2 = AdamWGS(S.param_groups({k: p.clone() for k, p in params.items()}), mode="adamw-gs")
     opt2.load_state_dict(sd)
     assert torch.equal(opt2.state.record, opt.state.record)
+
+
+@pytest.mark.parametrize("check", ["fused", "strict"])
+def test_pinned_host_grads_zero_copy_identical(check):
+    """Gradients in pinned host memory are read zero-copy by the kernel and
+    give bitwise the same step as device-resident gradients."""
+    from paper_2601_16736_b200 import synthetic as S
+    from paper_2601_16736_b200.engine import ConfigError
+    from paper_2601_16736_b200.optimizer import AdamWGS
+    cfg = S.WorkloadConfig(n=20_003, p_vis=0.3, seed=4)
+    host = S.make_params(cfg)
+    outs = []
+    for where in ("device", "pinned"):
+        params = {k: torch.from_numpy(v).to("cuda:0") for k, v in host.items()}
+        opt = AdamWGS(S.param_groups(params), mode="adamw-gs", lambda_o=1e-3, lambda_s=1e-5,
+                      check=check)
+        for s in range(3):
+            vis = S.visibility(cfg, s)
+            g = S.step_grads(cfg, s, vis)
+            if where == "device":
+                grads = {k: torch.from_numpy(x).to("cuda:0") for k, x in g.items()}
+            else:
+                grads = {k: torch.from_numpy(x).pin_memory() for k, x in g.items()}
+            opt.step(torch.from_numpy(vis).to("cuda:0"), cfg.n_pixels, grads=grads)
+        torch.cuda.synchronize()
+        outs.append(({k: v.cpu() for k, v in params.items()}, opt.state.record.cpu()))
+    for k in outs[0][0]:
+        assert torch.equal(outs[0][0][k], outs[1][0][k]), k
+    assert torch.equal(outs[0][1], outs[1][1])
+    # pageable host memory is refused, not silently copied
+    with pytest.raises(ConfigError):
+        opt.step(torch.from_numpy(vis).to("cuda:0"), cfg.n_pixels,
+                 grads={k: torch.from_numpy(x) for k, x in g.items()})
