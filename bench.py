@@ -87,6 +87,9 @@ def parse():
                     help="launch the timed steps eagerly instead of as one CUDA graph")
     ap.add_argument("--layout", default="rows", choices=["rows", "groups"],
                     help="optimizer-state layout (row records or per-group tensors)")
+    ap.add_argument("--params", default="record", choices=["record", "attr"],
+                    help="parameter / gradient HBM layout: attribute views of one "
+                         "row-interleaved record (records.py) or one tensor per attribute")
     return ap.parse_args()
 
 
@@ -107,11 +110,11 @@ def measured_hbm_peak():
         return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
-def traffic_from_profiles(workload, mask, p_vis):
+def traffic_from_profiles(workload, mask, p_vis, params):
     p = ROOT / "profiles" / "traffic.json"
     try:
         d = json.loads(p.read_text())
-        return d.get(f"{workload}/{mask}/{p_vis:g}")
+        return d.get(f"{workload}/{mask}/{p_vis:g}/{params}")
     except Exception:
         return None
 
@@ -270,6 +273,9 @@ def workload_config(args, wl, p_vis, world):
                     "interval": RSR_INTERVAL} if wl["rsr"] else None,
             "reset_fraction": wl["reset"] or None, "check": args.check,
             "state_layout": args.layout,
+            "param_layout": "record (attribute views of one (n, 60) fp32 row record, "
+                            "gradients likewise)" if args.params == "record"
+                            else "one tensor per attribute",
             "l2": "inputs larger than L2 (working set >> 126 MB)" if n >= 1_000_000 else
                   "L2 flushed between timed steps",
             "parallelism": f"index-sharded x{world}",
@@ -282,6 +288,7 @@ def ours(args, wl, p_vis):
     import torch
     import torch.distributed as dist
 
+    from paper_2601_16736_b200 import records as R
     from paper_2601_16736_b200 import synthetic as S
     from paper_2601_16736_b200.optimizer import AdamWGS
     from paper_2601_16736_b200.sampling import StSSchedule, shard_rows, stream, stss_sample
@@ -297,12 +304,16 @@ def ours(args, wl, p_vis):
     cfg = S.WorkloadConfig(n=n, p_vis=p_vis, mask_family=args.mask, seed=args.seed * 1000 + rank,
                            lambda_o=wl["lo"], lambda_s=wl["ls"])
     params = S.make_params_device(cfg, dev)
+    if args.params == "record":
+        _, params = R.pack(params)
     opt = AdamWGS(S.param_groups(params), mode=wl["mode"], lambda_o=wl["lo"], lambda_s=wl["ls"],
                   check=args.check, errors="defer", state_layout=args.layout)
     total_steps = args.warmup + args.steps
     masks = [S.visibility_device(cfg, s, dev) for s in range(total_steps)]
     n_vis = torch.stack([m.sum() for m in masks]).cpu().numpy().astype(np.int64)
     grad_sets = [S.grads_device(cfg, s, dev) for s in range(2)]
+    if args.params == "record":
+        grad_sets = [R.pack(g)[1] for g in grad_sets]
     # RSR / relocation samples are host-drawn with the reference RNG contract
     # (optimizer.py:379-386, rng.py:17-30) and uploaded before timing.
     events = {}
@@ -447,7 +458,8 @@ def ours(args, wl, p_vis):
             "config": workload_config(args, wl, p_vis, world),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak,
-                         "traffic": traffic_from_profiles(args.workload, args.mask, p_vis),
+                         "traffic": traffic_from_profiles(args.workload, args.mask, p_vis,
+                                                          args.params),
                          "kernel": "gs::step_ws_kernel<LayoutSH3> (K2, warp-specialised, via gs_step_rows)"
                                    if args.layout == "rows" else "gs::step_kernel (K2, gs_step)",
                          "peak_source": peak_src,
@@ -494,9 +506,18 @@ def run_e2e(args, opt, cfg, dev, world, masks, n_vis):
     import torch
     import torch.distributed as dist
 
-    host_grads = {k: torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
-                  for k, t in opt_grads_like(opt).items()}
-    dev_grads = {k: torch.empty_like(t) for k, t in opt_grads_like(opt).items()}
+    from paper_2601_16736_b200 import records as R
+
+    like = opt_grads_like(opt)
+    if args.params == "record":
+        # one pinned gradient record: a visible row is one 240-byte PCIe read
+        host_rec, host_grads = R.pack({k: torch.zeros(t.shape) for k, t in like.items()},
+                                      pin_memory=True)
+        dev_grads = R.views_like(torch.empty_like(host_rec, device=dev), like)
+    else:
+        host_grads = {k: torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+                      for k, t in like.items()}
+        dev_grads = {k: torch.empty_like(t) for k, t in like.items()}
     for k, t in host_grads.items():
         t.copy_(torch.randn(t.shape) * 1e-4)
     host_mask = torch.empty(masks[0].shape, dtype=torch.bool, pin_memory=True)
@@ -505,6 +526,9 @@ def run_e2e(args, opt, cfg, dev, world, masks, n_vis):
     stats_host = torch.empty(10, dtype=torch.float64, pin_memory=True)
     row_bytes = sum(t[0].numel() * 4 for t in host_grads.values())
     dense = sum(t.numel() * 4 for t in host_grads.values())
+    host_dense = ([host_rec] if args.params == "record" else list(host_grads.values()))
+    dev_dense = ([dev_grads[next(iter(dev_grads))]._base] if args.params == "record"
+                 else list(dev_grads.values()))
     d2h = stats_host.numel() * 8
     nv = float(host_mask.sum())
 
@@ -513,8 +537,8 @@ def run_e2e(args, opt, cfg, dev, world, masks, n_vis):
         if zero_copy:
             grads = host_grads
         else:
-            for k in dev_grads:
-                dev_grads[k].copy_(host_grads[k], non_blocking=True)
+            for d, h in zip(dev_dense, host_dense):
+                d.copy_(h, non_blocking=True)
             grads = dev_grads
         opt.step(dev_mask, 1_000_000, grads=grads)
         stats_host.copy_(opt.engine.stats, non_blocking=True)

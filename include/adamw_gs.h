@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define GS_ABI_VERSION 1
+#define GS_ABI_VERSION 2
 #define GS_MAX_GROUPS 8
 
 /* status codes */
@@ -87,6 +87,13 @@ typedef struct gs_group {
   int64_t width;
   int32_t role; /* GS_ROLE_* */
   float lr;     /* effective learning rate of this step */
+  /* Row strides (elements) of param and grad; 0 = width (dense rows).  A
+   * stride > width lets the attributes be views of one row-interleaved
+   * parameter record (and its gradient record): every visible row is then
+   * one contiguous run in HBM instead of one narrow piece per attribute.
+   * exp_avg / exp_avg_sq (per-group state layout) are always dense. */
+  int64_t param_stride;
+  int64_t grad_stride;
 } gs_group;
 
 typedef struct gs_step_cfg {
@@ -212,7 +219,9 @@ int gs_noise_perturb(float* position, const float* log_scale, const float* rotat
                      const float* opacity_logit, const uint8_t* alive, int64_t n, int32_t dims,
                      float lr_position, float eta_ratio, float lambda_mu, float lambda_t,
                      uint64_t seed, uint32_t iteration, float* delta_out, int32_t add_in_place,
-                     void* stream);
+                     const int64_t* row_strides, void* stream);
+/* row_strides: nullable; else 4 row strides (elements) of position,
+ * log_scale, rotation, opacity_logit (0 = dense), for record views. */
 
 size_t gs_step_rows_workspace_bytes(void);
 /* Select the (rows-in-flight, residency) variant of the SH-3 step kernel

@@ -13,7 +13,7 @@ from pathlib import Path
 
 LIB_PATH = Path(__file__).resolve().parent / "libadamw_gs_b200.so"
 
-GS_ABI_VERSION = 1
+GS_ABI_VERSION = 2
 GS_MAX_GROUPS = 8
 
 GS_OK = 0
@@ -37,7 +37,7 @@ class ExtensionMissing(RuntimeError):
 class GsGroup(C.Structure):
     _fields_ = [("param", C.c_void_p), ("grad", C.c_void_p), ("exp_avg", C.c_void_p),
                 ("exp_avg_sq", C.c_void_p), ("width", C.c_int64), ("role", C.c_int32),
-                ("lr", C.c_float)]
+                ("lr", C.c_float), ("param_stride", C.c_int64), ("grad_stride", C.c_int64)]
 
 
 class GsStepCfg(C.Structure):
@@ -84,7 +84,7 @@ SIGNATURES = {
     "gs_noise_perturb": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                    C.c_int64, C.c_int32, C.c_float, C.c_float, C.c_float,
                                    C.c_float, C.c_uint64, C.c_uint32, C.c_void_p, C.c_int32,
-                                   C.c_void_p]),
+                                   C.c_void_p, C.c_void_p]),
     "gs_step_rows_workspace_bytes": (C.c_size_t, []),
     "gs_set_rows_variant": (C.c_int32, [C.c_int32]),
     "gs_set_fixed_variant": (C.c_int32, [C.c_int32]),

@@ -46,13 +46,17 @@ __device__ __forceinline__ float sigmoidf_stable(float x) {
   return e / (1.0f + e);
 }
 
+struct RowStrides {
+  int64_t x, y, z, w;  // position, log_scale, rotation, opacity_logit
+};
+
 template <int D>
 __global__ void __launch_bounds__(256)
     noise_kernel(float* __restrict__ pos, const float* __restrict__ kappa,
                  const float* __restrict__ rot, const float* __restrict__ tau,
                  const uint8_t* __restrict__ alive, int64_t n, float coef, float lambda_mu,
                  float lambda_t, uint2 key, uint32_t iteration, float* __restrict__ delta_out,
-                 int add) {
+                 int add, RowStrides rs) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     float d[D];
@@ -63,20 +67,21 @@ __global__ void __launch_bounds__(256)
           make_uint4((uint32_t)i, (uint32_t)(i >> 32), iteration, 0x6e6f6973u /* "nois" */), key);
       const float2 g01 = box_muller(rnd.x, rnd.y);
       const float2 g23 = box_muller(rnd.z, rnd.w);
-      const float o = sigmoidf_stable(tau[i]);
+      const float o = sigmoidf_stable(tau[i * rs.w]);
       const float gate = sigmoidf_stable(-lambda_mu * (o - lambda_t));
       const float a = -coef * gate;
       if (D == 2) {
-        const float e0 = expf(2.0f * kappa[2 * i]), e1 = expf(2.0f * kappa[2 * i + 1]);
+        const float e0 = expf(2.0f * kappa[i * rs.y]), e1 = expf(2.0f * kappa[i * rs.y + 1]);
         float s, c;
-        sincosf(rot[i], &s, &c);
+        sincosf(rot[i * rs.z], &s, &c);
         const float sxx = c * c * e0 + s * s * e1;
         const float syy = s * s * e0 + c * c * e1;
         const float sxy = c * s * (e0 - e1);
         d[0] = a * (sxx * g01.x + sxy * g01.y);
         d[1] = a * (sxy * g01.x + syy * g01.y);
       } else {
-        const float4 q4 = reinterpret_cast<const float4*>(rot)[i];
+        const float* qp = rot + i * rs.z;
+        const float4 q4 = make_float4(qp[0], qp[1], qp[2], qp[3]);
         const float qn = rsqrtf(q4.x * q4.x + q4.y * q4.y + q4.z * q4.z + q4.w * q4.w);
         const float w = q4.x * qn, x = q4.y * qn, y = q4.z * qn, z = q4.w * qn;
         const float Rm[3][3] = {{1.f - 2.f * (y * y + z * z), 2.f * (x * y - w * z), 2.f * (x * z + w * y)},
@@ -86,7 +91,7 @@ __global__ void __launch_bounds__(256)
         float u[3];
 #pragma unroll
         for (int r = 0; r < 3; ++r)  // u = S^2 R^T gamma
-          u[r] = expf(2.0f * kappa[3 * i + r]) * (Rm[0][r] * g[0] + Rm[1][r] * g[1] + Rm[2][r] * g[2]);
+          u[r] = expf(2.0f * kappa[i * rs.y + r]) * (Rm[0][r] * g[0] + Rm[1][r] * g[1] + Rm[2][r] * g[2]);
 #pragma unroll
         for (int r = 0; r < 3; ++r) d[r] = a * (Rm[r][0] * u[0] + Rm[r][1] * u[1] + Rm[r][2] * u[2]);
       }
@@ -94,7 +99,7 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
     for (int k = 0; k < D; ++k) {
       if (delta_out) delta_out[D * i + k] = d[k];
-      if (add) pos[D * i + k] += d[k];
+      if (add) pos[i * rs.x + k] += d[k];
     }
   }
 }
@@ -106,16 +111,23 @@ extern "C" int gs_noise_perturb(float* position, const float* log_scale, const f
                                 int32_t dims, float lr_position, float eta_ratio,
                                 float lambda_mu, float lambda_t, uint64_t seed,
                                 uint32_t iteration, float* delta_out, int32_t add_in_place,
-                                void* stream) {
+                                const int64_t* row_strides, void* stream) {
   using namespace gs;
   if (n < 0 || !position || !log_scale || !rotation || !opacity_logit ||
       (dims != 2 && dims != 3) || (!delta_out && !add_in_place)) {
     gs_set_error("gs_noise_perturb: invalid arguments");
     return GS_ERR_ARG;
   }
-  if (dims == 3 && (reinterpret_cast<uintptr_t>(rotation) & 15u)) {
-    gs_set_error("gs_noise_perturb: quaternions must be 16-byte aligned");
-    return GS_ERR_ALIGN;
+  const int64_t dense[4] = {dims, dims, dims == 2 ? 1 : 4, 1};
+  RowStrides rs;
+  int64_t* rp = &rs.x;
+  for (int j = 0; j < 4; ++j) {
+    rp[j] = (row_strides && row_strides[j] != 0) ? row_strides[j] : dense[j];
+    if (rp[j] < dense[j]) {
+      gs_set_error("gs_noise_perturb: row stride %d (%lld) below the row width", j,
+                   (long long)rp[j]);
+      return GS_ERR_ARG;
+    }
   }
   if (n == 0) return GS_OK;
   const uint2 key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
@@ -125,10 +137,10 @@ extern "C" int gs_noise_perturb(float* position, const float* log_scale, const f
   if (dims == 2)
     noise_kernel<2><<<grid, 256, 0, s>>>(position, log_scale, rotation, opacity_logit, alive, n,
                                          coef, lambda_mu, lambda_t, key, iteration, delta_out,
-                                         add_in_place);
+                                         add_in_place, rs);
   else
     noise_kernel<3><<<grid, 256, 0, s>>>(position, log_scale, rotation, opacity_logit, alive, n,
                                          coef, lambda_mu, lambda_t, key, iteration, delta_out,
-                                         add_in_place);
+                                         add_in_place, rs);
   return gs_check_launch("gs_noise_perturb");
 }

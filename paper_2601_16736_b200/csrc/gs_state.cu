@@ -18,7 +18,22 @@ struct GroupPtrs {
   int width;
   int role;
   float lr;
+  int64_t ps;  // param row stride (elements)
+  int64_t gs;  // grad row stride
 };
+
+__host__ __forceinline__ GroupPtrs group_ptrs(const gs_group& g, bool with_grad, bool with_state,
+                                              float lr) {
+  return GroupPtrs{g.param, with_grad ? g.grad : nullptr, with_state ? g.exp_avg : nullptr,
+                   with_state ? g.exp_avg_sq : nullptr, (int)g.width, g.role, lr,
+                   g.param_stride ? g.param_stride : g.width,
+                   g.grad_stride ? g.grad_stride : g.width};
+}
+
+static bool strides_ok(const gs_group& g) {
+  return (g.param_stride == 0 || g.param_stride >= g.width) &&
+         (g.grad_stride == 0 || g.grad_stride >= g.width);
+}
 
 struct GroupSet {
   GroupPtrs g[GS_MAX_GROUPS];
@@ -35,11 +50,11 @@ static int fill_groups(const gs_group* groups, int32_t n_groups, GroupSet& S, co
   for (int i = 0; i < n_groups; ++i) {
     const gs_group& g = groups[i];
     if ((need_state && (!g.exp_avg || !g.exp_avg_sq)) || (need_grad && !g.grad) || g.width < 1 ||
-        g.width > 4096) {
+        g.width > 4096 || !strides_ok(g)) {
       gs_set_error("%s: group %d invalid", who, i);
       return GS_ERR_ARG;
     }
-    S.g[i] = GroupPtrs{g.param, g.grad, g.exp_avg, g.exp_avg_sq, (int)g.width, g.role, g.lr};
+    S.g[i] = group_ptrs(g, true, true, g.lr);
   }
   return GS_OK;
 }
@@ -65,9 +80,10 @@ __global__ void __launch_bounds__(kThreads)
     const int W = G.width;
     const int64_t total = n_rows * W;
     for (int64_t e = tid0; e < total; e += stride) {
-      if (!isfinite(__ldg(G.grad + e))) {
+      const int64_t row = e / W;
+      if (!isfinite(__ldg(G.grad + row * G.gs + (e - row * W)))) {
         flag |= 1;
-        if (bad_rows) mark_row(bad_rows, e / W, 1);
+        if (bad_rows) mark_row(bad_rows, row, 1);
       }
     }
     const double lam = G.role == GS_ROLE_OPACITY ? lam_op : G.role == GS_ROLE_SCALE ? lam_sc : 0.0;
@@ -75,7 +91,7 @@ __global__ void __launch_bounds__(kThreads)
       const int64_t tot = n_list * W;
       for (int64_t e = tid0; e < tot; e += stride) {
         const int64_t row = __ldg(rows + e / W);
-        if (domain_bad(G.role, G.param[row * W + e % W])) {
+        if (domain_bad(G.role, G.param[row * G.ps + e % W])) {
           flag |= 2;
           if (bad_rows) mark_row(bad_rows, row, 2);
         }
@@ -177,7 +193,7 @@ __global__ void __launch_bounds__(kThreads)
         m_rt = fmax(m_rt, rt);
       }
       if (G.role == GS_ROLE_OPACITY && G.width == 1 && G.param != nullptr)
-        acc[1] += __ldg(G.param + e) > active_logit;
+        acc[1] += __ldg(G.param + e * G.ps) > active_logit;
     }
     acc[2 + 5 * gi + 0] = s_sq;
     acc[2 + 5 * gi + 1] = m_sq;
@@ -263,7 +279,7 @@ __global__ void __launch_bounds__(kThreads)
         m_rt = fmax(m_rt, rt);
       }
       if (G.role == GS_ROLE_OPACITY && W == 1 && G.param != nullptr)
-        acc[1] += __ldg(G.param + e) > active_logit;
+        acc[1] += __ldg(G.param + row * G.ps) > active_logit;
     }
     acc[2 + 5 * gi + 0] = s_sq;
     acc[2 + 5 * gi + 1] = m_sq;
@@ -317,7 +333,7 @@ __global__ void __launch_bounds__(kThreads)
       const float vh = __fmul_rn(mv.y, bc.y);
       const float den = __fadd_rn(__fsqrt_rn(vh), eps);
       const float upd = __fdiv_rn(__fmul_rn(S.g[gi].lr, mh), den);
-      float* p = S.g[gi].param + (int64_t)row * W + c;
+      float* p = S.g[gi].param + (int64_t)row * S.g[gi].ps + c;
       *p = __fsub_rn(*p, upd);
     }
   }
@@ -386,9 +402,8 @@ extern "C" int gs_stats_all_rows(const gs_group* groups, int32_t n_groups, int64
   S.n = n_groups;
   int P = 0;
   for (int i = 0; i < n_groups; ++i) {
-    S.g[i] = GroupPtrs{groups[i].param, nullptr, nullptr, nullptr, (int)groups[i].width,
-                       groups[i].role, 0.f};
-    if (groups[i].width < 1) {
+    S.g[i] = group_ptrs(groups[i], false, false, 0.f);
+    if (groups[i].width < 1 || !strides_ok(groups[i])) {
       gs_set_error("gs_stats_all_rows: group %d invalid", i);
       return GS_ERR_ARG;
     }
@@ -526,13 +541,12 @@ extern "C" int gs_aiu_apply_rows(const gs_group* groups, int32_t n_groups, float
   S.n = n_groups;
   int P = 0;
   for (int i = 0; i < n_groups; ++i) {
-    if (!groups[i].param || groups[i].width < 1) {
+    if (!groups[i].param || groups[i].width < 1 || !strides_ok(groups[i])) {
       gs_set_error("gs_aiu_apply_rows: group %d invalid", i);
       return GS_ERR_ARG;
     }
     // lr carries fl32(lr * eta), set by the caller
-    S.g[i] = GroupPtrs{groups[i].param, nullptr, nullptr, nullptr, (int)groups[i].width,
-                       groups[i].role, groups[i].lr};
+    S.g[i] = group_ptrs(groups[i], false, false, groups[i].lr);
     P += (int)groups[i].width;
   }
   int rc = record_args(record, record_stride, P, "gs_aiu_apply_rows");

@@ -32,6 +32,8 @@ struct GroupDev {
   int role;
   float lr;
   int pad;
+  int64_t ps;  // param / grad row strides (elements)
+  int64_t gs;
 };
 
 struct StepParams {
@@ -120,10 +122,9 @@ __global__ void __launch_bounds__(kThreads, kStepBlocksPerSM) step_kernel(const 
         int lr = tid / W, lc = tid % W;
         for (int e = tid; e < E; e += kThreads) {
           const int32_t r = s_row[lr];
-          const int64_t off = (int64_t)r * W + lc;
-          const float gv = __ldg(G.grad + off);
+          const float gv = __ldg(G.grad + (int64_t)r * G.gs + lc);
           int bad = finitef(gv) ? 0 : 1;
-          if (dom && domain_bad(G.role, G.param[off])) bad |= 2;
+          if (dom && domain_bad(G.role, G.param[(int64_t)r * G.ps + lc])) bad |= 2;
           if (bad) atomicOr(&s_bad[lr], bad);
           lc += dr;
           lr += dq;
@@ -142,7 +143,7 @@ __global__ void __launch_bounds__(kThreads, kStepBlocksPerSM) step_kernel(const 
         P.clock[row] = tn;
         if (P.D.group >= 0) {
           const GroupDev& DG = P.g[P.D.group];
-          densify_row(P.D, (uint32_t)row, DG.grad + (int64_t)row * DG.width, DG.width, 1);
+          densify_row(P.D, (uint32_t)row, DG.grad + (int64_t)row * DG.gs, DG.width, 1);
         }
         const int tb = T::kDense ? P.global_t : tn;
         s_bc[tid] = bias_factors(P.lut, P.lut_len, tb, P.beta1, P.beta2);
@@ -173,9 +174,10 @@ __global__ void __launch_bounds__(kThreads, kStepBlocksPerSM) step_kernel(const 
         if (s_bad[this_lr] != 0) continue;
         const int32_t r = s_row[this_lr];
         const int64_t off = (int64_t)r * W + this_lc;
+        const int64_t poff = (int64_t)r * G.ps + this_lc;
         const float2 bc = s_bc[this_lr];
-        const float th = G.param[off];
-        const float gr = __ldg(G.grad + off);
+        const float th = G.param[poff];
+        const float gr = __ldg(G.grad + (int64_t)r * G.gs + this_lc);
         const float mm = G.m[off];
         const float vv = G.v[off];
         float tn, mn, vn, ex;
@@ -194,7 +196,7 @@ __global__ void __launch_bounds__(kThreads, kStepBlocksPerSM) step_kernel(const 
           c_apre += th > P.active_logit;
           c_apost += tn > P.active_logit;
         }
-        G.param[off] = tn;
+        G.param[poff] = tn;
         G.m[off] = mn;
         G.v[off] = vn;
       }
@@ -285,11 +287,15 @@ extern "C" int gs_step(const gs_group* groups, int32_t n_groups, const gs_step_c
   StepParams P{};
   for (int i = 0; i < n_groups; ++i) {
     const gs_group& g = groups[i];
-    if (!g.param || !g.grad || !g.exp_avg || !g.exp_avg_sq || g.width < 1 || g.width > 4096) {
+    if (!g.param || !g.grad || !g.exp_avg || !g.exp_avg_sq || g.width < 1 || g.width > 4096 ||
+        (g.param_stride != 0 && g.param_stride < g.width) ||
+        (g.grad_stride != 0 && g.grad_stride < g.width)) {
       gs_set_error("gs_step: group %d invalid", i);
       return GS_ERR_ARG;
     }
-    P.g[i] = GroupDev{g.param, g.grad, g.exp_avg, g.exp_avg_sq, (int)g.width, g.role, g.lr, 0};
+    P.g[i] = GroupDev{g.param, g.grad, g.exp_avg, g.exp_avg_sq, (int)g.width, g.role, g.lr, 0,
+                      g.param_stride ? g.param_stride : g.width,
+                      g.grad_stride ? g.grad_stride : g.width};
   }
   P.n_groups = n_groups;
   P.check = cfg->check;

@@ -43,6 +43,8 @@ struct RowGroup {
   int role;
   float lr;
   int offset;  // first element of the group in the record
+  int ps;      // param / grad row strides (elements)
+  int gs;
 };
 
 struct RowParams {
@@ -77,7 +79,8 @@ constexpr int kRowMaxBlocksPerSM = 8;  // workspace sizing over all variants
 struct Slot {
   float* param;
   const float* grad;
-  int width;
+  int ps;  // row strides of param / grad
+  int gs;
   int col;
   int role;  // -1 inactive, -2 clock, else GS_ROLE_*
   float lr;
@@ -118,7 +121,7 @@ __global__ void __launch_bounds__(kRowThreads, MINB)
 #pragma unroll
   for (int j = 0; j < J; ++j) {
     const int s = q + L * j;
-    Slot x{nullptr, nullptr, 1, 0, -1, 0.f};
+    Slot x{nullptr, nullptr, 1, 1, 0, -1, 0.f};
     if (s == P.P) {
       x.role = -2;
     } else if (s < P.P) {
@@ -127,7 +130,8 @@ __global__ void __launch_bounds__(kRowThreads, MINB)
         if (s >= G.offset && s < G.offset + G.width) {
           x.param = G.param;
           x.grad = G.grad;
-          x.width = G.width;
+          x.ps = G.ps;
+          x.gs = G.gs;
           x.col = s - G.offset;
           x.role = G.role;
           x.lr = G.lr;
@@ -169,9 +173,8 @@ __global__ void __launch_bounds__(kRowThreads, MINB)
         if (valid[r] && sl[j].role != -1) {
           mv[r][j] = *reinterpret_cast<const float2*>(rec + 2 * s);
           if (sl[j].role >= 0) {
-            const int64_t off = (int64_t)row[r] * sl[j].width + sl[j].col;
-            th[r][j] = sl[j].param[off];
-            gr[r][j] = __ldg(sl[j].grad + off);
+            th[r][j] = sl[j].param[(int64_t)row[r] * sl[j].ps + sl[j].col];
+            gr[r][j] = __ldg(sl[j].grad + (int64_t)row[r] * sl[j].gs + sl[j].col);
           }
         }
       }
@@ -214,7 +217,7 @@ __global__ void __launch_bounds__(kRowThreads, MINB)
         ++c_vis;
         if (!row_bad && P.D.group >= 0) {
           const RowGroup& DG = P.g[P.D.group];
-          densify_row(P.D, (uint32_t)row[r], DG.grad + (int64_t)row[r] * DG.width, DG.width, 1);
+          densify_row(P.D, (uint32_t)row[r], DG.grad + (int64_t)row[r] * DG.gs, DG.width, 1);
         }
         if (!row_bad) ++c_step;
         else if (b1) ++c_badg;
@@ -249,8 +252,7 @@ __global__ void __launch_bounds__(kRowThreads, MINB)
           c_apre += thv > P.active_logit;
           c_apost += tn_th > P.active_logit;
         }
-        const int64_t off = (int64_t)row[r] * sl[j].width + sl[j].col;
-        sl[j].param[off] = tn_th;
+        sl[j].param[(int64_t)row[r] * sl[j].ps + sl[j].col] = tn_th;
         *reinterpret_cast<float2*>(rec + 2 * s) = make_float2(mn, vn);
       }
     }
@@ -393,11 +395,15 @@ extern "C" int gs_step_rows(const gs_group* groups, int32_t n_groups, const gs_s
   int off = 0;
   for (int i = 0; i < n_groups; ++i) {
     const gs_group& g = groups[i];
-    if (!g.param || !g.grad || g.width < 1 || g.width > 127) {
+    if (!g.param || !g.grad || g.width < 1 || g.width > 127 ||
+        (g.param_stride != 0 && (g.param_stride < g.width || g.param_stride > INT32_MAX)) ||
+        (g.grad_stride != 0 && (g.grad_stride < g.width || g.grad_stride > INT32_MAX))) {
       gs_set_error("gs_step_rows: group %d invalid", i);
       return GS_ERR_ARG;
     }
-    P.g[i] = RowGroup{g.param, g.grad, (int)g.width, g.role, g.lr, off};
+    P.g[i] = RowGroup{g.param, g.grad, (int)g.width, g.role, g.lr, off,
+                      (int)(g.param_stride ? g.param_stride : g.width),
+                      (int)(g.grad_stride ? g.grad_stride : g.width)};
     off += (int)g.width;
   }
   if (record_stride < 2 * (off + 1) || (record_stride & 1)) {

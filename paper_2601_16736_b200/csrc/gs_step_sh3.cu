@@ -45,7 +45,8 @@ struct FixedGroup {
   float* param;
   const float* grad;
   float lr;
-  int pad;
+  uint32_t ps;  // param / grad row strides (elements; == width unless record views)
+  uint32_t gs;
 };
 
 struct FixedParams {
@@ -64,6 +65,13 @@ struct FixedParams {
   int64_t max_rows;
   float* record;
   int64_t stride;
+  // row-interleaved parameter / gradient records (REC kernels): the group
+  // pointers are prec + OFF(g) / grec + OFF(g) with row strides prs / grs
+  const float* prec;
+  const float* grec;
+  uint32_t prs;
+  uint32_t grs;
+  int grec_ca;  // gradient record copies through L1 (.ca): host-mapped gradients
   double* stats_out;
   double* partials;
   unsigned int* counter;
@@ -275,6 +283,10 @@ __device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async16_ca(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
@@ -822,12 +834,13 @@ __device__ __forceinline__ void named_sync(int id, int nthreads) {
 template <class L, int R>
 struct WsStage {
   static constexpr int kSlots = L::P + 1;
+  static constexpr int kPL = (L::P + 3) & ~3;  // staged theta / grad row (16-byte pieces)
   static constexpr int kRec = R * kSlots * 8;
-  static constexpr int kTh = R * L::P * 4;
+  static constexpr int kTh = R * kPL * 4;
   static constexpr int kBytes = kRec + 2 * kTh + R * 4;  // + row ids
 };
 
-template <class L, int MODE, bool STRICT, int R, int S, int NPW, int NCW, int MINB>
+template <class L, int MODE, bool STRICT, int R, int S, int NPW, int NCW, int MINB, bool REC>
 __global__ void __launch_bounds__((NPW + NCW) * 32, MINB) step_ws_kernel(const FixedParams P) {
   constexpr bool kDense = MODE == GS_MODE_COUPLED_ADAM;
   constexpr bool kCoupled = MODE == GS_MODE_COUPLED_ADAM || MODE == GS_MODE_SPARSE_ADAM;
@@ -856,6 +869,13 @@ __global__ void __launch_bounds__((NPW + NCW) * 32, MINB) step_ws_kernel(const F
     return rem <= 0 ? 0 : (rem < R ? (int)rem : R);
   };
   auto stage = [&](int st) { return smem + st * ST::kBytes; };
+  constexpr int PL = ST::kPL;
+  // staged theta / grad of chunk element i (row r) of group gg: group-major
+  // for per-attribute gathers, row-major (one 16-byte-piece copy per record
+  // row) for record views
+  auto sidx = [](int gg, int i, int r) -> int {
+    return REC ? r * PL + L::OFF(gg) + (i - r * L::W(gg)) : R * L::OFF(gg) + i;
+  };
 
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
@@ -902,20 +922,33 @@ __global__ void __launch_bounds__((NPW + NCW) * 32, MINB) step_ws_kernel(const F
                    P.record + (size_t)srows[r] * P.stride + 4 * kk);
       }
       float* sth = reinterpret_cast<float*>(sb + ST::kRec);
-      float* sg = sth + R * L::P;
-      using PS = ChunkShape<L, R, NP>;
+      float* sg = sth + R * PL;
+      if (REC) {
+        constexpr int kRowPieces = PL / 4;
+        for (int p = pt; p < nv * kRowPieces; p += NP) {
+          const int r = p / kRowPieces;
+          const int q = p - r * kRowPieces;
+          cp_async16(sth + r * PL + 4 * q, P.prec + srows[r] * P.prs + 4 * q);
+          if (P.grec_ca)
+            cp_async16_ca(sg + r * PL + 4 * q, P.grec + srows[r] * P.grs + 4 * q);
+          else
+            cp_async16(sg + r * PL + 4 * q, P.grec + srows[r] * P.grs + 4 * q);
+        }
+      } else {
+        using PS = ChunkShape<L, R, NP>;
 #pragma unroll
-      for (int gg = 0; gg < L::G; ++gg) {
-        const int W = L::W(gg);
+        for (int gg = 0; gg < L::G; ++gg) {
+          const int W = L::W(gg);
 #pragma unroll
-        for (int kk = 0; kk < PS::rounds(gg); ++kk) {
-          const int i = kk * NP + ((pt + NP - (R * L::OFF(gg)) % NP) % NP);
-          const int r = i / W;
-          if (i < R * W && r < nv) {
-            const uint32_t off = srows[r] * (uint32_t)W + (uint32_t)(i - r * W);
-            const int e = R * L::OFF(gg) + i;
-            cp_async4(sth + e, P.g[gg].param + off);
-            cp_async4(sg + e, P.g[gg].grad + off);
+          for (int kk = 0; kk < PS::rounds(gg); ++kk) {
+            const int i = kk * NP + ((pt + NP - (R * L::OFF(gg)) % NP) % NP);
+            const int r = i / W;
+            if (i < R * W && r < nv) {
+              const uint32_t c = (uint32_t)(i - r * W);
+              const int e = R * L::OFF(gg) + i;
+              cp_async4(sth + e, P.g[gg].param + srows[r] * P.g[gg].ps + c);
+              cp_async4(sg + e, P.g[gg].grad + srows[r] * P.g[gg].gs + c);
+            }
           }
         }
       }
@@ -946,7 +979,7 @@ __global__ void __launch_bounds__((NPW + NCW) * 32, MINB) step_ws_kernel(const F
       const unsigned char* sb = stage(st);
       const float2* srec = reinterpret_cast<const float2*>(sb);
       const float* sth = reinterpret_cast<const float*>(sb + ST::kRec);
-      const float* sg = sth + R * L::P;
+      const float* sg = sth + R * PL;
       const uint32_t* srow = s_crow[st];
       if (!STRICT) {
 #pragma unroll
@@ -959,7 +992,7 @@ __global__ void __launch_bounds__((NPW + NCW) * 32, MINB) step_ws_kernel(const F
             const int i = kk * NC + ((t + NC - (R * L::OFF(gg)) % NC) % NC);
             const int r = i / W;
             if (i < R * W && r < nvalid) {
-              const int e = R * L::OFF(gg) + i;
+              const int e = sidx(gg, i, r);
               int bad = isfinite(sg[e]) ? 0 : 1;
               if ((role == GS_ROLE_OPACITY || role == GS_ROLE_SCALE) && lam != 0.f &&
                   domain_bad(role, sth[e]))
@@ -990,7 +1023,7 @@ __global__ void __launch_bounds__((NPW + NCW) * 32, MINB) step_ws_kernel(const F
 #pragma unroll
             for (int gg = 0; gg < L::G; ++gg)
               if (gg == P.D.group)
-                densify_row(P.D, s_crow[st][t], sg + R * L::OFF(gg) + t * L::W(gg), L::W(gg), 1);
+                densify_row(P.D, s_crow[st][t], sg + sidx(gg, t * L::W(gg), t), L::W(gg), 1);
           }
           ++c_step;
         } else if (bad & 1) {
@@ -1004,7 +1037,7 @@ __global__ void __launch_bounds__((NPW + NCW) * 32, MINB) step_ws_kernel(const F
         const int W = L::W(gg);
         const int role = L::ROLE(gg);
         const int c = i - r * W;
-        const int e = R * L::OFF(gg) + i;
+        const int e = sidx(gg, i, r);
         const uint32_t row = srow[r];
         const float2 mv = srec[r * SLOTS + L::OFF(gg) + c];
         const float th = sth[e];
@@ -1023,7 +1056,7 @@ __global__ void __launch_bounds__((NPW + NCW) * 32, MINB) step_ws_kernel(const F
           c_apre += th > P.active_logit;
           c_apost += tnv > P.active_logit;
         }
-        P.g[gg].param[row * (uint32_t)W + (uint32_t)c] = tnv;
+        P.g[gg].param[row * P.g[gg].ps + (uint32_t)c] = tnv;
         rec_base[(size_t)row * rec_stride2 + L::OFF(gg) + c] = make_float2(mn, vn);
       };
       if (!any_bad) {
@@ -1071,19 +1104,20 @@ __global__ void __launch_bounds__((NPW + NCW) * 32, MINB) step_ws_kernel(const F
                                                is_max, s_red);
 }
 
-template <class L, int MODE, bool STRICT, int R, int S, int NPW, int NCW, int MINB>
+template <class L, int MODE, bool STRICT, int R, int S, int NPW, int NCW, int MINB,
+          bool REC = false>
 void launch_ws(const FixedParams& P, int64_t max_rows, cudaStream_t s) {
   constexpr int bytes = S * WsStage<L, R>::kBytes;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(step_ws_kernel<L, MODE, STRICT, R, S, NPW, NCW, MINB>,
+    cudaFuncSetAttribute(step_ws_kernel<L, MODE, STRICT, R, S, NPW, NCW, MINB, REC>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     attr_set = true;
   }
   const int64_t chunks = (max_rows + R - 1) / R;
   const int grid =
       (int)std::max<int64_t>(1, std::min<int64_t>(chunks, (int64_t)gs_sm_count() * MINB));
-  step_ws_kernel<L, MODE, STRICT, R, S, NPW, NCW, MINB>
+  step_ws_kernel<L, MODE, STRICT, R, S, NPW, NCW, MINB, REC>
       <<<grid, (NPW + NCW) * 32, bytes, s>>>(P);
 }
 
@@ -1108,10 +1142,17 @@ void launch_fixed_v(const FixedParams& P, int64_t max_rows, cudaStream_t s) {
   step_fixed_kernel<L, MODE, STRICT, R, MINB, NT><<<grid, NT, 0, s>>>(P);
 }
 
+// kind: 0 dense per-attribute rows, 1 strided rows (per-element gathers),
+// 2 row-interleaved parameter + gradient records
 template <class L, int MODE, bool STRICT>
-void launch_fixed(const FixedParams& P, int64_t max_rows, cudaStream_t s) {
-  // the densification statistics are fused into the warp-specialised kernel only
-  const int variant = P.D.group >= 0 ? 0 : fixed_variant();
+void launch_fixed(const FixedParams& P, int64_t max_rows, int kind, cudaStream_t s) {
+  if (kind == 2) {
+    launch_ws<L, MODE, STRICT, 32, 3, 3, 8, 2, true>(P, max_rows, s);
+    return;
+  }
+  // the densification statistics and strided rows are handled by the
+  // warp-specialised kernel only
+  const int variant = (P.D.group >= 0 || kind != 0) ? 0 : fixed_variant();
   switch (variant) {
     case 1: launch_fixed_v<L, MODE, STRICT, 64, 2>(P, max_rows, s); return;
     case 2: launch_pipe<L, MODE, STRICT, 32, 2, 3>(P, max_rows, s); return;
@@ -1124,16 +1165,60 @@ void launch_fixed(const FixedParams& P, int64_t max_rows, cudaStream_t s) {
 }
 
 template <class L, bool STRICT>
-void dispatch_fixed(int mode, const FixedParams& P, int64_t max_rows, cudaStream_t s) {
+void dispatch_fixed(int mode, const FixedParams& P, int64_t max_rows, int kind, cudaStream_t s) {
   switch (mode) {
-    case GS_MODE_COUPLED_ADAM: launch_fixed<L, GS_MODE_COUPLED_ADAM, STRICT>(P, max_rows, s); break;
-    case GS_MODE_SPARSE_ADAM: launch_fixed<L, GS_MODE_SPARSE_ADAM, STRICT>(P, max_rows, s); break;
-    case GS_MODE_ADAMW_CONST: launch_fixed<L, GS_MODE_ADAMW_CONST, STRICT>(P, max_rows, s); break;
-    case GS_MODE_ADAMW_CONST_CLIP:
-      launch_fixed<L, GS_MODE_ADAMW_CONST_CLIP, STRICT>(P, max_rows, s);
+    case GS_MODE_COUPLED_ADAM:
+      launch_fixed<L, GS_MODE_COUPLED_ADAM, STRICT>(P, max_rows, kind, s);
       break;
-    default: launch_fixed<L, GS_MODE_ADAMW_GS, STRICT>(P, max_rows, s); break;
+    case GS_MODE_SPARSE_ADAM:
+      launch_fixed<L, GS_MODE_SPARSE_ADAM, STRICT>(P, max_rows, kind, s);
+      break;
+    case GS_MODE_ADAMW_CONST:
+      launch_fixed<L, GS_MODE_ADAMW_CONST, STRICT>(P, max_rows, kind, s);
+      break;
+    case GS_MODE_ADAMW_CONST_CLIP:
+      launch_fixed<L, GS_MODE_ADAMW_CONST_CLIP, STRICT>(P, max_rows, kind, s);
+      break;
+    default: launch_fixed<L, GS_MODE_ADAMW_GS, STRICT>(P, max_rows, kind, s); break;
   }
+}
+
+// 0 dense, 1 strided, 2 records (see launch_fixed); -1 if 32-bit element
+// offsets could overflow
+template <class L>
+int rows_kind(const gs_group* groups, int64_t max_rows, FixedParams& P) {
+  constexpr int PL = WsStage<L, 32>::kPL;
+  bool dense = true, prec = true, grec = true;
+  int64_t smax = 1;
+  const int64_t ps0 = groups[0].param_stride ? groups[0].param_stride : groups[0].width;
+  const int64_t gs0 = groups[0].grad_stride ? groups[0].grad_stride : groups[0].width;
+  for (int i = 0; i < L::G; ++i) {
+    const gs_group& g = groups[i];
+    const int64_t ps = g.param_stride ? g.param_stride : g.width;
+    const int64_t gs = g.grad_stride ? g.grad_stride : g.width;
+    dense = dense && ps == g.width && gs == g.width;
+    prec = prec && ps == ps0 && g.param == groups[0].param + L::OFF(i);
+    grec = grec && gs == gs0 && g.grad == groups[0].grad + L::OFF(i);
+    smax = std::max(smax, std::max(ps, gs));
+  }
+  if (max_rows * smax + smax >= (int64_t)UINT32_MAX) return -1;
+  if (dense) return 0;
+  prec = prec && ps0 >= PL && ps0 % 4 == 0 && (reinterpret_cast<uintptr_t>(groups[0].param) & 15u) == 0;
+  grec = grec && gs0 >= PL && gs0 % 4 == 0 && (reinterpret_cast<uintptr_t>(groups[0].grad) & 15u) == 0;
+  if (prec && grec) {
+    P.prec = groups[0].param;
+    P.grec = groups[0].grad;
+    P.prs = (uint32_t)ps0;
+    P.grs = (uint32_t)gs0;
+    cudaPointerAttributes a{};
+    const bool host = cudaPointerGetAttributes(&a, groups[0].grad) == cudaSuccess &&
+                      a.type == cudaMemoryTypeHost;
+    (void)cudaGetLastError();
+    const char* e = getenv("GS_GREC_CA");
+    P.grec_ca = e ? atoi(e) : (host ? 1 : 0);
+    return 2;
+  }
+  return 1;
 }
 
 template <class L>
@@ -1162,10 +1247,14 @@ int gs_step_fixed_try(const gs_group* groups, int32_t n_groups, const gs_step_cf
   using namespace gs;
   if (fixed_variant() < 0) return 0;  // fixed-layout path disabled
   if (!layout_matches<LayoutSH3>(groups, n_groups)) return 0;
-  if (max_rows * 45 >= (int64_t)UINT32_MAX) return 0;  // 32-bit element offsets
   FixedParams P{};
+  const int kind = rows_kind<LayoutSH3>(groups, max_rows, P);
+  if (kind < 0) return 0;  // 32-bit element offsets
   for (int i = 0; i < n_groups; ++i)
-    P.g[i] = FixedGroup{groups[i].param, groups[i].grad, groups[i].lr, 0};
+    P.g[i] = FixedGroup{
+        groups[i].param, groups[i].grad, groups[i].lr,
+        (uint32_t)(groups[i].param_stride ? groups[i].param_stride : groups[i].width),
+        (uint32_t)(groups[i].grad_stride ? groups[i].grad_stride : groups[i].width)};
   P.active_logit = cfg->active_logit;
   P.K = make_consts(cfg);
   P.lut = cfg->bias_lut;
@@ -1186,8 +1275,8 @@ int gs_step_fixed_try(const gs_group* groups, int32_t n_groups, const gs_step_cf
   P.counter = counter;
   cudaStream_t s = (cudaStream_t)stream;
   if (cfg->check == GS_CHECK_STRICT)
-    dispatch_fixed<LayoutSH3, true>(cfg->mode, P, max_rows, s);
+    dispatch_fixed<LayoutSH3, true>(cfg->mode, P, max_rows, kind, s);
   else
-    dispatch_fixed<LayoutSH3, false>(cfg->mode, P, max_rows, s);
+    dispatch_fixed<LayoutSH3, false>(cfg->mode, P, max_rows, kind, s);
   return 1;
 }

@@ -99,6 +99,10 @@ def _ptr(t: torch.Tensor | None) -> int | None:
     return None if t is None else t.data_ptr()
 
 
+def _strides(t: torch.Tensor | None):
+    return None if t is None else (tuple(t.shape), t.stride())
+
+
 def _stream_handle(device: torch.device) -> int:
     return torch.cuda.current_stream(device).cuda_stream
 
@@ -124,15 +128,36 @@ class GroupBinding:
         return max(1, int(np.prod(t.shape[1:]))) if t.dim() > 1 else 1
 
 
-def _check_tensor(name, t: torch.Tensor, n_rows: int, width: int, device, dtype=torch.float32):
+def row_stride(name, t: torch.Tensor, n_rows: int, width: int) -> int:
+    """Row stride (elements) of a tensor whose rows are each one dense run of
+    ``width`` values: a contiguous tensor (stride == width) or a view of a
+    row-interleaved record (stride > width)."""
+    if t.dim() == 0 or t.shape[0] != n_rows or t.numel() != n_rows * width:
+        raise ConfigError(f"{name} has shape {tuple(t.shape)}, expected {n_rows} rows x {width}")
+    expect = 1
+    for d in range(t.dim() - 1, 0, -1):
+        if t.shape[d] != 1 and t.stride(d) != expect:
+            raise ConfigError(f"{name}: the values of one row must be contiguous")
+        expect *= t.shape[d]
+    rs = t.stride(0) if n_rows > 1 else width
+    if rs < width:
+        raise ConfigError(f"{name}: row stride {rs} is below the row width {width}")
+    return int(rs)
+
+
+def _check_tensor(name, t: torch.Tensor, n_rows: int, width: int, device, dtype=torch.float32,
+                  strided: bool = False) -> int:
     if t.device != device:
         raise ConfigError(f"{name} is on {t.device}, expected {device}")
     if t.dtype != dtype:
         raise ConfigError(f"{name} has dtype {t.dtype}, expected {dtype}")
+    if strided:
+        return row_stride(name, t, n_rows, width)
     if not t.is_contiguous():
         raise ConfigError(f"{name} must be contiguous")
     if t.shape[0] != n_rows or t.numel() != n_rows * width:
         raise ConfigError(f"{name} has shape {tuple(t.shape)}, expected {n_rows} rows x {width}")
+    return width
 
 
 class StepEngine:
@@ -175,7 +200,8 @@ class StepEngine:
     # ------------------------------------------------------------------ groups
     def group_array(self, groups: list[GroupBinding], need_grad: bool = True):
         key = tuple((g.role, float(g.lr), _ptr(g.param), _ptr(g.grad), _ptr(g.exp_avg),
-                     _ptr(g.exp_avg_sq)) for g in groups)
+                     _ptr(g.exp_avg_sq), _strides(g.param), _strides(g.grad),
+                     None if g.grad is None else g.grad.device.type) for g in groups)
         if key == self._group_cache_key:
             return self._group_cache
         if not 1 <= len(groups) <= L.GS_MAX_GROUPS:
@@ -183,8 +209,10 @@ class StepEngine:
         arr = (L.GsGroup * len(groups))()
         for i, g in enumerate(groups):
             w = g.width
+            ps = gs = 0
             if g.param is not None:
-                _check_tensor(f"{g.name}.param", g.param, self.n_rows, w, self.device)
+                ps = _check_tensor(f"{g.name}.param", g.param, self.n_rows, w, self.device,
+                                   strided=True)
             elif need_grad:
                 raise ConfigError(f"group {g.name} has no parameter tensor")
             if g.exp_avg is not None:  # per-group state (the row-record layout passes None)
@@ -195,25 +223,26 @@ class StepEngine:
                 if g.grad is None:
                     raise ConfigError(f"group {g.name} has no gradient")
                 if g.grad.device.type == "cpu":
-                    grad_ptr = self._host_mapped(f"{g.name}.grad", g.grad, w)
+                    grad_ptr, gs = self._host_mapped(f"{g.name}.grad", g.grad, w)
                 else:
-                    _check_tensor(f"{g.name}.grad", g.grad, self.n_rows, w, self.device)
+                    gs = _check_tensor(f"{g.name}.grad", g.grad, self.n_rows, w, self.device,
+                                       strided=True)
             arr[i] = L.GsGroup(_ptr(g.param), grad_ptr, _ptr(g.exp_avg), _ptr(g.exp_avg_sq),
-                               w, g.role, float(np.float32(g.lr)))
+                               w, g.role, float(np.float32(g.lr)), ps, gs)
         self._group_cache_key, self._group_cache = key, arr
         return arr
 
-    def _host_mapped(self, name: str, t: torch.Tensor, width: int) -> int:
+    def _host_mapped(self, name: str, t: torch.Tensor, width: int) -> tuple[int, int]:
         """Pinned host gradients are read zero-copy by the step kernel: only
         the visible rows' bytes cross PCIe (``gs_host_device_pointer``)."""
         if not t.is_pinned():
             raise ConfigError(f"{name} is in pageable host memory; pass a CUDA tensor or a "
                               "pinned (page-locked) host tensor")
-        _check_tensor(name, t, self.n_rows, width, t.device)
+        rs = _check_tensor(name, t, self.n_rows, width, t.device, strided=True)
         dptr = L.C.c_void_p()
         L.check(self.lib.gs_host_device_pointer(t.data_ptr(), L.C.byref(dptr)),
                 "gs_host_device_pointer")
-        return int(dptr.value)
+        return int(dptr.value), rs
 
     # ------------------------------------------------------------- compaction
     def compact(self, vis: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor]:
@@ -290,10 +319,11 @@ class StepEngine:
         self._check_record(record, groups)
         arr = (L.GsGroup * len(groups))()
         for i, g in enumerate(groups):
-            _check_tensor(f"{g.name}.param", g.param, self.n_rows, g.width, self.device)
+            ps = _check_tensor(f"{g.name}.param", g.param, self.n_rows, g.width, self.device,
+                               strided=True)
             # optimizer.py:449: lr * eta (no mu_lr_scale), rounded once
             arr[i] = L.GsGroup(_ptr(g.param), None, None, None, g.width, g.role,
-                               float(np.float32(g.lr * eta)))
+                               float(np.float32(g.lr * eta)), ps, 0)
         picked = torch.empty(max(max_k, 1), dtype=torch.int32, device=self.device)
         rc = self.lib.gs_aiu_apply_rows(arr, len(groups), record.data_ptr(), record.stride(0),
                                         inv_idx.data_ptr(), jlist.data_ptr(), k_dev.data_ptr(),

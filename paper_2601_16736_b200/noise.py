@@ -9,13 +9,14 @@ equivalent, reproducible, and free of a host round trip.
 
 from __future__ import annotations
 
+import ctypes as C
 from dataclasses import dataclass
 
 import numpy as np
 import torch
 
 from . import _lib as L
-from .engine import ConfigError
+from .engine import ConfigError, row_stride
 
 
 @dataclass(frozen=True)
@@ -28,9 +29,11 @@ class NoiseConfig:
     eta_ratio: float = 1.0    # eta_Ro / eta_mu
 
 
-def _check(name, t, n, w):
-    if t.dtype != torch.float32 or not t.is_cuda or not t.is_contiguous() or t.numel() != n * w:
-        raise ConfigError(f"{name} must be a contiguous CUDA fp32 tensor with {n} x {w} values")
+def _check(name, t, n, w) -> int:
+    """Row stride of a CUDA fp32 [n, w] tensor (dense or a record view)."""
+    if t.dtype != torch.float32 or not t.is_cuda:
+        raise ConfigError(f"{name} must be a CUDA fp32 tensor with {n} x {w} values")
+    return row_stride(name, t, n, w)
 
 
 @torch.no_grad()
@@ -44,10 +47,10 @@ def noise_perturb(position: torch.Tensor, log_scale: torch.Tensor, rotation: tor
     dims = position.numel() // max(n, 1) if n else (2 if rotation.dim() == 1 else 3)
     if dims not in (2, 3):
         raise ConfigError("positions must be 2-D or 3-D")
-    _check("position", position, n, dims)
-    _check("log_scale", log_scale, n, dims)
-    _check("rotation", rotation, n, 1 if dims == 2 else 4)
-    _check("opacity_logit", opacity_logit, n, 1)
+    strides = (C.c_int64 * 4)(_check("position", position, n, dims),
+                              _check("log_scale", log_scale, n, dims),
+                              _check("rotation", rotation, n, 1 if dims == 2 else 4),
+                              _check("opacity_logit", opacity_logit, n, 1))
     if alive is not None:
         alive = alive.to(torch.uint8).contiguous() if alive.dtype == torch.bool else alive
     delta = torch.empty((n, dims), dtype=torch.float32, device=position.device)
@@ -58,7 +61,7 @@ def noise_perturb(position: torch.Tensor, log_scale: torch.Tensor, rotation: tor
                               float(lr_position), float(cfg.eta_ratio), float(cfg.lambda_mu),
                               float(cfg.lambda_t), int(seed) & (2**64 - 1),
                               int(iteration) & 0xFFFFFFFF, delta.data_ptr(), int(bool(add)),
-                              torch.cuda.current_stream(position.device).cuda_stream)
+                              strides, torch.cuda.current_stream(position.device).cuda_stream)
     L.check(rc, "gs_noise_perturb")
     return delta
 

@@ -21,7 +21,8 @@ import numpy as np
 import torch
 
 from . import _lib as L
-from .engine import (ConfigError, DomainError, GradientError, GroupBinding, StepEngine,
+from .records import base_grad_view
+from .engine import (ConfigError, DomainError, GradientError, GroupBinding, StepEngine, row_stride,
                      round_pixel_count)
 
 MODES = ("coupled-adam", "sparse-adam", "adamw-const", "adamw-const-clip", "adamw-gs")
@@ -215,9 +216,11 @@ class AdamWGS:
 
     ``params``: list of dicts ``{"params": [tensor], "lr": float, "name": str}``
     (optionally ``"role"``: plain / position / opacity / scale), one tensor per
-    group, all with the same leading row count N, fp32, contiguous, on one
-    CUDA device.  Gradients are read from ``tensor.grad`` or from the
-    ``grads`` mapping passed to :meth:`step`.
+    group, all with the same leading row count N, fp32, on one CUDA device;
+    each row dense, either contiguous per attribute or attribute views of
+    one row-interleaved record (records.py, the faster HBM layout).
+    Gradients are read from ``tensor.grad``, from the record's ``.grad``
+    for record views, or from the ``grads`` mapping passed to :meth:`step`.
     """
 
     def __init__(self, params, *, mode: str = "adamw-gs", betas=(0.9, 0.999), eps: float = 1e-8,
@@ -255,8 +258,10 @@ class AdamWGS:
             p = g["params"][0]
             if p.device != self.device or p.shape[0] != self.n_rows:
                 raise ConfigError(f"group {g['name']}: all groups must share device and row count")
-            if p.dtype != torch.float32 or not p.is_contiguous():
-                raise ConfigError(f"group {g['name']}: parameters must be contiguous fp32")
+            if p.dtype != torch.float32:
+                raise ConfigError(f"group {g['name']}: parameters must be fp32")
+            w = max(1, int(np.prod(p.shape[1:]))) if p.dim() > 1 else 1
+            row_stride(f"group {g['name']}", p, self.n_rows, w)
         self.state = MomentState.zeros_like({g["name"]: g["params"][0] for g in self.param_groups},
                                             state_layout)
         self.engine = StepEngine(self.n_rows, self.device, self.beta1, self.beta2)
@@ -274,8 +279,10 @@ class AdamWGS:
             gr = None
             if grads is not None:
                 gr = grads[name]
-            elif p.grad is not None:
+            elif p.is_leaf and p.grad is not None:
                 gr = p.grad
+            else:  # attribute view of a leaf parameter record (records.py)
+                gr = base_grad_view(p)
             lr = g["lr"] * (mu_lr_scale if g["role"] == L.ROLE_POSITION else 1.0)
             rows = self.state.record is not None
             out.append(GroupBinding(name, g["role"], lr, p.data, gr,

@@ -1,0 +1,113 @@
+"""Row-interleaved parameter and gradient records.
+
+The reference keeps one array per attribute (``GaussianParams``,
+``src/primitives.py:95-112``; ``ParamGrads``, ``src/gradients.py:18-47``).
+With ~30% of rows visible per step, the step's gathers then touch each
+attribute's HBM separately. A 12-byte xyz row or a 4-byte opacity costs a
+whole 32/64-byte DRAM granule, shared with invisible neighbours. The partial
+writes are read-modify-written.
+
+A record stores the attributes of one row contiguously: SH-3 is 59 floats,
+padded to 60 (240 B, 15 16-byte pieces). The attributes stay ordinary
+tensors, as views of the record with the same shapes, so the renderer, the
+optimizer API and the checkpoint code see per-attribute tensors. The step
+kernel reads a visible row with one run of 16-byte copies.
+
+Gradients follow naturally from autograd. Make the record the leaf
+parameter and take the attribute views from it; backward then fills
+``record.grad`` with the same interleaving. :meth:`AdamWGS.step` picks up
+``view._base.grad`` by itself, or the caller passes :func:`views_like` of a
+gradient record, e.g. a pinned host buffer that the step kernel reads
+zero-copy.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from .engine import ConfigError
+
+
+def record_width(widths, align: int = 4) -> int:
+    """Floats per record row: the attribute widths summed, rounded up to
+    ``align`` (4 = 16-byte rows for the kernels' 16-byte copies)."""
+    p = int(sum(widths))
+    return (p + align - 1) // align * align
+
+
+def _width(t: torch.Tensor) -> int:
+    w = 1
+    for d in t.shape[1:]:
+        w *= int(d)
+    return w
+
+
+def views(record: torch.Tensor, shapes: dict[str, tuple]) -> dict[str, torch.Tensor]:
+    """Per-attribute views of a ``(n, PL)`` record. ``shapes`` gives each
+    attribute's per-row shape; attributes are packed in dict order."""
+    if record.dim() != 2 or not record.is_contiguous():
+        raise ConfigError("a record must be a contiguous (n, row_width) tensor")
+    n, pl = record.shape
+    out, off = {}, 0
+    for name, rs in shapes.items():
+        rs = tuple(int(d) for d in rs)
+        w = 1
+        for d in rs:
+            w *= d
+        if off + w > pl:
+            raise ConfigError(f"record row of {pl} floats is too narrow for {name}")
+        v = record[:, off:off + w]
+        out[name] = v.view(n, *rs) if rs else v.view(n)
+        off += w
+    return out
+
+
+def pack(tensors: dict[str, torch.Tensor], align: int = 4, pin_memory: bool = False,
+         requires_grad: bool = False) -> tuple[torch.Tensor, dict[str, torch.Tensor]]:
+    """Copy per-attribute tensors (same row count, dict order = record order)
+    into one new record; return ``(record, views)``. The views keep the
+    input shapes; with ``requires_grad`` the record is a leaf whose ``.grad``
+    has the same layout."""
+    if not tensors:
+        raise ConfigError("nothing to pack")
+    first = next(iter(tensors.values()))
+    n = int(first.shape[0])
+    shapes = {}
+    for name, t in tensors.items():
+        if t.dim() == 0 or int(t.shape[0]) != n:
+            raise ConfigError(f"{name}: every attribute needs the same row count {n}")
+        if t.dtype != torch.float32:
+            raise ConfigError(f"{name}: records hold fp32 attributes")
+        shapes[name] = tuple(t.shape[1:])
+    pl = record_width([_width(t) for t in tensors.values()], align)
+    record = torch.zeros((n, pl), dtype=torch.float32, device=first.device,
+                         pin_memory=pin_memory and first.device.type == "cpu")
+    vs = views(record, shapes)
+    with torch.no_grad():
+        for name, t in tensors.items():
+            vs[name].copy_(t)
+    if requires_grad:
+        record.requires_grad_(True)
+        vs = views(record, shapes)
+    return record, vs
+
+
+def views_like(record: torch.Tensor, like: dict[str, torch.Tensor]) -> dict[str, torch.Tensor]:
+    """Views of another record (a gradient record, a host staging buffer)
+    with the attribute shapes of ``like`` (e.g. the views :func:`pack`
+    returned)."""
+    return views(record, {k: tuple(v.shape[1:]) for k, v in like.items()})
+
+
+def base_grad_view(p: torch.Tensor) -> torch.Tensor | None:
+    """The gradient of an attribute view ``p`` of a leaf record: the same
+    view of ``p._base.grad``. None if ``p`` is not such a view or the record
+    has no gradient."""
+    base = getattr(p, "_base", None)
+    if base is None or base.grad is None:
+        return None
+    g = base.grad
+    if g.shape != base.shape or g.stride() != base.stride() or g.dtype != p.dtype:
+        return None
+    rel = p.storage_offset() - base.storage_offset()
+    return g.as_strided(p.shape, p.stride(), g.storage_offset() + rel)

@@ -468,31 +468,44 @@ def test_optimizer_error_semantics(check):
 
 @pytest.mark.parametrize("mode", ["adamw-gs", "sparse-adam", "adamw-const-clip",
                                   "coupled-adam"])
-def test_step_kernels_all_identical(mode):
-    """Every K2 implementation and tuning variant gives the same bits: the
-    fixed-layout SH-3 kernels (variants 0..6), the generic row-record kernel
-    (variants 0..6) and the per-group-state kernel."""
+@pytest.mark.parametrize("check", ["fused", "strict"])
+def test_step_kernels_all_identical(mode, check):
+    """Every K2 implementation, tuning variant and parameter layout gives the
+    same bits: the fixed-layout SH-3 kernels (variants 0..6), the generic
+    row-record kernel (variants 0..6) and the per-group-state kernel, with
+    per-attribute tensors, with parameters and gradients as views of
+    row-interleaved records (records.py), and with only the parameters in a
+    record (strided gathers)."""
     from paper_2601_16736_b200 import _lib
+    from paper_2601_16736_b200 import records as R
     from paper_2601_16736_b200 import synthetic as S
     from paper_2601_16736_b200.optimizer import AdamWGS
     lib = _lib.load()
     cfg = S.WorkloadConfig(n=20_011, p_vis=0.4, seed=9)
     host = S.make_params(cfg)
     results = []
-    runs = [("fixed", v) for v in range(7)] + [("rows", v) for v in range(7)] + [("groups", 0)]
+    runs = [("fixed", v, "attr") for v in range(7)] + [("rows", v, "attr") for v in range(7)]
+    runs += [("groups", 0, "attr")]
+    runs += [(k, 0, lay) for k in ("fixed", "rows", "groups") for lay in ("record", "param-record")]
+    if check == "strict":
+        runs = [r for r in runs if r[1] in (0, 3)]
     prev_f = lib.gs_set_fixed_variant(0)
     prev_r = lib.gs_set_rows_variant(0)
     try:
-        for kind, variant in runs:
+        for kind, variant, lay in runs:
             lib.gs_set_fixed_variant(variant if kind == "fixed" else -1)
             lib.gs_set_rows_variant(variant if kind == "rows" else 0)
             params = {k: torch.from_numpy(v).to(DEV) for k, v in host.items()}
+            if lay != "attr":
+                _, params = R.pack(params)
             layout = "groups" if kind == "groups" else "rows"
             opt = AdamWGS(S.param_groups(params), mode=mode, lambda_o=1e-3, lambda_s=1e-5,
-                          state_layout=layout)
+                          state_layout=layout, check=check)
             for s in range(3):
                 vis = S.visibility(cfg, s)
                 g = {k: torch.from_numpy(x).to(DEV) for k, x in S.step_grads(cfg, s, vis).items()}
+                if lay == "record":
+                    _, g = R.pack(g)
                 opt.step(torch.from_numpy(vis).to(DEV), cfg.n_pixels, grads=g)
             results.append(({k: p.cpu().numpy() for k, p in params.items()},
                             {k: t.contiguous().cpu().numpy() for k, t in opt.state.m.items()},
@@ -502,16 +515,64 @@ def test_step_kernels_all_identical(mode):
         lib.gs_set_fixed_variant(prev_f)
         lib.gs_set_rows_variant(prev_r)
     ref = results[0]
-    for (kind, variant), res in zip(runs[1:], results[1:]):
+    for run, res in zip(runs[1:], results[1:]):
         for i in range(3):
             for k in ref[i]:
-                assert np.array_equal(res[i][k], ref[i][k]), (kind, variant, i, k)
-        assert np.array_equal(res[3], ref[3]), (kind, variant)
+                assert np.array_equal(res[i][k], ref[i][k]), (run, i, k)
+        assert np.array_equal(res[3], ref[3]), run
         for f, x in ref[4].items():
             if f.startswith("sum_"):
-                assert res[4][f] == pytest.approx(x, rel=1e-12), (kind, variant, f)
+                assert res[4][f] == pytest.approx(x, rel=1e-12), (run, f)
             else:
-                assert res[4][f] == x, (kind, variant, f)
+                assert res[4][f] == x, (run, f)
+
+
+def test_record_params_autograd_grad_and_state_ops():
+    """Attribute views of a leaf record: backward fills record.grad, step()
+    picks the matching view of it; AIU, stats, noise and the error paths
+    work on the strided views, bitwise equal to per-attribute tensors."""
+    from paper_2601_16736_b200 import records as R
+    from paper_2601_16736_b200 import synthetic as S
+    from paper_2601_16736_b200.noise import NoiseConfig
+    from paper_2601_16736_b200.optimizer import AdamWGS
+    from paper_2601_16736_b200.sampling import AiuConfig
+    cfg = S.WorkloadConfig(n=10_007, p_vis=0.3, seed=21)
+    host = S.make_params(cfg)
+    outs = []
+    for lay in ("attr", "record"):
+        params = {k: torch.from_numpy(v).to(DEV) for k, v in host.items()}
+        if lay == "record":
+            rec, params = R.pack(params, requires_grad=True)
+        opt = AdamWGS(S.param_groups(params), mode="adamw-gs", lambda_o=1e-3, lambda_s=1e-5)
+        for s in range(3):
+            vis = S.visibility(cfg, s)
+            g = S.step_grads(cfg, s, vis)
+            if lay == "record":
+                # a toy loss whose gradient w.r.t. each view is the synthetic gradient
+                rec.grad = None
+                loss = sum((params[k] * torch.from_numpy(x).to(DEV).view(params[k].shape)).sum()
+                           for k, x in g.items())
+                loss.backward()
+                opt.step(torch.from_numpy(vis).to(DEV), cfg.n_pixels)
+            else:
+                opt.step(torch.from_numpy(vis).to(DEV), cfg.n_pixels,
+                         grads={k: torch.from_numpy(x).to(DEV) for k, x in g.items()})
+        vis = torch.from_numpy(S.visibility(cfg, 7)).to(DEV)
+        aiu = AiuConfig(start=0, end=100, prob_schedule=((0, 0.2),), eta_schedule=((0, 0.5),),
+                        enabled=True)
+        picked = opt.aiu_apply(vis, aiu, np.random.default_rng(3), 5)
+        opt.noise_perturb(1e-3, NoiseConfig(enabled=True), seed=11, iteration=5)
+        stats = opt.moment_stats()
+        act = opt.classify_active()
+        torch.cuda.synchronize()
+        outs.append(({k: p.detach().cpu().numpy() for k, p in params.items()},
+                     opt.state.record.cpu().numpy(), picked, stats, act))
+    a, b = outs
+    for k in a[0]:
+        assert np.array_equal(a[0][k], b[0][k]), k
+    assert np.array_equal(a[1], b[1])
+    assert np.array_equal(a[2], b[2])
+    assert repr(a[3]) == repr(b[3]) and repr(a[4]) == repr(b[4])
 
 
 def test_state_views_and_checkpoint_roundtrip():

@@ -1,0 +1,62 @@
+"""CPU tests of the row-interleaved record helpers (records.py) and the row
+stride rule the engine applies to parameter / gradient tensors."""
+
+import pytest
+import torch
+
+from paper_2601_16736_b200 import records as R
+from paper_2601_16736_b200.engine import ConfigError, row_stride
+
+
+def _attrs(n=7):
+    g = torch.Generator().manual_seed(0)
+    return {"xyz": torch.randn(n, 3, generator=g), "f_dc": torch.randn(n, 3, generator=g),
+            "f_rest": torch.randn(n, 15, 3, generator=g), "opacity": torch.randn(n, 1, generator=g),
+            "scaling": torch.randn(n, 3, generator=g), "rotation": torch.randn(n, 4, generator=g)}
+
+
+def test_pack_layout_and_views():
+    a = _attrs()
+    rec, v = R.pack(a)
+    assert rec.shape == (7, 60) and rec.is_contiguous()
+    off = 0
+    for k, t in a.items():
+        w = t[0].numel()
+        assert torch.equal(v[k], t) and v[k].shape == t.shape
+        assert torch.equal(rec[:, off:off + w].reshape(t.shape), t)
+        assert row_stride(k, v[k], 7, w) == 60
+        off += w
+    assert torch.all(rec[:, 59] == 0)  # pad
+
+
+def test_autograd_fills_record_grad_and_base_grad_view():
+    rec, v = R.pack(_attrs(), requires_grad=True)
+    loss = (v["xyz"] ** 2).sum() + 3.0 * v["f_rest"].sum()
+    loss.backward()
+    assert rec.grad.shape == rec.shape
+    assert torch.equal(R.base_grad_view(v["xyz"]), 2 * v["xyz"].detach())
+    assert torch.equal(R.base_grad_view(v["f_rest"]), torch.full((7, 15, 3), 3.0))
+    assert torch.equal(R.base_grad_view(v["opacity"]), torch.zeros(7, 1))
+    assert R.base_grad_view(torch.zeros(7, 3)) is None
+
+
+def test_views_like_matches_offsets():
+    a = _attrs()
+    _, v = R.pack(a)
+    other = torch.arange(7 * 60, dtype=torch.float32).view(7, 60)
+    w = R.views_like(other, v)
+    assert w["opacity"][2, 0] == other[2, 51]
+    assert torch.equal(w["rotation"][1], other[1, 55:59])
+
+
+def test_row_stride_rules():
+    assert row_stride("c", torch.zeros(5, 3), 5, 3) == 3
+    assert row_stride("v", torch.zeros(5, 8)[:, 2:5], 5, 3) == 8
+    with pytest.raises(ConfigError):
+        row_stride("t", torch.zeros(3, 5).t(), 5, 3)           # column-major rows
+    with pytest.raises(ConfigError):
+        row_stride("s", torch.zeros(5, 6)[:, ::2], 5, 3)       # gaps inside a row
+    with pytest.raises(ConfigError):
+        row_stride("n", torch.zeros(4, 3), 5, 3)               # wrong row count
+    with pytest.raises(ConfigError):
+        R.pack({"a": torch.zeros(3, 2), "b": torch.zeros(4, 2)})
