@@ -72,6 +72,7 @@ struct FixedParams {
   uint32_t prs;
   uint32_t grs;
   int grec_ca;  // gradient record copies through L1 (.ca): host-mapped gradients
+  int tma_ok;   // records and the state record allow 16-byte bulk copies
   double* stats_out;
   double* partials;
   unsigned int* counter;
@@ -831,6 +832,39 @@ __device__ __forceinline__ void named_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
 }
 
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(a), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, uint32_t bytes,
+                                         uint64_t* bar) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::
+          "r"(s),
+      "l"(gmem), "r"(bytes), "r"(b)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* gmem, const void* smem, uint32_t bytes) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(gmem), "r"(s),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() {
+  asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read1() {
+  asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+
 template <class L, int R>
 struct WsStage {
   static constexpr int kSlots = L::P + 1;
@@ -840,8 +874,12 @@ struct WsStage {
   static constexpr int kBytes = kRec + 2 * kTh + R * 4;  // + row ids
 };
 
-template <class L, int MODE, bool STRICT, int R, int S, int NPW, int NCW, int MINB, bool REC>
+template <class L, int MODE, bool STRICT, int R, int S, int NPW, int NCW, int MINB, bool REC,
+          bool BULKST = false>
 __global__ void __launch_bounds__((NPW + NCW) * 32, MINB) step_ws_kernel(const FixedParams P) {
+  // BULKST (records only): results are written into the stage in place and
+  // every good row leaves with two bulk stores (parameter row, moment record)
+  static_assert(REC || !BULKST, "bulk stores need row-contiguous records");
   constexpr bool kDense = MODE == GS_MODE_COUPLED_ADAM;
   constexpr bool kCoupled = MODE == GS_MODE_COUPLED_ADAM || MODE == GS_MODE_SPARSE_ADAM;
   constexpr int NC = NCW * 32;  // consumer threads
@@ -976,10 +1014,13 @@ __global__ void __launch_bounds__((NPW + NCW) * 32, MINB) step_ws_kernel(const F
                                              : (uint32_t)__ldg(P.rows + chunk_id(k) * R + t))
                                    : 0u;
       mbar_wait(&full_bar[st], (unsigned)((k / S) & 1));
-      const unsigned char* sb = stage(st);
+      unsigned char* sbw = stage(st);
+      const unsigned char* sb = sbw;
       const float2* srec = reinterpret_cast<const float2*>(sb);
       const float* sth = reinterpret_cast<const float*>(sb + ST::kRec);
       const float* sg = sth + R * PL;
+      float2* const srec_w = reinterpret_cast<float2*>(sbw);
+      float* const sth_w = reinterpret_cast<float*>(sbw + ST::kRec);
       const uint32_t* srow = s_crow[st];
       if (!STRICT) {
 #pragma unroll
@@ -1017,7 +1058,8 @@ __global__ void __launch_bounds__((NPW + NCW) * 32, MINB) step_ws_kernel(const F
         ++c_vis;
         const int bad = s_bad[st][t];
         if (bad == 0) {
-          reinterpret_cast<int*>(rec_base + (size_t)s_crow[st][t] * rec_stride2 + L::P)[0] = tn;
+          if (!BULKST)
+            reinterpret_cast<int*>(rec_base + (size_t)s_crow[st][t] * rec_stride2 + L::P)[0] = tn;
           s_bc[st][t] = bc;
           if (P.D.group >= 0) {
 #pragma unroll
@@ -1033,6 +1075,8 @@ __global__ void __launch_bounds__((NPW + NCW) * 32, MINB) step_ws_kernel(const F
         }
       }
       named_sync(1, NC);  // bias factors visible
+      if (BULKST && t < nvalid && s_bad[st][t] == 0)
+        reinterpret_cast<int*>(srec_w + t * SLOTS + L::P)[0] = tn;
       auto update = [&](int gg, int i, int r) {
         const int W = L::W(gg);
         const int role = L::ROLE(gg);
@@ -1056,8 +1100,13 @@ __global__ void __launch_bounds__((NPW + NCW) * 32, MINB) step_ws_kernel(const F
           c_apre += th > P.active_logit;
           c_apost += tnv > P.active_logit;
         }
-        P.g[gg].param[row * P.g[gg].ps + (uint32_t)c] = tnv;
-        rec_base[(size_t)row * rec_stride2 + L::OFF(gg) + c] = make_float2(mn, vn);
+        if (BULKST) {
+          sth_w[e] = tnv;
+          srec_w[r * SLOTS + L::OFF(gg) + c] = make_float2(mn, vn);
+        } else {
+          P.g[gg].param[row * P.g[gg].ps + (uint32_t)c] = tnv;
+          rec_base[(size_t)row * rec_stride2 + L::OFF(gg) + c] = make_float2(mn, vn);
+        }
       };
       if (!any_bad) {
 #pragma unroll
@@ -1080,11 +1129,32 @@ __global__ void __launch_bounds__((NPW + NCW) * 32, MINB) step_ws_kernel(const F
           }
         }
       }
-      named_sync(1, NC);  // all reads of this stage's flags / data done
-      if (t < R) s_bad[st][t] = 0;
-      if (t == 0) s_any[st] = 0;
-      mbar_arrive(&empty_bar[st]);
+      if (BULKST) {
+        fence_proxy_async_smem();  // generic-proxy smem writes -> bulk-store reads
+        named_sync(1, NC);         // the chunk's rows are final in shared memory
+        if (t < R) {
+          // stage released one chunk later, once the stores have read it
+          if (t < nvalid && s_bad[st][t] == 0) {
+            const uint32_t row = srow[t];
+            bulk_s2g(P.g[0].param + (size_t)row * P.prs, sth + t * PL, (uint32_t)(PL * 4));
+            bulk_s2g(P.record + (size_t)row * P.stride, srec + t * SLOTS, (uint32_t)(SLOTS * 8));
+          }
+          bulk_commit();
+          s_bad[st][t] = 0;
+          if (t == 0) s_any[st] = 0;
+          bulk_wait_read1();
+          if (k > 0) mbar_arrive(&empty_bar[(int)((k - 1) % S)]);
+        } else {
+          mbar_arrive(&empty_bar[st]);
+        }
+      } else {
+        named_sync(1, NC);  // all reads of this stage's flags / data done
+        if (t < R) s_bad[st][t] = 0;
+        if (t == 0) s_any[st] = 0;
+        mbar_arrive(&empty_bar[st]);
+      }
     }
+    if (BULKST) bulk_wait0();
   }
   cp_async_wait<0>();
 
@@ -1105,20 +1175,295 @@ __global__ void __launch_bounds__((NPW + NCW) * 32, MINB) step_ws_kernel(const F
 }
 
 template <class L, int MODE, bool STRICT, int R, int S, int NPW, int NCW, int MINB,
-          bool REC = false>
+          bool REC = false, bool BULKST = false>
 void launch_ws(const FixedParams& P, int64_t max_rows, cudaStream_t s) {
   constexpr int bytes = S * WsStage<L, R>::kBytes;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(step_ws_kernel<L, MODE, STRICT, R, S, NPW, NCW, MINB, REC>,
+    cudaFuncSetAttribute(step_ws_kernel<L, MODE, STRICT, R, S, NPW, NCW, MINB, REC, BULKST>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     attr_set = true;
   }
   const int64_t chunks = (max_rows + R - 1) / R;
   const int grid =
       (int)std::max<int64_t>(1, std::min<int64_t>(chunks, (int64_t)gs_sm_count() * MINB));
-  step_ws_kernel<L, MODE, STRICT, R, S, NPW, NCW, MINB, REC>
+  step_ws_kernel<L, MODE, STRICT, R, S, NPW, NCW, MINB, REC, BULKST>
       <<<grid, (NPW + NCW) * 32, bytes, s>>>(P);
+}
+
+// ---------------------------------------------------------------------------
+// TMA variant for row-interleaved records (parameters, gradients and the
+// optimizer-state record all row-contiguous): one producer warp moves each
+// visible row with three bulk copies (cp.async.bulk, SASS UBLKCP) — the
+// 480-byte moment record, the 240-byte parameter row and the 240-byte
+// gradient row — completing on the stage's "full" mbarrier by transaction
+// count.  Consumers update in shared memory in place, then every good row is
+// written back with two bulk stores (parameter row, moment record with the
+// new clock); bad rows are never stored, so they stay untouched.  Compared
+// with the cp.async gather variant this replaces ~60 16-byte copies and
+// ~120 scattered 4/8-byte stores per row with 5 bulk operations.
+// ---------------------------------------------------------------------------
+template <class L, int R>
+struct TmaStage {
+  static constexpr int kSlots = L::P + 1;
+  static constexpr int kPL = (L::P + 3) & ~3;
+  static constexpr int kRecRow = kSlots * 8;  // moment record row incl. the clock slot
+  static constexpr int kThRow = kPL * 4;      // parameter / gradient record row
+  static constexpr int kRec = R * kRecRow;
+  static constexpr int kTh = R * kThRow;
+  static constexpr int kBytes = kRec + 2 * kTh;
+  static_assert(kRecRow % 16 == 0 && kThRow % 16 == 0, "bulk copies move 16-byte multiples");
+};
+
+template <class L, int MODE, bool STRICT, int R, int S, int NCW, int MINB>
+__global__ void __launch_bounds__((NCW + 1) * 32, MINB) step_tma_kernel(const FixedParams P) {
+  static_assert(R == 32, "one producer lane per row");
+  constexpr bool kDense = MODE == GS_MODE_COUPLED_ADAM;
+  constexpr bool kCoupled = MODE == GS_MODE_COUPLED_ADAM || MODE == GS_MODE_SPARSE_ADAM;
+  constexpr int NC = NCW * 32;
+  using SH = ChunkShape<L, R, NC>;
+  using ST = TmaStage<L, R>;
+  constexpr int SLOTS = ST::kSlots;
+  constexpr int PL = ST::kPL;
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) uint64_t full_bar[S];
+  __shared__ __align__(8) uint64_t empty_bar[S];
+  __shared__ int s_bad[S][R];
+  __shared__ int s_any[S];
+  __shared__ float2 s_bc[S][R];
+  __shared__ uint32_t s_crow[S][R];
+  __shared__ double s_red[GS_STEP_STATS * (NCW + 1)];
+
+  const int tid = threadIdx.x;
+  const bool producer = tid >= NC;
+  int64_t n_rows = kDense ? P.max_rows : (int64_t)(*P.n_rows_dev);
+  if (STRICT && *P.abort_flag != 0) n_rows = 0;
+  const int64_t n_chunks = (n_rows + R - 1) / R;
+  auto chunk_id = [&](int64_t k) { return (int64_t)blockIdx.x + k * gridDim.x; };
+  auto chunk_rows = [&](int64_t k) -> int {
+    const int64_t rem = n_rows - chunk_id(k) * R;
+    return rem <= 0 ? 0 : (rem < R ? (int)rem : R);
+  };
+  auto stage = [&](int st) { return smem + st * ST::kBytes; };
+  auto sidx = [](int gg, int i, int r) -> int { return r * PL + L::OFF(gg) + (i - r * L::W(gg)); };
+
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], NC);
+    }
+  }
+  if (tid < R * S) s_bad[tid / R][tid % R] = 0;
+  if (tid < S) s_any[tid] = 0;
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  __syncthreads();
+
+  unsigned c_vis = 0, c_step = 0, c_badg = 0, c_badd = 0, c_apre = 0, c_apost = 0, c_clo = 0,
+           c_cls = 0;
+  double s_exo = 0.0, s_exs = 0.0;
+
+  if (producer) {
+    // ------------------------------------------------------------------ producer
+    const int lane = tid - NC;
+    auto fetch_id = [&](int64_t k) -> uint32_t {
+      if (lane >= chunk_rows(k)) return 0u;
+      const int64_t i = chunk_id(k) * R + lane;
+      return kDense ? (uint32_t)i : (uint32_t)__ldg(P.rows + i);
+    };
+    uint32_t next_id = fetch_id(0);
+    for (int64_t k = 0; chunk_id(k) < n_chunks; ++k) {
+      const int st = (int)(k % S);
+      const uint32_t row = next_id;
+      next_id = fetch_id(k + 1);
+      if (k >= S) mbar_wait(&empty_bar[st], (unsigned)(((k / S) - 1) & 1));
+      const int nv = chunk_rows(k);
+      unsigned char* sb = stage(st);
+      if (lane == 0)
+        mbar_arrive_expect_tx(&full_bar[st], (uint32_t)nv * (ST::kRecRow + 2 * ST::kThRow));
+      __syncwarp();
+      if (lane < nv) {
+        bulk_g2s(sb + lane * ST::kRecRow, P.record + (size_t)row * P.stride, ST::kRecRow,
+                 &full_bar[st]);
+        bulk_g2s(sb + ST::kRec + lane * ST::kThRow, P.prec + (size_t)row * P.prs, ST::kThRow,
+                 &full_bar[st]);
+        bulk_g2s(sb + ST::kRec + ST::kTh + lane * ST::kThRow, P.grec + (size_t)row * P.grs,
+                 ST::kThRow, &full_bar[st]);
+      }
+    }
+  } else {
+    // ------------------------------------------------------------------ consumers
+    const int t = tid;
+    StepConsts Kc = P.K;
+    if (kCoupled) {
+      const float nv = P.nv_dev ? (float)(*P.nv_dev) : (float)P.nv_host;
+      Kc.inv_nv = nv != 0.0f ? __frcp_rn(nv) : 0.0f;
+      if (nv == 0.0f) Kc.lam_op = Kc.lam_sc = 0.0f;
+    }
+    const StepConsts& K = kCoupled ? Kc : P.K;
+    float* const prec = const_cast<float*>(P.prec);
+    for (int64_t k = 0; chunk_id(k) < n_chunks; ++k) {
+      const int st = (int)(k % S);
+      const int nvalid = chunk_rows(k);
+      if (t < R)
+        s_crow[st][t] = t < nvalid ? (kDense ? (uint32_t)(chunk_id(k) * R + t)
+                                             : (uint32_t)__ldg(P.rows + chunk_id(k) * R + t))
+                                   : 0u;
+      mbar_wait(&full_bar[st], (unsigned)((k / S) & 1));
+      unsigned char* sb = stage(st);
+      float2* srec = reinterpret_cast<float2*>(sb);
+      float* sth = reinterpret_cast<float*>(sb + ST::kRec);
+      const float* sg = reinterpret_cast<const float*>(sb + ST::kRec + ST::kTh);
+      const uint32_t* srow = s_crow[st];
+      if (!STRICT) {
+#pragma unroll
+        for (int gg = 0; gg < L::G; ++gg) {
+          const int W = L::W(gg);
+          const int role = L::ROLE(gg);
+          const float lam = role == GS_ROLE_OPACITY ? K.lam_op : role == GS_ROLE_SCALE ? K.lam_sc : 0.f;
+#pragma unroll
+          for (int kk = 0; kk < SH::rounds(gg); ++kk) {
+            const int i = kk * NC + ((t + NC - (R * L::OFF(gg)) % NC) % NC);
+            const int r = i / W;
+            if (i < R * W && r < nvalid) {
+              const int e = sidx(gg, i, r);
+              int bad = isfinite(sg[e]) ? 0 : 1;
+              if ((role == GS_ROLE_OPACITY || role == GS_ROLE_SCALE) && lam != 0.f &&
+                  domain_bad(role, sth[e]))
+                bad |= 2;
+              if (bad) {
+                atomicOr(&s_bad[st][r], bad);
+                s_any[st] = 1;
+              }
+            }
+          }
+        }
+      }
+      int tn = 0;
+      float2 bc = make_float2(1.f, 1.f);
+      if (t < nvalid) {
+        tn = reinterpret_cast<const int*>(srec + t * SLOTS + L::P)[0] + 1;
+        bc = bias_factors(P.lut, P.lut_len, kDense ? P.global_t : tn, 0.0, 0.0);
+      }
+      named_sync(1, NC);  // bad flags final
+      const bool any_bad = s_any[st] != 0 || nvalid < R;
+      if (t < nvalid) {
+        ++c_vis;
+        const int bad = s_bad[st][t];
+        if (bad == 0) {
+          s_bc[st][t] = bc;
+          if (P.D.group >= 0) {
+#pragma unroll
+            for (int gg = 0; gg < L::G; ++gg)
+              if (gg == P.D.group)
+                densify_row(P.D, srow[t], sg + sidx(gg, t * L::W(gg), t), L::W(gg), 1);
+          }
+          ++c_step;
+        } else if (bad & 1) {
+          ++c_badg;
+        } else {
+          ++c_badd;
+        }
+      }
+      named_sync(1, NC);  // bias factors visible; the clock slots are read
+      if (t < nvalid && s_bad[st][t] == 0) reinterpret_cast<int*>(srec + t * SLOTS + L::P)[0] = tn;
+      auto update = [&](int gg, int i, int r) {
+        const int W = L::W(gg);
+        const int role = L::ROLE(gg);
+        const int c = i - r * W;
+        const int e = sidx(gg, i, r);
+        float2& mv = srec[r * SLOTS + L::OFF(gg) + c];
+        const float th = sth[e];
+        float tnv, mn, vn, ex;
+        bool clipped;
+        update_element<MODE>(role, P.g[gg].lr, th, sg[e], mv.x, mv.y, s_bc[st][r], K, tnv, mn,
+                             vn, ex, clipped);
+        if (!kCoupled && role == GS_ROLE_OPACITY) {
+          c_clo += clipped;
+          s_exo += (double)ex;
+        } else if (!kCoupled && role == GS_ROLE_SCALE) {
+          c_cls += clipped;
+          s_exs += (double)ex;
+        }
+        if (role == GS_ROLE_OPACITY) {
+          c_apre += th > P.active_logit;
+          c_apost += tnv > P.active_logit;
+        }
+        sth[e] = tnv;
+        mv = make_float2(mn, vn);
+      };
+      if (!any_bad) {
+#pragma unroll
+        for (int gg = 0; gg < L::G; ++gg) {
+#pragma unroll
+          for (int kk = 0; kk < SH::rounds(gg); ++kk) {
+            const int i = kk * NC + ((t + NC - (R * L::OFF(gg)) % NC) % NC);
+            const bool full = (kk + 1) * NC <= R * L::W(gg);  // compile-time
+            if (full || i < R * L::W(gg)) update(gg, i, i / L::W(gg));
+          }
+        }
+      } else {
+#pragma unroll
+        for (int gg = 0; gg < L::G; ++gg) {
+#pragma unroll
+          for (int kk = 0; kk < SH::rounds(gg); ++kk) {
+            const int i = kk * NC + ((t + NC - (R * L::OFF(gg)) % NC) % NC);
+            const int r = i / L::W(gg);
+            if (i < R * L::W(gg) && r < nvalid && s_bad[st][r] == 0) update(gg, i, r);
+          }
+        }
+      }
+      fence_proxy_async_smem();  // generic-proxy smem writes -> bulk-store reads
+      named_sync(1, NC);         // the chunk's rows are final in shared memory
+      if (t < R) {
+        // row t's stores; the stage is released one chunk later, once they
+        // have read shared memory (wait_group.read 1), so the store latency
+        // overlaps the next chunk's update instead of stalling this one
+        if (t < nvalid && s_bad[st][t] == 0) {
+          const uint32_t row = srow[t];
+          bulk_s2g(prec + (size_t)row * P.prs, sth + t * PL, ST::kThRow);
+          bulk_s2g(P.record + (size_t)row * P.stride, srec + t * SLOTS, ST::kRecRow);
+        }
+        bulk_commit();  // one (possibly empty) group per chunk
+        s_bad[st][t] = 0;
+        if (t == 0) s_any[st] = 0;
+        bulk_wait_read1();
+        if (k > 0) mbar_arrive(&empty_bar[(int)((k - 1) % S)]);
+      } else {
+        mbar_arrive(&empty_bar[st]);
+      }
+    }
+    bulk_wait0();
+  }
+
+  double acc[GS_STEP_STATS] = {(double)c_vis,  (double)c_step, (double)c_badg, (double)c_badd,
+                               (double)c_apre, (double)c_apost, (double)c_clo, (double)c_cls,
+                               s_exo,          s_exs};
+  const bool is_max[GS_STEP_STATS] = {false, false, false, false, false,
+                                      false, false, false, false, false};
+  block_reduce_n<GS_STEP_STATS, (NCW + 1)>(acc, is_max, s_red);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int f = 0; f < GS_STEP_STATS; ++f)
+      P.partials[(size_t)blockIdx.x * GS_STEP_STATS + f] = acc[f];
+  }
+  if (last_block_arrive(P.counter))
+    final_reduce_n<GS_STEP_STATS, (NCW + 1)>(P.partials, gridDim.x, GS_STEP_STATS, P.stats_out,
+                                             is_max, s_red);
+}
+
+template <class L, int MODE, bool STRICT, int R, int S, int NCW, int MINB>
+void launch_tma(const FixedParams& P, int64_t max_rows, cudaStream_t s) {
+  constexpr int bytes = S * TmaStage<L, R>::kBytes;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(step_tma_kernel<L, MODE, STRICT, R, S, NCW, MINB>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    attr_set = true;
+  }
+  const int64_t chunks = (max_rows + R - 1) / R;
+  const int grid =
+      (int)std::max<int64_t>(1, std::min<int64_t>(chunks, (int64_t)gs_sm_count() * MINB));
+  step_tma_kernel<L, MODE, STRICT, R, S, NCW, MINB><<<grid, (NCW + 1) * 32, bytes, s>>>(P);
 }
 
 static int g_fixed_variant = -1;
@@ -1147,7 +1492,24 @@ void launch_fixed_v(const FixedParams& P, int64_t max_rows, cudaStream_t s) {
 template <class L, int MODE, bool STRICT>
 void launch_fixed(const FixedParams& P, int64_t max_rows, int kind, cudaStream_t s) {
   if (kind == 2) {
-    launch_ws<L, MODE, STRICT, 32, 3, 3, 8, 2, true>(P, max_rows, s);
+    // records: bulk-copy (TMA) kernel when the state record allows 16-byte
+    // bulk copies, else the cp.async gather kernel on the record layout
+    // Default: cp.async record gathers + per-element stores.  The bulk-copy
+    // (TMA) kernels are kept as variants: for 240 / 480-byte rows the TMA
+    // unit's per-operation cost bounds them (~0.86 ms vs 0.67 ms on c3,
+    // profiles/r01/ncu_step_tma_c3_record.txt), loads and stores alike.
+    const int v = (P.D.group >= 0 || !P.tma_ok) ? 0 : fixed_variant();
+    if (v == 11) {
+      launch_ws<L, MODE, STRICT, 32, 3, 3, 8, 2, true, true>(P, max_rows, s);
+    } else if (v == 9) {
+      launch_tma<L, MODE, STRICT, 32, 6, 12, 1>(P, max_rows, s);
+    } else if (v == 10) {
+      launch_tma<L, MODE, STRICT, 32, 3, 4, 2>(P, max_rows, s);
+    } else if (v == 12) {
+      launch_tma<L, MODE, STRICT, 32, 3, 8, 2>(P, max_rows, s);
+    } else {
+      launch_ws<L, MODE, STRICT, 32, 3, 3, 8, 2, true>(P, max_rows, s);
+    }
     return;
   }
   // the densification statistics and strided rows are handled by the
@@ -1250,6 +1612,8 @@ int gs_step_fixed_try(const gs_group* groups, int32_t n_groups, const gs_step_cf
   FixedParams P{};
   const int kind = rows_kind<LayoutSH3>(groups, max_rows, P);
   if (kind < 0) return 0;  // 32-bit element offsets
+  P.tma_ok = kind == 2 && P.grec_ca == 0 && record_stride % 4 == 0 &&
+             (reinterpret_cast<uintptr_t>(record) & 15u) == 0;
   for (int i = 0; i < n_groups; ++i)
     P.g[i] = FixedGroup{
         groups[i].param, groups[i].grad, groups[i].lr,

@@ -4,6 +4,7 @@ cd ${GRAFT_REPO_ROOT:-.}
 mkdir -p gpurun_out
 python bench.py > gpurun_out/bench_c3.json 2> gpurun_out/bench_c3.err; echo "bench rc=$?"
 python bench.py --mask coherent --no-cpu --no-e2e > gpurun_out/bench_c3_coherent.json 2>&1; echo "coherent rc=$?"
+python bench.py --params attr --no-cpu --no-e2e > gpurun_out/bench_c3_attr.json 2>&1; echo "attr rc=$?"
 for w in c1 c2 c4; do
   python bench.py --workload $w --no-cpu --no-e2e > gpurun_out/bench_$w.json 2>&1; echo "$w rc=$?"
 done
