@@ -87,6 +87,9 @@ def parse():
                     help="launch the timed steps eagerly instead of as one CUDA graph")
     ap.add_argument("--layout", default="rows", choices=["rows", "groups"],
                     help="optimizer-state layout (row records or per-group tensors)")
+    ap.add_argument("--record-align", type=int, default=4,
+                    help="parameter / gradient record rows padded to a multiple of this "
+                         "many floats (4: 240-byte SH-3 rows; 16: 256-byte, granule-aligned)")
     ap.add_argument("--params", default="record", choices=["record", "attr"],
                     help="parameter / gradient HBM layout: attribute views of one "
                          "row-interleaved record (records.py) or one tensor per attribute")
@@ -305,7 +308,7 @@ def ours(args, wl, p_vis):
                            lambda_o=wl["lo"], lambda_s=wl["ls"])
     params = S.make_params_device(cfg, dev)
     if args.params == "record":
-        _, params = R.pack(params)
+        _, params = R.pack(params, align=args.record_align)
     opt = AdamWGS(S.param_groups(params), mode=wl["mode"], lambda_o=wl["lo"], lambda_s=wl["ls"],
                   check=args.check, errors="defer", state_layout=args.layout)
     total_steps = args.warmup + args.steps
@@ -313,7 +316,7 @@ def ours(args, wl, p_vis):
     n_vis = torch.stack([m.sum() for m in masks]).cpu().numpy().astype(np.int64)
     grad_sets = [S.grads_device(cfg, s, dev) for s in range(2)]
     if args.params == "record":
-        grad_sets = [R.pack(g)[1] for g in grad_sets]
+        grad_sets = [R.pack(g, align=args.record_align)[1] for g in grad_sets]
     # RSR / relocation samples are host-drawn with the reference RNG contract
     # (optimizer.py:379-386, rng.py:17-30) and uploaded before timing.
     events = {}
