@@ -285,6 +285,10 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
 }
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
+}
 __device__ __forceinline__ void cp_async16_ca(void* smem, const void* gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
@@ -1192,6 +1196,318 @@ void launch_ws(const FixedParams& P, int64_t max_rows, cudaStream_t s) {
 }
 
 // ---------------------------------------------------------------------------
+// Record kernel (the default for parameter/gradient records): the gather
+// ring of step_ws_kernel with the synchronisation cut to one named barrier
+// per chunk.
+//   * producers: each warp owns whole rows (r = warp, warp + NPW, ...); every
+//     lane holds the chunk's row id of its own index and the owner warp
+//     broadcasts it with a shuffle — no shared-memory row-id hand-off and no
+//     producer barrier.  A row is 60 16-byte pieces (30 moment record, 15
+//     theta, 15 gradient): two per lane.
+//   * consumers: the clock and bias factors of row t are fetched before the
+//     check pass, so the LUT latency hides behind it; bad-row flags carry the
+//     stage's use count (epoch) instead of being reset, so after the single
+//     barrier nothing else needs a block-wide ordering point.
+// ---------------------------------------------------------------------------
+template <class L, int MODE, bool STRICT, int R, int S, int NPW, int NCW, int MINB, bool FLAT>
+__global__ void __launch_bounds__((NPW + NCW) * 32, MINB) step_rec_kernel(const FixedParams P) {
+  static_assert(R == 32, "one lane per row id");
+  static_assert(S >= 2, "stage reuse relies on the next chunk's barrier");
+  constexpr bool kDense = MODE == GS_MODE_COUPLED_ADAM;
+  constexpr bool kCoupled = MODE == GS_MODE_COUPLED_ADAM || MODE == GS_MODE_SPARSE_ADAM;
+  constexpr int NC = NCW * 32;
+  constexpr int NP = NPW * 32;
+  constexpr int SLOTS = L::P + 1;
+  using SH = ChunkShape<L, R, NC>;
+  using ST = WsStage<L, R>;
+  constexpr int PL = ST::kPL;
+  constexpr int kRecPieces = SLOTS * 8 / 16;
+  constexpr int kRowPieces = PL / 4;
+  constexpr int kPiecesPerRow = kRecPieces + 2 * kRowPieces;
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ __align__(8) uint64_t full_bar[S];
+  __shared__ __align__(8) uint64_t empty_bar[S];
+  __shared__ int s_badg[S][R];  // == epoch: non-finite gradient in this use of the stage
+  __shared__ int s_badd[S][R];  // == epoch: activation-domain violation
+  __shared__ int s_any[S];
+  __shared__ float2 s_bc[S][R];
+  __shared__ uint32_t s_crow[S][R];
+  __shared__ double s_red[GS_STEP_STATS * (NPW + NCW)];
+
+  const int tid = threadIdx.x;
+  const bool producer = tid >= NC;
+  int64_t n_rows = kDense ? P.max_rows : (int64_t)(*P.n_rows_dev);
+  if (STRICT && *P.abort_flag != 0) n_rows = 0;
+  const int64_t n_chunks = (n_rows + R - 1) / R;
+  auto chunk_id = [&](int64_t k) { return (int64_t)blockIdx.x + k * gridDim.x; };
+  auto chunk_rows = [&](int64_t k) -> int {
+    const int64_t rem = n_rows - chunk_id(k) * R;
+    return rem <= 0 ? 0 : (rem < R ? (int)rem : R);
+  };
+  auto stage = [&](int st) { return smem + st * ST::kBytes; };
+  auto sidx = [](int gg, int i, int r) -> int { return r * PL + L::OFF(gg) + (i - r * L::W(gg)); };
+
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full_bar[s], NP);
+      mbar_init(&empty_bar[s], NC);
+    }
+  }
+  if (tid < R * S) {
+    s_badg[tid / R][tid % R] = 0;
+    s_badd[tid / R][tid % R] = 0;
+  }
+  if (tid < S) s_any[tid] = 0;
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  __syncthreads();
+
+  unsigned c_vis = 0, c_step = 0, c_badg = 0, c_badd = 0, c_apre = 0, c_apost = 0, c_clo = 0,
+           c_cls = 0;
+  double s_exo = 0.0, s_exs = 0.0;
+
+  if (producer) {
+    // ------------------------------------------------------------------ producer
+    const int pt = tid - NC;
+    const int lane = pt & 31;
+    const int warp = pt >> 5;
+    auto fetch_id = [&](int64_t k) -> uint32_t {
+      if (lane >= chunk_rows(k)) return 0u;
+      const int64_t i = chunk_id(k) * R + lane;
+      return kDense ? (uint32_t)i : (uint32_t)__ldg(P.rows + i);
+    };
+    uint32_t next_id = fetch_id(0);
+    for (int64_t k = 0; chunk_id(k) < n_chunks; ++k) {
+      const int st = (int)(k % S);
+      const uint32_t my_id = next_id;
+      next_id = fetch_id(k + 1);
+      if (k >= S) mbar_wait(&empty_bar[st], (unsigned)(((k / S) - 1) & 1));
+      const int nv = chunk_rows(k);
+      unsigned char* sb = stage(st);
+      float* srec = reinterpret_cast<float*>(sb);
+      float* sth = reinterpret_cast<float*>(sb + ST::kRec);
+      float* sg = sth + R * PL;
+      if (FLAT) {
+        // array by array over the chunk (all moment records, then theta, then
+        // gradients), 16-byte pieces spread over all producer threads; the row
+        // id of each piece comes from its lane in every warp by shuffle
+        auto id_of = [&](int r) { return __shfl_sync(0xffffffffu, my_id, r & 31); };
+#pragma unroll
+        for (int j = 0; j < (R * kRecPieces + NP - 1) / NP; ++j) {
+          const int p = j * NP + pt;
+          const int r = p / kRecPieces;
+          const uint32_t row = id_of(r);
+          if (r < nv) {
+            const int q = p - r * kRecPieces;
+            cp_async16(srec + r * (2 * SLOTS) + 4 * q, P.record + (size_t)row * P.stride + 4 * q);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < (R * kRowPieces + NP - 1) / NP; ++j) {
+          const int p = j * NP + pt;
+          const int r = p / kRowPieces;
+          const uint32_t row = id_of(r);
+          if (r < nv) {
+            const int q = p - r * kRowPieces;
+            cp_async16(sth + r * PL + 4 * q, P.prec + row * P.prs + 4 * q);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < (R * kRowPieces + NP - 1) / NP; ++j) {
+          const int p = j * NP + pt;
+          const int r = p / kRowPieces;
+          const uint32_t row = id_of(r);
+          if (r < nv) {
+            const int q = p - r * kRowPieces;
+            if (P.grec_ca)
+              cp_async16_ca(sg + r * PL + 4 * q, P.grec + row * P.grs + 4 * q);
+            else
+              cp_async16(sg + r * PL + 4 * q, P.grec + row * P.grs + 4 * q);
+          }
+        }
+      }
+      if (warp == 0 && lane < nv) {
+        // row ids and bias factors ride the stage too, so the consumers
+        // touch no global memory before their barrier; the clock read here
+        // stalls only this producer warp, which runs chunks ahead
+        if (!kDense) cp_async4(&s_crow[st][lane], P.rows + chunk_id(k) * R + lane);
+        const int tb = kDense ? P.global_t
+                              : __ldg(reinterpret_cast<const int*>(P.record + (size_t)my_id * P.stride +
+                                                                   2 * L::P)) + 1;
+        cp_async8(&s_bc[st][lane], P.lut + 2 * (tb < P.lut_len ? tb : P.lut_len - 1));
+      }
+      for (int r = warp; !FLAT && r < nv; r += NPW) {  // warp-uniform
+        const uint32_t row = __shfl_sync(0xffffffffu, my_id, r);
+#pragma unroll
+        for (int j = 0; j < (kPiecesPerRow + 31) / 32; ++j) {
+          const int p = lane + 32 * j;
+          if (p < kRecPieces) {
+            cp_async16(srec + r * (2 * SLOTS) + 4 * p, P.record + (size_t)row * P.stride + 4 * p);
+          } else if (p < kRecPieces + kRowPieces) {
+            const int q = p - kRecPieces;
+            cp_async16(sth + r * PL + 4 * q, P.prec + row * P.prs + 4 * q);
+          } else if (p < kPiecesPerRow) {
+            const int q = p - kRecPieces - kRowPieces;
+            if (P.grec_ca)
+              cp_async16_ca(sg + r * PL + 4 * q, P.grec + row * P.grs + 4 * q);
+            else
+              cp_async16(sg + r * PL + 4 * q, P.grec + row * P.grs + 4 * q);
+          }
+        }
+      }
+      mbar_arrive_cp_async(&full_bar[st]);
+    }
+  } else {
+    // ------------------------------------------------------------------ consumers
+    const int t = tid;
+    StepConsts Kc = P.K;
+    if (kCoupled) {
+      const float nv = P.nv_dev ? (float)(*P.nv_dev) : (float)P.nv_host;
+      Kc.inv_nv = nv != 0.0f ? __frcp_rn(nv) : 0.0f;
+      if (nv == 0.0f) Kc.lam_op = Kc.lam_sc = 0.0f;
+    }
+    const StepConsts& K = kCoupled ? Kc : P.K;
+    float2* const rec_base = reinterpret_cast<float2*>(P.record);
+    const uint32_t rec_stride2 = (uint32_t)(P.stride / 2);
+    for (int64_t k = 0; chunk_id(k) < n_chunks; ++k) {
+      const int st = (int)(k % S);
+      const int ep = (int)(k / S) + 1;  // this use of stage st
+      const int nvalid = chunk_rows(k);
+      if (kDense && t < R) s_crow[st][t] = (uint32_t)(chunk_id(k) * R + t);
+      mbar_wait(&full_bar[st], (unsigned)((k / S) & 1));
+      const unsigned char* sb = stage(st);
+      const float2* srec = reinterpret_cast<const float2*>(sb);
+      const float* sth = reinterpret_cast<const float*>(sb + ST::kRec);
+      const float* sg = sth + R * PL;
+      const uint32_t* srow = s_crow[st];
+      // row ids (sparse modes) and bias factors were staged by the producers
+      const int tn = t < nvalid ? reinterpret_cast<const int*>(srec + t * SLOTS + L::P)[0] + 1 : 0;
+      if (!STRICT) {
+#pragma unroll
+        for (int gg = 0; gg < L::G; ++gg) {
+          const int W = L::W(gg);
+          const int role = L::ROLE(gg);
+          const float lam = role == GS_ROLE_OPACITY ? K.lam_op : role == GS_ROLE_SCALE ? K.lam_sc : 0.f;
+#pragma unroll
+          for (int kk = 0; kk < SH::rounds(gg); ++kk) {
+            const int i = kk * NC + ((t + NC - (R * L::OFF(gg)) % NC) % NC);
+            const int r = i / W;
+            if (i < R * W && r < nvalid) {
+              const int e = sidx(gg, i, r);
+              const bool bg = !isfinite(sg[e]);
+              const bool bd = (role == GS_ROLE_OPACITY || role == GS_ROLE_SCALE) && lam != 0.f &&
+                              domain_bad(role, sth[e]);
+              if (bg) atomicMax(&s_badg[st][r], ep);
+              if (bd) atomicMax(&s_badd[st][r], ep);
+              if (bg || bd) s_any[st] = ep;
+            }
+          }
+        }
+      }
+      named_sync(1, NC);  // flags, row ids and bias factors of the chunk are final
+      const bool any_bad = s_any[st] == ep || nvalid < R;
+      auto row_ok = [&](int r) { return s_badg[st][r] != ep && s_badd[st][r] != ep; };
+      if (t < nvalid) {
+        ++c_vis;
+        if (row_ok(t)) {
+          reinterpret_cast<int*>(rec_base + (size_t)srow[t] * rec_stride2 + L::P)[0] = tn;
+          if (P.D.group >= 0) {
+#pragma unroll
+            for (int gg = 0; gg < L::G; ++gg)
+              if (gg == P.D.group)
+                densify_row(P.D, srow[t], sg + sidx(gg, t * L::W(gg), t), L::W(gg), 1);
+          }
+          ++c_step;
+        } else if (s_badg[st][t] == ep) {
+          ++c_badg;
+        } else {
+          ++c_badd;
+        }
+      }
+      auto update = [&](int gg, int i, int r) {
+        const int W = L::W(gg);
+        const int role = L::ROLE(gg);
+        const int c = i - r * W;
+        const int e = sidx(gg, i, r);
+        const uint32_t row = srow[r];
+        const float2 mv = srec[r * SLOTS + L::OFF(gg) + c];
+        const float th = sth[e];
+        float tnv, mn, vn, ex;
+        bool clipped;
+        update_element<MODE>(role, P.g[gg].lr, th, sg[e], mv.x, mv.y, s_bc[st][r], K, tnv, mn,
+                             vn, ex, clipped);
+        if (!kCoupled && role == GS_ROLE_OPACITY) {
+          c_clo += clipped;
+          s_exo += (double)ex;
+        } else if (!kCoupled && role == GS_ROLE_SCALE) {
+          c_cls += clipped;
+          s_exs += (double)ex;
+        }
+        if (role == GS_ROLE_OPACITY) {
+          c_apre += th > P.active_logit;
+          c_apost += tnv > P.active_logit;
+        }
+        P.g[gg].param[row * P.g[gg].ps + (uint32_t)c] = tnv;
+        rec_base[(size_t)row * rec_stride2 + L::OFF(gg) + c] = make_float2(mn, vn);
+      };
+      if (!any_bad) {
+#pragma unroll
+        for (int gg = 0; gg < L::G; ++gg) {
+#pragma unroll
+          for (int kk = 0; kk < SH::rounds(gg); ++kk) {
+            const int i = kk * NC + ((t + NC - (R * L::OFF(gg)) % NC) % NC);
+            const bool full = (kk + 1) * NC <= R * L::W(gg);  // compile-time
+            if (full || i < R * L::W(gg)) update(gg, i, i / L::W(gg));
+          }
+        }
+      } else {
+#pragma unroll
+        for (int gg = 0; gg < L::G; ++gg) {
+#pragma unroll
+          for (int kk = 0; kk < SH::rounds(gg); ++kk) {
+            const int i = kk * NC + ((t + NC - (R * L::OFF(gg)) % NC) % NC);
+            const int r = i / L::W(gg);
+            if (i < R * L::W(gg) && r < nvalid && row_ok(r)) update(gg, i, r);
+          }
+        }
+      }
+      mbar_arrive(&empty_bar[st]);  // this thread's reads of the stage are done
+    }
+  }
+  cp_async_wait<0>();
+
+  double acc[GS_STEP_STATS] = {(double)c_vis,  (double)c_step, (double)c_badg, (double)c_badd,
+                               (double)c_apre, (double)c_apost, (double)c_clo, (double)c_cls,
+                               s_exo,          s_exs};
+  const bool is_max[GS_STEP_STATS] = {false, false, false, false, false,
+                                      false, false, false, false, false};
+  block_reduce_n<GS_STEP_STATS, (NPW + NCW)>(acc, is_max, s_red);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int f = 0; f < GS_STEP_STATS; ++f)
+      P.partials[(size_t)blockIdx.x * GS_STEP_STATS + f] = acc[f];
+  }
+  if (last_block_arrive(P.counter))
+    final_reduce_n<GS_STEP_STATS, (NPW + NCW)>(P.partials, gridDim.x, GS_STEP_STATS, P.stats_out,
+                                               is_max, s_red);
+}
+
+template <class L, int MODE, bool STRICT, int R, int S, int NPW, int NCW, int MINB, bool FLAT>
+void launch_rec(const FixedParams& P, int64_t max_rows, cudaStream_t s) {
+  constexpr int bytes = S * WsStage<L, R>::kBytes;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(step_rec_kernel<L, MODE, STRICT, R, S, NPW, NCW, MINB, FLAT>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    attr_set = true;
+  }
+  const int64_t chunks = (max_rows + R - 1) / R;
+  const int grid =
+      (int)std::max<int64_t>(1, std::min<int64_t>(chunks, (int64_t)gs_sm_count() * MINB));
+  step_rec_kernel<L, MODE, STRICT, R, S, NPW, NCW, MINB, FLAT>
+      <<<grid, (NPW + NCW) * 32, bytes, s>>>(P);
+}
+
+// ---------------------------------------------------------------------------
 // TMA variant for row-interleaved records (parameters, gradients and the
 // optimizer-state record all row-contiguous): one producer warp moves each
 // visible row with three bulk copies (cp.async.bulk, SASS UBLKCP) — the
@@ -1499,7 +1815,13 @@ void launch_fixed(const FixedParams& P, int64_t max_rows, int kind, cudaStream_t
     // unit's per-operation cost bounds them (~0.86 ms vs 0.67 ms on c3,
     // profiles/r01/ncu_step_tma_c3_record.txt), loads and stores alike.
     const int v = (P.D.group >= 0 || !P.tma_ok) ? 0 : fixed_variant();
-    if (v == 11) {
+    if (v == 8) {
+      launch_ws<L, MODE, STRICT, 32, 3, 3, 8, 2, true>(P, max_rows, s);
+    } else if (v == 13) {
+      launch_rec<L, MODE, STRICT, 32, 3, 3, 8, 2, false>(P, max_rows, s);
+    } else if (v == 14) {
+      launch_rec<L, MODE, STRICT, 32, 3, 2, 8, 2, true>(P, max_rows, s);
+    } else if (v == 11) {
       launch_ws<L, MODE, STRICT, 32, 3, 3, 8, 2, true, true>(P, max_rows, s);
     } else if (v == 9) {
       launch_tma<L, MODE, STRICT, 32, 6, 12, 1>(P, max_rows, s);
@@ -1508,7 +1830,7 @@ void launch_fixed(const FixedParams& P, int64_t max_rows, int kind, cudaStream_t
     } else if (v == 12) {
       launch_tma<L, MODE, STRICT, 32, 3, 8, 2>(P, max_rows, s);
     } else {
-      launch_ws<L, MODE, STRICT, 32, 3, 3, 8, 2, true>(P, max_rows, s);
+      launch_rec<L, MODE, STRICT, 32, 3, 3, 8, 2, true>(P, max_rows, s);
     }
     return;
   }
@@ -1609,6 +1931,8 @@ int gs_step_fixed_try(const gs_group* groups, int32_t n_groups, const gs_step_cf
   using namespace gs;
   if (fixed_variant() < 0) return 0;  // fixed-layout path disabled
   if (!layout_matches<LayoutSH3>(groups, n_groups)) return 0;
+  // every fixed-layout kernel copies the state record in 16-byte pieces
+  if (record_stride % 4 != 0 || (reinterpret_cast<uintptr_t>(record) & 15u) != 0) return 0;
   FixedParams P{};
   const int kind = rows_kind<LayoutSH3>(groups, max_rows, P);
   if (kind < 0) return 0;  // 32-bit element offsets
