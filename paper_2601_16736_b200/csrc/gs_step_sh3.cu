@@ -1209,8 +1209,10 @@ void launch_ws(const FixedParams& P, int64_t max_rows, cudaStream_t s) {
 //     stage's use count (epoch) instead of being reset, so after the single
 //     barrier nothing else needs a block-wide ordering point.
 // ---------------------------------------------------------------------------
-template <class L, int MODE, bool STRICT, int R, int S, int NPW, int NCW, int MINB, bool FLAT>
-__global__ void __launch_bounds__((NPW + NCW) * 32, MINB) step_rec_kernel(const FixedParams P) {
+template <class L, int MODE, bool STRICT, int R, int S, int NPW, int NCW, int MINB, bool FLAT,
+          bool REC>
+__global__ void __launch_bounds__((NPW + NCW) * 32, MINB) step_ring_kernel(const FixedParams P) {
+  static_assert(REC || FLAT, "per-attribute gathers use the flattened producer");
   static_assert(R == 32, "one lane per row id");
   static_assert(S >= 2, "stage reuse relies on the next chunk's barrier");
   constexpr bool kDense = MODE == GS_MODE_COUPLED_ADAM;
@@ -1245,7 +1247,10 @@ __global__ void __launch_bounds__((NPW + NCW) * 32, MINB) step_rec_kernel(const 
     return rem <= 0 ? 0 : (rem < R ? (int)rem : R);
   };
   auto stage = [&](int st) { return smem + st * ST::kBytes; };
-  auto sidx = [](int gg, int i, int r) -> int { return r * PL + L::OFF(gg) + (i - r * L::W(gg)); };
+  // staged theta / grad: row-major for records, group-major for per-attribute gathers
+  auto sidx = [](int gg, int i, int r) -> int {
+    return REC ? r * PL + L::OFF(gg) + (i - r * L::W(gg)) : R * L::OFF(gg) + i;
+  };
 
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
@@ -1301,27 +1306,49 @@ __global__ void __launch_bounds__((NPW + NCW) * 32, MINB) step_rec_kernel(const 
             cp_async16(srec + r * (2 * SLOTS) + 4 * q, P.record + (size_t)row * P.stride + 4 * q);
           }
         }
+        if (REC) {
 #pragma unroll
-        for (int j = 0; j < (R * kRowPieces + NP - 1) / NP; ++j) {
-          const int p = j * NP + pt;
-          const int r = p / kRowPieces;
-          const uint32_t row = id_of(r);
-          if (r < nv) {
-            const int q = p - r * kRowPieces;
-            cp_async16(sth + r * PL + 4 * q, P.prec + row * P.prs + 4 * q);
+          for (int j = 0; j < (R * kRowPieces + NP - 1) / NP; ++j) {
+            const int p = j * NP + pt;
+            const int r = p / kRowPieces;
+            const uint32_t row = id_of(r);
+            if (r < nv) {
+              const int q = p - r * kRowPieces;
+              cp_async16(sth + r * PL + 4 * q, P.prec + row * P.prs + 4 * q);
+            }
           }
-        }
 #pragma unroll
-        for (int j = 0; j < (R * kRowPieces + NP - 1) / NP; ++j) {
-          const int p = j * NP + pt;
-          const int r = p / kRowPieces;
-          const uint32_t row = id_of(r);
-          if (r < nv) {
-            const int q = p - r * kRowPieces;
-            if (P.grec_ca)
-              cp_async16_ca(sg + r * PL + 4 * q, P.grec + row * P.grs + 4 * q);
-            else
-              cp_async16(sg + r * PL + 4 * q, P.grec + row * P.grs + 4 * q);
+          for (int j = 0; j < (R * kRowPieces + NP - 1) / NP; ++j) {
+            const int p = j * NP + pt;
+            const int r = p / kRowPieces;
+            const uint32_t row = id_of(r);
+            if (r < nv) {
+              const int q = p - r * kRowPieces;
+              if (P.grec_ca)
+                cp_async16_ca(sg + r * PL + 4 * q, P.grec + row * P.grs + 4 * q);
+              else
+                cp_async16(sg + r * PL + 4 * q, P.grec + row * P.grs + 4 * q);
+            }
+          }
+        } else {
+          // per-attribute tensors: 4-byte elements in chunk element order,
+          // rotated per group like the consumers (balanced warps)
+          using PS = ChunkShape<L, R, NP>;
+#pragma unroll
+          for (int gg = 0; gg < L::G; ++gg) {
+            const int W = L::W(gg);
+#pragma unroll
+            for (int kk = 0; kk < PS::rounds(gg); ++kk) {
+              const int i = kk * NP + ((pt + NP - (R * L::OFF(gg)) % NP) % NP);
+              const int r = i / W;
+              const uint32_t row = id_of(r);
+              if (i < R * W && r < nv) {
+                const uint32_t c = (uint32_t)(i - r * W);
+                const int e = R * L::OFF(gg) + i;
+                cp_async4(sth + e, P.g[gg].param + row * P.g[gg].ps + c);
+                cp_async4(sg + e, P.g[gg].grad + row * P.g[gg].gs + c);
+              }
+            }
           }
         }
       }
@@ -1491,19 +1518,20 @@ __global__ void __launch_bounds__((NPW + NCW) * 32, MINB) step_rec_kernel(const 
                                                is_max, s_red);
 }
 
-template <class L, int MODE, bool STRICT, int R, int S, int NPW, int NCW, int MINB, bool FLAT>
-void launch_rec(const FixedParams& P, int64_t max_rows, cudaStream_t s) {
+template <class L, int MODE, bool STRICT, int R, int S, int NPW, int NCW, int MINB, bool FLAT,
+          bool REC = true>
+void launch_ring(const FixedParams& P, int64_t max_rows, cudaStream_t s) {
   constexpr int bytes = S * WsStage<L, R>::kBytes;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(step_rec_kernel<L, MODE, STRICT, R, S, NPW, NCW, MINB, FLAT>,
+    cudaFuncSetAttribute(step_ring_kernel<L, MODE, STRICT, R, S, NPW, NCW, MINB, FLAT, REC>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     attr_set = true;
   }
   const int64_t chunks = (max_rows + R - 1) / R;
   const int grid =
       (int)std::max<int64_t>(1, std::min<int64_t>(chunks, (int64_t)gs_sm_count() * MINB));
-  step_rec_kernel<L, MODE, STRICT, R, S, NPW, NCW, MINB, FLAT>
+  step_ring_kernel<L, MODE, STRICT, R, S, NPW, NCW, MINB, FLAT, REC>
       <<<grid, (NPW + NCW) * 32, bytes, s>>>(P);
 }
 
@@ -1818,9 +1846,9 @@ void launch_fixed(const FixedParams& P, int64_t max_rows, int kind, cudaStream_t
     if (v == 8) {
       launch_ws<L, MODE, STRICT, 32, 3, 3, 8, 2, true>(P, max_rows, s);
     } else if (v == 13) {
-      launch_rec<L, MODE, STRICT, 32, 3, 3, 8, 2, false>(P, max_rows, s);
+      launch_ring<L, MODE, STRICT, 32, 3, 3, 8, 2, false>(P, max_rows, s);
     } else if (v == 14) {
-      launch_rec<L, MODE, STRICT, 32, 3, 2, 8, 2, true>(P, max_rows, s);
+      launch_ring<L, MODE, STRICT, 32, 3, 2, 8, 2, true>(P, max_rows, s);
     } else if (v == 11) {
       launch_ws<L, MODE, STRICT, 32, 3, 3, 8, 2, true, true>(P, max_rows, s);
     } else if (v == 9) {
@@ -1830,12 +1858,12 @@ void launch_fixed(const FixedParams& P, int64_t max_rows, int kind, cudaStream_t
     } else if (v == 12) {
       launch_tma<L, MODE, STRICT, 32, 3, 8, 2>(P, max_rows, s);
     } else {
-      launch_rec<L, MODE, STRICT, 32, 3, 3, 8, 2, true>(P, max_rows, s);
+      launch_ring<L, MODE, STRICT, 32, 3, 3, 8, 2, true>(P, max_rows, s);
     }
     return;
   }
   // the densification statistics and strided rows are handled by the
-  // warp-specialised kernel only
+  // default kernel only
   const int variant = (P.D.group >= 0 || kind != 0) ? 0 : fixed_variant();
   switch (variant) {
     case 1: launch_fixed_v<L, MODE, STRICT, 64, 2>(P, max_rows, s); return;
@@ -1844,6 +1872,9 @@ void launch_fixed(const FixedParams& P, int64_t max_rows, int kind, cudaStream_t
     case 4: launch_ws<L, MODE, STRICT, 32, 3, 2, 8, 2>(P, max_rows, s); return;
     case 5: launch_pipe2<L, MODE, STRICT, 32, 3, 2>(P, max_rows, s); return;
     case 6: launch_ws<L, MODE, STRICT, 32, 3, 2, 6, 2>(P, max_rows, s); return;
+    // ring kernel on per-attribute tensors: a shuffle per 4-byte element costs
+    // the producers more than the barrier it saves (0.81 vs 0.78 ms on c3)
+    case 7: launch_ring<L, MODE, STRICT, 32, 3, 3, 8, 2, true, false>(P, max_rows, s); return;
     default: launch_ws<L, MODE, STRICT, 32, 3, 3, 8, 2>(P, max_rows, s); return;
   }
 }

@@ -484,7 +484,7 @@ def test_step_kernels_all_identical(mode, check):
     cfg = S.WorkloadConfig(n=20_011, p_vis=0.4, seed=9)
     host = S.make_params(cfg)
     results = []
-    runs = [("fixed", v, "attr") for v in range(7)] + [("rows", v, "attr") for v in range(7)]
+    runs = [("fixed", v, "attr") for v in range(8)] + [("rows", v, "attr") for v in range(7)]
     runs += [("groups", 0, "attr")]
     runs += [(k, 0, lay) for k in ("fixed", "rows", "groups") for lay in ("record", "param-record")]
     # record layouts: 0/13/14 = record kernel shapes, 8 = record gathers in the generic ring,
@@ -492,7 +492,7 @@ def test_step_kernels_all_identical(mode, check):
     # 11 = cp.async gathers + bulk stores
     runs += [("fixed", v, "record") for v in (8, 9, 10, 11, 12, 13, 14)]
     if check == "strict":
-        runs = [r for r in runs if r[1] in (0, 3, 8, 11, 12)]
+        runs = [r for r in runs if r[1] in (0, 3, 7, 8, 11, 12)]
     prev_f = lib.gs_set_fixed_variant(0)
     prev_r = lib.gs_set_rows_variant(0)
     try:
