@@ -463,8 +463,11 @@ def ours(args, wl, p_vis):
                          "frac": achieved / peak,
                          "traffic": traffic_from_profiles(args.workload, args.mask, p_vis,
                                                           args.params),
-                         "kernel": "gs::step_ws_kernel<LayoutSH3> (K2, warp-specialised, via gs_step_rows)"
-                                   if args.layout == "rows" else "gs::step_kernel (K2, gs_step)",
+                         "kernel": ("gs::step_kernel (K2, gs_step)" if args.layout != "rows" else
+                                    "gs::step_ring_kernel<LayoutSH3, ..., REC> (K2, record "
+                                    "layout, via gs_step_rows)" if args.params == "record" else
+                                    "gs::step_ws_kernel<LayoutSH3> (K2, per-attribute "
+                                    "gathers, via gs_step_rows)"),
                          "peak_source": peak_src,
                          "k2_ms_avg": k2_avg_ms,
                          "k2_bytes_per_launch": sum(k2_bytes) / len(k2_bytes),

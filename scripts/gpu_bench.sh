@@ -11,6 +11,6 @@ done
 CMD="python bench.py --steps 3 --warmup 2 --no-e2e --no-cpu"
 $CMD > gpurun_out/plain_short.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launches.log 2>&1; echo "ncu launches rc=$?"
-ncu --set full --clock-control none --import-source on -k regex:step_ws_kernel -s 2 -c 1 -o gpurun_out/prof_step $CMD > gpurun_out/ncu_full.log 2>&1; echo "ncu full rc=$?"
-ncu --set full --clock-control none --import-source on -k regex:compact_kernel -s 2 -c 1 -o gpurun_out/prof_compact $CMD > gpurun_out/ncu_full_compact.log 2>&1; echo "ncu compact rc=$?"
+ncu --set full --clock-control none --import-source on -k regex:step_ring_kernel -s 2 -c 1 -o gpurun_out/prof_step $CMD > gpurun_out/ncu_full.log 2>&1; echo "ncu full rc=$?"
+python scripts/ncu_summary.py gpurun_out/prof_step.ncu-rep --bytes 2995021752 > gpurun_out/ncu_step_summary.txt 2>&1
 tail -c 3000 gpurun_out/bench_c3.json
