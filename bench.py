@@ -90,6 +90,9 @@ def parse():
     ap.add_argument("--record-align", type=int, default=4,
                     help="parameter / gradient record rows padded to a multiple of this "
                          "many floats (4: 240-byte SH-3 rows; 16: 256-byte, granule-aligned)")
+    ap.add_argument("--host-record-align", type=int, default=64,
+                    help="e2e: pinned host gradient record rows padded to a multiple of this "
+                         "many floats (64: 256-byte rows, two PCIe read lines)")
     ap.add_argument("--params", default="record", choices=["record", "attr"],
                     help="parameter / gradient HBM layout: attribute views of one "
                          "row-interleaved record (records.py) or one tensor per attribute")
@@ -516,9 +519,10 @@ def run_e2e(args, opt, cfg, dev, world, masks, n_vis):
 
     like = opt_grads_like(opt)
     if args.params == "record":
-        # one pinned gradient record: a visible row is one 240-byte PCIe read
+        # one pinned gradient record; rows padded to 256 B = two 128-byte
+        # lines, the granule the zero-copy reads cross PCIe in
         host_rec, host_grads = R.pack({k: torch.zeros(t.shape) for k, t in like.items()},
-                                      pin_memory=True)
+                                      align=args.host_record_align, pin_memory=True)
         dev_grads = R.views_like(torch.empty_like(host_rec, device=dev), like)
     else:
         host_grads = {k: torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
@@ -533,6 +537,7 @@ def run_e2e(args, opt, cfg, dev, world, masks, n_vis):
     row_bytes = sum(t[0].numel() * 4 for t in host_grads.values())
     dense = sum(t.numel() * 4 for t in host_grads.values())
     host_dense = ([host_rec] if args.params == "record" else list(host_grads.values()))
+    dense = sum(t.numel() * 4 for t in host_dense)
     dev_dense = ([dev_grads[next(iter(dev_grads))]._base] if args.params == "record"
                  else list(dev_grads.values()))
     d2h = stats_host.numel() * 8
