@@ -187,59 +187,103 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------ CPU baseline
-def cpu_reference_rate(wl: dict, p_vis: float, mask: str, budget_s: float, steps=None, warmup=1,
-                       seed=0):
-    """Time the reference algorithm (float64 oracle port of dar_step /
-    sparse_adam_step, optimizer.py:231-298) on a bounded sample of the
-    workload: the same layout, distributions, visibility fraction and mode,
-    on fewer rows.  Returns (visible/s, sample description, per-step rows)."""
+def _ref_shard_worker(wid, n_rows, p_vis, mask, seed, wl, n_steps, barrier, out_q):
+    """One host process of the reference arm: the float64 port of the
+    reference step (oracle/adamw_gs_oracle.py, optimizer.py:231-298) over its
+    own row shard. Rows are independent, so shards run in parallel. Every
+    step starts behind a barrier, and the step time is the slowest shard's."""
     import numpy as np
 
     from oracle import adamw_gs_oracle as O
     from paper_2601_16736_b200 import synthetic as S
 
-    def run(n_rows, n_steps):
-        cfg = S.WorkloadConfig(n=n_rows, p_vis=p_vis, mask_family=mask, seed=seed)
-        lay = O.LAYOUT_SH3
-        host = S.make_params(cfg)
-        p = {k: v.astype(np.float64) for k, v in host.items()}
-        m = {g.name: np.zeros((n_rows, g.width)) for g in lay}
-        v = {g.name: np.zeros((n_rows, g.width)) for g in lay}
-        t = np.zeros(n_rows, np.int64)
-        hp = O.Hyper(lr=S.LR_SH3, lambda_o=wl["lo"], lambda_s=wl["ls"])
-        grad_sets = []
-        for s in range(min(n_steps, 3)):
-            vis = S.visibility(cfg, s)
-            grad_sets.append({k: x.astype(np.float64)
-                              for k, x in S.step_grads(cfg, s, vis).items()})
-        times, nv = [], []
-        for s in range(n_steps):
-            vis = S.visibility(cfg, s)
-            g = {k: x.copy() for k, x in grad_sets[s % len(grad_sets)].items()}
-            t0 = time.perf_counter()
-            if wl["mode"] == "adamw-gs":
-                O.dar_step_f64(lay, p, g, m, v, t, vis, hp, cfg.n_pixels)
-            else:
-                reg = O.coupled_reg_grad_f64(lay, p, vis, wl["lo"], wl["ls"])
-                for k, r in reg.items():
-                    g[k] = g[k] + r
-                O.sparse_adam_step_f64(lay, p, g, m, v, t, vis, hp)
-            times.append(time.perf_counter() - t0)
-            nv.append(int(vis.sum()))
+    cfg = S.WorkloadConfig(n=n_rows, p_vis=p_vis, mask_family=mask, seed=seed * 1000 + wid)
+    lay = O.LAYOUT_SH3
+    host = S.make_params(cfg)
+    p = {k: v.astype(np.float64) for k, v in host.items()}
+    m = {g.name: np.zeros((n_rows, g.width)) for g in lay}
+    v = {g.name: np.zeros((n_rows, g.width)) for g in lay}
+    t = np.zeros(n_rows, np.int64)
+    hp = O.Hyper(lr=S.LR_SH3, lambda_o=wl["lo"], lambda_s=wl["ls"])
+    grad_sets, masks = [], []
+    for s in range(min(n_steps, 3)):
+        vis = S.visibility(cfg, s)
+        masks.append(vis)
+        grad_sets.append({k: x.astype(np.float64) for k, x in S.step_grads(cfg, s, vis).items()})
+    times, nv = [], []
+    for s in range(n_steps):
+        vis = masks[s % len(masks)]
+        g = {k: x.copy() for k, x in grad_sets[s % len(grad_sets)].items()}
+        if barrier is not None:
+            barrier.wait()
+        t0 = time.perf_counter()
+        if wl["mode"] == "adamw-gs":
+            O.dar_step_f64(lay, p, g, m, v, t, vis, hp, cfg.n_pixels)
+        else:
+            reg = O.coupled_reg_grad_f64(lay, p, vis, wl["lo"], wl["ls"])
+            for k, r in reg.items():
+                g[k] = g[k] + r
+            O.sparse_adam_step_f64(lay, p, g, m, v, t, vis, hp)
+        times.append(time.perf_counter() - t0)
+        nv.append(int(vis.sum()))
+    if out_q is None:
         return times, nv
+    out_q.put((wid, times, nv))
+    return None
 
-    # calibrate on a small sample, then size the sample to the budget
+
+def host_workers() -> int:
+    try:
+        return max(1, len(os.sched_getaffinity(0)))
+    except AttributeError:
+        return max(1, os.cpu_count() or 1)
+
+
+def cpu_reference_rate(wl: dict, p_vis: float, mask: str, budget_s: float, steps=None, warmup=1,
+                       seed=0, workers: int = 1):
+    """Time the reference algorithm (float64 oracle port of dar_step /
+    sparse_adam_step, optimizer.py:231-298) on a bounded sample of the
+    workload: the same layout, distributions, visibility fraction and mode.
+    ``workers`` host processes each own one row shard (rows are independent;
+    NumPy's elementwise kernels are single-threaded). Returns (visible/s,
+    sample description, rows, per-step times)."""
+    import multiprocessing as mp
+
+    # calibrate one process on a small shard, then size the sample to the budget
     n0 = 20_000
-    tt, nv = run(n0, 2)
-    rate = nv[-1] / max(tt[-1], 1e-9)
+    tt, nv = _ref_shard_worker(0, n0, p_vis, mask, seed, wl, 2, None, None)
+    rate1 = nv[-1] / max(tt[-1], 1e-9)
     n_steps = steps if steps is not None else 4
-    rows = int(min(wl["n"], max(n0, rate * budget_s / max(n_steps + warmup, 1) / p_vis)))
-    tt, nv = run(rows, n_steps + warmup)
-    tt, nv = tt[warmup:], nv[warmup:]
-    value = sum(nv) / sum(tt)
-    sample = (f"{rows} of {wl['n']} rows, {n_steps} timed steps after {warmup} warm-up, float64 "
-              f"NumPy port of the reference step (oracle/adamw_gs_oracle.py), 1 thread")
-    return value, sample, rows, tt
+    total = n_steps + warmup
+    workers = max(1, int(workers))
+    # memory-bandwidth contention: assume half the per-process rate when parallel
+    eff = rate1 * (workers if workers == 1 else workers / 2)
+    rows = int(min(wl["n"], max(n0 * workers, eff * budget_s / max(total, 1) / p_vis)))
+    shard = rows // workers
+    rows = shard * workers
+    if workers == 1:
+        per = [_ref_shard_worker(0, shard, p_vis, mask, seed, wl, total, None, None)]
+    else:
+        ctx = mp.get_context("spawn")
+        barrier = ctx.Barrier(workers)
+        q = ctx.Queue()
+        procs = [ctx.Process(target=_ref_shard_worker,
+                             args=(w, shard, p_vis, mask, seed, wl, total, barrier, q))
+                 for w in range(workers)]
+        for pr in procs:
+            pr.start()
+        got = [q.get() for _ in procs]
+        for pr in procs:
+            pr.join()
+        per = [(tm, n) for _, tm, n in sorted(got)]
+    step_t = [max(p[0][s] for p in per) for s in range(warmup, total)]
+    step_nv = [sum(p[1][s] for p in per) for s in range(warmup, total)]
+    value = sum(step_nv) / sum(step_t)
+    sample = (f"{rows} of {wl['n']} rows in {workers} row shard(s), {n_steps} timed steps after "
+              f"{warmup} warm-up, float64 NumPy port of the reference step "
+              f"(oracle/adamw_gs_oracle.py), {workers} host process(es) x 1 thread; "
+              f"step time = slowest shard")
+    return value, sample, rows, step_t
 
 
 def reference_arm(args, wl, p_vis):
@@ -248,10 +292,10 @@ def reference_arm(args, wl, p_vis):
         return
     budget = args.ref_seconds
     import numpy as np  # noqa: F401
+    cores = host_workers()
     value, sample, rows, tt = cpu_reference_rate(
         wl, p_vis, args.mask, budget_s=budget * 0.8, steps=args.steps, warmup=args.warmup,
-        seed=args.seed)
-    cores = 1
+        seed=args.seed, workers=cores)
     line = {
         "metric": "visible Gaussians updated/sec per optimizer step",
         "value": value, "unit": "visible Gaussians/s", "n_gpus": args.gpus, "steps": args.steps,
@@ -449,9 +493,10 @@ def ours(args, wl, p_vis):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
+        cores = host_workers()
         v, sample, _, _ = cpu_reference_rate(wl, p_vis, args.mask, budget_s=args.cpu_seconds,
-                                              seed=args.seed)
-        cpu = {"value": v, "unit": "visible Gaussians/s", "cores": 1, "kind": "port",
+                                              seed=args.seed, workers=cores)
+        cpu = {"value": v, "unit": "visible Gaussians/s", "cores": cores, "kind": "port",
                "sample": sample, "host_cpus": os.cpu_count()}
 
     if rank == 0:
