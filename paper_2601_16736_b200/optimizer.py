@@ -266,7 +266,9 @@ class AdamWGS:
                                             state_layout)
         self.engine = StepEngine(self.n_rows, self.device, self.beta1, self.beta2)
         self._stats_host = torch.zeros(L.GS_STEP_STATS, dtype=torch.float64, pin_memory=True)
+        self._abort_host = torch.zeros(1, dtype=torch.int32, pin_memory=True)
         self._pending = None
+        self._capturing = False
         self._last_ctx = None
         self._densify = None  # (accum, count, group index) when enabled
 
@@ -383,12 +385,41 @@ class AdamWGS:
         self._stats_host.copy_(stats, non_blocking=True)
         abort = None
         if self.check == "strict":
-            abort = self.engine.abort.to("cpu", non_blocking=True)
+            self._abort_host.copy_(self.engine.abort, non_blocking=True)
+            abort = self._abort_host
+        if self._capturing:  # StepGraph.replay() arms the check after each replay
+            return
         ev = torch.cuda.Event()
         ev.record(torch.cuda.current_stream(self.device))
         self._pending = (ev, abort)
         if self.errors == "raise":
             self._raise_pending()
+
+    def _arm_after_replay(self):
+        if self.errors == "ignore":
+            return
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(self.device))
+        self._pending = (ev, self._abort_host if self.check == "strict" else None)
+        if self.errors == "raise":
+            self._raise_pending()
+
+    # ------------------------------------------------------------ CUDA graphs
+    def capture(self, visibility: torch.Tensor, n_pixels: int | None = None, *,
+                grads=None, **step_kwargs) -> "StepGraph":
+        """Capture one :meth:`step` (compaction + fused step, statistics copy)
+        as a CUDA graph over static buffers, for clouds small enough that host
+        launch latency rivals the GPU work.  Refill ``visibility`` and the
+        gradient tensors in place, then call ``StepGraph.replay()``; scalars
+        (n_pixels, lambdas, clip, lr scale) are fixed at capture — capture
+        again when they change.  Errors surface after each replay as
+        configured (``errors="raise"`` synchronises, ``"defer"`` raises at
+        the next step / :meth:`check_errors`).  The dense coupled-adam mode
+        keeps a host-side global clock and is not capturable."""
+        if self.mode == "coupled-adam":
+            raise ConfigError("coupled-adam advances a host-side global clock; capture the "
+                              "sparse modes")
+        return StepGraph(self, visibility, n_pixels, grads, step_kwargs)
 
     def _raise_pending(self):
         if self._pending is None:
@@ -567,3 +598,40 @@ def _moment_stats(engine: StepEngine, bindings, alive, record=None) -> dict:
             "max_abs_m_over_sqrt_v": m_rt if n_pos else 0.0,
         }
     return res
+
+
+class StepGraph:
+    """A captured :meth:`AdamWGS.step` (see :meth:`AdamWGS.capture`)."""
+
+    def __init__(self, opt: AdamWGS, visibility: torch.Tensor, n_pixels, grads, step_kwargs):
+        self.opt = opt
+        self.visibility = visibility
+        self.grads = grads
+        opt._raise_pending()
+        dev = opt.device
+        # host-side caches (ctypes group array, lazily allocated scratch) are
+        # built outside the capture: one binding pass, no kernel launches
+        opt.engine.group_array(opt._bindings(grads, step_kwargs.get("mu_lr_scale", 1.0)))
+        self.graph = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream(dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        launches = opt.engine.launches
+        opt._capturing = True
+        try:
+            with torch.cuda.stream(side):
+                with torch.cuda.graph(self.graph, stream=side):
+                    opt.step(visibility, n_pixels, grads=grads, **step_kwargs)
+        finally:
+            opt._capturing = False
+        torch.cuda.current_stream(dev).wait_stream(side)
+        self.launches_per_replay = opt.engine.launches - launches
+        opt.engine.launches = launches
+
+    def replay(self):
+        """One optimizer step on the current contents of the static buffers."""
+        opt = self.opt
+        opt._raise_pending()
+        self.graph.replay()
+        opt.engine.launches += self.launches_per_replay
+        opt._arm_after_replay()
+

@@ -634,3 +634,53 @@ def test_pinned_host_grads_zero_copy_identical(check):
     with pytest.raises(ConfigError):
         opt.step(torch.from_numpy(vis).to("cuda:0"), cfg.n_pixels,
                  grads={k: torch.from_numpy(x) for k, x in g.items()})
+
+
+@pytest.mark.parametrize("mode", ["adamw-gs", "sparse-adam"])
+@pytest.mark.parametrize("check", ["fused", "strict"])
+def test_captured_step_graph_matches_eager(mode, check):
+    """AdamWGS.capture: K1 + K2 (+ strict check) replayed as one CUDA graph
+    over refilled static buffers gives bitwise the eager steps, and a bad
+    gradient still raises GradientError with its row after the replay."""
+    from paper_2601_16736_b200 import records as R
+    from paper_2601_16736_b200 import synthetic as S
+    from paper_2601_16736_b200.engine import ConfigError, GradientError
+    from paper_2601_16736_b200.optimizer import AdamWGS
+    cfg = S.WorkloadConfig(n=30_001, p_vis=0.3, seed=31)
+    host = S.make_params(cfg)
+    outs = []
+    for how in ("eager", "graph"):
+        _, params = R.pack({k: torch.from_numpy(v).to(DEV) for k, v in host.items()})
+        opt = AdamWGS(S.param_groups(params), mode=mode, lambda_o=1e-3, lambda_s=1e-5,
+                      check=check)
+        grec, grads = R.pack({k: torch.zeros(v.shape, device=DEV) for k, v in host.items()})
+        vis_buf = torch.zeros(cfg.n, dtype=torch.bool, device=DEV)
+        graph = opt.capture(vis_buf, cfg.n_pixels, grads=grads) if how == "graph" else None
+        for s in range(4):
+            vis = S.visibility(cfg, s)
+            g = S.step_grads(cfg, s, vis)
+            vis_buf.copy_(torch.from_numpy(vis))
+            for k, x in g.items():
+                grads[k].copy_(torch.from_numpy(x).view(grads[k].shape))
+            if graph is None:
+                opt.step(vis_buf, cfg.n_pixels, grads=grads)
+            else:
+                graph.replay()
+        torch.cuda.synchronize()
+        outs.append(({k: p.cpu().numpy() for k, p in params.items()},
+                     opt.state.record.cpu().numpy(), opt.last_stats()))
+        if graph is not None:
+            assert graph.launches_per_replay >= 3
+            bad = int(np.flatnonzero(vis)[5])
+            grads["f_rest"][bad, 2] = float("nan")
+            with pytest.raises(GradientError) as ei:
+                graph.replay()
+            assert bad in ei.value.ids.tolist()
+    a, b = outs
+    for k in a[0]:
+        assert np.array_equal(a[0][k], b[0][k]), k
+    assert np.array_equal(a[1], b[1])
+    assert a[2] == b[2]
+    with pytest.raises(ConfigError):
+        AdamWGS(S.param_groups({k: torch.from_numpy(v).to(DEV) for k, v in host.items()}),
+                mode="coupled-adam").capture(vis_buf, None)
