@@ -100,10 +100,16 @@ def _ptr(t: torch.Tensor | None) -> int | None:
 
 
 def _strides(t: torch.Tensor | None):
-    return None if t is None else (tuple(t.shape), t.stride())
+    return None if t is None else t.stride()
+
+
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
 
 
 def _stream_handle(device: torch.device) -> int:
+    if _raw_stream is not None:  # the current stream's handle without a Stream object
+        return _raw_stream(device.index if device.index is not None else
+                           torch.cuda.current_device())
     return torch.cuda.current_stream(device).cuda_stream
 
 
@@ -125,7 +131,7 @@ class GroupBinding:
         t = self.param if self.param is not None else self.exp_avg
         if t is None:
             return int(self.w)
-        return max(1, int(np.prod(t.shape[1:]))) if t.dim() > 1 else 1
+        return max(1, t.shape[1:].numel()) if t.dim() > 1 else 1
 
 
 def row_stride(name, t: torch.Tensor, n_rows: int, width: int) -> int:
@@ -196,6 +202,10 @@ class StepEngine:
         self.launches = 0  # C-ABI kernel launches issued (bench accounting)
         self._group_cache_key = None
         self._group_cache = None
+        self._record_ok = None
+        self._omb1 = float(np.float32(1.0 - self.beta1))
+        self._omb2 = float(np.float32(1.0 - self.beta2))
+        self._eps32 = {}
 
     # ------------------------------------------------------------------ groups
     def group_array(self, groups: list[GroupBinding], need_grad: bool = True):
@@ -358,9 +368,12 @@ class StepEngine:
         cfg = L.GsStepCfg()
         cfg.mode = L.MODE_IDS[mode]
         cfg.check = L.CHECK_STRICT if check == "strict" else L.CHECK_FUSED
-        cfg.one_minus_beta1 = float(np.float32(1.0 - self.beta1))
-        cfg.one_minus_beta2 = float(np.float32(1.0 - self.beta2))
-        cfg.eps = float(np.float32(eps))
+        cfg.one_minus_beta1 = self._omb1
+        cfg.one_minus_beta2 = self._omb2
+        e32 = self._eps32.get(eps)
+        if e32 is None:
+            e32 = self._eps32[eps] = float(np.float32(eps))
+        cfg.eps = e32
         cfg.active_logit = self.active_logit
         cfg.lambda_opacity = float(lambda_opacity)
         cfg.lambda_scale = float(lambda_scale)
@@ -406,12 +419,17 @@ class StepEngine:
         return self.stats
 
     def _check_record(self, record: torch.Tensor, groups):
+        key = (record.data_ptr(), tuple(record.shape), record.stride(), record.dtype,
+               tuple(g.width for g in groups))
+        if key == self._record_ok:
+            return
         p = sum(g.width for g in groups)
         if (record.device != self.device or record.dtype != torch.float32 or record.dim() != 2
                 or record.shape[0] != self.n_rows or record.stride(1) != 1
                 or record.shape[1] < 2 * (p + 1)):
             raise ConfigError(f"state record must be fp32 [{self.n_rows}, >= {2 * (p + 1)}] "
                               f"with unit column stride, got {tuple(record.shape)}")
+        self._record_ok = key
 
     def all_rows(self) -> tuple[torch.Tensor, torch.Tensor]:
         """Identity index list (dense mode domain checks, error ids)."""
