@@ -207,6 +207,16 @@ int gs_aiu_apply_rows(const gs_group* groups, int32_t n_groups, float* record,
                       const int32_t* k_dev, int64_t max_k, const float* bias_lut,
                       int32_t lut_len, float eps, int32_t* picked_out, void* stream);
 
+/* MCMC relocation (pipeline.py:197-233): for i < k, row dead[i] takes every
+ * attribute of row targets[i]; the opacity group (width 1) of both rows is set
+ * to tau_new[i] (the blend-preserving logit, float64 on the host); the state
+ * record row of dead[i] is zeroed (moments and clock, reset_rows,
+ * optimizer.py:159-165).  Dead rows must be distinct and disjoint from the
+ * targets (the reference's dead / live split guarantees it). */
+int gs_relocate_rows(const gs_group* groups, int32_t n_groups, int32_t opacity_group,
+                     const int32_t* dead, const int32_t* targets, const float* tau_new,
+                     int64_t k, float* record, int64_t record_stride, void* stream);
+
 /* Opacity-gated position noise (optimizer.py:453-486): for every alive row,
  * delta = -eta_ratio * lr_position * sigmoid(-lambda_mu (sigmoid(tau) -
  * lambda_t)) * Sigma gamma, Sigma = R diag(exp(2 log_scale)) R^T, gamma from a

@@ -640,3 +640,47 @@ def aiu_apply_fp32(layout, params, m, v, t, picked, lr, eta, eps, lut):
         vh = v[g.name][rows] * c2
         den = np.sqrt(vh) + F32(eps)
         params[g.name][rows] = params[g.name][rows] - (F32(lr[g.name] * eta) * mh) / den
+
+
+def _sigmoid_ref_f64(tau):
+    """activate_opacity (primitives.py:51-59), float64, branch-stable."""
+    t = np.asarray(tau, np.float64)
+    out = np.empty_like(t)
+    pos = t >= 0
+    out[pos] = 1.0 / (1.0 + np.exp(-t[pos]))
+    e = np.exp(t[~pos])
+    out[~pos] = e / (1.0 + e)
+    return out
+
+
+def mcmc_relocate_f64(layout, params, m, v, t, alive, rng, opacity="tau"):
+    """mcmc_relocate (pipeline.py:197-233) on host arrays, float64: dead rows
+    (alive, o <= 1/255) take the attributes of opacity-weighted live targets
+    drawn with ``rng.choice``; target and respawns share the blend-preserving
+    opacity 1 - (1 - o)^(1/(k+1)) (_clone_opacity, pipeline.py:110-113); the
+    respawns' moments and clocks are reset (optimizer.py:159-165).  Returns
+    the dead rows."""
+    o = _sigmoid_ref_f64(params[opacity].reshape(-1))
+    alive = np.ones(o.size, bool) if alive is None else np.asarray(alive, bool)
+    dead = np.flatnonzero(alive & (o <= 1.0 / 255.0))
+    live = np.flatnonzero(alive & (o > 1.0 / 255.0))
+    if live.size == 0:
+        raise RuntimeError("no alive primitives to relocate onto")
+    if dead.size == 0:
+        return dead
+    probs = o[live] / o[live].sum()
+    targets = live[rng.choice(live.size, size=dead.size, p=probs)]
+    uniq, inverse, counts = np.unique(targets, return_inverse=True, return_counts=True)
+    k = np.asarray(counts + 1.0, np.float64)
+    o_new = 1.0 - np.power(1.0 - o[uniq], 1.0 / k)
+    tau_new = np.log(o_new / (1.0 - o_new))
+    for g in layout:
+        if g.name != opacity:
+            params[g.name][dead] = params[g.name][targets]
+    params[opacity].reshape(-1)[dead] = tau_new[inverse]
+    params[opacity].reshape(-1)[uniq] = tau_new
+    for g in layout:
+        m[g.name][dead] = 0.0
+        v[g.name][dead] = 0.0
+    t[dead] = 0
+    return dead

@@ -81,6 +81,9 @@ SIGNATURES = {
     "gs_aiu_apply_rows": (C.c_int, [C.POINTER(GsGroup), C.c_int32, C.c_void_p, C.c_int64,
                                     C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
                                     C.c_int32, C.c_float, C.c_void_p, C.c_void_p]),
+    "gs_relocate_rows": (C.c_int, [C.POINTER(GsGroup), C.c_int32, C.c_int32, C.c_void_p,
+                                   C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,
+                                   C.c_void_p]),
     "gs_noise_perturb": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                    C.c_int64, C.c_int32, C.c_float, C.c_float, C.c_float,
                                    C.c_float, C.c_uint64, C.c_uint32, C.c_void_p, C.c_int32,

@@ -562,3 +562,80 @@ extern "C" int gs_aiu_apply_rows(const gs_group* groups, int32_t n_groups, float
       S, P, record, record_stride, inv_idx, jlist, k_dev, bias_lut, lut_len, eps, picked_out);
   return gs_check_launch("gs_aiu_apply_rows");
 }
+
+// ---------------------------------------------------------------------------
+// MCMC relocation (pipeline.py:197-233): every dead row takes its target's
+// attributes, the target and its respawns share the blend-preserving opacity
+// tau_new (computed on the host in float64 with the reference's formula,
+// 1 - (1 - o)^(1/(k+1)), since the host draws the targets anyway), and the
+// respawned rows restart with zero moments and clock (reset_rows,
+// optimizer.py:159-165).  A warp owns a dead row.  Dead rows are distinct and
+// never targets, and the kernel never reads tau, so the writes race with no
+// read: a target shared by several respawns receives the same value from each.
+// ---------------------------------------------------------------------------
+namespace gs {
+
+__global__ void __launch_bounds__(kThreads)
+    relocate_rows_kernel(const GroupSet S, int opacity_group, const int32_t* __restrict__ dead,
+                         const int32_t* __restrict__ targets, const float* __restrict__ tau_new,
+                         int64_t k, float* __restrict__ record, int64_t stride, int rec_elems) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (kThreads / 32);
+  for (int64_t i = (int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5); i < k; i += warps) {
+    const int64_t d = __ldg(dead + i);
+    const int64_t t = __ldg(targets + i);
+    for (int gi = 0; gi < S.n; ++gi) {
+      const GroupPtrs& G = S.g[gi];
+      if (gi == opacity_group) {
+        if (lane == 0) {
+          const float tn = __ldg(tau_new + i);
+          G.param[d * G.ps] = tn;
+          G.param[t * G.ps] = tn;
+        }
+        continue;
+      }
+      for (int c = lane; c < G.width; c += 32) G.param[d * G.ps + c] = G.param[t * G.ps + c];
+    }
+    float* rec = record + d * stride;
+    for (int c = lane; c < rec_elems; c += 32) rec[c] = 0.0f;  // (m, v) pairs, clock, pad
+  }
+}
+
+}  // namespace gs
+
+extern "C" int gs_relocate_rows(const gs_group* groups, int32_t n_groups, int32_t opacity_group,
+                                const int32_t* dead, const int32_t* targets,
+                                const float* tau_new, int64_t k, float* record,
+                                int64_t record_stride, void* stream) {
+  using namespace gs;
+  GroupSet S{};
+  if (!groups || n_groups < 1 || n_groups > GS_MAX_GROUPS || opacity_group < 0 ||
+      opacity_group >= n_groups || groups[opacity_group].width != 1) {
+    gs_set_error("gs_relocate_rows: bad group list / opacity group");
+    return GS_ERR_ARG;
+  }
+  S.n = n_groups;
+  int P = 0;
+  for (int i = 0; i < n_groups; ++i) {
+    if (!groups[i].param || groups[i].width < 1 || !strides_ok(groups[i])) {
+      gs_set_error("gs_relocate_rows: group %d invalid", i);
+      return GS_ERR_ARG;
+    }
+    S.g[i] = group_ptrs(groups[i], false, false, 0.f);
+    P += (int)groups[i].width;
+  }
+  int rc = record_args(record, record_stride, P, "gs_relocate_rows");
+  if (rc) return rc;
+  if (k < 0 || (k > 0 && (!dead || !targets || !tau_new))) {
+    gs_set_error("gs_relocate_rows: bad row lists");
+    return GS_ERR_ARG;
+  }
+  if (k == 0) return GS_OK;
+  const int64_t warps_needed = k;
+  const int grid = (int)std::max<int64_t>(
+      1, std::min<int64_t>((warps_needed + kThreads / 32 - 1) / (kThreads / 32),
+                           (int64_t)gs_sm_count() * 8));
+  relocate_rows_kernel<<<grid, kThreads, 0, (cudaStream_t)stream>>>(
+      S, opacity_group, dead, targets, tau_new, k, record, record_stride, 2 * (P + 1));
+  return gs_check_launch("gs_relocate_rows");
+}

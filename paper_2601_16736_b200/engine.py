@@ -431,6 +431,27 @@ class StepEngine:
                               f"with unit column stride, got {tuple(record.shape)}")
         self._record_ok = key
 
+    def relocate(self, groups: list[GroupBinding], record: torch.Tensor, opacity_group: int,
+                 dead: torch.Tensor, targets: torch.Tensor, tau_new: torch.Tensor):
+        """MCMC relocation row movement (gs_relocate_rows, pipeline.py:221-228)."""
+        self._check_record(record, groups)
+        arr = (L.GsGroup * len(groups))()
+        for i, g in enumerate(groups):
+            ps = _check_tensor(f"{g.name}.param", g.param, self.n_rows, g.width, self.device,
+                               strided=True)
+            arr[i] = L.GsGroup(_ptr(g.param), None, None, None, g.width, g.role, 0.0, ps, 0)
+        k = int(dead.numel())
+        for name, t, dt in (("dead", dead, torch.int32), ("targets", targets, torch.int32),
+                            ("tau_new", tau_new, torch.float32)):
+            if t.device != self.device or t.dtype != dt or t.numel() != k or not t.is_contiguous():
+                raise ConfigError(f"{name} must be a contiguous {dt} CUDA tensor of {k} entries")
+        rc = self.lib.gs_relocate_rows(arr, len(groups), int(opacity_group), dead.data_ptr(),
+                                       targets.data_ptr(), tau_new.data_ptr(), k,
+                                       record.data_ptr(), record.stride(0),
+                                       _stream_handle(self.device))
+        L.check(rc, "gs_relocate_rows")
+        self.launches += 1 if k else 0
+
     def all_rows(self) -> tuple[torch.Tensor, torch.Tensor]:
         """Identity index list (dense mode domain checks, error ids)."""
         if getattr(self, "_all_rows", None) is None:

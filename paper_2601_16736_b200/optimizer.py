@@ -404,6 +404,52 @@ class AdamWGS:
         if self.errors == "raise":
             self._raise_pending()
 
+    # ------------------------------------------------------ structural ops
+    def relocate_rows(self, plan) -> None:
+        """Apply a relocation plan (structural.RelocationPlan): respawn rows
+        take their target's attributes, target and respawn share the planned
+        opacity logit, respawn state is reset (pipeline.py:221-228)."""
+        if plan.count == 0:
+            return
+        opac = [i for i, g in enumerate(self.param_groups) if g["role"] == L.ROLE_OPACITY]
+        if len(opac) != 1:
+            raise ConfigError("relocation needs exactly one opacity group")
+        dev = self.device
+        dead = torch.from_numpy(plan.dead.astype(np.int32)).to(dev)
+        targets = torch.from_numpy(plan.targets.astype(np.int32)).to(dev)
+        tau_new = torch.from_numpy(plan.tau_new.astype(np.float32)).to(dev)
+        groups = self._state_bindings()
+        if self.state.record is not None:
+            self.engine.relocate(groups, self.state.record, opac[0], dead, targets, tau_new)
+            return
+        # per-group state layout: the row copies as device gathers, then K3 reset
+        with torch.no_grad():
+            for i, g in enumerate(self.param_groups):
+                p = g["params"][0]
+                if i == opac[0]:
+                    col = p.reshape(p.shape[0], -1)[:, 0]
+                    col[dead.long()] = tau_new
+                    col[targets.long()] = tau_new
+                else:
+                    p[dead.long()] = p[targets.long()]
+        self.reset_rows(dead)
+
+    def mcmc_relocate(self, rng: np.random.Generator, alive=None):
+        """mcmc_relocate (pipeline.py:197-233): plan on the host with the
+        caller's Generator (targets identical to the reference's), move rows
+        on the GPU. Returns the RelocationPlan (``count``, ``ids_hash()``
+        match the reference's relocate event)."""
+        from .structural import mcmc_plan
+        opac = [g for g in self.param_groups if g["role"] == L.ROLE_OPACITY]
+        if len(opac) != 1:
+            raise ConfigError("relocation needs exactly one opacity group")
+        tau = opac[0]["params"][0].detach().reshape(-1).cpu().numpy()
+        if alive is not None and isinstance(alive, torch.Tensor):
+            alive = alive.detach().cpu().numpy()
+        plan = mcmc_plan(tau, alive, rng)
+        self.relocate_rows(plan)
+        return plan
+
     # ------------------------------------------------------------ CUDA graphs
     def capture(self, visibility: torch.Tensor, n_pixels: int | None = None, *,
                 grads=None, **step_kwargs) -> "StepGraph":

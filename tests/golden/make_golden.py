@@ -320,6 +320,51 @@ def run_aiu(name="aiu", n=200, seed=21):
     save(name, meta, arrays)
 
 
+def run_relocate(name="relocate", n=300, seed=41):
+    """mcmc_relocate (pipeline.py:197-233) on the native 2-D layout: the
+    reference draws the targets and rewrites the set; recorded before/after."""
+    gradients, optimizer, primitives, loss = _import_reference()
+    import splatlab.pipeline as pipeline
+    rng = np.random.default_rng(seed)
+    p0 = {"mu": f32(rng.normal(0, 5, (n, 2))),
+          "kappa": f32(rng.uniform(math.log(1e-3), math.log(0.5), (n, 2))),
+          "rot": f32(rng.normal(0, 1, (n, 1))), "tau": f32(rng.normal(0.0, 2.0, (n, 1))),
+          "color": f32(rng.normal(0, 0.5, (n, 3)))}
+    dead = rng.random(n) < 0.25                 # well below 1/255
+    p0["tau"][dead, 0] = f32(rng.uniform(-12.0, -6.0, int(dead.sum())))
+    alive = rng.random(n) < 0.95
+    ps = primitives.PrimitiveSet(mu=p0["mu"].astype(np.float64),
+                                 kappa=p0["kappa"].astype(np.float64),
+                                 rot=p0["rot"][:, 0].astype(np.float64),
+                                 tau=p0["tau"][:, 0].astype(np.float64),
+                                 color=p0["color"].astype(np.float64), depth=np.zeros(n),
+                                 alive=alive)
+    st = optimizer.MomentState.zeros_like(ps)
+    t = rng.integers(1, 40, n)
+    m0, v0 = {}, {}
+    for a, w in REF2D:
+        m0[a] = f32(rng.standard_normal((n, w)) * 1e-3)
+        v0[a] = f32(rng.random((n, w)) * 1e-6)
+        st.m[a][:] = m0[a].reshape(st.m[a].shape)
+        st.v[a][:] = v0[a].reshape(st.v[a].shape)
+        st.t[a][:] = t
+    draw_seed = 99
+    out, out_st, events = pipeline.mcmc_relocate(ps, st, np.random.default_rng(draw_seed), 7)
+    arrays = {"alive": alive, "t": t.astype(np.int64),
+              "out_t": np.asarray(out_st.t["tau"], np.int64)}
+    for a, w in REF2D:
+        arrays[f"init_{a}"] = p0[a]
+        arrays[f"m_{a}"] = m0[a]
+        arrays[f"v_{a}"] = v0[a]
+        arrays[f"out_{a}"] = np.asarray(getattr(out, a), np.float64).reshape(n, w)
+        arrays[f"out_m_{a}"] = np.asarray(out_st.m[a], np.float64).reshape(n, w)
+        arrays[f"out_v_{a}"] = np.asarray(out_st.v[a], np.float64).reshape(n, w)
+    meta = dict(layout="ref2d", n=n, seed=seed, draw_seed=draw_seed,
+                event_count=int(events[0]["count"]) if events else 0,
+                event_hash=events[0]["affected_ids_hash"] if events else None)
+    save(name, meta, arrays)
+
+
 if __name__ == "__main__":
     run_sh3_case("sh3_dar", "adamw-gs")
     run_sh3_case("sh3_dar_clip", "adamw-gs", seed=1, lambda_o=0.1, lambda_s=0.05, n_pixels=1024,
@@ -332,3 +377,4 @@ if __name__ == "__main__":
     run_ref2d_coupled("ref2d_sync_coupled", "coupled-adam", seed=6, p_vis=0.7)
     run_rsr_stats()
     run_aiu()
+    run_relocate()

@@ -196,3 +196,40 @@ def test_structural_select_concat_keep_rows_consistent():
     assert len(cat) == keep.numel() + 10
     assert torch.equal(cat.clock[-10:], torch.zeros(10, dtype=torch.int32, device=DEV))
     assert torch.equal(cat.m["xyz"][: keep.numel(), 0], keep.float())
+
+
+@pytest.mark.parametrize("state_layout", ["rows", "groups"])
+@pytest.mark.parametrize("params_layout", ["attr", "record"])
+def test_mcmc_relocate_matches_reference_golden(state_layout, params_layout):
+    """AdamWGS.mcmc_relocate (pipeline.py:197-233) against the reference run:
+    relocated attributes bit-exact, shared opacity = fp32 of the reference's
+    float64 logit, respawn moments and clocks reset, other rows untouched."""
+    import json
+
+    from _golden import GOLDEN
+    from paper_2601_16736_b200 import records as R
+    from paper_2601_16736_b200.optimizer import AdamWGS
+    z = np.load(GOLDEN / "relocate.npz")
+    meta = json.loads(str(z["meta"]))
+    lay = O.LAYOUT_REF2D
+    params = {g.name: torch.from_numpy(z[f"init_{g.name}"]).to(DEV) for g in lay}
+    if params_layout == "record":
+        _, params = R.pack(params)
+    opt = AdamWGS([{"params": [params[g.name]], "lr": 1e-3, "name": g.name} for g in lay],
+                  mode="adamw-gs", state_layout=state_layout)
+    for g in lay:
+        opt.state.m[g.name][:] = torch.from_numpy(z[f"m_{g.name}"])
+        opt.state.v[g.name][:] = torch.from_numpy(z[f"v_{g.name}"])
+    opt.state.clock[:] = torch.from_numpy(z["t"].astype(np.int32))
+    plan = opt.mcmc_relocate(np.random.default_rng(meta["draw_seed"]),
+                             alive=torch.from_numpy(z["alive"]).to(DEV))
+    torch.cuda.synchronize()
+    assert plan.count == meta["event_count"] and plan.ids_hash() == meta["event_hash"]
+    for g in lay:
+        got = params[g.name].cpu().numpy()
+        assert np.array_equal(got, z[f"out_{g.name}"].astype(np.float32)), g.name
+        assert np.array_equal(opt.state.m[g.name].cpu().numpy(),
+                              z[f"out_m_{g.name}"].astype(np.float32)), g.name
+        assert np.array_equal(opt.state.v[g.name].cpu().numpy(),
+                              z[f"out_v_{g.name}"].astype(np.float32)), g.name
+    assert np.array_equal(opt.state.clock.cpu().numpy(), z["out_t"].astype(np.int32))

@@ -175,3 +175,30 @@ def test_aiu_f64_restatement_is_bitwise_reference():
     assert np.array_equal(picked, z["picked"])
     for g in lay:
         assert np.array_equal(p[g.name], z[f"out_{g.name}"]), g.name
+
+
+def test_relocate_f64_restatement_is_bitwise_reference():
+    """mcmc_relocate (pipeline.py:197-233): the oracle restatement and the
+    product's host plan (structural.mcmc_plan) against the reference run."""
+    import json
+
+    from paper_2601_16736_b200.structural import mcmc_plan
+    z = np.load(Case.__init__.__globals__["GOLDEN"] / "relocate.npz")
+    meta = json.loads(str(z["meta"]))
+    lay = O.LAYOUT_REF2D
+    p = {g.name: z[f"init_{g.name}"].astype(np.float64) for g in lay}
+    m = {g.name: z[f"m_{g.name}"].astype(np.float64) for g in lay}
+    v = {g.name: z[f"v_{g.name}"].astype(np.float64) for g in lay}
+    t = z["t"].copy()
+    dead = O.mcmc_relocate_f64(lay, p, m, v, t, z["alive"],
+                               np.random.default_rng(meta["draw_seed"]))
+    assert dead.size == meta["event_count"]
+    for g in lay:
+        assert np.array_equal(p[g.name], z[f"out_{g.name}"]), g.name
+        assert np.array_equal(m[g.name], z[f"out_m_{g.name}"]), g.name
+        assert np.array_equal(v[g.name], z[f"out_v_{g.name}"]), g.name
+    assert np.array_equal(t, z["out_t"])
+    plan = mcmc_plan(z["init_tau"], z["alive"], np.random.default_rng(meta["draw_seed"]))
+    assert plan.count == meta["event_count"] and plan.ids_hash() == meta["event_hash"]
+    assert np.array_equal(plan.dead, dead)
+    assert np.array_equal(plan.tau_new, z["out_tau"][plan.dead, 0])
