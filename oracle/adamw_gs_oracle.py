@@ -684,3 +684,57 @@ def mcmc_relocate_f64(layout, params, m, v, t, alive, rng, opacity="tau"):
         v[g.name][dead] = 0.0
     t[dead] = 0
     return dead
+
+
+def densify_adc_f64(params, m, v, t, alive, accum, count, cfg, rng):
+    """densify_adc (pipeline.py:116-185) on the 2-D layout's host arrays,
+    float64: clone (blend-preserving opacity), split (children sampled in the
+    parent footprint with ``rng``, scales shrunk), prune; children get zero
+    moments and clocks.  Returns (params, m, v, t, alive, src, event counts)."""
+    n = params["tau"].shape[0]
+    tau = params["tau"].reshape(-1).astype(np.float64).copy()
+    kappa = params["kappa"].astype(np.float64)
+    mean = accum / np.maximum(count, 1)
+    hot = alive & (mean > cfg["grad_threshold"]) & (count > 0)
+    smax = np.exp(kappa).max(axis=1)
+    clone = np.flatnonzero(hot & (smax <= cfg["split_scale_px"]))
+    split = np.flatnonzero(hot & (smax > cfg["split_scale_px"]))
+    if clone.size + 2 * split.size and n + clone.size + split.size > cfg["max_primitives"]:
+        clone = split = np.empty(0, np.int64)
+    pieces = {k: [a.astype(np.float64).reshape(n, -1)] for k, a in params.items()}
+    if clone.size:
+        o = _sigmoid_ref_f64(tau[clone])
+        o2 = 1.0 - np.power(1.0 - o, 1.0 / 2.0)
+        tc = np.log(o2 / (1.0 - o2))
+        for k in params:
+            pieces[k].append(pieces[k][0][clone].copy())
+        pieces["tau"][-1][:, 0] = tc
+        pieces["tau"][0][clone, 0] = tc
+    for _ in range(2 if split.size else 0):
+        child = {k: pieces[k][0][split].copy() for k in params}
+        gamma = rng.standard_normal((split.size, 2))
+        norms = np.linalg.norm(gamma, axis=1)
+        gamma *= (np.minimum(norms, 2.5) / np.maximum(norms, 1e-12))[:, None]
+        s = np.exp(child["kappa"])
+        c, sn = np.cos(child["rot"][:, 0]), np.sin(child["rot"][:, 0])
+        local = s * gamma
+        child["mu"][:, 0] += c * local[:, 0] - sn * local[:, 1]
+        child["mu"][:, 1] += sn * local[:, 0] + c * local[:, 1]
+        child["kappa"] -= np.log(cfg["split_shrink"])
+        for k in params:
+            pieces[k].append(child[k])
+    merged = {k: np.concatenate(p) for k, p in pieces.items()}
+    src = np.concatenate([np.arange(n), clone, split, split]).astype(np.int64)
+    nm = src.size
+    am = alive[src]
+    keep = np.ones(nm, bool)
+    keep[split] = False
+    prune = am & (_sigmoid_ref_f64(merged["tau"][:, 0]) <= cfg["prune_opacity"])
+    n_pruned = int((prune & keep).sum())
+    keep &= ~prune
+    fresh = np.arange(nm) >= n
+    out_m = {k: np.where(fresh[:, None], 0.0, x.reshape(n, -1)[src])[keep] for k, x in m.items()}
+    out_v = {k: np.where(fresh[:, None], 0.0, x.reshape(n, -1)[src])[keep] for k, x in v.items()}
+    out_t = np.where(fresh, 0, t[src])[keep]
+    return ({k: x[keep] for k, x in merged.items()}, out_m, out_v, out_t, am[keep], src[keep],
+            (int(clone.size), int(split.size), n_pruned))

@@ -405,6 +405,39 @@ class AdamWGS:
             self._raise_pending()
 
     # ------------------------------------------------------ structural ops
+    def rebind(self, params: dict, state: "MomentState | None" = None):
+        """Point the optimizer at new parameter tensors after a structural
+        change (densification, pruning, a loaded checkpoint): ``params`` maps
+        every group name to its new tensor, ``state`` holds their moments
+        (fresh zeros when None).  The row count may change; the
+        densification statistics, if enabled, restart from zero."""
+        self._raise_pending()
+        names = [g["name"] for g in self.param_groups]
+        if set(params) != set(names):
+            raise ConfigError(f"rebind needs exactly the groups {names}")
+        n = int(params[names[0]].shape[0])
+        for name in names:
+            p = params[name]
+            if p.device != self.device or p.dtype != torch.float32 or p.shape[0] != n:
+                raise ConfigError(f"group {name}: fp32 on {self.device} with {n} rows expected")
+            w = max(1, int(np.prod(p.shape[1:]))) if p.dim() > 1 else 1
+            row_stride(f"group {name}", p, n, w)
+        if state is None:
+            layout = "rows" if self.state.record is not None else "groups"
+            state = MomentState.zeros_like({k: params[k] for k in names}, layout)
+        if len(state) != n:
+            raise ConfigError(f"state has {len(state)} rows, parameters {n}")
+        for g in self.param_groups:
+            g["params"] = [params[g["name"]]]
+        self.state = state
+        if n != self.n_rows:
+            self.n_rows = n
+            self.engine = StepEngine(n, self.device, self.beta1, self.beta2)
+        self._last_ctx = None
+        if self._densify is not None:
+            self.enable_densify_stats(names[self._densify[2]])
+
+
     def relocate_rows(self, plan) -> None:
         """Apply a relocation plan (structural.RelocationPlan): respawn rows
         take their target's attributes, target and respawn share the planned
@@ -433,6 +466,15 @@ class AdamWGS:
                 else:
                     p[dead.long()] = p[targets.long()]
         self.reset_rows(dead)
+
+    def densify_adc(self, cfg, rng: np.random.Generator, alive=None, iteration: int = 0):
+        """densify_adc (pipeline.py:116-185) from the fused densification
+        statistics; see structural.densify_adc.  Rebinds the optimizer to
+        the new rows and returns the DensifyResult (new parameter tensors,
+        alive mask, source row per output row, the reference's events)."""
+        from .structural import densify_adc
+        acc, cnt = self.densify_stats()
+        return densify_adc(self, acc, cnt, cfg, rng, alive, iteration)
 
     def mcmc_relocate(self, rng: np.random.Generator, alive=None):
         """mcmc_relocate (pipeline.py:197-233): plan on the host with the

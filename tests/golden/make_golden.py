@@ -365,6 +365,58 @@ def run_relocate(name="relocate", n=300, seed=41):
     save(name, meta, arrays)
 
 
+def run_densify(name="densify", n=240, seed=51):
+    """densify_adc (pipeline.py:116-185) on the native 2-D layout: clone,
+    split (with the reference's rng draws), prune; recorded before/after."""
+    gradients, optimizer, primitives, loss = _import_reference()
+    import splatlab.config as config
+    import splatlab.pipeline as pipeline
+    rng = np.random.default_rng(seed)
+    p0 = {"mu": f32(rng.normal(0, 5, (n, 2))),
+          "kappa": f32(rng.uniform(math.log(0.3), math.log(8.0), (n, 2))),
+          "rot": f32(rng.normal(0, 1, (n, 1))), "tau": f32(rng.normal(0.0, 3.0, (n, 1))),
+          "color": f32(rng.normal(0, 0.5, (n, 3)))}
+    alive = rng.random(n) < 0.95
+    depth = np.arange(n, dtype=np.float64)            # row identity through the transform
+    ps = primitives.PrimitiveSet(mu=p0["mu"].astype(np.float64),
+                                 kappa=p0["kappa"].astype(np.float64),
+                                 rot=p0["rot"][:, 0].astype(np.float64),
+                                 tau=p0["tau"][:, 0].astype(np.float64),
+                                 color=p0["color"].astype(np.float64), depth=depth, alive=alive)
+    st = optimizer.MomentState.zeros_like(ps)
+    t = rng.integers(1, 40, n)
+    m0, v0 = {}, {}
+    for a, w in REF2D:
+        m0[a] = f32(rng.standard_normal((n, w)) * 1e-3)
+        v0[a] = f32(rng.random((n, w)) * 1e-6)
+        st.m[a][:] = m0[a].reshape(st.m[a].shape)
+        st.v[a][:] = v0[a].reshape(st.v[a].shape)
+        st.t[a][:] = t
+    accum = f32(rng.random(n) * 0.05).astype(np.float64)
+    count = rng.integers(0, 4, n)
+    stats = pipeline.DensifyStats(accum=accum.copy(), count=count.copy())
+    cfg = config.DensifyConfig(grad_threshold=0.012, prune_opacity=0.005, split_scale_px=3.0,
+                               split_shrink=1.6, max_primitives=2000)
+    draw_seed = 1234
+    out, out_st, events = pipeline.densify_adc(ps, st, stats, cfg, np.random.default_rng(draw_seed),
+                                               iteration=5)
+    arrays = {"alive": alive, "t": t.astype(np.int64), "accum": accum, "count": count,
+              "out_alive": out.alive, "out_src": out.depth.astype(np.int64),
+              "out_t": np.asarray(out_st.t["tau"], np.int64)}
+    for a, w in REF2D:
+        arrays[f"init_{a}"] = p0[a]
+        arrays[f"m_{a}"] = m0[a]
+        arrays[f"v_{a}"] = v0[a]
+        arrays[f"out_{a}"] = np.asarray(getattr(out, a), np.float64).reshape(len(out), w)
+        arrays[f"out_m_{a}"] = np.asarray(out_st.m[a], np.float64).reshape(len(out), w)
+        arrays[f"out_v_{a}"] = np.asarray(out_st.v[a], np.float64).reshape(len(out), w)
+    meta = dict(layout="ref2d", n=n, seed=seed, draw_seed=draw_seed, n_out=len(out),
+                cfg=dict(grad_threshold=0.012, prune_opacity=0.005, split_scale_px=3.0,
+                         split_shrink=1.6, max_primitives=2000),
+                events=[{k: e[k] for k in ("kind", "count", "affected_ids_hash")} for e in events])
+    save(name, meta, arrays)
+
+
 if __name__ == "__main__":
     run_sh3_case("sh3_dar", "adamw-gs")
     run_sh3_case("sh3_dar_clip", "adamw-gs", seed=1, lambda_o=0.1, lambda_s=0.05, n_pixels=1024,
@@ -378,3 +430,4 @@ if __name__ == "__main__":
     run_rsr_stats()
     run_aiu()
     run_relocate()
+    run_densify()

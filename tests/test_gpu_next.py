@@ -233,3 +233,52 @@ def test_mcmc_relocate_matches_reference_golden(state_layout, params_layout):
         assert np.array_equal(opt.state.v[g.name].cpu().numpy(),
                               z[f"out_v_{g.name}"].astype(np.float32)), g.name
     assert np.array_equal(opt.state.clock.cpu().numpy(), z["out_t"].astype(np.int32))
+
+
+@pytest.mark.parametrize("state_layout", ["rows", "groups"])
+@pytest.mark.parametrize("params_layout", ["attr", "record"])
+def test_densify_adc_matches_reference_golden(state_layout, params_layout):
+    """structural.densify_adc (pipeline.py:116-185) against the reference run:
+    clone / split (same rng draws) / prune decisions and events identical,
+    every output row bit-equal to fp32 of the reference's float64 value,
+    children with fresh state, parents' state carried."""
+    import json
+
+    from _golden import GOLDEN
+    from paper_2601_16736_b200 import records as R
+    from paper_2601_16736_b200.optimizer import AdamWGS
+    from paper_2601_16736_b200.structural import DensifyConfig, densify_adc
+    z = np.load(GOLDEN / "densify.npz")
+    meta = json.loads(str(z["meta"]))
+    lay = O.LAYOUT_REF2D
+    params = {g.name: torch.from_numpy(z[f"init_{g.name}"]).to(DEV) for g in lay}
+    if params_layout == "record":
+        _, params = R.pack(params)
+    opt = AdamWGS([{"params": [params[g.name]], "lr": 1e-3, "name": g.name} for g in lay],
+                  mode="adamw-gs", state_layout=state_layout)
+    for g in lay:
+        opt.state.m[g.name][:] = torch.from_numpy(z[f"m_{g.name}"])
+        opt.state.v[g.name][:] = torch.from_numpy(z[f"v_{g.name}"])
+    opt.state.clock[:] = torch.from_numpy(z["t"].astype(np.int32))
+    res = densify_adc(opt, z["accum"], z["count"], DensifyConfig(**meta["cfg"]),
+                      np.random.default_rng(meta["draw_seed"]), alive=z["alive"], iteration=5)
+    torch.cuda.synchronize()
+    assert [{k: e[k] for k in ("kind", "count", "affected_ids_hash")} for e in res.events] == \
+        meta["events"]
+    assert opt.n_rows == meta["n_out"] and len(opt.state) == meta["n_out"]
+    assert np.array_equal(res.src, z["out_src"]) and np.array_equal(res.alive, z["out_alive"])
+    for g in lay:
+        got = opt.param_groups[[x["name"] for x in opt.param_groups].index(g.name)]["params"][0]
+        assert got is res.params[g.name]
+        assert np.array_equal(got.cpu().numpy().reshape(meta["n_out"], -1),
+                              z[f"out_{g.name}"].astype(np.float32)), g.name
+        assert np.array_equal(opt.state.m[g.name].cpu().numpy().reshape(meta["n_out"], -1),
+                              z[f"out_m_{g.name}"].astype(np.float32)), g.name
+        assert np.array_equal(opt.state.v[g.name].cpu().numpy().reshape(meta["n_out"], -1),
+                              z[f"out_v_{g.name}"].astype(np.float32)), g.name
+    assert np.array_equal(opt.state.clock.cpu().numpy(), z["out_t"].astype(np.int32))
+    # the rebound optimizer steps on the new rows
+    vis = torch.rand(opt.n_rows, device=DEV) < 0.5
+    grads = {g.name: torch.randn_like(res.params[g.name]) * 1e-3 for g in lay}
+    opt.step(vis, 4096, grads=grads)
+    assert opt.last_stats()["n_stepped"] == int(vis.sum())

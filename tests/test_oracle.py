@@ -202,3 +202,23 @@ def test_relocate_f64_restatement_is_bitwise_reference():
     assert plan.count == meta["event_count"] and plan.ids_hash() == meta["event_hash"]
     assert np.array_equal(plan.dead, dead)
     assert np.array_equal(plan.tau_new, z["out_tau"][plan.dead, 0])
+
+
+def test_densify_adc_f64_restatement_is_bitwise_reference():
+    import json
+    z = np.load(Case.__init__.__globals__["GOLDEN"] / "densify.npz")
+    meta = json.loads(str(z["meta"]))
+    lay = O.LAYOUT_REF2D
+    p = {g.name: z[f"init_{g.name}"].astype(np.float64) for g in lay}
+    m = {g.name: z[f"m_{g.name}"].astype(np.float64) for g in lay}
+    v = {g.name: z[f"v_{g.name}"].astype(np.float64) for g in lay}
+    out, om, ov, ot, alive, src, counts = O.densify_adc_f64(
+        p, m, v, z["t"], z["alive"], z["accum"], z["count"], meta["cfg"],
+        np.random.default_rng(meta["draw_seed"]))
+    assert list(counts) == [e["count"] for e in meta["events"]]
+    assert np.array_equal(src, z["out_src"]) and np.array_equal(alive, z["out_alive"])
+    for g in lay:
+        assert np.array_equal(out[g.name], z[f"out_{g.name}"]), g.name
+        assert np.array_equal(om[g.name], z[f"out_m_{g.name}"]), g.name
+        assert np.array_equal(ov[g.name], z[f"out_v_{g.name}"]), g.name
+    assert np.array_equal(ot, z["out_t"])
