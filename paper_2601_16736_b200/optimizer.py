@@ -578,14 +578,15 @@ class AdamWGS:
 
     @torch.no_grad()
     def aiu_apply(self, visibility: torch.Tensor, aiu, rng: np.random.Generator, iteration: int,
-                  alive: torch.Tensor | None = None) -> np.ndarray:
+                  alive: torch.Tensor | None = None, draw=None) -> np.ndarray:
         """Artificial implicit updates (optimizer.py:425-450).
 
         The invisible alive rows are compacted on the GPU; the Bernoulli picks
         are drawn on the host from ``rng`` exactly as the reference does
         (``rng.random(invisible.size) < prob``), so the picked set is
         bit-identical; the frozen-moment update runs on the GPU.  Returns the
-        picked rows (int64, ascending).
+        picked rows (int64, ascending).  ``draw(n_invisible, prob)`` replaces
+        the local draw (the index-sharded wrapper's global-stream slice).
         """
         empty = np.empty(0, dtype=np.int64)
         if not aiu.active(iteration):
@@ -597,9 +598,14 @@ class AdamWGS:
         vis = visibility if visibility.dtype in (torch.bool, torch.uint8) else visibility > 0
         inv_idx, inv_cnt = eng.compact_select(vis, alive, invert=True)
         n_inv = int(inv_cnt.item())
-        if n_inv == 0 or prob <= 0.0 or eta == 0.0:
-            return empty
-        sel = rng.random(n_inv) < prob
+        if draw is not None:  # collective draw: every shard takes part, even an empty one
+            if prob <= 0.0 or eta == 0.0:
+                return empty
+            sel = draw(n_inv, prob)
+        else:
+            if n_inv == 0 or prob <= 0.0 or eta == 0.0:
+                return empty
+            sel = rng.random(n_inv) < prob
         k = int(sel.sum())
         if k == 0:
             return empty

@@ -133,3 +133,20 @@ def shard_rows(indices: np.ndarray, lo: int, hi: int) -> np.ndarray:
     a = np.searchsorted(indices, lo, side="left")
     b = np.searchsorted(indices, hi, side="left")
     return indices[a:b] - lo
+
+
+def aiu_shard_select(rng: np.random.Generator, prob: float, counts, rank: int) -> np.ndarray:
+    """AIU Bernoulli picks of one index shard, bit-identical to the
+    single-process draw (optimizer.py:437-440).
+
+    The reference draws ``rng.random(invisible.size) < prob`` over the global
+    invisible list. With contiguous row shards that list is the rank-ordered
+    concatenation of the local lists. So every rank draws the same global
+    vector from the same stream and keeps its slice at the exclusive scan of
+    ``counts``, the per-rank invisible counts (one all-gather).
+    """
+    counts = [int(c) for c in counts]
+    off = sum(counts[:rank])
+    draw = rng.random(sum(counts)) < prob
+    return draw[off:off + counts[rank]]
+

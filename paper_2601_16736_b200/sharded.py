@@ -90,3 +90,26 @@ class ShardedAdamWGS:
         import numpy as np
         local = shard_rows(np.asarray(global_indices, dtype=np.int64), self.lo, self.hi)
         self.opt.reset_rows(local)
+
+    def aiu_apply(self, visibility_local: torch.Tensor, aiu, rng, iteration: int,
+                  alive_local: torch.Tensor | None = None):
+        """Sharded AIU (optimizer.py:425-450), picks bit-identical to one process.
+
+        One all-gather of the per-rank invisible counts; every rank draws the
+        global Bernoulli vector from the same stream and keeps its slice
+        (sampling.aiu_shard_select). Returns this shard's picks in global
+        numbering."""
+        import numpy as np
+
+        from .sampling import aiu_shard_select
+
+        def draw(n_local, prob):
+            dev = self.opt.device if dist.get_backend(self.group) == "nccl" else "cpu"
+            mine = torch.tensor([n_local], dtype=torch.int64, device=dev)
+            allc = [torch.zeros_like(mine) for _ in range(self.world)]
+            dist.all_gather(allc, mine, group=self.group)
+            return aiu_shard_select(rng, prob, [int(c.item()) for c in allc], self.rank)
+
+        picked = self.opt.aiu_apply(visibility_local, aiu, rng, iteration, alive_local, draw=draw)
+        return np.asarray(picked, np.int64) + self.lo
+

@@ -282,3 +282,48 @@ def test_densify_adc_matches_reference_golden(state_layout, params_layout):
     grads = {g.name: torch.randn_like(res.params[g.name]) * 1e-3 for g in lay}
     opt.step(vis, 4096, grads=grads)
     assert opt.last_stats()["n_stepped"] == int(vis.sum())
+
+
+def test_sharded_aiu_single_rank_matches_unsharded():
+    """ShardedAdamWGS.aiu_apply (collective draw path) on a one-rank group
+    equals AdamWGS.aiu_apply: same picks, same parameters."""
+    import os
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_2601_16736_b200 import synthetic as S
+    from paper_2601_16736_b200.optimizer import AdamWGS
+    from paper_2601_16736_b200.sampling import AiuConfig
+    from paper_2601_16736_b200.sharded import ShardedAdamWGS
+    cfg = S.WorkloadConfig(n=20_000, p_vis=0.3, seed=8)
+    host = S.make_params(cfg)
+    aiu = AiuConfig(start=0, end=100, prob_schedule=((0, 0.25),), eta_schedule=((0, 0.5),),
+                    enabled=True)
+    vis = torch.from_numpy(S.visibility(cfg, 0)).to(DEV)
+    out = []
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        for sharded in (False, True):
+            params = {k: torch.from_numpy(v).to(DEV) for k, v in host.items()}
+            kw = dict(mode="adamw-gs", lambda_o=1e-3, lambda_s=1e-5)
+            if sharded:
+                opt = ShardedAdamWGS(S.param_groups(params), cfg.n, **kw)
+                inner = opt.opt
+            else:
+                opt = inner = AdamWGS(S.param_groups(params), **kw)
+            g = {k: torch.from_numpy(x).to(DEV) for k, x in S.step_grads(cfg, 0, S.visibility(
+                cfg, 0)).items()}
+            inner.step(vis, cfg.n_pixels, grads=g)
+            picked = opt.aiu_apply(vis, aiu, np.random.default_rng(3), 5)
+            out.append((np.asarray(picked), {k: p.cpu().numpy() for k, p in params.items()}))
+    finally:
+        dist.destroy_process_group()
+    assert out[0][0].size > 0 and np.array_equal(out[0][0], out[1][0])
+    for k in out[0][1]:
+        assert np.array_equal(out[0][1][k], out[1][1][k]), k

@@ -129,3 +129,46 @@ def test_two_rank_shards_equal_single_process(mode, lo, ls):
             assert np.array_equal(got[:8], want[:8])
             assert np.allclose(got[8:], want[8:], rtol=1e-12, atol=0)
     assert np.array_equal(np.concatenate([r[7] for r in res]), picked)
+
+
+def _aiu_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2601_16736_b200.sampling import aiu_shard_select
+        from paper_2601_16736_b200.sharded import shard_range
+        vis, alive = _aiu_problem()
+        a, b = shard_range(N, rank, world)
+        local_inv = np.flatnonzero(alive[a:b] & ~vis[a:b])
+        mine = torch.tensor([local_inv.size], dtype=torch.int64)
+        allc = [torch.zeros_like(mine) for _ in range(world)]
+        dist.all_gather(allc, mine)
+        sel = aiu_shard_select(np.random.default_rng(77), 0.3, [int(x) for x in allc], rank)
+        q.put((rank, local_inv[sel] + a))
+    finally:
+        dist.destroy_process_group()
+
+
+def _aiu_problem():
+    rng = np.random.default_rng(5)
+    return rng.random(N) < 0.4, rng.random(N) < 0.9
+
+
+def test_two_rank_aiu_picks_equal_single_process():
+    """AIU under index sharding: an all-gather of the per-rank
+    invisible counts plus the shared global draw reproduces the single-process
+    picks (optimizer.py:437-440) bit for bit."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_aiu_worker, args=(r, 2, port, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    res = sorted([q.get(timeout=300) for _ in procs], key=lambda x: x[0])
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    vis, alive = _aiu_problem()
+    invisible = np.flatnonzero(alive & ~vis)
+    want = invisible[np.random.default_rng(77).random(invisible.size) < 0.3]
+    assert np.array_equal(np.concatenate([r[1] for r in res]), want)
