@@ -67,31 +67,109 @@ __device__ __forceinline__ void mark_row(uint8_t* bad_rows, int64_t row, int bad
            (unsigned int)bad << (8 * (row & 3)));
 }
 
+// grec != nullptr: the gradients of all groups form one row record (group g
+// at column offset sum of the earlier widths, row stride grs, 16-byte rows):
+// the finite check is one pass with 16-byte loads, `lpr` lanes per row (a
+// power of two >= the row's 16-byte pieces), no index division.  Otherwise
+// each group is checked on its own: dense groups as one flat array (the row
+// is derived only for a non-finite value), strided groups element-wise.
 __global__ void __launch_bounds__(kThreads)
     check_grads_kernel(const GroupSet S, int64_t n_rows, const int32_t* __restrict__ rows,
                        const int32_t* __restrict__ n_list_dev, double lam_op, double lam_sc,
-                       uint8_t* __restrict__ bad_rows, int32_t* __restrict__ abort_flag) {
+                       uint8_t* __restrict__ bad_rows, int32_t* __restrict__ abort_flag,
+                       const float* __restrict__ grec, int64_t grs, int P, int lpr) {
   int flag = 0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t tid0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t n_list = rows ? (int64_t)(*n_list_dev) : 0;
+  if (grec) {
+    const int lane = threadIdx.x & 31;
+    const int sub = lane / lpr;           // row within the warp's group of rows
+    const int q0 = lane - sub * lpr;      // first 16-byte piece of this lane
+    const int rows_per_warp = 32 / lpr;
+    const int64_t warps = stride / 32;
+    const int nq = (P + 3) / 4;
+    constexpr int U = 4;  // row groups in flight per warp
+    const int64_t step = warps * rows_per_warp;
+    for (int64_t r0 = (tid0 / 32) * rows_per_warp; r0 < n_rows; r0 += U * step) {
+      float4 x[U];
+      int64_t row[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {  // issue all loads first
+        row[u] = r0 + u * step + sub;
+        x[u] = (row[u] < n_rows && q0 < nq)
+                   ? __ldg(reinterpret_cast<const float4*>(grec + row[u] * grs) + q0)
+                   : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (row[u] >= n_rows) continue;
+        const float* rp = grec + row[u] * grs;
+        int bad = 0;
+        for (int q = q0; q < nq; q += lpr) {  // one pass unless a row has > 32 pieces
+          const float4 y = q == q0 ? x[u] : __ldg(reinterpret_cast<const float4*>(rp) + q);
+          const int c = 4 * q;
+          bad |= !isfinite(y.x) | ((c + 1 < P) & !isfinite(y.y)) |
+                 ((c + 2 < P) & !isfinite(y.z)) | ((c + 3 < P) & !isfinite(y.w));
+        }
+        if (bad) {
+          flag |= 1;
+          if (bad_rows) mark_row(bad_rows, row[u], 1);
+        }
+      }
+    }
+  }
   for (int gi = 0; gi < S.n; ++gi) {
     const GroupPtrs G = S.g[gi];
     const int W = G.width;
-    const int64_t total = n_rows * W;
-    for (int64_t e = tid0; e < total; e += stride) {
-      const int64_t row = e / W;
-      if (!isfinite(__ldg(G.grad + row * G.gs + (e - row * W)))) {
-        flag |= 1;
-        if (bad_rows) mark_row(bad_rows, row, 1);
+    const int64_t total = grec ? 0 : n_rows * W;
+    if (G.gs == W) {
+      // dense: 16-byte loads from the first aligned element, 4 in flight per thread
+      const int64_t head = total == 0 ? 0 :
+          std::min<int64_t>(total, (16 - (reinterpret_cast<uintptr_t>(G.grad) & 15u)) / 4 & 3);
+      const int64_t nq4 = (total - head) / 4;
+      const float4* g4 = reinterpret_cast<const float4*>(G.grad + head);
+      auto check_elem = [&](int64_t e, float val) {
+        if (!isfinite(val)) {
+          flag |= 1;
+          if (bad_rows) mark_row(bad_rows, e / W, 1);
+        }
+      };
+      for (int64_t e = tid0; e < head; e += stride) check_elem(e, __ldg(G.grad + e));
+      for (int64_t q = tid0; q < nq4; q += 4 * stride) {
+        float4 x[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          x[u] = q + u * stride < nq4 ? __ldg(g4 + q + u * stride) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (!(isfinite(x[u].x) && isfinite(x[u].y) && isfinite(x[u].z) && isfinite(x[u].w))) {
+            const int64_t e = head + 4 * (q + u * stride);
+            check_elem(e, x[u].x);
+            check_elem(e + 1, x[u].y);
+            check_elem(e + 2, x[u].z);
+            check_elem(e + 3, x[u].w);
+          }
+        }
+      }
+      for (int64_t e = head + 4 * nq4 + tid0; e < total; e += stride) check_elem(e, __ldg(G.grad + e));
+    } else {
+      for (int64_t e = tid0; e < total; e += stride) {
+        const int64_t row = e / W;
+        if (!isfinite(__ldg(G.grad + row * G.gs + (e - row * W)))) {
+          flag |= 1;
+          if (bad_rows) mark_row(bad_rows, row, 1);
+        }
       }
     }
     const double lam = G.role == GS_ROLE_OPACITY ? lam_op : G.role == GS_ROLE_SCALE ? lam_sc : 0.0;
     if (lam != 0.0 && G.param != nullptr) {
       const int64_t tot = n_list * W;
+      const bool narrow = tot < (int64_t)UINT32_MAX;  // 32-bit index arithmetic
       for (int64_t e = tid0; e < tot; e += stride) {
-        const int64_t row = __ldg(rows + e / W);
-        if (domain_bad(G.role, G.param[row * G.ps + e % W])) {
+        const int64_t li = narrow ? (int64_t)((uint32_t)e / (uint32_t)W) : e / W;
+        const int64_t row = __ldg(rows + li);
+        if (domain_bad(G.role, G.param[row * G.ps + (e - li * W)])) {
           flag |= 2;
           if (bad_rows) mark_row(bad_rows, row, 2);
         }
@@ -452,8 +530,23 @@ extern "C" int gs_check_grads(const gs_group* groups, int32_t n_groups, int64_t 
     gs_set_error("gs_check_grads: rows given without their device count");
     return GS_ERR_ARG;
   }
+  // one gradient record?  (group g at offset sum of earlier widths, one stride)
+  const float* grec = groups[0].grad;
+  const int64_t grs = S.g[0].gs;
+  int P = 0;
+  for (int i = 0; i < n_groups && grec; ++i) {
+    if (groups[i].grad != groups[0].grad + P || S.g[i].gs != grs) grec = nullptr;
+    P += (int)groups[i].width;
+  }
+  // the 16-byte path needs 16-byte rows; the record may extend past P (pad)
+  const int nq = (P + 3) / 4;
+  if (grec && (grs < 4 * nq || grs % 4 != 0 || (reinterpret_cast<uintptr_t>(grec) & 15u)))
+    grec = nullptr;
+  int lpr = 1;
+  while (lpr < nq && lpr < 32) lpr <<= 1;
   check_grads_kernel<<<grid, kThreads, 0, s>>>(S, n_rows, rows, n_list_dev, lambda_opacity,
-                                               lambda_scale, bad_rows_out, abort_flag);
+                                               lambda_scale, bad_rows_out, abort_flag, grec, grs,
+                                               P, lpr);
   return gs_check_launch("gs_check_grads");
 }
 
