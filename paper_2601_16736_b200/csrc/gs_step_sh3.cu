@@ -73,6 +73,7 @@ struct FixedParams {
   uint32_t grs;
   int grec_ca;  // gradient record copies through L1 (.ca): host-mapped gradients
   int tma_ok;   // records and the state record allow 16-byte bulk copies
+  int contig;   // ring kernel: contiguous chunk runs per CTA instead of grid-stride
   double* stats_out;
   double* partials;
   unsigned int* counter;
@@ -1241,8 +1242,15 @@ __global__ void __launch_bounds__((NPW + NCW) * 32, MINB) step_ring_kernel(const
   int64_t n_rows = kDense ? P.max_rows : (int64_t)(*P.n_rows_dev);
   if (STRICT && *P.abort_flag != 0) n_rows = 0;
   const int64_t n_chunks = (n_rows + R - 1) / R;
-  auto chunk_id = [&](int64_t k) { return (int64_t)blockIdx.x + k * gridDim.x; };
+  // chunk order: grid-stride (default) or, with P.contig, a contiguous run of
+  // chunks per CTA
+  const int64_t cpb = (n_chunks + gridDim.x - 1) / gridDim.x;
+  auto chunk_id = [&](int64_t k) {
+    return P.contig ? (int64_t)blockIdx.x * cpb + k : (int64_t)blockIdx.x + k * gridDim.x;
+  };
+  auto chunk_ok = [&](int64_t k) { return (!P.contig || k < cpb) && chunk_id(k) < n_chunks; };
   auto chunk_rows = [&](int64_t k) -> int {
+    if (P.contig && k >= cpb) return 0;
     const int64_t rem = n_rows - chunk_id(k) * R;
     return rem <= 0 ? 0 : (rem < R ? (int)rem : R);
   };
@@ -1281,7 +1289,7 @@ __global__ void __launch_bounds__((NPW + NCW) * 32, MINB) step_ring_kernel(const
       return kDense ? (uint32_t)i : (uint32_t)__ldg(P.rows + i);
     };
     uint32_t next_id = fetch_id(0);
-    for (int64_t k = 0; chunk_id(k) < n_chunks; ++k) {
+    for (int64_t k = 0; chunk_ok(k); ++k) {
       const int st = (int)(k % S);
       const uint32_t my_id = next_id;
       next_id = fetch_id(k + 1);
@@ -1395,7 +1403,7 @@ __global__ void __launch_bounds__((NPW + NCW) * 32, MINB) step_ring_kernel(const
     const StepConsts& K = kCoupled ? Kc : P.K;
     float2* const rec_base = reinterpret_cast<float2*>(P.record);
     const uint32_t rec_stride2 = (uint32_t)(P.stride / 2);
-    for (int64_t k = 0; chunk_id(k) < n_chunks; ++k) {
+    for (int64_t k = 0; chunk_ok(k); ++k) {
       const int st = (int)(k % S);
       const int ep = (int)(k / S) + 1;  // this use of stage st
       const int nvalid = chunk_rows(k);
@@ -1847,6 +1855,10 @@ void launch_fixed(const FixedParams& P, int64_t max_rows, int kind, cudaStream_t
       launch_ws<L, MODE, STRICT, 32, 3, 3, 8, 2, true>(P, max_rows, s);
     } else if (v == 13) {
       launch_ring<L, MODE, STRICT, 32, 3, 3, 8, 2, false>(P, max_rows, s);
+    } else if (v == 15) {
+      FixedParams Q = P;
+      Q.contig = 1;
+      launch_ring<L, MODE, STRICT, 32, 3, 3, 8, 2, true>(Q, max_rows, s);
     } else if (v == 14) {
       launch_ring<L, MODE, STRICT, 32, 3, 2, 8, 2, true>(P, max_rows, s);
     } else if (v == 11) {
