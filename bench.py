@@ -87,12 +87,15 @@ def parse():
                     help="launch the timed steps eagerly instead of as one CUDA graph")
     ap.add_argument("--layout", default="rows", choices=["rows", "groups"],
                     help="optimizer-state layout (row records or per-group tensors)")
-    ap.add_argument("--record-align", type=int, default=4,
+    ap.add_argument("--state-align", type=int, default=16,
+                    help="moment-record rows padded to a multiple of this many floats "
+                         "(16: 512-byte SH-3 rows, whole 64-byte granules; 2: 480 bytes)")
+    ap.add_argument("--record-align", type=int, default=16,
                     help="parameter / gradient record rows padded to a multiple of this "
-                         "many floats (4: 240-byte SH-3 rows; 16: 256-byte, granule-aligned)")
-    ap.add_argument("--host-record-align", type=int, default=64,
+                         "many floats (16: 256-byte SH-3 rows, whole granules; 4: 240 bytes)")
+    ap.add_argument("--host-record-align", type=int, default=16,
                     help="e2e: pinned host gradient record rows padded to a multiple of this "
-                         "many floats (64: 256-byte rows, two PCIe read lines)")
+                         "many floats (16: 256-byte SH-3 rows, two PCIe read lines)")
     ap.add_argument("--params", default="record", choices=["record", "attr"],
                     help="parameter / gradient HBM layout: attribute views of one "
                          "row-interleaved record (records.py) or one tensor per attribute")
@@ -323,9 +326,11 @@ def workload_config(args, wl, p_vis, world):
                     "interval": RSR_INTERVAL} if wl["rsr"] else None,
             "reset_fraction": wl["reset"] or None, "check": args.check,
             "state_layout": args.layout,
-            "param_layout": "record (attribute views of one (n, 60) fp32 row record, "
-                            "gradients likewise)" if args.params == "record"
-                            else "one tensor per attribute",
+            "param_layout": (f"record (attribute views of one (n, "
+                             f"{(59 + args.record_align - 1) // args.record_align * args.record_align}"
+                             f") fp32 row record, gradients likewise; moment record rows of "
+                             f"{(120 + args.state_align - 1) // args.state_align * args.state_align * 4}"
+                             f" B)") if args.params == "record" else "one tensor per attribute",
             "l2": "inputs larger than L2 (working set >> 126 MB)" if n >= 1_000_000 else
                   "L2 flushed between timed steps",
             "parallelism": f"index-sharded x{world}",
@@ -357,7 +362,8 @@ def ours(args, wl, p_vis):
     if args.params == "record":
         _, params = R.pack(params, align=args.record_align)
     opt = AdamWGS(S.param_groups(params), mode=wl["mode"], lambda_o=wl["lo"], lambda_s=wl["ls"],
-                  check=args.check, errors="defer", state_layout=args.layout)
+                  check=args.check, errors="defer", state_layout=args.layout,
+                  state_row_align=args.state_align)
     total_steps = args.warmup + args.steps
     masks = [S.visibility_device(cfg, s, dev) for s in range(total_steps)]
     n_vis = torch.stack([m.sum() for m in masks]).cpu().numpy().astype(np.int64)
@@ -509,8 +515,11 @@ def ours(args, wl, p_vis):
             "config": workload_config(args, wl, p_vis, world),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak,
-                         "traffic": traffic_from_profiles(args.workload, args.mask, p_vis,
-                                                          args.params),
+                         "traffic": traffic_from_profiles(
+                             args.workload, args.mask, p_vis,
+                             args.params if args.params != "record" or
+                             (args.record_align, args.state_align) == (16, 16) else
+                             f"record-a{args.record_align}-s{args.state_align}"),
                          "kernel": ("gs::step_kernel (K2, gs_step)" if args.layout != "rows" else
                                     "gs::step_ring_kernel<LayoutSH3, ..., REC> (K2, record "
                                     "layout, via gs_step_rows)" if args.params == "record" else

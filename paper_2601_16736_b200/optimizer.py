@@ -157,7 +157,7 @@ class MomentState:
         return MomentState(m, v, clock, global_t, record, spec)
 
     @staticmethod
-    def zeros_like(params: dict, layout: str = "rows") -> "MomentState":
+    def zeros_like(params: dict, layout: str = "rows", row_align: int = 16) -> "MomentState":
         first = next(iter(params.values()))
         n = first.shape[0]
         if layout == "groups":
@@ -174,7 +174,12 @@ class MomentState:
             tail = tuple(p.shape[1:])
             spec.append((k, off, tail))
             off += int(np.prod(tail)) if tail else 1
-        record = torch.zeros((n, 2 * (off + 1)), dtype=torch.float32, device=first.device)
+        w = 2 * (off + 1)
+        # rows padded to a multiple of row_align floats; 16 = whole 64-byte
+        # DRAM granules (SH-3: 120 -> 128 floats, 512 B)
+        a = max(2, int(row_align))
+        w = (w + a - 1) // a * a
+        record = torch.zeros((n, w), dtype=torch.float32, device=first.device)
         return MomentState.from_record(record, tuple(spec))
 
     def copy(self) -> "MomentState":
@@ -226,7 +231,8 @@ class AdamWGS:
     def __init__(self, params, *, mode: str = "adamw-gs", betas=(0.9, 0.999), eps: float = 1e-8,
                  lambda_o: float = 0.0, lambda_s: float = 0.0, ct_opacity: float = 10.0,
                  ct_scale: float = 10.0, round_n_pixels: bool = True, check: str = "fused",
-                 errors: str = "raise", state_layout: str = "rows"):
+                 errors: str = "raise", state_layout: str = "rows",
+                 state_row_align: int = 16):
         validate_hyper(mode, betas[0], betas[1], eps, ct_opacity, ct_scale)
         if check not in CHECKS:
             raise ConfigError(f"check must be one of {CHECKS}")
@@ -262,8 +268,9 @@ class AdamWGS:
                 raise ConfigError(f"group {g['name']}: parameters must be fp32")
             w = max(1, int(np.prod(p.shape[1:]))) if p.dim() > 1 else 1
             row_stride(f"group {g['name']}", p, self.n_rows, w)
+        self.state_row_align = int(state_row_align)
         self.state = MomentState.zeros_like({g["name"]: g["params"][0] for g in self.param_groups},
-                                            state_layout)
+                                            state_layout, self.state_row_align)
         self.engine = StepEngine(self.n_rows, self.device, self.beta1, self.beta2)
         self._stats_host = torch.zeros(L.GS_STEP_STATS, dtype=torch.float64, pin_memory=True)
         self._abort_host = torch.zeros(1, dtype=torch.int32, pin_memory=True)
@@ -424,7 +431,8 @@ class AdamWGS:
             row_stride(f"group {name}", p, n, w)
         if state is None:
             layout = "rows" if self.state.record is not None else "groups"
-            state = MomentState.zeros_like({k: params[k] for k in names}, layout)
+            state = MomentState.zeros_like({k: params[k] for k in names}, layout,
+                                           self.state_row_align)
         if len(state) != n:
             raise ConfigError(f"state has {len(state)} rows, parameters {n}")
         for g in self.param_groups:

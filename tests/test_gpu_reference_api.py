@@ -491,6 +491,7 @@ def test_step_kernels_all_identical(mode, check):
     # 9/10/12 = bulk-copy (TMA) kernels,
     # 11 = cp.async gathers + bulk stores, 15 = ring kernel with contiguous chunk runs
     runs += [("fixed", v, "record") for v in (8, 9, 10, 11, 12, 13, 14, 15)]
+    runs += [(k, 0, "record240") for k in ("fixed", "rows")]  # compact 240-byte rows
     if check == "strict":
         runs = [r for r in runs if r[1] in (0, 3, 7, 8, 11, 12)]
     prev_f = lib.gs_set_fixed_variant(0)
@@ -501,15 +502,15 @@ def test_step_kernels_all_identical(mode, check):
             lib.gs_set_rows_variant(variant if kind == "rows" else 0)
             params = {k: torch.from_numpy(v).to(DEV) for k, v in host.items()}
             if lay != "attr":
-                _, params = R.pack(params)
+                _, params = R.pack(params, align=4 if lay == "record240" else 16)
             layout = "groups" if kind == "groups" else "rows"
             opt = AdamWGS(S.param_groups(params), mode=mode, lambda_o=1e-3, lambda_s=1e-5,
                           state_layout=layout, check=check)
             for s in range(3):
                 vis = S.visibility(cfg, s)
                 g = {k: torch.from_numpy(x).to(DEV) for k, x in S.step_grads(cfg, s, vis).items()}
-                if lay == "record":
-                    _, g = R.pack(g)
+                if lay in ("record", "record240"):
+                    _, g = R.pack(g, align=4 if lay == "record240" else 16)
                 opt.step(torch.from_numpy(vis).to(DEV), cfg.n_pixels, grads=g)
             results.append(({k: p.cpu().numpy() for k, p in params.items()},
                             {k: t.contiguous().cpu().numpy() for k, t in opt.state.m.items()},

@@ -18,15 +18,16 @@ def _attrs(n=7):
 def test_pack_layout_and_views():
     a = _attrs()
     rec, v = R.pack(a)
-    assert rec.shape == (7, 60) and rec.is_contiguous()
+    assert rec.shape == (7, 64) and rec.is_contiguous()   # 64-byte-granule rows
+    assert R.pack(a, align=4)[0].shape == (7, 60)          # compact rows
     off = 0
     for k, t in a.items():
         w = t[0].numel()
         assert torch.equal(v[k], t) and v[k].shape == t.shape
         assert torch.equal(rec[:, off:off + w].reshape(t.shape), t)
-        assert row_stride(k, v[k], 7, w) == 60
+        assert row_stride(k, v[k], 7, w) == 64
         off += w
-    assert torch.all(rec[:, 59] == 0)  # pad
+    assert torch.all(rec[:, 59:] == 0)  # pad
 
 
 def test_autograd_fills_record_grad_and_base_grad_view():
@@ -43,7 +44,7 @@ def test_autograd_fills_record_grad_and_base_grad_view():
 def test_views_like_matches_offsets():
     a = _attrs()
     _, v = R.pack(a)
-    other = torch.arange(7 * 60, dtype=torch.float32).view(7, 60)
+    other = torch.arange(7 * 64, dtype=torch.float32).view(7, 64)
     w = R.views_like(other, v)
     assert w["opacity"][2, 0] == other[2, 51]
     assert torch.equal(w["rotation"][1], other[1, 55:59])
