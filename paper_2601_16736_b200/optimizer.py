@@ -113,10 +113,11 @@ class MomentState:
 
     ``"rows"`` (default) — one fp32 record per primitive holding the (m, v)
         pairs of all its elements in group order followed by the int32 clock
-        (``record`` [N, 2*(P+1)]); ``m[g]``, ``v[g]`` and ``clock`` are strided
-        views into it.  A visible primitive's whole optimizer state is one
-        contiguous 8*(P+1)-byte span (480 B for SH-3), which is what the
-        fused B200 step streams.
+        (``record`` [N, >= 2*(P+1)], rows padded to ``row_align`` floats);
+        ``m[g]``, ``v[g]`` and ``clock`` are strided views into it.  A visible
+        primitive's whole optimizer state is one contiguous 8*(P+1)-byte span
+        (480 B for SH-3, in a 512-B granule-aligned row by default), which is
+        what the fused B200 step streams.
     ``"groups"`` — contiguous per-group ``m`` / ``v`` tensors and a separate
         int32 clock (the reference's own layout).
     """
