@@ -169,15 +169,23 @@ def test_golden_step_parity(name, check, layout):
 # C1: 100k SH3, 50% visibility, 100 steps (BASELINE.json configs[0])
 # --------------------------------------------------------------------------
 
-@pytest.mark.parametrize("family,layout", [("bernoulli", "rows"), ("coherent", "rows"),
-                                           ("bernoulli", "groups")])
-def test_c1_100_steps_vs_oracles(family, layout):
+@pytest.mark.parametrize("family,layout,params_layout", [
+    ("bernoulli", "rows", "attr"), ("coherent", "rows", "attr"), ("bernoulli", "groups", "attr"),
+    ("bernoulli", "rows", "record"), ("coherent", "rows", "record")])
+def test_c1_100_steps_vs_oracles(family, layout, params_layout):
+    """C1: 100 steps x 100k rows, bit-exact vs the fp32 order and
+    within 1e-6 normwise of the float64 reference; per-attribute tensors and
+    granule-aligned parameter/gradient records (the ring kernel)."""
+    from paper_2601_16736_b200 import records as R
     from paper_2601_16736_b200 import synthetic as S
     from paper_2601_16736_b200.optimizer import AdamWGS
     n, steps = 100_000, 100
     cfg = S.WorkloadConfig(n=n, p_vis=0.5, mask_family=family, seed=1)
     host = S.make_params(cfg)
     params = {k: torch.from_numpy(v).to(DEV) for k, v in host.items()}
+    if params_layout == "record":
+        _, params = R.pack(params)
+        grec, gviews = R.pack({k: torch.zeros_like(v) for k, v in params.items()})
     opt = AdamWGS(S.param_groups(params, cfg), mode="adamw-gs", lambda_o=cfg.lambda_o,
                   lambda_s=cfg.lambda_s, state_layout=layout)
     # oracles
@@ -195,8 +203,13 @@ def test_c1_100_steps_vs_oracles(family, layout):
     for s in range(steps):
         vis = S.visibility(cfg, s)
         g = S.step_grads(cfg, s, vis)
-        opt.step(torch.from_numpy(vis).to(DEV), cfg.n_pixels,
-                 grads={k: torch.from_numpy(x).to(DEV) for k, x in g.items()})
+        if params_layout == "record":
+            for k, x in g.items():
+                gviews[k].copy_(torch.from_numpy(x).view(gviews[k].shape))
+            opt.step(torch.from_numpy(vis).to(DEV), cfg.n_pixels, grads=gviews)
+        else:
+            opt.step(torch.from_numpy(vis).to(DEV), cfg.n_pixels,
+                     grads={k: torch.from_numpy(x).to(DEV) for k, x in g.items()})
         O.step_fp32("adamw-gs", lay, p32, g, m32, v32, c32, np.flatnonzero(vis), hp,
                     n_pixels=cfg.n_pixels, lut=lut)
         O.dar_step_f64(lay, p64, {k: x.astype(np.float64) for k, x in g.items()}, m64, v64, t64,
