@@ -138,8 +138,11 @@ int gs_host_device_pointer(const void* host_ptr, void** dev_ptr);
 /* K1 — visibility compaction: ascending int32 indices of nonzero mask bytes
  * (or radii > 0), count written to *count_out (device).  Bit-exact with
  * np.flatnonzero.  ws: gs_compact_workspace_bytes(n) bytes (one int per
- * 4096-row tile, overwritten by every call; graph-capturable).  Two launches:
- * per-tile counts, then prefix + ordered writes. */
+ * 8192-row tile, an arrival counter, one selection bit per row): zero it
+ * once before the first call; every call leaves the counter at zero
+ * (graph-capturable).  Two launches: per-tile counts plus the selection
+ * bitmap (the last CTA scans the counts into offsets), then ordered writes
+ * from the bitmap. */
 size_t gs_compact_workspace_bytes(int64_t n);
 int gs_compact_u8(const uint8_t* mask, int64_t n, int32_t* idx_out, int32_t* count_out,
                   void* ws, size_t ws_bytes, void* stream);

@@ -70,7 +70,7 @@ def test_workspace_queries_without_gpu():
     from paper_2601_16736_b200 import _lib
     lib = _lib.load()
     assert lib.gs_compact_workspace_bytes(0) >= 4
-    assert lib.gs_compact_workspace_bytes(6_000_000) == 4 * ((6_000_000 + 4095) // 4096)
+    assert lib.gs_compact_workspace_bytes(6_000_000) == 4 * (((6_000_000 + 8191) // 8192) * 257 + 1)
     assert lib.gs_step_workspace_bytes() > 0
 
 
