@@ -588,7 +588,10 @@ def run_e2e(args, opt, cfg, dev, world, masks, n_vis):
     host_mask.copy_(masks[0].cpu())
     dev_mask = torch.empty_like(masks[0])
     stats_host = torch.empty(10, dtype=torch.float64, pin_memory=True)
-    row_bytes = sum(t[0].numel() * 4 for t in host_grads.values())
+    # bytes the zero-copy gather moves per visible row: the whole host record
+    # row (pad included) for a record, the attribute rows otherwise
+    row_bytes = (host_rec.shape[1] * 4 if args.params == "record"
+                 else sum(t[0].numel() * 4 for t in host_grads.values()))
     dense = sum(t.numel() * 4 for t in host_grads.values())
     host_dense = ([host_rec] if args.params == "record" else list(host_grads.values()))
     dense = sum(t.numel() * 4 for t in host_dense)
