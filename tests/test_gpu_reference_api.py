@@ -605,9 +605,13 @@ def test_state_views_and_checkpoint_roundtrip():
 
 
 @pytest.mark.parametrize("check", ["fused", "strict"])
-def test_pinned_host_grads_zero_copy_identical(check):
+@pytest.mark.parametrize("layout", ["attr", "record"])
+def test_pinned_host_grads_zero_copy_identical(check, layout):
     """Gradients in pinned host memory are read zero-copy by the kernel and
-    give bitwise the same step as device-resident gradients."""
+    give bitwise the same step as device-resident gradients: per-attribute
+    tensors (gather kernel) and a pinned gradient record with device
+    parameter records (ring kernel, L1-allocating host copies)."""
+    from paper_2601_16736_b200 import records as R
     from paper_2601_16736_b200 import synthetic as S
     from paper_2601_16736_b200.engine import ConfigError
     from paper_2601_16736_b200.optimizer import AdamWGS
@@ -616,6 +620,8 @@ def test_pinned_host_grads_zero_copy_identical(check):
     outs = []
     for where in ("device", "pinned"):
         params = {k: torch.from_numpy(v).to("cuda:0") for k, v in host.items()}
+        if layout == "record":
+            _, params = R.pack(params)
         opt = AdamWGS(S.param_groups(params), mode="adamw-gs", lambda_o=1e-3, lambda_s=1e-5,
                       check=check)
         for s in range(3):
@@ -623,6 +629,11 @@ def test_pinned_host_grads_zero_copy_identical(check):
             g = S.step_grads(cfg, s, vis)
             if where == "device":
                 grads = {k: torch.from_numpy(x).to("cuda:0") for k, x in g.items()}
+                if layout == "record":
+                    grads = R.pack(grads)[1]
+            elif layout == "record":
+                grads = R.pack({k: torch.from_numpy(x) for k, x in g.items()},
+                               pin_memory=True)[1]
             else:
                 grads = {k: torch.from_numpy(x).pin_memory() for k, x in g.items()}
             opt.step(torch.from_numpy(vis).to("cuda:0"), cfg.n_pixels, grads=grads)
