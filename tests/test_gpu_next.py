@@ -11,17 +11,22 @@ pytestmark = pytest.mark.gpu
 DEV = "cuda:0"
 
 
-@pytest.mark.parametrize("path", ["fixed", "rows", "groups"])
+@pytest.mark.parametrize("path", ["fixed", "record", "rows", "groups"])
 def test_densify_stats_fused(path):
-    """DensifyStats.observe (pipeline.py:77-82) fused into K2."""
+    """DensifyStats.observe (pipeline.py:77-82) fused into K2: the gather
+    kernel, the ring kernel on parameter/gradient records, the generic
+    row-record kernel and the per-group-state kernel."""
     from paper_2601_16736_b200 import _lib
+    from paper_2601_16736_b200 import records as R
     from paper_2601_16736_b200 import synthetic as S
     from paper_2601_16736_b200.optimizer import AdamWGS
     lib = _lib.load()
     cfg = S.WorkloadConfig(n=30_011, p_vis=0.3, seed=12)
     host = S.make_params(cfg)
     params = {k: torch.from_numpy(v).to(DEV) for k, v in host.items()}
-    prev = lib.gs_set_fixed_variant(0 if path == "fixed" else -1)
+    if path == "record":
+        _, params = R.pack(params)
+    prev = lib.gs_set_fixed_variant(0 if path in ("fixed", "record") else -1)
     try:
         opt = AdamWGS(S.param_groups(params), mode="adamw-gs", lambda_o=1e-3, lambda_s=1e-5,
                       state_layout="groups" if path == "groups" else "rows")
@@ -34,8 +39,10 @@ def test_densify_stats_fused(path):
         for s in range(4):
             vis = S.visibility(cfg, s)
             g = S.step_grads(cfg, s, vis)
-            opt.step(torch.from_numpy(vis).to(DEV), cfg.n_pixels, densify_scale=scale,
-                     grads={k: torch.from_numpy(x).to(DEV) for k, x in g.items()})
+            gd = {k: torch.from_numpy(x).to(DEV) for k, x in g.items()}
+            if path == "record":
+                gd = R.pack(gd)[1]
+            opt.step(torch.from_numpy(vis).to(DEV), cfg.n_pixels, densify_scale=scale, grads=gd)
             O.densify_observe_fp32(g["xyz"], np.flatnonzero(vis), acc32, cnt32, scale)
             O.densify_observe_f64(g["xyz"], vis, acc64, cnt64, scale)
         acc, cnt = opt.densify_stats()
