@@ -1,25 +1,33 @@
-// K2 fast path — the fused AdamW-GS step specialised at compile time for a
-// fixed attribute layout (3DGS SH-3: xyz 3 | f_dc 3 | f_rest 45 | opacity 1 |
-// scaling 3 | rotation 4), row-record optimizer state (gs_step_rows.cu).
+// K2 fast path: the fused AdamW-GS step, specialised at compile time for the
+// 3DGS SH-3 attribute layout (xyz 3 | f_dc 3 | f_rest 45 | opacity 1 |
+// scaling 3 | rotation 4) with row-record optimizer state.  gs_step_rows
+// (gs_step_rows.cu) calls gs_step_fixed_try first.
 //
-// One warp owns a chunk of 32 visible rows.  Every loop below is unrolled
-// over the compile-time layout, so roles, widths, record offsets and the
-// penalty code paths cost no branches:
+// Every kernel here walks chunks of 32 visible rows.  The group loop is
+// unrolled over the compile-time layout, so widths, roles, record offsets and
+// the penalty code paths cost no branches.  The arithmetic is
+// gs_common.cuh::update_element, bit-identical to oracle step_fp32.  A row
+// with a non-finite gradient, or tau / kappa outside the activation domain
+// where a penalty is active, is skipped whole.
 //
-//   pass A  lane l loads, for every group g and k < W_g, the gradient of
-//           element e = 32k + l of the chunk's (row, column) sequence of g
-//           (row e / W_g, column e % W_g) — 59 coalesced loads per lane kept
-//           in registers — plus theta of the opacity / scale elements, and
-//           ORs a per-row bad mask (non-finite gradient, tau / kappa outside
-//           the activation domain where a penalty is active).  One warp
-//           reduction gives the 32-row validity mask: no gradient is read
-//           twice and no row is partially written.
-//   clocks  lane r bumps the clock of row r and fetches its bias factors.
-//   pass B  group by group, batches of elements: load theta and the (m, v)
-//           pair from the record, update (gs_common.cuh::update_element,
-//           bit-identical to oracle step_fp32), store.  The opacity group has
-//           exactly one element per lane and the scale group three, so the
-//           DAR terms are computed lane-parallel.
+// Shipped kernels:
+//   step_ring_kernel<..., REC=1>  default for parameter/gradient records.
+//       3 producer warps cp.async the chunk's moment records, theta rows and
+//       gradient rows (16-byte pieces, array by array; row ids by shuffle),
+//       plus the row ids and bias factors, into a 3-stage ring (full / empty
+//       mbarriers).  8 consumer warps check, update and store, with one
+//       named barrier per chunk (epoch-tagged row flags).
+//   step_ws_kernel<...>  default for per-attribute theta / gradient tensors.
+//       The same ring with 4-byte element gathers in chunk element order and
+//       three consumer barriers per chunk (cheaper there than per-element
+//       row-id shuffles).
+// Variants, kept because they are measured and tested bit-identical
+// (gs_set_fixed_variant):
+//   step_fixed_kernel (phase-separated), step_pipe / step_pipe2_kernel (the
+//   first cp.async rings), step_ws_kernel<REC=1> (+ BULKST bulk stores),
+//   step_tma_kernel (cp.async.bulk loads / stores: bound by the TMA unit's
+//   per-operation cost on 256/512-byte rows), step_ring_kernel shapes and
+//   contiguous chunk runs.
 #include <stdlib.h>
 
 #include "gs_common.cuh"
