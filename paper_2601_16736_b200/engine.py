@@ -203,6 +203,8 @@ class StepEngine:
         self._group_cache_key = None
         self._group_cache = None
         self._record_ok = None
+        self._cfg_key = None
+        self._cfg = None
         self._omb1 = float(np.float32(1.0 - self.beta1))
         self._omb2 = float(np.float32(1.0 - self.beta2))
         self._eps32 = {}
@@ -344,27 +346,9 @@ class StepEngine:
         self.launches += 1 if max_k else 0
         return picked[:max_k]
 
-    # ------------------------------------------------------------------ step
-    def step(self, groups: list[GroupBinding], mode: str, clock: torch.Tensor, *,
-             rows: torch.Tensor | None, count: torch.Tensor | None, eps: float,
-             lambda_opacity: float = 0.0, lambda_scale: float = 0.0, clip_opacity: float = 10.0,
-             clip_scale: float = 10.0, n_pixels_rounded: float = 0.0, global_t: int = 0,
-             n_visible_dev: torch.Tensor | None = None, n_visible_host: float = 0.0,
-             check: str = "fused", record: torch.Tensor | None = None,
-             densify: tuple | None = None) -> torch.Tensor:
-        """K2 (plus the strict pre-check when ``check == "strict"``).
-
-        ``record`` given: row-record state (gs_step_rows), ``clock`` ignored;
-        otherwise per-group m / v tensors and the int32 ``clock``.
-        """
-        if mode not in L.MODE_IDS:
-            raise ConfigError(f"unknown mode {mode!r}; expected one of {tuple(L.MODE_IDS)}")
-        if record is None:
-            _check_tensor("clock", clock, self.n_rows, 1, self.device, torch.int32)
-        else:
-            self._check_record(record, groups)
-        garr = self.group_array(groups)
-        s = _stream_handle(self.device)
+    def _build_cfg(self, mode, check, eps, lambda_opacity, lambda_scale, clip_opacity,
+                   clip_scale, n_pixels_rounded, global_t, n_visible_dev, n_visible_host,
+                   densify):
         cfg = L.GsStepCfg()
         cfg.mode = L.MODE_IDS[mode]
         cfg.check = L.CHECK_STRICT if check == "strict" else L.CHECK_FUSED
@@ -396,6 +380,41 @@ class StepEngine:
             cfg.densify_count = dcount.data_ptr()
             cfg.densify_scale = float(np.float32(dscale))
             cfg.densify_group = int(dgroup)
+        return cfg
+
+    # ------------------------------------------------------------------ step
+    def step(self, groups: list[GroupBinding], mode: str, clock: torch.Tensor, *,
+             rows: torch.Tensor | None, count: torch.Tensor | None, eps: float,
+             lambda_opacity: float = 0.0, lambda_scale: float = 0.0, clip_opacity: float = 10.0,
+             clip_scale: float = 10.0, n_pixels_rounded: float = 0.0, global_t: int = 0,
+             n_visible_dev: torch.Tensor | None = None, n_visible_host: float = 0.0,
+             check: str = "fused", record: torch.Tensor | None = None,
+             densify: tuple | None = None) -> torch.Tensor:
+        """K2 (plus the strict pre-check when ``check == "strict"``).
+
+        ``record`` given: row-record state (gs_step_rows), ``clock`` ignored;
+        otherwise per-group m / v tensors and the int32 ``clock``.
+        """
+        if mode not in L.MODE_IDS:
+            raise ConfigError(f"unknown mode {mode!r}; expected one of {tuple(L.MODE_IDS)}")
+        if record is None:
+            _check_tensor("clock", clock, self.n_rows, 1, self.device, torch.int32)
+        else:
+            self._check_record(record, groups)
+        garr = self.group_array(groups)
+        s = _stream_handle(self.device)
+        dkey = None if densify is None else (densify[0].data_ptr(), densify[1].data_ptr(),
+                                             float(densify[2]), int(densify[3]))
+        ckey = (mode, check, eps, float(lambda_opacity), float(lambda_scale),
+                float(clip_opacity), float(clip_scale), float(n_pixels_rounded), int(global_t),
+                _ptr(n_visible_dev), float(n_visible_host), dkey)
+        if ckey == self._cfg_key:  # same scalars as the last step: reuse the struct
+            cfg = self._cfg
+        else:
+            cfg = self._build_cfg(mode, check, eps, lambda_opacity, lambda_scale, clip_opacity,
+                                  clip_scale, n_pixels_rounded, global_t, n_visible_dev,
+                                  n_visible_host, densify)
+            self._cfg_key, self._cfg = ckey, cfg
         if check == "strict":
             # the penalty's activation domain is checked where the penalty
             # applies: listed rows, or every row for the dense coupled mode

@@ -295,7 +295,7 @@ class AdamWGS:
                 gr = base_grad_view(p)
             lr = g["lr"] * (mu_lr_scale if g["role"] == L.ROLE_POSITION else 1.0)
             rows = self.state.record is not None
-            out.append(GroupBinding(name, g["role"], lr, p.data, gr,
+            out.append(GroupBinding(name, g["role"], lr, p, gr,  # kernels see pointers only
                                     None if rows else self.state.m[name],
                                     None if rows else self.state.v[name]))
         return out
