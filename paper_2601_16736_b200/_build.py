@@ -17,7 +17,10 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libadamw_gs_b200.so"
-SOURCES = ("gs_abi.cu", "gs_compact.cu", "gs_step.cu", "gs_step_rows.cu", "gs_step_sh3.cu", "gs_state.cu", "gs_noise.cu")
+SOURCES = ("gs_abi.cu", "gs_compact.cu", "gs_step.cu", "gs_step_rows.cu", "gs_step_sh3.cu",
+           "gs_step_sh3_m_coupled.cu", "gs_step_sh3_m_sparse.cu", "gs_step_sh3_m_const.cu",
+           "gs_step_sh3_m_const_clip.cu", "gs_step_sh3_m_adamw_gs.cu", "gs_state.cu",
+           "gs_noise.cu")
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -25,6 +28,7 @@ NVCC_FLAGS = [
     "-Xcompiler", "-fPIC",
     "-Xptxas", "-v",
     "--expt-relaxed-constexpr",
+    "-Xfatbin", "-compress-all",
 ]
 
 
@@ -46,11 +50,13 @@ def _stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> Path:
     if not force and not _stale():
         return LIB
-    objs = []
+    from concurrent.futures import ThreadPoolExecutor
+
     build_dir = PKG / "build"
     build_dir.mkdir(exist_ok=True)
     nvcc = nvcc_path()
-    for src in SOURCES:
+
+    def compile_one(src: str) -> str:
         obj = build_dir / (Path(src).stem + ".o")
         cmd = [nvcc, *NVCC_FLAGS, "-I", str(ROOT / "include"), "-c", str(CSRC / src), "-o", str(obj)]
         res = subprocess.run(cmd, capture_output=True, text=True)
@@ -58,7 +64,12 @@ def build(force: bool = False, verbose: bool = False) -> Path:
             sys.stderr.write(res.stdout + res.stderr)
         if res.returncode != 0:
             raise RuntimeError(f"nvcc failed on {src}")
-        objs.append(str(obj))
+        return str(obj)
+
+    # translation units compile in parallel (the SH-3 kernels are split per mode)
+    workers = max(1, min(len(SOURCES), os.cpu_count() or 1))
+    with ThreadPoolExecutor(max_workers=workers) as pool:
+        objs = list(pool.map(compile_one, SOURCES))
     tmp = LIB.with_suffix(".so.tmp")
     cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", str(tmp), *objs,
            "-lcudart_static", "-Xcompiler", "-fPIC"]

@@ -1,0 +1,7 @@
+// SH-3 fast path kernels for GS_MODE_ADAMW_GS (explicit instantiation; see gs_step_sh3.cuh).
+#include "gs_step_sh3.cuh"
+
+namespace gs {
+template void launch_fixed<LayoutSH3, GS_MODE_ADAMW_GS, false>(const FixedParams&, int64_t, int, cudaStream_t);
+template void launch_fixed<LayoutSH3, GS_MODE_ADAMW_GS, true>(const FixedParams&, int64_t, int, cudaStream_t);
+}  // namespace gs
