@@ -1854,6 +1854,14 @@ void launch_fixed(const FixedParams& P, int64_t max_rows, int kind, cudaStream_t
       launch_ws<L, MODE, STRICT, 32, 3, 3, 8, 2, true>(P, max_rows, s);
     } else if (v == 13) {
       launch_ring<L, MODE, STRICT, 32, 3, 3, 8, 2, false>(P, max_rows, s);
+    } else if (v == 16) {
+      launch_ring<L, MODE, STRICT, 32, 2, 2, 6, 3, true>(P, max_rows, s);
+    } else if (v == 17) {  // the 3-stage ring (default before the 2-stage sweep)
+      launch_ring<L, MODE, STRICT, 32, 3, 3, 8, 2, true>(P, max_rows, s);
+    } else if (v == 18) {
+      launch_ring<L, MODE, STRICT, 32, 2, 2, 8, 2, true>(P, max_rows, s);
+    } else if (v == 19) {
+      launch_ring<L, MODE, STRICT, 32, 2, 4, 8, 2, true>(P, max_rows, s);
     } else if (v == 15) {
       FixedParams Q = P;
       Q.contig = 1;
@@ -1869,7 +1877,9 @@ void launch_fixed(const FixedParams& P, int64_t max_rows, int kind, cudaStream_t
     } else if (v == 12) {
       launch_tma<L, MODE, STRICT, 32, 3, 8, 2>(P, max_rows, s);
     } else {
-      launch_ring<L, MODE, STRICT, 32, 3, 3, 8, 2, true>(P, max_rows, s);
+      // 2 stages beat 3 on every workload measured (c3 K2 0.595 vs 0.627 ms,
+      // profiles/r01/ring_stage_sweep.txt); 2 or 4 producer warps do worse
+      launch_ring<L, MODE, STRICT, 32, 2, 3, 8, 2, true>(P, max_rows, s);
     }
     return;
   }
@@ -1886,7 +1896,8 @@ void launch_fixed(const FixedParams& P, int64_t max_rows, int kind, cudaStream_t
     // ring kernel on per-attribute tensors: a shuffle per 4-byte element costs
     // the producers more than the barrier it saves (0.81 vs 0.78 ms on c3)
     case 7: launch_ring<L, MODE, STRICT, 32, 3, 3, 8, 2, true, false>(P, max_rows, s); return;
-    default: launch_ws<L, MODE, STRICT, 32, 3, 3, 8, 2>(P, max_rows, s); return;
+    case 19: launch_ws<L, MODE, STRICT, 32, 3, 3, 8, 2>(P, max_rows, s); return;  // 3 stages
+    default: launch_ws<L, MODE, STRICT, 32, 2, 3, 8, 2>(P, max_rows, s); return;
   }
 }
 

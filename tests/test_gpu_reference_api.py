@@ -484,13 +484,13 @@ def test_step_kernels_all_identical(mode, check):
     cfg = S.WorkloadConfig(n=20_011, p_vis=0.4, seed=9)
     host = S.make_params(cfg)
     results = []
-    runs = [("fixed", v, "attr") for v in range(8)] + [("rows", v, "attr") for v in range(7)]
+    runs = [("fixed", v, "attr") for v in (*range(8), 19)] + [("rows", v, "attr") for v in range(7)]
     runs += [("groups", 0, "attr")]
     runs += [(k, 0, lay) for k in ("fixed", "rows", "groups") for lay in ("record", "param-record")]
     # record layouts: 0/13/14 = record kernel shapes, 8 = record gathers in the generic ring,
     # 9/10/12 = bulk-copy (TMA) kernels,
     # 11 = cp.async gathers + bulk stores, 15 = ring kernel with contiguous chunk runs
-    runs += [("fixed", v, "record") for v in (8, 9, 10, 11, 12, 13, 14, 15)]
+    runs += [("fixed", v, "record") for v in (8, 9, 10, 11, 12, 13, 14, 15, 16, 17, 18, 19)]
     runs += [(k, 0, "record240") for k in ("fixed", "rows")]  # compact 240-byte rows
     if check == "strict":
         runs = [r for r in runs if r[1] in (0, 3, 7, 8, 11, 12)]
