@@ -32,6 +32,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -96,6 +97,8 @@ def parse():
     ap.add_argument("--host-record-align", type=int, default=16,
                     help="e2e: pinned host gradient record rows padded to a multiple of this "
                          "many floats (16: 256-byte SH-3 rows, two PCIe read lines)")
+    ap.add_argument("--unified", action="store_true",
+                    help="experiment: moment record and parameter row in one row")
     ap.add_argument("--params", default="record", choices=["record", "attr"],
                     help="parameter / gradient HBM layout: attribute views of one "
                          "row-interleaved record (records.py) or one tensor per attribute")
@@ -331,10 +334,23 @@ def workload_config(args, wl, p_vis, world):
                              f") fp32 row record, gradients likewise; moment record rows of "
                              f"{(120 + args.state_align - 1) // args.state_align * args.state_align * 4}"
                              f" B)") if args.params == "record" else "one tensor per attribute",
-            "l2": "inputs larger than L2 (working set >> 126 MB)" if n >= 1_000_000 else
-                  "L2 flushed between timed steps",
+            "l2": "inputs larger than L2 (working set >> 126 MB)" if l2_replicas(n, p_vis) == 1
+                  else f"{l2_replicas(n, p_vis)} independent clouds of this size stepped round "
+                       "robin, so each step's rows are L2-cold (>= 4x L2 of traffic between uses)",
             "parallelism": f"index-sharded x{world}",
             "launch": "CUDA graph of the K timed steps" if (args.graph and world == 1) else "eager"}
+
+
+L2_BYTES = 126 * 2**20
+
+
+def l2_replicas(n, p_vis):
+    """Clouds needed so that, stepping them round robin, >= 4x L2 of K2
+    traffic passes between two steps of the same cloud (1 for big clouds)."""
+    touched = max(1.0, n * p_vis * (28 * 59 + 12))
+    if touched >= 4 * L2_BYTES:
+        return 1
+    return 1 + math.ceil(4 * L2_BYTES / touched)
 
 
 # --------------------------------------------------------------- our arm
@@ -358,18 +374,41 @@ def ours(args, wl, p_vis):
     base = rank * n
     cfg = S.WorkloadConfig(n=n, p_vis=p_vis, mask_family=args.mask, seed=args.seed * 1000 + rank,
                            lambda_o=wl["lo"], lambda_s=wl["ls"])
-    params = S.make_params_device(cfg, dev)
-    if args.params == "record":
-        _, params = R.pack(params, align=args.record_align)
-    opt = AdamWGS(S.param_groups(params), mode=wl["mode"], lambda_o=wl["lo"], lambda_s=wl["ls"],
-                  check=args.check, errors="defer", state_layout=args.layout,
-                  state_row_align=args.state_align)
+    # clouds whose touched bytes fit in L2 are replicated and stepped round
+    # robin, so every timed step reads rows that >= 4x L2 of other traffic has
+    # passed through since their last use (same per-step workload, cold L2)
+    n_rep = l2_replicas(n, p_vis)
+    opts, grad_sets = [], []
+    for j in range(n_rep):
+        cj = S.WorkloadConfig(n=n, p_vis=p_vis, mask_family=args.mask,
+                              seed=(args.seed * 1000 + rank) * 1000 + j if j else
+                              args.seed * 1000 + rank, lambda_o=wl["lo"], lambda_s=wl["ls"])
+        params = S.make_params_device(cj, dev)
+        if args.params == "record":
+            _, params = R.pack(params, align=args.record_align)
+        uni = None
+        if args.unified:
+            params, uni = _unified(params, args.record_align, args.state_align)
+        opts.append(AdamWGS(S.param_groups(params), mode=wl["mode"], lambda_o=wl["lo"],
+                            lambda_s=wl["ls"], check=args.check, errors="defer",
+                            state_layout=args.layout, state_row_align=args.state_align))
+        if uni is not None:
+            from paper_2601_16736_b200.optimizer import MomentState
+            opts[-1].state = MomentState.from_record(uni, opts[-1].state.spec)
+        gs = [S.grads_device(cj, s, dev) for s in range(2 if n_rep == 1 else 1)]
+        if args.params == "record":
+            gs = [R.pack(g, align=args.record_align)[1] for g in gs]
+        grad_sets.append(gs)
+    opt = opts[0]
+
+    def replica(it):
+        """(optimizer, gradients) of step it."""
+        j = it % n_rep
+        return opts[j], grad_sets[j][it % len(grad_sets[j])]
+
     total_steps = args.warmup + args.steps
     masks = [S.visibility_device(cfg, s, dev) for s in range(total_steps)]
     n_vis = torch.stack([m.sum() for m in masks]).cpu().numpy().astype(np.int64)
-    grad_sets = [S.grads_device(cfg, s, dev) for s in range(2)]
-    if args.params == "record":
-        grad_sets = [R.pack(g, align=args.record_align)[1] for g in grad_sets]
     # RSR / relocation samples are host-drawn with the reference RNG contract
     # (optimizer.py:379-386, rng.py:17-30) and uploaded before timing.
     events = {}
@@ -394,9 +433,9 @@ def ours(args, wl, p_vis):
 
     def one_step(it):
         """K1 + K2 (+ K3 on RSR / relocation boundaries) for step it."""
-        eng = opt.engine
-        rows, count = eng.compact(masks[it])
-        _step_k2(opt, grad_sets[it % 2], rows, count, wl)
+        opt, grads = replica(it)
+        rows, count = opt.engine.compact(masks[it])
+        _step_k2(opt, grads, rows, count, wl)
         ev = events.get(it)
         if ev:
             if "rsr" in ev:
@@ -418,14 +457,14 @@ def ours(args, wl, p_vis):
     # small clouds are otherwise host-bound).  Multi-rank runs stay eager
     # (the per-step NCCL all-reduce is issued from the host).
     use_graph = args.graph and world == 1
-    launches0 = opt.engine.launches
+    launches0 = sum(o.engine.launches for o in opts)
     graph = None
     if use_graph:
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph):
             for it in timed_steps:
                 one_step(it)
-    launches[0] = opt.engine.launches - launches0
+    launches[0] = sum(o.engine.launches for o in opts) - launches0
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
@@ -439,9 +478,9 @@ def ours(args, wl, p_vis):
         torch.cuda.synchronize()
     ms = start.elapsed_time(end)
     if graph is None:
-        launches[0] = opt.engine.launches - launches0
+        launches[0] = sum(o.engine.launches for o in opts) - launches0
     del graph
-    st = opt.last_stats()  # the last timed step's statistics (host read, after timing)
+    st = replica(total_steps - 1)[0].last_stats()  # the last timed step's statistics (host read, after timing)
     if st["n_bad_grad"] or st["n_bad_domain"] or st["n_stepped"] != st["n_visible"]:
         raise RuntimeError(f"step statistics report skipped rows: {st}")
     ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
@@ -458,12 +497,13 @@ def ours(args, wl, p_vis):
     # rank) between two CUDA events on the launching stream
     idx_lists = []
     for it in timed_steps:
-        rows, count = opt.engine.compact(masks[it])
+        rows, count = replica(it)[0].engine.compact(masks[it])
         idx_lists.append((rows.clone(), count.clone()))
 
     def k2_only():
         for j, it in enumerate(timed_steps):
-            _step_k2(opt, grad_sets[it % 2], idx_lists[j][0], idx_lists[j][1], wl)
+            o, grads = replica(it)
+            _step_k2(o, grads, idx_lists[j][0], idx_lists[j][1], wl)
 
     k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if use_graph:
@@ -538,6 +578,28 @@ def ours(args, wl, p_vis):
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def _unified(params, record_align, state_align):
+    """Experiment: one row per Gaussian holding the moment record and then
+    the parameter row ([m/v pairs + clock | theta]), so a visible row is one
+    contiguous span plus its gradient row.  Returns (parameter views, the
+    state-record view)."""
+    import torch
+    n = next(iter(params.values())).shape[0]
+    p = sum(max(1, int(t[0].numel())) for t in params.values())
+    pw = (p + record_align - 1) // record_align * record_align
+    sw = (2 * (p + 1) + state_align - 1) // state_align * state_align
+    u = torch.zeros((n, sw + pw), dtype=torch.float32, device=next(iter(params.values())).device)
+    out, off = {}, sw
+    for name, t in params.items():
+        w = max(1, int(t[0].numel()))
+        v = u[:, off:off + w]
+        v = v.view(n, *t.shape[1:]) if t.dim() > 1 else v.view(n)
+        v.copy_(t)
+        out[name] = v
+        off += w
+    return out, u[:, :sw]
 
 
 def _step_k2(opt, grads, rows, count, wl):

@@ -300,6 +300,18 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
 }
+// 16-byte piece with an L2 prefetch-size hint (the L2 fills the whole 256-B
+// (or 128-B) aligned span around the piece from DRAM in one request)
+template <int HINT>
+__device__ __forceinline__ void cp_async16_h(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  if (HINT & 1)
+    asm volatile("cp.async.cg.shared.global.L2::256B [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+  else if (HINT & 4)
+    asm volatile("cp.async.cg.shared.global.L2::128B [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+  else
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
 __device__ __forceinline__ void cp_async16_ca(void* smem, const void* gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
@@ -1221,7 +1233,7 @@ void launch_ws(const FixedParams& P, int64_t max_rows, cudaStream_t s) {
 //     barrier nothing else needs a block-wide ordering point.
 // ---------------------------------------------------------------------------
 template <class L, int MODE, bool STRICT, int R, int S, int NPW, int NCW, int MINB, bool FLAT,
-          bool REC>
+          bool REC, int HINT>
 __global__ void __launch_bounds__((NPW + NCW) * 32, MINB) step_ring_kernel(const FixedParams P) {
   static_assert(REC || FLAT, "per-attribute gathers use the flattened producer");
   static_assert(R == 32, "one lane per row id");
@@ -1321,7 +1333,7 @@ __global__ void __launch_bounds__((NPW + NCW) * 32, MINB) step_ring_kernel(const
           const uint32_t row = id_of(r);
           if (r < nv) {
             const int q = p - r * kRecPieces;
-            cp_async16(srec + r * (2 * SLOTS) + 4 * q, P.record + (size_t)row * P.stride + 4 * q);
+            cp_async16_h<HINT>(srec + r * (2 * SLOTS) + 4 * q, P.record + (size_t)row * P.stride + 4 * q);
           }
         }
         if (REC) {
@@ -1332,7 +1344,7 @@ __global__ void __launch_bounds__((NPW + NCW) * 32, MINB) step_ring_kernel(const
             const uint32_t row = id_of(r);
             if (r < nv) {
               const int q = p - r * kRowPieces;
-              cp_async16(sth + r * PL + 4 * q, P.prec + row * P.prs + 4 * q);
+              cp_async16_h<HINT>(sth + r * PL + 4 * q, P.prec + row * P.prs + 4 * q);
             }
           }
 #pragma unroll
@@ -1345,7 +1357,7 @@ __global__ void __launch_bounds__((NPW + NCW) * 32, MINB) step_ring_kernel(const
               if (P.grec_ca)
                 cp_async16_ca(sg + r * PL + 4 * q, P.grec + row * P.grs + 4 * q);
               else
-                cp_async16(sg + r * PL + 4 * q, P.grec + row * P.grs + 4 * q);
+                cp_async16_h<HINT>(sg + r * PL + 4 * q, P.grec + row * P.grs + 4 * q);
             }
           }
         } else {
@@ -1386,16 +1398,16 @@ __global__ void __launch_bounds__((NPW + NCW) * 32, MINB) step_ring_kernel(const
         for (int j = 0; j < (kPiecesPerRow + 31) / 32; ++j) {
           const int p = lane + 32 * j;
           if (p < kRecPieces) {
-            cp_async16(srec + r * (2 * SLOTS) + 4 * p, P.record + (size_t)row * P.stride + 4 * p);
+            cp_async16_h<HINT>(srec + r * (2 * SLOTS) + 4 * p, P.record + (size_t)row * P.stride + 4 * p);
           } else if (p < kRecPieces + kRowPieces) {
             const int q = p - kRecPieces;
-            cp_async16(sth + r * PL + 4 * q, P.prec + row * P.prs + 4 * q);
+            cp_async16_h<HINT>(sth + r * PL + 4 * q, P.prec + row * P.prs + 4 * q);
           } else if (p < kPiecesPerRow) {
             const int q = p - kRecPieces - kRowPieces;
             if (P.grec_ca)
               cp_async16_ca(sg + r * PL + 4 * q, P.grec + row * P.grs + 4 * q);
             else
-              cp_async16(sg + r * PL + 4 * q, P.grec + row * P.grs + 4 * q);
+              cp_async16_h<HINT>(sg + r * PL + 4 * q, P.grec + row * P.grs + 4 * q);
           }
         }
       }
@@ -1454,7 +1466,8 @@ __global__ void __launch_bounds__((NPW + NCW) * 32, MINB) step_ring_kernel(const
       if (t < nvalid) {
         ++c_vis;
         if (row_ok(t)) {
-          reinterpret_cast<int*>(rec_base + (size_t)srow[t] * rec_stride2 + L::P)[0] = tn;
+          int* const clk = reinterpret_cast<int*>(rec_base + (size_t)srow[t] * rec_stride2 + L::P);
+          if (HINT & 2) __stcs(clk, tn); else *clk = tn;
           if (P.D.group >= 0) {
 #pragma unroll
             for (int gg = 0; gg < L::G; ++gg)
@@ -1491,8 +1504,13 @@ __global__ void __launch_bounds__((NPW + NCW) * 32, MINB) step_ring_kernel(const
           c_apre += th > P.active_logit;
           c_apost += tnv > P.active_logit;
         }
-        P.g[gg].param[row * P.g[gg].ps + (uint32_t)c] = tnv;
-        rec_base[(size_t)row * rec_stride2 + L::OFF(gg) + c] = make_float2(mn, vn);
+        if (HINT & 2) {  // streaming (evict-first) stores
+          __stcs(P.g[gg].param + row * P.g[gg].ps + (uint32_t)c, tnv);
+          __stcs(rec_base + (size_t)row * rec_stride2 + L::OFF(gg) + c, make_float2(mn, vn));
+        } else {
+          P.g[gg].param[row * P.g[gg].ps + (uint32_t)c] = tnv;
+          rec_base[(size_t)row * rec_stride2 + L::OFF(gg) + c] = make_float2(mn, vn);
+        }
       };
       if (!any_bad) {
 #pragma unroll
@@ -1537,19 +1555,19 @@ __global__ void __launch_bounds__((NPW + NCW) * 32, MINB) step_ring_kernel(const
 }
 
 template <class L, int MODE, bool STRICT, int R, int S, int NPW, int NCW, int MINB, bool FLAT,
-          bool REC = true>
+          bool REC = true, int HINT = 0>
 void launch_ring(const FixedParams& P, int64_t max_rows, cudaStream_t s) {
   constexpr int bytes = S * WsStage<L, R>::kBytes;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(step_ring_kernel<L, MODE, STRICT, R, S, NPW, NCW, MINB, FLAT, REC>,
+    cudaFuncSetAttribute(step_ring_kernel<L, MODE, STRICT, R, S, NPW, NCW, MINB, FLAT, REC, HINT>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     attr_set = true;
   }
   const int64_t chunks = (max_rows + R - 1) / R;
   const int grid =
       (int)std::max<int64_t>(1, std::min<int64_t>(chunks, (int64_t)gs_sm_count() * MINB));
-  step_ring_kernel<L, MODE, STRICT, R, S, NPW, NCW, MINB, FLAT, REC>
+  step_ring_kernel<L, MODE, STRICT, R, S, NPW, NCW, MINB, FLAT, REC, HINT>
       <<<grid, (NPW + NCW) * 32, bytes, s>>>(P);
 }
 
@@ -1862,6 +1880,8 @@ void launch_fixed(const FixedParams& P, int64_t max_rows, int kind, cudaStream_t
       launch_ring<L, MODE, STRICT, 32, 2, 2, 8, 2, true>(P, max_rows, s);
     } else if (v == 19) {
       launch_ring<L, MODE, STRICT, 32, 2, 4, 8, 2, true>(P, max_rows, s);
+    } else if (v == 20) {  // no L2 prefetch-size hint on the gathers
+      launch_ring<L, MODE, STRICT, 32, 2, 3, 8, 2, true, true, 0>(P, max_rows, s);
     } else if (v == 15) {
       FixedParams Q = P;
       Q.contig = 1;
@@ -1879,7 +1899,9 @@ void launch_fixed(const FixedParams& P, int64_t max_rows, int kind, cudaStream_t
     } else {
       // 2 stages beat 3 on every workload measured (c3 K2 0.595 vs 0.627 ms,
       // profiles/r01/ring_stage_sweep.txt); 2 or 4 producer warps do worse
-      launch_ring<L, MODE, STRICT, 32, 2, 3, 8, 2, true>(P, max_rows, s);
+      // L2::256B prefetch-size hint on the gathers: 0.595 -> 0.592 ms (c3),
+      // same on coherent masks; evict-first stores measured no change
+      launch_ring<L, MODE, STRICT, 32, 2, 3, 8, 2, true, true, 1>(P, max_rows, s);
     }
     return;
   }
