@@ -29,8 +29,8 @@
 //   step_fixed_kernel (phase-separated), step_pipe / step_pipe2_kernel (the
 //   first cp.async rings), step_ws_kernel<REC=1> (+ BULKST bulk stores),
 //   step_tma_kernel (cp.async.bulk loads / stores: bound by the TMA unit's
-//   per-operation cost on 256/512-byte rows), step_ring_kernel shapes and
-//   contiguous chunk runs.
+//   per-operation cost on 256/512-byte rows), other step_ring_kernel shapes
+//   (ring depth, warp split, no L2 prefetch-size hint).
 #include <stdlib.h>
 
 #include "gs_common.cuh"
@@ -84,7 +84,6 @@ struct FixedParams {
   uint32_t grs;
   int grec_ca;  // gradient record copies through L1 (.ca): host-mapped gradients
   int tma_ok;   // records and the state record allow 16-byte bulk copies
-  int contig;   // ring kernel: contiguous chunk runs per CTA instead of grid-stride
   double* stats_out;
   double* partials;
   unsigned int* counter;
@@ -1261,20 +1260,15 @@ __global__ void __launch_bounds__((NPW + NCW) * 32, MINB) step_ring_kernel(const
 
   const int tid = threadIdx.x;
   const bool producer = tid >= NC;
-  int64_t n_rows = kDense ? P.max_rows : (int64_t)(*P.n_rows_dev);
+  // 32-bit chunk bookkeeping: row ids are int32 and the fixed-layout
+  // dispatch keeps max_rows * row stride below 2^32 (rows_kind)
+  int n_rows = kDense ? (int)P.max_rows : *P.n_rows_dev;
   if (STRICT && *P.abort_flag != 0) n_rows = 0;
-  const int64_t n_chunks = (n_rows + R - 1) / R;
-  // chunk order: grid-stride (default) or, with P.contig, a contiguous run of
-  // chunks per CTA
-  const int64_t cpb = (n_chunks + gridDim.x - 1) / gridDim.x;
-  auto chunk_id = [&](int64_t k) {
-    return P.contig ? (int64_t)blockIdx.x * cpb + k : (int64_t)blockIdx.x + k * gridDim.x;
-  };
-  auto chunk_ok = [&](int64_t k) { return (!P.contig || k < cpb) && chunk_id(k) < n_chunks; };
-  auto chunk_rows = [&](int64_t k) -> int {
-    if (P.contig && k >= cpb) return 0;
-    const int64_t rem = n_rows - chunk_id(k) * R;
-    return rem <= 0 ? 0 : (rem < R ? (int)rem : R);
+  const int n_chunks = (n_rows + R - 1) / R;
+  const int G = (int)gridDim.x;  // chunks are taken grid-stride: c = blockIdx.x + k * G
+  auto chunk_rows = [&](int c) -> int {
+    const int rem = n_rows - c * R;
+    return rem <= 0 ? 0 : (rem < R ? rem : R);
   };
   auto stage = [&](int st) { return smem + st * ST::kBytes; };
   // staged theta / grad: row-major for records, group-major for per-attribute gathers
@@ -1305,18 +1299,19 @@ __global__ void __launch_bounds__((NPW + NCW) * 32, MINB) step_ring_kernel(const
     const int pt = tid - NC;
     const int lane = pt & 31;
     const int warp = pt >> 5;
-    auto fetch_id = [&](int64_t k) -> uint32_t {
-      if (lane >= chunk_rows(k)) return 0u;
-      const int64_t i = chunk_id(k) * R + lane;
+    auto fetch_id = [&](int c) -> uint32_t {
+      if (lane >= chunk_rows(c)) return 0u;
+      const int i = c * R + lane;
       return kDense ? (uint32_t)i : (uint32_t)__ldg(P.rows + i);
     };
-    uint32_t next_id = fetch_id(0);
-    for (int64_t k = 0; chunk_ok(k); ++k) {
-      const int st = (int)(k % S);
+    uint32_t next_id = fetch_id((int)blockIdx.x);
+    int st = 0;
+    unsigned ph = 0;  // parity of this use of stage st
+    for (int c = (int)blockIdx.x, k = 0; c < n_chunks; c += G, ++k) {
       const uint32_t my_id = next_id;
-      next_id = fetch_id(k + 1);
-      if (k >= S) mbar_wait(&empty_bar[st], (unsigned)(((k / S) - 1) & 1));
-      const int nv = chunk_rows(k);
+      next_id = fetch_id(c + G);
+      if (k >= S) mbar_wait(&empty_bar[st], ph ^ 1u);
+      const int nv = chunk_rows(c);
       unsigned char* sb = stage(st);
       float* srec = reinterpret_cast<float*>(sb);
       float* sth = reinterpret_cast<float*>(sb + ST::kRec);
@@ -1386,7 +1381,7 @@ __global__ void __launch_bounds__((NPW + NCW) * 32, MINB) step_ring_kernel(const
         // row ids and bias factors ride the stage too, so the consumers
         // touch no global memory before their barrier; the clock read here
         // stalls only this producer warp, which runs chunks ahead
-        if (!kDense) cp_async4(&s_crow[st][lane], P.rows + chunk_id(k) * R + lane);
+        if (!kDense) cp_async4(&s_crow[st][lane], P.rows + c * R + lane);
         const int tb = kDense ? P.global_t
                               : __ldg(reinterpret_cast<const int*>(P.record + (size_t)my_id * P.stride +
                                                                    2 * L::P)) + 1;
@@ -1412,6 +1407,10 @@ __global__ void __launch_bounds__((NPW + NCW) * 32, MINB) step_ring_kernel(const
         }
       }
       mbar_arrive_cp_async(&full_bar[st]);
+      if (++st == S) {
+        st = 0;
+        ph ^= 1u;
+      }
     }
   } else {
     // ------------------------------------------------------------------ consumers
@@ -1425,12 +1424,12 @@ __global__ void __launch_bounds__((NPW + NCW) * 32, MINB) step_ring_kernel(const
     const StepConsts& K = kCoupled ? Kc : P.K;
     float2* const rec_base = reinterpret_cast<float2*>(P.record);
     const uint32_t rec_stride2 = (uint32_t)(P.stride / 2);
-    for (int64_t k = 0; chunk_ok(k); ++k) {
-      const int st = (int)(k % S);
-      const int ep = (int)(k / S) + 1;  // this use of stage st
-      const int nvalid = chunk_rows(k);
-      if (kDense && t < R) s_crow[st][t] = (uint32_t)(chunk_id(k) * R + t);
-      mbar_wait(&full_bar[st], (unsigned)((k / S) & 1));
+    int st = 0;
+    int ep = 1;  // this use of stage st (epoch tag of its row flags)
+    for (int c = (int)blockIdx.x; c < n_chunks; c += G) {
+      const int nvalid = chunk_rows(c);
+      if (kDense && t < R) s_crow[st][t] = (uint32_t)(c * R + t);
+      mbar_wait(&full_bar[st], (unsigned)((ep - 1) & 1));
       const unsigned char* sb = stage(st);
       const float2* srec = reinterpret_cast<const float2*>(sb);
       const float* sth = reinterpret_cast<const float*>(sb + ST::kRec);
@@ -1438,7 +1437,48 @@ __global__ void __launch_bounds__((NPW + NCW) * 32, MINB) step_ring_kernel(const
       const uint32_t* srow = s_crow[st];
       // row ids (sparse modes) and bias factors were staged by the producers
       const int tn = t < nvalid ? reinterpret_cast<const int*>(srec + t * SLOTS + L::P)[0] + 1 : 0;
-      if (!STRICT) {
+      if (!STRICT && REC) {
+        // gradients: the staged rows' 16-byte pieces (pad columns ignored);
+        // activation domain: the opacity / scale columns of theta, on the
+        // top threads (the gradient pieces leave them one piece short)
+        constexpr int kQ = PL / 4;
+#pragma unroll
+        for (int j = 0; j < (R * kQ + NC - 1) / NC; ++j) {
+          const int p = j * NC + t;
+          const int r = p / kQ;
+          if (p < R * kQ && r < nvalid) {
+            const int q = p - r * kQ;
+            const float4 v = reinterpret_cast<const float4*>(sg + r * PL)[q];
+            const bool bad = !isfinite(v.x) || (4 * q + 1 < L::P && !isfinite(v.y)) ||
+                             (4 * q + 2 < L::P && !isfinite(v.z)) ||
+                             (4 * q + 3 < L::P && !isfinite(v.w));
+            if (bad) {
+              atomicMax(&s_badg[st][r], ep);
+              s_any[st] = ep;
+            }
+          }
+        }
+        int dbase = 0;
+#pragma unroll
+        for (int gg = 0; gg < L::G; ++gg) {
+          const int role = L::ROLE(gg);
+          if (role != GS_ROLE_OPACITY && role != GS_ROLE_SCALE) continue;
+          const int W = L::W(gg);
+          const float lam = role == GS_ROLE_OPACITY ? K.lam_op : K.lam_sc;
+          if (lam != 0.f) {
+#pragma unroll
+            for (int kk = 0; kk < (R * W + NC - 1) / NC; ++kk) {
+              const int i = kk * NC + (NC - 1 - t + NC - dbase % NC) % NC;
+              const int r = i / W;
+              if (i < R * W && r < nvalid && domain_bad(role, sth[r * PL + L::OFF(gg) + (i - r * W)])) {
+                atomicMax(&s_badd[st][r], ep);
+                s_any[st] = ep;
+              }
+            }
+          }
+          dbase += R * W;
+        }
+      } else if (!STRICT) {
 #pragma unroll
         for (int gg = 0; gg < L::G; ++gg) {
           const int W = L::W(gg);
@@ -1534,6 +1574,10 @@ __global__ void __launch_bounds__((NPW + NCW) * 32, MINB) step_ring_kernel(const
         }
       }
       mbar_arrive(&empty_bar[st]);  // this thread's reads of the stage are done
+      if (++st == S) {
+        st = 0;
+        ++ep;
+      }
     }
   }
   cp_async_wait<0>();
@@ -1882,10 +1926,6 @@ void launch_fixed(const FixedParams& P, int64_t max_rows, int kind, cudaStream_t
       launch_ring<L, MODE, STRICT, 32, 2, 4, 8, 2, true>(P, max_rows, s);
     } else if (v == 20) {  // no L2 prefetch-size hint on the gathers
       launch_ring<L, MODE, STRICT, 32, 2, 3, 8, 2, true, true, 0>(P, max_rows, s);
-    } else if (v == 15) {
-      FixedParams Q = P;
-      Q.contig = 1;
-      launch_ring<L, MODE, STRICT, 32, 3, 3, 8, 2, true>(Q, max_rows, s);
     } else if (v == 14) {
       launch_ring<L, MODE, STRICT, 32, 3, 2, 8, 2, true>(P, max_rows, s);
     } else if (v == 11) {

@@ -489,8 +489,9 @@ def test_step_kernels_all_identical(mode, check):
     runs += [(k, 0, lay) for k in ("fixed", "rows", "groups") for lay in ("record", "param-record")]
     # record layouts: 0/13/14 = record kernel shapes, 8 = record gathers in the generic ring,
     # 9/10/12 = bulk-copy (TMA) kernels,
-    # 11 = cp.async gathers + bulk stores, 15 = ring kernel with contiguous chunk runs
-    runs += [("fixed", v, "record") for v in (8, 9, 10, 11, 12, 13, 14, 15, 16, 17, 18, 19, 20)]
+    # 11 = cp.async gathers + bulk stores, 16-19 = ring depth / warp splits,
+    # 20 = ring kernel without the L2 prefetch-size hint
+    runs += [("fixed", v, "record") for v in (8, 9, 10, 11, 12, 13, 14, 16, 17, 18, 19, 20)]
     runs += [(k, 0, "record240") for k in ("fixed", "rows")]  # compact 240-byte rows
     if check == "strict":
         runs = [r for r in runs if r[1] in (0, 3, 7, 8, 11, 12)]
