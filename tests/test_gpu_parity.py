@@ -227,3 +227,68 @@ def test_c1_100_steps_vs_oracles(family, layout, params_layout):
         assert normwise(got_p, p64[gname]) <= NORM_TOL, gname
         assert normwise(got_m, m64[gname]) <= NORM_TOL, gname
         assert normwise(got_v, v64[gname]) <= NORM_TOL, gname
+
+
+# --------------------------------------------------------------------------
+# Edge cases: empty, single-row and ragged visibility (chunk tails of the
+# ring kernel, zero-length launches), every step mode, both layouts
+# --------------------------------------------------------------------------
+
+def _edge_masks(n, rng):
+    out = [np.zeros(n, bool), np.ones(n, bool)]
+    one = np.zeros(n, bool)
+    one[n - 1] = True                      # only the last row
+    out.append(one)
+    out.append(rng.random(n) < 0.5)
+    alt = np.zeros(n, bool)
+    alt[::33] = True                       # one row per 33: never a full chunk-aligned run
+    out.append(alt)
+    return out
+
+
+@pytest.mark.parametrize("n", [1, 31, 32, 33, 1023])
+@pytest.mark.parametrize("params_layout", ["attr", "record"])
+@pytest.mark.parametrize("mode", ["adamw-gs", "sparse-adam", "adamw-const-clip"])
+def test_edge_visibility_bit_exact_vs_fp32_order(n, params_layout, mode):
+    """Empty, all-visible, last-row-only and ragged masks on tiny clouds: the
+    step (K1 + K2, including zero-length and partial-chunk launches) stays
+    bit-exact with the fp32 restatement, and invisible rows are untouched."""
+    from paper_2601_16736_b200 import records as R
+    from paper_2601_16736_b200 import synthetic as S
+    from paper_2601_16736_b200.optimizer import AdamWGS
+    rng = np.random.default_rng(n)
+    cfg = S.WorkloadConfig(n=n, p_vis=0.5, seed=n + 7)
+    host = S.make_params(cfg)
+    params = {k: torch.from_numpy(v).to(DEV) for k, v in host.items()}
+    if params_layout == "record":
+        _, params = R.pack(params)
+    lo = cfg.lambda_o if mode != "sparse-adam" else 0.01
+    ls = cfg.lambda_s if mode != "sparse-adam" else 0.0
+    opt = AdamWGS(S.param_groups(params, cfg), mode=mode, lambda_o=lo, lambda_s=ls)
+    lay = O.LAYOUT_SH3
+    hp = O.Hyper(lr=S.LR_SH3, lambda_o=lo, lambda_s=ls)
+    p32 = {k: v.copy() for k, v in host.items()}
+    m32 = {g.name: np.zeros((n, g.width), np.float32) for g in lay}
+    v32 = {g.name: np.zeros((n, g.width), np.float32) for g in lay}
+    c32 = np.zeros(n, np.int32)
+    masks = _edge_masks(n, rng)
+    lut = O.bias_lut_f32(0.9, 0.999, len(masks) + 2)
+    for s, vis in enumerate(masks):
+        g = S.step_grads(cfg, s, vis)
+        before = {k: p.detach().cpu().numpy().copy() for k, p in params.items()}
+        opt.step(torch.from_numpy(vis).to(DEV), cfg.n_pixels,
+                 grads={k: torch.from_numpy(x).to(DEV) for k, x in g.items()})
+        kw = dict(lambda_o=lo, lambda_s=ls, n_visible_norm=int(vis.sum())) \
+            if mode == "sparse-adam" else {}
+        O.step_fp32(mode, lay, p32, g, m32, v32, c32, np.flatnonzero(vis), hp,
+                    n_pixels=cfg.n_pixels, lut=lut, **kw)
+        st = opt.last_stats()
+        assert st["n_visible"] == int(vis.sum()) == st["n_stepped"], (s, st)
+        for k, p in params.items():
+            now = p.detach().cpu().numpy()
+            assert np.array_equal(now[~vis], before[k][~vis]), (s, k)
+    assert np.array_equal(opt.state.clock.contiguous().cpu().numpy(), c32)
+    for gname in host:
+        assert_close_ulp(params[gname].cpu().numpy(), p32[gname], f"{gname}/param")
+        assert_close_ulp(opt.state.m[gname].contiguous().cpu().numpy(), m32[gname], f"{gname}/m")
+        assert_close_ulp(opt.state.v[gname].contiguous().cpu().numpy(), v32[gname], f"{gname}/v")
