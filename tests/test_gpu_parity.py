@@ -292,3 +292,73 @@ def test_edge_visibility_bit_exact_vs_fp32_order(n, params_layout, mode):
         assert_close_ulp(params[gname].cpu().numpy(), p32[gname], f"{gname}/param")
         assert_close_ulp(opt.state.m[gname].contiguous().cpu().numpy(), m32[gname], f"{gname}/m")
         assert_close_ulp(opt.state.v[gname].contiguous().cpu().numpy(), v32[gname], f"{gname}/v")
+
+
+# --------------------------------------------------------------------------
+# Maximum sizes: the fixed-layout kernels use 32-bit row offsets up to
+# rows * row stride < 2^32 (60M granule-aligned rows); beyond that
+# (70M rows) the dispatch falls back to the generic 64-bit row kernel
+# --------------------------------------------------------------------------
+
+@pytest.mark.parametrize("n", [60_000_000, 70_000_000])
+def test_max_size_clouds_sampled_rows_vs_fp32_order(n):
+    """A 60M-row cloud (the fixed-layout kernel right below its 32-bit offset
+    limit) and a 70M-row cloud (past it: the generic kernel) in granule-aligned
+    records (~72 GB in HBM).  Two steps; 4096 sampled visible rows, including
+    the last rows of the cloud, are bit-exact with the fp32 restatement and a
+    sample of invisible rows is untouched."""
+    from paper_2601_16736_b200 import records as R
+    from paper_2601_16736_b200 import synthetic as S
+    from paper_2601_16736_b200.optimizer import AdamWGS
+    if torch.cuda.get_device_properties(0).total_memory < 150 * 2**30:
+        pytest.skip("needs a 180 GB B200")
+    g = torch.Generator(device=DEV)
+    g.manual_seed(n)
+    shapes = {name: (w,) for name, w in S.SH3_LAYOUT}
+    prec = torch.zeros((n, 64), dtype=torch.float32, device=DEV)
+    params = R.views(prec, shapes)
+    for name, p in params.items():  # in place, no full-size temporaries
+        if name == "scaling":
+            p.uniform_(-6.9, -0.7, generator=g)
+        elif name == "opacity":
+            p.normal_(-1.0, 2.0, generator=g)
+        else:
+            p.normal_(0.0, 1.0, generator=g)
+    grec = torch.zeros((n, 64), dtype=torch.float32, device=DEV)
+    grads = R.views(grec, shapes)
+    for gv in grads.values():
+        gv.normal_(0.0, 1e-3, generator=g)
+    vis = torch.rand(n, device=DEV, generator=g) < 0.3
+    vis[-3:] = True
+    vis[-4] = False
+    opt = AdamWGS(S.param_groups(params), mode="adamw-gs", lambda_o=1e-3, lambda_s=1e-5)
+    rng = np.random.default_rng(n)
+    vis_idx = torch.nonzero(vis).view(-1)
+    pick = torch.from_numpy(np.unique(np.concatenate([
+        rng.choice(vis_idx.numel(), 4093, replace=False), [vis_idx.numel() - k for k in (1, 2, 3)]])))
+    rows = vis_idx[pick.to(DEV)]
+    frozen = torch.tensor([n - 4, 0, n // 2 + 1], device=DEV)
+    frozen = frozen[~vis[frozen]]
+    host_p = {k: p[rows].cpu().numpy().reshape(rows.numel(), -1) for k, p in params.items()}
+    host_g = {k: x[rows].cpu().numpy().reshape(rows.numel(), -1) for k, x in grads.items()}
+    before_frozen = prec[frozen].cpu().numpy()
+    for _ in range(2):
+        opt.step(vis, 1_000_000, grads=grads)
+    k = rows.numel()
+    lay = O.LAYOUT_SH3
+    hp = O.Hyper(lr=S.LR_SH3, lambda_o=1e-3, lambda_s=1e-5)
+    m32 = {gr.name: np.zeros((k, gr.width), np.float32) for gr in lay}
+    v32 = {gr.name: np.zeros((k, gr.width), np.float32) for gr in lay}
+    c32 = np.zeros(k, np.int32)
+    lut = O.bias_lut_f32(0.9, 0.999, 4)
+    for _ in range(2):
+        O.step_fp32("adamw-gs", lay, host_p, host_g, m32, v32, c32, np.arange(k), hp,
+                    n_pixels=1_000_000, lut=lut)
+    assert np.array_equal(opt.state.clock[rows].cpu().numpy(), c32)
+    for name, p in params.items():
+        assert_close_ulp(p[rows].cpu().numpy().reshape(k, -1), host_p[name], f"{name}/param")
+        assert_close_ulp(opt.state.m[name][rows].cpu().numpy().reshape(k, -1), m32[name], f"{name}/m")
+        assert_close_ulp(opt.state.v[name][rows].cpu().numpy().reshape(k, -1), v32[name], f"{name}/v")
+    assert np.array_equal(prec[frozen].cpu().numpy(), before_frozen)
+    del opt, prec, grec, params, grads
+    torch.cuda.empty_cache()
