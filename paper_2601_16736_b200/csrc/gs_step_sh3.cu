@@ -76,8 +76,10 @@ int rows_kind(const gs_group* groups, int64_t max_rows, FixedParams& P) {
     grec = grec && gs == gs0 && g.grad == groups[0].grad + L::OFF(i);
     smax = std::max(smax, std::max(ps, gs));
   }
-  if (max_rows * smax + smax >= (int64_t)UINT32_MAX) return -1;
-  if (dense) return 0;
+  // past 2^32 elements of row offset only the record ring kernel runs, with
+  // 64-bit offsets (P.wide); everything else falls back to the generic kernels
+  const bool wide = max_rows * smax + smax >= (int64_t)UINT32_MAX;
+  if (dense && !wide) return 0;
   prec = prec && ps0 >= PL && ps0 % 4 == 0 && (reinterpret_cast<uintptr_t>(groups[0].param) & 15u) == 0;
   grec = grec && gs0 >= PL && gs0 % 4 == 0 && (reinterpret_cast<uintptr_t>(groups[0].grad) & 15u) == 0;
   if (prec && grec) {
@@ -91,9 +93,10 @@ int rows_kind(const gs_group* groups, int64_t max_rows, FixedParams& P) {
     (void)cudaGetLastError();
     const char* e = getenv("GS_GREC_CA");
     P.grec_ca = e ? atoi(e) : (host ? 1 : 0);
+    P.wide = wide ? 1 : 0;
     return 2;
   }
-  return 1;
+  return wide ? -1 : 1;
 }
 
 template <class L>

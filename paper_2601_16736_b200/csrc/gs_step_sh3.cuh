@@ -84,6 +84,7 @@ struct FixedParams {
   uint32_t grs;
   int grec_ca;  // gradient record copies through L1 (.ca): host-mapped gradients
   int tma_ok;   // records and the state record allow 16-byte bulk copies
+  int wide;     // records past 2^32 elements of row offset: 64-bit ring kernel only
   double* stats_out;
   double* partials;
   unsigned int* counter;
@@ -1271,6 +1272,14 @@ __global__ void __launch_bounds__((NPW + NCW) * 32, MINB) step_ring_kernel(const
     return rem <= 0 ? 0 : (rem < R ? rem : R);
   };
   auto stage = [&](int st) { return smem + st * ST::kBytes; };
+  // row offsets into the parameter / gradient arrays: 32-bit unless the
+  // cloud is past rows * stride >= 2^32 (HINT & 32, chosen by the dispatch)
+  auto roff = [](uint32_t row, uint32_t stride) {
+    if constexpr ((HINT & 32) != 0)
+      return (size_t)row * stride;
+    else
+      return row * stride;
+  };
   // staged theta / grad: row-major for records, group-major for per-attribute gathers
   auto sidx = [](int gg, int i, int r) -> int {
     return REC ? r * PL + L::OFF(gg) + (i - r * L::W(gg)) : R * L::OFF(gg) + i;
@@ -1339,7 +1348,7 @@ __global__ void __launch_bounds__((NPW + NCW) * 32, MINB) step_ring_kernel(const
             const uint32_t row = id_of(r);
             if (r < nv) {
               const int q = p - r * kRowPieces;
-              cp_async16_h<HINT>(sth + r * PL + 4 * q, P.prec + row * P.prs + 4 * q);
+              cp_async16_h<HINT>(sth + r * PL + 4 * q, P.prec + roff(row, P.prs) + 4 * q);
             }
           }
 #pragma unroll
@@ -1350,9 +1359,9 @@ __global__ void __launch_bounds__((NPW + NCW) * 32, MINB) step_ring_kernel(const
             if (r < nv) {
               const int q = p - r * kRowPieces;
               if (P.grec_ca)
-                cp_async16_ca(sg + r * PL + 4 * q, P.grec + row * P.grs + 4 * q);
+                cp_async16_ca(sg + r * PL + 4 * q, P.grec + roff(row, P.grs) + 4 * q);
               else
-                cp_async16_h<HINT>(sg + r * PL + 4 * q, P.grec + row * P.grs + 4 * q);
+                cp_async16_h<HINT>(sg + r * PL + 4 * q, P.grec + roff(row, P.grs) + 4 * q);
             }
           }
         } else {
@@ -1396,13 +1405,13 @@ __global__ void __launch_bounds__((NPW + NCW) * 32, MINB) step_ring_kernel(const
             cp_async16_h<HINT>(srec + r * (2 * SLOTS) + 4 * p, P.record + (size_t)row * P.stride + 4 * p);
           } else if (p < kRecPieces + kRowPieces) {
             const int q = p - kRecPieces;
-            cp_async16_h<HINT>(sth + r * PL + 4 * q, P.prec + row * P.prs + 4 * q);
+            cp_async16_h<HINT>(sth + r * PL + 4 * q, P.prec + roff(row, P.prs) + 4 * q);
           } else if (p < kPiecesPerRow) {
             const int q = p - kRecPieces - kRowPieces;
             if (P.grec_ca)
-              cp_async16_ca(sg + r * PL + 4 * q, P.grec + row * P.grs + 4 * q);
+              cp_async16_ca(sg + r * PL + 4 * q, P.grec + roff(row, P.grs) + 4 * q);
             else
-              cp_async16_h<HINT>(sg + r * PL + 4 * q, P.grec + row * P.grs + 4 * q);
+              cp_async16_h<HINT>(sg + r * PL + 4 * q, P.grec + roff(row, P.grs) + 4 * q);
           }
         }
       }
@@ -1545,10 +1554,10 @@ __global__ void __launch_bounds__((NPW + NCW) * 32, MINB) step_ring_kernel(const
           c_apost += tnv > P.active_logit;
         }
         if (HINT & 2) {  // streaming (evict-first) stores
-          __stcs(P.g[gg].param + row * P.g[gg].ps + (uint32_t)c, tnv);
+          __stcs(P.g[gg].param + roff(row, P.g[gg].ps) + (uint32_t)c, tnv);
           __stcs(rec_base + (size_t)row * rec_stride2 + L::OFF(gg) + c, make_float2(mn, vn));
         } else {
-          P.g[gg].param[row * P.g[gg].ps + (uint32_t)c] = tnv;
+          P.g[gg].param[roff(row, P.g[gg].ps) + (uint32_t)c] = tnv;
           rec_base[(size_t)row * rec_stride2 + L::OFF(gg) + c] = make_float2(mn, vn);
         }
       };
@@ -1911,6 +1920,10 @@ void launch_fixed(const FixedParams& P, int64_t max_rows, int kind, cudaStream_t
     // (TMA) kernels are kept as variants: for 240 / 480-byte rows the TMA
     // unit's per-operation cost bounds them (~0.86 ms vs 0.67 ms on c3,
     // profiles/r01/ncu_step_tma_c3_record.txt), loads and stores alike.
+    if (P.wide) {  // > 2^32 parameter-record elements: 64-bit row offsets
+      launch_ring<L, MODE, STRICT, 32, 2, 3, 8, 2, true, true, 1 | 32>(P, max_rows, s);
+      return;
+    }
     const int v = (P.D.group >= 0 || !P.tma_ok) ? 0 : fixed_variant();
     if (v == 8) {
       launch_ws<L, MODE, STRICT, 32, 3, 3, 8, 2, true>(P, max_rows, s);

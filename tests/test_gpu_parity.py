@@ -297,14 +297,14 @@ def test_edge_visibility_bit_exact_vs_fp32_order(n, params_layout, mode):
 # --------------------------------------------------------------------------
 # Maximum sizes: the fixed-layout kernels use 32-bit row offsets up to
 # rows * row stride < 2^32 (60M granule-aligned rows); beyond that
-# (70M rows) the dispatch falls back to the generic 64-bit row kernel
+# (70M rows) records run the ring kernel with 64-bit row offsets
 # --------------------------------------------------------------------------
 
 @pytest.mark.parametrize("n", [60_000_000, 70_000_000])
 def test_max_size_clouds_sampled_rows_vs_fp32_order(n):
-    """A 60M-row cloud (the fixed-layout kernel right below its 32-bit offset
-    limit) and a 70M-row cloud (past it: the generic kernel) in granule-aligned
-    records (~72 GB in HBM).  Two steps; 4096 sampled visible rows, including
+    """A 60M-row cloud (the ring kernel right below its 32-bit offset limit)
+    and a 70M-row cloud (past it: the 64-bit-offset ring kernel) in
+    granule-aligned records (~72 GB in HBM).  Two steps; 4096 sampled visible rows, including
     the last rows of the cloud, are bit-exact with the fp32 restatement and a
     sample of invisible rows is untouched."""
     from paper_2601_16736_b200 import records as R
