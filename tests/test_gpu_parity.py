@@ -229,6 +229,48 @@ def test_c1_100_steps_vs_oracles(family, layout, params_layout):
         assert normwise(got_v, v64[gname]) <= NORM_TOL, gname
 
 
+def test_adopted_parameters_backward_into_records_bit_exact():
+    """records.adopt: per-attribute nn.Parameters re-homed into a record, their
+    gradients filled by a real backward (loss = sum(theta * G), so dL/dtheta = G
+    exactly) and read from p.grad by step(); 6 steps bit-exact vs the fp32
+    order, and the kernel sees one row stride (64 floats) for every group."""
+    from paper_2601_16736_b200 import records as R
+    from paper_2601_16736_b200 import synthetic as S
+    from paper_2601_16736_b200.optimizer import AdamWGS
+    n, steps = 20_011, 6
+    cfg = S.WorkloadConfig(n=n, p_vis=0.3, seed=5)
+    host = S.make_params(cfg)
+    params = {k: torch.nn.Parameter(torch.from_numpy(v).to(DEV)) for k, v in host.items()}
+    rec, grec = R.adopt(params)
+    assert all(p.stride(0) == 64 and p.grad.stride(0) == 64 for p in params.values())
+    opt = AdamWGS(S.param_groups(params, cfg), mode="adamw-gs", lambda_o=cfg.lambda_o,
+                  lambda_s=cfg.lambda_s)
+    lay = O.LAYOUT_SH3
+    hp = O.Hyper(lr=S.LR_SH3, lambda_o=cfg.lambda_o, lambda_s=cfg.lambda_s)
+    p32 = {k: v.copy() for k, v in host.items()}
+    m32 = {g.name: np.zeros((n, g.width), np.float32) for g in lay}
+    v32 = {g.name: np.zeros((n, g.width), np.float32) for g in lay}
+    c32 = np.zeros(n, np.int32)
+    for s in range(steps):
+        vis = S.visibility(cfg, s)
+        g = S.step_grads(cfg, s, vis)
+        opt.zero_grad(set_to_none=False)
+        loss = sum((p * torch.from_numpy(g[k]).to(DEV).view(p.shape)).sum()
+                   for k, p in params.items())
+        loss.backward()
+        assert torch.equal(R.views_like(grec, params)["f_rest"].cpu(),
+                           torch.from_numpy(g["f_rest"]).view(n, 45))
+        opt.step(torch.from_numpy(vis).to(DEV), cfg.n_pixels)
+        O.step_fp32("adamw-gs", lay, p32, g, m32, v32, c32, np.flatnonzero(vis), hp,
+                    n_pixels=cfg.n_pixels)
+    assert np.array_equal(opt.state.clock.contiguous().cpu().numpy(), c32)
+    for k, p in params.items():
+        assert p.data_ptr() == R.views_like(rec, params)[k].data_ptr()
+        assert_close_ulp(p.detach().cpu().numpy(), p32[k], f"{k}/param")
+        assert_close_ulp(opt.state.m[k].contiguous().cpu().numpy(), m32[k], f"{k}/m")
+        assert_close_ulp(opt.state.v[k].contiguous().cpu().numpy(), v32[k], f"{k}/v")
+
+
 # --------------------------------------------------------------------------
 # Edge cases: empty, single-row and ragged visibility (chunk tails of the
 # ring kernel, zero-length launches), every step mode, both layouts

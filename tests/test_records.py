@@ -41,6 +41,35 @@ def test_autograd_fills_record_grad_and_base_grad_view():
     assert R.base_grad_view(torch.zeros(7, 3)) is None
 
 
+def test_adopt_rehomes_parameters_and_autograd_fills_the_record():
+    a = _attrs()
+    params = {k: torch.nn.Parameter(t.clone()) for k, t in a.items()}
+    ids = {k: id(p) for k, p in params.items()}
+    params["opacity"].grad = torch.full((7, 1), 0.5)   # an existing gradient is kept
+    rec, grec = R.adopt(params)
+    assert rec.shape == (7, 64) and grec.shape == (7, 64)
+    base, gbase = rec.data_ptr(), grec.data_ptr()
+    for k, p in params.items():
+        assert id(p) == ids[k] and p.is_leaf and p.requires_grad
+        assert torch.equal(p.detach(), a[k]) and p.stride(0) == 64
+        assert base <= p.data_ptr() < base + rec.numel() * 4
+        assert p.grad.stride(0) == 64 and gbase <= p.grad.data_ptr() < gbase + grec.numel() * 4
+    assert torch.all(grec[:, 51] == 0.5)
+    loss = (params["xyz"] ** 2).sum() + 3.0 * params["f_rest"].sum() + params["opacity"].sum()
+    loss.backward()
+    g = R.views_like(grec, params)
+    assert params["xyz"].grad.data_ptr() == g["xyz"].data_ptr()   # accumulated in place
+    assert torch.equal(g["xyz"], 2 * a["xyz"])
+    assert torch.equal(g["f_rest"], torch.full((7, 15, 3), 3.0))
+    assert torch.equal(g["opacity"], torch.full((7, 1), 1.5))
+    assert torch.equal(g["rotation"], torch.zeros(7, 4))
+    with torch.no_grad():                                        # in-place updates land in the record
+        params["scaling"].add_(1.0)
+    assert torch.equal(R.views_like(rec, params)["scaling"], a["scaling"] + 1.0)
+    with pytest.raises(ConfigError):
+        R.adopt({"x": params["xyz"] * 2})
+
+
 def test_views_like_matches_offsets():
     a = _attrs()
     _, v = R.pack(a)
