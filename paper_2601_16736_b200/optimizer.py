@@ -656,10 +656,19 @@ class AdamWGS:
         return self.state
 
     def zero_grad(self, set_to_none: bool = True):
+        """Gradients that are views of a gradient record (``records.adopt``)
+        are zeroed in place even with ``set_to_none``: dropping them would
+        detach the parameters from the record layout."""
+        bases = set()
         for g in self.param_groups:
             p = g["params"][0]
             if p.grad is not None:
-                if set_to_none:
+                base = p.grad._base
+                if base is not None and p.grad.dim() >= 1 and p.grad.stride(0) > math.prod(p.shape[1:]):
+                    if id(base) not in bases:
+                        bases.add(id(base))
+                        base.zero_()
+                elif set_to_none:
                     p.grad = None
                 else:
                     p.grad.zero_()

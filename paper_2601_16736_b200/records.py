@@ -104,10 +104,12 @@ def adopt(params: dict[str, torch.Tensor], align: int = 16,
     becomes the attribute view of a new record. With ``grads`` each ``.grad``
     becomes the same view of a zeroed gradient record (an existing gradient
     is copied in); autograd accumulates into a defined ``.grad`` in place, so
-    backward keeps filling the record. Clear it with
-    ``zero_grad(set_to_none=False)`` (or ``grad_record.zero_()``): setting
-    gradients to None detaches them from the record, and the step then
-    falls back to per-attribute gathers. Returns ``(record, grad_record)``.
+    backward keeps filling the record (PyTorch warns once that such a strided
+    ``.grad`` breaks its layout contract; the layout is intended). Clear it
+    with ``AdamWGS.zero_grad()``, which zeroes record views in place, or
+    ``grad_record.zero_()``: setting gradients to None detaches them from the
+    record, and the step then falls back to per-attribute gathers. Returns
+    ``(record, grad_record)``.
 
     This is the one-line switch from the reference's per-attribute arrays
     (``src/primitives.py:95-112``, ``src/gradients.py:18-47``) to the record

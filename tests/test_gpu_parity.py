@@ -254,7 +254,8 @@ def test_adopted_parameters_backward_into_records_bit_exact():
     for s in range(steps):
         vis = S.visibility(cfg, s)
         g = S.step_grads(cfg, s, vis)
-        opt.zero_grad(set_to_none=False)
+        opt.zero_grad()   # record-view gradients are zeroed in place, not dropped
+        assert all(p.grad is not None for p in params.values())
         loss = sum((p * torch.from_numpy(g[k]).to(DEV).view(p.shape)).sum()
                    for k, p in params.items())
         loss.backward()
