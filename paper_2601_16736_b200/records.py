@@ -46,6 +46,14 @@ def _width(t: torch.Tensor) -> int:
     return w
 
 
+def _tail_strides(tail: tuple) -> tuple:
+    out, acc = [], 1
+    for d in reversed(tail):
+        out.append(acc)
+        acc *= int(d)
+    return tuple(reversed(out))
+
+
 def views(record: torch.Tensor, shapes: dict[str, tuple]) -> dict[str, torch.Tensor]:
     """Per-attribute views of a ``(n, PL)`` record. ``shapes`` gives each
     attribute's per-row shape; attributes are packed in dict order."""
@@ -141,6 +149,40 @@ def views_like(record: torch.Tensor, like: dict[str, torch.Tensor]) -> dict[str,
     with the attribute shapes of ``like`` (e.g. the views :func:`pack`
     returned)."""
     return views(record, {k: tuple(v.shape[1:]) for k, v in like.items()})
+
+
+def record_of(tensors: dict[str, torch.Tensor]) -> torch.Tensor | None:
+    """The ``(n, row_width)`` record the attribute tensors are views of, or
+    None: views from :func:`pack` (a common ``_base``) and parameters
+    re-homed by :func:`adopt` (one storage, one row stride). The attributes
+    must sit at the offsets :func:`views` gives them in dict order, so that
+    :func:`views_like` of a gathered record maps back to the same names."""
+    ts = list(tensors.values())
+    if not ts or any(t.dim() < 1 or t.dtype != torch.float32 for t in ts):
+        return None
+    first = ts[0]
+    n, rs = int(first.shape[0]), first.stride(0)
+    base = first._base
+    if base is not None and all(t._base is base for t in ts):
+        if base.dim() != 2 or not base.is_contiguous() or base.shape[0] != n:
+            return None
+    else:
+        st = first.untyped_storage()
+        if any(t.untyped_storage().data_ptr() != st.data_ptr() or t.stride(0) != rs or
+               int(t.shape[0]) != n for t in ts):
+            return None
+        off0 = first.storage_offset()
+        if (off0 + n * rs) * first.element_size() > st.nbytes():
+            return None
+        base = torch.empty(0, dtype=first.dtype, device=first.device).set_(st, off0, (n, rs),
+                                                                           (rs, 1))
+    off = 0
+    for t in ts:
+        if t.stride(0) != rs or t.storage_offset() - base.storage_offset() != off or \
+                t.stride()[1:] != _tail_strides(tuple(t.shape[1:])):
+            return None
+        off += _width(t)
+    return base if off <= base.shape[1] else None
 
 
 def base_grad_view(p: torch.Tensor) -> torch.Tensor | None:

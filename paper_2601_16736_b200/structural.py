@@ -144,7 +144,7 @@ def densify_adc(opt, accum, count, cfg: DensifyConfig, rng: np.random.Generator,
     import torch
 
     from . import _lib as L
-    from .records import views_like
+    from .records import record_of, views_like
 
     roles = {g["role"]: g for g in opt.param_groups}
     need = (L.ROLE_POSITION, L.ROLE_SCALE, L.ROLE_OPACITY)
@@ -226,11 +226,9 @@ def densify_adc(opt, accum, count, cfg: DensifyConfig, rng: np.random.Generator,
     dev = opt.device
     idx = torch.from_numpy(final_src).to(dev)
     old = {g["name"]: g["params"][0] for g in opt.param_groups}
-    bases = {id(t._base) for t in old.values() if t._base is not None}
-    first_base = next(iter(old.values()))._base
-    if len(bases) == 1 and all(t._base is first_base for t in old.values()) and \
-            first_base.dim() == 2:
-        new_params = views_like(first_base.detach().index_select(0, idx), old)
+    rec = record_of(old)   # packed or adopted parameter record
+    if rec is not None:
+        new_params = views_like(rec.detach().index_select(0, idx), old)
     else:
         new_params = {k: t.detach().index_select(0, idx).contiguous() for k, t in old.items()}
     with torch.no_grad():

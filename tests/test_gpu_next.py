@@ -243,7 +243,7 @@ def test_mcmc_relocate_matches_reference_golden(state_layout, params_layout):
 
 
 @pytest.mark.parametrize("state_layout", ["rows", "groups"])
-@pytest.mark.parametrize("params_layout", ["attr", "record"])
+@pytest.mark.parametrize("params_layout", ["attr", "record", "adopt"])
 def test_densify_adc_matches_reference_golden(state_layout, params_layout):
     """structural.densify_adc (pipeline.py:116-185) against the reference run:
     clone / split (same rng draws) / prune decisions and events identical,
@@ -261,6 +261,9 @@ def test_densify_adc_matches_reference_golden(state_layout, params_layout):
     params = {g.name: torch.from_numpy(z[f"init_{g.name}"]).to(DEV) for g in lay}
     if params_layout == "record":
         _, params = R.pack(params)
+    elif params_layout == "adopt":
+        params = {k: torch.nn.Parameter(t) for k, t in params.items()}
+        R.adopt(params, grads=False)
     opt = AdamWGS([{"params": [params[g.name]], "lr": 1e-3, "name": g.name} for g in lay],
                   mode="adamw-gs", state_layout=state_layout)
     for g in lay:
@@ -274,6 +277,8 @@ def test_densify_adc_matches_reference_golden(state_layout, params_layout):
         meta["events"]
     assert opt.n_rows == meta["n_out"] and len(opt.state) == meta["n_out"]
     assert np.array_equal(res.src, z["out_src"]) and np.array_equal(res.alive, z["out_alive"])
+    # packed and adopted parameters come back as views of one gathered record
+    assert (R.record_of(res.params) is not None) == (params_layout != "attr")
     for g in lay:
         got = opt.param_groups[[x["name"] for x in opt.param_groups].index(g.name)]["params"][0]
         assert got is res.params[g.name]

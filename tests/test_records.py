@@ -90,3 +90,19 @@ def test_row_stride_rules():
         row_stride("n", torch.zeros(4, 3), 5, 3)               # wrong row count
     with pytest.raises(ConfigError):
         R.pack({"a": torch.zeros(3, 2), "b": torch.zeros(4, 2)})
+
+
+def test_record_of_packed_adopted_and_plain():
+    a = _attrs()
+    rec, v = R.pack(a)
+    assert R.record_of(v) is rec
+    params = {k: torch.nn.Parameter(t.clone()) for k, t in a.items()}
+    arec, _ = R.adopt(params, grads=False)
+    got = R.record_of(params)
+    assert got is not None and got.shape == arec.shape and got.data_ptr() == arec.data_ptr()
+    assert torch.equal(got, arec)
+    sel = R.views_like(got.detach().index_select(0, torch.tensor([4, 0])), params)
+    assert torch.equal(sel["f_rest"], a["f_rest"][[4, 0]])
+    assert R.record_of(a) is None                                  # separate tensors
+    assert R.record_of(dict(reversed(list(v.items())))) is None    # offsets out of dict order
+    assert R.record_of({"xyz": v["xyz"], "opacity": v["opacity"]}) is None   # a gap
