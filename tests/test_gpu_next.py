@@ -206,7 +206,7 @@ def test_structural_select_concat_keep_rows_consistent():
 
 
 @pytest.mark.parametrize("state_layout", ["rows", "groups"])
-@pytest.mark.parametrize("params_layout", ["attr", "record"])
+@pytest.mark.parametrize("params_layout", ["attr", "record", "adopt"])
 def test_mcmc_relocate_matches_reference_golden(state_layout, params_layout):
     """AdamWGS.mcmc_relocate (pipeline.py:197-233) against the reference run:
     relocated attributes bit-exact, shared opacity = fp32 of the reference's
@@ -222,6 +222,9 @@ def test_mcmc_relocate_matches_reference_golden(state_layout, params_layout):
     params = {g.name: torch.from_numpy(z[f"init_{g.name}"]).to(DEV) for g in lay}
     if params_layout == "record":
         _, params = R.pack(params)
+    elif params_layout == "adopt":
+        params = {k: torch.nn.Parameter(t) for k, t in params.items()}
+        R.adopt(params, grads=False)
     opt = AdamWGS([{"params": [params[g.name]], "lr": 1e-3, "name": g.name} for g in lay],
                   mode="adamw-gs", state_layout=state_layout)
     for g in lay:
@@ -233,7 +236,7 @@ def test_mcmc_relocate_matches_reference_golden(state_layout, params_layout):
     torch.cuda.synchronize()
     assert plan.count == meta["event_count"] and plan.ids_hash() == meta["event_hash"]
     for g in lay:
-        got = params[g.name].cpu().numpy()
+        got = params[g.name].detach().cpu().numpy()
         assert np.array_equal(got, z[f"out_{g.name}"].astype(np.float32)), g.name
         assert np.array_equal(opt.state.m[g.name].cpu().numpy(),
                               z[f"out_m_{g.name}"].astype(np.float32)), g.name
