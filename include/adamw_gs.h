@@ -38,8 +38,12 @@
 extern "C" {
 #endif
 
-#define GS_ABI_VERSION 2
+#define GS_ABI_VERSION 3
 #define GS_MAX_GROUPS 8
+
+/* gs_build_flags() bits */
+#define GS_BUILD_FLAG_VARIANTS 1 /* measured K2 alternatives compiled in (-DGS_BUILD_VARIANTS=1) */
+#define GS_BUILD_FLAG_TMA4 2     /* the 2-D TMA (tile::gather4 / scatter4) record kernel */
 
 /* status codes */
 #define GS_OK 0
@@ -179,9 +183,11 @@ int gs_check_grads(const gs_group* groups, int32_t n_groups, int64_t n_rows,
 /* K3 — re-state regularisation m *= alpha1, v *= alpha2 on the k rows
  * (clock untouched), and relocation resets m = v = 0, clock = 0. */
 int gs_rsr_apply(const gs_group* groups, int32_t n_groups, const int32_t* rows, int64_t k,
-                 double alpha1, double alpha2, void* stream);
+                 int64_t n_rows, double alpha1, double alpha2, void* stream);
 int gs_reset_rows(const gs_group* groups, int32_t n_groups, int32_t* clock,
-                  const int32_t* rows, int64_t k, void* stream);
+                  const int32_t* rows, int64_t k, int64_t n_rows, void* stream);
+/* (K3 entry points skip row ids outside [0, n_rows); the host validates and
+ * de-duplicates index lists before they reach the device.) */
 
 /* K4 — all-row statistics.  out (device doubles, 2 + 5*n_groups):
  *   [0] n_alive, [1] n_active (opacity group tau > active_logit, alive rows),
@@ -252,10 +258,23 @@ int gs_step_rows(const gs_group* groups, int32_t n_groups, const gs_step_cfg* cf
                  float* record, int64_t record_stride, double* stats_out, void* ws,
                  size_t ws_bytes, void* stream);
 int gs_rsr_apply_rows(float* record, int64_t record_stride, int32_t n_elems,
-                      const int32_t* rows, int64_t k, double alpha1, double alpha2,
-                      void* stream);
+                      const int32_t* rows, int64_t k, int64_t n_rows, double alpha1,
+                      double alpha2, void* stream);
 int gs_reset_rows_rows(float* record, int64_t record_stride, int32_t n_elems,
-                       const int32_t* rows, int64_t k, void* stream);
+                       const int32_t* rows, int64_t k, int64_t n_rows, void* stream);
+
+/* Densification statistics of the listed rows (DensifyStats.observe,
+ * pipeline.py:77-82): for i < *n_list_dev (<= max_rows), row r = rows[i]:
+ * accum[r] += ||grad[r, 0:width]||_2 * scale, count[r] += 1 (fp32, the
+ * fused kernels' order).  Used with the dense coupled-adam step, which
+ * updates every row but observes only the visible ones.  abort_flag
+ * (nullable): a strict pre-check's flag; non-zero makes the call a no-op. */
+int gs_densify_rows(const float* grad, int64_t grad_stride, int32_t width, const int32_t* rows,
+                    const int32_t* n_list_dev, int64_t max_rows, float* accum, int32_t* count,
+                    float scale, const int32_t* abort_flag, void* stream);
+
+/* GS_BUILD_FLAG_* bits of this build. */
+int32_t gs_build_flags(void);
 int gs_stats_all_rows(const gs_group* groups, int32_t n_groups, int64_t n_rows,
                       const float* record, int64_t record_stride, const uint8_t* alive,
                       float active_logit, double* out, void* ws, size_t ws_bytes,

@@ -13,7 +13,7 @@ from pathlib import Path
 
 LIB_PATH = Path(__file__).resolve().parent / "libadamw_gs_b200.so"
 
-GS_ABI_VERSION = 2
+GS_ABI_VERSION = 3
 GS_MAX_GROUPS = 8
 
 GS_OK = 0
@@ -71,10 +71,10 @@ SIGNATURES = {
     "gs_check_grads": (C.c_int, [C.POINTER(GsGroup), C.c_int32, C.c_int64, C.c_void_p,
                                  C.c_void_p, C.c_double, C.c_double, C.c_void_p, C.c_void_p,
                                  C.c_void_p]),
-    "gs_rsr_apply": (C.c_int, [C.POINTER(GsGroup), C.c_int32, C.c_void_p, C.c_int64, C.c_double,
-                               C.c_double, C.c_void_p]),
+    "gs_rsr_apply": (C.c_int, [C.POINTER(GsGroup), C.c_int32, C.c_void_p, C.c_int64, C.c_int64,
+                               C.c_double, C.c_double, C.c_void_p]),
     "gs_reset_rows": (C.c_int, [C.POINTER(GsGroup), C.c_int32, C.c_void_p, C.c_void_p,
-                                C.c_int64, C.c_void_p]),
+                                C.c_int64, C.c_int64, C.c_void_p]),
     "gs_stats_workspace_bytes": (C.c_size_t, [C.c_int32]),
     "gs_compact_select_u8": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int64, C.c_void_p,
                                        C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
@@ -95,9 +95,13 @@ SIGNATURES = {
                                C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p,
                                C.c_void_p, C.c_size_t, C.c_void_p]),
     "gs_rsr_apply_rows": (C.c_int, [C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_int64,
-                                    C.c_double, C.c_double, C.c_void_p]),
+                                    C.c_int64, C.c_double, C.c_double, C.c_void_p]),
     "gs_reset_rows_rows": (C.c_int, [C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_int64,
-                                     C.c_void_p]),
+                                     C.c_int64, C.c_void_p]),
+    "gs_densify_rows": (C.c_int, [C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p,
+                                  C.c_int64, C.c_void_p, C.c_void_p, C.c_float, C.c_void_p,
+                                  C.c_void_p]),
+    "gs_build_flags": (C.c_int32, []),
     "gs_stats_all_rows": (C.c_int, [C.POINTER(GsGroup), C.c_int32, C.c_int64, C.c_void_p,
                                     C.c_int64, C.c_void_p, C.c_float, C.c_void_p, C.c_void_p,
                                     C.c_size_t, C.c_void_p]),

@@ -39,6 +39,13 @@ extern "C" int32_t gs_abi_version(void) { return GS_ABI_VERSION; }
 extern "C" const char* gs_last_error(void) { return g_err; }
 extern "C" int32_t gs_device_sm_count(void) { return gs_sm_count(); }
 
+#ifndef GS_BUILD_VARIANTS
+#define GS_BUILD_VARIANTS 0
+#endif
+extern "C" int32_t gs_build_flags(void) {
+  return (GS_BUILD_VARIANTS ? GS_BUILD_FLAG_VARIANTS : 0) | GS_BUILD_FLAG_TMA4;
+}
+
 extern "C" int gs_host_device_pointer(const void* host_ptr, void** dev_ptr) {
   if (!host_ptr || !dev_ptr) {
     gs_set_error("gs_host_device_pointer: null pointer");

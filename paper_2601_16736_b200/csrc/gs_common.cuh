@@ -10,6 +10,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <atomic>
 
 #include "../../include/adamw_gs.h"
 
@@ -287,3 +288,26 @@ __device__ __forceinline__ void final_reduce_n(const double* partials, int nbloc
 void gs_set_error(const char* fmt, ...);
 int gs_check_launch(const char* what);
 int gs_sm_count();
+
+namespace gs {
+// Opt KERNEL into `bytes` of dynamic shared memory on the current device.
+// cudaFuncSetAttribute is per device, so the opt-in is cached per kernel in
+// a bitmask of devices (thread-safe); a failure is reported and retried on
+// the next launch (which then fails with the CUDA error).
+template <auto KERNEL>
+inline void smem_opt_in(int bytes) {
+  static std::atomic<uint64_t> done{0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return;
+  const uint64_t bit = dev < 64 ? (uint64_t{1} << dev) : 0;
+  if (bit != 0 && (done.load(std::memory_order_acquire) & bit)) return;
+  const cudaError_t e =
+      cudaFuncSetAttribute(KERNEL, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e != cudaSuccess) {
+    gs_set_error("cudaFuncSetAttribute(%d bytes of shared memory): %s", bytes,
+                 cudaGetErrorString(e));
+    return;
+  }
+  done.fetch_or(bit, std::memory_order_acq_rel);
+}
+}  // namespace gs

@@ -186,7 +186,7 @@ __global__ void __launch_bounds__(kThreads)
 template <bool RESET>
 __global__ void __launch_bounds__(kThreads)
     scatter_state_kernel(const GroupSet S, const int32_t* __restrict__ rows, int64_t k,
-                         double a1, double a2, int32_t* __restrict__ clock) {
+                         int64_t n_rows, double a1, double a2, int32_t* __restrict__ clock) {
   __shared__ int32_t s_row[kThreads];
   const int tid = threadIdx.x;
   const int64_t n_chunks = (k + kThreads - 1) / kThreads;
@@ -195,8 +195,9 @@ __global__ void __launch_bounds__(kThreads)
     const int nvalid = (int)(k - base < kThreads ? k - base : kThreads);
     if (tid < nvalid) {
       const int32_t r = __ldg(rows + base + tid);
-      s_row[tid] = r;
-      if (RESET && clock) clock[r] = 0;
+      const bool ok = r >= 0 && (int64_t)r < n_rows;  // ids outside the rows are skipped
+      s_row[tid] = ok ? r : -1;
+      if (RESET && clock && ok) clock[r] = 0;
     }
     __syncthreads();
     for (int gi = 0; gi < S.n; ++gi) {
@@ -207,7 +208,8 @@ __global__ void __launch_bounds__(kThreads)
       int lr = tid / W, lc = tid % W;
       for (int e = tid; e < E; e += kThreads) {
         const int64_t off = (int64_t)s_row[lr] * W + lc;
-        if (RESET) {
+        if (s_row[lr] < 0) {
+        } else if (RESET) {
           G.m[off] = 0.0f;
           G.v[off] = 0.0f;
         } else {
@@ -297,23 +299,71 @@ int stats_blocks() { return gs_sm_count() * 2; }
 // row-record state (see gs_step_rows.cu): slot s < P holds (m, v), slot P the
 // int32 clock.  A warp owns a row; lanes stride over its slots.
 // ---------------------------------------------------------------------------
-template <bool RESET>
+template <bool RESET, bool VEC4>
 __global__ void __launch_bounds__(kThreads)
     scatter_rows_kernel(float* __restrict__ record, int64_t stride, int P,
-                        const int32_t* __restrict__ rows, int64_t k, double a1, double a2) {
+                        const int32_t* __restrict__ rows, int64_t k, int64_t n_rows, double a1,
+                        double a2) {
+  // VEC4: a lane moves one 16-byte piece (two slots) of the row, so a row
+  // is one warp-wide access of 8(P+1) bytes; two rows per warp iteration
+  // keep two rows' loads in flight.  Ids outside [0, n_rows) are skipped.
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (kThreads / 32);
-  for (int64_t i = (int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5); i < k; i += warps) {
-    float* rec = record + (int64_t)__ldg(rows + i) * stride;
-    for (int s = lane; s <= P; s += 32) {
-      float2* p = reinterpret_cast<float2*>(rec + 2 * s);
-      if (RESET) {
-        if (s < P) *p = make_float2(0.f, 0.f);
-        else reinterpret_cast<int*>(rec)[2 * s] = 0;  // clock = 0, pad kept
-      } else if (s < P) {
-        const float2 x = *p;
-        *p = make_float2(__double2float_rn(__dmul_rn((double)x.x, a1)),
-                         __double2float_rn(__dmul_rn((double)x.y, a2)));
+  auto one = [&](float* rec, int s) {  // float2 slot s
+    float2* p = reinterpret_cast<float2*>(rec + 2 * s);
+    if (RESET) {
+      if (s < P) *p = make_float2(0.f, 0.f);
+      else if (s == P) reinterpret_cast<int*>(rec)[2 * s] = 0;  // clock = 0, pad kept
+    } else if (s < P) {
+      const float2 x = *p;  // m *= alpha1 in float64, rounded once (optimizer.py:338-339)
+      *p = make_float2(__double2float_rn(__dmul_rn((double)x.x, a1)),
+                       __double2float_rn(__dmul_rn((double)x.y, a2)));
+    }
+  };
+  for (int64_t i = ((int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5)) * 2; i < k;
+       i += 2 * warps) {
+    const int64_t r0 = __ldg(rows + i);
+    const int64_t r1 = i + 1 < k ? (int64_t)__ldg(rows + i + 1) : -1;
+    const bool ok0 = r0 >= 0 && r0 < n_rows, ok1 = r1 >= 0 && r1 < n_rows;
+    float* rec0 = record + (ok0 ? r0 : 0) * stride;
+    float* rec1 = record + (ok1 ? r1 : 0) * stride;
+    if (VEC4) {
+      const int nq = (P + 1) / 2;  // 16-byte pieces of a row (P + 1 even)
+      if (lane < nq) {
+        float4* q0 = reinterpret_cast<float4*>(rec0) + lane;
+        float4* q1 = reinterpret_cast<float4*>(rec1) + lane;
+        const int s = 2 * lane;  // first slot of the piece
+        if (RESET) {
+          const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (s + 1 < P) {
+            if (ok0) *q0 = z;
+            if (ok1) *q1 = z;
+          } else {
+            if (ok0) { one(rec0, s); one(rec0, s + 1); }
+            if (ok1) { one(rec1, s); one(rec1, s + 1); }
+          }
+        } else {
+          float4 x0 = make_float4(0.f, 0.f, 0.f, 0.f), x1 = x0;
+          if (ok0) x0 = *q0;
+          if (ok1) x1 = *q1;
+          auto sc = [&](float4 x) {
+            float4 y = x;
+            y.x = __double2float_rn(__dmul_rn((double)x.x, a1));
+            y.y = __double2float_rn(__dmul_rn((double)x.y, a2));
+            if (s + 1 < P) {
+              y.z = __double2float_rn(__dmul_rn((double)x.z, a1));
+              y.w = __double2float_rn(__dmul_rn((double)x.w, a2));
+            }
+            return y;  // slot P (clock, pad) is written back unchanged
+          };
+          if (ok0) *q0 = sc(x0);
+          if (ok1) *q1 = sc(x1);
+        }
+      }
+    } else {
+      for (int s = lane; s <= P; s += 32) {
+        if (ok0) one(rec0, s);
+        if (ok1) one(rec1, s);
       }
     }
   }
@@ -417,6 +467,21 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
+// Densification statistics of the listed rows (DensifyStats.observe,
+// pipeline.py:77-82) for the dense coupled-adam step, which updates every row
+// but observes only the visible ones: thread per listed row.
+__global__ void __launch_bounds__(kThreads)
+    densify_rows_kernel(const float* __restrict__ grad, int64_t grad_stride, int width,
+                        const int32_t* __restrict__ rows, const int32_t* __restrict__ n_list,
+                        DensifyArgs D, const int32_t* __restrict__ abort_flag) {
+  const int64_t n = (abort_flag && *abort_flag) ? 0 : *n_list;
+  for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * kThreads) {
+    const int32_t r = __ldg(rows + i);
+    densify_row(D, (uint32_t)r, grad + (int64_t)r * grad_stride, width, 1);
+  }
+}
+
 static int record_args(const float* record, int64_t stride, int P, const char* who) {
   if (!record || P < 1 || stride < 2 * (P + 1) || (stride & 1) ||
       (reinterpret_cast<uintptr_t>(record) & 7u)) {
@@ -428,9 +493,13 @@ static int record_args(const float* record, int64_t stride, int P, const char* w
 
 }  // namespace gs
 
+static bool rows_vec4(const float* record, int64_t stride, int P) {
+  return (P + 1) % 2 == 0 && stride % 4 == 0 && (reinterpret_cast<uintptr_t>(record) & 15u) == 0;
+}
+
 extern "C" int gs_rsr_apply_rows(float* record, int64_t record_stride, int32_t n_elems,
-                                 const int32_t* rows, int64_t k, double alpha1, double alpha2,
-                                 void* stream) {
+                                 const int32_t* rows, int64_t k, int64_t n_rows, double alpha1,
+                                 double alpha2, void* stream) {
   using namespace gs;
   int rc = record_args(record, record_stride, n_elems, "gs_rsr_apply_rows");
   if (rc) return rc;
@@ -443,15 +512,19 @@ extern "C" int gs_rsr_apply_rows(float* record, int64_t record_stride, int32_t n
     return GS_ERR_ARG;
   }
   if (k == 0) return GS_OK;
-  const int64_t need = (k + 7) / 8;
-  const int grid = (int)std::min<int64_t>(need, (int64_t)gs_sm_count() * 8);
-  scatter_rows_kernel<false><<<grid, kThreads, 0, (cudaStream_t)stream>>>(
-      record, record_stride, n_elems, rows, k, alpha1, alpha2);
+  const int64_t need = (k + 15) / 16;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)gs_sm_count() * 8));
+  if (rows_vec4(record, record_stride, n_elems))
+    scatter_rows_kernel<false, true><<<grid, kThreads, 0, (cudaStream_t)stream>>>(
+        record, record_stride, n_elems, rows, k, n_rows, alpha1, alpha2);
+  else
+    scatter_rows_kernel<false, false><<<grid, kThreads, 0, (cudaStream_t)stream>>>(
+        record, record_stride, n_elems, rows, k, n_rows, alpha1, alpha2);
   return gs_check_launch("gs_rsr_apply_rows");
 }
 
 extern "C" int gs_reset_rows_rows(float* record, int64_t record_stride, int32_t n_elems,
-                                  const int32_t* rows, int64_t k, void* stream) {
+                                  const int32_t* rows, int64_t k, int64_t n_rows, void* stream) {
   using namespace gs;
   int rc = record_args(record, record_stride, n_elems, "gs_reset_rows_rows");
   if (rc) return rc;
@@ -460,10 +533,14 @@ extern "C" int gs_reset_rows_rows(float* record, int64_t record_stride, int32_t 
     return GS_ERR_ARG;
   }
   if (k == 0) return GS_OK;
-  const int64_t need = (k + 7) / 8;
-  const int grid = (int)std::min<int64_t>(need, (int64_t)gs_sm_count() * 8);
-  scatter_rows_kernel<true><<<grid, kThreads, 0, (cudaStream_t)stream>>>(
-      record, record_stride, n_elems, rows, k, 0.0, 0.0);
+  const int64_t need = (k + 15) / 16;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)gs_sm_count() * 8));
+  if (rows_vec4(record, record_stride, n_elems))
+    scatter_rows_kernel<true, true><<<grid, kThreads, 0, (cudaStream_t)stream>>>(
+        record, record_stride, n_elems, rows, k, n_rows, 0.0, 0.0);
+  else
+    scatter_rows_kernel<true, false><<<grid, kThreads, 0, (cudaStream_t)stream>>>(
+        record, record_stride, n_elems, rows, k, n_rows, 0.0, 0.0);
   return gs_check_launch("gs_reset_rows_rows");
 }
 
@@ -551,7 +628,8 @@ extern "C" int gs_check_grads(const gs_group* groups, int32_t n_groups, int64_t 
 }
 
 extern "C" int gs_rsr_apply(const gs_group* groups, int32_t n_groups, const int32_t* rows,
-                            int64_t k, double alpha1, double alpha2, void* stream) {
+                            int64_t k, int64_t n_rows, double alpha1, double alpha2,
+                            void* stream) {
   using namespace gs;
   GroupSet S{};
   int rc = fill_groups(groups, n_groups, S, "gs_rsr_apply", false);
@@ -567,13 +645,13 @@ extern "C" int gs_rsr_apply(const gs_group* groups, int32_t n_groups, const int3
   if (k == 0) return GS_OK;
   const int64_t chunks = (k + kThreads - 1) / kThreads;
   int grid = (int)std::min<int64_t>(chunks, (int64_t)gs_sm_count() * 8);
-  scatter_state_kernel<false><<<grid, kThreads, 0, (cudaStream_t)stream>>>(S, rows, k, alpha1,
-                                                                           alpha2, nullptr);
+  scatter_state_kernel<false><<<grid, kThreads, 0, (cudaStream_t)stream>>>(S, rows, k, n_rows,
+                                                                           alpha1, alpha2, nullptr);
   return gs_check_launch("gs_rsr_apply");
 }
 
 extern "C" int gs_reset_rows(const gs_group* groups, int32_t n_groups, int32_t* clock,
-                             const int32_t* rows, int64_t k, void* stream) {
+                             const int32_t* rows, int64_t k, int64_t n_rows, void* stream) {
   using namespace gs;
   GroupSet S{};
   int rc = fill_groups(groups, n_groups, S, "gs_reset_rows", false);
@@ -585,8 +663,8 @@ extern "C" int gs_reset_rows(const gs_group* groups, int32_t n_groups, int32_t* 
   if (k == 0) return GS_OK;
   const int64_t chunks = (k + kThreads - 1) / kThreads;
   int grid = (int)std::min<int64_t>(chunks, (int64_t)gs_sm_count() * 8);
-  scatter_state_kernel<true><<<grid, kThreads, 0, (cudaStream_t)stream>>>(S, rows, k, 0.0, 0.0,
-                                                                          clock);
+  scatter_state_kernel<true><<<grid, kThreads, 0, (cudaStream_t)stream>>>(S, rows, k, n_rows, 0.0,
+                                                                          0.0, clock);
   return gs_check_launch("gs_reset_rows");
 }
 
@@ -731,4 +809,22 @@ extern "C" int gs_relocate_rows(const gs_group* groups, int32_t n_groups, int32_
   relocate_rows_kernel<<<grid, kThreads, 0, (cudaStream_t)stream>>>(
       S, opacity_group, dead, targets, tau_new, k, record, record_stride, 2 * (P + 1));
   return gs_check_launch("gs_relocate_rows");
+}
+
+extern "C" int gs_densify_rows(const float* grad, int64_t grad_stride, int32_t width,
+                               const int32_t* rows, const int32_t* n_list_dev, int64_t max_rows,
+                               float* accum, int32_t* count, float scale,
+                               const int32_t* abort_flag, void* stream) {
+  using namespace gs;
+  if (!grad || width < 1 || grad_stride < width || !rows || !n_list_dev || max_rows < 0 ||
+      !accum || !count) {
+    gs_set_error("gs_densify_rows: bad arguments");
+    return GS_ERR_ARG;
+  }
+  if (max_rows == 0) return GS_OK;
+  const int64_t need = (max_rows + kThreads - 1) / kThreads;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)gs_sm_count() * 4));
+  densify_rows_kernel<<<grid, kThreads, 0, (cudaStream_t)stream>>>(
+      grad, grad_stride, width, rows, n_list_dev, DensifyArgs{accum, count, scale, 0}, abort_flag);
+  return gs_check_launch("gs_densify_rows");
 }

@@ -5,26 +5,26 @@
 
 namespace gs {
 
-extern template void launch_fixed<LayoutSH3, GS_MODE_COUPLED_ADAM, false>(const FixedParams&, int64_t, int,
-                                                          cudaStream_t);
-extern template void launch_fixed<LayoutSH3, GS_MODE_COUPLED_ADAM, true>(const FixedParams&, int64_t, int,
-                                                          cudaStream_t);
-extern template void launch_fixed<LayoutSH3, GS_MODE_SPARSE_ADAM, false>(const FixedParams&, int64_t, int,
-                                                          cudaStream_t);
-extern template void launch_fixed<LayoutSH3, GS_MODE_SPARSE_ADAM, true>(const FixedParams&, int64_t, int,
-                                                          cudaStream_t);
-extern template void launch_fixed<LayoutSH3, GS_MODE_ADAMW_CONST, false>(const FixedParams&, int64_t, int,
-                                                          cudaStream_t);
-extern template void launch_fixed<LayoutSH3, GS_MODE_ADAMW_CONST, true>(const FixedParams&, int64_t, int,
-                                                          cudaStream_t);
-extern template void launch_fixed<LayoutSH3, GS_MODE_ADAMW_CONST_CLIP, false>(const FixedParams&, int64_t, int,
-                                                          cudaStream_t);
-extern template void launch_fixed<LayoutSH3, GS_MODE_ADAMW_CONST_CLIP, true>(const FixedParams&, int64_t, int,
-                                                          cudaStream_t);
-extern template void launch_fixed<LayoutSH3, GS_MODE_ADAMW_GS, false>(const FixedParams&, int64_t, int,
-                                                          cudaStream_t);
-extern template void launch_fixed<LayoutSH3, GS_MODE_ADAMW_GS, true>(const FixedParams&, int64_t, int,
-                                                          cudaStream_t);
+extern template void launch_fixed<LayoutSH3, GS_MODE_COUPLED_ADAM, false>(const FixedParams&, const TmaMaps*,
+                                                          int64_t, int, cudaStream_t);
+extern template void launch_fixed<LayoutSH3, GS_MODE_COUPLED_ADAM, true>(const FixedParams&, const TmaMaps*,
+                                                          int64_t, int, cudaStream_t);
+extern template void launch_fixed<LayoutSH3, GS_MODE_SPARSE_ADAM, false>(const FixedParams&, const TmaMaps*,
+                                                          int64_t, int, cudaStream_t);
+extern template void launch_fixed<LayoutSH3, GS_MODE_SPARSE_ADAM, true>(const FixedParams&, const TmaMaps*,
+                                                          int64_t, int, cudaStream_t);
+extern template void launch_fixed<LayoutSH3, GS_MODE_ADAMW_CONST, false>(const FixedParams&, const TmaMaps*,
+                                                          int64_t, int, cudaStream_t);
+extern template void launch_fixed<LayoutSH3, GS_MODE_ADAMW_CONST, true>(const FixedParams&, const TmaMaps*,
+                                                          int64_t, int, cudaStream_t);
+extern template void launch_fixed<LayoutSH3, GS_MODE_ADAMW_CONST_CLIP, false>(const FixedParams&, const TmaMaps*,
+                                                          int64_t, int, cudaStream_t);
+extern template void launch_fixed<LayoutSH3, GS_MODE_ADAMW_CONST_CLIP, true>(const FixedParams&, const TmaMaps*,
+                                                          int64_t, int, cudaStream_t);
+extern template void launch_fixed<LayoutSH3, GS_MODE_ADAMW_GS, false>(const FixedParams&, const TmaMaps*,
+                                                          int64_t, int, cudaStream_t);
+extern template void launch_fixed<LayoutSH3, GS_MODE_ADAMW_GS, true>(const FixedParams&, const TmaMaps*,
+                                                          int64_t, int, cudaStream_t);
 
 static int g_fixed_variant = -1;
 
@@ -40,21 +40,22 @@ int fixed_variant() {
 }
 
 template <class L, bool STRICT>
-void dispatch_fixed(int mode, const FixedParams& P, int64_t max_rows, int kind, cudaStream_t s) {
+void dispatch_fixed(int mode, const FixedParams& P, const TmaMaps* M, int64_t max_rows, int kind,
+                    cudaStream_t s) {
   switch (mode) {
     case GS_MODE_COUPLED_ADAM:
-      launch_fixed<L, GS_MODE_COUPLED_ADAM, STRICT>(P, max_rows, kind, s);
+      launch_fixed<L, GS_MODE_COUPLED_ADAM, STRICT>(P, M, max_rows, kind, s);
       break;
     case GS_MODE_SPARSE_ADAM:
-      launch_fixed<L, GS_MODE_SPARSE_ADAM, STRICT>(P, max_rows, kind, s);
+      launch_fixed<L, GS_MODE_SPARSE_ADAM, STRICT>(P, M, max_rows, kind, s);
       break;
     case GS_MODE_ADAMW_CONST:
-      launch_fixed<L, GS_MODE_ADAMW_CONST, STRICT>(P, max_rows, kind, s);
+      launch_fixed<L, GS_MODE_ADAMW_CONST, STRICT>(P, M, max_rows, kind, s);
       break;
     case GS_MODE_ADAMW_CONST_CLIP:
-      launch_fixed<L, GS_MODE_ADAMW_CONST_CLIP, STRICT>(P, max_rows, kind, s);
+      launch_fixed<L, GS_MODE_ADAMW_CONST_CLIP, STRICT>(P, M, max_rows, kind, s);
       break;
-    default: launch_fixed<L, GS_MODE_ADAMW_GS, STRICT>(P, max_rows, kind, s); break;
+    default: launch_fixed<L, GS_MODE_ADAMW_GS, STRICT>(P, M, max_rows, kind, s); break;
   }
 }
 
@@ -99,6 +100,49 @@ int rows_kind(const gs_group* groups, int64_t max_rows, FixedParams& P) {
   return wide ? -1 : 1;
 }
 
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static std::atomic<EncodeTiledFn> fn{nullptr};
+  EncodeTiledFn f = fn.load(std::memory_order_acquire);
+  if (f == nullptr) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || p == nullptr) {
+      (void)cudaGetLastError();
+      return nullptr;
+    }
+    f = reinterpret_cast<EncodeTiledFn>(p);
+    fn.store(f, std::memory_order_release);
+  }
+  return f;
+}
+
+// 2-D fp32 map [n_rows, stride] with a one-row box of `box` columns (the
+// gather4 / scatter4 operations move four such rows); rows past n_rows are
+// out of bounds (zero-filled on load, dropped on store).
+static bool encode_rows(CUtensorMap* m, const float* base, int64_t n_rows, int64_t stride, int box) {
+  EncodeTiledFn enc = encode_fn();
+  if (enc == nullptr || n_rows < 1 || n_rows > INT32_MAX) return false;
+  const cuuint64_t dim[2] = {(cuuint64_t)stride, (cuuint64_t)n_rows};
+  const cuuint64_t str[1] = {(cuuint64_t)stride * 4};
+  const cuuint32_t boxd[2] = {(cuuint32_t)box, 1};
+  const cuuint32_t es[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dim, str, boxd, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+bool encode_tma_maps(const FixedParams& P, int64_t n_rows, int rec_box, TmaMaps* out) {
+  return encode_rows(&out->rec, P.record, n_rows, P.stride, rec_box) &&
+         encode_rows(&out->prm, P.prec, n_rows, P.prs, Tma4Stage<LayoutSH3, 32>::kPT) &&
+         encode_rows(&out->grd, P.grec, n_rows, P.grs, Tma4Stage<LayoutSH3, 32>::kPT);
+}
+
 template <class L>
 bool layout_matches(const gs_group* groups, int n_groups) {
   if (n_groups != L::G) return false;
@@ -132,6 +176,12 @@ int gs_step_fixed_try(const gs_group* groups, int32_t n_groups, const gs_step_cf
   if (kind < 0) return 0;  // 32-bit element offsets
   P.tma_ok = kind == 2 && P.grec_ca == 0 && record_stride % 4 == 0 &&
              (reinterpret_cast<uintptr_t>(record) & 15u) == 0;
+  // 2-D TMA kernel: device-resident records, 16-byte row strides, whole
+  // 64-float parameter / gradient rows and a state row of >= 2(P+1) floats
+  constexpr int kPT = Tma4Stage<LayoutSH3, 32>::kPT;
+  const bool tma4 = P.tma_ok && P.prs >= kPT && P.grs >= kPT && P.prs % 4 == 0 &&
+                    P.grs % 4 == 0 && record_stride >= 2 * (LayoutSH3::P + 1) &&
+                    max_rows <= INT32_MAX;
   for (int i = 0; i < n_groups; ++i)
     P.g[i] = FixedGroup{
         groups[i].param, groups[i].grad, groups[i].lr,
@@ -156,9 +206,12 @@ int gs_step_fixed_try(const gs_group* groups, int32_t n_groups, const gs_step_cf
   P.partials = partials;
   P.counter = counter;
   cudaStream_t s = (cudaStream_t)stream;
+  TmaMaps maps;
+  const TmaMaps* M = nullptr;
+  if (tma4 && encode_tma_maps(P, max_rows, 2 * (LayoutSH3::P + 1), &maps)) M = &maps;
   if (cfg->check == GS_CHECK_STRICT)
-    dispatch_fixed<LayoutSH3, true>(cfg->mode, P, max_rows, kind, s);
+    dispatch_fixed<LayoutSH3, true>(cfg->mode, P, M, max_rows, kind, s);
   else
-    dispatch_fixed<LayoutSH3, false>(cfg->mode, P, max_rows, kind, s);
+    dispatch_fixed<LayoutSH3, false>(cfg->mode, P, M, max_rows, kind, s);
   return 1;
 }

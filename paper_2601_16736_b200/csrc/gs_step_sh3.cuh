@@ -14,23 +14,24 @@
 // where a penalty is active, is skipped whole.
 //
 // Shipped kernels:
-//   step_ring_kernel<..., REC=1>  default for parameter/gradient records.
+//   step_tma4_kernel (gs_step_sh3_tma.cuh)  default for device-resident
+//       parameter / gradient / moment records: 2-D TMA row gathers and
+//       scatters (tile::gather4 / tile::scatter4), loader / consumer / storer
+//       warps, 2-stage ring, in-place update in shared memory.
+//   step_ring_kernel<..., REC=1>  records the TMA kernel cannot take
+//       (host-mapped gradients, compact 240-byte rows, GS_FIXED_VARIANT=21):
 //       3 producer warps cp.async the chunk's moment records, theta rows and
 //       gradient rows (16-byte pieces, array by array; row ids by shuffle),
-//       plus the row ids and bias factors, into a 3-stage ring (full / empty
+//       plus the row ids and bias factors, into a 2-stage ring (full / empty
 //       mbarriers).  8 consumer warps check, update and store, with one
 //       named barrier per chunk (epoch-tagged row flags).
-//   step_ws_kernel<...>  default for per-attribute theta / gradient tensors.
-//       The same ring with 4-byte element gathers in chunk element order and
-//       three consumer barriers per chunk (cheaper there than per-element
-//       row-id shuffles).
-// Variants, kept because they are measured and tested bit-identical
-// (gs_set_fixed_variant):
-//   step_fixed_kernel (phase-separated), step_pipe / step_pipe2_kernel (the
-//   first cp.async rings), step_ws_kernel<REC=1> (+ BULKST bulk stores),
-//   step_tma_kernel (cp.async.bulk loads / stores: bound by the TMA unit's
-//   per-operation cost on 256/512-byte rows), other step_ring_kernel shapes
-//   (ring depth, warp split, no L2 prefetch-size hint).
+//   step_ws_kernel<...>  per-attribute theta / gradient tensors.  The same
+//       ring with 4-byte element gathers in chunk element order and three
+//       consumer barriers per chunk (cheaper there than per-element row-id
+//       shuffles).
+// Measured alternatives (phase-separated, the first cp.async rings, other
+// ring shapes, 1-D bulk copies) build only with -DGS_BUILD_VARIANTS=1
+// (gs_set_fixed_variant); their results are bit-identical.
 #include <stdlib.h>
 
 #include "gs_common.cuh"
@@ -109,6 +110,7 @@ struct ChunkShape {
 // loop is unrolled, so widths, roles, record offsets and the parameter
 // pointers are compile-time per round, and a round's warp-uniform predicate
 // (k*NT + t < R*W_g) is the only control flow.
+#if GS_BUILD_VARIANTS  // measured alternatives; -DGS_BUILD_VARIANTS=1
 template <class L, int MODE, bool STRICT, int R, int MINB, int NT>
 __global__ void __launch_bounds__(NT, MINB) step_fixed_kernel(const FixedParams P) {
   constexpr bool kDense = MODE == GS_MODE_COUPLED_ADAM;
@@ -276,6 +278,7 @@ __global__ void __launch_bounds__(NT, MINB) step_fixed_kernel(const FixedParams 
   if (last_block_arrive(P.counter))
     final_reduce<GS_STEP_STATS>(P.partials, gridDim.x, GS_STEP_STATS, P.stats_out, is_max, s_red);
 }
+#endif  // GS_BUILD_VARIANTS (phase-separated kernel)
 
 // ---------------------------------------------------------------------------
 // Pipelined variant: a persistent CTA walks its chunks through an S-stage
@@ -322,6 +325,7 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
+#if GS_BUILD_VARIANTS
 template <class L, int R>
 struct PipeStage {
   static constexpr int kSlots = L::P + 1;                  // record slots per row
@@ -558,12 +562,7 @@ __global__ void __launch_bounds__(kFixedThreads, MINB) step_pipe_kernel(const Fi
 template <class L, int MODE, bool STRICT, int R, int S, int MINB>
 void launch_pipe(const FixedParams& P, int64_t max_rows, cudaStream_t s) {
   constexpr int bytes = S * PipeStage<L, R>::kBytes;
-  static bool attr_set = false;  // per instantiation
-  if (!attr_set) {
-    cudaFuncSetAttribute(step_pipe_kernel<L, MODE, STRICT, R, S, MINB>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-    attr_set = true;
-  }
+  smem_opt_in<step_pipe_kernel<L, MODE, STRICT, R, S, MINB>>(bytes);
   const int64_t chunks = (max_rows + R - 1) / R;
   const int grid =
       (int)std::max<int64_t>(1, std::min<int64_t>(chunks, (int64_t)gs_sm_count() * MINB));
@@ -809,18 +808,14 @@ __global__ void __launch_bounds__(kFixedThreads, MINB) step_pipe2_kernel(const F
 template <class L, int MODE, bool STRICT, int R, int S, int MINB>
 void launch_pipe2(const FixedParams& P, int64_t max_rows, cudaStream_t s) {
   constexpr int bytes = S * PipeStage<L, R>::kBytes;
-  static bool attr_set = false;  // per instantiation
-  if (!attr_set) {
-    cudaFuncSetAttribute(step_pipe2_kernel<L, MODE, STRICT, R, S, MINB>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-    attr_set = true;
-  }
+  smem_opt_in<step_pipe2_kernel<L, MODE, STRICT, R, S, MINB>>(bytes);
   const int64_t chunks = (max_rows + R - 1) / R;
   const int grid =
       (int)std::max<int64_t>(1, std::min<int64_t>(chunks, (int64_t)gs_sm_count() * MINB));
   step_pipe2_kernel<L, MODE, STRICT, R, S, MINB><<<grid, kFixedThreads, bytes, s>>>(P);
 }
 
+#endif  // GS_BUILD_VARIANTS (pipe / pipe2)
 // ---------------------------------------------------------------------------
 // Warp-specialised variant: kProd producer warps fill an S-stage ring with
 // cp.async gathers (row ids, 16-byte record pieces, 4-byte theta / grad
@@ -1205,12 +1200,7 @@ template <class L, int MODE, bool STRICT, int R, int S, int NPW, int NCW, int MI
           bool REC = false, bool BULKST = false>
 void launch_ws(const FixedParams& P, int64_t max_rows, cudaStream_t s) {
   constexpr int bytes = S * WsStage<L, R>::kBytes;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(step_ws_kernel<L, MODE, STRICT, R, S, NPW, NCW, MINB, REC, BULKST>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-    attr_set = true;
-  }
+  smem_opt_in<step_ws_kernel<L, MODE, STRICT, R, S, NPW, NCW, MINB, REC, BULKST>>(bytes);
   const int64_t chunks = (max_rows + R - 1) / R;
   const int grid =
       (int)std::max<int64_t>(1, std::min<int64_t>(chunks, (int64_t)gs_sm_count() * MINB));
@@ -1611,12 +1601,7 @@ template <class L, int MODE, bool STRICT, int R, int S, int NPW, int NCW, int MI
           bool REC = true, int HINT = 0>
 void launch_ring(const FixedParams& P, int64_t max_rows, cudaStream_t s) {
   constexpr int bytes = S * WsStage<L, R>::kBytes;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(step_ring_kernel<L, MODE, STRICT, R, S, NPW, NCW, MINB, FLAT, REC, HINT>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-    attr_set = true;
-  }
+  smem_opt_in<step_ring_kernel<L, MODE, STRICT, R, S, NPW, NCW, MINB, FLAT, REC, HINT>>(bytes);
   const int64_t chunks = (max_rows + R - 1) / R;
   const int grid =
       (int)std::max<int64_t>(1, std::min<int64_t>(chunks, (int64_t)gs_sm_count() * MINB));
@@ -1624,6 +1609,7 @@ void launch_ring(const FixedParams& P, int64_t max_rows, cudaStream_t s) {
       <<<grid, (NPW + NCW) * 32, bytes, s>>>(P);
 }
 
+#if GS_BUILD_VARIANTS  // 1-D bulk-copy kernel (TMA op rate bound)
 // ---------------------------------------------------------------------------
 // TMA variant for row-interleaved records (parameters, gradients and the
 // optimizer-state record all row-contiguous): one producer warp moves each
@@ -1887,20 +1873,24 @@ __global__ void __launch_bounds__((NCW + 1) * 32, MINB) step_tma_kernel(const Fi
 template <class L, int MODE, bool STRICT, int R, int S, int NCW, int MINB>
 void launch_tma(const FixedParams& P, int64_t max_rows, cudaStream_t s) {
   constexpr int bytes = S * TmaStage<L, R>::kBytes;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(step_tma_kernel<L, MODE, STRICT, R, S, NCW, MINB>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-    attr_set = true;
-  }
+  smem_opt_in<step_tma_kernel<L, MODE, STRICT, R, S, NCW, MINB>>(bytes);
   const int64_t chunks = (max_rows + R - 1) / R;
   const int grid =
       (int)std::max<int64_t>(1, std::min<int64_t>(chunks, (int64_t)gs_sm_count() * MINB));
   step_tma_kernel<L, MODE, STRICT, R, S, NCW, MINB><<<grid, (NCW + 1) * 32, bytes, s>>>(P);
 }
 
+#endif  // GS_BUILD_VARIANTS (1-D bulk copies)
+
+}  // namespace gs
+
+#include "gs_step_sh3_tma.cuh"
+
+namespace gs {
+
 int fixed_variant();  // gs_step_sh3.cu: GS_FIXED_VARIANT / gs_set_fixed_variant
 
+#if GS_BUILD_VARIANTS
 template <class L, int MODE, bool STRICT, int R, int MINB, int NT = kFixedThreads>
 void launch_fixed_v(const FixedParams& P, int64_t max_rows, cudaStream_t s) {
   const int64_t chunks = (max_rows + R - 1) / R;
@@ -1909,71 +1899,83 @@ void launch_fixed_v(const FixedParams& P, int64_t max_rows, cudaStream_t s) {
   step_fixed_kernel<L, MODE, STRICT, R, MINB, NT><<<grid, NT, 0, s>>>(P);
 }
 
-// kind: 0 dense per-attribute rows, 1 strided rows (per-element gathers),
-// 2 row-interleaved parameter + gradient records
+// Measured alternatives of the record and per-attribute kernels (results
+// identical).  Returns false for an unknown variant.
 template <class L, int MODE, bool STRICT>
-void launch_fixed(const FixedParams& P, int64_t max_rows, int kind, cudaStream_t s) {
+bool launch_variant(const FixedParams& P, int64_t max_rows, int kind, int v, cudaStream_t s) {
   if (kind == 2) {
-    // records: bulk-copy (TMA) kernel when the state record allows 16-byte
-    // bulk copies, else the cp.async gather kernel on the record layout
-    // Default: cp.async record gathers + per-element stores.  The bulk-copy
-    // (TMA) kernels are kept as variants: for 240 / 480-byte rows the TMA
-    // unit's per-operation cost bounds them (~0.86 ms vs 0.67 ms on c3,
-    // profiles/r01/ncu_step_tma_c3_record.txt), loads and stores alike.
+    switch (v) {
+      case 8: launch_ws<L, MODE, STRICT, 32, 3, 3, 8, 2, true>(P, max_rows, s); return true;
+      case 9: launch_tma<L, MODE, STRICT, 32, 6, 12, 1>(P, max_rows, s); return true;
+      case 10: launch_tma<L, MODE, STRICT, 32, 3, 4, 2>(P, max_rows, s); return true;
+      case 11: launch_ws<L, MODE, STRICT, 32, 3, 3, 8, 2, true, true>(P, max_rows, s); return true;
+      case 12: launch_tma<L, MODE, STRICT, 32, 3, 8, 2>(P, max_rows, s); return true;
+      case 13: launch_ring<L, MODE, STRICT, 32, 3, 3, 8, 2, false>(P, max_rows, s); return true;
+      case 14: launch_ring<L, MODE, STRICT, 32, 3, 2, 8, 2, true>(P, max_rows, s); return true;
+      case 16: launch_ring<L, MODE, STRICT, 32, 2, 2, 6, 3, true>(P, max_rows, s); return true;
+      case 17: launch_ring<L, MODE, STRICT, 32, 3, 3, 8, 2, true>(P, max_rows, s); return true;
+      case 18: launch_ring<L, MODE, STRICT, 32, 2, 2, 8, 2, true>(P, max_rows, s); return true;
+      case 19: launch_ring<L, MODE, STRICT, 32, 2, 4, 8, 2, true>(P, max_rows, s); return true;
+      case 20: launch_ring<L, MODE, STRICT, 32, 2, 3, 8, 2, true, true, 0>(P, max_rows, s); return true;
+      default: return false;
+    }
+  }
+  switch (v) {
+    case 1: launch_fixed_v<L, MODE, STRICT, 64, 2>(P, max_rows, s); return true;
+    case 2: launch_pipe<L, MODE, STRICT, 32, 2, 3>(P, max_rows, s); return true;
+    case 3: launch_pipe2<L, MODE, STRICT, 32, 2, 3>(P, max_rows, s); return true;
+    case 4: launch_ws<L, MODE, STRICT, 32, 3, 2, 8, 2>(P, max_rows, s); return true;
+    case 5: launch_pipe2<L, MODE, STRICT, 32, 3, 2>(P, max_rows, s); return true;
+    case 6: launch_ws<L, MODE, STRICT, 32, 3, 2, 6, 2>(P, max_rows, s); return true;
+    // ring kernel on per-attribute tensors: a shuffle per 4-byte element costs
+    // the producers more than the barrier it saves (0.81 vs 0.78 ms on c3)
+    case 7: launch_ring<L, MODE, STRICT, 32, 3, 3, 8, 2, true, false>(P, max_rows, s); return true;
+    case 19: launch_ws<L, MODE, STRICT, 32, 3, 3, 8, 2>(P, max_rows, s); return true;  // 3 stages
+    default: return false;
+  }
+}
+#endif  // GS_BUILD_VARIANTS
+
+// kind: 0 dense per-attribute rows, 1 strided rows (per-element gathers),
+// 2 row-interleaved parameter + gradient records.  M: tensor maps of the
+// records when the TMA kernel may run (device-resident, 16-byte strides,
+// rows of >= 64 floats), else null.
+template <class L, int MODE, bool STRICT>
+void launch_fixed(const FixedParams& P, const TmaMaps* M, int64_t max_rows, int kind,
+                  cudaStream_t s) {
+  // the densification statistics run in the default kernels only
+  const int v = P.D.group >= 0 ? 0 : fixed_variant();
+#if GS_BUILD_VARIANTS
+  if (v > 0 && v != 21 && launch_variant<L, MODE, STRICT>(P, max_rows, kind, v, s)) return;
+#endif
+  if (kind == 2) {
+    // records: 2-D TMA row gathers / scatters (tile::gather4 / scatter4,
+    // gs_step_sh3_tma.cuh) when the records allow them; the cp.async ring
+    // otherwise (host-mapped gradients, compact 240-byte rows) or on request
+    // (variant 21)
+    if (M != nullptr && v != 21) {
+      static const int shape = getenv("GS_TMA4_SHAPE") ? atoi(getenv("GS_TMA4_SHAPE")) : 0;
+      switch (shape) {
+        case 1: launch_tma4<L, MODE, STRICT, 3, 8, 2>(P, *M, max_rows, s); return;
+        case 2: launch_tma4<L, MODE, STRICT, 2, 12, 2>(P, *M, max_rows, s); return;
+        case 3: launch_tma4<L, MODE, STRICT, 2, 8, 3>(P, *M, max_rows, s); return;
+        case 4: launch_tma4<L, MODE, STRICT, 3, 16, 1>(P, *M, max_rows, s); return;
+        case 5: launch_tma4<L, MODE, STRICT, 4, 16, 1>(P, *M, max_rows, s); return;
+        case 6: launch_tma4<L, MODE, STRICT, 3, 12, 2>(P, *M, max_rows, s); return;
+        default: launch_tma4<L, MODE, STRICT, 2, 8, 2>(P, *M, max_rows, s); return;
+      }
+    }
     if (P.wide) {  // > 2^32 parameter-record elements: 64-bit row offsets
       launch_ring<L, MODE, STRICT, 32, 2, 3, 8, 2, true, true, 1 | 32>(P, max_rows, s);
       return;
     }
-    const int v = (P.D.group >= 0 || !P.tma_ok) ? 0 : fixed_variant();
-    if (v == 8) {
-      launch_ws<L, MODE, STRICT, 32, 3, 3, 8, 2, true>(P, max_rows, s);
-    } else if (v == 13) {
-      launch_ring<L, MODE, STRICT, 32, 3, 3, 8, 2, false>(P, max_rows, s);
-    } else if (v == 16) {
-      launch_ring<L, MODE, STRICT, 32, 2, 2, 6, 3, true>(P, max_rows, s);
-    } else if (v == 17) {  // the 3-stage ring (default before the 2-stage sweep)
-      launch_ring<L, MODE, STRICT, 32, 3, 3, 8, 2, true>(P, max_rows, s);
-    } else if (v == 18) {
-      launch_ring<L, MODE, STRICT, 32, 2, 2, 8, 2, true>(P, max_rows, s);
-    } else if (v == 19) {
-      launch_ring<L, MODE, STRICT, 32, 2, 4, 8, 2, true>(P, max_rows, s);
-    } else if (v == 20) {  // no L2 prefetch-size hint on the gathers
-      launch_ring<L, MODE, STRICT, 32, 2, 3, 8, 2, true, true, 0>(P, max_rows, s);
-    } else if (v == 14) {
-      launch_ring<L, MODE, STRICT, 32, 3, 2, 8, 2, true>(P, max_rows, s);
-    } else if (v == 11) {
-      launch_ws<L, MODE, STRICT, 32, 3, 3, 8, 2, true, true>(P, max_rows, s);
-    } else if (v == 9) {
-      launch_tma<L, MODE, STRICT, 32, 6, 12, 1>(P, max_rows, s);
-    } else if (v == 10) {
-      launch_tma<L, MODE, STRICT, 32, 3, 4, 2>(P, max_rows, s);
-    } else if (v == 12) {
-      launch_tma<L, MODE, STRICT, 32, 3, 8, 2>(P, max_rows, s);
-    } else {
-      // 2 stages beat 3 on every workload measured (c3 K2 0.595 vs 0.627 ms,
-      // profiles/r01/ring_stage_sweep.txt); 2 or 4 producer warps do worse
-      // L2::256B prefetch-size hint on the gathers: 0.595 -> 0.592 ms (c3),
-      // same on coherent masks; evict-first stores measured no change
-      launch_ring<L, MODE, STRICT, 32, 2, 3, 8, 2, true, true, 1>(P, max_rows, s);
-    }
+    // 2 stages beat 3 on every workload measured (c3 K2 0.595 vs 0.627 ms,
+    // profiles/r01/ring_stage_sweep.txt); 2 or 4 producer warps do worse;
+    // L2::256B prefetch-size hint on the gathers: 0.595 -> 0.592 ms (c3)
+    launch_ring<L, MODE, STRICT, 32, 2, 3, 8, 2, true, true, 1>(P, max_rows, s);
     return;
   }
-  // the densification statistics and strided rows are handled by the
-  // default kernel only
-  const int variant = (P.D.group >= 0 || kind != 0) ? 0 : fixed_variant();
-  switch (variant) {
-    case 1: launch_fixed_v<L, MODE, STRICT, 64, 2>(P, max_rows, s); return;
-    case 2: launch_pipe<L, MODE, STRICT, 32, 2, 3>(P, max_rows, s); return;
-    case 3: launch_pipe2<L, MODE, STRICT, 32, 2, 3>(P, max_rows, s); return;
-    case 4: launch_ws<L, MODE, STRICT, 32, 3, 2, 8, 2>(P, max_rows, s); return;
-    case 5: launch_pipe2<L, MODE, STRICT, 32, 3, 2>(P, max_rows, s); return;
-    case 6: launch_ws<L, MODE, STRICT, 32, 3, 2, 6, 2>(P, max_rows, s); return;
-    // ring kernel on per-attribute tensors: a shuffle per 4-byte element costs
-    // the producers more than the barrier it saves (0.81 vs 0.78 ms on c3)
-    case 7: launch_ring<L, MODE, STRICT, 32, 3, 3, 8, 2, true, false>(P, max_rows, s); return;
-    case 19: launch_ws<L, MODE, STRICT, 32, 3, 3, 8, 2>(P, max_rows, s); return;  // 3 stages
-    default: launch_ws<L, MODE, STRICT, 32, 2, 3, 8, 2>(P, max_rows, s); return;
-  }
+  launch_ws<L, MODE, STRICT, 32, 2, 3, 8, 2>(P, max_rows, s);
 }
 
 }  // namespace gs

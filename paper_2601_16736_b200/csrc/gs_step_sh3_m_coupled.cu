@@ -2,6 +2,8 @@
 #include "gs_step_sh3.cuh"
 
 namespace gs {
-template void launch_fixed<LayoutSH3, GS_MODE_COUPLED_ADAM, false>(const FixedParams&, int64_t, int, cudaStream_t);
-template void launch_fixed<LayoutSH3, GS_MODE_COUPLED_ADAM, true>(const FixedParams&, int64_t, int, cudaStream_t);
+template void launch_fixed<LayoutSH3, GS_MODE_COUPLED_ADAM, false>(const FixedParams&, const TmaMaps*, int64_t, int,
+                                                              cudaStream_t);
+template void launch_fixed<LayoutSH3, GS_MODE_COUPLED_ADAM, true>(const FixedParams&, const TmaMaps*, int64_t, int,
+                                                              cudaStream_t);
 }  // namespace gs

@@ -1,0 +1,382 @@
+// K2 on the row records with Blackwell 2-D TMA row gathers and scatters
+// (cp.async.bulk.tensor.2d ... tile::gather4 / tile::scatter4, SASS UTMALDG /
+// UTMASTG): the default SH-3 step for device-resident parameter, gradient and
+// moment records (included by gs_step_sh3.cuh).
+//
+// A CTA walks chunks of 32 visible rows through an S-stage shared-memory
+// ring.  Warp roles:
+//   loader  (warp NCW)     per chunk, lanes 0..7 each issue three gather4
+//                          operations (4 rows each) for the moment records
+//                          (480 B of every 512-B row), the parameter rows and
+//                          the gradient rows (256 B each), completing on the
+//                          stage's "full" mbarrier by transaction bytes; every
+//                          lane also stages its row id and the bias factors of
+//                          its row's next clock (from the bias LUT).
+//   consumers (warps 0..NCW-1)  check, then update the staged rows IN PLACE
+//                          (theta, m, v, clock), then fence the async proxy
+//                          and arrive on the stage's "done" mbarrier.
+//   storer  (warp NCW+1)   lanes 0..7 scatter4 the parameter rows and the
+//                          moment records back, wait until the bulk stores
+//                          have read the stage, and hand it back to the
+//                          loader ("empty" mbarrier).
+// Rows past the end of the index list get row id n_rows: the gathers fill
+// them with zeros and the scatters drop them (out of the tensor's bounds).
+// A skipped (bad) row is left unchanged in the stage, so its scatter writes
+// back the bytes it read.  Per-row math is gs_common.cuh::update_element in
+// the same element order as step_ring_kernel, so results are bit-identical.
+//
+// Compared with the cp.async ring (60 16-byte LSU copies and ~120 scattered
+// 4/8-byte stores per row), a 32-row chunk costs 24 + 16 TMA operations and
+// the SM issue slots go to the arithmetic.  Probe on B200 (scripts/
+// tma4_probe.cu, profiles/r02/tma4_probe.txt): the data movement alone runs
+// at 0.86 of the copy peak for 30% i.i.d. rows and 0.94 for all rows.
+#pragma once
+
+#include <cuda.h>
+
+namespace gs {
+
+struct TmaMaps {
+  CUtensorMap rec;  // moment record  [n_rows, stride] fp32, box {2*(P+1), 1}
+  CUtensorMap prm;  // parameter record [n_rows, prs], box {64, 1}
+  CUtensorMap grd;  // gradient record  [n_rows, grs], box {64, 1}
+};
+
+template <class L, int R>
+struct Tma4Stage {
+  static constexpr int kSlots = L::P + 1;   // float2 slots of a moment record row
+  static constexpr int kRecRow = kSlots * 8;
+  static constexpr int kPT = 64;            // staged parameter / gradient row (floats)
+  static constexpr int kRec = R * kRecRow;
+  static constexpr int kTh = R * kPT * 4;
+  static constexpr int kBytes = kRec + 2 * kTh;
+  static_assert(kPT >= L::P, "parameter row box");
+  static_assert((4 * kRecRow) % 128 == 0 && (4 * kPT * 4) % 128 == 0 && kBytes % 128 == 0,
+                "every 4-row TMA box lands 128-byte aligned");
+};
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;\n" ::"r"(a), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma_gather4(void* smem, const CUtensorMap* map, int r0, int r1,
+                                            int r2, int r3, uint64_t* bar) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];\n" ::"r"(s),
+      "l"(map), "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(b)
+      : "memory");
+}
+__device__ __forceinline__ void tma_scatter4(const CUtensorMap* map, const void* smem, int r0,
+                                             int r1, int r2, int r3) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile(
+      "cp.async.bulk.tensor.2d.global.shared::cta.tile::scatter4.bulk_group"
+      " [%0, {%2, %3, %4, %5, %6}], [%1];\n" ::"l"(map),
+      "r"(s), "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3)
+      : "memory");
+}
+
+template <class L, int MODE, bool STRICT, int S, int NCW, int MINB>
+__global__ void __launch_bounds__((NCW + 2) * 32, MINB)
+    step_tma4_kernel(const FixedParams P, const __grid_constant__ TmaMaps M) {
+  constexpr int R = 32;
+  constexpr bool kDense = MODE == GS_MODE_COUPLED_ADAM;
+  constexpr bool kCoupled = MODE == GS_MODE_COUPLED_ADAM || MODE == GS_MODE_SPARSE_ADAM;
+  constexpr int NC = NCW * 32;
+  constexpr int SLOTS = L::P + 1;
+  using SH = ChunkShape<L, R, NC>;
+  using ST = Tma4Stage<L, R>;
+  constexpr int PT = ST::kPT;
+  extern __shared__ unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t full_bar[S];
+  __shared__ __align__(8) uint64_t done_bar[S];
+  __shared__ __align__(8) uint64_t empty_bar[S];
+  __shared__ int s_badg[S][R];  // == epoch: non-finite gradient in this use of the stage
+  __shared__ int s_badd[S][R];  // == epoch: activation-domain violation
+  __shared__ int s_any[S];
+  __shared__ float2 s_bc[S][R];
+  __shared__ uint32_t s_crow[S][R];
+  __shared__ double s_red[GS_STEP_STATS * (NCW + 2)];
+  // TMA boxes land 128-byte aligned (the host adds 128 bytes of slack)
+  unsigned char* const smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~static_cast<uintptr_t>(127));
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  int n_rows = kDense ? (int)P.max_rows : *P.n_rows_dev;
+  if (STRICT && *P.abort_flag != 0) n_rows = 0;
+  const int n_chunks = (n_rows + R - 1) / R;
+  const int G = (int)gridDim.x;
+  const int oob = (int)P.max_rows;  // row id past the tensors: zero-filled / dropped
+  auto chunk_rows = [&](int c) -> int {
+    const int rem = n_rows - c * R;
+    return rem <= 0 ? 0 : (rem < R ? rem : R);
+  };
+  auto stage = [&](int st) { return smem + st * ST::kBytes; };
+
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full_bar[s], 32);  // the loader warp's lanes (bias factors, row ids) + tx
+      mbar_init(&done_bar[s], NC);
+      mbar_init(&empty_bar[s], 1);
+    }
+  }
+  if (tid < R * S) {
+    s_badg[tid / R][tid % R] = 0;
+    s_badd[tid / R][tid % R] = 0;
+  }
+  if (tid < S) s_any[tid] = 0;
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  __syncthreads();
+
+  unsigned c_vis = 0, c_step = 0, c_badg = 0, c_badd = 0, c_apre = 0, c_apost = 0, c_clo = 0,
+           c_cls = 0;
+  double s_exo = 0.0, s_exs = 0.0;
+
+  if (warp == NCW) {
+    // ------------------------------------------------------------------ loader
+    auto fetch_id = [&](int c) -> int {
+      if (c >= n_chunks || lane >= chunk_rows(c)) return oob;
+      const int i = c * R + lane;
+      return kDense ? i : __ldg(P.rows + i);
+    };
+    int next_id = fetch_id((int)blockIdx.x);
+    int st = 0;
+    unsigned ph = 0;
+    for (int c = (int)blockIdx.x, k = 0; c < n_chunks; c += G, ++k) {
+      const int my_id = next_id;
+      next_id = fetch_id(c + G);
+      if (k >= S) mbar_wait(&empty_bar[st], ph ^ 1u);
+      unsigned char* sb = stage(st);
+      if (lane == 0) mbar_expect_tx(&full_bar[st], ST::kBytes);
+      __syncwarp();
+      const int q = (4 * lane) & 31;
+      const int r0 = __shfl_sync(0xffffffffu, my_id, q);
+      const int r1 = __shfl_sync(0xffffffffu, my_id, q + 1);
+      const int r2 = __shfl_sync(0xffffffffu, my_id, q + 2);
+      const int r3 = __shfl_sync(0xffffffffu, my_id, q + 3);
+      if (lane < R / 4) {
+        tma_gather4(sb + lane * 4 * ST::kRecRow, &M.rec, r0, r1, r2, r3, &full_bar[st]);
+        tma_gather4(sb + ST::kRec + lane * 4 * PT * 4, &M.prm, r0, r1, r2, r3, &full_bar[st]);
+        tma_gather4(sb + ST::kRec + ST::kTh + lane * 4 * PT * 4, &M.grd, r0, r1, r2, r3,
+                    &full_bar[st]);
+      }
+      // row ids and bias factors of the row's next clock ride the stage, so
+      // the consumers touch no global memory before their barrier
+      if (my_id != oob) {
+        s_crow[st][lane] = (uint32_t)my_id;
+        const int tb = kDense ? P.global_t
+                              : __ldg(reinterpret_cast<const int*>(P.record + (size_t)my_id * P.stride +
+                                                                   2 * L::P)) + 1;
+        s_bc[st][lane] = __ldg(reinterpret_cast<const float2*>(P.lut) + (tb < P.lut_len ? tb : P.lut_len - 1));
+      }
+      mbar_arrive(&full_bar[st]);
+      if (++st == S) {
+        st = 0;
+        ph ^= 1u;
+      }
+    }
+  } else if (warp == NCW + 1) {
+    // ------------------------------------------------------------------ storer
+    int st = 0;
+    unsigned ph = 0;
+    for (int c = (int)blockIdx.x; c < n_chunks; c += G) {
+      const int nv = chunk_rows(c);
+      mbar_wait(&done_bar[st], ph);
+      const int my_id = lane < nv ? (int)s_crow[st][lane] : oob;
+      const unsigned char* sb = stage(st);
+      const int q = (4 * lane) & 31;
+      const int r0 = __shfl_sync(0xffffffffu, my_id, q);
+      const int r1 = __shfl_sync(0xffffffffu, my_id, q + 1);
+      const int r2 = __shfl_sync(0xffffffffu, my_id, q + 2);
+      const int r3 = __shfl_sync(0xffffffffu, my_id, q + 3);
+      if (lane < R / 4 && 4 * lane < nv) {
+        tma_scatter4(&M.rec, sb + lane * 4 * ST::kRecRow, r0, r1, r2, r3);
+        tma_scatter4(&M.prm, sb + ST::kRec + lane * 4 * PT * 4, r0, r1, r2, r3);
+        bulk_commit();
+        bulk_wait_read0();  // the stage may be refilled once the stores have read it
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty_bar[st]);
+      if (++st == S) {
+        st = 0;
+        ph ^= 1u;
+      }
+    }
+    bulk_wait0();  // global writes complete before the CTA retires
+  } else {
+    // ---------------------------------------------------------------- consumers
+    const int t = tid;
+    StepConsts Kc = P.K;
+    if (kCoupled) {
+      const float nv = P.nv_dev ? (float)(*P.nv_dev) : (float)P.nv_host;
+      Kc.inv_nv = nv != 0.0f ? __frcp_rn(nv) : 0.0f;
+      if (nv == 0.0f) Kc.lam_op = Kc.lam_sc = 0.0f;
+    }
+    const StepConsts& K = kCoupled ? Kc : P.K;
+    int st = 0;
+    int ep = 1;  // this use of stage st (epoch tag of its row flags)
+    for (int c = (int)blockIdx.x; c < n_chunks; c += G) {
+      const int nvalid = chunk_rows(c);
+      mbar_wait(&full_bar[st], (unsigned)((ep - 1) & 1));
+      unsigned char* sb = stage(st);
+      float2* srec = reinterpret_cast<float2*>(sb);
+      float* sth = reinterpret_cast<float*>(sb + ST::kRec);
+      const float* sg = sth + R * PT;
+      const uint32_t* srow = s_crow[st];
+      const int tn = t < nvalid ? reinterpret_cast<const int*>(srec + t * SLOTS + L::P)[0] + 1 : 0;
+      if (!STRICT) {
+        // gradients in 16-byte pieces (columns >= P are pad and ignored);
+        // activation domain on the opacity / scale columns of theta
+        constexpr int kQ = (L::P + 3) / 4;
+#pragma unroll
+        for (int j = 0; j < (R * kQ + NC - 1) / NC; ++j) {
+          const int p = j * NC + t;
+          const int r = p / kQ;
+          if (p < R * kQ && r < nvalid) {
+            const int qq = p - r * kQ;
+            const float4 v = reinterpret_cast<const float4*>(sg + r * PT)[qq];
+            const bool bad = !isfinite(v.x) || (4 * qq + 1 < L::P && !isfinite(v.y)) ||
+                             (4 * qq + 2 < L::P && !isfinite(v.z)) ||
+                             (4 * qq + 3 < L::P && !isfinite(v.w));
+            if (bad) {
+              atomicMax(&s_badg[st][r], ep);
+              s_any[st] = ep;
+            }
+          }
+        }
+        int dbase = 0;
+#pragma unroll
+        for (int gg = 0; gg < L::G; ++gg) {
+          const int role = L::ROLE(gg);
+          if (role != GS_ROLE_OPACITY && role != GS_ROLE_SCALE) continue;
+          const int W = L::W(gg);
+          const float lam = role == GS_ROLE_OPACITY ? K.lam_op : K.lam_sc;
+          if (lam != 0.f) {
+#pragma unroll
+            for (int kk = 0; kk < (R * W + NC - 1) / NC; ++kk) {
+              const int i = kk * NC + (NC - 1 - t + NC - dbase % NC) % NC;
+              const int r = i / W;
+              if (i < R * W && r < nvalid && domain_bad(role, sth[r * PT + L::OFF(gg) + (i - r * W)])) {
+                atomicMax(&s_badd[st][r], ep);
+                s_any[st] = ep;
+              }
+            }
+          }
+          dbase += R * W;
+        }
+      }
+      named_sync(1, NC);  // flags of the chunk are final; nobody has written the stage yet
+      const bool any_bad = s_any[st] == ep || nvalid < R;
+      auto row_ok = [&](int r) { return s_badg[st][r] != ep && s_badd[st][r] != ep; };
+      // every thread reads the elements it updates before writing them, and
+      // the element sets of different threads are disjoint, so in-place
+      // updates need no further barrier
+      auto update = [&](int gg, int i, int r) {
+        const int W = L::W(gg);
+        const int role = L::ROLE(gg);
+        const int cc = i - r * W;
+        const int e = r * PT + L::OFF(gg) + cc;
+        float2* mvp = srec + r * SLOTS + L::OFF(gg) + cc;
+        const float2 mv = *mvp;
+        const float th = sth[e];
+        float tnv, mn, vn, ex;
+        bool clipped;
+        update_element<MODE>(role, P.g[gg].lr, th, sg[e], mv.x, mv.y, s_bc[st][r], K, tnv, mn, vn,
+                             ex, clipped);
+        if (!kCoupled && role == GS_ROLE_OPACITY) {
+          c_clo += clipped;
+          s_exo += (double)ex;
+        } else if (!kCoupled && role == GS_ROLE_SCALE) {
+          c_cls += clipped;
+          s_exs += (double)ex;
+        }
+        if (role == GS_ROLE_OPACITY) {
+          c_apre += th > P.active_logit;
+          c_apost += tnv > P.active_logit;
+        }
+        sth[e] = tnv;
+        *mvp = make_float2(mn, vn);
+      };
+      if (!any_bad) {
+#pragma unroll
+        for (int gg = 0; gg < L::G; ++gg) {
+#pragma unroll
+          for (int kk = 0; kk < SH::rounds(gg); ++kk) {
+            const int i = kk * NC + ((t + NC - (R * L::OFF(gg)) % NC) % NC);
+            const bool full = (kk + 1) * NC <= R * L::W(gg);  // compile-time
+            if (full || i < R * L::W(gg)) update(gg, i, i / L::W(gg));
+          }
+        }
+      } else {
+#pragma unroll
+        for (int gg = 0; gg < L::G; ++gg) {
+#pragma unroll
+          for (int kk = 0; kk < SH::rounds(gg); ++kk) {
+            const int i = kk * NC + ((t + NC - (R * L::OFF(gg)) % NC) % NC);
+            const int r = i / L::W(gg);
+            if (i < R * L::W(gg) && r < nvalid && row_ok(r)) update(gg, i, r);
+          }
+        }
+      }
+      if (t < nvalid) {
+        ++c_vis;
+        if (row_ok(t)) {
+          // the clock slot belongs to no element: thread t owns it
+          reinterpret_cast<int*>(srec + t * SLOTS + L::P)[0] = tn;
+          if (P.D.group >= 0) {
+#pragma unroll
+            for (int gg = 0; gg < L::G; ++gg)
+              if (gg == P.D.group) densify_row(P.D, srow[t], sg + t * PT + L::OFF(gg), L::W(gg), 1);
+          }
+          ++c_step;
+        } else if (s_badg[st][t] == ep) {
+          ++c_badg;
+        } else {
+          ++c_badd;
+        }
+      }
+      fence_proxy_async_smem();     // generic-proxy writes of the stage -> the bulk stores
+      mbar_arrive(&done_bar[st]);
+      if (++st == S) {
+        st = 0;
+        ++ep;
+      }
+    }
+  }
+
+  double acc[GS_STEP_STATS] = {(double)c_vis,  (double)c_step, (double)c_badg, (double)c_badd,
+                               (double)c_apre, (double)c_apost, (double)c_clo, (double)c_cls,
+                               s_exo,          s_exs};
+  const bool is_max[GS_STEP_STATS] = {false, false, false, false, false,
+                                      false, false, false, false, false};
+  block_reduce_n<GS_STEP_STATS, (NCW + 2)>(acc, is_max, s_red);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int f = 0; f < GS_STEP_STATS; ++f)
+      P.partials[(size_t)blockIdx.x * GS_STEP_STATS + f] = acc[f];
+  }
+  if (last_block_arrive(P.counter))
+    final_reduce_n<GS_STEP_STATS, (NCW + 2)>(P.partials, gridDim.x, GS_STEP_STATS, P.stats_out,
+                                             is_max, s_red);
+}
+
+// Host: tensor maps of the three records (cuTensorMapEncodeTiled through the
+// runtime's driver entry point; no libcuda link dependency).
+bool encode_tma_maps(const FixedParams& P, int64_t n_rows, int rec_box, TmaMaps* out);
+
+template <class L, int MODE, bool STRICT, int S, int NCW, int MINB>
+void launch_tma4(const FixedParams& P, const TmaMaps& M, int64_t max_rows, cudaStream_t s) {
+  constexpr int bytes = S * Tma4Stage<L, 32>::kBytes + 128;
+  smem_opt_in<step_tma4_kernel<L, MODE, STRICT, S, NCW, MINB>>(bytes);
+  const int64_t chunks = (max_rows + 31) / 32;
+  const int grid =
+      (int)std::max<int64_t>(1, std::min<int64_t>(chunks, (int64_t)gs_sm_count() * MINB));
+  step_tma4_kernel<L, MODE, STRICT, S, NCW, MINB><<<grid, (NCW + 2) * 32, bytes, s>>>(P, M);
+}
+
+}  // namespace gs

@@ -73,20 +73,24 @@ def active_logit_threshold() -> float:
     return float(t)
 
 
-def bias_lut(beta1: float, beta2: float, cap: int = 1 << 22) -> np.ndarray:
-    """fp32 factors 1/(1-beta^t) from float64, t in [0, L); beyond L both are 1.0f.
-
-    Denominators as in ``_corrected`` (optimizer.py:202-203).  The table is
-    extended until both factors round to exactly 1.0f, so clamping the clock
-    to the last entry is exact; otherwise the kernel evaluates the float64
-    formula for clocks past the table.
-    """
+def bias_lut_exact_len(beta1: float, beta2: float) -> int:
+    """Entries t = 0 .. L-1 after which both fp32 factors 1/(1-beta^t) are
+    exactly 1.0f (beta^t < 2^-26), so a kernel clamping t to L-1 is exact."""
     b = max(beta1, beta2)
     if b <= 0.0:
-        n = 2
-    else:
-        n = int(min(cap, math.ceil(math.log(2.0 ** -26) / math.log(b)) + 2))
-    n = max(n, 2)
+        return 2
+    return max(2, int(math.ceil(math.log(2.0 ** -26) / math.log(b))) + 2)
+
+
+def bias_lut(beta1: float, beta2: float, length: int | None = None) -> np.ndarray:
+    """fp32 factors 1/(1-beta^t) rounded once from float64, t in [0, length).
+
+    Denominators as in ``_corrected`` (optimizer.py:202-203).  The kernels
+    read entry t for a clock t (clamped to the last entry): exact as long as
+    the table covers every clock in use or reaches bias_lut_exact_len
+    (StepEngine.ensure_lut keeps that true; oracle.step_fp32 computes the
+    same float64 formula)."""
+    n = bias_lut_exact_len(beta1, beta2) if length is None else max(2, int(length))
     t = np.arange(n, dtype=np.float64)
     with np.errstate(divide="ignore"):
         c1 = 1.0 / (1.0 - np.power(beta1, t))
@@ -189,8 +193,12 @@ class StepEngine:
                                        dtype=torch.uint8, device=dev)
             self.stats = torch.zeros(L.GS_STEP_STATS, dtype=torch.float64, device=dev)
             self.abort = torch.zeros(1, dtype=torch.int32, device=dev)
-            lut = bias_lut(self.beta1, self.beta2)
-            self.lut = torch.from_numpy(lut).to(dev)
+            # the bias LUT grows with the clocks in use (ensure_lut), up to the
+            # exact length past which both factors are 1.0f
+            self.lut_exact_len = bias_lut_exact_len(self.beta1, self.beta2)
+            self.lut = torch.from_numpy(
+                bias_lut(self.beta1, self.beta2, min(self.lut_exact_len, 1 << 14))).to(dev)
+            self._old_luts = []
             self.stats_ws = torch.zeros(int(self.lib.gs_stats_workspace_bytes(L.GS_MAX_GROUPS)),
                                         dtype=torch.uint8, device=dev)
             self.stats_all_out = torch.zeros(2 + 5 * L.GS_MAX_GROUPS, dtype=torch.float64,
@@ -208,6 +216,18 @@ class StepEngine:
         self._omb1 = float(np.float32(1.0 - self.beta1))
         self._omb2 = float(np.float32(1.0 - self.beta2))
         self._eps32 = {}
+
+    def ensure_lut(self, t_max: int):
+        """Make the bias LUT exact for every clock <= t_max (it doubles, up to
+        the exact length).  Earlier tables stay alive: a captured CUDA graph
+        keeps reading the table it was captured with, so capture first
+        extends the table to its exact length (AdamWGS.capture)."""
+        if t_max < self.lut.shape[0] or self.lut.shape[0] >= self.lut_exact_len:
+            return
+        n = min(self.lut_exact_len, max(2 * self.lut.shape[0], int(t_max) + 1))
+        self._old_luts.append(self.lut)
+        self.lut = torch.from_numpy(bias_lut(self.beta1, self.beta2, n)).to(self.device)
+        self._cfg_key = None  # the cached configuration holds the table pointer
 
     # ------------------------------------------------------------------ groups
     def group_array(self, groups: list[GroupBinding], need_grad: bool = True):
@@ -389,11 +409,18 @@ class StepEngine:
              clip_scale: float = 10.0, n_pixels_rounded: float = 0.0, global_t: int = 0,
              n_visible_dev: torch.Tensor | None = None, n_visible_host: float = 0.0,
              check: str = "fused", record: torch.Tensor | None = None,
-             densify: tuple | None = None) -> torch.Tensor:
+             densify: tuple | None = None, abort_hook=None,
+             densify_rows: tuple | None = None) -> torch.Tensor:
         """K2 (plus the strict pre-check when ``check == "strict"``).
 
         ``record`` given: row-record state (gs_step_rows), ``clock`` ignored;
         otherwise per-group m / v tensors and the int32 ``clock``.
+        ``abort_hook(flag)``: called between the strict pre-check and the
+        step with the device abort flag (index-sharded runs all-reduce it so
+        every shard aborts together).  ``densify_rows``: (rows, count) of the
+        visible rows for the dense mode, whose kernels step every row: the
+        densification statistics then observe only those rows
+        (gs_densify_rows) instead of being fused into the step.
         """
         if mode not in L.MODE_IDS:
             raise ConfigError(f"unknown mode {mode!r}; expected one of {tuple(L.MODE_IDS)}")
@@ -403,8 +430,9 @@ class StepEngine:
             self._check_record(record, groups)
         garr = self.group_array(groups)
         s = _stream_handle(self.device)
-        dkey = None if densify is None else (densify[0].data_ptr(), densify[1].data_ptr(),
-                                             float(densify[2]), int(densify[3]))
+        fused_densify = None if (densify_rows is not None and mode == "coupled-adam") else densify
+        dkey = None if fused_densify is None else (densify[0].data_ptr(), densify[1].data_ptr(),
+                                                   float(densify[2]), int(densify[3]))
         ckey = (mode, check, eps, float(lambda_opacity), float(lambda_scale),
                 float(clip_opacity), float(clip_scale), float(n_pixels_rounded), int(global_t),
                 _ptr(n_visible_dev), float(n_visible_host), dkey)
@@ -413,7 +441,7 @@ class StepEngine:
         else:
             cfg = self._build_cfg(mode, check, eps, lambda_opacity, lambda_scale, clip_opacity,
                                   clip_scale, n_pixels_rounded, global_t, n_visible_dev,
-                                  n_visible_host, densify)
+                                  n_visible_host, fused_densify)
             self._cfg_key, self._cfg = ckey, cfg
         if check == "strict":
             # the penalty's activation domain is checked where the penalty
@@ -423,6 +451,8 @@ class StepEngine:
                                          _ptr(dcount), float(lambda_opacity),
                                          float(lambda_scale), None, self.abort.data_ptr(), s)
             L.check(rc, "gs_check_grads")
+            if abort_hook is not None:
+                abort_hook(self.abort)
         if record is None:
             rc = self.lib.gs_step(garr, len(groups), C.byref(cfg), _ptr(rows), _ptr(count),
                                   self.n_rows, clock.data_ptr(), self.stats.data_ptr(),
@@ -435,7 +465,23 @@ class StepEngine:
                                        self.rows_ws.numel(), s)
             L.check(rc, "gs_step_rows")
         self.launches += 2 if check == "strict" else 1
+        if densify_rows is not None and densify is not None and mode == "coupled-adam":
+            self._densify_listed(garr, densify, *densify_rows, strict=check == "strict")
         return self.stats
+
+    def _densify_listed(self, garr, densify, rows, count, strict: bool):
+        """DensifyStats.observe (pipeline.py:77-82) on the listed rows only
+        (a no-op when the strict pre-check aborted the step)."""
+        accum, dcount, dscale, dgroup = densify
+        g = garr[dgroup]
+        gs = g.grad_stride if g.grad_stride else g.width
+        rc = self.lib.gs_densify_rows(g.grad, gs, g.width, rows.data_ptr(), count.data_ptr(),
+                                      self.n_rows, accum.data_ptr(), dcount.data_ptr(),
+                                      float(np.float32(dscale)),
+                                      self.abort.data_ptr() if strict else None,
+                                      _stream_handle(self.device))
+        L.check(rc, "gs_densify_rows")
+        self.launches += 1
 
     def _check_record(self, record: torch.Tensor, groups):
         key = (record.data_ptr(), tuple(record.shape), record.stride(), record.dtype,
@@ -498,13 +544,50 @@ class StepEngine:
 
     # --------------------------------------------------------- RSR / reset
     def _rows_device(self, indices) -> tuple[torch.Tensor, int]:
+        """Row ids for K3 with NumPy fancy-index semantics: a boolean mask
+        selects its true rows, negative ids count from the end, out-of-range
+        ids raise IndexError, and a repeated id acts once (``m[idx] *= a``
+        assigns each selected row once).  Returns sorted distinct int32 ids
+        on the device.  Inside CUDA-graph capture a device tensor cannot be
+        inspected: it is taken as given (the kernels skip ids outside the
+        rows; the caller owns distinctness)."""
+        n = self.n_rows
+        if isinstance(indices, torch.Tensor) and indices.device.type == "cuda" \
+                and indices.dtype != torch.bool:
+            if indices.dtype.is_floating_point or indices.dtype.is_complex:
+                raise IndexError("row indices must be integers or a boolean mask")
+            t = indices.reshape(-1)
+            if torch.cuda.is_current_stream_capturing():
+                t = t.to(device=self.device, dtype=torch.int32).contiguous()
+                return t, int(t.numel())
+            t = t.to(device=self.device, dtype=torch.int64)
+            if t.numel():
+                t = torch.where(t < 0, t + n, t)
+                lo, hi, mono = torch.stack([t.min(), t.max(),
+                                            (t[1:] > t[:-1]).all().to(torch.int64)]).tolist()
+                if lo < 0 or hi >= n:
+                    raise IndexError(f"row index out of range for {n} rows")
+                if not mono:
+                    t = torch.unique(t, sorted=True)
+            t = t.to(torch.int32).contiguous()
+            return t, int(t.numel())
         if isinstance(indices, torch.Tensor):
-            t = indices.to(device=self.device, dtype=torch.int32).contiguous()
-        else:
-            arr = np.asarray(indices, dtype=np.int64).reshape(-1)
-            if arr.size and (arr.min() < 0 or arr.max() >= self.n_rows):
-                raise IndexError("row index out of range")
-            t = torch.from_numpy(arr.astype(np.int32)).to(self.device, non_blocking=False)
+            indices = indices.detach().cpu().numpy()
+        arr = np.asarray(indices)
+        if arr.dtype == np.bool_:
+            if arr.ndim != 1 or arr.size != n:
+                raise IndexError(f"boolean index of shape {arr.shape} does not match {n} rows")
+            arr = np.flatnonzero(arr)
+        elif arr.size and not np.issubdtype(arr.dtype, np.integer):
+            raise IndexError("row indices must be integers or a boolean mask")
+        arr = arr.astype(np.int64).reshape(-1)
+        if arr.size:
+            arr = np.where(arr < 0, arr + n, arr)
+            if arr.min() < 0 or arr.max() >= n:
+                raise IndexError(f"row index out of range for {n} rows")
+            if not np.all(arr[1:] > arr[:-1]):
+                arr = np.unique(arr)
+        t = torch.from_numpy(arr.astype(np.int32)).to(self.device, non_blocking=False)
         return t, int(t.numel())
 
     def rsr_apply(self, groups: list[GroupBinding], indices, alpha1: float, alpha2: float,
@@ -517,12 +600,12 @@ class StepEngine:
             self._check_record(record, groups)
             rc = self.lib.gs_rsr_apply_rows(record.data_ptr(), record.stride(0),
                                             sum(g.width for g in groups),
-                                            rows.data_ptr() if k else None, k, float(alpha1),
-                                            float(alpha2), s)
+                                            rows.data_ptr() if k else None, k, self.n_rows,
+                                            float(alpha1), float(alpha2), s)
         else:
             garr = self.group_array(groups, need_grad=False)
             rc = self.lib.gs_rsr_apply(garr, len(groups), rows.data_ptr() if k else None, k,
-                                       float(alpha1), float(alpha2), s)
+                                       self.n_rows, float(alpha1), float(alpha2), s)
         L.check(rc, "gs_rsr_apply")
         self.launches += 1 if k else 0
         self._rows_tmp = rows  # keep alive until the kernel has consumed it
@@ -535,11 +618,11 @@ class StepEngine:
             self._check_record(record, groups)
             rc = self.lib.gs_reset_rows_rows(record.data_ptr(), record.stride(0),
                                              sum(g.width for g in groups),
-                                             rows.data_ptr() if k else None, k, s)
+                                             rows.data_ptr() if k else None, k, self.n_rows, s)
         else:
             garr = self.group_array(groups, need_grad=False)
             rc = self.lib.gs_reset_rows(garr, len(groups), clock.data_ptr(),
-                                        rows.data_ptr() if k else None, k, s)
+                                        rows.data_ptr() if k else None, k, self.n_rows, s)
         L.check(rc, "gs_reset_rows")
         self.launches += 1 if k else 0
         self._rows_tmp = rows

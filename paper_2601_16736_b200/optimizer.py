@@ -14,6 +14,7 @@ this module is host plumbing.  There is no CPU path.
 
 from __future__ import annotations
 
+import collections
 import math
 from dataclasses import dataclass, field
 
@@ -21,6 +22,7 @@ import numpy as np
 import torch
 
 from . import _lib as L
+from . import records as _records
 from .records import base_grad_view
 from .engine import (ConfigError, DomainError, GradientError, GroupBinding, StepEngine, row_stride,
                      round_pixel_count)
@@ -229,11 +231,13 @@ class AdamWGS:
     for record views, or from the ``grads`` mapping passed to :meth:`step`.
     """
 
+    ERROR_SLOTS = 4  # steps whose error check may be outstanding (errors="defer")
+
     def __init__(self, params, *, mode: str = "adamw-gs", betas=(0.9, 0.999), eps: float = 1e-8,
                  lambda_o: float = 0.0, lambda_s: float = 0.0, ct_opacity: float = 10.0,
                  ct_scale: float = 10.0, round_n_pixels: bool = True, check: str = "fused",
-                 errors: str = "raise", state_layout: str = "rows",
-                 state_row_align: int = 16):
+                 errors: str = "defer", state_layout: str = "rows",
+                 state_row_align: int = 16, adopt="auto"):
         validate_hyper(mode, betas[0], betas[1], eps, ct_opacity, ct_scale)
         if check not in CHECKS:
             raise ConfigError(f"check must be one of {CHECKS}")
@@ -269,16 +273,46 @@ class AdamWGS:
                 raise ConfigError(f"group {g['name']}: parameters must be fp32")
             w = max(1, int(np.prod(p.shape[1:]))) if p.dim() > 1 else 1
             row_stride(f"group {g['name']}", p, self.n_rows, w)
+        self.param_record = self.grad_record = None
+        self._maybe_adopt(adopt)
         self.state_row_align = int(state_row_align)
         self.state = MomentState.zeros_like({g["name"]: g["params"][0] for g in self.param_groups},
                                             state_layout, self.state_row_align)
         self.engine = StepEngine(self.n_rows, self.device, self.beta1, self.beta2)
-        self._stats_host = torch.zeros(L.GS_STEP_STATS, dtype=torch.float64, pin_memory=True)
-        self._abort_host = torch.zeros(1, dtype=torch.int32, pin_memory=True)
-        self._pending = None
+        # pinned slots for the asynchronous error check: a step copies its
+        # statistics (and strict abort flag) into a slot and records an
+        # event; the host inspects completed slots at the next step
+        self._slots = [(torch.zeros(L.GS_STEP_STATS, dtype=torch.float64, pin_memory=True),
+                        torch.zeros(1, dtype=torch.int32, pin_memory=True))
+                       for _ in range(self.ERROR_SLOTS)]
+        self._slot = 0
+        self._pending = collections.deque()
         self._capturing = False
         self._last_ctx = None
         self._densify = None  # (accum, count, group index) when enabled
+        # index-sharded hooks (sharded.ShardedAdamWGS): the global N_v from
+        # the local count, and the all-shard abort flag of the strict check
+        self._nv_reduce = None
+        self._abort_reduce = None
+        self._clock_bound = 0  # upper bound of every clock (and global_t): sizes the bias LUT
+
+    def _maybe_adopt(self, adopt):
+        """Per-attribute leaf parameters -> one parameter record and one
+        gradient record (records.adopt), see the class docstring."""
+        if adopt is False or adopt is None:
+            return
+        if adopt not in (True, "auto"):
+            raise ConfigError("adopt must be 'auto', True or False")
+        ps = {g["name"]: g["params"][0] for g in self.param_groups}
+        if len(ps) < 2 or _records.record_of(ps) is not None:
+            return  # already views of one record
+        if not all(p.is_leaf and p.is_contiguous() and p.device.type == "cuda" for p in ps.values()):
+            if adopt is True:
+                raise ConfigError("adopt=True needs contiguous leaf CUDA tensors")
+            return
+        if adopt == "auto" and not all(p.requires_grad for p in ps.values()):
+            return
+        self.param_record, self.grad_record = _records.adopt(ps)
 
     # ------------------------------------------------------------------ helpers
     def _bindings(self, grads=None, mu_lr_scale: float = 1.0) -> list[GroupBinding]:
@@ -333,10 +367,16 @@ class AdamWGS:
         ||grad_position|| * densify_scale and a count per stepped row, fused
         into the step (DensifyStats.observe, pipeline.py:67-91).
         """
-        self._raise_pending()
+        # deferred checks of earlier steps: only those already complete,
+        # except that a strict coupled-adam abort must roll back the clock
+        # before the next step advances it
+        self._poll(block=self.errors == "raise" or
+                   (self.mode == "coupled-adam" and self.check == "strict"))
         mode = self.mode
         b = self._bindings(grads, mu_lr_scale)
         eng = self.engine
+        self._clock_bound += 1
+        eng.ensure_lut(self._clock_bound + 1)
         lo = self.lambda_o if lambda_o is None else float(lambda_o)
         ls = self.lambda_s if lambda_s is None else float(lambda_s)
         kw = dict(eps=self.eps, check=self.check, record=self.state.record)
@@ -348,21 +388,29 @@ class AdamWGS:
         if mode == "coupled-adam":
             self.state.global_t += 1
             nv = None
-            if (lo != 0.0 or ls != 0.0):
-                if n_visible is None:
-                    if visibility is None:
-                        raise ConfigError("coupled-adam regularization needs the visibility mask")
-                    _, nv = eng.compact(visibility)
-                else:
-                    nv = n_visible
+            listed = None
+            regular = lo != 0.0 or ls != 0.0
+            if (regular and n_visible is None) or "densify" in kw:
+                if visibility is None:
+                    raise ConfigError("coupled-adam regularization and densification statistics "
+                                      "need the visibility mask")
+                vrows, vcount = eng.compact(visibility)
+                if "densify" in kw:
+                    listed = (vrows, vcount)  # observe the visible rows only (pipeline.py:338-339)
+                if regular:
+                    nv = vcount if self._nv_reduce is None else self._nv_reduce(vcount)
+            if regular and n_visible is not None:
+                nv = n_visible
             stats = eng.step(b, mode, self.state.clock, rows=None, count=None,
                              lambda_opacity=lo, lambda_scale=ls, global_t=self.state.global_t,
-                             n_visible_dev=nv, **kw)
+                             n_visible_dev=nv, abort_hook=self._abort_reduce, densify_rows=listed,
+                             **kw)
             rows = count = None
         else:
             if visibility is None:
                 raise ConfigError(f"{mode} needs the visibility mask")
             rows, count = eng.compact(visibility)
+            kw["abort_hook"] = self._abort_reduce
             if mode == "adamw-gs":
                 if n_pixels is None:
                     raise ConfigError("adamw-gs needs n_pixels (N_I)")
@@ -380,37 +428,55 @@ class AdamWGS:
                                  lambda_opacity=lo, lambda_scale=ls, clip_opacity=cv,
                                  clip_scale=cv, **kw)
             else:  # sparse-adam (+ coupled)
+                nv = n_visible
+                if nv is None:
+                    nv = count if (self._nv_reduce is None or (lo == 0.0 and ls == 0.0)) \
+                        else self._nv_reduce(count)
                 stats = eng.step(b, mode, self.state.clock, rows=rows, count=count,
-                                 lambda_opacity=lo, lambda_scale=ls,
-                                 n_visible_dev=count if n_visible is None else n_visible, **kw)
+                                 lambda_opacity=lo, lambda_scale=ls, n_visible_dev=nv, **kw)
         self._last_ctx = (b, rows, count, lo, ls, mode)
         self._after_step(stats)
 
     # ---------------------------------------------------------------- errors
     def _after_step(self, stats: torch.Tensor):
-        if self.errors == "ignore":
-            return
-        self._stats_host.copy_(stats, non_blocking=True)
-        abort = None
-        if self.check == "strict":
-            self._abort_host.copy_(self.engine.abort, non_blocking=True)
-            abort = self._abort_host
-        if self._capturing:  # StepGraph.replay() arms the check after each replay
-            return
-        ev = torch.cuda.Event()
-        ev.record(torch.cuda.current_stream(self.device))
-        self._pending = (ev, abort)
-        if self.errors == "raise":
-            self._raise_pending()
+        if self.errors == "ignore" or self._capturing:
+            return  # (StepGraph.replay() enqueues the check after each replay)
+        self._enqueue_check()
 
-    def _arm_after_replay(self):
-        if self.errors == "ignore":
-            return
+    def _enqueue_check(self):
+        """Copy this step's statistics (and strict abort flag) into a pinned
+        slot and record an event; no host synchronisation unless every slot
+        is still outstanding (the host is ERROR_SLOTS steps ahead)."""
+        if len(self._pending) >= self.ERROR_SLOTS:
+            self._poll(block=True, limit=1)
+        st_host, ab_host = self._slots[self._slot]
+        self._slot = (self._slot + 1) % self.ERROR_SLOTS
+        st_host.copy_(self.engine.stats, non_blocking=True)
+        strict = self.check == "strict"
+        if strict:
+            ab_host.copy_(self.engine.abort, non_blocking=True)
         ev = torch.cuda.Event()
         ev.record(torch.cuda.current_stream(self.device))
-        self._pending = (ev, self._abort_host if self.check == "strict" else None)
+        self._pending.append((ev, st_host, ab_host if strict else None, self._last_ctx))
         if self.errors == "raise":
-            self._raise_pending()
+            self._poll(block=True)
+
+    def _poll(self, block: bool, limit: int | None = None):
+        """Inspect the outstanding step checks in order; raise the first
+        error.  ``block=False`` stops at the first step still running."""
+        n = 0
+        while self._pending and (limit is None or n < limit):
+            ev = self._pending[0][0]
+            if not block and not ev.query():
+                return
+            _, st_host, ab_host, ctx = self._pending.popleft()
+            ev.synchronize()
+            n += 1
+            self._raise_for(_stats_dict(st_host.tolist()),
+                            int(ab_host.item()) if ab_host is not None else 0, ctx)
+
+    def _raise_pending(self):
+        self._poll(block=True)
 
     # ------------------------------------------------------ structural ops
     def rebind(self, params: dict, state: "MomentState | None" = None):
@@ -439,6 +505,9 @@ class AdamWGS:
         for g in self.param_groups:
             g["params"] = [params[g["name"]]]
         self.state = state
+        if n:
+            self._clock_bound = max(self._clock_bound, int(state.clock.max().item()),
+                                    state.global_t)
         if n != self.n_rows:
             self.n_rows = n
             self.engine = StepEngine(n, self.device, self.beta1, self.beta2)
@@ -516,31 +585,35 @@ class AdamWGS:
         if self.mode == "coupled-adam":
             raise ConfigError("coupled-adam advances a host-side global clock; capture the "
                               "sparse modes")
+        # replays advance the clocks without the host: the captured bias
+        # table must be exact for every clock
+        self.engine.ensure_lut(self.engine.lut_exact_len)
         return StepGraph(self, visibility, n_pixels, grads, step_kwargs)
 
-    def _raise_pending(self):
-        if self._pending is None:
-            return
-        ev, abort = self._pending
-        self._pending = None
-        ev.synchronize()
-        st = _stats_dict(self._stats_host.tolist())
-        flag = int(abort.item()) if abort is not None else 0
+    def _raise_for(self, st: dict, flag: int, ctx):
+        if flag and self.mode == "coupled-adam":
+            # the strict check aborted the step before any mutation: the
+            # reference checks before advancing the clock (optimizer.py:225-226)
+            self.state.global_t -= 1
         bad_g = st["n_bad_grad"] > 0 or (flag & 1)
         bad_d = st["n_bad_domain"] > 0 or (flag & 2)
         if not (bad_g or bad_d):
             return
-        b, rows, count, lo, ls, mode = self._last_ctx
+        self._pending.clear()  # later steps' checks are superseded by this error
+        b, rows, count, lo, ls, mode = ctx
         if mode == "coupled-adam":
             rows, count = self.engine.all_rows()
+        # ids from the failing step's gradient bindings (deferred: the caller
+        # keeps those buffers until the error surfaces, or uses errors="raise")
         g_ids, d_ids = self.engine.bad_rows(b, rows, count, lo, ls)
         if bad_g:
             raise GradientError(g_ids)
         raise DomainError("tau must be finite / log-scale above 80.0 would overflow", d_ids)
 
     def check_errors(self):
-        """Raise a deferred GradientError / DomainError of the last step, if any."""
-        self._raise_pending()
+        """Wait for the outstanding steps and raise a deferred GradientError /
+        DomainError, if any."""
+        self._poll(block=True)
 
     def last_stats(self) -> dict:
         """Per-step statistics of the last step (host sync)."""
@@ -694,6 +767,8 @@ class AdamWGS:
                 self.state.v[k].copy_(sd["v"][k])
         # (views into the row record are written in place)
         self.state.global_t = int(sd["global_t"])
+        clock = sd["clock"]
+        self._clock_bound = max(int(clock.max()) if clock.numel() else 0, self.state.global_t)
 
 
 def _moment_stats(engine: StepEngine, bindings, alive, record=None) -> dict:
@@ -742,8 +817,9 @@ class StepGraph:
     def replay(self):
         """One optimizer step on the current contents of the static buffers."""
         opt = self.opt
-        opt._raise_pending()
+        opt._poll(block=opt.errors == "raise")
         self.graph.replay()
         opt.engine.launches += self.launches_per_replay
-        opt._arm_after_replay()
+        if opt.errors != "ignore":
+            opt._enqueue_check()
 

@@ -62,6 +62,13 @@ def _engine(n_rows: int, device, beta1: float, beta2: float) -> StepEngine:
     return eng
 
 
+def _cover_clocks(eng: StepEngine, state: MomentState, ahead: int) -> None:
+    """Size the engine's bias LUT for the state's clocks (this shim is
+    synchronous anyway; the caller owns the state and may edit it)."""
+    t = int(state.clock.max().item()) if len(state) else 0
+    eng.ensure_lut(max(t, state.global_t) + ahead + 1)
+
+
 def _get(obj, name):
     return obj[name] if isinstance(obj, dict) else getattr(obj, name)
 
@@ -95,6 +102,7 @@ def _run(mode, state, pset, grads, vis, cfg, *, mu_lr_scale=1.0, lam_o=0.0, lam_
     dev = state.clock.device
     eng = _engine(n, dev, cfg.beta1, cfg.beta2)
     b = _bindings(state, pset, grads, cfg, mu_lr_scale)
+    _cover_clocks(eng, state, 1)
     if mode == "coupled-adam":
         rows = count = None
         nv = None
@@ -254,6 +262,7 @@ def aiu_apply(state, pset, vis, cfg, aiu, rng, iteration: int, alive=None) -> np
     if alive is not None and not isinstance(alive, torch.Tensor):
         alive = torch.from_numpy(np.asarray(alive, dtype=bool)).to(state.clock.device)
     prob, eta = aiu.prob_at(iteration), aiu.eta_at(iteration)
+    _cover_clocks(eng, state, 0)
     inv_idx, inv_cnt = eng.compact_select(vis_t, alive, invert=True)
     n_inv = int(inv_cnt.item())
     if n_inv == 0 or prob <= 0.0 or eta == 0.0:

@@ -1,0 +1,288 @@
+"""Drop-in behaviour of AdamWGS on the GPU (marked gpu): deferred errors with
+no host synchronisation, NumPy index semantics of the state scatters,
+visible-only densification statistics in the dense mode, automatic record
+adoption of per-attribute parameters, and the 2-D TMA record kernel on bad
+rows and ragged chunks."""
+
+import time
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import adamw_gs_oracle as O
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda:0"
+
+
+def _cloud(n, p=0.3, seed=1):
+    from paper_2601_16736_b200 import synthetic as S
+    cfg = S.WorkloadConfig(n=n, p_vis=p, seed=seed)
+    return cfg, S.make_params(cfg)
+
+
+def _fp32_state(host, n):
+    lay = O.LAYOUT_SH3
+    return ({k: v.copy() for k, v in host.items()},
+            {g.name: np.zeros((n, g.width), np.float32) for g in lay},
+            {g.name: np.zeros((n, g.width), np.float32) for g in lay},
+            np.zeros(n, np.int32))
+
+
+# --------------------------------------------------------------------------
+# errors="defer" (default): no host synchronisation inside step()
+# --------------------------------------------------------------------------
+
+def test_default_step_never_waits_for_the_gpu():
+    """With the default deferred error check, step() only enqueues work: with
+    the GPU held busy by a ~0.5 s sleep kernel, three steps return to the
+    host long before the GPU has finished, and torch's sync debug mode sees
+    no synchronising call."""
+    from paper_2601_16736_b200 import records as R
+    from paper_2601_16736_b200 import synthetic as S
+    from paper_2601_16736_b200.optimizer import AdamWGS
+    cfg, host = _cloud(200_003)
+    _, params = R.pack({k: torch.from_numpy(v).to(DEV) for k, v in host.items()})
+    opt = AdamWGS(S.param_groups(params), mode="adamw-gs", lambda_o=1e-3, lambda_s=1e-5)
+    assert opt.errors == "defer"
+    _, grads = R.pack({k: torch.from_numpy(x).to(DEV) for k, x in
+                       S.step_grads(cfg, 0, S.visibility(cfg, 0)).items()})
+    masks = [torch.from_numpy(S.visibility(cfg, s)).to(DEV) for s in range(3)]
+    opt.step(masks[0], cfg.n_pixels, grads=grads)  # warm the host caches
+    opt.check_errors()
+    torch.cuda.synchronize()
+    torch.cuda._sleep(1_000_000_000)  # ~0.5 s of GPU time ahead of the steps
+    t0 = time.perf_counter()
+    torch.cuda.set_sync_debug_mode("error")
+    try:
+        for s in range(3):
+            opt.step(masks[s], cfg.n_pixels, grads=grads)
+    finally:
+        torch.cuda.set_sync_debug_mode(0)
+    host_s = time.perf_counter() - t0
+    t1 = time.perf_counter()
+    torch.cuda.synchronize()
+    gpu_left = time.perf_counter() - t1
+    assert gpu_left > 0.1, "the sleep kernel did not keep the GPU busy"
+    assert host_s < 0.5 * gpu_left, (host_s, gpu_left)
+    opt.check_errors()
+
+
+def test_deferred_error_surfaces_at_check_with_ids():
+    """A non-finite gradient under errors="defer": the step returns, the
+    error (with the reference's row ids, gradients.py:50-58) surfaces at
+    check_errors(); the bad row is untouched and the others stepped."""
+    from paper_2601_16736_b200 import synthetic as S
+    from paper_2601_16736_b200.engine import GradientError
+    from paper_2601_16736_b200.optimizer import AdamWGS
+    cfg, host = _cloud(10_007)
+    params = {k: torch.from_numpy(v).to(DEV) for k, v in host.items()}
+    opt = AdamWGS(S.param_groups(params), mode="adamw-gs", lambda_o=1e-3, lambda_s=1e-5)
+    vis = S.visibility(cfg, 0)
+    g = {k: torch.from_numpy(x).to(DEV) for k, x in S.step_grads(cfg, 0, vis).items()}
+    bad = int(np.flatnonzero(vis)[3])
+    g["xyz"][bad, 1] = float("inf")
+    opt.step(torch.from_numpy(vis).to(DEV), cfg.n_pixels, grads=g)
+    with pytest.raises(GradientError) as ei:
+        opt.check_errors()
+    assert ei.value.ids.tolist() == [bad]
+    clock = opt.state.clock.cpu().numpy()
+    assert clock[bad] == 0 and clock.sum() == vis.sum() - 1
+    opt.check_errors()  # reported once
+
+
+def test_strict_abort_rolls_back_the_coupled_global_clock():
+    """coupled-adam + strict: an aborted step mutates nothing and does not
+    advance global_t (the reference checks before the increment,
+    optimizer.py:225-226); the next step uses the right bias correction."""
+    from paper_2601_16736_b200 import synthetic as S
+    from paper_2601_16736_b200.engine import GradientError
+    from paper_2601_16736_b200.optimizer import AdamWGS
+    cfg, host = _cloud(5_003)
+    params = {k: torch.from_numpy(v).to(DEV) for k, v in host.items()}
+    opt = AdamWGS(S.param_groups(params), mode="coupled-adam", check="strict")
+    vis = S.visibility(cfg, 0)
+    g = {k: torch.from_numpy(x).to(DEV) for k, x in S.step_grads(cfg, 0, vis).items()}
+    opt.step(torch.from_numpy(vis).to(DEV), grads=g)
+    g["f_rest"][17, 3] = float("nan")  # an invisible row: the all-row check still aborts
+    before = {k: p.clone() for k, p in params.items()}
+    opt.step(torch.from_numpy(vis).to(DEV), grads=g)
+    with pytest.raises(GradientError):
+        opt.check_errors()
+    assert opt.state.global_t == 1
+    for k in params:
+        assert torch.equal(params[k], before[k])
+
+
+# --------------------------------------------------------------------------
+# K3 index semantics (NumPy fancy indexing)
+# --------------------------------------------------------------------------
+
+@pytest.mark.parametrize("kind", ["bool", "negative", "duplicates", "torch-dup", "torch-neg"])
+def test_state_scatter_index_semantics(kind):
+    """rsr_apply / reset_rows take indices as the reference's NumPy
+    assignment does: a boolean mask selects its rows, negative ids count
+    from the end, a repeated id acts once; out-of-range ids raise."""
+    from paper_2601_16736_b200 import synthetic as S
+    from paper_2601_16736_b200.optimizer import AdamWGS
+    cfg, host = _cloud(4_099)
+    n = cfg.n
+    params = {k: torch.from_numpy(v).to(DEV) for k, v in host.items()}
+    opt = AdamWGS(S.param_groups(params), mode="adamw-gs", lambda_o=1e-3, lambda_s=1e-5)
+    for s in range(2):
+        vis = S.visibility(cfg, s)
+        opt.step(torch.from_numpy(vis).to(DEV), cfg.n_pixels,
+                 grads={k: torch.from_numpy(x).to(DEV) for k, x in S.step_grads(cfg, s, vis).items()})
+    rng = np.random.default_rng(7)
+    sel = np.sort(rng.choice(n, 300, replace=False))
+    if kind == "bool":
+        idx = np.zeros(n, bool)
+        idx[sel] = True
+    elif kind == "negative":
+        idx = np.where(np.arange(sel.size) % 2 == 0, sel - n, sel)
+    elif kind == "duplicates":
+        idx = np.concatenate([sel, sel[::3]])[::-1]
+    elif kind == "torch-dup":
+        idx = torch.from_numpy(np.concatenate([sel, sel[:50]])).to(DEV)
+    else:
+        idx = torch.from_numpy(sel - n).to(DEV)
+    m0 = {k: t.contiguous().cpu().numpy().astype(np.float64) for k, t in opt.state.m.items()}
+    v0 = {k: t.contiguous().cpu().numpy().astype(np.float64) for k, t in opt.state.v.items()}
+    opt.rsr_apply(idx, 0.2, 0.04)
+    m_ref = {k: x.copy() for k, x in m0.items()}
+    v_ref = {k: x.copy() for k, x in v0.items()}
+    O.rsr_apply_f64(O.LAYOUT_SH3, m_ref, v_ref, sel, 0.2, 0.04)
+    for k in m_ref:
+        assert np.array_equal(opt.state.m[k].contiguous().cpu().numpy(), m_ref[k].astype(np.float32))
+        assert np.array_equal(opt.state.v[k].contiguous().cpu().numpy(), v_ref[k].astype(np.float32))
+    clock0 = opt.state.clock.cpu().numpy().copy()
+    opt.reset_rows(idx)
+    clock = opt.state.clock.cpu().numpy()
+    want = clock0.copy()
+    want[sel] = 0
+    assert np.array_equal(clock, want)
+    for bad in (np.array([n]), np.array([-n - 1]), torch.tensor([n + 5], device=DEV)):
+        with pytest.raises(IndexError):
+            opt.rsr_apply(bad, 0.2, 0.04)
+    with pytest.raises(IndexError):
+        opt.reset_rows(np.zeros(n + 1, bool))
+
+
+# --------------------------------------------------------------------------
+# dense coupled-adam: densification statistics observe visible rows only
+# --------------------------------------------------------------------------
+
+@pytest.mark.parametrize("check", ["fused", "strict"])
+def test_coupled_adam_densify_stats_visible_rows_only(check):
+    """DensifyStats.observe(grads.mu, vis, scale) (pipeline.py:338-339) touches
+    only visible rows, also in the dense coupled-adam mode whose step
+    updates every row: accum / count bit-exact vs the fp32 order over the
+    visible lists."""
+    from paper_2601_16736_b200 import synthetic as S
+    from paper_2601_16736_b200.optimizer import AdamWGS
+    cfg, host = _cloud(30_011)
+    params = {k: torch.from_numpy(v).to(DEV) for k, v in host.items()}
+    opt = AdamWGS(S.param_groups(params), mode="coupled-adam", lambda_o=0.01, lambda_s=0.001,
+                  check=check)
+    opt.enable_densify_stats()
+    acc = np.zeros(cfg.n, np.float32)
+    cnt = np.zeros(cfg.n, np.int32)
+    for s in range(3):
+        vis = S.visibility(cfg, s)
+        g = S.step_grads(cfg, s, vis)
+        opt.step(torch.from_numpy(vis).to(DEV), grads={k: torch.from_numpy(x).to(DEV)
+                                                       for k, x in g.items()},
+                 densify_scale=0.5)
+        O.densify_observe_fp32(g["xyz"], np.flatnonzero(vis), acc, cnt, 0.5)
+    a, c = opt.densify_stats()
+    assert np.array_equal(c.cpu().numpy(), cnt)
+    assert np.array_equal(a.cpu().numpy(), acc)
+
+
+# --------------------------------------------------------------------------
+# adopt="auto": per-attribute nn.Parameters get the record kernel
+# --------------------------------------------------------------------------
+
+def test_auto_adopt_parameters_bit_exact_and_on_records():
+    from paper_2601_16736_b200 import synthetic as S
+    from paper_2601_16736_b200.optimizer import AdamWGS
+    cfg, host = _cloud(20_011)
+    n = cfg.n
+    params = {k: torch.nn.Parameter(torch.from_numpy(v).to(DEV)) for k, v in host.items()}
+    ids = {k: id(p) for k, p in params.items()}
+    opt = AdamWGS(S.param_groups(params), mode="adamw-gs", lambda_o=1e-3, lambda_s=1e-5)
+    assert opt.param_record is not None and opt.grad_record is not None
+    assert all(id(p) == ids[k] for k, p in params.items())          # same Parameter objects
+    assert all(p.stride(0) == 64 and p.grad.stride(0) == 64 for p in params.values())
+    lay = O.LAYOUT_SH3
+    hp = O.Hyper(lr=S.LR_SH3, lambda_o=1e-3, lambda_s=1e-5)
+    p32, m32, v32, c32 = _fp32_state(host, n)
+    for s in range(4):
+        vis = S.visibility(cfg, s)
+        g = S.step_grads(cfg, s, vis)
+        opt.zero_grad()
+        loss = sum((p * torch.from_numpy(g[k]).to(DEV).view(p.shape)).sum()
+                   for k, p in params.items())
+        loss.backward()
+        opt.step(torch.from_numpy(vis).to(DEV), cfg.n_pixels)
+        O.step_fp32("adamw-gs", lay, p32, g, m32, v32, c32, np.flatnonzero(vis), hp,
+                    n_pixels=cfg.n_pixels)
+    opt.check_errors()
+    for k in host:
+        assert np.array_equal(params[k].detach().cpu().numpy(), p32[k]), k
+        assert np.array_equal(opt.state.v[k].contiguous().cpu().numpy(), v32[k]), k
+    assert np.array_equal(opt.state.clock.cpu().numpy(), c32)
+    plain = {k: torch.from_numpy(v).to(DEV) for k, v in host.items()}
+    assert AdamWGS(S.param_groups(plain)).param_record is None        # plain tensors: untouched
+
+
+# --------------------------------------------------------------------------
+# the 2-D TMA record kernel: ragged chunks, bad rows, every mode
+# --------------------------------------------------------------------------
+
+@pytest.mark.parametrize("n", [1, 31, 33, 4_099, 70_001])
+@pytest.mark.parametrize("mode", ["adamw-gs", "sparse-adam", "adamw-const-clip", "coupled-adam"])
+def test_tma_record_kernel_ragged_and_bad_rows(n, mode):
+    """Records (TMA path) vs the cp.async ring (GS_FIXED_VARIANT 21) and the
+    fp32 order: ragged last chunks (rows past the list are out of the
+    tensor maps' bounds), a non-finite gradient row and a kappa > 80 row are
+    skipped whole and left bit-identical, statistics agree."""
+    from paper_2601_16736_b200 import _lib
+    from paper_2601_16736_b200 import records as R
+    from paper_2601_16736_b200 import synthetic as S
+    from paper_2601_16736_b200.optimizer import AdamWGS
+    lib = _lib.load()
+    cfg, host = _cloud(n, p=0.6, seed=n)
+    vis = S.visibility(cfg, 0)
+    vis[0] = True
+    rows = np.flatnonzero(vis)
+    g = S.step_grads(cfg, 0, vis)
+    if rows.size > 2:
+        g["f_rest"][rows[1], 44] = float("nan")
+        host = {k: v.copy() for k, v in host.items()}
+        host["scaling"][rows[-1], 2] = 81.0
+    outs = []
+    prev = lib.gs_set_fixed_variant(0)
+    try:
+        for variant in (0, 21):
+            lib.gs_set_fixed_variant(variant)
+            _, params = R.pack({k: torch.from_numpy(v).to(DEV) for k, v in host.items()})
+            _, gr = R.pack({k: torch.from_numpy(x).to(DEV) for k, x in g.items()})
+            opt = AdamWGS(S.param_groups(params), mode=mode, lambda_o=1e-3, lambda_s=1e-5,
+                          errors="ignore")
+            for _ in range(2):
+                opt.step(torch.from_numpy(vis).to(DEV), cfg.n_pixels, grads=gr)
+            outs.append(({k: p.cpu().numpy() for k, p in params.items()},
+                         opt.state.record.cpu().numpy(), opt.last_stats()))
+    finally:
+        lib.gs_set_fixed_variant(prev)
+    (pa, ra, sa), (pb, rb, sb) = outs
+    for k in pa:
+        assert np.array_equal(pa[k], pb[k]), k
+    assert np.array_equal(ra[:, :120].view(np.int32), rb[:, :120].view(np.int32))
+    assert sa == sb
+    if rows.size > 2 and mode != "coupled-adam":
+        for k in pa:
+            assert np.array_equal(pa[k][rows[1]], host[k][rows[1]])
+        assert sa["n_bad_grad"] == 1 and sa["n_bad_domain"] == 1

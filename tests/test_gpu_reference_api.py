@@ -442,7 +442,7 @@ def test_optimizer_error_semantics(check):
     host = S.make_params(cfg)
     params = {k: torch.from_numpy(v).to(DEV) for k, v in host.items()}
     opt = AdamWGS(S.param_groups(params), mode="adamw-gs", lambda_o=1e-3, lambda_s=1e-5,
-                  check=check)
+                  check=check, errors="raise")
     vis = S.visibility(cfg, 0)
     g = {k: torch.from_numpy(x).to(DEV) for k, x in S.step_grads(cfg, 0, vis).items()}
     bad_row = int(np.flatnonzero(vis)[7])
@@ -471,8 +471,9 @@ def test_optimizer_error_semantics(check):
 @pytest.mark.parametrize("check", ["fused", "strict"])
 def test_step_kernels_all_identical(mode, check):
     """Every K2 implementation, tuning variant and parameter layout gives the
-    same bits: the fixed-layout SH-3 kernels (variants 0..6), the generic
-    row-record kernel (variants 0..6) and the per-group-state kernel, with
+    same bits: the fixed-layout SH-3 kernels (2-D TMA, cp.async ring,
+    per-attribute gathers, plus the measured alternatives when built), the
+    generic row-record kernel (variants 0..6) and the per-group-state kernel, with
     per-attribute tensors, with parameters and gradients as views of
     row-interleaved records (records.py), and with only the parameters in a
     record (strided gathers)."""
@@ -484,17 +485,18 @@ def test_step_kernels_all_identical(mode, check):
     cfg = S.WorkloadConfig(n=20_011, p_vis=0.4, seed=9)
     host = S.make_params(cfg)
     results = []
-    runs = [("fixed", v, "attr") for v in (*range(8), 19)] + [("rows", v, "attr") for v in range(7)]
+    runs = [("fixed", 0, "attr")] + [("rows", v, "attr") for v in range(7)]
     runs += [("groups", 0, "attr")]
+    # record layouts: fixed 0 = the 2-D TMA gather4 / scatter4 kernel, 21 = the
+    # cp.async ring kernel; "param-record" = only the parameters in a record
     runs += [(k, 0, lay) for k in ("fixed", "rows", "groups") for lay in ("record", "param-record")]
-    # record layouts: 0/13/14 = record kernel shapes, 8 = record gathers in the generic ring,
-    # 9/10/12 = bulk-copy (TMA) kernels,
-    # 11 = cp.async gathers + bulk stores, 16-19 = ring depth / warp splits,
-    # 20 = ring kernel without the L2 prefetch-size hint
-    runs += [("fixed", v, "record") for v in (8, 9, 10, 11, 12, 13, 14, 16, 17, 18, 19, 20)]
+    runs += [("fixed", 21, "record")]
+    if lib.gs_build_flags() & 1:  # measured alternatives compiled in (-DGS_BUILD_VARIANTS=1)
+        runs += [("fixed", v, "attr") for v in (1, 2, 3, 4, 5, 6, 7, 19)]
+        runs += [("fixed", v, "record") for v in (8, 9, 10, 11, 12, 13, 14, 16, 17, 18, 19, 20)]
     runs += [(k, 0, "record240") for k in ("fixed", "rows")]  # compact 240-byte rows
     if check == "strict":
-        runs = [r for r in runs if r[1] in (0, 3, 7, 8, 11, 12)]
+        runs = [r for r in runs if r[1] in (0, 3, 7, 8, 11, 12, 21)]
     prev_f = lib.gs_set_fixed_variant(0)
     prev_r = lib.gs_set_rows_variant(0)
     try:
@@ -665,7 +667,7 @@ def test_captured_step_graph_matches_eager(mode, check):
     for how in ("eager", "graph"):
         _, params = R.pack({k: torch.from_numpy(v).to(DEV) for k, v in host.items()})
         opt = AdamWGS(S.param_groups(params), mode=mode, lambda_o=1e-3, lambda_s=1e-5,
-                      check=check)
+                      check=check, errors="raise")
         grec, grads = R.pack({k: torch.zeros(v.shape, device=DEV) for k, v in host.items()})
         vis_buf = torch.zeros(cfg.n, dtype=torch.bool, device=DEV)
         graph = opt.capture(vis_buf, cfg.n_pixels, grads=grads) if how == "graph" else None
