@@ -6,21 +6,28 @@
 A *step* is one pass of the hot path over one batch of synthetic input:
 visibility compaction (K1) + the fused AdamW-GS step (K2, with the per-step
 statistics) + the Re-State Regularization scatter on RSR boundaries (K3),
-exactly as ``run_training`` composes them (pipeline.py:316-370).
+exactly as ``run_training`` composes them (pipeline.py:316-370), through the
+public optimizer (``AdamWGS.step``; ``ShardedAdamWGS.step`` on N > 1 GPUs,
+which adds the statistics all-reduce).
 
-Default workload (N=1): BASELINE.json configs[2] — 6M Gaussians, SH-3,
+Default workload: BASELINE.json configs[2] — 6M Gaussians per GPU, SH-3,
 30% i.i.d. visibility, full AdamW-GS (DAR lambda_o=1e-3, lambda_s=1e-5,
-N_I=1e6) with RSR (ratio 0.25, alpha 0.2/0.04, interval 100).  Multi-GPU
-runs shard rows by contiguous index; each rank owns the workload's N rows
-(weak scaling) and the per-step statistics are summed over ranks with one
-NCCL all-reduce.
+N_I=1e6) with RSR (ratio 0.25, alpha 0.2/0.04, interval 100); N GPUs own
+N index shards of 6M rows each (weak scaling; ``--strong`` splits one cloud).
+Every line also carries the north star's scaling cloud as extra legs:
+``c5_strong`` = 50M Gaussians in total split over the N GPUs (strong
+scaling) at 30% and at 1% visibility.
+
+``--gpus N`` without torchrun launches N ranks itself (torch.distributed.run,
+127.0.0.1); under torchrun N must equal WORLD_SIZE.
 
 ``value``  visible Gaussians updated / s, inputs resident in HBM, device time
-           (CUDA events on the launching stream, max over ranks).
+           (CUDA events on the launching stream around one CUDA graph of the
+           K steps, max over ranks), RSR amortised at its interval.
 ``e2e``    the same metric through the public API with host buffers: per
-           step the mask is copied H2D from pinned memory, the step kernel
-           gathers the visible rows' gradients zero-copy from pinned host
-           memory, and the step statistics are read back D2H (the dense
+           step a fresh mask is copied H2D from pinned memory, the step
+           kernel gathers the visible rows' gradients zero-copy from pinned
+           host memory, and the step statistics are read back D2H (the dense
            H2D-copy variant is reported beside it as ``dense_copy``).
 ``roofline`` the fused step kernel (K2): algorithmic bytes per launch /
            its CUDA-event duration vs the measured HBM copy peak.
@@ -34,6 +41,7 @@ import argparse
 import json
 import math
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -79,7 +87,10 @@ def parse():
     ap.add_argument("--check", default="fused", choices=["fused", "strict"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-legs", action="store_true", help="skip the c5 strong-scaling legs")
+    ap.add_argument("--sharded", action="store_true",
+                    help="run ShardedAdamWGS (NCCL process group) even on one GPU")
+    ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-seconds", type=float, default=150.0,
                     help="budget of the whole --impl reference run")
@@ -97,8 +108,6 @@ def parse():
     ap.add_argument("--host-record-align", type=int, default=16,
                     help="e2e: pinned host gradient record rows padded to a multiple of this "
                          "many floats (16: 256-byte SH-3 rows, two PCIe read lines)")
-    ap.add_argument("--unified", action="store_true",
-                    help="experiment: moment record and parameter row in one row")
     ap.add_argument("--params", default="record", choices=["record", "attr"],
                     help="parameter / gradient HBM layout: attribute views of one "
                          "row-interleaved record (records.py) or one tensor per attribute")
@@ -319,11 +328,14 @@ def reference_arm(args, wl, p_vis):
     print(json.dumps(line), flush=True)
 
 
-def workload_config(args, wl, p_vis, world):
-    n = args.n if args.n is not None else wl["n"]
-    return {"workload": f"{args.workload}: {wl['desc']}", "n_per_gpu": n // world if args.strong
-            else n, "n_total": n if args.strong else n * world, "p_visible": p_vis,
-            "mask": args.mask, "mode": wl["mode"], "layout": "SH3 (59 fp32 / Gaussian)",
+def workload_config(args, wl, p_vis, world, strong=None, mask=None):
+    strong = args.strong if strong is None else strong
+    mask = args.mask if mask is None else mask
+    n = wl["n"]
+    return {"workload": f"{wl['name']}: {wl['desc']}",
+            "n_per_gpu": n // world if strong else n, "n_total": n if strong else n * world,
+            "p_visible": p_vis, "mask": mask, "mode": wl["mode"],
+            "layout": "SH3 (59 fp32 / Gaussian)",
             "lambda_o": wl["lo"], "lambda_s": wl["ls"], "n_pixels": 1_000_000,
             "rsr": {"ratio": RSR_RATIO, "alpha1": ALPHA1, "alpha2": ALPHA2,
                     "interval": RSR_INTERVAL} if wl["rsr"] else None,
@@ -334,11 +346,12 @@ def workload_config(args, wl, p_vis, world):
                              f") fp32 row record, gradients likewise; moment record rows of "
                              f"{(120 + args.state_align - 1) // args.state_align * args.state_align * 4}"
                              f" B)") if args.params == "record" else "one tensor per attribute",
-            "l2": "inputs larger than L2 (working set >> 126 MB)" if l2_replicas(n, p_vis) == 1
+            "l2": "inputs larger than L2 (working set >> 126 MB)"
+                  if l2_replicas(n // world if strong else n, p_vis) == 1
                   else f"{l2_replicas(n, p_vis)} independent clouds of this size stepped round "
                        "robin, so each step's rows are L2-cold (>= 4x L2 of traffic between uses)",
-            "parallelism": f"index-sharded x{world}",
-            "launch": "CUDA graph of the K timed steps" if (args.graph and world == 1) else "eager"}
+            "parallelism": f"index-sharded x{world} ({'strong' if strong else 'weak'})",
+            "launch": "one CUDA graph of the K timed steps per rank" if args.graph else "eager"}
 
 
 L2_BYTES = 126 * 2**20
@@ -354,156 +367,183 @@ def l2_replicas(n, p_vis):
 
 
 # --------------------------------------------------------------- our arm
-def ours(args, wl, p_vis):
-    import numpy as np
+class Workload:
+    """One rank's shard of a benchmark cloud: optimizers (replicas for small
+    clouds), gradient records, per-step masks and the RSR / reset samples."""
+
+    def __init__(self, args, wl, p_vis, rank, world, dev, strong, mask, steps, warmup):
+        import numpy as np
+        import torch
+
+        from paper_2601_16736_b200 import records as R
+        from paper_2601_16736_b200 import synthetic as S
+        from paper_2601_16736_b200.optimizer import AdamWGS
+        from paper_2601_16736_b200.sampling import StSSchedule, shard_rows, stream, stss_sample
+        from paper_2601_16736_b200.sharded import ShardedAdamWGS, shard_range
+
+        self.wl, self.world, self.dev, self.args = wl, world, dev, args
+        n_total = wl["n"] * (1 if strong else world)
+        lo, hi = shard_range(n_total, rank, world)
+        n = hi - lo
+        self.n, self.n_total, self.lo = n, n_total, lo
+        seed = args.seed * 1000 + rank
+        self.cfg = S.WorkloadConfig(n=n, p_vis=p_vis, mask_family=mask, seed=seed,
+                                    lambda_o=wl["lo"], lambda_s=wl["ls"])
+        self.n_rep = l2_replicas(n, p_vis)
+        kw = dict(mode=wl["mode"], lambda_o=wl["lo"], lambda_s=wl["ls"], check=args.check,
+                  errors="ignore", state_layout=args.layout, state_row_align=args.state_align,
+                  adopt=False)
+        self.opts, self.shards, self.grad_sets = [], [], []
+        for j in range(self.n_rep):
+            cj = S.WorkloadConfig(n=n, p_vis=p_vis, mask_family=mask,
+                                  seed=seed * 1000 + j if j else seed, lambda_o=wl["lo"],
+                                  lambda_s=wl["ls"])
+            params = S.make_params_device(cj, dev)
+            if args.params == "record":
+                _, params = R.pack(params, align=args.record_align)
+            if world > 1 or args.sharded:
+                sh = ShardedAdamWGS(S.param_groups(params), n_total, **kw)
+                self.shards.append(sh)
+                self.opts.append(sh.opt)
+            else:
+                self.opts.append(AdamWGS(S.param_groups(params), **kw))
+                self.shards.append(None)
+            gs = [S.grads_device(cj, s, dev) for s in range(2 if self.n_rep == 1 else 1)]
+            if args.params == "record":
+                gs = [R.pack(g, align=args.record_align)[1] for g in gs]
+            self.grad_sets.append(gs)
+        self.total = warmup + steps
+        self.warmup, self.steps = warmup, steps
+        self.masks = [S.visibility_device(self.cfg, s, dev) for s in range(self.total)]
+        self.n_vis = torch.stack([m.sum() for m in self.masks]).cpu().numpy().astype(np.int64)
+        # RSR / relocation samples: host-drawn with the reference RNG contract
+        # (optimizer.py:379-386, rng.py:17-30), sliced per shard, uploaded
+        # before timing (rank-identical global draws, SURVEY §8(e))
+        self.events = {}
+        sched = StSSchedule(milestones=((0, RSR_RATIO),), interval=RSR_INTERVAL)
+        for it in range(self.total):
+            boundary = it + 1
+            if boundary % RSR_INTERVAL:
+                continue
+            self.events[it] = self._event(boundary, sched, stss_sample, stream, shard_rows)
+        self.rsr_probe = (self._event(RSR_INTERVAL, sched, stss_sample, stream, shard_rows)
+                          if (wl["rsr"] or wl["reset"]) else None)
+
+    def _event(self, boundary, sched, stss_sample, stream, shard_rows):
+        import numpy as np
+        import torch
+        ev = {}
+        hi = self.lo + self.n
+        if self.wl["rsr"]:
+            picked = stss_sample(sched, boundary, self.n_total,
+                                 stream(self.args.seed, "stss", boundary))
+            ev["rsr"] = torch.from_numpy(shard_rows(picked, self.lo, hi).astype(np.int32)).to(
+                self.dev)
+        if self.wl["reset"]:
+            rng = stream(self.args.seed, "relocate", boundary)
+            dead = np.sort(rng.choice(self.n_total, int(self.wl["reset"] * self.n_total),
+                                      replace=False))
+            ev["reset"] = torch.from_numpy(shard_rows(dead, self.lo, hi).astype(np.int32)).to(
+                self.dev)
+        return ev
+
+    def replica(self, it):
+        j = it % self.n_rep
+        return self.opts[j], self.shards[j], self.grad_sets[j][it % len(self.grad_sets[j])]
+
+    def apply_events(self, opt, ev):
+        if "rsr" in ev:
+            opt.rsr_apply(ev["rsr"], ALPHA1, ALPHA2)
+        if "reset" in ev:
+            opt.reset_rows(ev["reset"])
+
+    def one_step(self, it):
+        """The public step (K1 + K2, + the statistics all-reduce on N > 1),
+        then K3 on RSR / relocation boundaries."""
+        opt, sh, grads = self.replica(it)
+        if sh is not None:
+            sh.step(self.masks[it], 1_000_000, grads=grads)
+        else:
+            opt.step(self.masks[it], 1_000_000, grads=grads)
+        ev = self.events.get(it)
+        if ev:
+            self.apply_events(opt, ev)
+
+    def launches(self):
+        return sum(o.engine.launches for o in self.opts)
+
+
+def _prep_capture(w):
+    """No outstanding host-side event waits may cross into a capture."""
+    import torch
+    torch.cuda.synchronize()
+    for sh in w.shards:
+        if sh is not None:
+            sh.capture_begin()
+
+
+def _time_steps(w, use_graph):
+    """Device time of the K timed steps (CUDA events on the launching stream
+    around one graph replay, or around eager launches)."""
     import torch
     import torch.distributed as dist
-
-    from paper_2601_16736_b200 import records as R
-    from paper_2601_16736_b200 import synthetic as S
-    from paper_2601_16736_b200.optimizer import AdamWGS
-    from paper_2601_16736_b200.sampling import StSSchedule, shard_rows, stream, stss_sample
-
-    rank, world, local = dist_env()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
-    n_total = args.n if args.n is not None else wl["n"]
-    n = n_total // world if args.strong else n_total
-    base = rank * n
-    cfg = S.WorkloadConfig(n=n, p_vis=p_vis, mask_family=args.mask, seed=args.seed * 1000 + rank,
-                           lambda_o=wl["lo"], lambda_s=wl["ls"])
-    # clouds whose touched bytes fit in L2 are replicated and stepped round
-    # robin, so every timed step reads rows that >= 4x L2 of other traffic has
-    # passed through since their last use (same per-step workload, cold L2)
-    n_rep = l2_replicas(n, p_vis)
-    opts, grad_sets = [], []
-    for j in range(n_rep):
-        cj = S.WorkloadConfig(n=n, p_vis=p_vis, mask_family=args.mask,
-                              seed=(args.seed * 1000 + rank) * 1000 + j if j else
-                              args.seed * 1000 + rank, lambda_o=wl["lo"], lambda_s=wl["ls"])
-        params = S.make_params_device(cj, dev)
-        if args.params == "record":
-            _, params = R.pack(params, align=args.record_align)
-        uni = None
-        if args.unified:
-            params, uni = _unified(params, args.record_align, args.state_align)
-        opts.append(AdamWGS(S.param_groups(params), mode=wl["mode"], lambda_o=wl["lo"],
-                            lambda_s=wl["ls"], check=args.check, errors="defer",
-                            state_layout=args.layout, state_row_align=args.state_align))
-        if uni is not None:
-            from paper_2601_16736_b200.optimizer import MomentState
-            opts[-1].state = MomentState.from_record(uni, opts[-1].state.spec)
-        gs = [S.grads_device(cj, s, dev) for s in range(2 if n_rep == 1 else 1)]
-        if args.params == "record":
-            gs = [R.pack(g, align=args.record_align)[1] for g in gs]
-        grad_sets.append(gs)
-    opt = opts[0]
-
-    def replica(it):
-        """(optimizer, gradients) of step it."""
-        j = it % n_rep
-        return opts[j], grad_sets[j][it % len(grad_sets[j])]
-
-    total_steps = args.warmup + args.steps
-    masks = [S.visibility_device(cfg, s, dev) for s in range(total_steps)]
-    n_vis = torch.stack([m.sum() for m in masks]).cpu().numpy().astype(np.int64)
-    # RSR / relocation samples are host-drawn with the reference RNG contract
-    # (optimizer.py:379-386, rng.py:17-30) and uploaded before timing.
-    events = {}
-    sched = StSSchedule(milestones=((0, RSR_RATIO),), interval=RSR_INTERVAL)
-    n_global = n * world
-    for it in range(total_steps):
-        boundary = it + 1
-        if boundary % RSR_INTERVAL:
-            continue
-        ev = {}
-        if wl["rsr"]:
-            picked = stss_sample(sched, boundary, n_global, stream(args.seed, "stss", boundary))
-            ev["rsr"] = torch.from_numpy(shard_rows(picked, base, base + n).astype(np.int32)).to(dev)
-        if wl["reset"]:
-            rng = stream(args.seed, "relocate", boundary)
-            k = int(wl["reset"] * n_global)
-            dead = np.sort(rng.choice(n_global, k, replace=False))
-            ev["reset"] = torch.from_numpy(shard_rows(dead, base, base + n).astype(np.int32)).to(dev)
-        events[it] = ev
-    stats_sum = torch.zeros(10, dtype=torch.float64, device=dev)
-    launches = [0]
-
-    def one_step(it):
-        """K1 + K2 (+ K3 on RSR / relocation boundaries) for step it."""
-        opt, grads = replica(it)
-        rows, count = opt.engine.compact(masks[it])
-        _step_k2(opt, grads, rows, count, wl)
-        ev = events.get(it)
-        if ev:
-            if "rsr" in ev:
-                opt.rsr_apply(ev["rsr"], ALPHA1, ALPHA2)
-            if "reset" in ev:
-                opt.reset_rows(ev["reset"])
-        if world > 1:
-            stats_sum.copy_(opt.engine.stats)
-            dist.all_reduce(stats_sum)
-
-    for it in range(args.warmup):
-        one_step(it)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    timed_steps = range(args.warmup, total_steps)
-    # CUDA graph: the K timed steps are captured once and replayed as one
-    # launch, so host launch latency never shows up in device time (the
-    # small clouds are otherwise host-bound).  Multi-rank runs stay eager
-    # (the per-step NCCL all-reduce is issued from the host).
-    use_graph = args.graph and world == 1
-    launches0 = sum(o.engine.launches for o in opts)
+    timed = range(w.warmup, w.total)
+    l0 = w.launches()
     graph = None
     if use_graph:
+        _prep_capture(w)
         graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph):
-            for it in timed_steps:
-                one_step(it)
-    launches[0] = sum(o.engine.launches for o in opts) - launches0
+        for o in w.opts:
+            o._capturing = True
+        try:
+            with torch.cuda.graph(graph):
+                for it in timed:
+                    w.one_step(it)
+                for sh in w.shards:
+                    if sh is not None:
+                        sh.wait_stats()  # join the side stream inside the graph
+        finally:
+            for o in w.opts:
+                o._capturing = False
+            for sh in w.shards:
+                if sh is not None:
+                    sh.capture_end()
+    launches = w.launches() - l0
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
-        torch.cuda.synchronize()
-        start.record()
-        if graph is not None:
-            graph.replay()
-        else:
-            for it in timed_steps:
-                one_step(it)
-        end.record()
-        torch.cuda.synchronize()
+    if w.world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    start.record()
+    if graph is not None:
+        graph.replay()
+    else:
+        for it in timed:
+            w.one_step(it)
+        launches = w.launches() - l0
+    end.record()
+    torch.cuda.synchronize()
+    if w.world > 1:
+        dist.barrier()
     ms = start.elapsed_time(end)
-    if graph is None:
-        launches[0] = sum(o.engine.launches for o in opts) - launches0
     del graph
-    st = replica(total_steps - 1)[0].last_stats()  # the last timed step's statistics (host read, after timing)
-    if st["n_bad_grad"] or st["n_bad_domain"] or st["n_stepped"] != st["n_visible"]:
-        raise RuntimeError(f"step statistics report skipped rows: {st}")
-    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    vis_t = torch.tensor([float(n_vis[args.warmup:].sum())], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
-        dist.all_reduce(vis_t)
-    ms_max = float(ms_t.item())
-    total_visible = float(vis_t.item())
-    value = total_visible / (ms_max / 1000.0)
+    return ms, launches
 
-    # K2 alone, for the roofline: the timed steps' index lists are compacted
-    # up front, then K2 is launched K times back to back (as a graph on one
-    # rank) between two CUDA events on the launching stream
+
+def _time_k2(w, use_graph):
+    """K2 alone, for the roofline: the timed steps' index lists are compacted
+    up front, then K2 is launched K times back to back (as a graph) between
+    two CUDA events on the launching stream."""
+    import torch
+    timed = list(range(w.warmup, w.total))
     idx_lists = []
-    for it in timed_steps:
-        rows, count = replica(it)[0].engine.compact(masks[it])
+    for it in timed:
+        rows, count = w.replica(it)[0].engine.compact(w.masks[it])
         idx_lists.append((rows.clone(), count.clone()))
 
     def k2_only():
-        for j, it in enumerate(timed_steps):
-            o, grads = replica(it)
-            _step_k2(o, grads, idx_lists[j][0], idx_lists[j][1], wl)
+        for j, it in enumerate(timed):
+            o, _, grads = w.replica(it)
+            _step_k2(o, grads, idx_lists[j][0], idx_lists[j][1], w.wl)
 
     k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if use_graph:
@@ -520,23 +560,127 @@ def ours(args, wl, p_vis):
         k2_only()
         k1.record()
     torch.cuda.synchronize()
-    k2_ms = [k0.elapsed_time(k1) / len(idx_lists)]
-    del idx_lists
+    return k0.elapsed_time(k1) / len(idx_lists)
 
-    # roofline of K2 (this rank's launches)
+
+def _time_rsr(w):
+    """Device time of one RSR / reset event (K3) of this workload."""
+    import torch
+    if not w.rsr_probe:
+        return 0.0
+    opt = w.opts[0]
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    w.apply_events(opt, w.rsr_probe)  # warm
+    torch.cuda.synchronize()
+    a.record()
+    for _ in range(3):
+        w.apply_events(opt, w.rsr_probe)
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / 3
+
+
+def run_workload(args, wl, p_vis, rank, world, dev, *, strong, mask, steps, warmup, e2e,
+                 clocks=None):
+    """Time one workload on this rank; every rank returns the same dict
+    (times max-reduced over ranks, counts summed)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2601_16736_b200 import synthetic as S
+    w = Workload(args, wl, p_vis, rank, world, dev, strong, mask, steps, warmup)
+    for it in range(w.warmup):
+        w.one_step(it)
+    torch.cuda.synchronize()
+    use_graph = args.graph
+    if clocks is not None:
+        with clocks:
+            ms, launches = _time_steps(w, use_graph)
+    else:
+        ms, launches = _time_steps(w, use_graph)
+    # the statistics of the last timed step: no skipped rows anywhere
+    o_last, sh_last, _ = w.replica(w.total - 1)
+    st_vec = (sh_last.wait_stats() if sh_last is not None else o_last.engine.stats).tolist()
+    from paper_2601_16736_b200.optimizer import _stats_dict
+    st = _stats_dict(st_vec)
+    if st["n_bad_grad"] or st["n_bad_domain"] or st["n_stepped"] != st["n_visible"]:
+        raise RuntimeError(f"step statistics report skipped rows: {st}")
+    k2_ms = _time_k2(w, use_graph)
+    rsr_ms = _time_rsr(w)
+    # RSR / reset events at their interval: the ones inside the timed window
+    # ran; when the window is shorter than the interval the expected share of
+    # one event is added from its measured device time
+    ev_in = sum(1 for it in range(w.warmup, w.total) if w.events.get(it))
+    ev_due = w.steps / RSR_INTERVAL if (wl["rsr"] or wl["reset"]) else 0.0
+    extra_ms = max(0.0, ev_due - ev_in) * rsr_ms
+    nvis_local = float(w.n_vis[w.warmup:].sum())
+    vec = torch.tensor([ms, ms + extra_ms, k2_ms, rsr_ms, nvis_local, float(launches)],
+                       dtype=torch.float64, device=dev)
+    if world > 1:
+        mx = vec.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = vec.clone()
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        vec = torch.cat([mx[:4], sm[4:]])
+    ms_max, ms_amort, k2_max, rsr_max, total_visible, launches_all = vec.tolist()
     width = S.SH3_WIDTH
-    k2_bytes = [int(nv) * (28 * width + 12) for nv in n_vis[args.warmup:]]
-    k2_avg_ms = statistics.mean(k2_ms)
-    achieved = (sum(k2_bytes) / len(k2_bytes)) / (k2_avg_ms / 1000.0) / 1e9
+    k2_bytes = [int(nv) * (28 * width + 12) for nv in w.n_vis[w.warmup:]]
+    achieved = (sum(k2_bytes) / len(k2_bytes)) / (k2_ms / 1000.0) / 1e9  # this rank's K2
     peak, peak_src = measured_hbm_peak()
-    step_bytes = [S.algorithmic_bytes(n, int(nv)) for nv in n_vis[args.warmup:]]
-    step_gbs = sum(step_bytes) / (ms / 1000.0) / 1e9
+    step_bytes = sum(S.algorithmic_bytes(w.n, int(nv)) for nv in w.n_vis[w.warmup:])
+    out = {
+        "value": total_visible / (ms_amort / 1000.0),
+        "value_no_rsr_amortisation": total_visible / (ms_max / 1000.0),
+        "ms_per_step": ms_amort / w.steps, "ms_per_step_timed": ms_max / w.steps,
+        "rsr_events_timed": ev_in, "rsr_ms_per_event": rsr_max,
+        "rsr_amortised_ms": extra_ms, "visible_per_step": total_visible / w.steps,
+        "gpu_launches": int(launches_all),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "k2_ms_avg": k2_ms, "k2_ms_max_over_ranks": k2_max,
+                     "k2_bytes_per_launch": sum(k2_bytes) / len(k2_bytes),
+                     "bytes_per_visible": 28 * width + 12, "peak_source": peak_src,
+                     "step_gbs_algorithmic": step_bytes / (ms / 1000.0) / 1e9,
+                     "step_frac": step_bytes / (ms / 1000.0) / 1e9 / peak},
+        "config": workload_config(args, wl, p_vis, world, strong, mask),
+    }
+    if e2e:
+        out["e2e"] = run_e2e(args, w, dev, world)
+    del w
+    torch.cuda.empty_cache()
+    return out
 
-    # e2e through the public API with host buffers (rank-local, then max)
-    e2e = None
-    if not args.no_e2e:
-        e2e = run_e2e(args, opt, cfg, dev, world, masks, n_vis)
 
+def ours(args, wl, p_vis):
+    import torch
+    import torch.distributed as dist
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1 or args.sharded:
+        # communicator lines (rank / nranks) for the driver's rank check
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", str(_free_port()))
+        dist.init_process_group("nccl", device_id=dev, rank=rank, world_size=world)
+    clk = ClockSampler(local)
+    main = run_workload(args, wl, p_vis, rank, world, dev, strong=args.strong, mask=args.mask,
+                        steps=args.steps, warmup=args.warmup, e2e=not args.no_e2e, clocks=clk)
+    legs = {}
+    if not args.no_legs:
+        c5 = dict(WORKLOADS["c5"], name="c5")
+        for p, key in ((0.3, "c5_strong"), (0.01, "c5_strong_1pct")):
+            r = run_workload(args, c5, p, rank, world, dev, strong=True, mask="bernoulli",
+                             steps=min(args.steps, 20), warmup=max(3, min(args.warmup, 5)),
+                             e2e=False)
+            legs[key] = {"metric": "visible Gaussians updated/sec per optimizer step",
+                         "value": r["value"], "unit": "visible Gaussians/s",
+                         "ms_per_step": r["ms_per_step"], "n_gpus": world, "scaling": "strong",
+                         "steps": min(args.steps, 20),
+                         "roofline": {k: r["roofline"][k] for k in ("achieved", "peak", "frac",
+                                                                    "k2_ms_avg", "step_frac")},
+                         "gpu_launches": r["gpu_launches"], "config": r["config"]}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cores = host_workers()
@@ -544,62 +688,45 @@ def ours(args, wl, p_vis):
                                               seed=args.seed, workers=cores)
         cpu = {"value": v, "unit": "visible Gaussians/s", "cores": cores, "kind": "port",
                "sample": sample, "host_cpus": os.cpu_count()}
-
     if rank == 0:
+        roof = dict(main["roofline"])
+        roof.update({
+            "traffic": traffic_from_profiles(
+                args.workload, args.mask, p_vis,
+                args.params if args.params != "record" or
+                (args.record_align, args.state_align) == (16, 16) else
+                f"record-a{args.record_align}-s{args.state_align}"),
+            "traffic_source": "dram__bytes_read.sum + dram__bytes_write.sum of one ncu --set "
+                              "full capture of this K2 configuration (profiles/traffic.json; "
+                              "not measured in this run)",
+            "kernel": ("gs::step_kernel (K2, gs_step)" if args.layout != "rows" else
+                       "gs::step_tma4_kernel<LayoutSH3, ...> (K2, record layout, 2-D TMA "
+                       "gather4 / scatter4, via gs_step_rows)" if args.params == "record" else
+                       "gs::step_ws_kernel<LayoutSH3> (K2, per-attribute gathers, via "
+                       "gs_step_rows)")})
         line = {
             "metric": "visible Gaussians updated/sec per optimizer step",
-            "value": value, "unit": "visible Gaussians/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-            "scaling": "strong" if args.strong else "weak", "vs_baseline": None, "dtype": "f32",
+            "value": main["value"], "unit": "visible Gaussians/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": main["ms_per_step"],
+            "higher_is_better": True, "scaling": "strong" if args.strong else "weak",
+            "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded Gaussian cloud, SURVEY §8(d) distributions)",
-            "config": workload_config(args, wl, p_vis, world),
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak,
-                         "traffic": traffic_from_profiles(
-                             args.workload, args.mask, p_vis,
-                             args.params if args.params != "record" or
-                             (args.record_align, args.state_align) == (16, 16) else
-                             f"record-a{args.record_align}-s{args.state_align}"),
-                         "kernel": ("gs::step_kernel (K2, gs_step)" if args.layout != "rows" else
-                                    "gs::step_ring_kernel<LayoutSH3, ..., REC> (K2, record "
-                                    "layout, via gs_step_rows)" if args.params == "record" else
-                                    "gs::step_ws_kernel<LayoutSH3> (K2, per-attribute "
-                                    "gathers, via gs_step_rows)"),
-                         "peak_source": peak_src,
-                         "k2_ms_avg": k2_avg_ms,
-                         "k2_bytes_per_launch": sum(k2_bytes) / len(k2_bytes),
-                         "bytes_per_visible": 28 * width + 12,
-                         "step_gbs_algorithmic": step_gbs,
-                         "step_frac": step_gbs / peak},
-            "e2e": e2e, "gpu_launches": launches[0], "clocks": clk.summary(),
-            "cpu_baseline": cpu,
-            "visible_per_step": float(n_vis[args.warmup:].mean()),
+            "config": dict(main["config"],
+                           rsr_timing=f"{main['rsr_events_timed']} RSR event(s) inside the timed "
+                                      f"window; {main['rsr_amortised_ms']:.4f} ms added = one "
+                                      f"measured event ({main['rsr_ms_per_event']:.4f} ms) x "
+                                      f"(K / {RSR_INTERVAL} - events timed)"),
+            "roofline": roof, "e2e": main.get("e2e"), "gpu_launches": main["gpu_launches"],
+            "clocks": clk.summary(), "cpu_baseline": cpu,
+            "visible_per_step": main["visible_per_step"],
+            "ms_per_step_timed": main["ms_per_step_timed"],
+            "value_no_rsr_amortisation": main["value_no_rsr_amortisation"],
+            "legs": legs or None,
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist.is_initialized():
+        dist.barrier()
         dist.destroy_process_group()
-
-
-def _unified(params, record_align, state_align):
-    """Experiment: one row per Gaussian holding the moment record and then
-    the parameter row ([m/v pairs + clock | theta]), so a visible row is one
-    contiguous span plus its gradient row.  Returns (parameter views, the
-    state-record view)."""
-    import torch
-    n = next(iter(params.values())).shape[0]
-    p = sum(max(1, int(t[0].numel())) for t in params.values())
-    pw = (p + record_align - 1) // record_align * record_align
-    sw = (2 * (p + 1) + state_align - 1) // state_align * state_align
-    u = torch.zeros((n, sw + pw), dtype=torch.float32, device=next(iter(params.values())).device)
-    out, off = {}, sw
-    for name, t in params.items():
-        w = max(1, int(t[0].numel()))
-        v = u[:, off:off + w]
-        v = v.view(n, *t.shape[1:]) if t.dim() > 1 else v.view(n)
-        v.copy_(t)
-        out[name] = v
-        off += w
-    return out, u[:, :sw]
 
 
 def _step_k2(opt, grads, rows, count, wl):
@@ -621,10 +748,11 @@ def _step_k2(opt, grads, rows, count, wl):
     opt._last_ctx = (b, rows, count, wl["lo"], wl["ls"], wl["mode"])
 
 
-def run_e2e(args, opt, cfg, dev, world, masks, n_vis):
-    """Public-API step with host buffers, every step: H2D copy of the mask
-    from pinned memory, opt.step() with the gradients in pinned host memory,
-    D2H read of the step statistics.  Default: the step kernel gathers the
+def run_e2e(args, w, dev, world):
+    """Public-API step with host buffers, every step: H2D copy of that step's
+    mask from pinned memory (a fresh mask per step), the step (through
+    ShardedAdamWGS on N > 1) with the gradients in pinned host memory, D2H
+    read of the step statistics.  Default: the step kernel gathers the
     visible rows' gradients zero-copy over PCIe (only N_v rows cross the
     bus).  The dense-copy variant (every gradient row copied H2D first) is
     timed too and reported as ``dense_copy``."""
@@ -632,82 +760,117 @@ def run_e2e(args, opt, cfg, dev, world, masks, n_vis):
     import torch.distributed as dist
 
     from paper_2601_16736_b200 import records as R
-
-    like = opt_grads_like(opt)
+    opt, sh, _ = w.replica(0)
+    like = {g["name"]: g["params"][0] for g in opt.param_groups}
     if args.params == "record":
         # one pinned gradient record; rows padded to 256 B = two 128-byte
         # lines, the granule the zero-copy reads cross PCIe in
         host_rec, host_grads = R.pack({k: torch.zeros(t.shape) for k, t in like.items()},
                                       align=args.host_record_align, pin_memory=True)
         dev_grads = R.views_like(torch.empty_like(host_rec, device=dev), like)
+        host_dense = [host_rec]
+        dev_dense = [dev_grads[next(iter(dev_grads))]._base]
+        row_bytes = host_rec.shape[1] * 4
     else:
         host_grads = {k: torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
                       for k, t in like.items()}
         dev_grads = {k: torch.empty_like(t) for k, t in like.items()}
-    for k, t in host_grads.items():
+        host_dense = list(host_grads.values())
+        dev_dense = list(dev_grads.values())
+        row_bytes = sum(t[0].numel() * 4 for t in host_grads.values())
+    for t in host_grads.values():
         t.copy_(torch.randn(t.shape) * 1e-4)
-    host_mask = torch.empty(masks[0].shape, dtype=torch.bool, pin_memory=True)
-    host_mask.copy_(masks[0].cpu())
-    dev_mask = torch.empty_like(masks[0])
+    n_steps = max(1, args.e2e_steps)
+    n_masks = min(n_steps, len(w.masks))
+    host_masks = []
+    for j in range(n_masks):
+        hm = torch.empty(w.masks[j].shape, dtype=torch.bool, pin_memory=True)
+        hm.copy_(w.masks[j].cpu())
+        host_masks.append(hm)
+    mask_vis = [float(m.sum()) for m in host_masks]
+    dev_mask = torch.empty_like(w.masks[0])
     stats_host = torch.empty(10, dtype=torch.float64, pin_memory=True)
-    # bytes the zero-copy gather moves per visible row: the whole host record
-    # row (pad included) for a record, the attribute rows otherwise
-    row_bytes = (host_rec.shape[1] * 4 if args.params == "record"
-                 else sum(t[0].numel() * 4 for t in host_grads.values()))
-    dense = sum(t.numel() * 4 for t in host_grads.values())
-    host_dense = ([host_rec] if args.params == "record" else list(host_grads.values()))
     dense = sum(t.numel() * 4 for t in host_dense)
-    dev_dense = ([dev_grads[next(iter(dev_grads))]._base] if args.params == "record"
-                 else list(dev_grads.values()))
     d2h = stats_host.numel() * 8
-    nv = float(host_mask.sum())
+    step = sh.step if sh is not None else opt.step
 
-    def one(zero_copy):
-        dev_mask.copy_(host_mask, non_blocking=True)
+    def one(j, zero_copy):
+        dev_mask.copy_(host_masks[j % n_masks], non_blocking=True)
         if zero_copy:
             grads = host_grads
         else:
             for d, h in zip(dev_dense, host_dense):
                 d.copy_(h, non_blocking=True)
             grads = dev_grads
-        opt.step(dev_mask, 1_000_000, grads=grads)
-        stats_host.copy_(opt.engine.stats, non_blocking=True)
+        step(dev_mask, 1_000_000, grads=grads)
+        st = sh.wait_stats() if sh is not None else opt.engine.stats
+        stats_host.copy_(st, non_blocking=True)
         torch.cuda.current_stream().synchronize()
 
     def timed(zero_copy):
-        for _ in range(2):
-            one(zero_copy)
+        for j in range(2):
+            one(j, zero_copy)
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        for _ in range(args.e2e_steps):
-            one(zero_copy)
-        ms = (time.perf_counter() - t0) * 1000.0 / args.e2e_steps
+        for j in range(n_steps):
+            one(j, zero_copy)
+        ms = (time.perf_counter() - t0) * 1000.0 / n_steps
         ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
         return float(ms_t.item())
 
+    nv = sum(mask_vis[j % n_masks] for j in range(n_steps)) / n_steps
+    nv_t = torch.tensor([nv], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(nv_t)
+    nv_all = float(nv_t.item())
     ms_dense = timed(False)
     ms = timed(True)
-    return {"value": nv * world / (ms / 1000.0), "unit": "visible Gaussians/s",
-            "h2d_bytes_per_step": int(host_mask.numel() + nv * row_bytes),
-            "d2h_bytes_per_step": d2h, "ms_per_step": ms, "steps": args.e2e_steps,
+    return {"value": nv_all / (ms / 1000.0), "unit": "visible Gaussians/s",
+            "h2d_bytes_per_step": int(host_masks[0].numel() + nv * row_bytes),
+            "d2h_bytes_per_step": d2h, "ms_per_step": ms, "steps": n_steps,
+            "masks": f"{n_masks} distinct pinned host masks, one per step (cycled)",
             "h2d_mode": "mask copied H2D; gradients gathered zero-copy from pinned host "
                         "memory by the step kernel (visible rows only)",
-            "timing": "host wall clock around H2D + step + D2H + sync",
-            "dense_copy": {"value": nv * world / (ms_dense / 1000.0), "ms_per_step": ms_dense,
-                           "h2d_bytes_per_step": int(host_mask.numel() + dense)}}
+            "timing": "host wall clock around H2D + step + D2H + sync, max over ranks",
+            "dense_copy": {"value": nv_all / (ms_dense / 1000.0), "ms_per_step": ms_dense,
+                           "h2d_bytes_per_step": int(host_masks[0].numel() + dense)}}
 
 
-def opt_grads_like(opt):
-    return {g["name"]: g["params"][0] for g in opt.param_groups}
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def self_launch(args) -> int:
+    """``--gpus N`` outside torchrun: start N ranks on this node."""
+    import torch
+    have = torch.cuda.device_count() if torch.cuda.is_available() else 0
+    if have < args.gpus:
+        print(f"bench.py: --gpus {args.gpus} needs {args.gpus} GPUs, this node has {have}",
+              file=sys.stderr)
+        return 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           f"--master-port={_free_port()}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 def main():
     args = parse()
-    wl = dict(WORKLOADS[args.workload])
+    rank, world, _ = dist_env()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(self_launch(args))
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        sys.exit(2)
+    wl = dict(WORKLOADS[args.workload], name=args.workload)
     if args.n is not None:
         wl["n"] = args.n
     p_vis = args.vis if args.vis is not None else wl["p"]

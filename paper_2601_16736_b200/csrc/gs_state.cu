@@ -428,6 +428,123 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
+// One-pass K4 on the row record: a warp reads one 8(P+1)-byte record row per
+// iteration (lane q takes the 16-byte piece of slots 2q, 2q+1), so every
+// row is one coalesced warp access and nothing is divided by the width.  A
+// lane's slots belong to fixed groups across rows, so it keeps J x 2
+// accumulator sets (group id fixed per lane); the block then folds them in a
+// fixed (warp, lane) order and the last CTA folds the blocks: deterministic
+// for a given grid.
+template <int J>
+__global__ void __launch_bounds__(kThreads)
+    stats_rows_vec_kernel(const GroupSet S, int P, const float* __restrict__ record,
+                          int64_t stride, int64_t n_rows, const uint8_t* __restrict__ alive,
+                          float active_logit, double* __restrict__ out, double* partials,
+                          unsigned int* counter) {
+  constexpr int NW = kThreads / 32;
+  constexpr int NF = 5;  // sum sqrt v, max sqrt v, n(v > 0), sum |m|/sqrt v, max |m|/sqrt v
+  __shared__ signed char s_grp[128];
+  __shared__ double s_acc[NW][32][2 * J][NF];
+  __shared__ double s_red[kStatsFields * NW];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x < 128) {
+    int g = -1, off = 0;
+    for (int i = 0; i < S.n; ++i) {
+      if ((int)threadIdx.x >= off && (int)threadIdx.x < off + S.g[i].width) g = i;
+      off += S.g[i].width;
+    }
+    s_grp[threadIdx.x] = (signed char)((int)threadIdx.x < P ? g : -1);
+  }
+  __syncthreads();
+  int opac = -1;
+  for (int i = 0; i < S.n; ++i)
+    if (S.g[i].role == GS_ROLE_OPACITY && S.g[i].width == 1 && S.g[i].param != nullptr) opac = i;
+  double a[2 * J][NF];
+#pragma unroll
+  for (int k = 0; k < 2 * J; ++k)
+#pragma unroll
+    for (int f = 0; f < NF; ++f) a[k][f] = 0.0;
+  double n_alive = 0.0, n_active = 0.0;
+  const int nq = (P + 1) / 2;  // 16-byte pieces holding slots < P
+  const int64_t warps = (int64_t)gridDim.x * NW;
+  for (int64_t r = (int64_t)blockIdx.x * NW + warp; r < n_rows; r += warps) {
+    if (alive != nullptr && alive[r] == 0) continue;  // warp-uniform
+    if (lane == 0) {
+      n_alive += 1.0;
+      if (opac >= 0) n_active += __ldg(S.g[opac].param + r * S.g[opac].ps) > active_logit;
+    }
+    const float4* row = reinterpret_cast<const float4*>(record + r * stride);
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      const int q = lane + 32 * j;
+      if (q < nq) {
+        const float4 x = __ldg(row + q);
+        const float mm[2] = {x.x, x.z}, vv[2] = {x.y, x.w};
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          if (2 * q + h >= P) continue;
+          const double sq = sqrt((double)vv[h]);
+          double* A = a[2 * j + h];
+          A[0] += sq;
+          A[1] = fmax(A[1], sq);
+          if (sq > 0.0) {
+            const double rt = __ddiv_rn(fabs((double)mm[h]), sq);
+            A[2] += 1.0;
+            A[3] += rt;
+            A[4] = fmax(A[4], rt);
+          }
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 2 * J; ++k)
+#pragma unroll
+    for (int f = 0; f < NF; ++f) s_acc[warp][lane][k][f] = a[k][f];
+  n_alive = warp_sum(n_alive);
+  n_active = warp_sum(n_active);
+  if (lane == 0) {
+    s_red[warp] = n_alive;
+    s_red[NW + warp] = n_active;
+  }
+  __syncthreads();
+  // block fold in a fixed order: thread t < kStatsFields owns one output field
+  double acc[kStatsFields];
+  bool is_max[kStatsFields];
+#pragma unroll
+  for (int f = 0; f < kStatsFields; ++f) {
+    acc[f] = 0.0;
+    is_max[f] = f >= 2 && (((f - 2) % 5) == 1 || ((f - 2) % 5) == 4);
+  }
+  if (threadIdx.x == 0) {
+    for (int w = 0; w < NW; ++w) {
+      acc[0] += s_red[w];
+      acc[1] += s_red[NW + w];
+    }
+    for (int w = 0; w < NW; ++w)
+      for (int l = 0; l < 32; ++l)
+        for (int k = 0; k < 2 * J; ++k) {
+          const int sl = 2 * (l + 32 * (k / 2)) + (k & 1);
+          const int g = sl < 128 ? s_grp[sl] : -1;
+          if (g < 0) continue;
+          const double* A = s_acc[w][l][k];
+          double* o = acc + 2 + 5 * g;
+          o[0] += A[0];
+          o[1] = fmax(o[1], A[1]);
+          o[2] += A[2];
+          o[3] += A[3];
+          o[4] = fmax(o[4], A[4]);
+        }
+    for (int f = 0; f < kStatsFields; ++f) partials[(size_t)blockIdx.x * kStatsFields + f] = acc[f];
+  }
+  if (last_block_arrive(counter)) {
+    double tmp[kStatsFields];
+    final_reduce<kStatsFields>(partials, gridDim.x, kStatsFields, tmp, is_max, s_red);
+    if (threadIdx.x == 0)
+      for (int f = 0; f < 2 + 5 * S.n; ++f) out[f] = tmp[f];
+  }
+}
+
 // AIU (optimizer.py:425-450): picked invisible rows take one extra step with
 // their frozen moments and clock, state untouched.  picked row i is
 // inv_idx[jlist[i]]; lr_eta is fl32(lr * eta) per group (the reference does
@@ -572,9 +689,22 @@ extern "C" int gs_stats_all_rows(const gs_group* groups, int32_t n_groups, int64
   }
   auto* hdr = reinterpret_cast<StatsWorkspace*>(ws);
   auto* partials = reinterpret_cast<double*>(reinterpret_cast<char*>(ws) + sizeof(StatsWorkspace));
+  cudaStream_t s = (cudaStream_t)stream;
+  if (record_stride % 4 == 0 && (reinterpret_cast<uintptr_t>(record) & 15u) == 0 && P <= 127) {
+    // one pass, a warp per record row
+    const int64_t need = (n_rows + kThreads / 32 - 1) / (kThreads / 32);
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, stats_blocks()));
+    if ((P + 1) / 2 <= 32)
+      stats_rows_vec_kernel<1><<<grid, kThreads, 0, s>>>(S, P, record, record_stride, n_rows, alive,
+                                                        active_logit, out, partials, &hdr->counter);
+    else
+      stats_rows_vec_kernel<2><<<grid, kThreads, 0, s>>>(S, P, record, record_stride, n_rows, alive,
+                                                        active_logit, out, partials, &hdr->counter);
+    return gs_check_launch("gs_stats_all_rows");
+  }
   const int64_t need = (n_rows * 4 + kThreads - 1) / kThreads;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, stats_blocks()));
-  stats_rows_kernel<<<grid, kThreads, 0, (cudaStream_t)stream>>>(
+  stats_rows_kernel<<<grid, kThreads, 0, s>>>(
       S, record, record_stride, n_rows, alive, active_logit, out, partials, &hdr->counter);
   return gs_check_launch("gs_stats_all_rows");
 }

@@ -17,7 +17,7 @@
 //   step_tma4_kernel (gs_step_sh3_tma.cuh)  default for device-resident
 //       parameter / gradient / moment records: 2-D TMA row gathers and
 //       scatters (tile::gather4 / tile::scatter4), loader / consumer / storer
-//       warps, 2-stage ring, in-place update in shared memory.
+//       warps, 3-stage ring, in-place update in shared memory.
 //   step_ring_kernel<..., REC=1>  records the TMA kernel cannot take
 //       (host-mapped gradients, compact 240-byte rows, GS_FIXED_VARIANT=21):
 //       3 producer warps cp.async the chunk's moment records, theta rows and
@@ -1954,15 +1954,18 @@ void launch_fixed(const FixedParams& P, const TmaMaps* M, int64_t max_rows, int 
     // otherwise (host-mapped gradients, compact 240-byte rows) or on request
     // (variant 21)
     if (M != nullptr && v != 21) {
+      // shape: (stages, consumer warps, CTAs / SM).  3 x 8 x 2 measured best
+      // on c3 (K2 0.532 ms, 0.86 of the copy peak; 2 stages 0.567 ms) and
+      // on c5 at 100% visibility (0.94); profiles/r02/tma4_shape_sweep.txt.
+      // GS_TMA4_SHAPE selects the measured alternatives (identical results).
       static const int shape = getenv("GS_TMA4_SHAPE") ? atoi(getenv("GS_TMA4_SHAPE")) : 0;
       switch (shape) {
-        case 1: launch_tma4<L, MODE, STRICT, 3, 8, 2>(P, *M, max_rows, s); return;
-        case 2: launch_tma4<L, MODE, STRICT, 2, 12, 2>(P, *M, max_rows, s); return;
+        case 1: launch_tma4<L, MODE, STRICT, 2, 8, 2>(P, *M, max_rows, s); return;
+        case 2: launch_tma4<L, MODE, STRICT, 3, 12, 2>(P, *M, max_rows, s); return;
         case 3: launch_tma4<L, MODE, STRICT, 2, 8, 3>(P, *M, max_rows, s); return;
-        case 4: launch_tma4<L, MODE, STRICT, 3, 16, 1>(P, *M, max_rows, s); return;
-        case 5: launch_tma4<L, MODE, STRICT, 4, 16, 1>(P, *M, max_rows, s); return;
-        case 6: launch_tma4<L, MODE, STRICT, 3, 12, 2>(P, *M, max_rows, s); return;
-        default: launch_tma4<L, MODE, STRICT, 2, 8, 2>(P, *M, max_rows, s); return;
+        case 4: launch_tma4<L, MODE, STRICT, 3, 6, 2>(P, *M, max_rows, s); return;
+        case 5: launch_tma4<L, MODE, STRICT, 3, 10, 2>(P, *M, max_rows, s); return;
+        default: launch_tma4<L, MODE, STRICT, 3, 8, 2>(P, *M, max_rows, s); return;
       }
     }
     if (P.wide) {  // > 2^32 parameter-record elements: 64-bit row offsets

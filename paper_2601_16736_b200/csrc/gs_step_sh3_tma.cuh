@@ -4,7 +4,7 @@
 // moment records (included by gs_step_sh3.cuh).
 //
 // A CTA walks chunks of 32 visible rows through an S-stage shared-memory
-// ring.  Warp roles:
+// ring (3 stages, 2 CTAs per SM by default).  Warp roles:
 //   loader  (warp NCW)     per chunk, lanes 0..7 each issue three gather4
 //                          operations (4 rows each) for the moment records
 //                          (480 B of every 512-B row), the parameter rows and
@@ -28,8 +28,9 @@
 // Compared with the cp.async ring (60 16-byte LSU copies and ~120 scattered
 // 4/8-byte stores per row), a 32-row chunk costs 24 + 16 TMA operations and
 // the SM issue slots go to the arithmetic.  Probe on B200 (scripts/
-// tma4_probe.cu, profiles/r02/tma4_probe.txt): the data movement alone runs
-// at 0.86 of the copy peak for 30% i.i.d. rows and 0.94 for all rows.
+// tma4_probe.cu, profiles/r02/tma4_probe*.txt): the data movement alone runs
+// at 0.86 of the copy peak for 30% i.i.d. rows and 0.94 for all rows; the
+// kernel reaches 0.86 / 0.94 (profiles/r02/tma4_shape_sweep.txt).
 #pragma once
 
 #include <cuda.h>

@@ -155,6 +155,20 @@ class ShardedAdamWGS:
             self._enqueue_check(i)
         return buf
 
+    def capture_begin(self):
+        """Before an outside CUDA-graph capture of steps: nothing outstanding,
+        no waits on events recorded outside the capture."""
+        self.check_errors()
+        torch.cuda.synchronize(self.opt.device)
+        self._free = [None] * self.STAT_SLOTS
+        self.stats_event = None
+
+    def capture_end(self):
+        """After the capture (whose last step joined the side stream with
+        wait_stats()): events recorded inside it are not waited on outside."""
+        self._free = [None] * self.STAT_SLOTS
+        self.stats_event = None
+
     def wait_stats(self) -> torch.Tensor:
         """The last step's reduced statistics, ordered on the current stream."""
         if getattr(self, "stats_event", None) is not None:
@@ -281,13 +295,11 @@ class ShardStepGraph:
     def __init__(self, sh: ShardedAdamWGS, visibility, n_pixels, step_kwargs):
         self.sh = sh
         opt = sh.opt
-        sh.check_errors()
         dev = opt.device
         opt.engine.group_array(opt._bindings(step_kwargs.get("grads"),
                                              step_kwargs.get("mu_lr_scale", 1.0)))
         cap = torch.cuda.Stream(dev)
-        torch.cuda.synchronize(dev)
-        sh._free = [None] * sh.STAT_SLOTS  # nothing outstanding: no waits on outside events
+        sh.capture_begin()
         self.slot = sh._slot
         self.graph = torch.cuda.CUDAGraph()
         launches = opt.engine.launches
@@ -302,8 +314,7 @@ class ShardStepGraph:
         finally:
             opt._capturing = False
         torch.cuda.current_stream(dev).wait_stream(cap)
-        sh._free = [None] * sh.STAT_SLOTS
-        sh.stats_event = None  # replays join the side stream inside the graph
+        sh.capture_end()  # replays join the side stream inside the graph
         self.stats = buf
         self.launches_per_replay = opt.engine.launches - launches
         opt.engine.launches = launches

@@ -10,9 +10,9 @@ run() {  # label, env, args
   env $envs python bench.py --steps 20 --warmup 5 --no-cpu --no-e2e "$@" 2>/dev/null | tail -1 | \
     python -c "import sys,json; d=json.loads(sys.stdin.read()); r=d['roofline']; print('%-34s step %.4f ms  K2 %.4f ms  frac %.3f' % ('$label', d['ms_per_step'], r['k2_ms_avg'], r['frac']))" >> $out
 }
-for sh in 0 1 2 3 4 5 6; do run "c3 tma4 shape $sh" "GS_TMA4_SHAPE=$sh"; done
+for sh in 0 1 2 3 4 5; do run "c3 tma4 shape $sh" "GS_TMA4_SHAPE=$sh"; done
 run "c3 ring (variant 21)" "GS_FIXED_VARIANT=21"
-for sh in 0 1 3; do run "c3 coherent tma4 shape $sh" "GS_TMA4_SHAPE=$sh" --mask coherent; done
+for sh in 0 1; do run "c3 coherent tma4 shape $sh" "GS_TMA4_SHAPE=$sh" --mask coherent; done
 run "c3 coherent ring" "GS_FIXED_VARIANT=21" --mask coherent
 for sh in 0 1; do run "c5 100% tma4 shape $sh" "GS_TMA4_SHAPE=$sh" --workload c5 --vis 1.0 --steps 5 --warmup 3; done
 run "c5 100% ring" "GS_FIXED_VARIANT=21" --workload c5 --vis 1.0 --steps 5 --warmup 3

@@ -146,3 +146,45 @@ def test_two_rank_sharded_step_equals_single_process(mode, check):
         assert r[2] == [bad], r[2]
         if check == "strict":
             assert r[4], "a strict abort on one shard must leave every shard unmutated"
+
+
+def test_sharded_capture_nccl_single_rank_matches_eager():
+    """ShardedAdamWGS.capture on an NCCL group (one rank on this box): the
+    captured step — compaction, the fused step, the statistics all-reduce on
+    the side stream joined inside the graph — replays bitwise like eager
+    steps, with the reduced statistics."""
+    from paper_2601_16736_b200 import records as R
+    from paper_2601_16736_b200 import synthetic as S
+    from paper_2601_16736_b200.sharded import ShardedAdamWGS
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_free_port()))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device(DEV))
+    try:
+        cfg, host, masks, grads = _problem()
+        outs = []
+        for how in ("eager", "graph"):
+            _, params = R.pack({k: torch.from_numpy(v.copy()).to(DEV) for k, v in host.items()})
+            _, gv = R.pack({k: torch.zeros(v.shape, device=DEV) for k, v in host.items()})
+            sh = ShardedAdamWGS(S.param_groups(params), N, mode="adamw-gs", lambda_o=1e-3,
+                                lambda_s=1e-5)
+            vis_buf = torch.zeros(N, dtype=torch.bool, device=DEV)
+            graph = sh.capture(vis_buf, cfg.n_pixels, grads=gv) if how == "graph" else None
+            stats = []
+            for s in range(STEPS):
+                vis_buf.copy_(torch.from_numpy(masks[s]))
+                for k, x in grads[s].items():
+                    gv[k].copy_(torch.from_numpy(x).view(gv[k].shape))
+                st = graph.replay() if graph is not None else sh.step(vis_buf, cfg.n_pixels,
+                                                                      grads=gv)
+                stats.append(sh.wait_stats().cpu().numpy().copy())
+            sh.check_errors()
+            outs.append(({k: p.cpu().numpy() for k, p in params.items()},
+                         sh.opt.state.record.cpu().numpy(), stats))
+        (pa, ra, sa), (pb, rb, sb) = outs
+        for k in pa:
+            assert np.array_equal(pa[k], pb[k]), k
+        assert np.array_equal(ra.view(np.int32), rb.view(np.int32))
+        for x, y in zip(sa, sb):
+            assert np.array_equal(x, y)
+        assert sa[-1][0] == masks[-1].sum()
+    finally:
+        dist.destroy_process_group()
