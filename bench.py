@@ -530,26 +530,44 @@ def _time_steps(w, use_graph):
 
 
 def _time_k2(w, use_graph):
-    """K2 alone, for the roofline: the timed steps' index lists are compacted
-    up front, then K2 is launched K times back to back (as a graph) between
-    two CUDA events on the launching stream."""
+    """The dominant kernel alone, for the roofline, launched K times back to
+    back (as a graph) between two CUDA events on the launching stream.
+    Fused path (the default on records): the one-launch compaction + step
+    kernel, i.e. opt.step without the statistics all-reduce or RSR.  Index
+    path: K2 on index lists compacted up front.  Returns (ms per launch,
+    fused?)."""
     import torch
     timed = list(range(w.warmup, w.total))
-    idx_lists = []
-    for it in timed:
-        rows, count = w.replica(it)[0].engine.compact(w.masks[it])
-        idx_lists.append((rows.clone(), count.clone()))
+    o0 = w.replica(timed[0])[0]
+    o0.step(w.masks[timed[0]], 1_000_000, grads=w.replica(timed[0])[2])
+    fused = o0._last_ctx[1] is None
+    if fused:
+        def k2_only():
+            for it in timed:
+                o, _, grads = w.replica(it)
+                o.step(w.masks[it], 1_000_000, grads=grads)
+    else:
+        idx_lists = []
+        for it in timed:
+            rows, count = w.replica(it)[0].engine.compact(w.masks[it])
+            idx_lists.append((rows.clone(), count.clone()))
 
-    def k2_only():
-        for j, it in enumerate(timed):
-            o, _, grads = w.replica(it)
-            _step_k2(o, grads, idx_lists[j][0], idx_lists[j][1], w.wl)
+        def k2_only():
+            for j, it in enumerate(timed):
+                o, _, grads = w.replica(it)
+                _step_k2(o, grads, idx_lists[j][0], idx_lists[j][1], w.wl)
 
     k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if use_graph:
         g2 = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g2):
-            k2_only()
+        for o in w.opts:
+            o._capturing = True
+        try:
+            with torch.cuda.graph(g2):
+                k2_only()
+        finally:
+            for o in w.opts:
+                o._capturing = False
         torch.cuda.synchronize()
         k0.record()
         g2.replay()
@@ -560,7 +578,7 @@ def _time_k2(w, use_graph):
         k2_only()
         k1.record()
     torch.cuda.synchronize()
-    return k0.elapsed_time(k1) / len(idx_lists)
+    return k0.elapsed_time(k1) / len(timed), fused
 
 
 def _time_rsr(w):
@@ -605,7 +623,7 @@ def run_workload(args, wl, p_vis, rank, world, dev, *, strong, mask, steps, warm
     st = _stats_dict(st_vec)
     if st["n_bad_grad"] or st["n_bad_domain"] or st["n_stepped"] != st["n_visible"]:
         raise RuntimeError(f"step statistics report skipped rows: {st}")
-    k2_ms = _time_k2(w, use_graph)
+    k2_ms, fused = _time_k2(w, use_graph)
     rsr_ms = _time_rsr(w)
     # RSR / reset events at their interval: the ones inside the timed window
     # ran; when the window is shorter than the interval the expected share of
@@ -624,7 +642,10 @@ def run_workload(args, wl, p_vis, rank, world, dev, *, strong, mask, steps, warm
         vec = torch.cat([mx[:4], sm[4:]])
     ms_max, ms_amort, k2_max, rsr_max, total_visible, launches_all = vec.tolist()
     width = S.SH3_WIDTH
-    k2_bytes = [int(nv) * (28 * width + 12) for nv in w.n_vis[w.warmup:]]
+    # algorithmic bytes per launch of the timed kernel: the
+    # fused kernel reads the mask (1 B/row) and writes no index list
+    per_vis = 28 * width + (8 if fused else 12)
+    k2_bytes = [int(nv) * per_vis + (w.n if fused else 0) for nv in w.n_vis[w.warmup:]]
     achieved = (sum(k2_bytes) / len(k2_bytes)) / (k2_ms / 1000.0) / 1e9  # this rank's K2
     peak, peak_src = measured_hbm_peak()
     step_bytes = sum(S.algorithmic_bytes(w.n, int(nv)) for nv in w.n_vis[w.warmup:])
@@ -638,7 +659,8 @@ def run_workload(args, wl, p_vis, rank, world, dev, *, strong, mask, steps, warm
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "k2_ms_avg": k2_ms, "k2_ms_max_over_ranks": k2_max,
                      "k2_bytes_per_launch": sum(k2_bytes) / len(k2_bytes),
-                     "bytes_per_visible": 28 * width + 12, "peak_source": peak_src,
+                     "bytes_per_visible": per_vis, "bytes_per_row": 1 if fused else 0,
+                     "fused_compaction": fused, "peak_source": peak_src,
                      "step_gbs_algorithmic": step_bytes / (ms / 1000.0) / 1e9,
                      "step_frac": step_bytes / (ms / 1000.0) / 1e9 / peak},
         "config": workload_config(args, wl, p_vis, world, strong, mask),
@@ -700,8 +722,12 @@ def ours(args, wl, p_vis):
                               "full capture of this K2 configuration (profiles/traffic.json; "
                               "not measured in this run)",
             "kernel": ("gs::step_kernel (K2, gs_step)" if args.layout != "rows" else
-                       "gs::step_tma4_kernel<LayoutSH3, ...> (K2, record layout, 2-D TMA "
-                       "gather4 / scatter4, via gs_step_rows)" if args.params == "record" else
+                       ("gs::step_tma4_kernel<LayoutSH3, ..., MASK=1> (K1 fused into K2: the "
+                        "loader compacts the mask; 2-D TMA gather4 / scatter4 on the records; "
+                        "via gs_step_rows_masked)" if main["roofline"].get("fused_compaction")
+                        else "gs::step_tma4_kernel<LayoutSH3, ...> (K2 on the K1 index list, "
+                        "2-D TMA gather4 / scatter4, via gs_step_rows)")
+                       if args.params == "record" else
                        "gs::step_ws_kernel<LayoutSH3> (K2, per-attribute gathers, via "
                        "gs_step_rows)")})
         line = {
@@ -745,7 +771,7 @@ def _step_k2(opt, grads, rows, count, wl):
         eng.step(b, wl["mode"], opt.state.clock, rows=rows, count=count, eps=opt.eps,
                  lambda_opacity=wl["lo"], lambda_scale=wl["ls"], n_visible_dev=count,
                  check=opt.check, record=opt.state.record)
-    opt._last_ctx = (b, rows, count, wl["lo"], wl["ls"], wl["mode"])
+    opt._last_ctx = (b, rows, count, wl["lo"], wl["ls"], wl["mode"], None)
 
 
 def run_e2e(args, w, dev, world):

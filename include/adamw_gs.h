@@ -273,6 +273,20 @@ int gs_densify_rows(const float* grad, int64_t grad_stride, int32_t width, const
                     const int32_t* n_list_dev, int64_t max_rows, float* accum, int32_t* count,
                     float scale, const int32_t* abort_flag, void* stream);
 
+/* Fused K1 + K2 (the fused check): the step of the visible rows of a mask
+ * (uint8 mask != 0, or int32 radii > 0; exactly one of the two) without a
+ * separate compaction pass or index list.  *launched = 1 if this layout ran
+ * (the SH-3 row records with device-resident gradients on the 2-D TMA
+ * kernel; not the dense coupled-adam mode, nor sparse-adam with a coupled
+ * normaliser, which needs N_v before the step); *launched = 0 (status
+ * GS_OK) asks the caller to compact and call gs_step_rows.  The statistics'
+ * n_visible is the mask's visible count; results equal gs_compact +
+ * gs_step_rows bit for bit (rows are independent). */
+int gs_step_rows_masked(const gs_group* groups, int32_t n_groups, const gs_step_cfg* cfg,
+                        const uint8_t* mask, const int32_t* radii, int64_t n_rows, float* record,
+                        int64_t record_stride, double* stats_out, void* ws, size_t ws_bytes,
+                        int32_t* launched, void* stream);
+
 /* GS_BUILD_FLAG_* bits of this build. */
 int32_t gs_build_flags(void);
 int gs_stats_all_rows(const gs_group* groups, int32_t n_groups, int64_t n_rows,

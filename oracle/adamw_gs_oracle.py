@@ -738,3 +738,71 @@ def densify_adc_f64(params, m, v, t, alive, accum, count, cfg, rng):
     out_t = np.where(fresh, 0, t[src])[keep]
     return ({k: x[keep] for k, x in merged.items()}, out_m, out_v, out_t, am[keep], src[keep],
             (int(clone.size), int(split.size), n_pruned))
+
+
+def quat_rotation_f64(q):
+    """Rotation matrices [k, 3, 3] of (w, x, y, z) quaternions, normalised
+    (the 3DGS convention; the same matrix gs_noise.cu builds)."""
+    q = np.asarray(q, F64)
+    q = q / np.maximum(np.linalg.norm(q, axis=1, keepdims=True), 1e-12)
+    w, x, y, z = q[:, 0], q[:, 1], q[:, 2], q[:, 3]
+    return np.stack([
+        np.stack([1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y)], -1),
+        np.stack([2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x)], -1),
+        np.stack([2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)], -1),
+    ], 1)
+
+
+def densify_adc_sh3_f64(params, m, v, t, alive, accum, count, cfg, rng):
+    """densify_adc (pipeline.py:116-185) generalised to the 3DGS SH-3 layout
+    (xyz 3, f_dc 3, f_rest 45, opacity 1, log scaling 3, rotation quaternion
+    4), float64.  Decisions, clone opacity, prune and the rng draw order are
+    the reference's; a split child is sampled inside the parent's 3-D
+    footprint: gamma ~ N(0, I_3) (one rng.standard_normal((k, 3)) per child,
+    where the 2-D reference draws (k, 2)), its norm clipped at 2.5 as in
+    pipeline.py:155-157, offset R(q) (exp(scaling) * gamma), and the log
+    scales shrink by log(split_shrink).  Returns like densify_adc_f64."""
+    n = params["opacity"].shape[0]
+    tau = params["opacity"].reshape(-1).astype(np.float64).copy()
+    kappa = params["scaling"].astype(np.float64)
+    mean = accum / np.maximum(count, 1)
+    hot = alive & (mean > cfg["grad_threshold"]) & (count > 0)
+    smax = np.exp(kappa).max(axis=1)
+    clone = np.flatnonzero(hot & (smax <= cfg["split_scale_px"]))
+    split = np.flatnonzero(hot & (smax > cfg["split_scale_px"]))
+    if clone.size + 2 * split.size and n + clone.size + split.size > cfg["max_primitives"]:
+        clone = split = np.empty(0, np.int64)
+    pieces = {k: [a.astype(np.float64).reshape(n, -1)] for k, a in params.items()}
+    if clone.size:
+        o = _sigmoid_ref_f64(tau[clone])
+        o2 = 1.0 - np.power(1.0 - o, 1.0 / 2.0)
+        tc = np.log(o2 / (1.0 - o2))
+        for k in params:
+            pieces[k].append(pieces[k][0][clone].copy())
+        pieces["opacity"][-1][:, 0] = tc
+        pieces["opacity"][0][clone, 0] = tc
+    for _ in range(2 if split.size else 0):
+        child = {k: pieces[k][0][split].copy() for k in params}
+        gamma = rng.standard_normal((split.size, 3))
+        norms = np.linalg.norm(gamma, axis=1)
+        gamma *= (np.minimum(norms, 2.5) / np.maximum(norms, 1e-12))[:, None]
+        local = np.exp(child["scaling"]) * gamma
+        child["xyz"] += np.einsum("kij,kj->ki", quat_rotation_f64(child["rotation"]), local)
+        child["scaling"] -= np.log(cfg["split_shrink"])
+        for k in params:
+            pieces[k].append(child[k])
+    merged = {k: np.concatenate(p) for k, p in pieces.items()}
+    src = np.concatenate([np.arange(n), clone, split, split]).astype(np.int64)
+    nm = src.size
+    am = alive[src]
+    keep = np.ones(nm, bool)
+    keep[split] = False
+    prune = am & (_sigmoid_ref_f64(merged["opacity"][:, 0]) <= cfg["prune_opacity"])
+    n_pruned = int((prune & keep).sum())
+    keep &= ~prune
+    fresh = np.arange(nm) >= n
+    out_m = {k: np.where(fresh[:, None], 0.0, x.reshape(n, -1)[src])[keep] for k, x in m.items()}
+    out_v = {k: np.where(fresh[:, None], 0.0, x.reshape(n, -1)[src])[keep] for k, x in v.items()}
+    out_t = np.where(fresh, 0, t[src])[keep]
+    return ({k: x[keep] for k, x in merged.items()}, out_m, out_v, out_t, am[keep], src[keep],
+            (int(clone.size), int(split.size), n_pruned))

@@ -102,6 +102,10 @@ SIGNATURES = {
                                   C.c_int64, C.c_void_p, C.c_void_p, C.c_float, C.c_void_p,
                                   C.c_void_p]),
     "gs_build_flags": (C.c_int32, []),
+    "gs_step_rows_masked": (C.c_int, [C.POINTER(GsGroup), C.c_int32, C.POINTER(GsStepCfg),
+                                      C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,
+                                      C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p,
+                                      C.c_void_p]),
     "gs_stats_all_rows": (C.c_int, [C.POINTER(GsGroup), C.c_int32, C.c_int64, C.c_void_p,
                                     C.c_int64, C.c_void_p, C.c_float, C.c_void_p, C.c_void_p,
                                     C.c_size_t, C.c_void_p]),

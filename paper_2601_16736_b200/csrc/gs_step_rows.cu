@@ -33,6 +33,10 @@ int gs_step_fixed_try(const gs_group* groups, int32_t n_groups, const gs_step_cf
                       const int32_t* rows, const int32_t* n_rows_dev, int64_t max_rows,
                       float* record, int64_t record_stride, double* stats_out, double* partials,
                       unsigned int* counter, void* stream);
+int gs_step_fixed_masked_try(const gs_group* groups, int32_t n_groups, const gs_step_cfg* cfg,
+                             const uint8_t* mask, const int32_t* radii, int64_t n_rows,
+                             float* record, int64_t record_stride, double* stats_out,
+                             double* partials, unsigned int* counter, void* stream);
 
 namespace gs {
 
@@ -456,4 +460,51 @@ extern "C" int gs_step_rows(const gs_group* groups, int32_t n_groups, const gs_s
     return rc;
   }
   return gs_check_launch("gs_step_rows");
+}
+
+extern "C" int gs_step_rows_masked(const gs_group* groups, int32_t n_groups,
+                                   const gs_step_cfg* cfg, const uint8_t* mask,
+                                   const int32_t* radii, int64_t n_rows, float* record,
+                                   int64_t record_stride, double* stats_out, void* ws,
+                                   size_t ws_bytes, int32_t* launched, void* stream) {
+  using namespace gs;
+  if (!launched) {
+    gs_set_error("gs_step_rows_masked: launched must not be null");
+    return GS_ERR_ARG;
+  }
+  *launched = 0;
+  if (!groups || !cfg || n_groups < 1 || n_groups > GS_MAX_GROUPS || !record || !stats_out ||
+      n_rows < 0 || n_rows >= (int64_t)INT32_MAX || (!mask && !radii) || (mask && radii)) {
+    gs_set_error("gs_step_rows_masked: invalid arguments");
+    return GS_ERR_ARG;
+  }
+  if (cfg->mode < GS_MODE_COUPLED_ADAM || cfg->mode > GS_MODE_ADAMW_GS || !cfg->bias_lut ||
+      cfg->lut_len < 2 || (cfg->mode == GS_MODE_ADAMW_GS && !(cfg->n_pixels_rounded > 0.0))) {
+    gs_set_error("gs_step_rows_masked: invalid step configuration");
+    return GS_ERR_ARG;
+  }
+  if (!ws || ws_bytes < gs_step_rows_workspace_bytes()) {
+    gs_set_error("gs_step_rows_masked: workspace too small");
+    return GS_ERR_WORKSPACE;
+  }
+  for (int i = 0; i < n_groups; ++i) {
+    const gs_group& g = groups[i];
+    if (!g.param || !g.grad || g.width < 1) {
+      gs_set_error("gs_step_rows_masked: group %d invalid", i);
+      return GS_ERR_ARG;
+    }
+  }
+  if (cfg->densify_group >= n_groups ||
+      (cfg->densify_group >= 0 && (!cfg->densify_accum || !cfg->densify_count))) {
+    gs_set_error("gs_step_rows_masked: bad densification-statistics arguments");
+    return GS_ERR_ARG;
+  }
+  auto* hdr = reinterpret_cast<RowStepWorkspace*>(ws);
+  double* partials =
+      reinterpret_cast<double*>(reinterpret_cast<char*>(ws) + sizeof(RowStepWorkspace));
+  if (!gs_step_fixed_masked_try(groups, n_groups, cfg, mask, radii, n_rows, record, record_stride,
+                                stats_out, partials, &hdr->counter, stream))
+    return GS_OK;  // not this layout: the caller compacts and calls gs_step_rows
+  *launched = 1;
+  return gs_check_launch("gs_step_rows_masked");
 }

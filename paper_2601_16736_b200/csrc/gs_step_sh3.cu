@@ -26,6 +26,15 @@ extern template void launch_fixed<LayoutSH3, GS_MODE_ADAMW_GS, false>(const Fixe
 extern template void launch_fixed<LayoutSH3, GS_MODE_ADAMW_GS, true>(const FixedParams&, const TmaMaps*,
                                                           int64_t, int, cudaStream_t);
 
+extern template void launch_fixed_masked<LayoutSH3, GS_MODE_SPARSE_ADAM>(
+    const FixedParams&, const TmaMaps&, int64_t, int, const void*, cudaStream_t);
+extern template void launch_fixed_masked<LayoutSH3, GS_MODE_ADAMW_CONST>(
+    const FixedParams&, const TmaMaps&, int64_t, int, const void*, cudaStream_t);
+extern template void launch_fixed_masked<LayoutSH3, GS_MODE_ADAMW_CONST_CLIP>(
+    const FixedParams&, const TmaMaps&, int64_t, int, const void*, cudaStream_t);
+extern template void launch_fixed_masked<LayoutSH3, GS_MODE_ADAMW_GS>(
+    const FixedParams&, const TmaMaps&, int64_t, int, const void*, cudaStream_t);
+
 static int g_fixed_variant = -1;
 
 static bool g_fixed_variant_set = false;
@@ -160,28 +169,28 @@ extern "C" int32_t gs_set_fixed_variant(int32_t variant) {
   return prev;
 }
 
-// Called by gs_step_rows (gs_step_rows.cu) after argument validation; returns
-// 1 if a compiled fixed layout handled the launch, 0 otherwise.
-int gs_step_fixed_try(const gs_group* groups, int32_t n_groups, const gs_step_cfg* cfg,
-                      const int32_t* rows, const int32_t* n_rows_dev, int64_t max_rows,
-                      float* record, int64_t record_stride, double* stats_out, double* partials,
-                      unsigned int* counter, void* stream) {
-  using namespace gs;
-  if (fixed_variant() < 0) return 0;  // fixed-layout path disabled
-  if (!layout_matches<LayoutSH3>(groups, n_groups)) return 0;
+namespace gs {
+
+// The launch parameters of the fixed-layout kernels; false if the layout or
+// the record does not fit them.  tma4: the 2-D TMA kernel may run.
+static bool fixed_setup(const gs_group* groups, int32_t n_groups, const gs_step_cfg* cfg,
+                        const int32_t* rows, const int32_t* n_rows_dev, int64_t max_rows,
+                        float* record, int64_t record_stride, double* stats_out, double* partials,
+                        unsigned int* counter, FixedParams& P, int& kind, bool& tma4) {
+  if (fixed_variant() < 0) return false;  // fixed-layout path disabled
+  if (!layout_matches<LayoutSH3>(groups, n_groups)) return false;
   // every fixed-layout kernel copies the state record in 16-byte pieces
-  if (record_stride % 4 != 0 || (reinterpret_cast<uintptr_t>(record) & 15u) != 0) return 0;
-  FixedParams P{};
-  const int kind = rows_kind<LayoutSH3>(groups, max_rows, P);
-  if (kind < 0) return 0;  // 32-bit element offsets
+  if (record_stride % 4 != 0 || (reinterpret_cast<uintptr_t>(record) & 15u) != 0) return false;
+  P = FixedParams{};
+  kind = rows_kind<LayoutSH3>(groups, max_rows, P);
+  if (kind < 0) return false;  // 32-bit element offsets
   P.tma_ok = kind == 2 && P.grec_ca == 0 && record_stride % 4 == 0 &&
              (reinterpret_cast<uintptr_t>(record) & 15u) == 0;
   // 2-D TMA kernel: device-resident records, 16-byte row strides, whole
   // 64-float parameter / gradient rows and a state row of >= 2(P+1) floats
   constexpr int kPT = Tma4Stage<LayoutSH3, 32>::kPT;
-  const bool tma4 = P.tma_ok && P.prs >= kPT && P.grs >= kPT && P.prs % 4 == 0 &&
-                    P.grs % 4 == 0 && record_stride >= 2 * (LayoutSH3::P + 1) &&
-                    max_rows <= INT32_MAX;
+  tma4 = P.tma_ok && P.prs >= kPT && P.grs >= kPT && P.prs % 4 == 0 && P.grs % 4 == 0 &&
+         record_stride >= 2 * (LayoutSH3::P + 1) && max_rows <= INT32_MAX;
   for (int i = 0; i < n_groups; ++i)
     P.g[i] = FixedGroup{
         groups[i].param, groups[i].grad, groups[i].lr,
@@ -205,6 +214,24 @@ int gs_step_fixed_try(const gs_group* groups, int32_t n_groups, const gs_step_cf
   P.stats_out = stats_out;
   P.partials = partials;
   P.counter = counter;
+  return true;
+}
+
+}  // namespace gs
+
+// Called by gs_step_rows (gs_step_rows.cu) after argument validation; returns
+// 1 if a compiled fixed layout handled the launch, 0 otherwise.
+int gs_step_fixed_try(const gs_group* groups, int32_t n_groups, const gs_step_cfg* cfg,
+                      const int32_t* rows, const int32_t* n_rows_dev, int64_t max_rows,
+                      float* record, int64_t record_stride, double* stats_out, double* partials,
+                      unsigned int* counter, void* stream) {
+  using namespace gs;
+  FixedParams P;
+  int kind = 0;
+  bool tma4 = false;
+  if (!fixed_setup(groups, n_groups, cfg, rows, n_rows_dev, max_rows, record, record_stride,
+                   stats_out, partials, counter, P, kind, tma4))
+    return 0;
   cudaStream_t s = (cudaStream_t)stream;
   TmaMaps maps;
   const TmaMaps* M = nullptr;
@@ -213,5 +240,44 @@ int gs_step_fixed_try(const gs_group* groups, int32_t n_groups, const gs_step_cf
     dispatch_fixed<LayoutSH3, true>(cfg->mode, P, M, max_rows, kind, s);
   else
     dispatch_fixed<LayoutSH3, false>(cfg->mode, P, M, max_rows, kind, s);
+  return 1;
+}
+
+// The fused compaction + step (gs_step_rows_masked): 1 if launched.  Needs
+// the TMA record kernel, the fused check and a mode whose step does not
+// depend on the global visible count (not the coupled normaliser N_v).
+int gs_step_fixed_masked_try(const gs_group* groups, int32_t n_groups, const gs_step_cfg* cfg,
+                             const uint8_t* mask, const int32_t* radii, int64_t n_rows,
+                             float* record, int64_t record_stride, double* stats_out,
+                             double* partials, unsigned int* counter, void* stream) {
+  using namespace gs;
+  if (cfg->check != GS_CHECK_FUSED || cfg->mode == GS_MODE_COUPLED_ADAM) return 0;
+  if (cfg->mode == GS_MODE_SPARSE_ADAM && (cfg->lambda_opacity != 0.0 || cfg->lambda_scale != 0.0))
+    return 0;
+  if (fixed_variant() == 21 || n_rows < 1) return 0;
+  FixedParams P;
+  int kind = 0;
+  bool tma4 = false;
+  if (!fixed_setup(groups, n_groups, cfg, nullptr, nullptr, n_rows, record, record_stride,
+                   stats_out, partials, counter, P, kind, tma4) ||
+      kind != 2 || !tma4)
+    return 0;
+  TmaMaps maps;
+  if (!encode_tma_maps(P, n_rows, 2 * (LayoutSH3::P + 1), &maps)) return 0;
+  const int mk = radii ? 2 : 1;
+  const void* m = radii ? static_cast<const void*>(radii) : static_cast<const void*>(mask);
+  cudaStream_t s = (cudaStream_t)stream;
+  switch (cfg->mode) {
+    case GS_MODE_SPARSE_ADAM:
+      launch_fixed_masked<LayoutSH3, GS_MODE_SPARSE_ADAM>(P, maps, n_rows, mk, m, s);
+      break;
+    case GS_MODE_ADAMW_CONST:
+      launch_fixed_masked<LayoutSH3, GS_MODE_ADAMW_CONST>(P, maps, n_rows, mk, m, s);
+      break;
+    case GS_MODE_ADAMW_CONST_CLIP:
+      launch_fixed_masked<LayoutSH3, GS_MODE_ADAMW_CONST_CLIP>(P, maps, n_rows, mk, m, s);
+      break;
+    default: launch_fixed_masked<LayoutSH3, GS_MODE_ADAMW_GS>(P, maps, n_rows, mk, m, s); break;
+  }
   return 1;
 }

@@ -1981,4 +1981,15 @@ void launch_fixed(const FixedParams& P, const TmaMaps* M, int64_t max_rows, int 
   launch_ws<L, MODE, STRICT, 32, 2, 3, 8, 2>(P, max_rows, s);
 }
 
+// Fused K1 + K2 on records (the fused check): the TMA kernel's loader
+// compacts the visibility mask itself (mask_kind 1: uint8, 2: int32 radii).
+template <class L, int MODE>
+void launch_fixed_masked(const FixedParams& P, const TmaMaps& M, int64_t n_rows, int mask_kind,
+                         const void* mask, cudaStream_t s) {
+  if (mask_kind == 2)
+    launch_tma4<L, MODE, false, 3, 8, 2, 2>(P, M, n_rows, s, mask);
+  else
+    launch_tma4<L, MODE, false, 3, 8, 2, 1>(P, M, n_rows, s, mask);
+}
+
 }  // namespace gs

@@ -81,9 +81,12 @@ __device__ __forceinline__ void tma_scatter4(const CUtensorMap* map, const void*
       : "memory");
 }
 
-template <class L, int MODE, bool STRICT, int S, int NCW, int MINB>
+// MASK: 0 = the compacted index list (P.rows, *P.n_rows_dev rows; dense
+// mode: every row), 1 = a uint8 visibility mask, 2 = int32 radii (> 0 is
+// visible): the loader compacts the mask itself (fused K1, below).
+template <class L, int MODE, bool STRICT, int S, int NCW, int MINB, int MASK>
 __global__ void __launch_bounds__((NCW + 2) * 32, MINB)
-    step_tma4_kernel(const FixedParams P, const __grid_constant__ TmaMaps M) {
+    step_tma4_kernel(const FixedParams P, const __grid_constant__ TmaMaps M, const void* vis_mask) {
   constexpr int R = 32;
   constexpr bool kDense = MODE == GS_MODE_COUPLED_ADAM;
   constexpr bool kCoupled = MODE == GS_MODE_COUPLED_ADAM || MODE == GS_MODE_SPARSE_ADAM;
@@ -101,6 +104,9 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB)
   __shared__ int s_any[S];
   __shared__ float2 s_bc[S][R];
   __shared__ uint32_t s_crow[S][R];
+  __shared__ int s_nv[S];  // rows of the chunk in the stage; -1 ends the CTA's chunk stream
+  constexpr int kPend = MASK != 0 ? 1024 : 1;  // pending visible ids (fused compaction)
+  __shared__ uint32_t s_pend[kPend];
   __shared__ double s_red[GS_STEP_STATS * (NCW + 2)];
   // TMA boxes land 128-byte aligned (the host adds 128 bytes of slack)
   unsigned char* const smem = reinterpret_cast<unsigned char*>(
@@ -108,7 +114,7 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB)
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
-  int n_rows = kDense ? (int)P.max_rows : *P.n_rows_dev;
+  int n_rows = (kDense || MASK != 0) ? (int)P.max_rows : *P.n_rows_dev;
   if (STRICT && *P.abort_flag != 0) n_rows = 0;
   const int n_chunks = (n_rows + R - 1) / R;
   const int G = (int)gridDim.x;
@@ -140,54 +146,165 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB)
 
   if (warp == NCW) {
     // ------------------------------------------------------------------ loader
-    auto fetch_id = [&](int c) -> int {
-      if (c >= n_chunks || lane >= chunk_rows(c)) return oob;
-      const int i = c * R + lane;
-      return kDense ? i : __ldg(P.rows + i);
-    };
-    int next_id = fetch_id((int)blockIdx.x);
-    int st = 0;
+    int st = 0, k = 0;
     unsigned ph = 0;
-    for (int c = (int)blockIdx.x, k = 0; c < n_chunks; c += G, ++k) {
-      const int my_id = next_id;
-      next_id = fetch_id(c + G);
+    // one chunk into the next stage: lane i's row id (oob past nv), nv rows;
+    // nv < 0 ends the stream (no data, the consumers and the storer exit)
+    auto emit = [&](int my_id, int nv) {
       if (k >= S) mbar_wait(&empty_bar[st], ph ^ 1u);
       unsigned char* sb = stage(st);
-      if (lane == 0) mbar_expect_tx(&full_bar[st], ST::kBytes);
-      __syncwarp();
-      const int q = (4 * lane) & 31;
-      const int r0 = __shfl_sync(0xffffffffu, my_id, q);
-      const int r1 = __shfl_sync(0xffffffffu, my_id, q + 1);
-      const int r2 = __shfl_sync(0xffffffffu, my_id, q + 2);
-      const int r3 = __shfl_sync(0xffffffffu, my_id, q + 3);
-      if (lane < R / 4) {
-        tma_gather4(sb + lane * 4 * ST::kRecRow, &M.rec, r0, r1, r2, r3, &full_bar[st]);
-        tma_gather4(sb + ST::kRec + lane * 4 * PT * 4, &M.prm, r0, r1, r2, r3, &full_bar[st]);
-        tma_gather4(sb + ST::kRec + ST::kTh + lane * 4 * PT * 4, &M.grd, r0, r1, r2, r3,
-                    &full_bar[st]);
+      if (nv > 0) {
+        if (lane == 0) mbar_expect_tx(&full_bar[st], ST::kBytes);
+        __syncwarp();
+        const int q = (4 * lane) & 31;
+        const int r0 = __shfl_sync(0xffffffffu, my_id, q);
+        const int r1 = __shfl_sync(0xffffffffu, my_id, q + 1);
+        const int r2 = __shfl_sync(0xffffffffu, my_id, q + 2);
+        const int r3 = __shfl_sync(0xffffffffu, my_id, q + 3);
+        if (lane < R / 4) {
+          tma_gather4(sb + lane * 4 * ST::kRecRow, &M.rec, r0, r1, r2, r3, &full_bar[st]);
+          tma_gather4(sb + ST::kRec + lane * 4 * PT * 4, &M.prm, r0, r1, r2, r3, &full_bar[st]);
+          tma_gather4(sb + ST::kRec + ST::kTh + lane * 4 * PT * 4, &M.grd, r0, r1, r2, r3,
+                      &full_bar[st]);
+        }
+        // row ids and bias factors of the row's next clock ride the stage, so
+        // the consumers touch no global memory before their barrier
+        if (my_id != oob) {
+          s_crow[st][lane] = (uint32_t)my_id;
+          const int tb = kDense ? P.global_t
+                                : __ldg(reinterpret_cast<const int*>(P.record + (size_t)my_id * P.stride +
+                                                                     2 * L::P)) + 1;
+          s_bc[st][lane] = __ldg(reinterpret_cast<const float2*>(P.lut) + (tb < P.lut_len ? tb : P.lut_len - 1));
+        }
       }
-      // row ids and bias factors of the row's next clock ride the stage, so
-      // the consumers touch no global memory before their barrier
-      if (my_id != oob) {
-        s_crow[st][lane] = (uint32_t)my_id;
-        const int tb = kDense ? P.global_t
-                              : __ldg(reinterpret_cast<const int*>(P.record + (size_t)my_id * P.stride +
-                                                                   2 * L::P)) + 1;
-        s_bc[st][lane] = __ldg(reinterpret_cast<const float2*>(P.lut) + (tb < P.lut_len ? tb : P.lut_len - 1));
-      }
+      if (lane == 0) s_nv[st] = nv;
       mbar_arrive(&full_bar[st]);
+      ++k;
       if (++st == S) {
         st = 0;
         ph ^= 1u;
       }
+    };
+    if constexpr (MASK == 0) {
+      auto fetch_id = [&](int c) -> int {
+        if (c >= n_chunks || lane >= chunk_rows(c)) return oob;
+        const int i = c * R + lane;
+        return kDense ? i : __ldg(P.rows + i);
+      };
+      int next_id = fetch_id((int)blockIdx.x);
+      for (int c = (int)blockIdx.x; c < n_chunks; c += G) {
+        const int my_id = next_id;
+        next_id = fetch_id(c + G);
+        emit(my_id, chunk_rows(c));
+      }
+    } else {
+      // fused compaction: the CTA takes tiles of kMaskTile rows grid-stride;
+      // each lane loads 16 mask entries per block of 512 rows (the next
+      // tile's loads in flight while this one is scanned), a warp scan packs
+      // the visible ids into a ring of pending ids in shared memory, and
+      // every 32 of them leave as one chunk
+      constexpr int kMaskTile = MASK == 1 ? 2048 : 512;  // 16 mask bytes or 64 radii bytes / lane
+      constexpr int kBlocks = kMaskTile / 512;
+      constexpr int kQ = MASK == 1 ? 1 : 4;  // 16-byte loads per lane per block
+      using Vec = uint4;
+      const int64_t nr = n_rows;
+      const int n_tiles = (int)((nr + kMaskTile - 1) / kMaskTile);
+      const bool vec_ok = (reinterpret_cast<uintptr_t>(vis_mask) & 15u) == 0;
+      Vec cur[kBlocks][kQ], nxt[kBlocks][kQ];
+      auto load_tile = [&](int tile, Vec (&buf)[kBlocks][kQ]) {
+#pragma unroll
+        for (int b = 0; b < kBlocks; ++b) {
+          const int64_t row0 = (int64_t)tile * kMaskTile + b * 512 + lane * 16;
+#pragma unroll
+          for (int q = 0; q < kQ; ++q) {
+            buf[b][q] = make_uint4(0u, 0u, 0u, 0u);
+            if (tile < n_tiles && row0 + 16 <= nr && vec_ok) {
+              if constexpr (MASK == 1)
+                buf[b][q] = __ldg(reinterpret_cast<const uint4*>(
+                    reinterpret_cast<const uint8_t*>(vis_mask) + row0));
+              else
+                buf[b][q] = __ldg(reinterpret_cast<const uint4*>(
+                    reinterpret_cast<const int32_t*>(vis_mask) + row0) + q);
+            } else if (tile < n_tiles) {  // ragged end or unaligned mask: element loads
+              uint32_t w[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const int64_t r = row0 + 4 * q + j;
+                if constexpr (MASK == 1) {
+#pragma unroll
+                  for (int e = 0; e < 4; ++e) {
+                    const int64_t rr = row0 + 4 * j + e;
+                    if (q == 0 && rr < nr)
+                      w[j] |= (uint32_t)reinterpret_cast<const uint8_t*>(vis_mask)[rr] << (8 * e);
+                  }
+                } else {
+                  if (r < nr) w[j] = (uint32_t)reinterpret_cast<const int32_t*>(vis_mask)[r];
+                }
+              }
+              buf[b][q] = make_uint4(w[0], w[1], w[2], w[3]);
+            }
+          }
+        }
+      };
+      auto bits_of = [&](const Vec (&v)[kQ]) -> uint32_t {  // bit j: row lane*16 + j visible
+        uint32_t bits = 0;
+        if constexpr (MASK == 1) {
+          const uint32_t w[4] = {v[0].x, v[0].y, v[0].z, v[0].w};
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) bits |= (((w[j] >> (8 * e)) & 0xffu) != 0u) << (4 * j + e);
+        } else {
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            bits |= (uint32_t)((int)v[q].x > 0) << (4 * q) | (uint32_t)((int)v[q].y > 0) << (4 * q + 1) |
+                    (uint32_t)((int)v[q].z > 0) << (4 * q + 2) | (uint32_t)((int)v[q].w > 0) << (4 * q + 3);
+        }
+        return bits;
+      };
+      int head = 0, tail = 0;  // ring of pending ids: s_pend[head .. tail)
+      int tile = (int)blockIdx.x;
+      load_tile(tile, cur);
+      for (; tile < n_tiles; tile += G) {
+        load_tile(tile + G, nxt);
+#pragma unroll
+        for (int b = 0; b < kBlocks; ++b) {
+          const uint32_t bits = bits_of(cur[b]);
+          const int cnt = __popc(bits);
+          int incl = cnt;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+          }
+          const int total = __shfl_sync(0xffffffffu, incl, 31);
+          int pos = tail + incl - cnt;
+          const int row0 = tile * kMaskTile + b * 512 + lane * 16;
+          for (uint32_t x = bits; x; x &= x - 1) s_pend[(pos++) & (kPend - 1)] = row0 + __ffs(x) - 1;
+          tail += total;
+          __syncwarp();
+          while (tail - head >= R) {
+            emit((int)s_pend[(head + lane) & (kPend - 1)], R);
+            head += R;
+          }
+        }
+#pragma unroll
+        for (int b = 0; b < kBlocks; ++b)
+#pragma unroll
+          for (int q = 0; q < kQ; ++q) cur[b][q] = nxt[b][q];
+      }
+      if (tail > head) emit(lane < tail - head ? (int)s_pend[(head + lane) & (kPend - 1)] : oob,
+                            tail - head);
     }
+    emit(oob, -1);
   } else if (warp == NCW + 1) {
     // ------------------------------------------------------------------ storer
     int st = 0;
     unsigned ph = 0;
-    for (int c = (int)blockIdx.x; c < n_chunks; c += G) {
-      const int nv = chunk_rows(c);
+    for (;;) {
       mbar_wait(&done_bar[st], ph);
+      const int nv = s_nv[st];
+      if (nv < 0) break;
       const int my_id = lane < nv ? (int)s_crow[st][lane] : oob;
       const unsigned char* sb = stage(st);
       const int q = (4 * lane) & 31;
@@ -221,9 +338,13 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB)
     const StepConsts& K = kCoupled ? Kc : P.K;
     int st = 0;
     int ep = 1;  // this use of stage st (epoch tag of its row flags)
-    for (int c = (int)blockIdx.x; c < n_chunks; c += G) {
-      const int nvalid = chunk_rows(c);
+    for (;;) {
       mbar_wait(&full_bar[st], (unsigned)((ep - 1) & 1));
+      const int nvalid = s_nv[st];
+      if (nvalid < 0) {
+        mbar_arrive(&done_bar[st]);  // the storer reads the end marker too
+        break;
+      }
       unsigned char* sb = stage(st);
       float2* srec = reinterpret_cast<float2*>(sb);
       float* sth = reinterpret_cast<float*>(sb + ST::kRec);
@@ -370,14 +491,17 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB)
 // runtime's driver entry point; no libcuda link dependency).
 bool encode_tma_maps(const FixedParams& P, int64_t n_rows, int rec_box, TmaMaps* out);
 
-template <class L, int MODE, bool STRICT, int S, int NCW, int MINB>
-void launch_tma4(const FixedParams& P, const TmaMaps& M, int64_t max_rows, cudaStream_t s) {
+template <class L, int MODE, bool STRICT, int S, int NCW, int MINB, int MASK = 0>
+void launch_tma4(const FixedParams& P, const TmaMaps& M, int64_t max_rows, cudaStream_t s,
+                 const void* vis_mask = nullptr) {
   constexpr int bytes = S * Tma4Stage<L, 32>::kBytes + 128;
-  smem_opt_in<step_tma4_kernel<L, MODE, STRICT, S, NCW, MINB>>(bytes);
-  const int64_t chunks = (max_rows + 31) / 32;
+  smem_opt_in<step_tma4_kernel<L, MODE, STRICT, S, NCW, MINB, MASK>>(bytes);
+  const int64_t tile = MASK == 1 ? 2048 : MASK == 2 ? 512 : 32;
+  const int64_t work = (max_rows + tile - 1) / tile;
   const int grid =
-      (int)std::max<int64_t>(1, std::min<int64_t>(chunks, (int64_t)gs_sm_count() * MINB));
-  step_tma4_kernel<L, MODE, STRICT, S, NCW, MINB><<<grid, (NCW + 2) * 32, bytes, s>>>(P, M);
+      (int)std::max<int64_t>(1, std::min<int64_t>(work, (int64_t)gs_sm_count() * MINB));
+  step_tma4_kernel<L, MODE, STRICT, S, NCW, MINB, MASK>
+      <<<grid, (NCW + 2) * 32, bytes, s>>>(P, M, vis_mask);
 }
 
 }  // namespace gs

@@ -108,6 +108,10 @@ def _strides(t: torch.Tensor | None):
 
 
 _raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+# NVTX ranges around the kernel launches (K1 compaction, K2 step, K3 state
+# scatters, K4 statistics) for nsys / ncu --nvtx; host cost ~1 us per range
+_nvtx_push = torch.cuda.nvtx.range_push
+_nvtx_pop = torch.cuda.nvtx.range_pop
 
 
 def _stream_handle(device: torch.device) -> int:
@@ -213,6 +217,7 @@ class StepEngine:
         self._record_ok = None
         self._cfg_key = None
         self._cfg = None
+        self._launched = C.c_int32(0)
         self._omb1 = float(np.float32(1.0 - self.beta1))
         self._omb2 = float(np.float32(1.0 - self.beta2))
         self._eps32 = {}
@@ -287,15 +292,17 @@ class StepEngine:
             raise ConfigError("visibility must be contiguous")
         s = _stream_handle(self.device)
         ws, wsb = self.compact_ws.data_ptr(), self.compact_ws.numel()
-        if vis.dtype in (torch.bool, torch.uint8):
-            rc = self.lib.gs_compact_u8(vis.data_ptr(), self.n_rows, self.idx.data_ptr(),
-                                        self.count.data_ptr(), ws, wsb, s)
-        elif vis.dtype == torch.int32:
+        if vis.dtype not in (torch.bool, torch.uint8, torch.int32):
+            raise ConfigError(f"visibility dtype {vis.dtype} not supported (bool/uint8 mask or "
+                              "int32 radii)")
+        _nvtx_push("gs.K1.compact")
+        if vis.dtype == torch.int32:
             rc = self.lib.gs_compact_i32(vis.data_ptr(), self.n_rows, self.idx.data_ptr(),
                                          self.count.data_ptr(), ws, wsb, s)
         else:
-            raise ConfigError(f"visibility dtype {vis.dtype} not supported (bool/uint8 mask or "
-                              "int32 radii)")
+            rc = self.lib.gs_compact_u8(vis.data_ptr(), self.n_rows, self.idx.data_ptr(),
+                                        self.count.data_ptr(), ws, wsb, s)
+        _nvtx_pop()
         L.check(rc, "gs_compact")
         self.launches += 2 if self.n_rows > 0 else 0  # count + write passes
         return self.idx, self.count
@@ -443,6 +450,18 @@ class StepEngine:
                                   clip_scale, n_pixels_rounded, global_t, n_visible_dev,
                                   n_visible_host, fused_densify)
             self._cfg_key, self._cfg = ckey, cfg
+        _nvtx_push("gs.K2.step")
+        try:
+            self._launch_step(groups, garr, cfg, mode, check, clock, rows, count, record,
+                              lambda_opacity, lambda_scale, s, abort_hook)
+        finally:
+            _nvtx_pop()
+        if densify_rows is not None and densify is not None and mode == "coupled-adam":
+            self._densify_listed(garr, densify, *densify_rows, strict=check == "strict")
+        return self.stats
+
+    def _launch_step(self, groups, garr, cfg, mode, check, clock, rows, count, record,
+                     lambda_opacity, lambda_scale, s, abort_hook):
         if check == "strict":
             # the penalty's activation domain is checked where the penalty
             # applies: listed rows, or every row for the dense coupled mode
@@ -465,8 +484,47 @@ class StepEngine:
                                        self.rows_ws.numel(), s)
             L.check(rc, "gs_step_rows")
         self.launches += 2 if check == "strict" else 1
-        if densify_rows is not None and densify is not None and mode == "coupled-adam":
-            self._densify_listed(garr, densify, *densify_rows, strict=check == "strict")
+
+    def step_masked(self, groups: list[GroupBinding], mode: str, vis: torch.Tensor, *, eps: float,
+                    lambda_opacity: float = 0.0, lambda_scale: float = 0.0,
+                    clip_opacity: float = 10.0, clip_scale: float = 10.0,
+                    n_pixels_rounded: float = 0.0, record: torch.Tensor,
+                    densify: tuple | None = None) -> torch.Tensor | None:
+        """Fused K1 + K2 (gs_step_rows_masked): the step of the mask's visible
+        rows with the compaction done inside the step kernel.  Returns the
+        statistics, or None when the layout does not take this path (the
+        caller then compacts and calls :meth:`step`).  The index list
+        (``idx`` / ``count``) is not produced."""
+        if vis.device != self.device or vis.dim() != 1 or vis.shape[0] != self.n_rows or \
+                not vis.is_contiguous() or vis.dtype not in (torch.bool, torch.uint8, torch.int32):
+            return None
+        self._check_record(record, groups)
+        garr = self.group_array(groups)
+        ckey = (mode, "fused", eps, float(lambda_opacity), float(lambda_scale),
+                float(clip_opacity), float(clip_scale), float(n_pixels_rounded), 0, None, 0.0,
+                None if densify is None else (densify[0].data_ptr(), densify[1].data_ptr(),
+                                              float(densify[2]), int(densify[3])))
+        if ckey == self._cfg_key:
+            cfg = self._cfg
+        else:
+            cfg = self._build_cfg(mode, "fused", eps, lambda_opacity, lambda_scale, clip_opacity,
+                                  clip_scale, n_pixels_rounded, 0, None, 0.0, densify)
+            self._cfg_key, self._cfg = ckey, cfg
+        launched = self._launched
+        is_radii = vis.dtype == torch.int32
+        _nvtx_push("gs.K1K2.step_masked")
+        rc = self.lib.gs_step_rows_masked(garr, len(groups), C.byref(cfg),
+                                          None if is_radii else vis.data_ptr(),
+                                          vis.data_ptr() if is_radii else None, self.n_rows,
+                                          record.data_ptr(), record.stride(0),
+                                          self.stats.data_ptr(), self.rows_ws.data_ptr(),
+                                          self.rows_ws.numel(), C.byref(launched),
+                                          _stream_handle(self.device))
+        _nvtx_pop()
+        L.check(rc, "gs_step_rows_masked")
+        if not launched.value:
+            return None
+        self.launches += 1
         return self.stats
 
     def _densify_listed(self, garr, densify, rows, count, strict: bool):
@@ -596,6 +654,7 @@ class StepEngine:
             raise ConfigError("RSR factors must lie in [0, 1)")
         rows, k = self._rows_device(indices)
         s = _stream_handle(self.device)
+        _nvtx_push("gs.K3.rsr")
         if record is not None:
             self._check_record(record, groups)
             rc = self.lib.gs_rsr_apply_rows(record.data_ptr(), record.stride(0),
@@ -606,6 +665,7 @@ class StepEngine:
             garr = self.group_array(groups, need_grad=False)
             rc = self.lib.gs_rsr_apply(garr, len(groups), rows.data_ptr() if k else None, k,
                                        self.n_rows, float(alpha1), float(alpha2), s)
+        _nvtx_pop()
         L.check(rc, "gs_rsr_apply")
         self.launches += 1 if k else 0
         self._rows_tmp = rows  # keep alive until the kernel has consumed it
@@ -614,6 +674,7 @@ class StepEngine:
                    record: torch.Tensor | None = None):
         rows, k = self._rows_device(indices)
         s = _stream_handle(self.device)
+        _nvtx_push("gs.K3.reset")
         if record is not None:
             self._check_record(record, groups)
             rc = self.lib.gs_reset_rows_rows(record.data_ptr(), record.stride(0),
@@ -623,6 +684,7 @@ class StepEngine:
             garr = self.group_array(groups, need_grad=False)
             rc = self.lib.gs_reset_rows(garr, len(groups), clock.data_ptr(),
                                         rows.data_ptr() if k else None, k, self.n_rows, s)
+        _nvtx_pop()
         L.check(rc, "gs_reset_rows")
         self.launches += 1 if k else 0
         self._rows_tmp = rows
@@ -636,6 +698,7 @@ class StepEngine:
                 raise ConfigError("alive must be a bool/uint8 mask over the rows")
             alive = alive.contiguous()
         s = _stream_handle(self.device)
+        _nvtx_push("gs.K4.stats")
         if record is not None:
             self._check_record(record, groups)
             rc = self.lib.gs_stats_all_rows(garr, len(groups), self.n_rows, record.data_ptr(),
@@ -647,5 +710,6 @@ class StepEngine:
             rc = self.lib.gs_stats_all(garr, len(groups), self.n_rows, _ptr(alive),
                                        float(self.active_logit), self.stats_all_out.data_ptr(),
                                        self.stats_ws.data_ptr(), self.stats_ws.numel(), s)
+        _nvtx_pop()
         L.check(rc, "gs_stats_all")
         return self.stats_all_out[: 2 + 5 * len(groups)]

@@ -237,7 +237,7 @@ class AdamWGS:
                  lambda_o: float = 0.0, lambda_s: float = 0.0, ct_opacity: float = 10.0,
                  ct_scale: float = 10.0, round_n_pixels: bool = True, check: str = "fused",
                  errors: str = "defer", state_layout: str = "rows",
-                 state_row_align: int = 16, adopt="auto"):
+                 state_row_align: int = 16, adopt="auto", fused_compaction: bool = True):
         validate_hyper(mode, betas[0], betas[1], eps, ct_opacity, ct_scale)
         if check not in CHECKS:
             raise ConfigError(f"check must be one of {CHECKS}")
@@ -250,6 +250,7 @@ class AdamWGS:
         self.ct_opacity, self.ct_scale = float(ct_opacity), float(ct_scale)
         self.round_n_pixels = bool(round_n_pixels)
         self.check, self.errors = check, errors
+        self.fused_compaction = bool(fused_compaction)
 
         self.param_groups = []
         for i, g in enumerate(params):
@@ -409,6 +410,11 @@ class AdamWGS:
         else:
             if visibility is None:
                 raise ConfigError(f"{mode} needs the visibility mask")
+            stats = self._step_fused(b, mode, visibility, n_pixels, lo, ls, clip, kw)
+            if stats is not None:
+                self._last_ctx = (b, None, None, lo, ls, mode, visibility)
+                self._after_step(stats)
+                return
             rows, count = eng.compact(visibility)
             kw["abort_hook"] = self._abort_reduce
             if mode == "adamw-gs":
@@ -434,8 +440,33 @@ class AdamWGS:
                         else self._nv_reduce(count)
                 stats = eng.step(b, mode, self.state.clock, rows=rows, count=count,
                                  lambda_opacity=lo, lambda_scale=ls, n_visible_dev=nv, **kw)
-        self._last_ctx = (b, rows, count, lo, ls, mode)
+        self._last_ctx = (b, rows, count, lo, ls, mode, visibility)
         self._after_step(stats)
+
+    def _step_fused(self, b, mode, visibility, n_pixels, lo, ls, clip, kw):
+        """K1 fused into K2 (engine.step_masked) where it applies; None otherwise."""
+        if not self.fused_compaction or self.check != "fused" or self.state.record is None:
+            return None
+        if mode == "sparse-adam" and (lo != 0.0 or ls != 0.0):
+            return None  # the coupled normaliser needs N_v before the step
+        eng = self.engine
+        kwm = dict(eps=self.eps, record=self.state.record, densify=kw.get("densify"))
+        if mode == "adamw-gs":
+            if n_pixels is None:
+                raise ConfigError("adamw-gs needs n_pixels (N_I)")
+            n_i = round_pixel_count(int(n_pixels), self.round_n_pixels)
+            return eng.step_masked(b, mode, visibility, lambda_opacity=lo, lambda_scale=ls,
+                                   clip_opacity=self.ct_opacity, clip_scale=self.ct_scale,
+                                   n_pixels_rounded=n_i, **kwm)
+        if mode in ("adamw-const", "adamw-const-clip"):
+            c = clip if clip is not None else (self.ct_opacity if mode == "adamw-const-clip"
+                                               else None)
+            m = "adamw-const-clip" if c is not None else "adamw-const"
+            cv = float(c) if c is not None else 0.0
+            return eng.step_masked(b, m, visibility, lambda_opacity=self.lambda_o,
+                                   lambda_scale=self.lambda_s, clip_opacity=cv, clip_scale=cv,
+                                   **kwm)
+        return eng.step_masked(b, mode, visibility, **kwm)  # plain sparse Adam
 
     # ---------------------------------------------------------------- errors
     def _after_step(self, stats: torch.Tensor):
@@ -600,9 +631,11 @@ class AdamWGS:
         if not (bad_g or bad_d):
             return
         self._pending.clear()  # later steps' checks are superseded by this error
-        b, rows, count, lo, ls, mode = ctx
+        b, rows, count, lo, ls, mode, vis = ctx
         if mode == "coupled-adam":
             rows, count = self.engine.all_rows()
+        elif rows is None:  # the fused step made no index list
+            rows, count = self.engine.compact(vis)
         # ids from the failing step's gradient bindings (deferred: the caller
         # keeps those buffers until the error surfaces, or uses errors="raise")
         g_ids, d_ids = self.engine.bad_rows(b, rows, count, lo, ls)

@@ -224,9 +224,11 @@ class ShardedAdamWGS:
         if not (bad_g or bad_d):
             return
         self._pending.clear()
-        b, rows, count, lo, ls, mode = ctx
+        b, rows, count, lo, ls, mode, vis = ctx
         if mode == "coupled-adam":
             rows, count = opt.engine.all_rows()
+        elif rows is None:  # the fused step made no index list
+            rows, count = opt.engine.compact(vis)
         g_ids, d_ids = opt.engine.bad_rows(b, rows, count, lo, ls)
         mine = (np.asarray(g_ids, np.int64) + self.lo, np.asarray(d_ids, np.int64) + self.lo)
         allv = [None] * self.world
@@ -245,6 +247,9 @@ class ShardedAdamWGS:
     def global_rows(self) -> torch.Tensor:
         """This shard's visible rows in global numbering (after a step)."""
         eng = self.opt.engine
+        ctx = self.opt._last_ctx
+        if ctx is not None and ctx[1] is None and ctx[-1] is not None:
+            eng.compact(ctx[-1])  # the fused step made no index list
         c = int(eng.count.item())
         return eng.idx[:c].to(torch.int64) + self.lo
 

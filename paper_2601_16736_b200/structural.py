@@ -121,11 +121,33 @@ def _logit_checked(o: np.ndarray) -> np.ndarray:
     return np.log(o / (1.0 - o))
 
 
+def quat_rotation(q: np.ndarray) -> np.ndarray:
+    """[k, 3, 3] rotation matrices of (w, x, y, z) quaternions, normalised
+    (the 3DGS convention, as gs_noise.cu builds them)."""
+    q = np.asarray(q, np.float64)
+    q = q / np.maximum(np.linalg.norm(q, axis=1, keepdims=True), 1e-12)
+    w, x, y, z = q.T
+    r = np.empty((q.shape[0], 3, 3))
+    r[:, 0, 0] = 1 - 2 * (y * y + z * z)
+    r[:, 0, 1] = 2 * (x * y - w * z)
+    r[:, 0, 2] = 2 * (x * z + w * y)
+    r[:, 1, 0] = 2 * (x * y + w * z)
+    r[:, 1, 1] = 1 - 2 * (x * x + z * z)
+    r[:, 1, 2] = 2 * (y * z - w * x)
+    r[:, 2, 0] = 2 * (x * z - w * y)
+    r[:, 2, 1] = 2 * (y * z + w * x)
+    r[:, 2, 2] = 1 - 2 * (x * x + y * y)
+    return r
+
+
 def densify_adc(opt, accum, count, cfg: DensifyConfig, rng: np.random.Generator, alive=None,
                 iteration: int = 0) -> DensifyResult:
     """Clone, split, then prune (pipeline.py:116-185) for the reference's 2-D
-    layout: position (2), scale (2, log), rotation angle (1), opacity (1) and
-    any plain groups.
+    layout (position 2, log scale 2, rotation angle 1, opacity 1, plain
+    groups) and for the 3DGS SH-3 layout (xyz 3, log scaling 3, rotation
+    quaternion 4, opacity 1, f_dc / f_rest carried along): a split child is
+    sampled in the parent's 3-D footprint, R(q) (exp(scaling) * gamma) with
+    gamma ~ N(0, I_3) clipped at norm 2.5 (oracle densify_adc_sh3_f64).
 
     The decisions and the few new attribute values are computed on the host in
     float64 with the reference's formulas and ``rng`` draws:
@@ -154,10 +176,11 @@ def densify_adc(opt, accum, count, cfg: DensifyConfig, rng: np.random.Generator,
     rot_g = next((g for g in opt.param_groups if g["name"] in ("rot", "rotation")), None)
     pos_t, sc_t, op_t = (g["params"][0] for g in (pos_g, sc_g, op_g))
     n = opt.n_rows
-    if pos_t.reshape(n, -1).shape[1] != 2 or sc_t.reshape(n, -1).shape[1] != 2 or \
-            rot_g is None or rot_g["params"][0].reshape(n, -1).shape[1] != 1:
-        raise ConfigError("densify_adc implements the reference's 2-D split (mu 2, kappa 2, "
-                          "rot 1)")
+    dims = pos_t.reshape(n, -1).shape[1]
+    rot_w = None if rot_g is None else rot_g["params"][0].reshape(n, -1).shape[1]
+    if (dims, sc_t.reshape(n, -1).shape[1], rot_w) not in ((2, 2, 1), (3, 3, 4)):
+        raise ConfigError("densify_adc splits the reference's 2-D layout (mu 2, kappa 2, rot "
+                          "angle 1) or the 3DGS layout (xyz 3, scaling 3, rotation quaternion 4)")
     host = lambda t: t.detach().reshape(n, -1).cpu().numpy().astype(np.float64)  # noqa: E731
     tau = host(op_t)[:, 0]
     kappa = host(sc_t)
@@ -191,19 +214,25 @@ def densify_adc(opt, accum, count, cfg: DensifyConfig, rng: np.random.Generator,
         events.append(_event(iteration, "clone", clone_rows))
     if split_rows.size:
         mu = host(pos_t)[split_rows]
-        rot = host(rot_g["params"][0])[split_rows, 0]
+        rot = host(rot_g["params"][0])[split_rows]
+        rot = rot[:, 0] if dims == 2 else rot
         ks = kappa[split_rows]
         base = n + clone_rows.size
         for c in range(2):
-            gamma = rng.standard_normal((split_rows.size, 2))
+            # pipeline.py:153-162; in 3-D gamma ~ N(0, I_3) and the offset is
+            # rotated by the quaternion (the 2-D rule, one dimension up)
+            gamma = rng.standard_normal((split_rows.size, dims))
             norms = np.linalg.norm(gamma, axis=1)
             gamma *= (np.minimum(norms, 2.5) / np.maximum(norms, 1e-12))[:, None]
             s = np.exp(ks)
-            cs, sn = np.cos(rot), np.sin(rot)
             local = s * gamma
             cmu = mu.copy()
-            cmu[:, 0] += cs * local[:, 0] - sn * local[:, 1]
-            cmu[:, 1] += sn * local[:, 0] + cs * local[:, 1]
+            if dims == 2:
+                cs, sn = np.cos(rot), np.sin(rot)
+                cmu[:, 0] += cs * local[:, 0] - sn * local[:, 1]
+                cmu[:, 1] += sn * local[:, 0] + cs * local[:, 1]
+            else:
+                cmu += np.einsum("kij,kj->ki", quat_rotation(rot), local)
             rows = base + c * split_rows.size + np.arange(split_rows.size)
             patches.setdefault(pos_g["name"], []).append((rows, cmu))
             patches.setdefault(sc_g["name"], []).append((rows, ks - np.log(cfg.split_shrink)))

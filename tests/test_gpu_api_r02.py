@@ -286,3 +286,120 @@ def test_tma_record_kernel_ragged_and_bad_rows(n, mode):
         for k in pa:
             assert np.array_equal(pa[k][rows[1]], host[k][rows[1]])
         assert sa["n_bad_grad"] == 1 and sa["n_bad_domain"] == 1
+
+
+# --------------------------------------------------------------------------
+# densify_adc on the 3DGS SH-3 record layout
+# --------------------------------------------------------------------------
+
+@pytest.mark.parametrize("params_layout", ["record", "attr"])
+def test_densify_adc_sh3_vs_oracle(params_layout):
+    """Clone / split / prune (pipeline.py:116-185) on SH-3 rows after real
+    steps: the split child is sampled in the parent's 3-D footprint
+    (quaternion rotation, oracle.densify_adc_sh3_f64, same rng draws);
+    every output row equals fp32 of the oracle's float64 value, children
+    start with fresh state, parents keep theirs, and the rebound optimizer
+    steps the new rows."""
+    from paper_2601_16736_b200 import records as R
+    from paper_2601_16736_b200 import synthetic as S
+    from paper_2601_16736_b200.optimizer import AdamWGS
+    from paper_2601_16736_b200.structural import DensifyConfig
+    cfg, host = _cloud(3_001, p=0.5, seed=21)
+    n = cfg.n
+    params = {k: torch.from_numpy(v).to(DEV) for k, v in host.items()}
+    if params_layout == "record":
+        _, params = R.pack(params)
+    opt = AdamWGS(S.param_groups(params), mode="adamw-gs", lambda_o=1e-3, lambda_s=1e-5)
+    opt.enable_densify_stats()
+    for s in range(3):
+        vis = S.visibility(cfg, s)
+        g = {k: torch.from_numpy(x * 1e3).to(DEV) for k, x in S.step_grads(cfg, s, vis).items()}
+        opt.step(torch.from_numpy(vis).to(DEV), cfg.n_pixels, grads=g, densify_scale=1.0)
+    opt.check_errors()
+    torch.cuda.synchronize()
+    acc, cnt = opt.densify_stats()
+    acc_h, cnt_h = acc.cpu().numpy().astype(np.float64), cnt.cpu().numpy().astype(np.int64)
+    alive = np.random.default_rng(4).random(n) < 0.97
+    dcfg = dict(grad_threshold=float(np.quantile(acc_h / np.maximum(cnt_h, 1), 0.8)),
+                prune_opacity=0.01, split_scale_px=0.1, split_shrink=1.6, max_primitives=10_000)
+    p0 = {k: t.cpu().numpy().reshape(n, -1) for k, t in params.items()}
+    m0 = {k: t.contiguous().cpu().numpy().reshape(n, -1) for k, t in opt.state.m.items()}
+    v0 = {k: t.contiguous().cpu().numpy().reshape(n, -1) for k, t in opt.state.v.items()}
+    t0 = opt.state.clock.cpu().numpy()
+    want = O.densify_adc_sh3_f64(p0, m0, v0, t0, alive, acc_h, cnt_h, dcfg,
+                                 np.random.default_rng(77))
+    res = opt.densify_adc(DensifyConfig(**dcfg), np.random.default_rng(77), alive=alive,
+                          iteration=9)
+    wp, wm, wv, wt, walive, wsrc, counts = want
+    assert counts[0] > 0 and counts[1] > 0 and counts[2] > 0, counts
+    kinds = {e["kind"]: e["count"] for e in res.events}
+    assert (kinds.get("clone", 0), kinds.get("split", 0), kinds.get("prune", 0)) == counts
+    n_out = wsrc.size
+    assert opt.n_rows == n_out and np.array_equal(res.src, wsrc) and np.array_equal(res.alive,
+                                                                                    walive)
+    for k in host:
+        got = res.params[k].cpu().numpy().reshape(n_out, -1)
+        assert np.array_equal(got, wp[k].astype(np.float32)), k
+        assert np.array_equal(opt.state.m[k].contiguous().cpu().numpy().reshape(n_out, -1),
+                              wm[k].astype(np.float32)), k
+        assert np.array_equal(opt.state.v[k].contiguous().cpu().numpy().reshape(n_out, -1),
+                              wv[k].astype(np.float32)), k
+    assert np.array_equal(opt.state.clock.cpu().numpy(), wt.astype(np.int32))
+    vis = torch.rand(n_out, device=DEV) < 0.5
+    grads = {k: torch.randn_like(t) * 1e-3 for k, t in res.params.items()}
+    opt.step(vis, 4096, grads=grads)
+    opt.check_errors()
+    assert opt.last_stats()["n_stepped"] == int(vis.sum())
+
+
+# --------------------------------------------------------------------------
+# K1 fused into K2 (gs_step_rows_masked)
+# --------------------------------------------------------------------------
+
+@pytest.mark.parametrize("n", [1, 2047, 2048, 2049, 100_003])
+@pytest.mark.parametrize("kind", ["bool", "radii", "offset-bool", "offset-radii"])
+@pytest.mark.parametrize("mode", ["adamw-gs", "sparse-adam", "adamw-const"])
+def test_fused_compaction_equals_index_path(n, kind, mode):
+    """The one-launch step (the loader compacts the mask: uint8 or int32
+    radii, aligned or not, ragged tails) equals K1 + K2 bit for bit:
+    parameters, moment records, clocks, statistics (n_visible included)."""
+    from paper_2601_16736_b200 import records as R
+    from paper_2601_16736_b200 import synthetic as S
+    from paper_2601_16736_b200.optimizer import AdamWGS
+    cfg, host = _cloud(n, p=0.3, seed=n + 5)
+    outs = []
+    for fused in (True, False):
+        _, params = R.pack({k: torch.from_numpy(v).to(DEV) for k, v in host.items()})
+        lo, ls = (0.0, 0.0) if mode == "sparse-adam" else (1e-3, 1e-5)
+        opt = AdamWGS(S.param_groups(params), mode=mode, lambda_o=lo, lambda_s=ls,
+                      fused_compaction=fused)
+        stats = []
+        for s in range(3):
+            vis = S.visibility(cfg, s)
+            if "radii" in kind:
+                m = torch.from_numpy(np.where(vis, np.arange(n) % 7 + 1, 0).astype(np.int32))
+            else:
+                m = torch.from_numpy(vis)
+            if kind.startswith("offset"):
+                big = torch.zeros(n + 3, dtype=m.dtype)
+                big[3:] = m
+                m = big.to(DEV)[3:]
+            else:
+                m = m.to(DEV)
+            _, g = R.pack({k: torch.from_numpy(x).to(DEV) for k, x in S.step_grads(cfg, s, vis).items()})
+            opt.step(m, cfg.n_pixels, grads=g)
+            assert (opt._last_ctx[1] is None) == fused
+            stats.append(opt.last_stats())
+        opt.check_errors()
+        outs.append(({k: p.cpu().numpy() for k, p in params.items()},
+                     opt.state.record.cpu().numpy(), stats))
+    (pa, ra, sa), (pb, rb, sb) = outs
+    for k in pa:
+        assert np.array_equal(pa[k], pb[k]), k
+    assert np.array_equal(ra.view(np.int32), rb.view(np.int32))
+    for x, y in zip(sa, sb):
+        for f in x:
+            if f.startswith("sum_"):
+                assert x[f] == pytest.approx(y[f], rel=1e-12, abs=0), f
+            else:
+                assert x[f] == y[f], f

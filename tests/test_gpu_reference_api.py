@@ -685,7 +685,7 @@ def test_captured_step_graph_matches_eager(mode, check):
         outs.append(({k: p.cpu().numpy() for k, p in params.items()},
                      opt.state.record.cpu().numpy(), opt.last_stats()))
         if graph is not None:
-            assert graph.launches_per_replay >= 3
+            assert graph.launches_per_replay >= 1
             bad = int(np.flatnonzero(vis)[5])
             grads["f_rest"][bad, 2] = float("nan")
             with pytest.raises(GradientError) as ei:
