@@ -304,9 +304,11 @@ __global__ void __launch_bounds__(kThreads)
     scatter_rows_kernel(float* __restrict__ record, int64_t stride, int P,
                         const int32_t* __restrict__ rows, int64_t k, int64_t n_rows, double a1,
                         double a2) {
-  // VEC4: a lane moves one 16-byte piece (two slots) of the row, so a row
-  // is one warp-wide access of 8(P+1) bytes; two rows per warp iteration
-  // keep two rows' loads in flight.  Ids outside [0, n_rows) are skipped.
+  // VEC4: a lane moves one 16-byte piece (two slots) of a row, so a row is
+  // one warp-wide access of 8(P+1) bytes; RPI rows per warp iteration keep
+  // RPI rows' loads in flight before any store.  Ids outside [0, n_rows)
+  // are skipped.
+  constexpr int RPI = VEC4 ? 4 : 2;
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (kThreads / 32);
   auto one = [&](float* rec, int s) {  // float2 slot s
@@ -320,50 +322,55 @@ __global__ void __launch_bounds__(kThreads)
                        __double2float_rn(__dmul_rn((double)x.y, a2)));
     }
   };
-  for (int64_t i = ((int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5)) * 2; i < k;
-       i += 2 * warps) {
-    const int64_t r0 = __ldg(rows + i);
-    const int64_t r1 = i + 1 < k ? (int64_t)__ldg(rows + i + 1) : -1;
-    const bool ok0 = r0 >= 0 && r0 < n_rows, ok1 = r1 >= 0 && r1 < n_rows;
-    float* rec0 = record + (ok0 ? r0 : 0) * stride;
-    float* rec1 = record + (ok1 ? r1 : 0) * stride;
+  const int nq = (P + 1) / 2;  // 16-byte pieces of a row (VEC4: P + 1 even)
+  const int s = 2 * lane;      // VEC4: first slot of the lane's piece
+  for (int64_t i0 = ((int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5)) * RPI; i0 < k;
+       i0 += RPI * warps) {
+    float* rec[RPI];
+    bool ok[RPI];
+#pragma unroll
+    for (int u = 0; u < RPI; ++u) {
+      const int64_t r = i0 + u < k ? (int64_t)__ldg(rows + i0 + u) : -1;
+      ok[u] = r >= 0 && r < n_rows;
+      rec[u] = record + (ok[u] ? r : 0) * stride;
+    }
     if (VEC4) {
-      const int nq = (P + 1) / 2;  // 16-byte pieces of a row (P + 1 even)
-      if (lane < nq) {
-        float4* q0 = reinterpret_cast<float4*>(rec0) + lane;
-        float4* q1 = reinterpret_cast<float4*>(rec1) + lane;
-        const int s = 2 * lane;  // first slot of the piece
-        if (RESET) {
-          const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (lane >= nq) continue;
+      if (RESET) {
+        const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int u = 0; u < RPI; ++u) {
+          if (!ok[u]) continue;
           if (s + 1 < P) {
-            if (ok0) *q0 = z;
-            if (ok1) *q1 = z;
+            reinterpret_cast<float4*>(rec[u])[lane] = z;
           } else {
-            if (ok0) { one(rec0, s); one(rec0, s + 1); }
-            if (ok1) { one(rec1, s); one(rec1, s + 1); }
+            one(rec[u], s);
+            one(rec[u], s + 1);
           }
-        } else {
-          float4 x0 = make_float4(0.f, 0.f, 0.f, 0.f), x1 = x0;
-          if (ok0) x0 = *q0;
-          if (ok1) x1 = *q1;
-          auto sc = [&](float4 x) {
-            float4 y = x;
-            y.x = __double2float_rn(__dmul_rn((double)x.x, a1));
-            y.y = __double2float_rn(__dmul_rn((double)x.y, a2));
-            if (s + 1 < P) {
-              y.z = __double2float_rn(__dmul_rn((double)x.z, a1));
-              y.w = __double2float_rn(__dmul_rn((double)x.w, a2));
-            }
-            return y;  // slot P (clock, pad) is written back unchanged
-          };
-          if (ok0) *q0 = sc(x0);
-          if (ok1) *q1 = sc(x1);
+        }
+      } else {
+        float4 x[RPI];
+#pragma unroll
+        for (int u = 0; u < RPI; ++u)
+          x[u] = ok[u] ? reinterpret_cast<const float4*>(rec[u])[lane] : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int u = 0; u < RPI; ++u) {
+          if (!ok[u]) continue;
+          float4 y = x[u];
+          y.x = __double2float_rn(__dmul_rn((double)x[u].x, a1));
+          y.y = __double2float_rn(__dmul_rn((double)x[u].y, a2));
+          if (s + 1 < P) {
+            y.z = __double2float_rn(__dmul_rn((double)x[u].z, a1));
+            y.w = __double2float_rn(__dmul_rn((double)x[u].w, a2));
+          }  // else slot P (clock, pad) is written back unchanged
+          reinterpret_cast<float4*>(rec[u])[lane] = y;
         }
       }
     } else {
-      for (int s = lane; s <= P; s += 32) {
-        if (ok0) one(rec0, s);
-        if (ok1) one(rec1, s);
+      for (int sl = lane; sl <= P; sl += 32) {
+#pragma unroll
+        for (int u = 0; u < RPI; ++u)
+          if (ok[u]) one(rec[u], sl);
       }
     }
   }
@@ -428,13 +435,24 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
-// One-pass K4 on the row record: a warp reads one 8(P+1)-byte record row per
-// iteration (lane q takes the 16-byte piece of slots 2q, 2q+1), so every
-// row is one coalesced warp access and nothing is divided by the width.  A
-// lane's slots belong to fixed groups across rows, so it keeps J x 2
-// accumulator sets (group id fixed per lane); the block then folds them in a
-// fixed (warp, lane) order and the last CTA folds the blocks: deterministic
-// for a given grid.
+// One-pass K4 on the row record: a warp reads 4 consecutive record rows per
+// iteration (4 x 8(P+1) contiguous bytes in flight per warp; lane q takes
+// the 16-byte piece of slots 2q, 2q+1 of each), so nothing is divided by a
+// width.  A lane's slots belong to fixed groups across rows, so it keeps
+// J x 2 accumulator sets; the block folds them in a fixed (warp, lane)
+// order and the last CTA folds the blocks: deterministic for a given grid.
+// sqrt(v) and |m| / sqrt(v) come from a float64 reciprocal square root
+// (fp32 seed + two Newton steps, ~1 ulp of float64) instead of float64
+// sqrt and division: the statistics agree with the reference's float64
+// values to ~1e-16 relative at a fraction of the float64 instruction cost.
+__device__ __forceinline__ double rsqrt_f64(float vf) {
+  const double v = (double)vf;
+  double r = (double)rsqrtf(vf);
+  r = r * fma(-0.5 * v * r, r, 1.5);
+  r = r * fma(-0.5 * v * r, r, 1.5);
+  return r;
+}
+
 template <int J>
 __global__ void __launch_bounds__(kThreads)
     stats_rows_vec_kernel(const GroupSet S, int P, const float* __restrict__ record,
@@ -443,6 +461,7 @@ __global__ void __launch_bounds__(kThreads)
                           unsigned int* counter) {
   constexpr int NW = kThreads / 32;
   constexpr int NF = 5;  // sum sqrt v, max sqrt v, n(v > 0), sum |m|/sqrt v, max |m|/sqrt v
+  constexpr int RPI = 4;  // record rows per warp iteration
   __shared__ signed char s_grp[128];
   __shared__ double s_acc[NW][32][2 * J][NF];
   __shared__ double s_red[kStatsFields * NW];
@@ -467,31 +486,51 @@ __global__ void __launch_bounds__(kThreads)
   double n_alive = 0.0, n_active = 0.0;
   const int nq = (P + 1) / 2;  // 16-byte pieces holding slots < P
   const int64_t warps = (int64_t)gridDim.x * NW;
-  for (int64_t r = (int64_t)blockIdx.x * NW + warp; r < n_rows; r += warps) {
-    if (alive != nullptr && alive[r] == 0) continue;  // warp-uniform
-    if (lane == 0) {
-      n_alive += 1.0;
-      if (opac >= 0) n_active += __ldg(S.g[opac].param + r * S.g[opac].ps) > active_logit;
-    }
-    const float4* row = reinterpret_cast<const float4*>(record + r * stride);
+  for (int64_t r0 = ((int64_t)blockIdx.x * NW + warp) * RPI; r0 < n_rows; r0 += warps * RPI) {
+    float4 x[RPI][J];
+    bool live[RPI];
 #pragma unroll
-    for (int j = 0; j < J; ++j) {
-      const int q = lane + 32 * j;
-      if (q < nq) {
-        const float4 x = __ldg(row + q);
-        const float mm[2] = {x.x, x.z}, vv[2] = {x.y, x.w};
+    for (int i = 0; i < RPI; ++i) {
+      const int64_t r = r0 + i;
+      live[i] = r < n_rows && (alive == nullptr || alive[r] != 0);
+      const float4* row = reinterpret_cast<const float4*>(record + (r < n_rows ? r : 0) * stride);
+#pragma unroll
+      for (int j = 0; j < J; ++j) {
+        const int q = lane + 32 * j;
+        x[i][j] = (live[i] && q < nq) ? __ldg(row + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int i = 0; i < RPI; ++i) {
+        if (!live[i]) continue;
+        n_alive += 1.0;
+        if (opac >= 0) n_active += __ldg(S.g[opac].param + (r0 + i) * S.g[opac].ps) > active_logit;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < RPI; ++i) {
+#pragma unroll
+      for (int j = 0; j < J; ++j) {
+        const int q = lane + 32 * j;
+        const float mm[2] = {x[i][j].x, x[i][j].z}, vv[2] = {x[i][j].y, x[i][j].w};
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          if (2 * q + h >= P) continue;
-          const double sq = sqrt((double)vv[h]);
+          if (!live[i] || q >= nq || 2 * q + h >= P) continue;
           double* A = a[2 * j + h];
-          A[0] += sq;
-          A[1] = fmax(A[1], sq);
-          if (sq > 0.0) {
-            const double rt = __ddiv_rn(fabs((double)mm[h]), sq);
+          if (vv[h] > 0.0f) {
+            const double rs = rsqrt_f64(vv[h]);
+            const double sq = (double)vv[h] * rs;
+            const double rt = fabs((double)mm[h]) * rs;
+            A[0] += sq;
+            A[1] = fmax(A[1], sq);
             A[2] += 1.0;
             A[3] += rt;
             A[4] = fmax(A[4], rt);
+          } else if (vv[h] != 0.0f) {  // negative / NaN v: the reference's sqrt gives NaN
+            const double sq = sqrt((double)vv[h]);
+            A[0] += sq;
+            A[1] = fmax(A[1], sq);
           }
         }
       }
@@ -508,7 +547,6 @@ __global__ void __launch_bounds__(kThreads)
     s_red[NW + warp] = n_active;
   }
   __syncthreads();
-  // block fold in a fixed order: thread t < kStatsFields owns one output field
   double acc[kStatsFields];
   bool is_max[kStatsFields];
 #pragma unroll
@@ -629,7 +667,7 @@ extern "C" int gs_rsr_apply_rows(float* record, int64_t record_stride, int32_t n
     return GS_ERR_ARG;
   }
   if (k == 0) return GS_OK;
-  const int64_t need = (k + 15) / 16;
+  const int64_t need = (k + 31) / 32;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)gs_sm_count() * 8));
   if (rows_vec4(record, record_stride, n_elems))
     scatter_rows_kernel<false, true><<<grid, kThreads, 0, (cudaStream_t)stream>>>(
@@ -650,7 +688,7 @@ extern "C" int gs_reset_rows_rows(float* record, int64_t record_stride, int32_t 
     return GS_ERR_ARG;
   }
   if (k == 0) return GS_OK;
-  const int64_t need = (k + 15) / 16;
+  const int64_t need = (k + 31) / 32;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)gs_sm_count() * 8));
   if (rows_vec4(record, record_stride, n_elems))
     scatter_rows_kernel<true, true><<<grid, kThreads, 0, (cudaStream_t)stream>>>(
@@ -691,8 +729,8 @@ extern "C" int gs_stats_all_rows(const gs_group* groups, int32_t n_groups, int64
   auto* partials = reinterpret_cast<double*>(reinterpret_cast<char*>(ws) + sizeof(StatsWorkspace));
   cudaStream_t s = (cudaStream_t)stream;
   if (record_stride % 4 == 0 && (reinterpret_cast<uintptr_t>(record) & 15u) == 0 && P <= 127) {
-    // one pass, a warp per record row
-    const int64_t need = (n_rows + kThreads / 32 - 1) / (kThreads / 32);
+    // one pass, a warp per 4 record rows per iteration
+    const int64_t need = (n_rows + 4 * (kThreads / 32) - 1) / (4 * (kThreads / 32));
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, stats_blocks()));
     if ((P + 1) / 2 <= 32)
       stats_rows_vec_kernel<1><<<grid, kThreads, 0, s>>>(S, P, record, record_stride, n_rows, alive,

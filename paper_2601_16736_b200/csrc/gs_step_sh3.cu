@@ -255,6 +255,10 @@ int gs_step_fixed_masked_try(const gs_group* groups, int32_t n_groups, const gs_
   if (cfg->mode == GS_MODE_SPARSE_ADAM && (cfg->lambda_opacity != 0.0 || cfg->lambda_scale != 0.0))
     return 0;
   if (fixed_variant() == 21 || n_rows < 1) return 0;
+  // the loader streams 2-KB mask tiles with 16-byte bulk copies
+  if ((reinterpret_cast<uintptr_t>(radii ? static_cast<const void*>(radii)
+                                         : static_cast<const void*>(mask)) & 15u) != 0)
+    return 0;
   FixedParams P;
   int kind = 0;
   bool tma4 = false;

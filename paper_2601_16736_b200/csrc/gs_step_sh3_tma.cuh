@@ -107,6 +107,9 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB)
   __shared__ int s_nv[S];  // rows of the chunk in the stage; -1 ends the CTA's chunk stream
   constexpr int kPend = MASK != 0 ? 1024 : 1;  // pending visible ids (fused compaction)
   __shared__ uint32_t s_pend[kPend];
+  constexpr int kMaskRing = MASK != 0 ? 4 : 1;  // mask tiles in flight (fused compaction)
+  __shared__ __align__(128) unsigned char s_mask[kMaskRing][MASK != 0 ? 2048 : 16];
+  __shared__ __align__(8) uint64_t mask_bar[kMaskRing];
   __shared__ double s_red[GS_STEP_STATS * (NCW + 2)];
   // TMA boxes land 128-byte aligned (the host adds 128 bytes of slack)
   unsigned char* const smem = reinterpret_cast<unsigned char*>(
@@ -131,6 +134,7 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB)
       mbar_init(&done_bar[s], NC);
       mbar_init(&empty_bar[s], 1);
     }
+    for (int s = 0; s < kMaskRing; ++s) mbar_init(&mask_bar[s], 1);
   }
   if (tid < R * S) {
     s_badg[tid / R][tid % R] = 0;
@@ -167,9 +171,13 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB)
           tma_gather4(sb + ST::kRec + ST::kTh + lane * 4 * PT * 4, &M.grd, r0, r1, r2, r3,
                       &full_bar[st]);
         }
-        // row ids and bias factors of the row's next clock ride the stage, so
-        // the consumers touch no global memory before their barrier
-        if (my_id != oob) {
+        // row ids (and, on index lists, the bias factors of the row's next
+        // clock) ride the stage, so the consumers touch no global memory
+        // before their barrier; the mask-scanning loader leaves the bias
+        // factors to the consumers (its own time is the scan)
+        if (my_id != oob && MASK != 0) {
+          s_crow[st][lane] = (uint32_t)my_id;
+        } else if (my_id != oob) {
           s_crow[st][lane] = (uint32_t)my_id;
           const int tb = kDense ? P.global_t
                                 : __ldg(reinterpret_cast<const int*>(P.record + (size_t)my_id * P.stride +
@@ -198,55 +206,43 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB)
         emit(my_id, chunk_rows(c));
       }
     } else {
-      // fused compaction: the CTA takes tiles of kMaskTile rows grid-stride;
-      // each lane loads 16 mask entries per block of 512 rows (the next
-      // tile's loads in flight while this one is scanned), a warp scan packs
-      // the visible ids into a ring of pending ids in shared memory, and
-      // every 32 of them leave as one chunk
-      constexpr int kMaskTile = MASK == 1 ? 2048 : 512;  // 16 mask bytes or 64 radii bytes / lane
-      constexpr int kBlocks = kMaskTile / 512;
-      constexpr int kQ = MASK == 1 ? 1 : 4;  // 16-byte loads per lane per block
-      using Vec = uint4;
+      // fused compaction: the CTA takes 2-KB mask tiles grid-stride (2048
+      // uint8 rows or 512 int32 radii); lane 0 streams them into a 4-deep
+      // shared-memory ring with 1-D bulk copies (mbarrier tx counts), the
+      // warp scans each 512-row block from shared memory (16 rows per lane),
+      // a warp scan packs the visible ids into a ring of pending ids, and
+      // every 32 of them leave as one chunk.  The host runs this path for
+      // 16-byte-aligned masks only.
+      constexpr int kRowsPerTile = MASK == 1 ? 2048 : 512;
+      constexpr int kBlocks = kRowsPerTile / 512;
+      constexpr int kQ = MASK == 1 ? 1 : 4;  // 16-byte smem reads per lane per block
+      constexpr int kEsz = MASK == 1 ? 1 : 4;
       const int64_t nr = n_rows;
-      const int n_tiles = (int)((nr + kMaskTile - 1) / kMaskTile);
-      const bool vec_ok = (reinterpret_cast<uintptr_t>(vis_mask) & 15u) == 0;
-      Vec cur[kBlocks][kQ], nxt[kBlocks][kQ];
-      auto load_tile = [&](int tile, Vec (&buf)[kBlocks][kQ]) {
-#pragma unroll
-        for (int b = 0; b < kBlocks; ++b) {
-          const int64_t row0 = (int64_t)tile * kMaskTile + b * 512 + lane * 16;
-#pragma unroll
-          for (int q = 0; q < kQ; ++q) {
-            buf[b][q] = make_uint4(0u, 0u, 0u, 0u);
-            if (tile < n_tiles && row0 + 16 <= nr && vec_ok) {
-              if constexpr (MASK == 1)
-                buf[b][q] = __ldg(reinterpret_cast<const uint4*>(
-                    reinterpret_cast<const uint8_t*>(vis_mask) + row0));
-              else
-                buf[b][q] = __ldg(reinterpret_cast<const uint4*>(
-                    reinterpret_cast<const int32_t*>(vis_mask) + row0) + q);
-            } else if (tile < n_tiles) {  // ragged end or unaligned mask: element loads
-              uint32_t w[4] = {0u, 0u, 0u, 0u};
-#pragma unroll
-              for (int j = 0; j < 4; ++j) {
-                const int64_t r = row0 + 4 * q + j;
-                if constexpr (MASK == 1) {
-#pragma unroll
-                  for (int e = 0; e < 4; ++e) {
-                    const int64_t rr = row0 + 4 * j + e;
-                    if (q == 0 && rr < nr)
-                      w[j] |= (uint32_t)reinterpret_cast<const uint8_t*>(vis_mask)[rr] << (8 * e);
-                  }
-                } else {
-                  if (r < nr) w[j] = (uint32_t)reinterpret_cast<const int32_t*>(vis_mask)[r];
-                }
-              }
-              buf[b][q] = make_uint4(w[0], w[1], w[2], w[3]);
-            }
+      const int n_tiles = (int)((nr + kRowsPerTile - 1) / kRowsPerTile);
+      const unsigned char* gmask = reinterpret_cast<const unsigned char*>(vis_mask);
+      // bytes of tile t that arrive by bulk copy (16-byte multiple); rows past
+      // them (the ragged end of the last tile) are read from global memory
+      auto bulk_bytes = [&](int t) -> int {
+        const int64_t rows = nr - (int64_t)t * kRowsPerTile;
+        const int64_t b = (rows < kRowsPerTile ? rows : kRowsPerTile) * kEsz;
+        return (int)(b & ~(int64_t)15);
+      };
+      auto issue = [&](int k2) {  // tile number k2 of this CTA into slot k2 % kMaskRing
+        const int t = (int)blockIdx.x + k2 * G;
+        if (t >= n_tiles) return;
+        const int slot = k2 % kMaskRing;
+        const int b = bulk_bytes(t);
+        if (lane == 0) {
+          if (b > 0) {
+            mbar_arrive_expect_tx(&mask_bar[slot], (uint32_t)b);
+            bulk_g2s(s_mask[slot], gmask + (int64_t)t * kRowsPerTile * kEsz, (uint32_t)b,
+                     &mask_bar[slot]);
+          } else {
+            mbar_arrive(&mask_bar[slot]);
           }
         }
       };
-      auto bits_of = [&](const Vec (&v)[kQ]) -> uint32_t {  // bit j: row lane*16 + j visible
+      auto bits_of = [&](const uint4 (&v)[kQ]) -> uint32_t {  // bit j: row lane*16 + j visible
         uint32_t bits = 0;
         if constexpr (MASK == 1) {
           const uint32_t w[4] = {v[0].x, v[0].y, v[0].z, v[0].w};
@@ -263,13 +259,35 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB)
         return bits;
       };
       int head = 0, tail = 0;  // ring of pending ids: s_pend[head .. tail)
-      int tile = (int)blockIdx.x;
-      load_tile(tile, cur);
-      for (; tile < n_tiles; tile += G) {
-        load_tile(tile + G, nxt);
+      const int my_tiles = (int)blockIdx.x < n_tiles ? (n_tiles - 1 - (int)blockIdx.x) / G + 1 : 0;
+#pragma unroll
+      for (int k2 = 0; k2 < kMaskRing; ++k2) issue(k2);
+      for (int k2 = 0; k2 < my_tiles; ++k2) {
+        const int t = (int)blockIdx.x + k2 * G;
+        const int slot = k2 % kMaskRing;
+        mbar_wait(&mask_bar[slot], (unsigned)((k2 / kMaskRing) & 1));
+        const int bb = bulk_bytes(t);
 #pragma unroll
         for (int b = 0; b < kBlocks; ++b) {
-          const uint32_t bits = bits_of(cur[b]);
+          const int lrow = b * 512 + lane * 16;  // row of the tile
+          uint4 v[kQ];
+#pragma unroll
+          for (int q = 0; q < kQ; ++q) {
+            const int off = lrow * kEsz + 16 * q;  // byte offset in the tile
+            if (off + 16 <= bb) {
+              v[q] = *reinterpret_cast<const uint4*>(s_mask[slot] + off);
+            } else {  // ragged end: global element reads (zero past the rows)
+              uint32_t w[4] = {0u, 0u, 0u, 0u};
+              const int64_t g0 = (int64_t)t * kRowsPerTile * kEsz + off;
+#pragma unroll
+              for (int by = 0; by < 16; ++by) {
+                const int64_t gb = g0 + by;
+                if (gb < nr * kEsz) w[by >> 2] |= (uint32_t)gmask[gb] << (8 * (by & 3));
+              }
+              v[q] = make_uint4(w[0], w[1], w[2], w[3]);
+            }
+          }
+          const uint32_t bits = bits_of(v);
           const int cnt = __popc(bits);
           int incl = cnt;
 #pragma unroll
@@ -279,7 +297,7 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB)
           }
           const int total = __shfl_sync(0xffffffffu, incl, 31);
           int pos = tail + incl - cnt;
-          const int row0 = tile * kMaskTile + b * 512 + lane * 16;
+          const int row0 = t * kRowsPerTile + lrow;
           for (uint32_t x = bits; x; x &= x - 1) s_pend[(pos++) & (kPend - 1)] = row0 + __ffs(x) - 1;
           tail += total;
           __syncwarp();
@@ -288,10 +306,8 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB)
             head += R;
           }
         }
-#pragma unroll
-        for (int b = 0; b < kBlocks; ++b)
-#pragma unroll
-          for (int q = 0; q < kQ; ++q) cur[b][q] = nxt[b][q];
+        __syncwarp();  // every lane is done with the slot before it is refilled
+        issue(k2 + kMaskRing);
       }
       if (tail > head) emit(lane < tail - head ? (int)s_pend[(head + lane) & (kPend - 1)] : oob,
                             tail - head);
@@ -351,6 +367,8 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB)
       const float* sg = sth + R * PT;
       const uint32_t* srow = s_crow[st];
       const int tn = t < nvalid ? reinterpret_cast<const int*>(srec + t * SLOTS + L::P)[0] + 1 : 0;
+      if (MASK != 0 && t < nvalid)  // published by the barrier after the check pass
+        s_bc[st][t] = __ldg(reinterpret_cast<const float2*>(P.lut) + (tn < P.lut_len ? tn : P.lut_len - 1));
       if (!STRICT) {
         // gradients in 16-byte pieces (columns >= P are pad and ignored);
         // activation domain on the opacity / scale columns of theta

@@ -281,7 +281,11 @@ def test_tma_record_kernel_ragged_and_bad_rows(n, mode):
     for k in pa:
         assert np.array_equal(pa[k], pb[k]), k
     assert np.array_equal(ra[:, :120].view(np.int32), rb[:, :120].view(np.int32))
-    assert sa == sb
+    for f in sa:  # the fused compaction groups rows into chunks differently: sums reorder
+        if f.startswith("sum_"):
+            assert sa[f] == pytest.approx(sb[f], rel=1e-12, abs=0), f
+        else:
+            assert sa[f] == sb[f], f
     if rows.size > 2 and mode != "coupled-adam":
         for k in pa:
             assert np.array_equal(pa[k][rows[1]], host[k][rows[1]])
