@@ -287,6 +287,15 @@ int gs_step_rows_masked(const gs_group* groups, int32_t n_groups, const gs_step_
                         int64_t record_stride, double* stats_out, void* ws, size_t ws_bytes,
                         int32_t* launched, void* stream);
 
+/* The reference's host Bernoulli draw (aiu_apply, optimizer.py:437-440:
+ * rng.random(n) < prob with rng a numpy Generator over Philox4x64-10,
+ * rng.py:17-30) on the device, bit for bit: out[i] = (u(first + i) < prob)
+ * with u(j) = (philox4x64_10(counter + 1 + j/4, key)[j % 4] >> 11) * 2^-53,
+ * i.e. draw j of a generator with an empty buffer at that counter.
+ * counter: 4 uint64 (host pointer), key: 2 uint64 (host pointer). */
+int gs_philox_bernoulli(const uint64_t* counter, const uint64_t* key, int64_t first, int64_t n,
+                        double prob, uint8_t* out, void* stream);
+
 /* GS_BUILD_FLAG_* bits of this build. */
 int32_t gs_build_flags(void);
 int gs_stats_all_rows(const gs_group* groups, int32_t n_groups, int64_t n_rows,

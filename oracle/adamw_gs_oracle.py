@@ -806,3 +806,51 @@ def densify_adc_sh3_f64(params, m, v, t, alive, accum, count, cfg, rng):
     out_t = np.where(fresh, 0, t[src])[keep]
     return ({k: x[keep] for k, x in merged.items()}, out_m, out_v, out_t, am[keep], src[keep],
             (int(clone.size), int(split.size), n_pruned))
+
+
+# --------------------------------------------------------------------------
+# NumPy's Philox4x64-10 (the reference's rng.stream bit generator,
+# rng.py:17-30) and Generator.random, restated: pins the GPU Bernoulli draw
+# (gs_philox_bernoulli) that replaces the host draw of aiu_apply
+# (optimizer.py:437-440).  Third-party algorithm: numpy.random.Philox
+# (numpy/random/src/philox/philox.h, Random123 philox4x64 with 10 rounds);
+# numpy 2.3 in this image.
+# --------------------------------------------------------------------------
+_M64 = (1 << 64) - 1
+PHILOX_M0, PHILOX_M1 = 0xD2E7470EE14C6C93, 0xCA5A826395121157
+PHILOX_W0, PHILOX_W1 = 0x9E3779B97F4A7C15, 0xBB67AE8584CAA73B
+
+
+def philox4x64_block(ctr, key):
+    """Random123 philox4x64_R(10, ctr, key): four uint64 outputs."""
+    c = [int(x) & _M64 for x in ctr]
+    k0, k1 = int(key[0]) & _M64, int(key[1]) & _M64
+    for r in range(10):
+        if r:
+            k0 = (k0 + PHILOX_W0) & _M64
+            k1 = (k1 + PHILOX_W1) & _M64
+        p0 = PHILOX_M0 * c[0]
+        p1 = PHILOX_M1 * c[2]
+        c = [(p1 >> 64) ^ c[1] ^ k0, p1 & _M64, (p0 >> 64) ^ c[3] ^ k1, p0 & _M64]
+    return c
+
+
+def philox_uniforms(state: dict, n: int) -> np.ndarray:
+    """Generator(Philox).random(n) from a bit_generator.state dict: the
+    buffered outputs first, then one block per counter increment
+    (philox_next), each uint64 -> (x >> 11) * 2^-53 (next_double)."""
+    st = state["state"]
+    ctr = [int(x) for x in st["counter"]]
+    key = [int(x) for x in st["key"]]
+    buf = [int(x) for x in state["buffer"]]
+    pos = int(state["buffer_pos"])
+    out = np.empty(n, F64)
+    for i in range(n):
+        if pos >= 4:
+            v = (ctr[0] + (ctr[1] << 64) + (ctr[2] << 128) + (ctr[3] << 192) + 1) % (1 << 256)
+            ctr = [(v >> (64 * j)) & _M64 for j in range(4)]
+            buf = philox4x64_block(ctr, key)
+            pos = 0
+        out[i] = (buf[pos] >> 11) * (1.0 / 9007199254740992.0)
+        pos += 1
+    return out

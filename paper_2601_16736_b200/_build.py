@@ -20,7 +20,7 @@ LIB = PKG / "libadamw_gs_b200.so"
 SOURCES = ("gs_abi.cu", "gs_compact.cu", "gs_step.cu", "gs_step_rows.cu", "gs_step_sh3.cu",
            "gs_step_sh3_m_coupled.cu", "gs_step_sh3_m_sparse.cu", "gs_step_sh3_m_const.cu",
            "gs_step_sh3_m_const_clip.cu", "gs_step_sh3_m_adamw_gs.cu", "gs_state.cu",
-           "gs_noise.cu")
+           "gs_noise.cu", "gs_rng.cu")
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -24,6 +24,7 @@ import torch
 from . import _lib as L
 from . import records as _records
 from .records import base_grad_view
+from .sampling import device_bernoulli
 from .engine import (ConfigError, DomainError, GradientError, GroupBinding, StepEngine, row_stride,
                      round_pixel_count)
 
@@ -697,8 +698,9 @@ class AdamWGS:
         """Artificial implicit updates (optimizer.py:425-450).
 
         The invisible alive rows are compacted on the GPU; the Bernoulli picks
-        are drawn on the host from ``rng`` exactly as the reference does
-        (``rng.random(invisible.size) < prob``), so the picked set is
+        ``rng.random(invisible.size) < prob`` are drawn on the GPU from the
+        reference's Philox stream, bit for bit, and ``rng`` advances as the
+        host draw would (sampling.device_bernoulli), so the picked set is
         bit-identical; the frozen-moment update runs on the GPU.  Returns the
         picked rows (int64, ascending).  ``draw(n_invisible, prob)`` replaces
         the local draw (the index-sharded wrapper's global-stream slice).
@@ -716,17 +718,22 @@ class AdamWGS:
         if draw is not None:  # collective draw: every shard takes part, even an empty one
             if prob <= 0.0 or eta == 0.0:
                 return empty
-            sel = draw(n_inv, prob)
+            jmask = draw(n_inv, prob)
         else:
             if n_inv == 0 or prob <= 0.0 or eta == 0.0:
                 return empty
-            sel = rng.random(n_inv) < prob
-        k = int(sel.sum())
-        if k == 0:
+            # rng.random(n_inv) < prob, drawn on the device bit for bit
+            # (sampling.device_bernoulli: the reference's Philox stream)
+            jmask = device_bernoulli(rng, n_inv, prob, 0, n_inv, self.device)
+        if not isinstance(jmask, torch.Tensor):
+            jmask = torch.from_numpy(np.asarray(jmask, bool).view(np.uint8)).to(self.device)
+        if n_inv == 0:
             return empty
-        jmask = torch.from_numpy(sel.view(np.uint8)).to(self.device)
         # positions of the picks inside the invisible list (bit-exact order)
         jlist, jcnt = eng.compact_positions(jmask)
+        k = int(jcnt.item())
+        if k == 0:
+            return empty
         picked = eng.aiu(self._state_bindings(), self.state.record, inv_idx, jlist, jcnt, k, eta,
                          self.eps)
         return picked.cpu().numpy().astype(np.int64)

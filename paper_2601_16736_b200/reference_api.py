@@ -267,11 +267,12 @@ def aiu_apply(state, pset, vis, cfg, aiu, rng, iteration: int, alive=None) -> np
     n_inv = int(inv_cnt.item())
     if n_inv == 0 or prob <= 0.0 or eta == 0.0:
         return np.empty(0, dtype=np.int64)
-    sel = rng.random(n_inv) < prob
-    k = int(sel.sum())
+    from .sampling import device_bernoulli
+    sel = device_bernoulli(rng, n_inv, prob, 0, n_inv, inv_idx.device)  # rng.random(n) < prob
+    jlist, jcnt = eng.compact_positions(sel)
+    k = int(jcnt.item())
     if k == 0:
         return np.empty(0, dtype=np.int64)
-    jlist, jcnt = eng.compact_positions(torch.from_numpy(sel.view(np.uint8)).to(inv_idx.device))
     groups = [GroupBinding(k_, role_of(k_), cfg.lr(k_), _get(pset, k_), None, None, None)
               for k_ in state.m]
     picked = eng.aiu(groups, state.record, inv_idx, jlist, jcnt, k, eta, cfg.eps)

@@ -150,3 +150,59 @@ def aiu_shard_select(rng: np.random.Generator, prob: float, counts, rank: int) -
     draw = rng.random(sum(counts)) < prob
     return draw[off:off + counts[rank]]
 
+
+def device_bernoulli(rng: np.random.Generator, n_total: int, prob: float, first: int, n: int,
+                     device):
+    """``(rng.random(n_total) < prob)[first:first + n]`` as a uint8 CUDA
+    tensor, and ``rng`` advanced exactly as that host draw advances it.
+
+    With the reference's Philox streams (rng.py:17-30) the draws are made
+    on the device by gs_philox_bernoulli, bit for bit (the numbers the
+    buffered outputs still hold come from the host); any other bit
+    generator is drawn on the host and uploaded."""
+    import torch
+
+    from . import _lib as L
+    n_total, first, n = int(n_total), int(first), int(n)
+    out = torch.empty(max(n, 0), dtype=torch.uint8, device=device)
+    if n_total <= 0:
+        return out
+    st = rng.bit_generator.state
+    if st.get("bit_generator") != "Philox":
+        sel = rng.random(n_total) < prob
+        out.copy_(torch.from_numpy(sel[first:first + n].view(np.uint8)))
+        return out
+    pos = int(st["buffer_pos"])
+    pre = min(4 - pos, n_total) if pos < 4 else 0
+    head = (rng.random(pre) < prob) if pre else np.empty(0, bool)   # the buffered draws
+    a, b = first, min(first + n, pre)
+    if b > a:
+        out[: b - a].copy_(torch.from_numpy(head[a:b].view(np.uint8)))
+    rest = n_total - pre
+    if rest <= 0:
+        return out
+    st2 = rng.bit_generator.state           # buffer empty now: draw j >= pre is block (j-pre)/4
+    ctr = np.asarray(st2["state"]["counter"], np.uint64)
+    key = np.asarray(st2["state"]["key"], np.uint64)
+    d0 = max(first, pre)
+    dn = first + n - d0
+    if dn > 0:
+        lib = L.load()
+        c = (L.C.c_uint64 * 4)(*[int(x) for x in ctr])
+        k = (L.C.c_uint64 * 2)(*[int(x) for x in key])
+        with torch.cuda.device(out.device):
+            rc = lib.gs_philox_bernoulli(c, k, d0 - pre, dn, float(prob),
+                                         out[d0 - first:].data_ptr(),
+                                         torch.cuda.current_stream(out.device).cuda_stream)
+        L.check(rc, "gs_philox_bernoulli")
+    # advance the host generator past the `rest` device draws: the counter
+    # moves by all but the last block, which a host draw regenerates into
+    # the buffer with the right position
+    blocks = (rest + 3) // 4
+    v = sum(int(x) << (64 * i) for i, x in enumerate(ctr)) + blocks - 1
+    st2["state"]["counter"] = np.array([(v >> (64 * i)) & ((1 << 64) - 1) for i in range(4)],
+                                       dtype=np.uint64)
+    st2["buffer_pos"] = 4
+    rng.bit_generator.state = st2
+    rng.random(rest - 4 * (blocks - 1))
+    return out

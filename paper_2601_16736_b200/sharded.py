@@ -270,14 +270,18 @@ class ShardedAdamWGS:
         global Bernoulli vector from the same stream and keeps its slice
         (sampling.aiu_shard_select). Returns this shard's picks in global
         numbering."""
-        from .sampling import aiu_shard_select
+        from .sampling import device_bernoulli
 
         def draw(n_local, prob):
             dev = self.opt.device if not _host_collective(self.group) else "cpu"
             mine = torch.tensor([n_local], dtype=torch.int64, device=dev)
             allc = [torch.zeros_like(mine) for _ in range(self.world)]
             dist.all_gather(allc, mine, group=self.group)
-            return aiu_shard_select(rng, prob, [int(c.item()) for c in allc], self.rank)
+            counts = [int(c.item()) for c in allc]
+            # this shard's slice of the global draw, on the device
+            # (sampling.aiu_shard_select restated there)
+            return device_bernoulli(rng, sum(counts), prob, sum(counts[:self.rank]), n_local,
+                                    self.opt.device)
 
         picked = self.opt.aiu_apply(visibility_local, aiu, rng, iteration, alive_local, draw=draw)
         return np.asarray(picked, np.int64) + self.lo

@@ -407,3 +407,25 @@ def test_fused_compaction_equals_index_path(n, kind, mode):
                 assert x[f] == pytest.approx(y[f], rel=1e-12, abs=0), f
             else:
                 assert x[f] == y[f], f
+
+
+# --------------------------------------------------------------------------
+# the AIU Bernoulli draw on the device (reference Philox stream, bit for bit)
+# --------------------------------------------------------------------------
+
+@pytest.mark.parametrize("skip", [0, 1, 3, 4, 6])
+@pytest.mark.parametrize("n_total,first,n", [(1, 0, 1), (3, 0, 3), (4_099, 0, 4_099),
+                                             (1_000_003, 0, 1_000_003), (50_001, 17, 30_000),
+                                             (50_001, 2, 1), (10, 10, 0)])
+def test_device_bernoulli_is_host_draw(skip, n_total, first, n):
+    """sampling.device_bernoulli == (rng.random(n_total) < prob)[first:first+n]
+    for every buffer position, and the generator ends in the same state as
+    after the host draw (the next draws agree)."""
+    from paper_2601_16736_b200.sampling import device_bernoulli, stream
+    a, b = stream(5, "aiu", 3), stream(5, "aiu", 3)
+    a.random(skip)
+    b.random(skip)
+    want = (a.random(n_total) < 0.3)[first:first + n]
+    got = device_bernoulli(b, n_total, 0.3, first, n, torch.device(DEV)).cpu().numpy()
+    assert np.array_equal(got.astype(bool), want)
+    assert np.array_equal(a.random(9), b.random(9))

@@ -222,3 +222,16 @@ def test_densify_adc_f64_restatement_is_bitwise_reference():
         assert np.array_equal(om[g.name], z[f"out_m_{g.name}"]), g.name
         assert np.array_equal(ov[g.name], z[f"out_v_{g.name}"]), g.name
     assert np.array_equal(ot, z["out_t"])
+
+
+@pytest.mark.parametrize("skip", [0, 1, 2, 3, 4, 9])
+def test_philox_restatement_is_numpy_generator_random(skip):
+    """oracle.philox_uniforms (NumPy's Philox4x64-10 + next_double, the
+    reference's rng.stream, rng.py:17-30) reproduces Generator.random bit
+    for bit from any buffer position: it pins the GPU AIU draw."""
+    from paper_2601_16736_b200.sampling import stream
+    rng = stream(3, "aiu", 17)
+    rng.random(skip)
+    st = rng.bit_generator.state
+    want = rng.random(41)
+    assert np.array_equal(O.philox_uniforms(st, 41), want)
