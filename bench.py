@@ -610,6 +610,8 @@ def run_workload(args, wl, p_vis, rank, world, dev, *, strong, mask, steps, warm
     for it in range(w.warmup):
         w.one_step(it)
     torch.cuda.synchronize()
+    for o in w.opts:
+        o.last_stats()  # the visible fraction the optimizer picks its kernel shape by
     use_graph = args.graph
     if clocks is not None:
         with clocks:

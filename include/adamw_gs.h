@@ -281,11 +281,14 @@ int gs_densify_rows(const float* grad, int64_t grad_stride, int32_t width, const
  * normaliser, which needs N_v before the step); *launched = 0 (status
  * GS_OK) asks the caller to compact and call gs_step_rows.  The statistics'
  * n_visible is the mask's visible count; results equal gs_compact +
- * gs_step_rows bit for bit (rows are independent). */
+ * gs_step_rows bit for bit (rows are independent).  flags:
+ * GS_MASKED_LOW_VISIBILITY picks the kernel shape for sparse masks (a few %
+ * visible; same results). */
+#define GS_MASKED_LOW_VISIBILITY 1
 int gs_step_rows_masked(const gs_group* groups, int32_t n_groups, const gs_step_cfg* cfg,
                         const uint8_t* mask, const int32_t* radii, int64_t n_rows, float* record,
                         int64_t record_stride, double* stats_out, void* ws, size_t ws_bytes,
-                        int32_t* launched, void* stream);
+                        int32_t flags, int32_t* launched, void* stream);
 
 /* The reference's host Bernoulli draw (aiu_apply, optimizer.py:437-440:
  * rng.random(n) < prob with rng a numpy Generator over Philox4x64-10,

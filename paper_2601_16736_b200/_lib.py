@@ -15,6 +15,7 @@ LIB_PATH = Path(__file__).resolve().parent / "libadamw_gs_b200.so"
 
 GS_ABI_VERSION = 3
 GS_MAX_GROUPS = 8
+GS_MASKED_LOW_VISIBILITY = 1
 
 GS_OK = 0
 
@@ -106,8 +107,8 @@ SIGNATURES = {
                                       C.c_int64, C.c_double, C.c_void_p, C.c_void_p]),
     "gs_step_rows_masked": (C.c_int, [C.POINTER(GsGroup), C.c_int32, C.POINTER(GsStepCfg),
                                       C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,
-                                      C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p,
-                                      C.c_void_p]),
+                                      C.c_void_p, C.c_void_p, C.c_size_t, C.c_int32,
+                                      C.c_void_p, C.c_void_p]),
     "gs_stats_all_rows": (C.c_int, [C.POINTER(GsGroup), C.c_int32, C.c_int64, C.c_void_p,
                                     C.c_int64, C.c_void_p, C.c_float, C.c_void_p, C.c_void_p,
                                     C.c_size_t, C.c_void_p]),

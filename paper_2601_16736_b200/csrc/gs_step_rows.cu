@@ -36,7 +36,8 @@ int gs_step_fixed_try(const gs_group* groups, int32_t n_groups, const gs_step_cf
 int gs_step_fixed_masked_try(const gs_group* groups, int32_t n_groups, const gs_step_cfg* cfg,
                              const uint8_t* mask, const int32_t* radii, int64_t n_rows,
                              float* record, int64_t record_stride, double* stats_out,
-                             double* partials, unsigned int* counter, void* stream);
+                             double* partials, unsigned int* counter, int32_t flags,
+                             void* stream);
 
 namespace gs {
 
@@ -466,7 +467,8 @@ extern "C" int gs_step_rows_masked(const gs_group* groups, int32_t n_groups,
                                    const gs_step_cfg* cfg, const uint8_t* mask,
                                    const int32_t* radii, int64_t n_rows, float* record,
                                    int64_t record_stride, double* stats_out, void* ws,
-                                   size_t ws_bytes, int32_t* launched, void* stream) {
+                                   size_t ws_bytes, int32_t flags, int32_t* launched,
+                                   void* stream) {
   using namespace gs;
   if (!launched) {
     gs_set_error("gs_step_rows_masked: launched must not be null");
@@ -503,7 +505,7 @@ extern "C" int gs_step_rows_masked(const gs_group* groups, int32_t n_groups,
   double* partials =
       reinterpret_cast<double*>(reinterpret_cast<char*>(ws) + sizeof(RowStepWorkspace));
   if (!gs_step_fixed_masked_try(groups, n_groups, cfg, mask, radii, n_rows, record, record_stride,
-                                stats_out, partials, &hdr->counter, stream))
+                                stats_out, partials, &hdr->counter, flags, stream))
     return GS_OK;  // not this layout: the caller compacts and calls gs_step_rows
   *launched = 1;
   return gs_check_launch("gs_step_rows_masked");

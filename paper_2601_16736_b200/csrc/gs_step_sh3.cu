@@ -27,13 +27,13 @@ extern template void launch_fixed<LayoutSH3, GS_MODE_ADAMW_GS, true>(const Fixed
                                                           int64_t, int, cudaStream_t);
 
 extern template void launch_fixed_masked<LayoutSH3, GS_MODE_SPARSE_ADAM>(
-    const FixedParams&, const TmaMaps&, int64_t, int, const void*, cudaStream_t);
+    const FixedParams&, const TmaMaps&, int64_t, int, const void*, bool, cudaStream_t);
 extern template void launch_fixed_masked<LayoutSH3, GS_MODE_ADAMW_CONST>(
-    const FixedParams&, const TmaMaps&, int64_t, int, const void*, cudaStream_t);
+    const FixedParams&, const TmaMaps&, int64_t, int, const void*, bool, cudaStream_t);
 extern template void launch_fixed_masked<LayoutSH3, GS_MODE_ADAMW_CONST_CLIP>(
-    const FixedParams&, const TmaMaps&, int64_t, int, const void*, cudaStream_t);
+    const FixedParams&, const TmaMaps&, int64_t, int, const void*, bool, cudaStream_t);
 extern template void launch_fixed_masked<LayoutSH3, GS_MODE_ADAMW_GS>(
-    const FixedParams&, const TmaMaps&, int64_t, int, const void*, cudaStream_t);
+    const FixedParams&, const TmaMaps&, int64_t, int, const void*, bool, cudaStream_t);
 
 static int g_fixed_variant = -1;
 
@@ -249,7 +249,8 @@ int gs_step_fixed_try(const gs_group* groups, int32_t n_groups, const gs_step_cf
 int gs_step_fixed_masked_try(const gs_group* groups, int32_t n_groups, const gs_step_cfg* cfg,
                              const uint8_t* mask, const int32_t* radii, int64_t n_rows,
                              float* record, int64_t record_stride, double* stats_out,
-                             double* partials, unsigned int* counter, void* stream) {
+                             double* partials, unsigned int* counter, int32_t flags,
+                             void* stream) {
   using namespace gs;
   if (cfg->check != GS_CHECK_FUSED || cfg->mode == GS_MODE_COUPLED_ADAM) return 0;
   if (cfg->mode == GS_MODE_SPARSE_ADAM && (cfg->lambda_opacity != 0.0 || cfg->lambda_scale != 0.0))
@@ -269,19 +270,20 @@ int gs_step_fixed_masked_try(const gs_group* groups, int32_t n_groups, const gs_
   TmaMaps maps;
   if (!encode_tma_maps(P, n_rows, 2 * (LayoutSH3::P + 1), &maps)) return 0;
   const int mk = radii ? 2 : 1;
+  const bool low = (flags & GS_MASKED_LOW_VISIBILITY) != 0;
   const void* m = radii ? static_cast<const void*>(radii) : static_cast<const void*>(mask);
   cudaStream_t s = (cudaStream_t)stream;
   switch (cfg->mode) {
     case GS_MODE_SPARSE_ADAM:
-      launch_fixed_masked<LayoutSH3, GS_MODE_SPARSE_ADAM>(P, maps, n_rows, mk, m, s);
+      launch_fixed_masked<LayoutSH3, GS_MODE_SPARSE_ADAM>(P, maps, n_rows, mk, m, low, s);
       break;
     case GS_MODE_ADAMW_CONST:
-      launch_fixed_masked<LayoutSH3, GS_MODE_ADAMW_CONST>(P, maps, n_rows, mk, m, s);
+      launch_fixed_masked<LayoutSH3, GS_MODE_ADAMW_CONST>(P, maps, n_rows, mk, m, low, s);
       break;
     case GS_MODE_ADAMW_CONST_CLIP:
-      launch_fixed_masked<LayoutSH3, GS_MODE_ADAMW_CONST_CLIP>(P, maps, n_rows, mk, m, s);
+      launch_fixed_masked<LayoutSH3, GS_MODE_ADAMW_CONST_CLIP>(P, maps, n_rows, mk, m, low, s);
       break;
-    default: launch_fixed_masked<LayoutSH3, GS_MODE_ADAMW_GS>(P, maps, n_rows, mk, m, s); break;
+    default: launch_fixed_masked<LayoutSH3, GS_MODE_ADAMW_GS>(P, maps, n_rows, mk, m, low, s); break;
   }
   return 1;
 }

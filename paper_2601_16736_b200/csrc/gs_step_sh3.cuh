@@ -1983,13 +1983,22 @@ void launch_fixed(const FixedParams& P, const TmaMaps* M, int64_t max_rows, int 
 
 // Fused K1 + K2 on records (the fused check): the TMA kernel's loader
 // compacts the visibility mask itself (mask_kind 1: uint8, 2: int32 radii).
+// low_vis: the bias warp variant, for sparse masks where the loader's scan
+// is the bottleneck (c5 at 1%: 0.190 against 0.223 ms); on dense masks the
+// loader-staged bias factors win (c3: 0.534 against 0.580 ms)
+// (profiles/r02/fused_k1_bias_warp.txt).  GS_TMA4_BW=0/1 forces one.
 template <class L, int MODE>
 void launch_fixed_masked(const FixedParams& P, const TmaMaps& M, int64_t n_rows, int mask_kind,
-                         const void* mask, cudaStream_t s) {
-  if (mask_kind == 2)
-    launch_tma4<L, MODE, false, 3, 8, 2, 2>(P, M, n_rows, s, mask);
-  else
-    launch_tma4<L, MODE, false, 3, 8, 2, 1>(P, M, n_rows, s, mask);
+                         const void* mask, bool low_vis, cudaStream_t s) {
+  static const int force = getenv("GS_TMA4_BW") ? atoi(getenv("GS_TMA4_BW")) : -1;
+  const bool bw = force >= 0 ? force != 0 : low_vis;
+  if (mask_kind == 2) {
+    if (bw) launch_tma4<L, MODE, false, 3, 8, 2, 2, true>(P, M, n_rows, s, mask);
+    else launch_tma4<L, MODE, false, 3, 8, 2, 2, false>(P, M, n_rows, s, mask);
+  } else {
+    if (bw) launch_tma4<L, MODE, false, 3, 8, 2, 1, true>(P, M, n_rows, s, mask);
+    else launch_tma4<L, MODE, false, 3, 8, 2, 1, false>(P, M, n_rows, s, mask);
+  }
 }
 
 }  // namespace gs

@@ -7,5 +7,5 @@ template void launch_fixed<LayoutSH3, GS_MODE_ADAMW_CONST, false>(const FixedPar
 template void launch_fixed<LayoutSH3, GS_MODE_ADAMW_CONST, true>(const FixedParams&, const TmaMaps*, int64_t, int,
                                                               cudaStream_t);
 template void launch_fixed_masked<LayoutSH3, GS_MODE_ADAMW_CONST>(const FixedParams&, const TmaMaps&, int64_t, int,
-                                                                const void*, cudaStream_t);
+                                                                const void*, bool, cudaStream_t);
 }  // namespace gs

@@ -7,5 +7,5 @@ template void launch_fixed<LayoutSH3, GS_MODE_SPARSE_ADAM, false>(const FixedPar
 template void launch_fixed<LayoutSH3, GS_MODE_SPARSE_ADAM, true>(const FixedParams&, const TmaMaps*, int64_t, int,
                                                               cudaStream_t);
 template void launch_fixed_masked<LayoutSH3, GS_MODE_SPARSE_ADAM>(const FixedParams&, const TmaMaps&, int64_t, int,
-                                                                const void*, cudaStream_t);
+                                                                const void*, bool, cudaStream_t);
 }  // namespace gs

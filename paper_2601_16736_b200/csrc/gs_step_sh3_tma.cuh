@@ -84,9 +84,14 @@ __device__ __forceinline__ void tma_scatter4(const CUtensorMap* map, const void*
 // MASK: 0 = the compacted index list (P.rows, *P.n_rows_dev rows; dense
 // mode: every row), 1 = a uint8 visibility mask, 2 = int32 radii (> 0 is
 // visible): the loader compacts the mask itself (fused K1, below).
-template <class L, int MODE, bool STRICT, int S, int NCW, int MINB, int MASK>
-__global__ void __launch_bounds__((NCW + 2) * 32, MINB)
+// BW: a fourth role, the bias warp (warp NCW+2), turns the staged clocks
+// into bias factors after the gathers land, so the loader's per-chunk work
+// is only the TMA issue (the mask-scanning loader); without it the loader
+// reads each row's clock and LUT entry itself.
+template <class L, int MODE, bool STRICT, int S, int NCW, int MINB, int MASK, bool BW = false>
+__global__ void __launch_bounds__((NCW + 2 + (BW ? 1 : 0)) * 32, MINB)
     step_tma4_kernel(const FixedParams P, const __grid_constant__ TmaMaps M, const void* vis_mask) {
+  constexpr int NWARPS = NCW + 2 + (BW ? 1 : 0);
   constexpr int R = 32;
   constexpr bool kDense = MODE == GS_MODE_COUPLED_ADAM;
   constexpr bool kCoupled = MODE == GS_MODE_COUPLED_ADAM || MODE == GS_MODE_SPARSE_ADAM;
@@ -97,6 +102,7 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB)
   constexpr int PT = ST::kPT;
   extern __shared__ unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t full_bar[S];
+  __shared__ __align__(8) uint64_t data_bar[BW ? S : 1];  // BW: the gathers of the stage landed
   __shared__ __align__(8) uint64_t done_bar[S];
   __shared__ __align__(8) uint64_t empty_bar[S];
   __shared__ int s_badg[S][R];  // == epoch: non-finite gradient in this use of the stage
@@ -105,12 +111,12 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB)
   __shared__ float2 s_bc[S][R];
   __shared__ uint32_t s_crow[S][R];
   __shared__ int s_nv[S];  // rows of the chunk in the stage; -1 ends the CTA's chunk stream
-  constexpr int kPend = MASK != 0 ? 1024 : 1;  // pending visible ids (fused compaction)
+  constexpr int kPend = MASK != 0 ? 2048 : 1;  // pending visible ids (fused compaction)
   __shared__ uint32_t s_pend[kPend];
-  constexpr int kMaskRing = MASK != 0 ? 4 : 1;  // mask tiles in flight (fused compaction)
-  __shared__ __align__(128) unsigned char s_mask[kMaskRing][MASK != 0 ? 2048 : 16];
+  constexpr int kMaskRing = MASK != 0 ? 6 : 1;  // 1-KB mask tiles in flight (fused compaction)
+  __shared__ __align__(128) unsigned char s_mask[kMaskRing][MASK != 0 ? 1024 : 16];
   __shared__ __align__(8) uint64_t mask_bar[kMaskRing];
-  __shared__ double s_red[GS_STEP_STATS * (NCW + 2)];
+  __shared__ double s_red[GS_STEP_STATS * NWARPS];
   // TMA boxes land 128-byte aligned (the host adds 128 bytes of slack)
   unsigned char* const smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~static_cast<uintptr_t>(127));
@@ -130,7 +136,8 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB)
 
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
-      mbar_init(&full_bar[s], 32);  // the loader warp's lanes (bias factors, row ids) + tx
+      mbar_init(&full_bar[s], 32);  // the loader's (or bias warp's) lanes (+ tx without BW)
+      if (BW) mbar_init(&data_bar[s], 1);  // loader lane 0 + tx
       mbar_init(&done_bar[s], NC);
       mbar_init(&empty_bar[s], 1);
     }
@@ -157,8 +164,9 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB)
     auto emit = [&](int my_id, int nv) {
       if (k >= S) mbar_wait(&empty_bar[st], ph ^ 1u);
       unsigned char* sb = stage(st);
+      uint64_t* tbar = BW ? &data_bar[st] : &full_bar[st];  // the gathers complete here
       if (nv > 0) {
-        if (lane == 0) mbar_expect_tx(&full_bar[st], ST::kBytes);
+        if (lane == 0) mbar_expect_tx(tbar, ST::kBytes);
         __syncwarp();
         const int q = (4 * lane) & 31;
         const int r0 = __shfl_sync(0xffffffffu, my_id, q);
@@ -166,16 +174,15 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB)
         const int r2 = __shfl_sync(0xffffffffu, my_id, q + 2);
         const int r3 = __shfl_sync(0xffffffffu, my_id, q + 3);
         if (lane < R / 4) {
-          tma_gather4(sb + lane * 4 * ST::kRecRow, &M.rec, r0, r1, r2, r3, &full_bar[st]);
-          tma_gather4(sb + ST::kRec + lane * 4 * PT * 4, &M.prm, r0, r1, r2, r3, &full_bar[st]);
-          tma_gather4(sb + ST::kRec + ST::kTh + lane * 4 * PT * 4, &M.grd, r0, r1, r2, r3,
-                      &full_bar[st]);
+          tma_gather4(sb + lane * 4 * ST::kRecRow, &M.rec, r0, r1, r2, r3, tbar);
+          tma_gather4(sb + ST::kRec + lane * 4 * PT * 4, &M.prm, r0, r1, r2, r3, tbar);
+          tma_gather4(sb + ST::kRec + ST::kTh + lane * 4 * PT * 4, &M.grd, r0, r1, r2, r3, tbar);
         }
-        // row ids (and, on index lists, the bias factors of the row's next
-        // clock) ride the stage, so the consumers touch no global memory
-        // before their barrier; the mask-scanning loader leaves the bias
-        // factors to the consumers (its own time is the scan)
-        if (my_id != oob && MASK != 0) {
+        // row ids and the bias factors of the row's next clock ride the
+        // stage, so the consumers touch no global memory before their
+        // barrier (bias factors read by the consumers: c3 K2 0.585 ms
+        // against 0.535)
+        if (my_id != oob && BW) {
           s_crow[st][lane] = (uint32_t)my_id;
         } else if (my_id != oob) {
           s_crow[st][lane] = (uint32_t)my_id;
@@ -186,7 +193,14 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB)
         }
       }
       if (lane == 0) s_nv[st] = nv;
-      mbar_arrive(&full_bar[st]);
+      if (BW) {
+        __syncwarp();  // row ids and the chunk size are written before lane 0 arrives
+        if (lane == 0) {
+          mbar_arrive(&data_bar[st]);
+        }
+      } else {
+        mbar_arrive(&full_bar[st]);
+      }
       ++k;
       if (++st == S) {
         st = 0;
@@ -206,17 +220,18 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB)
         emit(my_id, chunk_rows(c));
       }
     } else {
-      // fused compaction: the CTA takes 2-KB mask tiles grid-stride (2048
-      // uint8 rows or 512 int32 radii); lane 0 streams them into a 4-deep
-      // shared-memory ring with 1-D bulk copies (mbarrier tx counts), the
-      // warp scans each 512-row block from shared memory (16 rows per lane),
-      // a warp scan packs the visible ids into a ring of pending ids, and
-      // every 32 of them leave as one chunk.  The host runs this path for
-      // 16-byte-aligned masks only.
-      constexpr int kRowsPerTile = MASK == 1 ? 2048 : 512;
-      constexpr int kBlocks = kRowsPerTile / 512;
-      constexpr int kQ = MASK == 1 ? 1 : 4;  // 16-byte smem reads per lane per block
+      // fused compaction: the CTA takes 1-KB mask tiles grid-stride (1024
+      // uint8 rows or 256 int32 radii); lane 0 streams them into a
+      // kMaskRing-deep shared-memory ring with 1-D bulk copies (mbarrier tx
+      // counts); each lane takes 32 uint8 rows (two 16-byte reads, rows
+      // 512 b + 16 lane + j) or 16 radii, one warp scan per tile packs the
+      // visible ids into a ring of pending ids, and every 32 of them leave
+      // as one chunk (ids need no order: rows are independent).  The host
+      // runs this path for 16-byte-aligned masks only.
+      constexpr int kTileBytes = 1024;
       constexpr int kEsz = MASK == 1 ? 1 : 4;
+      constexpr int kRowsPerTile = kTileBytes / kEsz;
+      constexpr int kReads = MASK == 1 ? 2 : 4;  // 16-byte smem reads per lane per tile
       const int64_t nr = n_rows;
       const int n_tiles = (int)((nr + kRowsPerTile - 1) / kRowsPerTile);
       const unsigned char* gmask = reinterpret_cast<const unsigned char*>(vis_mask);
@@ -235,28 +250,18 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB)
         if (lane == 0) {
           if (b > 0) {
             mbar_arrive_expect_tx(&mask_bar[slot], (uint32_t)b);
-            bulk_g2s(s_mask[slot], gmask + (int64_t)t * kRowsPerTile * kEsz, (uint32_t)b,
-                     &mask_bar[slot]);
+            bulk_g2s(s_mask[slot], gmask + (int64_t)t * kTileBytes, (uint32_t)b, &mask_bar[slot]);
           } else {
             mbar_arrive(&mask_bar[slot]);
           }
         }
       };
-      auto bits_of = [&](const uint4 (&v)[kQ]) -> uint32_t {  // bit j: row lane*16 + j visible
-        uint32_t bits = 0;
-        if constexpr (MASK == 1) {
-          const uint32_t w[4] = {v[0].x, v[0].y, v[0].z, v[0].w};
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-#pragma unroll
-            for (int e = 0; e < 4; ++e) bits |= (((w[j] >> (8 * e)) & 0xffu) != 0u) << (4 * j + e);
-        } else {
-#pragma unroll
-          for (int q = 0; q < 4; ++q)
-            bits |= (uint32_t)((int)v[q].x > 0) << (4 * q) | (uint32_t)((int)v[q].y > 0) << (4 * q + 1) |
-                    (uint32_t)((int)v[q].z > 0) << (4 * q + 2) | (uint32_t)((int)v[q].w > 0) << (4 * q + 3);
-        }
-        return bits;
+      // byte offset in the tile of the lane's 16-byte read q, and its first row
+      auto read_off = [&](int q) -> int {
+        return MASK == 1 ? q * 512 + lane * 16 : (lane & 15) * 64 + 16 * q;
+      };
+      auto row_of_bit = [&](int k) -> int {  // bit k of the lane's mask -> row of the tile
+        return MASK == 1 ? (k >> 4) * 512 + lane * 16 + (k & 15) : (lane & 15) * 16 + k;
       };
       int head = 0, tail = 0;  // ring of pending ids: s_pend[head .. tail)
       const int my_tiles = (int)blockIdx.x < n_tiles ? (n_tiles - 1 - (int)blockIdx.x) / G + 1 : 0;
@@ -267,52 +272,81 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB)
         const int slot = k2 % kMaskRing;
         mbar_wait(&mask_bar[slot], (unsigned)((k2 / kMaskRing) & 1));
         const int bb = bulk_bytes(t);
+        uint32_t bits = 0;
+        if (MASK == 1 || lane < 16) {
 #pragma unroll
-        for (int b = 0; b < kBlocks; ++b) {
-          const int lrow = b * 512 + lane * 16;  // row of the tile
-          uint4 v[kQ];
-#pragma unroll
-          for (int q = 0; q < kQ; ++q) {
-            const int off = lrow * kEsz + 16 * q;  // byte offset in the tile
+          for (int q = 0; q < kReads; ++q) {
+            const int off = read_off(q);
+            uint4 v;
             if (off + 16 <= bb) {
-              v[q] = *reinterpret_cast<const uint4*>(s_mask[slot] + off);
+              v = *reinterpret_cast<const uint4*>(s_mask[slot] + off);
             } else {  // ragged end: global element reads (zero past the rows)
               uint32_t w[4] = {0u, 0u, 0u, 0u};
-              const int64_t g0 = (int64_t)t * kRowsPerTile * kEsz + off;
+              const int64_t g0 = (int64_t)t * kTileBytes + off;
 #pragma unroll
               for (int by = 0; by < 16; ++by) {
                 const int64_t gb = g0 + by;
                 if (gb < nr * kEsz) w[by >> 2] |= (uint32_t)gmask[gb] << (8 * (by & 3));
               }
-              v[q] = make_uint4(w[0], w[1], w[2], w[3]);
+              v = make_uint4(w[0], w[1], w[2], w[3]);
+            }
+            if constexpr (MASK == 1) {
+              const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+              for (int j = 0; j < 4; ++j)
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                  bits |= (((w[j] >> (8 * e)) & 0xffu) != 0u) << (16 * q + 4 * j + e);
+            } else {
+              bits |= (uint32_t)((int)v.x > 0) << (4 * q) | (uint32_t)((int)v.y > 0) << (4 * q + 1) |
+                      (uint32_t)((int)v.z > 0) << (4 * q + 2) | (uint32_t)((int)v.w > 0) << (4 * q + 3);
             }
           }
-          const uint32_t bits = bits_of(v);
-          const int cnt = __popc(bits);
-          int incl = cnt;
-#pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += y;
-          }
-          const int total = __shfl_sync(0xffffffffu, incl, 31);
-          int pos = tail + incl - cnt;
-          const int row0 = t * kRowsPerTile + lrow;
-          for (uint32_t x = bits; x; x &= x - 1) s_pend[(pos++) & (kPend - 1)] = row0 + __ffs(x) - 1;
-          tail += total;
-          __syncwarp();
-          while (tail - head >= R) {
-            emit((int)s_pend[(head + lane) & (kPend - 1)], R);
-            head += R;
-          }
         }
-        __syncwarp();  // every lane is done with the slot before it is refilled
+        const int cnt = __popc(bits);
+        int incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        const int total = __shfl_sync(0xffffffffu, incl, 31);
+        int pos = tail + incl - cnt;
+        const int row0 = t * kRowsPerTile;
+        for (uint32_t x = bits; x; x &= x - 1)
+          s_pend[(pos++) & (kPend - 1)] = row0 + row_of_bit(__ffs(x) - 1);
+        tail += total;
+        __syncwarp();  // ids written; every lane is done with the slot
         issue(k2 + kMaskRing);
+        while (tail - head >= R) {
+          emit((int)s_pend[(head + lane) & (kPend - 1)], R);
+          head += R;
+        }
       }
       if (tail > head) emit(lane < tail - head ? (int)s_pend[(head + lane) & (kPend - 1)] : oob,
                             tail - head);
     }
     emit(oob, -1);
+  } else if (BW && warp == NCW + 2) {
+    // ------------------------------------------------------------ bias warp
+    int st = 0;
+    unsigned ph = 0;
+    for (;;) {
+      mbar_wait(&data_bar[st], ph);
+      const int nv = s_nv[st];
+      if (lane < nv) {
+        const float2* srec = reinterpret_cast<const float2*>(stage(st));
+        const int tb = kDense ? P.global_t
+                              : reinterpret_cast<const int*>(srec + lane * SLOTS + L::P)[0] + 1;
+        s_bc[st][lane] = __ldg(reinterpret_cast<const float2*>(P.lut) + (tb < P.lut_len ? tb : P.lut_len - 1));
+      }
+      mbar_arrive(&full_bar[st]);
+      if (nv < 0) break;
+      if (++st == S) {
+        st = 0;
+        ph ^= 1u;
+      }
+    }
   } else if (warp == NCW + 1) {
     // ------------------------------------------------------------------ storer
     int st = 0;
@@ -355,7 +389,9 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB)
     int st = 0;
     int ep = 1;  // this use of stage st (epoch tag of its row flags)
     for (;;) {
-      mbar_wait(&full_bar[st], (unsigned)((ep - 1) & 1));
+      // BW: start on the landed gathers (data barrier); the bias factors
+      // (full barrier, the bias warp) are awaited only after the check pass
+      mbar_wait(BW ? &data_bar[st] : &full_bar[st], (unsigned)((ep - 1) & 1));
       const int nvalid = s_nv[st];
       if (nvalid < 0) {
         mbar_arrive(&done_bar[st]);  // the storer reads the end marker too
@@ -367,8 +403,6 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB)
       const float* sg = sth + R * PT;
       const uint32_t* srow = s_crow[st];
       const int tn = t < nvalid ? reinterpret_cast<const int*>(srec + t * SLOTS + L::P)[0] + 1 : 0;
-      if (MASK != 0 && t < nvalid)  // published by the barrier after the check pass
-        s_bc[st][t] = __ldg(reinterpret_cast<const float2*>(P.lut) + (tn < P.lut_len ? tn : P.lut_len - 1));
       if (!STRICT) {
         // gradients in 16-byte pieces (columns >= P are pad and ignored);
         // activation domain on the opacity / scale columns of theta
@@ -410,6 +444,7 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB)
           dbase += R * W;
         }
       }
+      if (BW) mbar_wait(&full_bar[st], (unsigned)((ep - 1) & 1));  // bias factors staged
       named_sync(1, NC);  // flags of the chunk are final; nobody has written the stage yet
       const bool any_bad = s_any[st] == ep || nvalid < R;
       auto row_ok = [&](int r) { return s_badg[st][r] != ep && s_badd[st][r] != ep; };
@@ -494,14 +529,14 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB)
                                s_exo,          s_exs};
   const bool is_max[GS_STEP_STATS] = {false, false, false, false, false,
                                       false, false, false, false, false};
-  block_reduce_n<GS_STEP_STATS, (NCW + 2)>(acc, is_max, s_red);
+  block_reduce_n<GS_STEP_STATS, NWARPS>(acc, is_max, s_red);
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int f = 0; f < GS_STEP_STATS; ++f)
       P.partials[(size_t)blockIdx.x * GS_STEP_STATS + f] = acc[f];
   }
   if (last_block_arrive(P.counter))
-    final_reduce_n<GS_STEP_STATS, (NCW + 2)>(P.partials, gridDim.x, GS_STEP_STATS, P.stats_out,
+    final_reduce_n<GS_STEP_STATS, NWARPS>(P.partials, gridDim.x, GS_STEP_STATS, P.stats_out,
                                              is_max, s_red);
 }
 
@@ -509,17 +544,17 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB)
 // runtime's driver entry point; no libcuda link dependency).
 bool encode_tma_maps(const FixedParams& P, int64_t n_rows, int rec_box, TmaMaps* out);
 
-template <class L, int MODE, bool STRICT, int S, int NCW, int MINB, int MASK = 0>
+template <class L, int MODE, bool STRICT, int S, int NCW, int MINB, int MASK = 0, bool BW = false>
 void launch_tma4(const FixedParams& P, const TmaMaps& M, int64_t max_rows, cudaStream_t s,
                  const void* vis_mask = nullptr) {
   constexpr int bytes = S * Tma4Stage<L, 32>::kBytes + 128;
-  smem_opt_in<step_tma4_kernel<L, MODE, STRICT, S, NCW, MINB, MASK>>(bytes);
-  const int64_t tile = MASK == 1 ? 2048 : MASK == 2 ? 512 : 32;
+  smem_opt_in<step_tma4_kernel<L, MODE, STRICT, S, NCW, MINB, MASK, BW>>(bytes);
+  const int64_t tile = MASK == 1 ? 1024 : MASK == 2 ? 256 : 32;
   const int64_t work = (max_rows + tile - 1) / tile;
   const int grid =
       (int)std::max<int64_t>(1, std::min<int64_t>(work, (int64_t)gs_sm_count() * MINB));
-  step_tma4_kernel<L, MODE, STRICT, S, NCW, MINB, MASK>
-      <<<grid, (NCW + 2) * 32, bytes, s>>>(P, M, vis_mask);
+  step_tma4_kernel<L, MODE, STRICT, S, NCW, MINB, MASK, BW>
+      <<<grid, (NCW + 2 + (BW ? 1 : 0)) * 32, bytes, s>>>(P, M, vis_mask);
 }
 
 }  // namespace gs

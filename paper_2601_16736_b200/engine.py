@@ -153,7 +153,8 @@ def row_stride(name, t: torch.Tensor, n_rows: int, width: int) -> int:
         if t.shape[d] != 1 and t.stride(d) != expect:
             raise ConfigError(f"{name}: the values of one row must be contiguous")
         expect *= t.shape[d]
-    rs = t.stride(0) if n_rows > 1 else width
+    # one row: its stride is unconstrained by the shape (keep a record view's)
+    rs = t.stride(0) if (n_rows > 1 or t.stride(0) >= width) else width
     if rs < width:
         raise ConfigError(f"{name}: row stride {rs} is below the row width {width}")
     return int(rs)
@@ -489,7 +490,8 @@ class StepEngine:
                     lambda_opacity: float = 0.0, lambda_scale: float = 0.0,
                     clip_opacity: float = 10.0, clip_scale: float = 10.0,
                     n_pixels_rounded: float = 0.0, record: torch.Tensor,
-                    densify: tuple | None = None) -> torch.Tensor | None:
+                    densify: tuple | None = None, low_visibility: bool = False
+                    ) -> torch.Tensor | None:
         """Fused K1 + K2 (gs_step_rows_masked): the step of the mask's visible
         rows with the compaction done inside the step kernel.  Returns the
         statistics, or None when the layout does not take this path (the
@@ -518,8 +520,9 @@ class StepEngine:
                                           vis.data_ptr() if is_radii else None, self.n_rows,
                                           record.data_ptr(), record.stride(0),
                                           self.stats.data_ptr(), self.rows_ws.data_ptr(),
-                                          self.rows_ws.numel(), C.byref(launched),
-                                          _stream_handle(self.device))
+                                          self.rows_ws.numel(),
+                                          L.GS_MASKED_LOW_VISIBILITY if low_visibility else 0,
+                                          C.byref(launched), _stream_handle(self.device))
         _nvtx_pop()
         L.check(rc, "gs_step_rows_masked")
         if not launched.value:

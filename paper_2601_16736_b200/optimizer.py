@@ -297,6 +297,7 @@ class AdamWGS:
         self._nv_reduce = None
         self._abort_reduce = None
         self._clock_bound = 0  # upper bound of every clock (and global_t): sizes the bias LUT
+        self._vis_frac = None  # visible fraction of the last step whose statistics were read
 
     def _maybe_adopt(self, adopt):
         """Per-attribute leaf parameters -> one parameter record and one
@@ -451,7 +452,11 @@ class AdamWGS:
         if mode == "sparse-adam" and (lo != 0.0 or ls != 0.0):
             return None  # the coupled normaliser needs N_v before the step
         eng = self.engine
-        kwm = dict(eps=self.eps, record=self.state.record, densify=kw.get("densify"))
+        # the kernel shape for sparse masks when the last known step (the
+        # deferred statistics; no synchronisation) saw under 5% visible
+        low = self._vis_frac is not None and self._vis_frac < 0.05
+        kwm = dict(eps=self.eps, record=self.state.record, densify=kw.get("densify"),
+                   low_visibility=low)
         if mode == "adamw-gs":
             if n_pixels is None:
                 raise ConfigError("adamw-gs needs n_pixels (N_I)")
@@ -623,6 +628,8 @@ class AdamWGS:
         return StepGraph(self, visibility, n_pixels, grads, step_kwargs)
 
     def _raise_for(self, st: dict, flag: int, ctx):
+        if self.n_rows:
+            self._vis_frac = st["n_visible"] / self.n_rows
         if flag and self.mode == "coupled-adam":
             # the strict check aborted the step before any mutation: the
             # reference checks before advancing the clock (optimizer.py:225-226)
@@ -651,7 +658,10 @@ class AdamWGS:
 
     def last_stats(self) -> dict:
         """Per-step statistics of the last step (host sync)."""
-        return _stats_dict(self.engine.stats.tolist())
+        st = _stats_dict(self.engine.stats.tolist())
+        if self.n_rows:
+            self._vis_frac = st["n_visible"] / self.n_rows
+        return st
 
     # ----------------------------------------------- densification statistics
     def enable_densify_stats(self, group: str | None = None):

@@ -217,6 +217,8 @@ class ShardedAdamWGS:
         """Every rank sees the same reduced statistics and flag, so every
         rank takes this branch together; the ids are gathered globally."""
         opt = self.opt
+        if self.n_global:
+            opt._vis_frac = st["n_visible"] / self.n_global  # the kernel-shape hint
         if flag and opt.mode == "coupled-adam":
             opt.state.global_t -= 1  # aborted everywhere before any mutation
         bad_g = st["n_bad_grad"] > 0 or (flag & 1)

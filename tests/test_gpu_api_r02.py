@@ -392,7 +392,9 @@ def test_fused_compaction_equals_index_path(n, kind, mode):
                 m = m.to(DEV)
             _, g = R.pack({k: torch.from_numpy(x).to(DEV) for k, x in S.step_grads(cfg, s, vis).items()})
             opt.step(m, cfg.n_pixels, grads=g)
-            assert (opt._last_ctx[1] is None) == fused
+            # unaligned masks (offset views) take K1 + K2: the fused loader
+            # streams 16-byte-aligned mask tiles
+            assert (opt._last_ctx[1] is None) == (fused and not kind.startswith("offset")) or n == 1
             stats.append(opt.last_stats())
         opt.check_errors()
         outs.append(({k: p.cpu().numpy() for k, p in params.items()},
