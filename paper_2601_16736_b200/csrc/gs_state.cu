@@ -547,34 +547,38 @@ __global__ void __launch_bounds__(kThreads)
     s_red[NW + warp] = n_active;
   }
   __syncthreads();
-  double acc[kStatsFields];
+  // block fold: thread f owns output field f and walks (warp, lane, set) in
+  // a fixed order
+  const int nf = 2 + 5 * S.n;
+  if ((int)threadIdx.x < nf) {
+    const int f = threadIdx.x;
+    double o = 0.0;
+    if (f < 2) {
+      for (int w = 0; w < NW; ++w) o += s_red[f * NW + w];
+    } else {
+      const int g = (f - 2) / 5, fld = (f - 2) % 5;
+      const bool mx = fld == 1 || fld == 4;
+      for (int w = 0; w < NW; ++w)
+        for (int l = 0; l < 32; ++l)
+#pragma unroll
+          for (int k = 0; k < 2 * J; ++k) {
+            const int sl = 2 * (l + 32 * (k / 2)) + (k & 1);
+            if (sl < 128 && s_grp[sl] == g) {
+              const double x = s_acc[w][l][k][fld];
+              o = mx ? fmax(o, x) : o + x;
+            }
+          }
+    }
+    partials[(size_t)blockIdx.x * kStatsFields + f] = o;
+    __threadfence();  // every writer publishes its partial before the last-block count
+  } else if ((int)threadIdx.x < kStatsFields) {
+    partials[(size_t)blockIdx.x * kStatsFields + threadIdx.x] = 0.0;
+    __threadfence();
+  }
   bool is_max[kStatsFields];
 #pragma unroll
-  for (int f = 0; f < kStatsFields; ++f) {
-    acc[f] = 0.0;
+  for (int f = 0; f < kStatsFields; ++f)
     is_max[f] = f >= 2 && (((f - 2) % 5) == 1 || ((f - 2) % 5) == 4);
-  }
-  if (threadIdx.x == 0) {
-    for (int w = 0; w < NW; ++w) {
-      acc[0] += s_red[w];
-      acc[1] += s_red[NW + w];
-    }
-    for (int w = 0; w < NW; ++w)
-      for (int l = 0; l < 32; ++l)
-        for (int k = 0; k < 2 * J; ++k) {
-          const int sl = 2 * (l + 32 * (k / 2)) + (k & 1);
-          const int g = sl < 128 ? s_grp[sl] : -1;
-          if (g < 0) continue;
-          const double* A = s_acc[w][l][k];
-          double* o = acc + 2 + 5 * g;
-          o[0] += A[0];
-          o[1] = fmax(o[1], A[1]);
-          o[2] += A[2];
-          o[3] += A[3];
-          o[4] = fmax(o[4], A[4]);
-        }
-    for (int f = 0; f < kStatsFields; ++f) partials[(size_t)blockIdx.x * kStatsFields + f] = acc[f];
-  }
   if (last_block_arrive(counter)) {
     double tmp[kStatsFields];
     final_reduce<kStatsFields>(partials, gridDim.x, kStatsFields, tmp, is_max, s_red);
@@ -609,7 +613,6 @@ __global__ void __launch_bounds__(kThreads)
         if (sl < off + S.g[gi].width) break;
         off += S.g[gi].width;
       }
-      const int W = S.g[gi].width;
       const int c = sl - off;
       const float2 mv = reinterpret_cast<const float2*>(rec)[sl];
       const float mh = __fmul_rn(mv.x, bc.x);

@@ -256,6 +256,11 @@ int gs_step_fixed_masked_try(const gs_group* groups, int32_t n_groups, const gs_
   if (cfg->mode == GS_MODE_SPARSE_ADAM && (cfg->lambda_opacity != 0.0 || cfg->lambda_scale != 0.0))
     return 0;
   if (fixed_variant() == 21 || n_rows < 1) return 0;
+  // one CTA per 1-KB mask tile: below ~2 tiles per CTA slot the fused grid
+  // would leave SMs idle (c1, 100k rows: 98 CTAs); K1 + K2 spreads the
+  // visible rows over the whole GPU instead
+  const int64_t tile_rows = radii ? 256 : 1024;
+  if ((n_rows + tile_rows - 1) / tile_rows < 2 * (int64_t)gs_sm_count() * 2) return 0;
   // the loader streams 2-KB mask tiles with 16-byte bulk copies
   if ((reinterpret_cast<uintptr_t>(radii ? static_cast<const void*>(radii)
                                          : static_cast<const void*>(mask)) & 15u) != 0)

@@ -223,8 +223,8 @@ __global__ void __launch_bounds__((NCW + 2 + (BW ? 1 : 0)) * 32, MINB)
       // fused compaction: the CTA takes 1-KB mask tiles grid-stride (1024
       // uint8 rows or 256 int32 radii); lane 0 streams them into a
       // kMaskRing-deep shared-memory ring with 1-D bulk copies (mbarrier tx
-      // counts); each lane takes 32 uint8 rows (two 16-byte reads, rows
-      // 512 b + 16 lane + j) or 16 radii, one warp scan per tile packs the
+      // counts); each lane takes 32 consecutive uint8 rows (two 16-byte
+      // reads) or 16 radii, one warp scan per tile packs the
       // visible ids into a ring of pending ids, and every 32 of them leave
       // as one chunk (ids need no order: rows are independent).  The host
       // runs this path for 16-byte-aligned masks only.
@@ -257,11 +257,14 @@ __global__ void __launch_bounds__((NCW + 2 + (BW ? 1 : 0)) * 32, MINB)
         }
       };
       // byte offset in the tile of the lane's 16-byte read q, and its first row
+      // each lane owns contiguous rows (32 uint8 rows or 16 radii), so the
+      // pending ids, and hence the chunks, stay in ascending row order within
+      // a tile (index-coherent masks keep their DRAM locality)
       auto read_off = [&](int q) -> int {
-        return MASK == 1 ? q * 512 + lane * 16 : (lane & 15) * 64 + 16 * q;
+        return MASK == 1 ? lane * 32 + 16 * q : (lane & 15) * 64 + 16 * q;
       };
       auto row_of_bit = [&](int k) -> int {  // bit k of the lane's mask -> row of the tile
-        return MASK == 1 ? (k >> 4) * 512 + lane * 16 + (k & 15) : (lane & 15) * 16 + k;
+        return MASK == 1 ? lane * 32 + k : (lane & 15) * 16 + k;
       };
       int head = 0, tail = 0;  // ring of pending ids: s_pend[head .. tail)
       const int my_tiles = (int)blockIdx.x < n_tiles ? (n_tiles - 1 - (int)blockIdx.x) / G + 1 : 0;
