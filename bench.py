@@ -88,6 +88,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-legs", action="store_true", help="skip the c5 strong-scaling legs")
+    ap.add_argument("--no-fused", dest="fused", action="store_false",
+                    help="K1 then K2 on the index list instead of the fused one-launch step")
     ap.add_argument("--sharded", action="store_true",
                     help="run ShardedAdamWGS (NCCL process group) even on one GPU")
     ap.add_argument("--e2e-steps", type=int, default=20)
@@ -392,7 +394,7 @@ class Workload:
         self.n_rep = l2_replicas(n, p_vis)
         kw = dict(mode=wl["mode"], lambda_o=wl["lo"], lambda_s=wl["ls"], check=args.check,
                   errors="ignore", state_layout=args.layout, state_row_align=args.state_align,
-                  adopt=False)
+                  adopt=False, fused_compaction=args.fused)
         self.opts, self.shards, self.grad_sets = [], [], []
         for j in range(self.n_rep):
             cj = S.WorkloadConfig(n=n, p_vis=p_vis, mask_family=mask,
@@ -817,7 +819,8 @@ def run_e2e(args, w, dev, world):
         host_masks.append(hm)
     mask_vis = [float(m.sum()) for m in host_masks]
     dev_mask = torch.empty_like(w.masks[0])
-    stats_host = torch.empty(10, dtype=torch.float64, pin_memory=True)
+    from paper_2601_16736_b200 import _lib as L
+    stats_host = torch.empty(L.GS_STEP_STATS, dtype=torch.float64, pin_memory=True)
     dense = sum(t.numel() * 4 for t in host_dense)
     d2h = stats_host.numel() * 8
     step = sh.step if sh is not None else opt.step

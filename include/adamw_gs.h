@@ -80,7 +80,10 @@ extern "C" {
 #define GS_STAT_N_CLIP_SCALE 7   /* scale penalty terms that hit C_t / clip */
 #define GS_STAT_SUM_EXTRA_OPACITY 8
 #define GS_STAT_SUM_EXTRA_SCALE 9
-#define GS_STEP_STATS 10
+#define GS_STAT_N_RUNS 10        /* layout hint: row runs that start a new run within a chunk of
+                                  * the record kernels (0 from the other kernels); n_visible /
+                                  * n_runs near 1 = scattered rows, >> 1 = index-coherent masks */
+#define GS_STEP_STATS 11
 
 /* One attribute group: row-major [n_rows, width] fp32, contiguous rows. */
 typedef struct gs_group {

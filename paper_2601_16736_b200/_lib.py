@@ -27,8 +27,11 @@ CHECK_FUSED, CHECK_STRICT = 0, 1
 
 STAT_FIELDS = ("n_visible", "n_stepped", "n_bad_grad", "n_bad_domain", "n_active_pre",
                "n_active_post", "n_clip_opacity", "n_clip_scale", "sum_extra_opacity",
-               "sum_extra_scale")
+               "sum_extra_scale", "n_runs")
 GS_STEP_STATS = len(STAT_FIELDS)
+# n_runs is a layout hint (how index-coherent the visible rows were), not a
+# reference statistic: it depends on the kernel's chunking
+HINT_FIELDS = ("n_runs",)
 
 
 class ExtensionMissing(RuntimeError):

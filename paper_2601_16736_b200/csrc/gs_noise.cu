@@ -50,6 +50,13 @@ struct RowStrides {
   int64_t x, y, z, w;  // position, log_scale, rotation, opacity_logit
 };
 
+// 3DGS rows of the SH-3 parameter record (records.py): position at column
+// 0, opacity 51, log-scales 52..54, quaternion 55..58 of one 16-byte-aligned
+// row (stride a multiple of 4).  Four 16-byte loads bring a row's inputs
+// (columns 0..3 and 48..59), one 16-byte store writes the position back
+// (column 3, f_dc[0], is rewritten unchanged).
+constexpr int kRecOpac = 51, kRecScale = 52, kRecRot = 55;
+
 template <int D>
 __global__ void __launch_bounds__(256)
     noise_kernel(float* __restrict__ pos, const float* __restrict__ kappa,
@@ -104,6 +111,67 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+__device__ __forceinline__ float3 noise_delta3(const float4 q4, const float3 ks, float tau,
+                                               uint32_t row_lo, uint32_t row_hi, uint32_t it,
+                                               uint2 key, float coef, float lambda_mu,
+                                               float lambda_t) {
+  const uint4 rnd = philox4x32_10(make_uint4(row_lo, row_hi, it, 0x6e6f6973u), key);
+  const float2 g01 = box_muller(rnd.x, rnd.y);
+  const float2 g23 = box_muller(rnd.z, rnd.w);
+  const float o = sigmoidf_stable(tau);
+  const float gate = sigmoidf_stable(-lambda_mu * (o - lambda_t));
+  const float a = -coef * gate;
+  const float qn = rsqrtf(q4.x * q4.x + q4.y * q4.y + q4.z * q4.z + q4.w * q4.w);
+  const float w = q4.x * qn, x = q4.y * qn, y = q4.z * qn, z = q4.w * qn;
+  const float Rm[3][3] = {{1.f - 2.f * (y * y + z * z), 2.f * (x * y - w * z), 2.f * (x * z + w * y)},
+                          {2.f * (x * y + w * z), 1.f - 2.f * (x * x + z * z), 2.f * (y * z - w * x)},
+                          {2.f * (x * z - w * y), 2.f * (y * z + w * x), 1.f - 2.f * (x * x + y * y)}};
+  const float g[3] = {g01.x, g01.y, g23.x};
+  const float e[3] = {expf(2.0f * ks.x), expf(2.0f * ks.y), expf(2.0f * ks.z)};
+  float u[3];
+#pragma unroll
+  for (int r = 0; r < 3; ++r)  // u = S^2 R^T gamma
+    u[r] = e[r] * (Rm[0][r] * g[0] + Rm[1][r] * g[1] + Rm[2][r] * g[2]);
+  return make_float3(a * (Rm[0][0] * u[0] + Rm[0][1] * u[1] + Rm[0][2] * u[2]),
+                     a * (Rm[1][0] * u[0] + Rm[1][1] * u[1] + Rm[1][2] * u[2]),
+                     a * (Rm[2][0] * u[0] + Rm[2][1] * u[1] + Rm[2][2] * u[2]));
+}
+
+// The same noise as noise_kernel<3> (identical draws and arithmetic) on SH-3
+// parameter records, 16-byte accesses.
+__global__ void __launch_bounds__(256)
+    noise_rec_kernel(float* __restrict__ rec, int64_t stride, const uint8_t* __restrict__ alive,
+                     int64_t n, float coef, float lambda_mu, float lambda_t, uint2 key,
+                     uint32_t iteration, float* __restrict__ delta_out, int add) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float* row = rec + i * stride;
+    const bool live = alive == nullptr || alive[i];
+    float3 d = make_float3(0.f, 0.f, 0.f);
+    float4 p4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (live) {
+      p4 = *reinterpret_cast<const float4*>(row);
+      const float4 c48 = *reinterpret_cast<const float4*>(row + 48);  // .w = opacity (51)
+      const float4 c52 = *reinterpret_cast<const float4*>(row + 52);  // log-scales, q.w
+      const float4 c56 = *reinterpret_cast<const float4*>(row + 56);  // q.x, q.y, q.z, pad
+      d = noise_delta3(make_float4(c52.w, c56.x, c56.y, c56.z), make_float3(c52.x, c52.y, c52.z),
+                       c48.w, (uint32_t)i, (uint32_t)(i >> 32), iteration, key, coef, lambda_mu,
+                       lambda_t);
+    }
+    if (delta_out) {
+      delta_out[3 * i] = d.x;
+      delta_out[3 * i + 1] = d.y;
+      delta_out[3 * i + 2] = d.z;
+    }
+    if (add && live) {
+      p4.x += d.x;
+      p4.y += d.y;
+      p4.z += d.z;
+      *reinterpret_cast<float4*>(row) = p4;
+    }
+  }
+}
+
 }  // namespace gs
 
 extern "C" int gs_noise_perturb(float* position, const float* log_scale, const float* rotation,
@@ -132,9 +200,16 @@ extern "C" int gs_noise_perturb(float* position, const float* log_scale, const f
   if (n == 0) return GS_OK;
   const uint2 key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
   const float coef = eta_ratio * lr_position;
-  const int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)gs_sm_count() * 8);
+  const int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)gs_sm_count() * 32);
   cudaStream_t s = (cudaStream_t)stream;
-  if (dims == 2)
+  const bool rec = dims == 3 && rs.x == rs.y && rs.x == rs.z && rs.x == rs.w && rs.x % 4 == 0 &&
+                   rs.x >= 60 && (reinterpret_cast<uintptr_t>(position) & 15u) == 0 &&
+                   opacity_logit == position + kRecOpac && log_scale == position + kRecScale &&
+                   rotation == position + kRecRot;
+  if (rec) {
+    noise_rec_kernel<<<grid, 256, 0, s>>>(position, rs.x, alive, n, coef, lambda_mu, lambda_t,
+                                          key, iteration, delta_out, add_in_place);
+  } else if (dims == 2)
     noise_kernel<2><<<grid, 256, 0, s>>>(position, log_scale, rotation, opacity_logit, alive, n,
                                          coef, lambda_mu, lambda_t, key, iteration, delta_out,
                                          add_in_place, rs);

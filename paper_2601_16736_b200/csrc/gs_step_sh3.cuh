@@ -1991,10 +1991,14 @@ template <class L, int MODE>
 void launch_fixed_masked(const FixedParams& P, const TmaMaps& M, int64_t n_rows, int mask_kind,
                          const void* mask, bool low_vis, cudaStream_t s) {
   static const int force = getenv("GS_TMA4_BW") ? atoi(getenv("GS_TMA4_BW")) : -1;
+  static const int mtb = getenv("GS_TMA4_MTB") ? atoi(getenv("GS_TMA4_MTB")) : 1024;
   const bool bw = force >= 0 ? force != 0 : low_vis;
   if (mask_kind == 2) {
     if (bw) launch_tma4<L, MODE, false, 3, 8, 2, 2, true>(P, M, n_rows, s, mask);
     else launch_tma4<L, MODE, false, 3, 8, 2, 2, false>(P, M, n_rows, s, mask);
+  } else if (mtb == 512) {
+    if (bw) launch_tma4<L, MODE, false, 3, 8, 2, 1, true, 512>(P, M, n_rows, s, mask);
+    else launch_tma4<L, MODE, false, 3, 8, 2, 1, false, 512>(P, M, n_rows, s, mask);
   } else {
     if (bw) launch_tma4<L, MODE, false, 3, 8, 2, 1, true>(P, M, n_rows, s, mask);
     else launch_tma4<L, MODE, false, 3, 8, 2, 1, false>(P, M, n_rows, s, mask);

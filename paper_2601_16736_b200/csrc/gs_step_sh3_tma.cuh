@@ -88,7 +88,8 @@ __device__ __forceinline__ void tma_scatter4(const CUtensorMap* map, const void*
 // into bias factors after the gathers land, so the loader's per-chunk work
 // is only the TMA issue (the mask-scanning loader); without it the loader
 // reads each row's clock and LUT entry itself.
-template <class L, int MODE, bool STRICT, int S, int NCW, int MINB, int MASK, bool BW = false>
+template <class L, int MODE, bool STRICT, int S, int NCW, int MINB, int MASK, bool BW = false,
+          int MTB = 1024>
 __global__ void __launch_bounds__((NCW + 2 + (BW ? 1 : 0)) * 32, MINB)
     step_tma4_kernel(const FixedParams P, const __grid_constant__ TmaMaps M, const void* vis_mask) {
   constexpr int NWARPS = NCW + 2 + (BW ? 1 : 0);
@@ -113,8 +114,8 @@ __global__ void __launch_bounds__((NCW + 2 + (BW ? 1 : 0)) * 32, MINB)
   __shared__ int s_nv[S];  // rows of the chunk in the stage; -1 ends the CTA's chunk stream
   constexpr int kPend = MASK != 0 ? 2048 : 1;  // pending visible ids (fused compaction)
   __shared__ uint32_t s_pend[kPend];
-  constexpr int kMaskRing = MASK != 0 ? 6 : 1;  // 1-KB mask tiles in flight (fused compaction)
-  __shared__ __align__(128) unsigned char s_mask[kMaskRing][MASK != 0 ? 1024 : 16];
+  constexpr int kMaskRing = MASK != 0 ? 6 * 1024 / MTB : 1;  // 6 KB of mask tiles in flight
+  __shared__ __align__(128) unsigned char s_mask[kMaskRing][MASK != 0 ? MTB : 16];
   __shared__ __align__(8) uint64_t mask_bar[kMaskRing];
   __shared__ double s_red[GS_STEP_STATS * NWARPS];
   // TMA boxes land 128-byte aligned (the host adds 128 bytes of slack)
@@ -152,7 +153,7 @@ __global__ void __launch_bounds__((NCW + 2 + (BW ? 1 : 0)) * 32, MINB)
   __syncthreads();
 
   unsigned c_vis = 0, c_step = 0, c_badg = 0, c_badd = 0, c_apre = 0, c_apost = 0, c_clo = 0,
-           c_cls = 0;
+           c_cls = 0, c_runs = 0;
   double s_exo = 0.0, s_exs = 0.0;
 
   if (warp == NCW) {
@@ -173,6 +174,11 @@ __global__ void __launch_bounds__((NCW + 2 + (BW ? 1 : 0)) * 32, MINB)
         const int r1 = __shfl_sync(0xffffffffu, my_id, q + 1);
         const int r2 = __shfl_sync(0xffffffffu, my_id, q + 2);
         const int r3 = __shfl_sync(0xffffffffu, my_id, q + 3);
+        // layout hint: rows that do not continue the previous row's run
+        const int prev = __shfl_up_sync(0xffffffffu, my_id, 1);
+        const unsigned starts =
+            __ballot_sync(0xffffffffu, lane < nv && (lane == 0 || prev + 1 != my_id));
+        if (lane == 0) c_runs += __popc(starts);
         if (lane < R / 4) {
           tma_gather4(sb + lane * 4 * ST::kRecRow, &M.rec, r0, r1, r2, r3, tbar);
           tma_gather4(sb + ST::kRec + lane * 4 * PT * 4, &M.prm, r0, r1, r2, r3, tbar);
@@ -228,10 +234,12 @@ __global__ void __launch_bounds__((NCW + 2 + (BW ? 1 : 0)) * 32, MINB)
       // visible ids into a ring of pending ids, and every 32 of them leave
       // as one chunk (ids need no order: rows are independent).  The host
       // runs this path for 16-byte-aligned masks only.
-      constexpr int kTileBytes = 1024;
+      constexpr int kTileBytes = MTB;
+      static_assert(MASK != 1 || MTB == 512 || MTB == 1024, "16 or 32 mask bytes per lane");
       constexpr int kEsz = MASK == 1 ? 1 : 4;
       constexpr int kRowsPerTile = kTileBytes / kEsz;
-      constexpr int kReads = MASK == 1 ? 2 : 4;  // 16-byte smem reads per lane per tile
+      constexpr int kLane = MASK == 1 ? MTB / 32 : 64;  // mask bytes per lane
+      constexpr int kReads = kLane / 16;              // 16-byte smem reads per lane per tile
       const int64_t nr = n_rows;
       const int n_tiles = (int)((nr + kRowsPerTile - 1) / kRowsPerTile);
       const unsigned char* gmask = reinterpret_cast<const unsigned char*>(vis_mask);
@@ -261,10 +269,10 @@ __global__ void __launch_bounds__((NCW + 2 + (BW ? 1 : 0)) * 32, MINB)
       // pending ids, and hence the chunks, stay in ascending row order within
       // a tile (index-coherent masks keep their DRAM locality)
       auto read_off = [&](int q) -> int {
-        return MASK == 1 ? lane * 32 + 16 * q : (lane & 15) * 64 + 16 * q;
+        return MASK == 1 ? lane * kLane + 16 * q : (lane & (MTB / 64 - 1)) * 64 + 16 * q;
       };
       auto row_of_bit = [&](int k) -> int {  // bit k of the lane's mask -> row of the tile
-        return MASK == 1 ? lane * 32 + k : (lane & 15) * 16 + k;
+        return MASK == 1 ? lane * kLane + k : (lane & (MTB / 64 - 1)) * 16 + k;
       };
       int head = 0, tail = 0;  // ring of pending ids: s_pend[head .. tail)
       const int my_tiles = (int)blockIdx.x < n_tiles ? (n_tiles - 1 - (int)blockIdx.x) / G + 1 : 0;
@@ -276,7 +284,7 @@ __global__ void __launch_bounds__((NCW + 2 + (BW ? 1 : 0)) * 32, MINB)
         mbar_wait(&mask_bar[slot], (unsigned)((k2 / kMaskRing) & 1));
         const int bb = bulk_bytes(t);
         uint32_t bits = 0;
-        if (MASK == 1 || lane < 16) {
+        if (MASK == 1 || lane < MTB / 64) {
 #pragma unroll
           for (int q = 0; q < kReads; ++q) {
             const int off = read_off(q);
@@ -529,7 +537,7 @@ __global__ void __launch_bounds__((NCW + 2 + (BW ? 1 : 0)) * 32, MINB)
 
   double acc[GS_STEP_STATS] = {(double)c_vis,  (double)c_step, (double)c_badg, (double)c_badd,
                                (double)c_apre, (double)c_apost, (double)c_clo, (double)c_cls,
-                               s_exo,          s_exs};
+                               s_exo,          s_exs,          (double)c_runs};
   const bool is_max[GS_STEP_STATS] = {false, false, false, false, false,
                                       false, false, false, false, false};
   block_reduce_n<GS_STEP_STATS, NWARPS>(acc, is_max, s_red);
@@ -547,16 +555,17 @@ __global__ void __launch_bounds__((NCW + 2 + (BW ? 1 : 0)) * 32, MINB)
 // runtime's driver entry point; no libcuda link dependency).
 bool encode_tma_maps(const FixedParams& P, int64_t n_rows, int rec_box, TmaMaps* out);
 
-template <class L, int MODE, bool STRICT, int S, int NCW, int MINB, int MASK = 0, bool BW = false>
+template <class L, int MODE, bool STRICT, int S, int NCW, int MINB, int MASK = 0, bool BW = false,
+          int MTB = 1024>
 void launch_tma4(const FixedParams& P, const TmaMaps& M, int64_t max_rows, cudaStream_t s,
                  const void* vis_mask = nullptr) {
   constexpr int bytes = S * Tma4Stage<L, 32>::kBytes + 128;
-  smem_opt_in<step_tma4_kernel<L, MODE, STRICT, S, NCW, MINB, MASK, BW>>(bytes);
-  const int64_t tile = MASK == 1 ? 1024 : MASK == 2 ? 256 : 32;
+  smem_opt_in<step_tma4_kernel<L, MODE, STRICT, S, NCW, MINB, MASK, BW, MTB>>(bytes);
+  const int64_t tile = MASK == 1 ? MTB : MASK == 2 ? MTB / 4 : 32;
   const int64_t work = (max_rows + tile - 1) / tile;
   const int grid =
       (int)std::max<int64_t>(1, std::min<int64_t>(work, (int64_t)gs_sm_count() * MINB));
-  step_tma4_kernel<L, MODE, STRICT, S, NCW, MINB, MASK, BW>
+  step_tma4_kernel<L, MODE, STRICT, S, NCW, MINB, MASK, BW, MTB>
       <<<grid, (NCW + 2 + (BW ? 1 : 0)) * 32, bytes, s>>>(P, M, vis_mask);
 }
 

@@ -217,8 +217,10 @@ class ShardedAdamWGS:
         """Every rank sees the same reduced statistics and flag, so every
         rank takes this branch together; the ids are gathered globally."""
         opt = self.opt
-        if self.n_global:
-            opt._vis_frac = st["n_visible"] / self.n_global  # the kernel-shape hint
+        if self.n_global:  # the kernel-choice hints (global view)
+            opt._vis_frac = st["n_visible"] / self.n_global
+            if st.get("n_runs", 0) > 0:
+                opt._vis_run = st["n_visible"] / st["n_runs"]
         if flag and opt.mode == "coupled-adam":
             opt.state.global_t -= 1  # aborted everywhere before any mutation
         bad_g = st["n_bad_grad"] > 0 or (flag & 1)

@@ -1,7 +1,8 @@
 """Drop-in path timing on one B200: the c3 workload (6M SH-3 Gaussians, 30%
 i.i.d. visibility, adamw-gs) stepped through the public API with gradients
-read from ``p.grad`` of per-attribute ``nn.Parameter``s, with and without
-``records.adopt``.  Eager ``opt.step(mask, n_pixels)`` calls, 10 warm-up and
+read from ``p.grad`` of per-attribute ``nn.Parameter``s: the default
+construction (``adopt="auto"``: AdamWGS re-homes them into records) and
+``adopt=False`` (per-attribute gathers).  Eager ``opt.step(mask, n_pixels)`` calls, 10 warm-up and
 50 timed steps between CUDA events, fresh mask per step (pre-generated).
 
 usage: python scripts/adopt_bench.py [n]"""
@@ -22,17 +23,14 @@ def run(adopt: bool, n: int, warm: int = 10, steps: int = 50) -> dict:
     cfg = S.WorkloadConfig(n=n, p_vis=0.3, seed=0)
     params = {k: torch.nn.Parameter(t) for k, t in S.make_params_device(cfg, dev).items()}
     grads = S.grads_device(cfg, 0, dev)
-    if adopt:
-        R.adopt(params)
     for k, p in params.items():
-        if p.grad is None:
-            p.grad = grads[k].view(p.shape).clone()
-        else:
-            with torch.no_grad():
-                p.grad.copy_(grads[k].view(p.shape))
+        p.grad = grads[k].view(p.shape).clone()
     del grads
+    # reference-style construction; the default adopt="auto" re-homes the
+    # Parameters (and their .grad) into records
     opt = AdamWGS(S.param_groups(params), mode="adamw-gs", lambda_o=cfg.lambda_o,
-                  lambda_s=cfg.lambda_s, errors="defer")
+                  lambda_s=cfg.lambda_s, adopt="auto" if adopt else False)
+    assert (opt.param_record is not None) == adopt
     masks = [S.visibility_device(cfg, s, dev) for s in range(warm + steps)]
     n_vis = sum(int(m.sum()) for m in masks[warm:])
     for s in range(warm):
@@ -48,7 +46,8 @@ def run(adopt: bool, n: int, warm: int = 10, steps: int = 50) -> dict:
     ms = a.elapsed_time(b) / steps
     st = opt.last_stats()
     assert st["n_stepped"] == st["n_visible"], st
-    return {"params": "adopted record" if adopt else "per-attribute nn.Parameters",
+    return {"params": "per-attribute nn.Parameters, AdamWGS(adopt='auto') (default)" if adopt
+            else "per-attribute nn.Parameters, AdamWGS(adopt=False)",
             "n": n, "ms_per_step": ms, "visible_per_s": n_vis / steps / (ms / 1e3)}
 
 

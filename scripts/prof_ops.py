@@ -117,6 +117,9 @@ def main():
     aiu = AiuConfig(start=0, end=100, prob_schedule=((0, 0.1),), eta_schedule=((0, 0.5),),
                     enabled=True)
     opt._capturing = False
+    # one step with every row visible, so every AIU pick has a clock > 0 and
+    # takes the full update (the byte count below assumes it)
+    opt.step(torch.ones(n, dtype=torch.bool, device=dev), cfg.n_pixels, grads=grads)
     opt.aiu_apply(vis, aiu, stream(0, "aiu", 4), 4)
     torch.cuda.synchronize()
     t0 = torch.cuda.Event(enable_timing=True)

@@ -282,6 +282,8 @@ def test_tma_record_kernel_ragged_and_bad_rows(n, mode):
         assert np.array_equal(pa[k], pb[k]), k
     assert np.array_equal(ra[:, :120].view(np.int32), rb[:, :120].view(np.int32))
     for f in sa:  # the fused compaction groups rows into chunks differently: sums reorder
+        if f == "n_runs":  # layout hint, depends on the chunking
+            continue
         if f.startswith("sum_"):
             assert sa[f] == pytest.approx(sb[f], rel=1e-12, abs=0), f
         else:
@@ -409,6 +411,8 @@ def test_fused_compaction_equals_index_path(n, kind, mode):
     assert np.array_equal(ra.view(np.int32), rb.view(np.int32))
     for x, y in zip(sa, sb):
         for f in x:
+            if f == "n_runs":
+                continue
             if f.startswith("sum_"):
                 assert x[f] == pytest.approx(y[f], rel=1e-12, abs=0), f
             else:
@@ -435,3 +439,27 @@ def test_device_bernoulli_is_host_draw(skip, n_total, first, n):
     got = device_bernoulli(b, n_total, 0.3, first, n, torch.device(DEV)).cpu().numpy()
     assert np.array_equal(got.astype(bool), want)
     assert np.array_equal(a.random(9), b.random(9))
+
+
+def test_noise_record_fast_path_matches_generic():
+    """gs_noise_perturb on SH-3 parameter records (16-byte row accesses)
+    draws the same noise as the generic strided path: same Philox counters,
+    same arithmetic (agreement to fp32 rounding)."""
+    from paper_2601_16736_b200 import records as R
+    from paper_2601_16736_b200 import synthetic as S
+    from paper_2601_16736_b200.noise import NoiseConfig
+    from paper_2601_16736_b200.optimizer import AdamWGS
+    cfg, host = _cloud(50_001, seed=3)
+    outs = []
+    for rec in (True, False):
+        params = {k: torch.from_numpy(v).to(DEV) for k, v in host.items()}
+        if rec:
+            _, params = R.pack(params)
+        opt = AdamWGS(S.param_groups(params), mode="adamw-gs", adopt=False)
+        alive = torch.from_numpy(np.random.default_rng(1).random(cfg.n) < 0.9).to(DEV)
+        d = opt.noise_perturb(1e-3, NoiseConfig(enabled=True), seed=77, iteration=5, alive=alive)
+        outs.append((d.cpu().numpy(), params["xyz"].cpu().numpy()))
+    (da, xa), (db, xb) = outs
+    assert np.abs(da - db).max() <= 1e-6 * np.abs(db).max()
+    assert np.abs(xa - xb).max() <= 1e-6 * np.abs(xb).max()
+    assert np.count_nonzero(da) > 0

@@ -529,6 +529,8 @@ def test_step_kernels_all_identical(mode, check):
                 assert np.array_equal(res[i][k], ref[i][k]), (run, i, k)
         assert np.array_equal(res[3], ref[3]), run
         for f, x in ref[4].items():
+            if f == "n_runs":  # layout hint: depends on the kernel's chunking
+                continue
             if f.startswith("sum_"):
                 assert res[4][f] == pytest.approx(x, rel=1e-12), (run, f)
             else:
