@@ -137,6 +137,17 @@ __device__ __forceinline__ float3 noise_delta3(const float4 q4, const float3 ks,
                      a * (Rm[2][0] * u[0] + Rm[2][1] * u[1] + Rm[2][2] * u[2]));
 }
 
+// 16-byte load with a 64-byte L2 fetch: a record row's inputs sit in two
+// 64-byte granules (columns 0..3 and 48..59 of 64); the default 128-byte
+// fetch would pull the whole 256-byte row
+__device__ __forceinline__ float4 ld_l2_64(const float* p) {
+  float4 v;
+  asm volatile("ld.global.nc.L2::64B.v4.f32 {%0, %1, %2, %3}, [%4];\n"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p));
+  return v;
+}
+
 // The same noise as noise_kernel<3> (identical draws and arithmetic) on SH-3
 // parameter records, 16-byte accesses.
 __global__ void __launch_bounds__(256)
@@ -150,10 +161,10 @@ __global__ void __launch_bounds__(256)
     float3 d = make_float3(0.f, 0.f, 0.f);
     float4 p4 = make_float4(0.f, 0.f, 0.f, 0.f);
     if (live) {
-      p4 = *reinterpret_cast<const float4*>(row);
-      const float4 c48 = *reinterpret_cast<const float4*>(row + 48);  // .w = opacity (51)
-      const float4 c52 = *reinterpret_cast<const float4*>(row + 52);  // log-scales, q.w
-      const float4 c56 = *reinterpret_cast<const float4*>(row + 56);  // q.x, q.y, q.z, pad
+      p4 = ld_l2_64(row);
+      const float4 c48 = ld_l2_64(row + 48);  // .w = opacity (51)
+      const float4 c52 = ld_l2_64(row + 52);  // log-scales, q.w
+      const float4 c56 = ld_l2_64(row + 56);  // q.x, q.y, q.z, pad
       d = noise_delta3(make_float4(c52.w, c56.x, c56.y, c56.z), make_float3(c52.x, c52.y, c52.z),
                        c48.w, (uint32_t)i, (uint32_t)(i >> 32), iteration, key, coef, lambda_mu,
                        lambda_t);
