@@ -312,6 +312,9 @@ class ShardStepGraph:
         opt.engine.group_array(opt._bindings(step_kwargs.get("grads"),
                                              step_kwargs.get("mu_lr_scale", 1.0)))
         cap = torch.cuda.Stream(dev)
+        # the communicator must exist before capture (NCCL initialises lazily
+        # on the first collective, which cannot happen inside a graph)
+        dist.all_reduce(torch.zeros(1, dtype=torch.float64, device=dev), group=sh.group)
         sh.capture_begin()
         self.slot = sh._slot
         self.graph = torch.cuda.CUDAGraph()
