@@ -282,8 +282,9 @@ int gs_densify_rows(const float* grad, int64_t grad_stride, int32_t width, const
  * (the SH-3 row records with device-resident gradients on the 2-D TMA
  * kernel; not the dense coupled-adam mode, nor sparse-adam with a coupled
  * normaliser, which needs N_v before the step); *launched = 0 (status
- * GS_OK) asks the caller to compact and call gs_step_rows.  The statistics'
- * n_visible is the mask's visible count; results equal gs_compact +
+ * GS_OK) asks the caller to compact and call gs_step_rows.  sparse-adam with
+ * a coupled penalty runs here when cfg->n_visible_norm is given (e.g. by
+ * gs_count_visible).  The statistics' n_visible is the mask's visible count; results equal gs_compact +
  * gs_step_rows bit for bit (rows are independent).  flags:
  * GS_MASKED_LOW_VISIBILITY picks the kernel shape for sparse masks (a few %
  * visible; same results). */
@@ -301,6 +302,13 @@ int gs_step_rows_masked(const gs_group* groups, int32_t n_groups, const gs_step_
  * counter: 4 uint64 (host pointer), key: 2 uint64 (host pointer). */
 int gs_philox_bernoulli(const uint64_t* counter, const uint64_t* key, int64_t first, int64_t n,
                         double prob, uint8_t* out, void* stream);
+
+/* The visible count alone (the count pass of gs_compact_u8 / _i32, no
+ * index list): N_v = popcount(vis) (loss.py:190) for the coupled
+ * normaliser ahead of gs_step_rows_masked.  Exactly one of mask / radii;
+ * workspace as gs_compact. */
+int gs_count_visible(const uint8_t* mask, const int32_t* radii, int64_t n, int32_t* count_out,
+                     void* ws, size_t ws_bytes, void* stream);
 
 /* GS_BUILD_FLAG_* bits of this build. */
 int32_t gs_build_flags(void);

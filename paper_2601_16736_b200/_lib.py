@@ -106,6 +106,8 @@ SIGNATURES = {
                                   C.c_int64, C.c_void_p, C.c_void_p, C.c_float, C.c_void_p,
                                   C.c_void_p]),
     "gs_build_flags": (C.c_int32, []),
+    "gs_count_visible": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
+                                   C.c_size_t, C.c_void_p]),
     "gs_philox_bernoulli": (C.c_int, [C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.c_int64,
                                       C.c_int64, C.c_double, C.c_void_p, C.c_void_p]),
     "gs_step_rows_masked": (C.c_int, [C.POINTER(GsGroup), C.c_int32, C.POINTER(GsStepCfg),

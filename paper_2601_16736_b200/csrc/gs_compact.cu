@@ -214,8 +214,9 @@ __global__ void __launch_bounds__(kThreads)
 template <typename T>
 int compact_launch(const T* mask, int64_t n, int32_t* idx_out, int32_t* count_out, void* ws,
                    size_t ws_bytes, void* stream, const uint8_t* alive = nullptr,
-                   bool invert = false) {
-  if (n < 0 || (n > 0 && (!mask || !idx_out)) || !count_out || n >= (int64_t)INT32_MAX) {
+                   bool invert = false, bool write_pass = true) {
+  if (n < 0 || (n > 0 && (!mask || (write_pass && !idx_out))) || !count_out ||
+      n >= (int64_t)INT32_MAX) {
     gs_set_error("gs_compact: invalid arguments (n=%lld)", (long long)n);
     return GS_ERR_ARG;
   }
@@ -239,7 +240,7 @@ int compact_launch(const T* mask, int64_t n, int32_t* idx_out, int32_t* count_ou
   const int grid = (int)std::min<int64_t>(tiles, (int64_t)gs_sm_count() * 8);
   compact_count_kernel<T><<<grid, kThreads, 0, s>>>(mask, alive, invert, n, (int)tiles, counts,
                                                     counter, count_out, bitmap, vec_ok);
-  compact_write_kernel<<<(unsigned)tiles, kThreads, 0, s>>>(bitmap, counts, idx_out);
+  if (write_pass) compact_write_kernel<<<(unsigned)tiles, kThreads, 0, s>>>(bitmap, counts, idx_out);
   return gs_check_launch("gs_compact");
 }
 
@@ -267,4 +268,17 @@ extern "C" int gs_compact_select_u8(const uint8_t* mask, const uint8_t* alive, i
                                     size_t ws_bytes, void* stream) {
   return gs::compact_launch<uint8_t>(mask, n, idx_out, count_out, ws, ws_bytes, stream, alive,
                                      invert != 0);
+}
+
+extern "C" int gs_count_visible(const uint8_t* mask, const int32_t* radii, int64_t n,
+                                int32_t* count_out, void* ws, size_t ws_bytes, void* stream) {
+  if ((mask != nullptr) == (radii != nullptr)) {
+    gs_set_error("gs_count_visible: exactly one of mask / radii");
+    return GS_ERR_ARG;
+  }
+  if (radii)
+    return gs::compact_launch<int32_t>(radii, n, nullptr, count_out, ws, ws_bytes, stream,
+                                       nullptr, false, false);
+  return gs::compact_launch<uint8_t>(mask, n, nullptr, count_out, ws, ws_bytes, stream, nullptr,
+                                     false, false);
 }

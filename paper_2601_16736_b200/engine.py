@@ -308,6 +308,22 @@ class StepEngine:
         self.launches += 2 if self.n_rows > 0 else 0  # count + write passes
         return self.idx, self.count
 
+    def count_visible(self, vis: torch.Tensor) -> torch.Tensor:
+        """N_v on the device (K1's count pass only; no index list)."""
+        if vis.device != self.device or vis.dim() != 1 or vis.shape[0] != self.n_rows or \
+                not vis.is_contiguous() or vis.dtype not in (torch.bool, torch.uint8, torch.int32):
+            raise ConfigError("visibility must be a contiguous bool/uint8/int32 row vector")
+        is_radii = vis.dtype == torch.int32
+        _nvtx_push("gs.K1.count")
+        rc = self.lib.gs_count_visible(None if is_radii else vis.data_ptr(),
+                                       vis.data_ptr() if is_radii else None, self.n_rows,
+                                       self.count.data_ptr(), self.compact_ws.data_ptr(),
+                                       self.compact_ws.numel(), _stream_handle(self.device))
+        _nvtx_pop()
+        L.check(rc, "gs_count_visible")
+        self.launches += 1 if self.n_rows > 0 else 0
+        return self.count
+
     def compact_select(self, mask: torch.Tensor, alive: torch.Tensor | None = None,
                        invert: bool = False) -> tuple[torch.Tensor, torch.Tensor]:
         """Rows with mask != 0 (or == 0 when ``invert``), alive only; into a
@@ -490,8 +506,8 @@ class StepEngine:
                     lambda_opacity: float = 0.0, lambda_scale: float = 0.0,
                     clip_opacity: float = 10.0, clip_scale: float = 10.0,
                     n_pixels_rounded: float = 0.0, record: torch.Tensor,
-                    densify: tuple | None = None, low_visibility: bool = False
-                    ) -> torch.Tensor | None:
+                    densify: tuple | None = None, low_visibility: bool = False,
+                    n_visible_dev: torch.Tensor | None = None) -> torch.Tensor | None:
         """Fused K1 + K2 (gs_step_rows_masked): the step of the mask's visible
         rows with the compaction done inside the step kernel.  Returns the
         statistics, or None when the layout does not take this path (the
@@ -503,14 +519,15 @@ class StepEngine:
         self._check_record(record, groups)
         garr = self.group_array(groups)
         ckey = (mode, "fused", eps, float(lambda_opacity), float(lambda_scale),
-                float(clip_opacity), float(clip_scale), float(n_pixels_rounded), 0, None, 0.0,
+                float(clip_opacity), float(clip_scale), float(n_pixels_rounded), 0,
+                _ptr(n_visible_dev), 0.0,
                 None if densify is None else (densify[0].data_ptr(), densify[1].data_ptr(),
                                               float(densify[2]), int(densify[3])))
         if ckey == self._cfg_key:
             cfg = self._cfg
         else:
             cfg = self._build_cfg(mode, "fused", eps, lambda_opacity, lambda_scale, clip_opacity,
-                                  clip_scale, n_pixels_rounded, 0, None, 0.0, densify)
+                                  clip_scale, n_pixels_rounded, 0, n_visible_dev, 0.0, densify)
             self._cfg_key, self._cfg = ckey, cfg
         launched = self._launched
         is_radii = vis.dtype == torch.int32

@@ -413,7 +413,7 @@ class AdamWGS:
         else:
             if visibility is None:
                 raise ConfigError(f"{mode} needs the visibility mask")
-            stats = self._step_fused(b, mode, visibility, n_pixels, lo, ls, clip, kw)
+            stats = self._step_fused(b, mode, visibility, n_pixels, lo, ls, clip, kw, n_visible)
             if stats is not None:
                 self._last_ctx = (b, None, None, lo, ls, mode, visibility)
                 self._after_step(stats)
@@ -446,13 +446,30 @@ class AdamWGS:
         self._last_ctx = (b, rows, count, lo, ls, mode, visibility)
         self._after_step(stats)
 
-    def _step_fused(self, b, mode, visibility, n_pixels, lo, ls, clip, kw):
+    def _fused_eligible(self, vis: torch.Tensor) -> bool:
+        """Whether gs_step_rows_masked would take this mask (the checks the
+        library makes that the host can see: alignment and cloud size)."""
+        if vis.data_ptr() % 16 or not vis.is_contiguous():
+            return False
+        tile_rows = 256 if vis.dtype == torch.int32 else 1024
+        return -(-self.n_rows // tile_rows) >= 16 * 2 * L.load().gs_device_sm_count()
+
+    def _step_fused(self, b, mode, visibility, n_pixels, lo, ls, clip, kw, n_visible=None):
         """K1 fused into K2 (engine.step_masked) where it applies; None otherwise."""
         if not self.fused_compaction or self.check != "fused" or self.state.record is None:
             return None
-        if mode == "sparse-adam" and (lo != 0.0 or ls != 0.0):
-            return None  # the coupled normaliser needs N_v before the step
         eng = self.engine
+        nv = None
+        if mode == "sparse-adam" and (lo != 0.0 or ls != 0.0):
+            # the coupled normaliser N_v (loss.py:190) before the step: the
+            # count pass only (or the caller's / all ranks' count)
+            nv = n_visible
+            if nv is None:
+                if not self._fused_eligible(visibility):
+                    return None
+                nv = eng.count_visible(visibility)
+                if self._nv_reduce is not None:
+                    nv = self._nv_reduce(nv)
         # the last known step (the deferred statistics; no synchronisation)
         # steers the choice: index-coherent visible rows (long runs) keep the
         # global index order of K1 + K2, which streams DRAM better there
@@ -478,7 +495,8 @@ class AdamWGS:
             return eng.step_masked(b, m, visibility, lambda_opacity=self.lambda_o,
                                    lambda_scale=self.lambda_s, clip_opacity=cv, clip_scale=cv,
                                    **kwm)
-        return eng.step_masked(b, mode, visibility, **kwm)  # plain sparse Adam
+        return eng.step_masked(b, mode, visibility, lambda_opacity=lo, lambda_scale=ls,
+                               n_visible_dev=nv, **kwm)  # sparse Adam (+ coupled L1)
 
     # ---------------------------------------------------------------- errors
     def _after_step(self, stats: torch.Tensor):

@@ -362,10 +362,13 @@ def test_densify_adc_sh3_vs_oracle(params_layout):
 # K1 fused into K2 (gs_step_rows_masked)
 # --------------------------------------------------------------------------
 
-@pytest.mark.parametrize("n", [1, 2047, 2049, 100_003, 700_001])
-@pytest.mark.parametrize("kind", ["bool", "radii", "offset-bool", "offset-radii"])
-@pytest.mark.parametrize("mode", ["adamw-gs", "sparse-adam", "adamw-const"])
+@pytest.mark.parametrize("n,kind", [(n, k) for n in (1, 2047, 100_003, 1_300_001)
+                                    for k in ("bool", "radii", "offset-bool", "offset-radii")]
+                         + [(4_900_001, "bool")])
+@pytest.mark.parametrize("mode", ["adamw-gs", "sparse-adam", "sparse-coupled", "adamw-const"])
 def test_fused_compaction_equals_index_path(n, kind, mode):
+    if n > 2_000_000 and mode != "adamw-gs":
+        pytest.skip("the largest cloud runs in one mode (host-side data generation time)")
     """The one-launch step (the loader compacts the mask: uint8 or int32
     radii, aligned or not, ragged tails) equals K1 + K2 bit for bit:
     parameters, moment records, clocks, statistics (n_visible included)."""
@@ -377,8 +380,9 @@ def test_fused_compaction_equals_index_path(n, kind, mode):
     for fused in (True, False):
         _, params = R.pack({k: torch.from_numpy(v).to(DEV) for k, v in host.items()})
         lo, ls = (0.0, 0.0) if mode == "sparse-adam" else (1e-3, 1e-5)
-        opt = AdamWGS(S.param_groups(params), mode=mode, lambda_o=lo, lambda_s=ls,
-                      fused_compaction=fused)
+        # sparse-coupled: the coupled normaliser from the count pass, then the fused step
+        opt = AdamWGS(S.param_groups(params), mode="sparse-adam" if mode == "sparse-coupled"
+                      else mode, lambda_o=lo, lambda_s=ls, fused_compaction=fused)
         stats = []
         for s in range(3):
             vis = S.visibility(cfg, s)
@@ -395,10 +399,10 @@ def test_fused_compaction_equals_index_path(n, kind, mode):
             _, g = R.pack({k: torch.from_numpy(x).to(DEV) for k, x in S.step_grads(cfg, s, vis).items()})
             opt.step(m, cfg.n_pixels, grads=g)
             # K1 + K2 for unaligned masks (offset views: the fused loader
-            # streams 16-byte-aligned tiles) and for clouds under ~2 mask
+            # streams 16-byte-aligned tiles) and for clouds under 16 mask
             # tiles per CTA slot (1 KB tiles: 1024 uint8 rows, 256 radii)
             tiles = -(-n // (256 if "radii" in kind else 1024))
-            eligible = not kind.startswith("offset") and tiles >= 4 * torch.cuda.get_device_properties(
+            eligible = not kind.startswith("offset") and tiles >= 32 * torch.cuda.get_device_properties(
                 DEV).multi_processor_count
             assert (opt._last_ctx[1] is None) == (fused and eligible)
             stats.append(opt.last_stats())
