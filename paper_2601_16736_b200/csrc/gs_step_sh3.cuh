@@ -1958,6 +1958,7 @@ void launch_fixed(const FixedParams& P, const TmaMaps* M, int64_t max_rows, int 
       // on c3 (K2 0.532 ms, 0.86 of the copy peak; 2 stages 0.567 ms) and
       // on c5 at 100% visibility (0.94); profiles/r02/tma4_shape_sweep.txt.
       // GS_TMA4_SHAPE selects the measured alternatives (identical results).
+#if GS_BUILD_VARIANTS
       static const int shape = getenv("GS_TMA4_SHAPE") ? atoi(getenv("GS_TMA4_SHAPE")) : 0;
       switch (shape) {
         case 1: launch_tma4<L, MODE, STRICT, 2, 8, 2>(P, *M, max_rows, s); return;
@@ -1965,8 +1966,11 @@ void launch_fixed(const FixedParams& P, const TmaMaps* M, int64_t max_rows, int 
         case 3: launch_tma4<L, MODE, STRICT, 2, 8, 3>(P, *M, max_rows, s); return;
         case 4: launch_tma4<L, MODE, STRICT, 3, 6, 2>(P, *M, max_rows, s); return;
         case 5: launch_tma4<L, MODE, STRICT, 3, 10, 2>(P, *M, max_rows, s); return;
-        default: launch_tma4<L, MODE, STRICT, 3, 8, 2>(P, *M, max_rows, s); return;
+        default: break;
       }
+#endif
+      launch_tma4<L, MODE, STRICT, 3, 8, 2>(P, *M, max_rows, s);
+      return;
     }
     if (P.wide) {  // > 2^32 parameter-record elements: 64-bit row offsets
       launch_ring<L, MODE, STRICT, 32, 2, 3, 8, 2, true, true, 1 | 32>(P, max_rows, s);
@@ -1986,19 +1990,23 @@ void launch_fixed(const FixedParams& P, const TmaMaps* M, int64_t max_rows, int 
 // low_vis: the bias warp variant, for sparse masks where the loader's scan
 // is the bottleneck (c5 at 1%: 0.190 against 0.223 ms); on dense masks the
 // loader-staged bias factors win (c3: 0.534 against 0.580 ms)
-// (profiles/r02/fused_k1_bias_warp.txt).  GS_TMA4_BW=0/1 forces one.
+// (profiles/r02/fused_k1_variants.txt).  GS_TMA4_BW=0/1 forces one.
 template <class L, int MODE>
 void launch_fixed_masked(const FixedParams& P, const TmaMaps& M, int64_t n_rows, int mask_kind,
                          const void* mask, bool low_vis, cudaStream_t s) {
   static const int force = getenv("GS_TMA4_BW") ? atoi(getenv("GS_TMA4_BW")) : -1;
-  static const int mtb = getenv("GS_TMA4_MTB") ? atoi(getenv("GS_TMA4_MTB")) : 1024;
   const bool bw = force >= 0 ? force != 0 : low_vis;
+#if GS_BUILD_VARIANTS
+  static const int mtb = getenv("GS_TMA4_MTB") ? atoi(getenv("GS_TMA4_MTB")) : 1024;
+  if (mask_kind == 1 && mtb == 512) {
+    if (bw) launch_tma4<L, MODE, false, 3, 8, 2, 1, true, 512>(P, M, n_rows, s, mask);
+    else launch_tma4<L, MODE, false, 3, 8, 2, 1, false, 512>(P, M, n_rows, s, mask);
+    return;
+  }
+#endif
   if (mask_kind == 2) {
     if (bw) launch_tma4<L, MODE, false, 3, 8, 2, 2, true>(P, M, n_rows, s, mask);
     else launch_tma4<L, MODE, false, 3, 8, 2, 2, false>(P, M, n_rows, s, mask);
-  } else if (mtb == 512) {
-    if (bw) launch_tma4<L, MODE, false, 3, 8, 2, 1, true, 512>(P, M, n_rows, s, mask);
-    else launch_tma4<L, MODE, false, 3, 8, 2, 1, false, 512>(P, M, n_rows, s, mask);
   } else {
     if (bw) launch_tma4<L, MODE, false, 3, 8, 2, 1, true>(P, M, n_rows, s, mask);
     else launch_tma4<L, MODE, false, 3, 8, 2, 1, false>(P, M, n_rows, s, mask);
