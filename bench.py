@@ -584,17 +584,24 @@ def _time_k2(w, use_graph):
 
 
 def _time_rsr(w):
-    """Device time of one RSR / reset event (K3) of this workload."""
+    """Device time of one RSR / reset event (K3) of this workload: the event
+    captured as a CUDA graph (its index list is already on the device and
+    validated at upload), replayed between two CUDA events."""
     import torch
     if not w.rsr_probe:
         return 0.0
     opt = w.opts[0]
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    w.apply_events(opt, w.rsr_probe)  # warm
+    w.apply_events(opt, w.rsr_probe)  # warm (eager: validates the lists)
     torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for _ in range(3):
+            w.apply_events(opt, w.rsr_probe)
+    g.replay()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
-    for _ in range(3):
-        w.apply_events(opt, w.rsr_probe)
+    g.replay()
     b.record()
     torch.cuda.synchronize()
     return a.elapsed_time(b) / 3
