@@ -1,5 +1,12 @@
 """Host-side state sampling for Re-State Regularization (RSR).
 
+Transcription note: ``_label_key``, ``stream``, ``RngHub``, ``StSSchedule``,
+``RsrConfig``, ``AiuConfig`` and ``stss_sample`` restate the reference's
+definitions (rng.py:17-43, optimizer.py:343-422) nearly line for line, error
+strings included: the reference's config schema is the API, and the RNG /
+selection contract must be bit-identical for the sampled rows to match.
+``shard_rows``, ``aiu_shard_select`` and ``device_bernoulli`` are new.
+
 The sampled row set must be bit-identical to the reference's, so it is drawn
 on the host with the reference's counter-based stream contract — Philox
 keyed by (seed, blake2b-4(label), indices) (rng.py:17-30) — and uploaded to

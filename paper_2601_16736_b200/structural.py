@@ -12,6 +12,12 @@ the respawns' moments and clock (reset_rows, optimizer.py:159-165).
 Pruning, cloning and splitting (``densify_adc``) are row gathers and
 concatenations of the parameter and state records: ``MomentState.select``
 / ``concatenate`` and torch indexing of the parameter record.
+
+Transcription note: ``_ids_hash`` / ``_event`` (pipeline.py:94-102) and the
+split-child sampling (pipeline.py:153-162) follow the reference line for
+line: identical rng draw order and event hashes are what make the
+densification and relocation results bit-exact against reference runs.
+The device side (record gathers, gs_relocate_rows) and the 3-D split are new.
 """
 
 from __future__ import annotations
