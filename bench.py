@@ -82,8 +82,10 @@ def parse():
     ap.add_argument("--workload", default="c3", choices=sorted(WORKLOADS))
     ap.add_argument("--mask", default="bernoulli", choices=["bernoulli", "coherent"])
     ap.add_argument("--vis", type=float, default=None, help="override visibility fraction")
-    ap.add_argument("--n", type=int, default=None, help="override rows per GPU")
-    ap.add_argument("--strong", action="store_true", help="split --n across ranks (strong)")
+    ap.add_argument("--rows", type=int, default=None,
+                    help="override rows per GPU (not --n: torchrun would claim it as an "
+                    "abbreviation of its own --nnodes/--nproc-per-node)")
+    ap.add_argument("--strong", action="store_true", help="split --rows across ranks (strong)")
     ap.add_argument("--check", default="fused", choices=["fused", "strict"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -909,8 +911,8 @@ def main():
         print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
         sys.exit(2)
     wl = dict(WORKLOADS[args.workload], name=args.workload)
-    if args.n is not None:
-        wl["n"] = args.n
+    if args.rows is not None:
+        wl["n"] = args.rows
     p_vis = args.vis if args.vis is not None else wl["p"]
     if args.impl == "reference":
         reference_arm(args, wl, p_vis)

@@ -14,7 +14,7 @@ import pytest
 
 pytestmark = pytest.mark.gpu
 ROOT = Path(__file__).resolve().parent.parent
-ARGS = ["--steps", "3", "--warmup", "3", "--no-cpu", "--no-legs", "--n", "300000",
+ARGS = ["--steps", "3", "--warmup", "3", "--no-cpu", "--no-legs", "--rows", "300000",
         "--e2e-steps", "3"]
 
 
