@@ -367,7 +367,10 @@ def l2_replicas(n, p_vis):
     touched = max(1.0, n * p_vis * (28 * 59 + 12))
     if touched >= 4 * L2_BYTES:
         return 1
-    return 1 + math.ceil(4 * L2_BYTES / touched)
+    # at most 64 clouds and ~32 GB of them (a cloud holds ~1.1 KB per row):
+    # near-empty masks touch so little that L2 residency no longer matters
+    cap = max(1, min(64, int(32e9 // (1100 * max(n, 1)))))
+    return min(cap, 1 + math.ceil(4 * L2_BYTES / touched))
 
 
 # --------------------------------------------------------------- our arm

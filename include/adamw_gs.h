@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define GS_ABI_VERSION 3
+#define GS_ABI_VERSION 4
 #define GS_MAX_GROUPS 8
 
 /* gs_build_flags() bits */
@@ -246,6 +246,10 @@ int gs_noise_perturb(float* position, const float* log_scale, const float* rotat
  * log_scale, rotation, opacity_logit (0 = dense), for record views. */
 
 size_t gs_step_rows_workspace_bytes(void);
+/* Workspace of gs_step_rows_masked that enables the two-phase kernel for a
+ * mask of n_rows rows (the base workspace + per-CTA counts + an n_rows
+ * int32 id list).  No reference counterpart (device workspace). */
+size_t gs_step_rows_masked_workspace_bytes(int64_t n_rows);
 /* Select the (rows-in-flight, residency) variant of the SH-3 step kernel
  * (0 = default; tuning only, results are identical).  Returns the previous
  * variant.  The GS_ROWS_VARIANT environment variable sets the initial one. */
@@ -280,14 +284,20 @@ int gs_densify_rows(const float* grad, int64_t grad_stride, int32_t width, const
  * (uint8 mask != 0, or int32 radii > 0; exactly one of the two) without a
  * separate compaction pass or index list.  *launched = 1 if this layout ran
  * (the SH-3 row records with device-resident gradients on the 2-D TMA
- * kernel; not the dense coupled-adam mode, nor sparse-adam with a coupled
- * normaliser, which needs N_v before the step); *launched = 0 (status
- * GS_OK) asks the caller to compact and call gs_step_rows.  sparse-adam with
- * a coupled penalty runs here when cfg->n_visible_norm is given (e.g. by
- * gs_count_visible).  The statistics' n_visible is the mask's visible count; results equal gs_compact +
- * gs_step_rows bit for bit (rows are independent).  flags:
- * GS_MASKED_LOW_VISIBILITY picks the kernel shape for sparse masks (a few %
- * visible; same results). */
+ * kernel; not the dense coupled-adam mode); *launched = 0 (status GS_OK)
+ * asks the caller to compact and call gs_step_rows.  Two kernels serve it:
+ * large clouds stream the mask through the step kernel's loader; with a
+ * workspace of gs_step_rows_masked_workspace_bytes(n_rows) bytes (16-byte
+ * aligned) smaller clouds run the two-phase kernel (the mask compacted into
+ * the workspace, a grid barrier, even shares of the visible rows per CTA),
+ * which also serves sparse-adam with a coupled penalty on its own visible
+ * count.  With the base workspace (gs_step_rows_workspace_bytes) small
+ * clouds are declined, and a coupled sparse-adam step needs
+ * cfg->n_visible_norm (e.g. from gs_count_visible; the sharded global count
+ * always comes this way).  The statistics' n_visible is the mask's visible
+ * count; results equal gs_compact + gs_step_rows bit for bit (rows are
+ * independent).  flags: GS_MASKED_LOW_VISIBILITY picks the kernel shape for
+ * sparse masks (a few % visible; same results). */
 #define GS_MASKED_LOW_VISIBILITY 1
 int gs_step_rows_masked(const gs_group* groups, int32_t n_groups, const gs_step_cfg* cfg,
                         const uint8_t* mask, const int32_t* radii, int64_t n_rows, float* record,

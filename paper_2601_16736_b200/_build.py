@@ -58,7 +58,10 @@ def build(force: bool = False, verbose: bool = False) -> Path:
 
     def compile_one(src: str) -> str:
         obj = build_dir / (Path(src).stem + ".o")
-        cmd = [nvcc, *NVCC_FLAGS, "-I", str(ROOT / "include"), "-c", str(CSRC / src), "-o", str(obj)]
+        # GS_NVCC_EXTRA: measurement builds only (e.g. -DGS_TRACE=1, -DGS_BUILD_VARIANTS=1)
+        extra = os.environ.get("GS_NVCC_EXTRA", "").split()
+        cmd = [nvcc, *NVCC_FLAGS, *extra, "-I", str(ROOT / "include"), "-c", str(CSRC / src), "-o",
+               str(obj)]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if verbose or res.returncode != 0:
             sys.stderr.write(res.stdout + res.stderr)

@@ -13,7 +13,7 @@ from pathlib import Path
 
 LIB_PATH = Path(__file__).resolve().parent / "libadamw_gs_b200.so"
 
-GS_ABI_VERSION = 3
+GS_ABI_VERSION = 4
 GS_MAX_GROUPS = 8
 GS_MASKED_LOW_VISIBILITY = 1
 
@@ -93,6 +93,7 @@ SIGNATURES = {
                                    C.c_float, C.c_uint64, C.c_uint32, C.c_void_p, C.c_int32,
                                    C.c_void_p, C.c_void_p]),
     "gs_step_rows_workspace_bytes": (C.c_size_t, []),
+    "gs_step_rows_masked_workspace_bytes": (C.c_size_t, [C.c_int64]),
     "gs_set_rows_variant": (C.c_int32, [C.c_int32]),
     "gs_set_fixed_variant": (C.c_int32, [C.c_int32]),
     "gs_step_rows": (C.c_int, [C.POINTER(GsGroup), C.c_int32, C.POINTER(GsStepCfg), C.c_void_p,

@@ -36,6 +36,12 @@ int gs_sm_count() {
 }
 
 extern "C" int32_t gs_abi_version(void) { return GS_ABI_VERSION; }
+#ifdef GS_TRACE
+// measurement builds only: 16 uint64 per CTA of the next step launches
+extern "C" void gs_debug_set_trace(void* buf) {
+  gs::trace_buf() = static_cast<unsigned long long*>(buf);
+}
+#endif
 extern "C" const char* gs_last_error(void) { return g_err; }
 extern "C" int32_t gs_device_sm_count(void) { return gs_sm_count(); }
 

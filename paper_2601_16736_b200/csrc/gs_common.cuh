@@ -187,18 +187,59 @@ __device__ __forceinline__ void block_reduce_n(double (&v)[NV], const bool (&is_
 
 // Last-block-done finalisation: every CTA writes its partials, the last one
 // to arrive reduces them in CTA order (deterministic) and re-arms the counter.
-// Returns true in thread 0 of the last CTA.
+// Returns true in every thread of the last CTA.  Thread 0's increment is
+// acquire-release at GPU scope: it releases the CTA's writes (ordered before
+// it by the barrier) and, in the last CTA, acquires every other CTA's; the
+// second barrier extends that to the CTA's other threads.  (Two
+// __threadfence()s around a relaxed atomicInc cost ~0.4 us more per launch,
+// scripts/launch_probe.cu.)
 __device__ __forceinline__ bool last_block_arrive(unsigned int* counter) {
   __shared__ bool s_last;
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
-    unsigned int prev = atomicInc(counter, gridDim.x - 1);  // wraps to 0 on the last
+    unsigned int prev;  // wraps to 0 on the last arrival
+    asm volatile("atom.acq_rel.gpu.global.inc.u32 %0, [%1], %2;\n"
+                 : "=r"(prev)
+                 : "l"(counter), "r"(gridDim.x - 1)
+                 : "memory");
     s_last = (prev == gridDim.x - 1);
   }
   __syncthreads();
-  if (s_last) __threadfence();
   return s_last;
+}
+
+// Grid-wide barrier for kernels whose CTAs are all resident (the two-phase
+// step kernel, launched with at most one wave of CTAs): bar[0] counts
+// arrivals, bar[1] is the generation.  Thread 0 reads the generation, then
+// arrives (acquire-release); the last arrival re-arms the count and releases
+// the next generation, the others spin on it.  Both words start at any
+// generation with bar[0] == 0 (zeroed workspace) and stay re-armed between
+// launches.  A barrier that never opens (a CTA that cannot become resident)
+// traps after ~seconds instead of hanging the device.
+__device__ __forceinline__ void grid_barrier(unsigned int* bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned int gen, old;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(gen) : "l"(bar + 1) : "memory");
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;\n"
+                 : "=r"(old)
+                 : "l"(bar)
+                 : "memory");
+    if (old == gridDim.x - 1) {
+      asm volatile("st.relaxed.gpu.global.u32 [%0], 0;\n" ::"l"(bar) : "memory");
+      asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(bar + 1), "r"(gen + 1u)
+                   : "memory");
+    } else {
+      unsigned int cur;
+      long long spins = 0;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(cur) : "l"(bar + 1) : "memory");
+        if (++spins > (1ll << 26)) __trap();
+        if (spins > 64) __nanosleep(64);
+      } while (cur == gen);
+    }
+  }
+  __syncthreads();
 }
 
 // Densification statistics of one row from its position-group gradient
@@ -290,6 +331,35 @@ int gs_check_launch(const char* what);
 int gs_sm_count();
 
 namespace gs {
+// Measurement builds only (-DGS_TRACE=1): a device buffer of per-CTA
+// globaltimer stamps the step kernel writes (gs_debug_set_trace); the
+// product build passes nullptr and compiles no stamps.
+inline unsigned long long*& trace_buf() {
+  static unsigned long long* p = nullptr;
+  return p;
+}
+#ifdef GS_TRACE
+#define GS_STAMP(buf, slot)                                                   \
+  do {                                                                        \
+    if (buf) {                                                                \
+      unsigned long long t_;                                                  \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                  \
+      (buf)[(size_t)blockIdx.x * 16 + (slot)] = t_;                           \
+    }                                                                         \
+  } while (0)
+#define GS_TRACE_VAL(buf, slot, v) \
+  do {                             \
+    if (buf) (buf)[(size_t)blockIdx.x * 16 + (slot)] = (v); \
+  } while (0)
+#else
+#define GS_STAMP(buf, slot) \
+  do {                      \
+  } while (0)
+#define GS_TRACE_VAL(buf, slot, v) \
+  do {                             \
+  } while (0)
+#endif
+
 // Opt KERNEL into `bytes` of dynamic shared memory on the current device.
 // cudaFuncSetAttribute is per device, so the opt-in is cached per kernel in
 // a bitmask of devices (thread-safe); a failure is reported and retried on

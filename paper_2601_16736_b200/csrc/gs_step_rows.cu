@@ -36,8 +36,8 @@ int gs_step_fixed_try(const gs_group* groups, int32_t n_groups, const gs_step_cf
 int gs_step_fixed_masked_try(const gs_group* groups, int32_t n_groups, const gs_step_cfg* cfg,
                              const uint8_t* mask, const int32_t* radii, int64_t n_rows,
                              float* record, int64_t record_stride, double* stats_out,
-                             double* partials, unsigned int* counter, int32_t flags,
-                             void* stream);
+                             double* partials, unsigned int* counter, unsigned int* tp_bar,
+                             int32_t* tp_counts, int32_t* tp_ids, int32_t flags, void* stream);
 
 namespace gs {
 
@@ -279,8 +279,9 @@ __global__ void __launch_bounds__(kRowThreads, MINB)
 }
 
 struct RowStepWorkspace {
-  unsigned int counter;
-  unsigned int pad[15];
+  unsigned int counter;  // last-block-done counter of the statistics
+  unsigned int bar[2];   // grid barrier of the two-phase fused kernel
+  unsigned int pad[13];
 };
 
 int max_row_blocks() { return gs_sm_count() * kRowMaxBlocksPerSM; }
@@ -355,6 +356,14 @@ extern "C" int32_t gs_set_rows_variant(int32_t variant) {
 extern "C" size_t gs_step_rows_workspace_bytes(void) {
   return sizeof(gs::RowStepWorkspace) +
          (size_t)gs::max_row_blocks() * GS_STEP_STATS * sizeof(double);
+}
+
+// gs_step_rows_masked with the two-phase compaction: the base workspace, then
+// the per-CTA counts and an n_rows id list (16-byte aligned pieces).
+extern "C" size_t gs_step_rows_masked_workspace_bytes(int64_t n_rows) {
+  const size_t counts = ((size_t)gs::max_row_blocks() * sizeof(int32_t) + 15) & ~(size_t)15;
+  return ((gs_step_rows_workspace_bytes() + 15) & ~(size_t)15) + counts +
+         (((size_t)(n_rows > 0 ? n_rows : 0) * sizeof(int32_t) + 15) & ~(size_t)15);
 }
 
 extern "C" int gs_step_rows(const gs_group* groups, int32_t n_groups, const gs_step_cfg* cfg,
@@ -504,8 +513,20 @@ extern "C" int gs_step_rows_masked(const gs_group* groups, int32_t n_groups,
   auto* hdr = reinterpret_cast<RowStepWorkspace*>(ws);
   double* partials =
       reinterpret_cast<double*>(reinterpret_cast<char*>(ws) + sizeof(RowStepWorkspace));
+  // the two-phase compaction needs its counts and id list in the workspace
+  int32_t* tp_counts = nullptr;
+  int32_t* tp_ids = nullptr;
+  if (ws_bytes >= gs_step_rows_masked_workspace_bytes(n_rows) &&
+      (reinterpret_cast<uintptr_t>(ws) & 15u) == 0) {
+    char* base = reinterpret_cast<char*>(ws) + gs_step_rows_workspace_bytes();
+    base += (16 - (reinterpret_cast<uintptr_t>(base) & 15u)) & 15u;
+    tp_counts = reinterpret_cast<int32_t*>(base);
+    tp_ids = reinterpret_cast<int32_t*>(
+        base + (((size_t)max_row_blocks() * sizeof(int32_t) + 15) & ~(size_t)15));
+  }
   if (!gs_step_fixed_masked_try(groups, n_groups, cfg, mask, radii, n_rows, record, record_stride,
-                                stats_out, partials, &hdr->counter, flags, stream))
+                                stats_out, partials, &hdr->counter, hdr->bar, tp_counts, tp_ids,
+                                flags, stream))
     return GS_OK;  // not this layout: the caller compacts and calls gs_step_rows
   *launched = 1;
   return gs_check_launch("gs_step_rows_masked");

@@ -251,20 +251,29 @@ constexpr int kFusedMinTilesPerSlot = 16;
 int gs_step_fixed_masked_try(const gs_group* groups, int32_t n_groups, const gs_step_cfg* cfg,
                              const uint8_t* mask, const int32_t* radii, int64_t n_rows,
                              float* record, int64_t record_stride, double* stats_out,
-                             double* partials, unsigned int* counter, int32_t flags,
-                             void* stream) {
+                             double* partials, unsigned int* counter, unsigned int* tp_bar,
+                             int32_t* tp_counts, int32_t* tp_ids, int32_t flags, void* stream) {
   using namespace gs;
   if (cfg->check != GS_CHECK_FUSED || cfg->mode == GS_MODE_COUPLED_ADAM) return 0;
-  // the coupled normaliser N_v must be on the device before the step
-  if (cfg->mode == GS_MODE_SPARSE_ADAM && (cfg->lambda_opacity != 0.0 || cfg->lambda_scale != 0.0) &&
-      cfg->n_visible_norm == nullptr)
-    return 0;
   if (fixed_variant() == 21 || n_rows < 1) return 0;
+  // GS_FUSED_MODE (measurement): 1 = the streaming loader, 2 = two-phase
+  static const int fm = getenv("GS_FUSED_MODE") ? atoi(getenv("GS_FUSED_MODE")) : 0;
+  const bool tp_ok = tp_ids != nullptr && tp_counts != nullptr;
   // the fused grid deals whole 1-KB mask tiles to the CTAs; under ~16 tiles
   // per CTA slot the last round leaves SMs idle (c2, 1M rows: 3.3 tiles per
   // CTA, 0.119 ms against 0.108 ms for K1 + K2, whose chunks spread evenly)
   const int64_t tile_rows = radii ? 256 : 1024;
-  if ((n_rows + tile_rows - 1) / tile_rows < kFusedMinTilesPerSlot * 2 * (int64_t)gs_sm_count())
+  const bool small =
+      (n_rows + tile_rows - 1) / tile_rows < kFusedMinTilesPerSlot * 2 * (int64_t)gs_sm_count();
+  bool two;
+  if (fm == 2) two = tp_ok;
+  else if (fm == 1) two = false;
+  else two = tp_ok && small;
+  if (!two && fm != 1 && small) return 0;
+  // the coupled normaliser N_v must be on the device before the step (the
+  // two-phase kernel counts the mask itself)
+  if (!two && cfg->mode == GS_MODE_SPARSE_ADAM &&
+      (cfg->lambda_opacity != 0.0 || cfg->lambda_scale != 0.0) && cfg->n_visible_norm == nullptr)
     return 0;
   // the loader streams 2-KB mask tiles with 16-byte bulk copies
   if ((reinterpret_cast<uintptr_t>(radii ? static_cast<const void*>(radii)
@@ -279,7 +288,12 @@ int gs_step_fixed_masked_try(const gs_group* groups, int32_t n_groups, const gs_
     return 0;
   TmaMaps maps;
   if (!encode_tma_maps(P, n_rows, 2 * (LayoutSH3::P + 1), &maps)) return 0;
-  const int mk = radii ? 2 : 1;
+  const int mk = (radii ? 2 : 1) + (two ? 2 : 0);
+  if (two) {
+    P.tp_ids = tp_ids;
+    P.tp_counts = tp_counts;
+    P.tp_bar = tp_bar;
+  }
   const bool low = (flags & GS_MASKED_LOW_VISIBILITY) != 0;
   const void* m = radii ? static_cast<const void*>(radii) : static_cast<const void*>(mask);
   cudaStream_t s = (cudaStream_t)stream;

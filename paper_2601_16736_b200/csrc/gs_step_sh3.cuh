@@ -89,6 +89,11 @@ struct FixedParams {
   double* stats_out;
   double* partials;
   unsigned int* counter;
+  // two-phase fused compaction (step_tma4_kernel MASK 3 / 4): the visible
+  // ids of every CTA's mask range, the per-CTA counts and the grid barrier
+  int32_t* tp_ids;
+  int32_t* tp_counts;
+  unsigned int* tp_bar;
 };
 
 constexpr int kFixedThreads = 256;
@@ -1969,7 +1974,16 @@ void launch_fixed(const FixedParams& P, const TmaMaps* M, int64_t max_rows, int 
         default: break;
       }
 #endif
-      launch_tma4<L, MODE, STRICT, 3, 8, 2>(P, *M, max_rows, s);
+      // short lists (under 16 chunks per CTA slot whatever the count): the
+      // bias warp, so the loader's per-chunk work is only the TMA issue
+      // (c1 K2 0.0258 against 0.0277 ms; c3 0.566 against 0.544 ms,
+      // profiles/r02/small_clouds.txt).  GS_TMA4_BW=0/1 forces one.
+      static const int force = getenv("GS_TMA4_BW") ? atoi(getenv("GS_TMA4_BW")) : -1;
+      const bool bw = force >= 0 ? force != 0
+                                 : (max_rows + 31) / 32 < (int64_t)kBalancedChunksPerCta * 2 *
+                                                              gs_sm_count();
+      if (bw) launch_tma4<L, MODE, STRICT, 3, 8, 2, 0, true>(P, *M, max_rows, s);
+      else launch_tma4<L, MODE, STRICT, 3, 8, 2>(P, *M, max_rows, s);
       return;
     }
     if (P.wide) {  // > 2^32 parameter-record elements: 64-bit row offsets
@@ -1986,7 +2000,10 @@ void launch_fixed(const FixedParams& P, const TmaMaps* M, int64_t max_rows, int 
 }
 
 // Fused K1 + K2 on records (the fused check): the TMA kernel's loader
-// compacts the visibility mask itself (mask_kind 1: uint8, 2: int32 radii).
+// compacts the visibility mask itself (mask_kind 1: uint8, 2: int32 radii;
+// 3 / 4: the same, two-phase compaction with balanced shares, for clouds
+// under 16 mask tiles per CTA slot: c1 step 0.0316 against 0.0345 ms for
+// K1 + K2, c2 0.105 against 0.111; ties from 400k rows to 3M).
 // low_vis: the bias warp variant, for sparse masks where the loader's scan
 // is the bottleneck (c5 at 1%: 0.190 against 0.223 ms); on dense masks the
 // loader-staged bias factors win (c3: 0.534 against 0.580 ms)
@@ -2004,6 +2021,16 @@ void launch_fixed_masked(const FixedParams& P, const TmaMaps& M, int64_t n_rows,
     return;
   }
 #endif
+  if (mask_kind >= 3) {  // two-phase: the bias warp (c3-sized: 0.563 against 0.652 ms)
+    if (force == 0) {
+      if (mask_kind == 4) launch_tma4<L, MODE, false, 3, 8, 2, 4, false>(P, M, n_rows, s, mask);
+      else launch_tma4<L, MODE, false, 3, 8, 2, 3, false>(P, M, n_rows, s, mask);
+    } else {
+      if (mask_kind == 4) launch_tma4<L, MODE, false, 3, 8, 2, 4, true>(P, M, n_rows, s, mask);
+      else launch_tma4<L, MODE, false, 3, 8, 2, 3, true>(P, M, n_rows, s, mask);
+    }
+    return;
+  }
   if (mask_kind == 2) {
     if (bw) launch_tma4<L, MODE, false, 3, 8, 2, 2, true>(P, M, n_rows, s, mask);
     else launch_tma4<L, MODE, false, 3, 8, 2, 2, false>(P, M, n_rows, s, mask);

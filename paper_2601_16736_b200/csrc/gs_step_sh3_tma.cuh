@@ -83,15 +83,47 @@ __device__ __forceinline__ void tma_scatter4(const CUtensorMap* map, const void*
 
 // MASK: 0 = the compacted index list (P.rows, *P.n_rows_dev rows; dense
 // mode: every row), 1 = a uint8 visibility mask, 2 = int32 radii (> 0 is
-// visible): the loader compacts the mask itself (fused K1, below).
+// visible): the loader compacts the mask itself (fused K1, below);
+// 3 / 4 = the same masks compacted in two phases (below): every CTA first
+// compacts an even slice of the mask into P.tp_ids, a grid barrier
+// publishes the per-CTA counts, then every CTA steps an even contiguous
+// share of the visible rows (one wave of CTAs, all resident).
 // BW: a fourth role, the bias warp (warp NCW+2), turns the staged clocks
 // into bias factors after the gathers land, so the loader's per-chunk work
 // is only the TMA issue (the mask-scanning loader); without it the loader
 // reads each row's clock and LUT entry itself.
+// Index lists shorter than this many chunks per CTA deal whole rounds of G
+// chunks grid-stride and split the last, partial round evenly over the CTAs.
+constexpr int kBalancedChunksPerCta = 16;
+
+// A list of n positions over G CTAs: spans k < full of CTA b are the chunks
+// (k * G + b) * 32 .. + 32; the last span is the CTA's even share of the
+// remaining n - 32 * G * full positions (< 32 each, possibly empty).
+struct TailSplit {
+  int full;  // whole rounds of G chunks
+  int n;
+  __device__ int n_spans() const { return full + 1; }
+  __device__ void span(int k, int b, int G, int& lo, int& hi) const {
+    if (k < full) {
+      lo = (k * G + b) * 32;
+      hi = lo + 32;
+    } else if (k == full) {
+      const int base = full * G * 32;
+      const int64_t rem = n - base;
+      lo = base + (int)(rem * b / G);
+      hi = base + (int)(rem * (b + 1) / G);
+    } else {
+      lo = hi = 0;
+    }
+  }
+};
+__device__ __forceinline__ TailSplit tail_split(int n, int G) { return TailSplit{n / (32 * G), n}; }
+
 template <class L, int MODE, bool STRICT, int S, int NCW, int MINB, int MASK, bool BW = false,
           int MTB = 1024>
 __global__ void __launch_bounds__((NCW + 2 + (BW ? 1 : 0)) * 32, MINB)
-    step_tma4_kernel(const FixedParams P, const __grid_constant__ TmaMaps M, const void* vis_mask) {
+    step_tma4_kernel(const FixedParams P, const __grid_constant__ TmaMaps M, const void* vis_mask,
+                     unsigned long long* trc) {
   constexpr int NWARPS = NCW + 2 + (BW ? 1 : 0);
   constexpr int R = 32;
   constexpr bool kDense = MODE == GS_MODE_COUPLED_ADAM;
@@ -112,18 +144,24 @@ __global__ void __launch_bounds__((NCW + 2 + (BW ? 1 : 0)) * 32, MINB)
   __shared__ float2 s_bc[S][R];
   __shared__ uint32_t s_crow[S][R];
   __shared__ int s_nv[S];  // rows of the chunk in the stage; -1 ends the CTA's chunk stream
-  constexpr int kPend = MASK != 0 ? 2048 : 1;  // pending visible ids (fused compaction)
+  constexpr bool kStreamMask = MASK == 1 || MASK == 2;
+  constexpr int kPend = kStreamMask ? 2048 : 1;  // pending visible ids (fused compaction)
   __shared__ uint32_t s_pend[kPend];
-  constexpr int kMaskRing = MASK != 0 ? 6 * 1024 / MTB : 1;  // 6 KB of mask tiles in flight
-  __shared__ __align__(128) unsigned char s_mask[kMaskRing][MASK != 0 ? MTB : 16];
+  constexpr int kMaskRing = kStreamMask ? 6 * 1024 / MTB : 1;  // 6 KB of mask tiles in flight
+  __shared__ __align__(128) unsigned char s_mask[kMaskRing][kStreamMask ? MTB : 16];
   __shared__ __align__(8) uint64_t mask_bar[kMaskRing];
   __shared__ double s_red[GS_STEP_STATS * NWARPS];
+  constexpr bool kTwoPhase = MASK >= 3;
+  constexpr int kNT = NWARPS * 32;
+  __shared__ int s_pref[kTwoPhase ? kNT + 1 : 1];  // exclusive prefix of the CTA counts
+  __shared__ int s_wsum[kTwoPhase ? NWARPS : 1];
   // TMA boxes land 128-byte aligned (the host adds 128 bytes of slack)
   unsigned char* const smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~static_cast<uintptr_t>(127));
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) GS_STAMP(trc, 0);
   int n_rows = (kDense || MASK != 0) ? (int)P.max_rows : *P.n_rows_dev;
   if (STRICT && *P.abort_flag != 0) n_rows = 0;
   const int n_chunks = (n_rows + R - 1) / R;
@@ -151,6 +189,92 @@ __global__ void __launch_bounds__((NCW + 2 + (BW ? 1 : 0)) * 32, MINB)
   if (tid < S) s_any[tid] = 0;
   asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   __syncthreads();
+
+  int tp_total = 0;  // two-phase: the mask's visible count
+  if constexpr (kTwoPhase) {
+    // ---- phase A (every thread): compact granules [g0, g1) of the mask
+    // (16 bytes each: 16 uint8 rows or 4 radii) into P.tp_ids from row
+    // g0 * Q on, in ascending row order, one block-wide scan per pass
+    constexpr int kEsz = MASK == 3 ? 1 : 4;
+    constexpr int Q = 16 / kEsz;
+    const int64_t nr = n_rows;
+    const int64_t ng = (nr + Q - 1) / Q;
+    const int64_t g0 = ng * blockIdx.x / G, g1 = ng * (blockIdx.x + 1) / G;
+    const unsigned char* gm = reinterpret_cast<const unsigned char*>(vis_mask);
+    int run = 0;
+    for (int64_t gb = g0; gb < g1; gb += kNT) {
+      const int64_t g = gb + tid;
+      uint32_t bits = 0;
+      if (g < g1) {
+        uint32_t w[4] = {0u, 0u, 0u, 0u};
+        if ((g + 1) * Q <= nr) {
+          const uint4 v = __ldg(reinterpret_cast<const uint4*>(gm) + g);
+          w[0] = v.x, w[1] = v.y, w[2] = v.z, w[3] = v.w;
+        } else {  // ragged end of the mask: element reads, zero past the rows
+          for (int by = 0; by < 16; ++by)
+            if (g * 16 + by < nr * kEsz) w[by >> 2] |= (uint32_t)gm[g * 16 + by] << (8 * (by & 3));
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if constexpr (MASK == 3) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) bits |= (((w[j] >> (8 * e)) & 0xffu) != 0u) << (4 * j + e);
+          } else {
+            bits |= (uint32_t)((int)w[j] > 0) << j;
+          }
+        }
+      }
+      const int cnt = __popc(bits);
+      int incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      if (lane == 31) s_wsum[warp] = incl;
+      __syncthreads();
+      int wpre = 0, tot = 0;
+#pragma unroll
+      for (int w2 = 0; w2 < NWARPS; ++w2) {
+        const int x = s_wsum[w2];
+        wpre += w2 < warp ? x : 0;
+        tot += x;
+      }
+      int pos = run + wpre + incl - cnt;
+      int32_t* dst = P.tp_ids + g0 * Q;
+      for (uint32_t x = bits; x; x &= x - 1) dst[pos++] = (int32_t)(g * Q + __ffs(x) - 1);
+      run += tot;
+      __syncthreads();  // s_wsum is rewritten by the next pass
+    }
+    if (tid == 0) {
+      P.tp_counts[blockIdx.x] = run;
+      GS_STAMP(trc, 12);
+    }
+    grid_barrier(P.tp_bar);
+    if (tid == 0) GS_STAMP(trc, 13);
+    // ---- phase B: exclusive prefix of the G counts (G <= kNT), this CTA's
+    // even share [p0, p1) of the visible positions
+    const int cnt = tid < G ? __ldcg(P.tp_counts + tid) : 0;
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) s_wsum[warp] = incl;
+    __syncthreads();
+    int wpre = 0, tot = 0;
+#pragma unroll
+    for (int w2 = 0; w2 < NWARPS; ++w2) {
+      const int x = s_wsum[w2];
+      wpre += w2 < warp ? x : 0;
+      tot += x;
+    }
+    if (tid < G) s_pref[tid] = wpre + incl - cnt;
+    if (tid == 0) s_pref[G] = tot;
+    __syncthreads();
+    tp_total = tot;
+  }
 
   unsigned c_vis = 0, c_step = 0, c_badg = 0, c_badd = 0, c_apre = 0, c_apost = 0, c_clo = 0,
            c_cls = 0, c_runs = 0;
@@ -207,6 +331,7 @@ __global__ void __launch_bounds__((NCW + 2 + (BW ? 1 : 0)) * 32, MINB)
       } else {
         mbar_arrive(&full_bar[st]);
       }
+      if (k == 0 && lane == 0) GS_STAMP(trc, 1);
       ++k;
       if (++st == S) {
         st = 0;
@@ -214,16 +339,70 @@ __global__ void __launch_bounds__((NCW + 2 + (BW ? 1 : 0)) * 32, MINB)
       }
     };
     if constexpr (MASK == 0) {
-      auto fetch_id = [&](int c) -> int {
-        if (c >= n_chunks || lane >= chunk_rows(c)) return oob;
-        const int i = c * R + lane;
-        return kDense ? i : __ldg(P.rows + i);
+      if (n_chunks < kBalancedChunksPerCta * G) {
+        // few chunks per CTA: whole rounds of G chunks grid-stride (the
+        // CTAs stay on one window of the list: DRAM locality), then the
+        // last partial round split evenly, so the CTAs finish together
+        // (grid-stride alone leaves a chunk of imbalance: 5 vs 6 at c1)
+        const TailSplit ts = tail_split(n_rows, G);
+        auto fetch = [&](int k) -> int {
+          int b, e;
+          ts.span(k, (int)blockIdx.x, G, b, e);
+          const int i = b + lane;
+          return i < e ? (kDense ? i : __ldg(P.rows + i)) : oob;
+        };
+        int next_id = fetch(0);
+        for (int k = 0; k < ts.n_spans(); ++k) {
+          const int my_id = next_id;
+          int b, e;
+          ts.span(k, (int)blockIdx.x, G, b, e);
+          next_id = fetch(k + 1);
+          if (e > b) emit(my_id, e - b);
+        }
+      } else {
+        auto fetch_id = [&](int c) -> int {
+          if (c >= n_chunks || lane >= chunk_rows(c)) return oob;
+          const int i = c * R + lane;
+          return kDense ? i : __ldg(P.rows + i);
+        };
+        int next_id = fetch_id((int)blockIdx.x);
+        for (int c = (int)blockIdx.x; c < n_chunks; c += G) {
+          const int my_id = next_id;
+          next_id = fetch_id(c + G);
+          emit(my_id, chunk_rows(c));
+        }
+      }
+    } else if constexpr (kTwoPhase) {
+      // two-phase: positions [p0, p1) of the visible list; position p lives
+      // in the slice of CTA c = max{c : pref[c] <= p} at row offset
+      // g0(c) * Q, index p - pref[c]
+      // positions dealt like the short index lists above: whole rounds of
+      // G chunks grid-stride, the last round split evenly
+      constexpr int Q = MASK == 3 ? 16 : 4;
+      const int64_t ng = ((int64_t)n_rows + Q - 1) / Q;
+      const TailSplit ts = tail_split(tp_total, G);
+      int owner = 0;  // positions only grow: search from the last owner
+      auto fetch = [&](int k) -> int {
+        int b, e;
+        ts.span(k, (int)blockIdx.x, G, b, e);
+        const int p = b + lane;
+        if (p >= e) return oob;
+        int lo = owner, hi = G - 1;
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (s_pref[mid] <= p) lo = mid;
+          else hi = mid - 1;
+        }
+        owner = lo;
+        return __ldcg(P.tp_ids + ng * owner / G * Q + (p - s_pref[owner]));
       };
-      int next_id = fetch_id((int)blockIdx.x);
-      for (int c = (int)blockIdx.x; c < n_chunks; c += G) {
+      int next_id = fetch(0);
+      for (int k = 0; k < ts.n_spans(); ++k) {
         const int my_id = next_id;
-        next_id = fetch_id(c + G);
-        emit(my_id, chunk_rows(c));
+        int b, e;
+        ts.span(k, (int)blockIdx.x, G, b, e);
+        next_id = fetch(k + 1);
+        if (e > b) emit(my_id, e - b);
       }
     } else {
       // fused compaction: the CTA takes 1-KB mask tiles grid-stride (1024
@@ -338,6 +517,7 @@ __global__ void __launch_bounds__((NCW + 2 + (BW ? 1 : 0)) * 32, MINB)
                             tail - head);
     }
     emit(oob, -1);
+    if (lane == 0) GS_STAMP(trc, 2);
   } else if (BW && warp == NCW + 2) {
     // ------------------------------------------------------------ bias warp
     int st = 0;
@@ -386,13 +566,18 @@ __global__ void __launch_bounds__((NCW + 2 + (BW ? 1 : 0)) * 32, MINB)
         ph ^= 1u;
       }
     }
-    bulk_wait0();  // global writes complete before the CTA retires
+    // every bulk store has read its stage (per-chunk wait above); the writes
+    // themselves complete with the kernel, so the CTA does not wait for them
+    if (lane == 0) GS_STAMP(trc, 5);
   } else {
     // ---------------------------------------------------------------- consumers
     const int t = tid;
     StepConsts Kc = P.K;
     if (kCoupled) {
-      const float nv = P.nv_dev ? (float)(*P.nv_dev) : (float)P.nv_host;
+      // the coupled normaliser N_v: given (sharded: the global count), or
+      // the two-phase total of this mask
+      const float nv = P.nv_dev ? (float)(*P.nv_dev)
+                                : kTwoPhase ? (float)s_pref[G] : (float)P.nv_host;
       Kc.inv_nv = nv != 0.0f ? __frcp_rn(nv) : 0.0f;
       if (nv == 0.0f) Kc.lam_op = Kc.lam_sc = 0.0f;
     }
@@ -404,8 +589,10 @@ __global__ void __launch_bounds__((NCW + 2 + (BW ? 1 : 0)) * 32, MINB)
       // (full barrier, the bias warp) are awaited only after the check pass
       mbar_wait(BW ? &data_bar[st] : &full_bar[st], (unsigned)((ep - 1) & 1));
       const int nvalid = s_nv[st];
+      if (tid == 0 && ep == 1 && st == 0) GS_STAMP(trc, 3);
       if (nvalid < 0) {
         mbar_arrive(&done_bar[st]);  // the storer reads the end marker too
+        if (tid == 0) GS_STAMP(trc, 4);
         break;
       }
       unsigned char* sb = stage(st);
@@ -542,13 +729,32 @@ __global__ void __launch_bounds__((NCW + 2 + (BW ? 1 : 0)) * 32, MINB)
                                       false, false, false, false, false};
   block_reduce_n<GS_STEP_STATS, NWARPS>(acc, is_max, s_red);
   if (threadIdx.x == 0) {
+    GS_STAMP(trc, 6);
+    GS_TRACE_VAL(trc, 9, (unsigned long long)acc[0]);
 #pragma unroll
     for (int f = 0; f < GS_STEP_STATS; ++f)
       P.partials[(size_t)blockIdx.x * GS_STEP_STATS + f] = acc[f];
   }
-  if (last_block_arrive(P.counter))
+  if (last_block_arrive(P.counter)) {
+    if (threadIdx.x == 0) GS_STAMP(trc, 7);
     final_reduce_n<GS_STEP_STATS, NWARPS>(P.partials, gridDim.x, GS_STEP_STATS, P.stats_out,
                                              is_max, s_red);
+    if (threadIdx.x == 0) GS_STAMP(trc, 8);
+  }
+#ifdef GS_TRACE
+  if (threadIdx.x == 0 && trc) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    GS_TRACE_VAL(trc, 10, (unsigned long long)smid);
+    GS_STAMP(trc, 11);
+  }
+#endif
+}
+
+// Largest grid of the two-phase kernel: one CTA count per thread of a CTA.
+template <int NCW, bool BW>
+constexpr int tma4_two_phase_max_grid() {
+  return (NCW + 2 + (BW ? 1 : 0)) * 32;
 }
 
 // Host: tensor maps of the three records (cuTensorMapEncodeTiled through the
@@ -560,13 +766,42 @@ template <class L, int MODE, bool STRICT, int S, int NCW, int MINB, int MASK = 0
 void launch_tma4(const FixedParams& P, const TmaMaps& M, int64_t max_rows, cudaStream_t s,
                  const void* vis_mask = nullptr) {
   constexpr int bytes = S * Tma4Stage<L, 32>::kBytes + 128;
-  smem_opt_in<step_tma4_kernel<L, MODE, STRICT, S, NCW, MINB, MASK, BW, MTB>>(bytes);
+  constexpr auto kern = step_tma4_kernel<L, MODE, STRICT, S, NCW, MINB, MASK, BW, MTB>;
+  smem_opt_in<kern>(bytes);
+  if constexpr (MASK >= 3) {
+    // two-phase: one wave of CTAs (the grid barrier needs every CTA
+    // resident), at least 256 mask rows each, launched cooperatively
+    static int resident = -1;
+    if (resident < 0) {
+      int per_sm = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (NCW + 2 + (BW ? 1 : 0)) * 32,
+                                                        bytes) != cudaSuccess)
+        per_sm = 0;
+      resident = per_sm * gs_sm_count();
+    }
+    const int64_t want = (max_rows + 255) / 256;
+    const int grid = (int)std::max<int64_t>(
+        1, std::min<int64_t>({want, (int64_t)gs_sm_count() * MINB, (int64_t)resident,
+                              (int64_t)tma4_two_phase_max_grid<NCW, BW>()}));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3((NCW + 2 + (BW ? 1 : 0)) * 32);
+    cfg.dynamicSmemBytes = bytes;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, P, M, vis_mask, trace_buf());
+    return;
+  }
   const int64_t tile = MASK == 1 ? MTB : MASK == 2 ? MTB / 4 : 32;
   const int64_t work = (max_rows + tile - 1) / tile;
   const int grid =
       (int)std::max<int64_t>(1, std::min<int64_t>(work, (int64_t)gs_sm_count() * MINB));
   step_tma4_kernel<L, MODE, STRICT, S, NCW, MINB, MASK, BW, MTB>
-      <<<grid, (NCW + 2 + (BW ? 1 : 0)) * 32, bytes, s>>>(P, M, vis_mask);
+      <<<grid, (NCW + 2 + (BW ? 1 : 0)) * 32, bytes, s>>>(P, M, vis_mask, trace_buf());
 }
 
 }  // namespace gs

@@ -194,7 +194,8 @@ class StepEngine:
                                           dtype=torch.uint8, device=dev)
             self.step_ws = torch.zeros(int(self.lib.gs_step_workspace_bytes()), dtype=torch.uint8,
                                        device=dev)
-            self.rows_ws = torch.zeros(int(self.lib.gs_step_rows_workspace_bytes()),
+            # the base step workspace + the two-phase fused kernel's counts and id list
+            self.rows_ws = torch.zeros(int(self.lib.gs_step_rows_masked_workspace_bytes(n)),
                                        dtype=torch.uint8, device=dev)
             self.stats = torch.zeros(L.GS_STEP_STATS, dtype=torch.float64, device=dev)
             self.abort = torch.zeros(1, dtype=torch.int32, device=dev)

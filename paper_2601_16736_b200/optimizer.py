@@ -447,12 +447,15 @@ class AdamWGS:
         self._after_step(stats)
 
     def _fused_eligible(self, vis: torch.Tensor) -> bool:
-        """Whether gs_step_rows_masked would take this mask (the checks the
-        library makes that the host can see: alignment and cloud size)."""
-        if vis.data_ptr() % 16 or not vis.is_contiguous():
-            return False
+        """Whether gs_step_rows_masked would take this mask (the check the
+        library makes that the host can see: 16-byte alignment)."""
+        return vis.data_ptr() % 16 == 0 and vis.is_contiguous()
+
+    def _fused_two_phase(self, vis: torch.Tensor) -> bool:
+        """Whether the library runs the two-phase fused kernel for this mask:
+        clouds under 16 one-KB mask tiles per CTA slot (gs_step_sh3.cu)."""
         tile_rows = 256 if vis.dtype == torch.int32 else 1024
-        return -(-self.n_rows // tile_rows) >= 16 * 2 * L.load().gs_device_sm_count()
+        return -(-self.n_rows // tile_rows) < 16 * 2 * L.load().gs_device_sm_count()
 
     def _step_fused(self, b, mode, visibility, n_pixels, lo, ls, clip, kw, n_visible=None):
         """K1 fused into K2 (engine.step_masked) where it applies; None otherwise."""
@@ -460,13 +463,15 @@ class AdamWGS:
             return None
         eng = self.engine
         nv = None
+        if not self._fused_eligible(visibility):
+            return None
+        two_phase = self._fused_two_phase(visibility)
         if mode == "sparse-adam" and (lo != 0.0 or ls != 0.0):
             # the coupled normaliser N_v (loss.py:190) before the step: the
-            # count pass only (or the caller's / all ranks' count)
+            # caller's / all ranks' count, or the count pass; the two-phase
+            # kernel counts the mask itself
             nv = n_visible
-            if nv is None:
-                if not self._fused_eligible(visibility):
-                    return None
+            if nv is None and (self._nv_reduce is not None or not two_phase):
                 nv = eng.count_visible(visibility)
                 if self._nv_reduce is not None:
                     nv = self._nv_reduce(nv)
@@ -474,8 +479,9 @@ class AdamWGS:
         # steers the choice: index-coherent visible rows (long runs) keep the
         # global index order of K1 + K2, which streams DRAM better there
         # (c3, 64-row blocks: 0.52 against 0.58 ms); sparse masks take the
-        # fused kernel's bias-warp shape (c5 at 1%: 0.19 against 0.22 ms)
-        if self._vis_run is not None and self._vis_run >= 4.0:
+        # fused kernel's bias-warp shape (c5 at 1%: 0.19 against 0.22 ms).
+        # The two-phase kernel keeps ascending rows per CTA.
+        if not two_phase and self._vis_run is not None and self._vis_run >= 4.0:
             return None
         low = self._vis_frac is not None and self._vis_frac < 0.05
         kwm = dict(eps=self.eps, record=self.state.record, densify=kw.get("densify"),

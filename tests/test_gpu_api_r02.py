@@ -398,12 +398,12 @@ def test_fused_compaction_equals_index_path(n, kind, mode):
                 m = m.to(DEV)
             _, g = R.pack({k: torch.from_numpy(x).to(DEV) for k, x in S.step_grads(cfg, s, vis).items()})
             opt.step(m, cfg.n_pixels, grads=g)
-            # K1 + K2 for unaligned masks (offset views: the fused loader
-            # streams 16-byte-aligned tiles) and for clouds under 16 mask
-            # tiles per CTA slot (1 KB tiles: 1024 uint8 rows, 256 radii)
-            tiles = -(-n // (256 if "radii" in kind else 1024))
-            eligible = not kind.startswith("offset") and tiles >= 32 * torch.cuda.get_device_properties(
-                DEV).multi_processor_count
+            # K1 + K2 for unaligned masks (offset views: both fused kernels
+            # read the mask in 16-byte pieces); clouds under 16 mask tiles per
+            # CTA slot (1 KB tiles: 1024 uint8 rows, 256 radii) run the
+            # two-phase kernel, larger ones the streaming loader; a one-row
+            # cloud has no row stride to describe records by (index path)
+            eligible = not kind.startswith("offset") and n > 1
             assert (opt._last_ctx[1] is None) == (fused and eligible)
             stats.append(opt.last_stats())
         opt.check_errors()
@@ -421,6 +421,60 @@ def test_fused_compaction_equals_index_path(n, kind, mode):
                 assert x[f] == pytest.approx(y[f], rel=1e-12, abs=0), f
             else:
                 assert x[f] == y[f], f
+
+
+@pytest.mark.parametrize("pattern", ["empty", "all", "last-row", "first-tile", "burst", "every-17th"])
+@pytest.mark.parametrize("n,kind", [(4_099, "bool"), (300_017, "bool"), (300_017, "radii"),
+                                    (77, "radii")])
+def test_two_phase_fused_edge_masks(pattern, n, kind):
+    """The two-phase fused kernel (clouds under 16 mask tiles per CTA slot)
+    on degenerate masks: nothing visible, everything, one row at the ragged
+    end, one dense tile, one dense burst inside one CTA's mask slice (its
+    ids are served to every CTA), a regular stride; equals K1 + K2 bit for
+    bit, over two steps (the grid barrier re-arms), and counts the mask's
+    N_v itself for a coupled sparse-adam step."""
+    from paper_2601_16736_b200 import records as R
+    from paper_2601_16736_b200 import synthetic as S
+    from paper_2601_16736_b200.optimizer import AdamWGS
+    cfg, host = _cloud(n, seed=n + 11)
+    vis = np.zeros(n, bool)
+    if pattern == "all":
+        vis[:] = True
+    elif pattern == "last-row":
+        vis[-1] = True
+    elif pattern == "first-tile":
+        vis[:1024] = True
+    elif pattern == "burst":
+        vis[n // 3:n // 3 + min(n // 10 + 1, 40_000)] = True
+    elif pattern == "every-17th":
+        vis[::17] = True
+    outs = []
+    for fused in (True, False):
+        for mode in ("adamw-gs", "sparse-coupled"):
+            _, params = R.pack({k: torch.from_numpy(v).to(DEV) for k, v in host.items()})
+            opt = AdamWGS(S.param_groups(params), mode="sparse-adam" if mode != "adamw-gs" else mode,
+                          lambda_o=1e-3, lambda_s=1e-5, fused_compaction=fused)
+            stats = []
+            for s in range(2):
+                m = (torch.from_numpy(np.where(vis, np.arange(n) % 5 + 1, 0).astype(np.int32))
+                     if kind == "radii" else torch.from_numpy(vis)).to(DEV)
+                _, g = R.pack({k: torch.from_numpy(x).to(DEV)
+                               for k, x in S.step_grads(cfg, s, vis).items()})
+                opt.step(m, cfg.n_pixels, grads=g)
+                assert (opt._last_ctx[1] is None) == fused
+                stats.append(opt.last_stats())
+            opt.check_errors()
+            outs.append(({k: p.cpu().numpy() for k, p in params.items()},
+                         opt.state.record.cpu().numpy(), stats))
+    for (pa, ra, sa), (pb, rb, sb) in zip(outs[:2], outs[2:]):
+        for k in pa:
+            assert np.array_equal(pa[k], pb[k]), k
+        assert np.array_equal(ra.view(np.int32), rb.view(np.int32))
+        for x, y in zip(sa, sb):
+            assert x["n_visible"] == y["n_visible"] == int(vis.sum())
+            for f in x:
+                if f != "n_runs" and not f.startswith("sum_"):
+                    assert x[f] == y[f], f
 
 
 # --------------------------------------------------------------------------
