@@ -288,17 +288,21 @@ int gs_densify_rows(const float* grad, int64_t grad_stride, int32_t width, const
  * asks the caller to compact and call gs_step_rows.  Two kernels serve it:
  * large clouds stream the mask through the step kernel's loader; with a
  * workspace of gs_step_rows_masked_workspace_bytes(n_rows) bytes (16-byte
- * aligned) smaller clouds run the two-phase kernel (the mask compacted into
- * the workspace, a grid barrier, even shares of the visible rows per CTA),
- * which also serves sparse-adam with a coupled penalty on its own visible
- * count.  With the base workspace (gs_step_rows_workspace_bytes) small
- * clouds are declined, and a coupled sparse-adam step needs
- * cfg->n_visible_norm (e.g. from gs_count_visible; the sharded global count
- * always comes this way).  The statistics' n_visible is the mask's visible
- * count; results equal gs_compact + gs_step_rows bit for bit (rows are
- * independent).  flags: GS_MASKED_LOW_VISIBILITY picks the kernel shape for
- * sparse masks (a few % visible; same results). */
+ * aligned), smaller clouds with index-coherent masks (GS_MASKED_COHERENT)
+ * or a coupled sparse-adam step without cfg->n_visible_norm run the
+ * two-phase kernel (the mask compacted into the workspace, a grid barrier,
+ * even shares of the visible rows per CTA; it counts N_v itself).
+ * Otherwise a coupled sparse-adam step needs cfg->n_visible_norm (e.g. from
+ * gs_count_visible; the sharded global count always comes this way).  The
+ * statistics' n_visible is the mask's visible count; results equal
+ * gs_compact + gs_step_rows bit for bit (rows are independent).  flags:
+ * GS_MASKED_LOW_VISIBILITY picks the kernel shape for sparse masks (a few %
+ * visible), GS_MASKED_COHERENT the two-phase kernel for small clouds (same
+ * results either way). */
 #define GS_MASKED_LOW_VISIBILITY 1
+/* flags: the mask's visible rows come in long index runs (e.g. the last
+ * step's GS_STAT_N_RUNS hint); small clouds then balance them (two-phase). */
+#define GS_MASKED_COHERENT 2
 int gs_step_rows_masked(const gs_group* groups, int32_t n_groups, const gs_step_cfg* cfg,
                         const uint8_t* mask, const int32_t* radii, int64_t n_rows, float* record,
                         int64_t record_stride, double* stats_out, void* ws, size_t ws_bytes,

@@ -16,6 +16,7 @@ LIB_PATH = Path(__file__).resolve().parent / "libadamw_gs_b200.so"
 GS_ABI_VERSION = 4
 GS_MAX_GROUPS = 8
 GS_MASKED_LOW_VISIBILITY = 1
+GS_MASKED_COHERENT = 2
 
 GS_OK = 0
 

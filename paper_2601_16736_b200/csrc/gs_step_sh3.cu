@@ -259,22 +259,25 @@ int gs_step_fixed_masked_try(const gs_group* groups, int32_t n_groups, const gs_
   // GS_FUSED_MODE (measurement): 1 = the streaming loader, 2 = two-phase
   static const int fm = getenv("GS_FUSED_MODE") ? atoi(getenv("GS_FUSED_MODE")) : 0;
   const bool tp_ok = tp_ids != nullptr && tp_counts != nullptr;
-  // the fused grid deals whole 1-KB mask tiles to the CTAs; under ~16 tiles
-  // per CTA slot the last round leaves SMs idle (c2, 1M rows: 3.3 tiles per
-  // CTA, 0.119 ms against 0.108 ms for K1 + K2, whose chunks spread evenly)
+  // small clouds (under 16 one-KB mask tiles per CTA slot): the streaming
+  // loader gives every CTA its own mask slice (dealt whole tiles, a few
+  // tiles would idle most SMs); index-coherent masks (the caller's
+  // GS_MASKED_COHERENT hint) pile their visible rows into a few slices, and
+  // the coupled normaliser needs N_v first: both take the two-phase kernel,
+  // which balances the visible rows and counts them
+  // (profiles/r02/small_clouds.txt)
   const int64_t tile_rows = radii ? 256 : 1024;
   const bool small =
       (n_rows + tile_rows - 1) / tile_rows < kFusedMinTilesPerSlot * 2 * (int64_t)gs_sm_count();
+  const bool coupled_nv = cfg->mode == GS_MODE_SPARSE_ADAM &&
+                          (cfg->lambda_opacity != 0.0 || cfg->lambda_scale != 0.0) &&
+                          cfg->n_visible_norm == nullptr;
   bool two;
   if (fm == 2) two = tp_ok;
   else if (fm == 1) two = false;
-  else two = tp_ok && small;
-  if (!two && fm != 1 && small) return 0;
-  // the coupled normaliser N_v must be on the device before the step (the
-  // two-phase kernel counts the mask itself)
-  if (!two && cfg->mode == GS_MODE_SPARSE_ADAM &&
-      (cfg->lambda_opacity != 0.0 || cfg->lambda_scale != 0.0) && cfg->n_visible_norm == nullptr)
-    return 0;
+  else two = tp_ok && small && ((flags & GS_MASKED_COHERENT) != 0 || coupled_nv);
+  // the streaming kernels need N_v on the device before the step
+  if (!two && coupled_nv) return 0;
   // the loader streams 2-KB mask tiles with 16-byte bulk copies
   if ((reinterpret_cast<uintptr_t>(radii ? static_cast<const void*>(radii)
                                          : static_cast<const void*>(mask)) & 15u) != 0)

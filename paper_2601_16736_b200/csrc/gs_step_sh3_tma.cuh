@@ -406,7 +406,8 @@ __global__ void __launch_bounds__((NCW + 2 + (BW ? 1 : 0)) * 32, MINB)
       }
     } else {
       // fused compaction: the CTA takes 1-KB mask tiles grid-stride (1024
-      // uint8 rows or 256 int32 radii); lane 0 streams them into a
+      // uint8 rows or 256 int32 radii; small masks: tiles of its own slice,
+      // below); lane 0 streams them into a
       // kMaskRing-deep shared-memory ring with 1-D bulk copies (mbarrier tx
       // counts); each lane takes 32 consecutive uint8 rows (two 16-byte
       // reads) or 16 radii, one warp scan per tile packs the
@@ -422,22 +423,42 @@ __global__ void __launch_bounds__((NCW + 2 + (BW ? 1 : 0)) * 32, MINB)
       const int64_t nr = n_rows;
       const int n_tiles = (int)((nr + kRowsPerTile - 1) / kRowsPerTile);
       const unsigned char* gmask = reinterpret_cast<const unsigned char*>(vis_mask);
-      // bytes of tile t that arrive by bulk copy (16-byte multiple); rows past
-      // them (the ragged end of the last tile) are read from global memory
-      auto bulk_bytes = [&](int t) -> int {
-        const int64_t rows = nr - (int64_t)t * kRowsPerTile;
-        const int64_t b = (rows < kRowsPerTile ? rows : kRowsPerTile) * kEsz;
-        return (int)(b & ~(int64_t)15);
+      // small masks (under kBalancedChunksPerCta tiles per CTA): every CTA
+      // scans its own contiguous 16-byte-aligned slice of the rows, in 1-KB
+      // tiles (dealt grid-stride, a few tiles would leave most CTAs idle)
+      constexpr int64_t kAlign = 16 / kEsz;  // rows per 16 mask bytes
+      const bool range_mode = n_tiles < kBalancedChunksPerCta * G;
+      int64_t r_lo = 0, r_hi = nr;
+      if (range_mode) {
+        const int64_t na = (nr + kAlign - 1) / kAlign;
+        r_lo = na * blockIdx.x / G * kAlign;
+        r_hi = na * (blockIdx.x + 1) / G * kAlign;
+        r_hi = r_hi < nr ? r_hi : nr;
+      }
+      auto tile_start = [&](int k2) -> int64_t {
+        return range_mode ? r_lo + (int64_t)k2 * kRowsPerTile
+                          : ((int64_t)blockIdx.x + (int64_t)k2 * G) * kRowsPerTile;
       };
+      auto tile_end = [&](int64_t st) -> int64_t {
+        return st + kRowsPerTile < r_hi ? st + kRowsPerTile : r_hi;
+      };
+      // bytes of the tile that arrive by bulk copy (16-byte multiple); rows
+      // past them (the ragged end of the mask) are read from global memory
+      auto bulk_bytes = [&](int64_t st) -> int {
+        return (int)(((tile_end(st) - st) * kEsz) & ~(int64_t)15);
+      };
+      const int my_tiles =
+          range_mode ? (r_hi > r_lo ? (int)((r_hi - r_lo + kRowsPerTile - 1) / kRowsPerTile) : 0)
+                     : ((int)blockIdx.x < n_tiles ? (n_tiles - 1 - (int)blockIdx.x) / G + 1 : 0);
       auto issue = [&](int k2) {  // tile number k2 of this CTA into slot k2 % kMaskRing
-        const int t = (int)blockIdx.x + k2 * G;
-        if (t >= n_tiles) return;
+        if (k2 >= my_tiles) return;
         const int slot = k2 % kMaskRing;
-        const int b = bulk_bytes(t);
+        const int64_t st = tile_start(k2);
+        const int b = bulk_bytes(st);
         if (lane == 0) {
           if (b > 0) {
             mbar_arrive_expect_tx(&mask_bar[slot], (uint32_t)b);
-            bulk_g2s(s_mask[slot], gmask + (int64_t)t * kTileBytes, (uint32_t)b, &mask_bar[slot]);
+            bulk_g2s(s_mask[slot], gmask + st * kEsz, (uint32_t)b, &mask_bar[slot]);
           } else {
             mbar_arrive(&mask_bar[slot]);
           }
@@ -454,14 +475,14 @@ __global__ void __launch_bounds__((NCW + 2 + (BW ? 1 : 0)) * 32, MINB)
         return MASK == 1 ? lane * kLane + k : (lane & (MTB / 64 - 1)) * 16 + k;
       };
       int head = 0, tail = 0;  // ring of pending ids: s_pend[head .. tail)
-      const int my_tiles = (int)blockIdx.x < n_tiles ? (n_tiles - 1 - (int)blockIdx.x) / G + 1 : 0;
 #pragma unroll
       for (int k2 = 0; k2 < kMaskRing; ++k2) issue(k2);
       for (int k2 = 0; k2 < my_tiles; ++k2) {
-        const int t = (int)blockIdx.x + k2 * G;
+        const int64_t st = tile_start(k2);
         const int slot = k2 % kMaskRing;
         mbar_wait(&mask_bar[slot], (unsigned)((k2 / kMaskRing) & 1));
-        const int bb = bulk_bytes(t);
+        const int bb = bulk_bytes(st);
+        const int64_t gend = tile_end(st) * kEsz;  // the tile's last mask byte + 1
         uint32_t bits = 0;
         if (MASK == 1 || lane < MTB / 64) {
 #pragma unroll
@@ -472,11 +493,11 @@ __global__ void __launch_bounds__((NCW + 2 + (BW ? 1 : 0)) * 32, MINB)
               v = *reinterpret_cast<const uint4*>(s_mask[slot] + off);
             } else {  // ragged end: global element reads (zero past the rows)
               uint32_t w[4] = {0u, 0u, 0u, 0u};
-              const int64_t g0 = (int64_t)t * kTileBytes + off;
+              const int64_t g0 = st * kEsz + off;
 #pragma unroll
               for (int by = 0; by < 16; ++by) {
                 const int64_t gb = g0 + by;
-                if (gb < nr * kEsz) w[by >> 2] |= (uint32_t)gmask[gb] << (8 * (by & 3));
+                if (gb < gend) w[by >> 2] |= (uint32_t)gmask[gb] << (8 * (by & 3));
               }
               v = make_uint4(w[0], w[1], w[2], w[3]);
             }
@@ -502,7 +523,7 @@ __global__ void __launch_bounds__((NCW + 2 + (BW ? 1 : 0)) * 32, MINB)
         }
         const int total = __shfl_sync(0xffffffffu, incl, 31);
         int pos = tail + incl - cnt;
-        const int row0 = t * kRowsPerTile;
+        const int row0 = (int)st;
         for (uint32_t x = bits; x; x &= x - 1)
           s_pend[(pos++) & (kPend - 1)] = row0 + row_of_bit(__ffs(x) - 1);
         tail += total;
@@ -797,7 +818,11 @@ void launch_tma4(const FixedParams& P, const TmaMaps& M, int64_t max_rows, cudaS
     return;
   }
   const int64_t tile = MASK == 1 ? MTB : MASK == 2 ? MTB / 4 : 32;
-  const int64_t work = (max_rows + tile - 1) / tile;
+  int64_t work = (max_rows + tile - 1) / tile;
+  // streamed masks under kBalancedChunksPerCta tiles per CTA slot: the
+  // kernel gives every CTA a contiguous slice (>= 256 rows each)
+  if ((MASK == 1 || MASK == 2) && work < (int64_t)kBalancedChunksPerCta * gs_sm_count() * MINB)
+    work = (max_rows + 255) / 256;
   const int grid =
       (int)std::max<int64_t>(1, std::min<int64_t>(work, (int64_t)gs_sm_count() * MINB));
   step_tma4_kernel<L, MODE, STRICT, S, NCW, MINB, MASK, BW, MTB>

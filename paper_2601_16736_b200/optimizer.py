@@ -451,9 +451,10 @@ class AdamWGS:
         library makes that the host can see: 16-byte alignment)."""
         return vis.data_ptr() % 16 == 0 and vis.is_contiguous()
 
-    def _fused_two_phase(self, vis: torch.Tensor) -> bool:
-        """Whether the library runs the two-phase fused kernel for this mask:
-        clouds under 16 one-KB mask tiles per CTA slot (gs_step_sh3.cu)."""
+    def _fused_small(self, vis: torch.Tensor) -> bool:
+        """Clouds under 16 one-KB mask tiles per CTA slot (gs_step_sh3.cu):
+        the library balances coherent masks there and counts a coupled
+        sparse-adam step's N_v itself (the two-phase kernel)."""
         tile_rows = 256 if vis.dtype == torch.int32 else 1024
         return -(-self.n_rows // tile_rows) < 16 * 2 * L.load().gs_device_sm_count()
 
@@ -465,27 +466,29 @@ class AdamWGS:
         nv = None
         if not self._fused_eligible(visibility):
             return None
-        two_phase = self._fused_two_phase(visibility)
+        small = self._fused_small(visibility)
         if mode == "sparse-adam" and (lo != 0.0 or ls != 0.0):
             # the coupled normaliser N_v (loss.py:190) before the step: the
-            # caller's / all ranks' count, or the count pass; the two-phase
-            # kernel counts the mask itself
+            # caller's / all ranks' count, or the count pass; on small clouds
+            # the two-phase kernel counts the mask itself
             nv = n_visible
-            if nv is None and (self._nv_reduce is not None or not two_phase):
+            if nv is None and (self._nv_reduce is not None or not small):
                 nv = eng.count_visible(visibility)
                 if self._nv_reduce is not None:
                     nv = self._nv_reduce(nv)
         # the last known step (the deferred statistics; no synchronisation)
         # steers the choice: index-coherent visible rows (long runs) keep the
-        # global index order of K1 + K2, which streams DRAM better there
-        # (c3, 64-row blocks: 0.52 against 0.58 ms); sparse masks take the
-        # fused kernel's bias-warp shape (c5 at 1%: 0.19 against 0.22 ms).
-        # The two-phase kernel keeps ascending rows per CTA.
-        if not two_phase and self._vis_run is not None and self._vis_run >= 4.0:
+        # global index order of K1 + K2 on big clouds, which streams DRAM
+        # better there (c3, 64-row blocks: 0.52 against 0.58 ms), and take
+        # the balanced two-phase kernel on small ones (c1: 0.032 against
+        # 0.039 ms streaming); sparse masks take the fused kernel's
+        # bias-warp shape (c5 at 1%: 0.19 against 0.22 ms)
+        coherent = self._vis_run is not None and self._vis_run >= 4.0
+        if coherent and not small:
             return None
         low = self._vis_frac is not None and self._vis_frac < 0.05
         kwm = dict(eps=self.eps, record=self.state.record, densify=kw.get("densify"),
-                   low_visibility=low)
+                   low_visibility=low, coherent=coherent)
         if mode == "adamw-gs":
             if n_pixels is None:
                 raise ConfigError("adamw-gs needs n_pixels (N_I)")

@@ -426,13 +426,15 @@ def test_fused_compaction_equals_index_path(n, kind, mode):
 @pytest.mark.parametrize("pattern", ["empty", "all", "last-row", "first-tile", "burst", "every-17th"])
 @pytest.mark.parametrize("n,kind", [(4_099, "bool"), (300_017, "bool"), (300_017, "radii"),
                                     (77, "radii")])
-def test_two_phase_fused_edge_masks(pattern, n, kind):
-    """The two-phase fused kernel (clouds under 16 mask tiles per CTA slot)
+def test_small_cloud_fused_edge_masks(pattern, n, kind):
+    """The fused kernels of small clouds (under 16 mask tiles per CTA slot)
     on degenerate masks: nothing visible, everything, one row at the ragged
-    end, one dense tile, one dense burst inside one CTA's mask slice (its
-    ids are served to every CTA), a regular stride; equals K1 + K2 bit for
-    bit, over two steps (the grid barrier re-arms), and counts the mask's
-    N_v itself for a coupled sparse-adam step."""
+    end, one dense tile, one dense burst inside one CTA's mask slice, a
+    regular stride.  adamw-gs steps stream per-CTA mask slices (the second
+    step of a coherent pattern takes the balanced two-phase kernel: the
+    burst's ids are served to every CTA); coupled sparse-adam runs two-phase
+    (it counts the mask's N_v itself).  Equals K1 + K2 bit for bit over two
+    steps (the grid barrier re-arms)."""
     from paper_2601_16736_b200 import records as R
     from paper_2601_16736_b200 import synthetic as S
     from paper_2601_16736_b200.optimizer import AdamWGS
