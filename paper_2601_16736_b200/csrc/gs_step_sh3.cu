@@ -291,6 +291,8 @@ int gs_step_fixed_masked_try(const gs_group* groups, int32_t n_groups, const gs_
     return 0;
   TmaMaps maps;
   if (!encode_tma_maps(P, n_rows, 2 * (LayoutSH3::P + 1), &maps)) return 0;
+  static const int slices = getenv("GS_MASK_SLICES") ? atoi(getenv("GS_MASK_SLICES")) : 0;
+  P.mask_slices = slices;  // measurement override of the streaming kernel's mask dealing
   const int mk = (radii ? 2 : 1) + (two ? 2 : 0);
   if (two) {
     P.tp_ids = tp_ids;

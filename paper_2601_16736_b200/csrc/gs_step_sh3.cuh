@@ -94,6 +94,7 @@ struct FixedParams {
   int32_t* tp_ids;
   int32_t* tp_counts;
   unsigned int* tp_bar;
+  int mask_slices;  // streaming fused kernel: 0 = by size, 1 = per-CTA slices, 2 = tiles grid-stride
 };
 
 constexpr int kFixedThreads = 256;

@@ -35,6 +35,8 @@
 
 #include <cuda.h>
 
+#include <type_traits>
+
 namespace gs {
 
 struct TmaMaps {
@@ -427,7 +429,8 @@ __global__ void __launch_bounds__((NCW + 2 + (BW ? 1 : 0)) * 32, MINB)
       // scans its own contiguous 16-byte-aligned slice of the rows, in 1-KB
       // tiles (dealt grid-stride, a few tiles would leave most CTAs idle)
       constexpr int64_t kAlign = 16 / kEsz;  // rows per 16 mask bytes
-      const bool range_mode = n_tiles < kBalancedChunksPerCta * G;
+      const bool range_mode =
+          P.mask_slices == 0 ? n_tiles < kBalancedChunksPerCta * G : P.mask_slices == 1;
       int64_t r_lo = 0, r_hi = nr;
       if (range_mode) {
         const int64_t na = (nr + kAlign - 1) / kAlign;
@@ -435,107 +438,114 @@ __global__ void __launch_bounds__((NCW + 2 + (BW ? 1 : 0)) * 32, MINB)
         r_hi = na * (blockIdx.x + 1) / G * kAlign;
         r_hi = r_hi < nr ? r_hi : nr;
       }
-      auto tile_start = [&](int k2) -> int64_t {
-        return range_mode ? r_lo + (int64_t)k2 * kRowsPerTile
-                          : ((int64_t)blockIdx.x + (int64_t)k2 * G) * kRowsPerTile;
-      };
-      auto tile_end = [&](int64_t st) -> int64_t {
-        return st + kRowsPerTile < r_hi ? st + kRowsPerTile : r_hi;
-      };
-      // bytes of the tile that arrive by bulk copy (16-byte multiple); rows
-      // past them (the ragged end of the mask) are read from global memory
-      auto bulk_bytes = [&](int64_t st) -> int {
-        return (int)(((tile_end(st) - st) * kEsz) & ~(int64_t)15);
-      };
-      const int my_tiles =
-          range_mode ? (r_hi > r_lo ? (int)((r_hi - r_lo + kRowsPerTile - 1) / kRowsPerTile) : 0)
-                     : ((int)blockIdx.x < n_tiles ? (n_tiles - 1 - (int)blockIdx.x) / G + 1 : 0);
-      auto issue = [&](int k2) {  // tile number k2 of this CTA into slot k2 % kMaskRing
-        if (k2 >= my_tiles) return;
-        const int slot = k2 % kMaskRing;
-        const int64_t st = tile_start(k2);
-        const int b = bulk_bytes(st);
-        if (lane == 0) {
-          if (b > 0) {
-            mbar_arrive_expect_tx(&mask_bar[slot], (uint32_t)b);
-            bulk_g2s(s_mask[slot], gmask + st * kEsz, (uint32_t)b, &mask_bar[slot]);
-          } else {
-            mbar_arrive(&mask_bar[slot]);
-          }
-        }
-      };
-      // byte offset in the tile of the lane's 16-byte read q, and its first row
-      // each lane owns contiguous rows (32 uint8 rows or 16 radii), so the
-      // pending ids, and hence the chunks, stay in ascending row order within
-      // a tile (index-coherent masks keep their DRAM locality)
-      auto read_off = [&](int q) -> int {
-        return MASK == 1 ? lane * kLane + 16 * q : (lane & (MTB / 64 - 1)) * 64 + 16 * q;
-      };
-      auto row_of_bit = [&](int k) -> int {  // bit k of the lane's mask -> row of the tile
-        return MASK == 1 ? lane * kLane + k : (lane & (MTB / 64 - 1)) * 16 + k;
-      };
-      int head = 0, tail = 0;  // ring of pending ids: s_pend[head .. tail)
-#pragma unroll
-      for (int k2 = 0; k2 < kMaskRing; ++k2) issue(k2);
-      for (int k2 = 0; k2 < my_tiles; ++k2) {
-        const int64_t st = tile_start(k2);
-        const int slot = k2 % kMaskRing;
-        mbar_wait(&mask_bar[slot], (unsigned)((k2 / kMaskRing) & 1));
-        const int bb = bulk_bytes(st);
-        const int64_t gend = tile_end(st) * kEsz;  // the tile's last mask byte + 1
-        uint32_t bits = 0;
-        if (MASK == 1 || lane < MTB / 64) {
-#pragma unroll
-          for (int q = 0; q < kReads; ++q) {
-            const int off = read_off(q);
-            uint4 v;
-            if (off + 16 <= bb) {
-              v = *reinterpret_cast<const uint4*>(s_mask[slot] + off);
-            } else {  // ragged end: global element reads (zero past the rows)
-              uint32_t w[4] = {0u, 0u, 0u, 0u};
-              const int64_t g0 = st * kEsz + off;
-#pragma unroll
-              for (int by = 0; by < 16; ++by) {
-                const int64_t gb = g0 + by;
-                if (gb < gend) w[by >> 2] |= (uint32_t)gmask[gb] << (8 * (by & 3));
-              }
-              v = make_uint4(w[0], w[1], w[2], w[3]);
-            }
-            if constexpr (MASK == 1) {
-              const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-              for (int j = 0; j < 4; ++j)
-#pragma unroll
-                for (int e = 0; e < 4; ++e)
-                  bits |= (((w[j] >> (8 * e)) & 0xffu) != 0u) << (16 * q + 4 * j + e);
+      // the tile walk, specialised for the two dealings (index arithmetic on
+      // the loader's critical path: c5 at 1% is loader-bound)
+      auto scan_tiles = [&](auto slice_tag) {
+        constexpr bool kSlice = decltype(slice_tag)::value;
+        auto tile_start = [&](int k2) -> int64_t {
+          if constexpr (kSlice) return r_lo + (int64_t)k2 * kRowsPerTile;
+          else return (int64_t)((int)blockIdx.x + k2 * G) * kRowsPerTile;
+        };
+        auto tile_end = [&](int64_t st) -> int64_t {
+          return st + kRowsPerTile < r_hi ? st + kRowsPerTile : r_hi;
+        };
+        // bytes of the tile that arrive by bulk copy (16-byte multiple); rows
+        // past them (the ragged end of the mask) are read from global memory
+        auto bulk_bytes = [&](int64_t st) -> int {
+          return (int)(((tile_end(st) - st) * kEsz) & ~(int64_t)15);
+        };
+        const int my_tiles =
+            kSlice ? (r_hi > r_lo ? (int)((r_hi - r_lo + kRowsPerTile - 1) / kRowsPerTile) : 0)
+                   : ((int)blockIdx.x < n_tiles ? (n_tiles - 1 - (int)blockIdx.x) / G + 1 : 0);
+        auto issue = [&](int k2) {  // tile number k2 of this CTA into slot k2 % kMaskRing
+          if (k2 >= my_tiles) return;
+          const int slot = k2 % kMaskRing;
+          const int64_t st = tile_start(k2);
+          const int b = bulk_bytes(st);
+          if (lane == 0) {
+            if (b > 0) {
+              mbar_arrive_expect_tx(&mask_bar[slot], (uint32_t)b);
+              bulk_g2s(s_mask[slot], gmask + st * kEsz, (uint32_t)b, &mask_bar[slot]);
             } else {
-              bits |= (uint32_t)((int)v.x > 0) << (4 * q) | (uint32_t)((int)v.y > 0) << (4 * q + 1) |
-                      (uint32_t)((int)v.z > 0) << (4 * q + 2) | (uint32_t)((int)v.w > 0) << (4 * q + 3);
+              mbar_arrive(&mask_bar[slot]);
             }
           }
+        };
+        // byte offset in the tile of the lane's 16-byte read q, and its first row
+        // each lane owns contiguous rows (32 uint8 rows or 16 radii), so the
+        // pending ids, and hence the chunks, stay in ascending row order within
+        // a tile (index-coherent masks keep their DRAM locality)
+        auto read_off = [&](int q) -> int {
+          return MASK == 1 ? lane * kLane + 16 * q : (lane & (MTB / 64 - 1)) * 64 + 16 * q;
+        };
+        auto row_of_bit = [&](int k) -> int {  // bit k of the lane's mask -> row of the tile
+          return MASK == 1 ? lane * kLane + k : (lane & (MTB / 64 - 1)) * 16 + k;
+        };
+        int head = 0, tail = 0;  // ring of pending ids: s_pend[head .. tail)
+  #pragma unroll
+        for (int k2 = 0; k2 < kMaskRing; ++k2) issue(k2);
+        for (int k2 = 0; k2 < my_tiles; ++k2) {
+          const int64_t st = tile_start(k2);
+          const int slot = k2 % kMaskRing;
+          mbar_wait(&mask_bar[slot], (unsigned)((k2 / kMaskRing) & 1));
+          const int bb = bulk_bytes(st);
+          const int64_t gend = tile_end(st) * kEsz;  // the tile's last mask byte + 1
+          uint32_t bits = 0;
+          if (MASK == 1 || lane < MTB / 64) {
+  #pragma unroll
+            for (int q = 0; q < kReads; ++q) {
+              const int off = read_off(q);
+              uint4 v;
+              if (off + 16 <= bb) {
+                v = *reinterpret_cast<const uint4*>(s_mask[slot] + off);
+              } else {  // ragged end: global element reads (zero past the rows)
+                uint32_t w[4] = {0u, 0u, 0u, 0u};
+                const int64_t g0 = st * kEsz + off;
+  #pragma unroll
+                for (int by = 0; by < 16; ++by) {
+                  const int64_t gb = g0 + by;
+                  if (gb < gend) w[by >> 2] |= (uint32_t)gmask[gb] << (8 * (by & 3));
+                }
+                v = make_uint4(w[0], w[1], w[2], w[3]);
+              }
+              if constexpr (MASK == 1) {
+                const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+  #pragma unroll
+                for (int j = 0; j < 4; ++j)
+  #pragma unroll
+                  for (int e = 0; e < 4; ++e)
+                    bits |= (((w[j] >> (8 * e)) & 0xffu) != 0u) << (16 * q + 4 * j + e);
+              } else {
+                bits |= (uint32_t)((int)v.x > 0) << (4 * q) | (uint32_t)((int)v.y > 0) << (4 * q + 1) |
+                        (uint32_t)((int)v.z > 0) << (4 * q + 2) | (uint32_t)((int)v.w > 0) << (4 * q + 3);
+              }
+            }
+          }
+          const int cnt = __popc(bits);
+          int incl = cnt;
+  #pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+          }
+          const int total = __shfl_sync(0xffffffffu, incl, 31);
+          int pos = tail + incl - cnt;
+          const int row0 = (int)st;
+          for (uint32_t x = bits; x; x &= x - 1)
+            s_pend[(pos++) & (kPend - 1)] = row0 + row_of_bit(__ffs(x) - 1);
+          tail += total;
+          __syncwarp();  // ids written; every lane is done with the slot
+          issue(k2 + kMaskRing);
+          while (tail - head >= R) {
+            emit((int)s_pend[(head + lane) & (kPend - 1)], R);
+            head += R;
+          }
         }
-        const int cnt = __popc(bits);
-        int incl = cnt;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int y = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= o) incl += y;
-        }
-        const int total = __shfl_sync(0xffffffffu, incl, 31);
-        int pos = tail + incl - cnt;
-        const int row0 = (int)st;
-        for (uint32_t x = bits; x; x &= x - 1)
-          s_pend[(pos++) & (kPend - 1)] = row0 + row_of_bit(__ffs(x) - 1);
-        tail += total;
-        __syncwarp();  // ids written; every lane is done with the slot
-        issue(k2 + kMaskRing);
-        while (tail - head >= R) {
-          emit((int)s_pend[(head + lane) & (kPend - 1)], R);
-          head += R;
-        }
-      }
-      if (tail > head) emit(lane < tail - head ? (int)s_pend[(head + lane) & (kPend - 1)] : oob,
-                            tail - head);
+        if (tail > head) emit(lane < tail - head ? (int)s_pend[(head + lane) & (kPend - 1)] : oob,
+                              tail - head);
+      };
+      if (range_mode) scan_tiles(std::true_type{});
+      else scan_tiles(std::false_type{});
     }
     emit(oob, -1);
     if (lane == 0) GS_STAMP(trc, 2);
@@ -821,7 +831,9 @@ void launch_tma4(const FixedParams& P, const TmaMaps& M, int64_t max_rows, cudaS
   int64_t work = (max_rows + tile - 1) / tile;
   // streamed masks under kBalancedChunksPerCta tiles per CTA slot: the
   // kernel gives every CTA a contiguous slice (>= 256 rows each)
-  if ((MASK == 1 || MASK == 2) && work < (int64_t)kBalancedChunksPerCta * gs_sm_count() * MINB)
+  if ((MASK == 1 || MASK == 2) &&
+      (P.mask_slices == 1 ||
+       (P.mask_slices == 0 && work < (int64_t)kBalancedChunksPerCta * gs_sm_count() * MINB)))
     work = (max_rows + 255) / 256;
   const int grid =
       (int)std::max<int64_t>(1, std::min<int64_t>(work, (int64_t)gs_sm_count() * MINB));
