@@ -740,7 +740,9 @@ def ours(args, wl, p_vis):
             "kernel": ("gs::step_kernel (K2, gs_step)" if args.layout != "rows" else
                        ("gs::step_tma4_kernel<LayoutSH3, ..., MASK=1> (K1 fused into K2: the "
                         "loader compacts the mask; 2-D TMA gather4 / scatter4 on the records; "
-                        "via gs_step_rows_masked)" if main["roofline"].get("fused_compaction")
+                        "via gs_step_rows_masked; on clouds under ~4.8M rows coherent masks "
+                        "and coupled sparse-adam take MASK=3, the two-phase variant)"
+                        if main["roofline"].get("fused_compaction")
                         else "gs::step_tma4_kernel<LayoutSH3, ...> (K2 on the K1 index list, "
                         "2-D TMA gather4 / scatter4, via gs_step_rows)")
                        if args.params == "record" else

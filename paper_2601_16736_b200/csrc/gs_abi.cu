@@ -13,7 +13,16 @@ void gs_set_error(const char* fmt, ...) {
   va_end(ap);
 }
 
+// a launch helper that could not launch (and said why with gs_set_error)
+static thread_local bool g_launch_failed = false;
+void gs_fail_launch() { g_launch_failed = true; }
+
 int gs_check_launch(const char* what) {
+  if (g_launch_failed) {
+    g_launch_failed = false;
+    (void)cudaGetLastError();
+    return GS_ERR_LAUNCH;
+  }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     gs_set_error("%s: %s", what, cudaGetErrorString(e));

@@ -327,6 +327,7 @@ __device__ __forceinline__ void final_reduce_n(const double* partials, int nbloc
 
 // host-side error plumbing (gs_abi.cu)
 void gs_set_error(const char* fmt, ...);
+void gs_fail_launch();  // the next gs_check_launch reports GS_ERR_LAUNCH
 int gs_check_launch(const char* what);
 int gs_sm_count();
 

@@ -802,13 +802,23 @@ void launch_tma4(const FixedParams& P, const TmaMaps& M, int64_t max_rows, cudaS
   if constexpr (MASK >= 3) {
     // two-phase: one wave of CTAs (the grid barrier needs every CTA
     // resident), at least 256 mask rows each, launched cooperatively
-    static int resident = -1;
-    if (resident < 0) {
+    // resident CTAs of this kernel on the current device (cached per device)
+    static std::atomic<int> resident_of[64];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int resident = dev < 64 ? resident_of[dev].load(std::memory_order_relaxed) : 0;
+    if (resident <= 0) {
       int per_sm = 0;
       if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (NCW + 2 + (BW ? 1 : 0)) * 32,
                                                         bytes) != cudaSuccess)
         per_sm = 0;
       resident = per_sm * gs_sm_count();
+      if (dev < 64 && resident > 0) resident_of[dev].store(resident, std::memory_order_relaxed);
+    }
+    if (resident <= 0) {
+      gs_set_error("two-phase step kernel: no resident CTA (occupancy query failed)");
+      gs_fail_launch();
+      return;
     }
     const int64_t want = (max_rows + 255) / 256;
     const int grid = (int)std::max<int64_t>(
@@ -824,7 +834,12 @@ void launch_tma4(const FixedParams& P, const TmaMaps& M, int64_t max_rows, cudaS
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, kern, P, M, vis_mask, trace_buf());
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, P, M, vis_mask, trace_buf());
+    if (e != cudaSuccess) {
+      gs_set_error("two-phase step kernel (cooperative launch of %d CTAs): %s", grid,
+                   cudaGetErrorString(e));
+      gs_fail_launch();
+    }
     return;
   }
   const int64_t tile = MASK == 1 ? MTB : MASK == 2 ? MTB / 4 : 32;
