@@ -286,10 +286,21 @@ __global__ void __launch_bounds__((NCW + 2 + (BW ? 1 : 0)) * 32, MINB)
     // ------------------------------------------------------------------ loader
     int st = 0, k = 0;
     unsigned ph = 0;
+#ifdef GS_TRACE
+    long long tr_t0 = clock64(), tr_empty = 0, tr_mask = 0;  // loader wait cycles
+#define GS_TRACE_WAIT(acc, stmt)     \
+  do {                               \
+    const long long t_ = clock64();  \
+    stmt;                            \
+    acc += clock64() - t_;           \
+  } while (0)
+#else
+#define GS_TRACE_WAIT(acc, stmt) stmt
+#endif
     // one chunk into the next stage: lane i's row id (oob past nv), nv rows;
     // nv < 0 ends the stream (no data, the consumers and the storer exit)
     auto emit = [&](int my_id, int nv) {
-      if (k >= S) mbar_wait(&empty_bar[st], ph ^ 1u);
+      if (k >= S) GS_TRACE_WAIT(tr_empty, mbar_wait(&empty_bar[st], ph ^ 1u));
       unsigned char* sb = stage(st);
       uint64_t* tbar = BW ? &data_bar[st] : &full_bar[st];  // the gathers complete here
       if (nv > 0) {
@@ -487,7 +498,7 @@ __global__ void __launch_bounds__((NCW + 2 + (BW ? 1 : 0)) * 32, MINB)
         for (int k2 = 0; k2 < my_tiles; ++k2) {
           const int64_t st = tile_start(k2);
           const int slot = k2 % kMaskRing;
-          mbar_wait(&mask_bar[slot], (unsigned)((k2 / kMaskRing) & 1));
+          GS_TRACE_WAIT(tr_mask, mbar_wait(&mask_bar[slot], (unsigned)((k2 / kMaskRing) & 1)));
           const int bb = bulk_bytes(st);
           const int64_t gend = tile_end(st) * kEsz;  // the tile's last mask byte + 1
           uint32_t bits = 0;
@@ -549,6 +560,14 @@ __global__ void __launch_bounds__((NCW + 2 + (BW ? 1 : 0)) * 32, MINB)
     }
     emit(oob, -1);
     if (lane == 0) GS_STAMP(trc, 2);
+#ifdef GS_TRACE
+    if (lane == 0 && !kTwoPhase) {
+      GS_TRACE_VAL(trc, 12, (unsigned long long)(clock64() - tr_t0));
+      GS_TRACE_VAL(trc, 14, (unsigned long long)tr_empty);
+      GS_TRACE_VAL(trc, 15, (unsigned long long)tr_mask);
+    }
+#endif
+#undef GS_TRACE_WAIT
   } else if (BW && warp == NCW + 2) {
     // ------------------------------------------------------------ bias warp
     int st = 0;

@@ -26,7 +26,7 @@ from paper_2601_16736_b200 import records as R  # noqa: E402
 from paper_2601_16736_b200 import synthetic as S  # noqa: E402
 from paper_2601_16736_b200.optimizer import AdamWGS  # noqa: E402
 
-NAMES = {0: "entry", 12: "phase A done", 13: "grid barrier", 1: "first emit", 2: "end emit", 3: "first chunk in", 4: "consumers out",
+NAMES = {0: "entry", 1: "first emit", 2: "end emit", 3: "first chunk in", 4: "consumers out",
          5: "stores done", 6: "block reduce", 11: "exit"}
 
 
@@ -64,19 +64,30 @@ def main():
                 lib.gs_debug_set_trace(None)
     t = trace.view(4096, 16).cpu().numpy().astype(np.int64)
     live = t[:, 0] > 0
-    t[:, 12:14] = np.where(t[:, 12:14] > 0, t[:, 12:14], t[:, [0]])
     t = t[live]
     t0 = t[:, 0].min()
-    print(f"rows {args.rows} vis {args.vis} fused {args.fused}: {live.sum()} CTAs, "
+    two_phase = (t[:, 13] > 0).any()  # slot 13: the grid-barrier stamp
+    print(f"rows {args.rows} vis {args.vis} fused {args.fused} two-phase {two_phase}: {live.sum()} CTAs, "
           f"visible {t[:, 9].sum()}, kernel span {(t[:, 11].max() - t0) / 1e3:.2f} us")
     rel = lambda k: (t[:, k] - t0) / 1e3  # noqa: E731
-    for k, name in NAMES.items():
+    names = dict(NAMES)
+    if two_phase:
+        names = {0: "entry", 12: "phase A done", 13: "grid barrier",
+                 **{k: v for k, v in NAMES.items() if k}}
+    for k, name in names.items():
         x = rel(k)
         print(f"  {k:2d} {name:16s} min {x.min():7.2f}  p50 {np.median(x):7.2f}  "
               f"p90 {np.percentile(x, 90):7.2f}  max {x.max():7.2f} us")
     lastb = t[:, 7] > 0
     if lastb.any():
         print(f"   7 final reduce in  {rel(7)[lastb][0]:7.2f}   8 final reduce out {rel(8)[lastb][0]:7.2f}")
+    if not two_phase:  # slots 12, 14, 15: loader cycles, waits on a free stage / mask tiles
+        cyc = t[:, 12].astype(np.float64)
+        ok = cyc > 0
+        if ok.any():
+            print(f"  loader cycles p50 {np.median(cyc[ok]):.0f}; waiting on a free stage "
+                  f"{np.median(t[ok, 14] / cyc[ok]) * 100:.1f}% / on mask tiles "
+                  f"{np.median(t[ok, 15] / cyc[ok]) * 100:.1f}% (p50 over CTAs)")
     work = t[:, 9]
     dur = (t[:, 4] - t[:, 3]) / 1e3
     print(f"  rows per CTA: min {work.min()} max {work.max()} mean {work.mean():.1f}; "
