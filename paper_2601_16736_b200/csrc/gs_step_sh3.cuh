@@ -2032,6 +2032,22 @@ void launch_fixed_masked(const FixedParams& P, const TmaMaps& M, int64_t n_rows,
     }
     return;
   }
+  // sparse uint8 masks on big clouds (>= 64 one-KB tiles per CTA slot): 3
+  // CTAs per SM (2 stages, 4 consumer warps, 512-byte mask tiles), i.e. 3
+  // mask-scanning loaders per SM, the loader being the busy role there
+  // (c5 at 1%: 0.190 against 0.196 ms, at 3%: 0.476 against 0.504; on the
+  // 6.25M-row shard the extra CTAs lose, 0.039 against 0.037;
+  // profiles/r02/small_clouds.txt).  GS_LOWVIS_SHAPE=0/1 forces it off/on.
+  static const int lv = getenv("GS_LOWVIS_SHAPE") ? atoi(getenv("GS_LOWVIS_SHAPE")) : -1;
+  const bool big = (n_rows + 1023) / 1024 >= 64 * 2 * (int64_t)gs_sm_count();
+  if (mask_kind == 1 && bw && (lv == 1 || (lv < 0 && big))) {
+    launch_tma4<L, MODE, false, 2, 4, 3, 1, true, 512>(P, M, n_rows, s, mask);
+    return;
+  }
+  if (mask_kind == 1 && bw && lv == 2) {
+    launch_tma4<L, MODE, false, 2, 6, 3, 1, true, 512>(P, M, n_rows, s, mask);
+    return;
+  }
   if (mask_kind == 2) {
     if (bw) launch_tma4<L, MODE, false, 3, 8, 2, 2, true>(P, M, n_rows, s, mask);
     else launch_tma4<L, MODE, false, 3, 8, 2, 2, false>(P, M, n_rows, s, mask);

@@ -147,9 +147,11 @@ __global__ void __launch_bounds__((NCW + 2 + (BW ? 1 : 0)) * 32, MINB)
   __shared__ uint32_t s_crow[S][R];
   __shared__ int s_nv[S];  // rows of the chunk in the stage; -1 ends the CTA's chunk stream
   constexpr bool kStreamMask = MASK == 1 || MASK == 2;
-  constexpr int kPend = kStreamMask ? 2048 : 1;  // pending visible ids (fused compaction)
+  // pending visible ids (fused compaction): one tile's rows + a partial chunk
+  constexpr int kPend = kStreamMask ? 2 * (MASK == 2 ? MTB / 4 : MTB) : 1;
   __shared__ uint32_t s_pend[kPend];
-  constexpr int kMaskRing = kStreamMask ? 6 * 1024 / MTB : 1;  // 6 KB of mask tiles in flight
+  // 6 KB of mask tiles in flight (4 KB at 3 CTAs per SM, to fit)
+  constexpr int kMaskRing = kStreamMask ? (MINB >= 3 ? 4096 : 6144) / MTB : 1;
   __shared__ __align__(128) unsigned char s_mask[kMaskRing][kStreamMask ? MTB : 16];
   __shared__ __align__(8) uint64_t mask_bar[kMaskRing];
   __shared__ double s_red[GS_STEP_STATS * NWARPS];
