@@ -481,9 +481,15 @@ class Workload:
 
 
 def _prep_capture(w):
-    """No outstanding host-side event waits may cross into a capture."""
+    """No outstanding host-side event waits may cross into a capture, and the
+    warm-up steps' statistics are read, so the layout hints they carry
+    (visible fraction, run length) steer the captured steps as they steer a
+    training loop's later steps (without the poll, whether a warm-up step
+    had completed when the host issued the next one decides the shape)."""
     import torch
     torch.cuda.synchronize()
+    for o in w.opts:
+        o.check_errors()
     for sh in w.shards:
         if sh is not None:
             sh.capture_begin()
