@@ -297,12 +297,17 @@ int gs_densify_rows(const float* grad, int64_t grad_stride, int32_t width, const
  * statistics' n_visible is the mask's visible count; results equal
  * gs_compact + gs_step_rows bit for bit (rows are independent).  flags:
  * GS_MASKED_LOW_VISIBILITY picks the kernel shape for sparse masks (a few %
- * visible), GS_MASKED_COHERENT the two-phase kernel for small clouds (same
- * results either way). */
+ * visible), GS_MASKED_COHERENT the two-phase kernel for small clouds,
+ * GS_MASKED_BALANCE_TAIL the dynamic tail of the tile dealing (same results
+ * in every case). */
 #define GS_MASKED_LOW_VISIBILITY 1
 /* flags: the mask's visible rows come in long index runs (e.g. the last
  * step's GS_STAT_N_RUNS hint); small clouds then balance them (two-phase). */
 #define GS_MASKED_COHERENT 2
+/* flags: the mask is not very sparse (>= ~2 % visible, e.g. the last step's
+ * statistics): the streaming kernel claims its last mask tiles dynamically
+ * so that the CTAs finish together (same results). */
+#define GS_MASKED_BALANCE_TAIL 4
 int gs_step_rows_masked(const gs_group* groups, int32_t n_groups, const gs_step_cfg* cfg,
                         const uint8_t* mask, const int32_t* radii, int64_t n_rows, float* record,
                         int64_t record_stride, double* stats_out, void* ws, size_t ws_bytes,

@@ -17,6 +17,7 @@ GS_ABI_VERSION = 4
 GS_MAX_GROUPS = 8
 GS_MASKED_LOW_VISIBILITY = 1
 GS_MASKED_COHERENT = 2
+GS_MASKED_BALANCE_TAIL = 4
 
 GS_OK = 0
 

@@ -37,7 +37,8 @@ int gs_step_fixed_masked_try(const gs_group* groups, int32_t n_groups, const gs_
                              const uint8_t* mask, const int32_t* radii, int64_t n_rows,
                              float* record, int64_t record_stride, double* stats_out,
                              double* partials, unsigned int* counter, unsigned int* tp_bar,
-                             int32_t* tp_counts, int32_t* tp_ids, int32_t flags, void* stream);
+                             int32_t* tp_counts, int32_t* tp_ids, unsigned int* tile_ctr,
+                             int32_t flags, void* stream);
 
 namespace gs {
 
@@ -281,7 +282,8 @@ __global__ void __launch_bounds__(kRowThreads, MINB)
 struct RowStepWorkspace {
   unsigned int counter;  // last-block-done counter of the statistics
   unsigned int bar[2];   // grid barrier of the two-phase fused kernel
-  unsigned int pad[13];
+  unsigned int tile_ctr; // claim counter of the streaming fused kernel's dynamic tail
+  unsigned int pad[12];
 };
 
 int max_row_blocks() { return gs_sm_count() * kRowMaxBlocksPerSM; }
@@ -526,7 +528,7 @@ extern "C" int gs_step_rows_masked(const gs_group* groups, int32_t n_groups,
   }
   if (!gs_step_fixed_masked_try(groups, n_groups, cfg, mask, radii, n_rows, record, record_stride,
                                 stats_out, partials, &hdr->counter, hdr->bar, tp_counts, tp_ids,
-                                flags, stream))
+                                &hdr->tile_ctr, flags, stream))
     return GS_OK;  // not this layout: the caller compacts and calls gs_step_rows
   *launched = 1;
   return gs_check_launch("gs_step_rows_masked");

@@ -252,7 +252,8 @@ int gs_step_fixed_masked_try(const gs_group* groups, int32_t n_groups, const gs_
                              const uint8_t* mask, const int32_t* radii, int64_t n_rows,
                              float* record, int64_t record_stride, double* stats_out,
                              double* partials, unsigned int* counter, unsigned int* tp_bar,
-                             int32_t* tp_counts, int32_t* tp_ids, int32_t flags, void* stream) {
+                             int32_t* tp_counts, int32_t* tp_ids, unsigned int* tile_ctr,
+                             int32_t flags, void* stream) {
   using namespace gs;
   if (cfg->check != GS_CHECK_FUSED || cfg->mode == GS_MODE_COUPLED_ADAM) return 0;
   if (fixed_variant() == 21 || n_rows < 1) return 0;
@@ -293,6 +294,16 @@ int gs_step_fixed_masked_try(const gs_group* groups, int32_t n_groups, const gs_
   if (!encode_tma_maps(P, n_rows, 2 * (LayoutSH3::P + 1), &maps)) return 0;
   static const int slices = getenv("GS_MASK_SLICES") ? atoi(getenv("GS_MASK_SLICES")) : 0;
   P.mask_slices = slices;  // measurement override of the streaming kernel's mask dealing
+  // the streaming kernel deals the last eighth of its mask tiles dynamically
+  // when the caller's hint says the mask is not very sparse (>= 2 % visible:
+  // c5 30% 4.22 against 4.34 ms, 3% 0.452 against 0.479, c3 0.5345 against
+  // 0.5366; at 1% the claims cost more than the balance gains, 0.198 against
+  // 0.185; profiles/r02/small_clouds.txt).  GS_DYN_TAIL=0/k forces off /
+  // k eighths (measurement).
+  static const int dyn_env = getenv("GS_DYN_TAIL") ? atoi(getenv("GS_DYN_TAIL")) : -1;
+  const int dyn = dyn_env >= 0 ? dyn_env : ((flags & GS_MASKED_BALANCE_TAIL) ? 1 : 0);
+  P.tile_ctr = (!two && dyn >= 1) ? tile_ctr : nullptr;
+  P.dyn_eighths = dyn >= 1 ? (dyn < 8 ? dyn : 7) : 0;
   const int mk = (radii ? 2 : 1) + (two ? 2 : 0);
   if (two) {
     P.tp_ids = tp_ids;

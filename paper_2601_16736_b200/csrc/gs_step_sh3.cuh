@@ -95,6 +95,8 @@ struct FixedParams {
   int32_t* tp_counts;
   unsigned int* tp_bar;
   int mask_slices;  // streaming fused kernel: 0 = by size, 1 = per-CTA slices, 2 = tiles grid-stride
+  unsigned int* tile_ctr;  // streaming fused kernel: the dynamic tail's claim counter (null: off)
+  int dyn_eighths;         // eighths of the tiles in the dynamic tail
 };
 
 constexpr int kFixedThreads = 256;

@@ -453,10 +453,37 @@ __global__ void __launch_bounds__((NCW + 2 + (BW ? 1 : 0)) * 32, MINB)
       }
       // the tile walk, specialised for the two dealings (index arithmetic on
       // the loader's critical path: c5 at 1% is loader-bound)
-      auto scan_tiles = [&](auto slice_tag) {
-        constexpr bool kSlice = decltype(slice_tag)::value;
+      // dynamic tail (sparse masks, tiles dealt grid-stride): the first
+      // kStaticRounds rounds of G tiles are dealt grid-stride, the rest are
+      // claimed one by one from a global counter (P.tile_ctr) by whichever
+      // loader is free, so the CTAs finish together.  Lane 0 keeps claims in
+      // flight (issued two tiles ahead of their use), so the atomic's latency
+      // stays off the loader's path (two claims in flight); claims land in
+      // s_claim (one per ring slot), -1 once the pool is empty.
+      const int n_static = P.tile_ctr != nullptr && !range_mode
+                               ? (int)((int64_t)n_tiles * (8 - P.dyn_eighths) / 8) / G * G
+                               : n_tiles;
+      const int n_dyn = n_tiles - n_static;
+      __shared__ int s_claim[kStreamMask ? kMaskRing : 1];
+      auto scan_tiles = [&](auto deal_tag) {
+        constexpr int kDeal = decltype(deal_tag)::value;  // 0 grid-stride, 1 slices, 2 + dynamic tail
+        constexpr bool kSlice = kDeal == 1;
+        constexpr bool kDyn = kDeal == 2;
+        const int my_static = kDyn ? n_static / G : 0;  // static tiles of this CTA (dynamic dealing)
+        unsigned next_claim = 0, next_claim2 = 0;  // two claims in flight (lane 0)
+        if constexpr (kDyn) {
+          if (lane == 0) {
+            next_claim = atomicAdd(P.tile_ctr, 1u);
+            next_claim2 = atomicAdd(P.tile_ctr, 1u);
+          }
+        }
+        auto tile_of = [&](int k2) -> int {  // dynamic dealing: tile number, -1 past the pool
+          if (k2 < my_static) return (int)blockIdx.x + k2 * G;
+          return s_claim[k2 % kMaskRing];
+        };
         auto tile_start = [&](int k2) -> int64_t {
           if constexpr (kSlice) return r_lo + (int64_t)k2 * kRowsPerTile;
+          else if constexpr (kDyn) return (int64_t)tile_of(k2) * kRowsPerTile;
           else return (int64_t)((int)blockIdx.x + k2 * G) * kRowsPerTile;
         };
         auto tile_end = [&](int64_t st) -> int64_t {
@@ -468,11 +495,25 @@ __global__ void __launch_bounds__((NCW + 2 + (BW ? 1 : 0)) * 32, MINB)
           return (int)(((tile_end(st) - st) * kEsz) & ~(int64_t)15);
         };
         const int my_tiles =
-            kSlice ? (r_hi > r_lo ? (int)((r_hi - r_lo + kRowsPerTile - 1) / kRowsPerTile) : 0)
-                   : ((int)blockIdx.x < n_tiles ? (n_tiles - 1 - (int)blockIdx.x) / G + 1 : 0);
+            kDyn ? INT32_MAX
+                 : kSlice ? (r_hi > r_lo ? (int)((r_hi - r_lo + kRowsPerTile - 1) / kRowsPerTile) : 0)
+                          : ((int)blockIdx.x < n_tiles ? (n_tiles - 1 - (int)blockIdx.x) / G + 1 : 0);
         auto issue = [&](int k2) {  // tile number k2 of this CTA into slot k2 % kMaskRing
           if (k2 >= my_tiles) return;
           const int slot = k2 % kMaskRing;
+          if constexpr (kDyn) {
+            if (k2 >= my_static) {  // take the claim in flight, put the next one in flight
+              int c = -1;
+              if (lane == 0) {
+                c = (int)next_claim < n_dyn ? n_static + (int)next_claim : -1;
+                next_claim = next_claim2;
+                if (c >= 0) next_claim2 = atomicAdd(P.tile_ctr, 1u);
+                s_claim[slot] = c;
+              }
+              c = __shfl_sync(0xffffffffu, c, 0);
+              if (c < 0) return;
+            }
+          }
           const int64_t st = tile_start(k2);
           const int b = bulk_bytes(st);
           if (lane == 0) {
@@ -498,6 +539,9 @@ __global__ void __launch_bounds__((NCW + 2 + (BW ? 1 : 0)) * 32, MINB)
   #pragma unroll
         for (int k2 = 0; k2 < kMaskRing; ++k2) issue(k2);
         for (int k2 = 0; k2 < my_tiles; ++k2) {
+          if constexpr (kDyn) {
+            if (k2 >= my_static && s_claim[k2 % kMaskRing] < 0) break;  // the pool is empty
+          }
           const int64_t st = tile_start(k2);
           const int slot = k2 % kMaskRing;
           GS_TRACE_WAIT(tr_mask, mbar_wait(&mask_bar[slot], (unsigned)((k2 / kMaskRing) & 1)));
@@ -557,8 +601,9 @@ __global__ void __launch_bounds__((NCW + 2 + (BW ? 1 : 0)) * 32, MINB)
         if (tail > head) emit(lane < tail - head ? (int)s_pend[(head + lane) & (kPend - 1)] : oob,
                               tail - head);
       };
-      if (range_mode) scan_tiles(std::true_type{});
-      else scan_tiles(std::false_type{});
+      if (range_mode) scan_tiles(std::integral_constant<int, 1>{});
+      else if (n_dyn > 0) scan_tiles(std::integral_constant<int, 2>{});
+      else scan_tiles(std::integral_constant<int, 0>{});
     }
     emit(oob, -1);
     if (lane == 0) GS_STAMP(trc, 2);
@@ -789,6 +834,7 @@ __global__ void __launch_bounds__((NCW + 2 + (BW ? 1 : 0)) * 32, MINB)
   }
   if (last_block_arrive(P.counter)) {
     if (threadIdx.x == 0) GS_STAMP(trc, 7);
+    if (threadIdx.x == 0 && P.tile_ctr != nullptr) *P.tile_ctr = 0u;  // every claim is done
     final_reduce_n<GS_STEP_STATS, NWARPS>(P.partials, gridDim.x, GS_STEP_STATS, P.stats_out,
                                              is_max, s_red);
     if (threadIdx.x == 0) GS_STAMP(trc, 8);

@@ -508,7 +508,7 @@ class StepEngine:
                     clip_opacity: float = 10.0, clip_scale: float = 10.0,
                     n_pixels_rounded: float = 0.0, record: torch.Tensor,
                     densify: tuple | None = None, low_visibility: bool = False,
-                    coherent: bool = False,
+                    coherent: bool = False, balance_tail: bool = False,
                     n_visible_dev: torch.Tensor | None = None) -> torch.Tensor | None:
         """Fused K1 + K2 (gs_step_rows_masked): the step of the mask's visible
         rows with the compaction done inside the step kernel.  Returns the
@@ -541,7 +541,8 @@ class StepEngine:
                                           self.stats.data_ptr(), self.rows_ws.data_ptr(),
                                           self.rows_ws.numel(),
                                           (L.GS_MASKED_LOW_VISIBILITY if low_visibility else 0)
-                                          | (L.GS_MASKED_COHERENT if coherent else 0),
+                                          | (L.GS_MASKED_COHERENT if coherent else 0)
+                                          | (L.GS_MASKED_BALANCE_TAIL if balance_tail else 0),
                                           C.byref(launched), _stream_handle(self.device))
         _nvtx_pop()
         L.check(rc, "gs_step_rows_masked")

@@ -487,8 +487,11 @@ class AdamWGS:
         if coherent and not small:
             return None
         low = self._vis_frac is not None and self._vis_frac < 0.05
+        # masks >= 2 % visible: the last mask tiles are claimed dynamically
+        # (c5 at 30%: 4.22 against 4.34 ms; at 1% the claims cost more)
+        balance = self._vis_frac is not None and self._vis_frac >= 0.02
         kwm = dict(eps=self.eps, record=self.state.record, densify=kw.get("densify"),
-                   low_visibility=low, coherent=coherent)
+                   low_visibility=low, coherent=coherent, balance_tail=balance)
         if mode == "adamw-gs":
             if n_pixels is None:
                 raise ConfigError("adamw-gs needs n_pixels (N_I)")

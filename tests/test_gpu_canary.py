@@ -88,6 +88,7 @@ def _verify(n, bufs):
     (5_000_011, 0.3, "adamw-gs", True, "fused", False),      # tiles dealt grid-stride
     (5_000_011, 0.3, "adamw-gs", False, "fused", False),     # K1 + K2, long list
     (20_000_003, 0.02, "adamw-gs", True, "fused", False),    # sparse: bias warp, 3 CTAs/SM
+    (20_000_003, 0.3, "adamw-gs", True, "fused", False),     # dynamic tail (from step 2 on)
 ])
 def test_step_paths_write_only_their_rows(n, p, mode, fused, check, radii):
     cfg, _, opt, grads, bufs = _setup(n, p, mode, fused, check)

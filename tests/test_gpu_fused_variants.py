@@ -3,8 +3,9 @@ measurement switches (environment, read once per process, hence one
 subprocess per case): the two-phase kernel on i.i.d. masks of every size
 (GS_FUSED_MODE=2), per-CTA mask slices on a big cloud (GS_MASK_SLICES=1),
 tiles dealt grid-stride on a small one (GS_MASK_SLICES=2), the bias warp on
-both (GS_TMA4_BW=1), and the 3-CTA-per-SM sparse-mask shape on any cloud
-(GS_LOWVIS_SHAPE).  Each equals K1 + K2 bit for bit (marked
+both (GS_TMA4_BW=1), the 3-CTA-per-SM sparse-mask shape on any cloud
+(GS_LOWVIS_SHAPE), and dynamic tails of the tile dealing from one to seven
+eighths (GS_DYN_TAIL).  Each equals K1 + K2 bit for bit (marked
 gpu)."""
 
 import os
@@ -31,6 +32,9 @@ BODY = Path(__file__).resolve().parent / "_fused_env_check.py"
     ({"GS_TMA4_BW": "1", "GS_LOWVIS_SHAPE": "1"}, 5_000_011, "bool", "adamw-gs", 0.02),
     ({"GS_TMA4_BW": "1", "GS_LOWVIS_SHAPE": "1"}, 200_003, "bool", "sparse-adam", 0.02),
     ({"GS_TMA4_BW": "1", "GS_LOWVIS_SHAPE": "2"}, 1_000_003, "bool", "adamw-const", 0.3),
+    ({"GS_DYN_TAIL": "1"}, 5_000_011, "bool", "adamw-gs", 0.3),
+    ({"GS_DYN_TAIL": "7"}, 5_000_011, "radii", "adamw-const", 0.1),
+    ({"GS_DYN_TAIL": "4", "GS_TMA4_BW": "1"}, 5_000_011, "bool", "sparse-adam", 0.02),
 ])
 def test_forced_fused_dealing_equals_index_path(env, n, kind, mode, p):
     e = dict(os.environ)
