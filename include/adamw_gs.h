@@ -329,6 +329,15 @@ int gs_philox_bernoulli(const uint64_t* counter, const uint64_t* key, int64_t fi
 int gs_count_visible(const uint8_t* mask, const int32_t* radii, int64_t n, int32_t* count_out,
                      void* ws, size_t ws_bytes, void* stream);
 
+/* Copy up to two small device buffers (4-byte multiples, <= 4 KB each; a
+ * size of 0 skips one) into page-locked host memory through mapped
+ * pointers, with one small kernel in the stream: the step statistics and
+ * the strict abort flag for an asynchronous error check (the reference
+ * raises in step(), optimizer.py:181-184; the optimizer reads the copies
+ * once the stream has passed them).  No reference counterpart. */
+int gs_mirror_to_host(const void* src0, void* dst0_host, size_t bytes0, const void* src1,
+                      void* dst1_host, size_t bytes1, void* stream);
+
 /* GS_BUILD_FLAG_* bits of this build. */
 int32_t gs_build_flags(void);
 int gs_stats_all_rows(const gs_group* groups, int32_t n_groups, int64_t n_rows,

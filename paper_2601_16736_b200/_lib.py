@@ -96,6 +96,8 @@ SIGNATURES = {
                                    C.c_void_p, C.c_void_p]),
     "gs_step_rows_workspace_bytes": (C.c_size_t, []),
     "gs_step_rows_masked_workspace_bytes": (C.c_size_t, [C.c_int64]),
+    "gs_mirror_to_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p,
+                                    C.c_size_t, C.c_void_p]),
     "gs_set_rows_variant": (C.c_int32, [C.c_int32]),
     "gs_set_fixed_variant": (C.c_int32, [C.c_int32]),
     "gs_step_rows": (C.c_int, [C.POINTER(GsGroup), C.c_int32, C.POINTER(GsStepCfg), C.c_void_p,

@@ -76,3 +76,36 @@ extern "C" int gs_host_device_pointer(const void* host_ptr, void** dev_ptr) {
   *dev_ptr = d;
   return GS_OK;
 }
+
+// The step statistics (and the strict abort flag) into page-locked host
+// memory for the asynchronous error check: one warp stores them through the
+// mapped pointers, a few hundred ns in the stream instead of a copy-engine
+// transfer (a D2H cudaMemcpyAsync between two small steps costs the stream
+// ~15-20 us, profiles/r02/small_clouds.txt).
+static __global__ void mirror_kernel(const uint32_t* __restrict__ s0, uint32_t* d0, int n0,
+                                     const uint32_t* __restrict__ s1, uint32_t* d1, int n1) {
+  for (int i = threadIdx.x; i < n0; i += 32) d0[i] = s0[i];
+  for (int i = threadIdx.x; i < n1; i += 32) d1[i] = s1[i];
+}
+
+extern "C" int gs_mirror_to_host(const void* src0, void* dst0_host, size_t bytes0,
+                                 const void* src1, void* dst1_host, size_t bytes1, void* stream) {
+  if ((bytes0 && (!src0 || !dst0_host)) || (bytes1 && (!src1 || !dst1_host)) || bytes0 % 4 ||
+      bytes1 % 4 || bytes0 > 4096 || bytes1 > 4096) {
+    gs_set_error("gs_mirror_to_host: invalid arguments");
+    return GS_ERR_ARG;
+  }
+  void* d0 = nullptr;
+  void* d1 = nullptr;
+  if (bytes0 && cudaHostGetDevicePointer(&d0, dst0_host, 0) != cudaSuccess) d0 = nullptr;
+  if (bytes1 && cudaHostGetDevicePointer(&d1, dst1_host, 0) != cudaSuccess) d1 = nullptr;
+  if ((bytes0 && !d0) || (bytes1 && !d1)) {
+    (void)cudaGetLastError();
+    gs_set_error("gs_mirror_to_host: destination is not page-locked mapped host memory");
+    return GS_ERR_ARG;
+  }
+  mirror_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(
+      static_cast<const uint32_t*>(src0), static_cast<uint32_t*>(d0), (int)(bytes0 / 4),
+      static_cast<const uint32_t*>(src1), static_cast<uint32_t*>(d1), (int)(bytes1 / 4));
+  return gs_check_launch("gs_mirror_to_host");
+}

@@ -1,6 +1,7 @@
 // The SH-3 fast path: variant switch, dispatch over the step modes and the
 // C-ABI hook.  The kernels are in gs_step_sh3.cuh; each mode is instantiated
 // in its own translation unit (gs_step_sh3_m<mode>.cu).
+#include <cstring>
 #include "gs_step_sh3.cuh"
 
 namespace gs {
@@ -147,9 +148,36 @@ static bool encode_rows(CUtensorMap* m, const float* base, int64_t n_rows, int64
 }
 
 bool encode_tma_maps(const FixedParams& P, int64_t n_rows, int rec_box, TmaMaps* out) {
-  return encode_rows(&out->rec, P.record, n_rows, P.stride, rec_box) &&
-         encode_rows(&out->prm, P.prec, n_rows, P.prs, Tma4Stage<LayoutSH3, 32>::kPT) &&
-         encode_rows(&out->grd, P.grec, n_rows, P.grs, Tma4Stage<LayoutSH3, 32>::kPT);
+  // the last encoding per host thread is reused when the records did not
+  // move (three cuTensorMapEncodeTiled calls cost a few us of the host's
+  // per-step time, which small clouds feel)
+  struct Key {
+    const void *rec, *prm, *grd;
+    int64_t n, st, ps, gs;
+    int box;
+    int dev;
+  };
+  static thread_local Key last{};
+  static thread_local TmaMaps cached;
+  static thread_local bool valid = false;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const Key k{P.record, P.prec, P.grec, n_rows, P.stride, (int64_t)P.prs, (int64_t)P.grs, rec_box,
+              dev};
+  if (valid && std::memcmp(&k, &last, sizeof(Key)) == 0) {
+    *out = cached;
+    return true;
+  }
+  valid = false;
+  const bool ok = encode_rows(&out->rec, P.record, n_rows, P.stride, rec_box) &&
+                  encode_rows(&out->prm, P.prec, n_rows, P.prs, Tma4Stage<LayoutSH3, 32>::kPT) &&
+                  encode_rows(&out->grd, P.grec, n_rows, P.grs, Tma4Stage<LayoutSH3, 32>::kPT);
+  if (ok) {
+    last = k;
+    cached = *out;
+    valid = true;
+  }
+  return ok;
 }
 
 template <class L>

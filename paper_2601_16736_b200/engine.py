@@ -9,6 +9,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -109,9 +110,17 @@ def _strides(t: torch.Tensor | None):
 
 _raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
 # NVTX ranges around the kernel launches (K1 compaction, K2 step, K3 state
-# scatters, K4 statistics) for nsys / ncu --nvtx; host cost ~1 us per range
-_nvtx_push = torch.cuda.nvtx.range_push
-_nvtx_pop = torch.cuda.nvtx.range_pop
+# scatters, K4 statistics) for nsys / ncu --nvtx, with GS_NVTX=1 (host cost
+# ~1 us per range, which small clouds' eager steps feel)
+if os.environ.get("GS_NVTX", "0") not in ("", "0"):
+    _nvtx_push = torch.cuda.nvtx.range_push
+    _nvtx_pop = torch.cuda.nvtx.range_pop
+else:
+    def _nvtx_push(name):
+        pass
+
+    def _nvtx_pop():
+        pass
 
 
 def _stream_handle(device: torch.device) -> int:
@@ -238,9 +247,18 @@ class StepEngine:
 
     # ------------------------------------------------------------------ groups
     def group_array(self, groups: list[GroupBinding], need_grad: bool = True):
-        key = tuple((g.role, float(g.lr), _ptr(g.param), _ptr(g.grad), _ptr(g.exp_avg),
-                     _ptr(g.exp_avg_sq), _strides(g.param), _strides(g.grad),
-                     None if g.grad is None else g.grad.device.type) for g in groups)
+        # cache key: pointers and row strides (every step rebuilds the
+        # bindings; the array is rebuilt only when a tensor moved)
+        key = [need_grad]
+        for g in groups:
+            p, gr = g.param, g.grad
+            key += (g.role, g.lr, p.data_ptr() if p is not None else 0,
+                    p.stride() if p is not None else None,
+                    gr.data_ptr() if gr is not None else 0,
+                    gr.stride() if gr is not None else None,
+                    gr.is_cuda if gr is not None else None,
+                    g.exp_avg.data_ptr() if g.exp_avg is not None else 0,
+                    g.exp_avg_sq.data_ptr() if g.exp_avg_sq is not None else 0)
         if key == self._group_cache_key:
             return self._group_cache
         if not 1 <= len(groups) <= L.GS_MAX_GROUPS:
@@ -566,8 +584,8 @@ class StepEngine:
         self.launches += 1
 
     def _check_record(self, record: torch.Tensor, groups):
-        key = (record.data_ptr(), tuple(record.shape), record.stride(), record.dtype,
-               tuple(g.width for g in groups))
+        key = (record.data_ptr(), record.shape, record.stride(), record.dtype,
+               tuple(g.param.shape if g.param is not None else g.w for g in groups))
         if key == self._record_ok:
             return
         p = sum(g.width for g in groups)

@@ -25,8 +25,8 @@ from . import _lib as L
 from . import records as _records
 from .records import base_grad_view
 from .sampling import device_bernoulli
-from .engine import (ConfigError, DomainError, GradientError, GroupBinding, StepEngine, row_stride,
-                     round_pixel_count)
+from .engine import (ConfigError, DomainError, GradientError, GroupBinding, StepEngine,
+                     _stream_handle, round_pixel_count, row_stride)
 
 MODES = ("coupled-adam", "sparse-adam", "adamw-const", "adamw-const-clip", "adamw-gs")
 CHECKS = ("fused", "strict")
@@ -288,6 +288,9 @@ class AdamWGS:
                         torch.zeros(1, dtype=torch.int32, pin_memory=True))
                        for _ in range(self.ERROR_SLOTS)]
         self._slot = 0
+        self._slot_events = [torch.cuda.Event() for _ in range(self.ERROR_SLOTS)]
+        self._dev_index = self.device.index if self.device.index is not None else \
+            torch.cuda.current_device()
         self._pending = collections.deque()
         self._capturing = False
         self._last_ctx = None
@@ -523,13 +526,24 @@ class AdamWGS:
         if len(self._pending) >= self.ERROR_SLOTS:
             self._poll(block=True, limit=1)
         st_host, ab_host = self._slots[self._slot]
+        # the slot's event is free: at most ERROR_SLOTS checks are pending
+        ev = self._slot_events[self._slot]
         self._slot = (self._slot + 1) % self.ERROR_SLOTS
-        st_host.copy_(self.engine.stats, non_blocking=True)
         strict = self.check == "strict"
-        if strict:
-            ab_host.copy_(self.engine.abort, non_blocking=True)
-        ev = torch.cuda.Event()
-        ev.record(torch.cuda.current_stream(self.device))
+        eng = self.engine
+        # one small kernel stores the statistics (and the abort flag) into the
+        # pinned slot through its mapped pointer (no copy-engine transfer)
+        L.check(eng.lib.gs_mirror_to_host(eng.stats.data_ptr(), st_host.data_ptr(),
+                                          eng.stats.numel() * 8,
+                                          eng.abort.data_ptr() if strict else None,
+                                          ab_host.data_ptr() if strict else None,
+                                          4 if strict else 0, _stream_handle(self.device)),
+                "gs_mirror_to_host")
+        # the engine launched on the current stream of the optimizer's device
+        if torch.cuda.current_device() == self._dev_index:
+            ev.record()
+        else:
+            ev.record(torch.cuda.current_stream(self._dev_index))
         self._pending.append((ev, st_host, ab_host if strict else None, self._last_ctx))
         if self.errors == "raise":
             self._poll(block=True)
@@ -545,8 +559,16 @@ class AdamWGS:
             _, st_host, ab_host, ctx = self._pending.popleft()
             ev.synchronize()
             n += 1
-            self._raise_for(_stats_dict(st_host.tolist()),
-                            int(ab_host.item()) if ab_host is not None else 0, ctx)
+            vals = st_host.tolist()
+            flag = int(ab_host.item()) if ab_host is not None else 0
+            if flag == 0 and vals[2] == 0.0 and vals[3] == 0.0:
+                # no bad rows: only the layout hints (the common case, cheap)
+                if self.n_rows:
+                    self._vis_frac = vals[0] / self.n_rows
+                if vals[10] > 0:
+                    self._vis_run = vals[0] / vals[10]
+                continue
+            self._raise_for(_stats_dict(vals), flag, ctx)
 
     def _raise_pending(self):
         self._poll(block=True)
