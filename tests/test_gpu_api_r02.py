@@ -69,6 +69,33 @@ def test_default_step_never_waits_for_the_gpu():
     opt.check_errors()
 
 
+def test_mirror_to_host_stores_through_mapped_pointers():
+    """gs_mirror_to_host (the deferred check's statistics store): both
+    buffers land in pinned host memory in stream order; a pageable or
+    unaligned destination is refused with an error, not written."""
+    from paper_2601_16736_b200 import _lib as L
+    lib = L.load()
+    src0 = torch.arange(11, dtype=torch.float64, device=DEV) * 1.5
+    src1 = torch.tensor([7], dtype=torch.int32, device=DEV)
+    dst0 = torch.zeros(11, dtype=torch.float64, pin_memory=True)
+    dst1 = torch.zeros(1, dtype=torch.int32, pin_memory=True)
+    s = torch.cuda.current_stream().cuda_stream
+    assert lib.gs_mirror_to_host(src0.data_ptr(), dst0.data_ptr(), 88, src1.data_ptr(),
+                                 dst1.data_ptr(), 4, s) == 0
+    torch.cuda.synchronize()
+    assert dst0.tolist() == src0.tolist() and int(dst1.item()) == 7
+    # one buffer only (the fused check has no abort flag)
+    src0.mul_(2.0)
+    assert lib.gs_mirror_to_host(src0.data_ptr(), dst0.data_ptr(), 88, None, None, 0, s) == 0
+    torch.cuda.synchronize()
+    assert dst0.tolist() == src0.tolist()
+    pageable = torch.zeros(11, dtype=torch.float64)
+    assert lib.gs_mirror_to_host(src0.data_ptr(), pageable.data_ptr(), 88, None, None, 0, s) != 0
+    assert b"page-locked" in lib.gs_last_error()
+    assert lib.gs_mirror_to_host(src0.data_ptr(), dst0.data_ptr(), 6, None, None, 0, s) != 0
+    assert pageable.abs().sum().item() == 0
+
+
 def test_deferred_error_surfaces_at_check_with_ids():
     """A non-finite gradient under errors="defer": the step returns, the
     error (with the reference's row ids, gradients.py:50-58) surfaces at
