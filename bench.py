@@ -630,6 +630,11 @@ def run_workload(args, wl, p_vis, rank, world, dev, *, strong, mask, steps, warm
     w = Workload(args, wl, p_vis, rank, world, dev, strong, mask, steps, warmup)
     for it in range(w.warmup):
         w.one_step(it)
+    # untimed: every replica steps at least once (small clouds rotate up to
+    # 64 replicas), so the statistics its layout hints come from exist
+    for j in range(w.warmup, w.n_rep):
+        opt, sh, grads = w.opts[j], w.shards[j], w.grad_sets[j][0]
+        (sh if sh is not None else opt).step(w.masks[j % len(w.masks)], 1_000_000, grads=grads)
     torch.cuda.synchronize()
     for o in w.opts:
         o.last_stats()  # the visible fraction the optimizer picks its kernel shape by

@@ -723,7 +723,8 @@ class AdamWGS:
     def last_stats(self) -> dict:
         """Per-step statistics of the last step (host sync)."""
         st = _stats_dict(self.engine.stats.tolist())
-        self._note_layout(st)
+        if self.engine.launches:  # zeros before the first step are no layout hint
+            self._note_layout(st)
         return st
 
     # ----------------------------------------------- densification statistics
