@@ -16,22 +16,21 @@ from paper_2601_16736_b200.optimizer import AdamWGS  # noqa: E402
 
 
 def main(n, kind, mode, p):
-    dev = "cuda:0"
+    dev = torch.device("cuda:0")
     cfg = S.WorkloadConfig(n=n, p_vis=p, seed=n % 97 + 1)
-    host = S.make_params(cfg)
+    base = S.make_params_device(cfg, dev)  # device-generated: big clouds in seconds
     outs = []
     for fused in (True, False):
-        _, params = R.pack({k: torch.from_numpy(v).to(dev) for k, v in host.items()})
+        _, params = R.pack({k: v.clone() for k, v in base.items()})
         lo, ls = (1e-3, 1e-5)
         opt = AdamWGS(S.param_groups(params), mode=mode, lambda_o=lo, lambda_s=ls,
                       fused_compaction=fused)
         stats = []
         for s in range(2):
-            vis = S.visibility(cfg, s)
-            m = (torch.from_numpy(np.where(vis, np.arange(n) % 7 + 1, 0).astype(np.int32))
-                 if kind == "radii" else torch.from_numpy(vis)).to(dev)
-            _, g = R.pack({k: torch.from_numpy(x).to(dev)
-                           for k, x in S.step_grads(cfg, s, vis).items()})
+            vis = S.visibility_device(cfg, s, dev)
+            m = (torch.where(vis, torch.arange(n, device=dev, dtype=torch.int32) % 7 + 1, 0)
+                 .to(torch.int32).contiguous() if kind == "radii" else vis)
+            _, g = R.pack(S.grads_device(cfg, s, dev, vis))
             opt.step(m, cfg.n_pixels, grads=g)
             assert (opt._last_ctx[1] is None) == fused, "path"
             stats.append(opt.last_stats())
