@@ -4,7 +4,12 @@
 // moment records (included by gs_step_sh3.cuh).
 //
 // A CTA walks chunks of 32 visible rows through an S-stage shared-memory
-// ring (3 stages, 2 CTAs per SM by default).  Warp roles:
+// ring (3 stages, 2 CTAs per SM by default; 2 stages, 3 CTAs per SM for
+// sparse masks on big clouds).  Where the chunks come from (MASK, below):
+// an index list (dealt grid-stride, the last round split evenly), a mask
+// streamed through the loader (1-KB tiles grid-stride with an optional
+// dynamic tail, or per-CTA slices on small clouds), or a mask compacted in
+// two phases around a grid barrier.  Warp roles:
 //   loader  (warp NCW)     per chunk, lanes 0..7 each issue three gather4
 //                          operations (4 rows each) for the moment records
 //                          (480 B of every 512-B row), the parameter rows and
@@ -19,6 +24,10 @@
 //                          moment records back, wait until the bulk stores
 //                          have read the stage, and hand it back to the
 //                          loader ("empty" mbarrier).
+//   bias    (warp NCW+2, BW only)  turns the landed clocks into bias factors,
+//                          so the loader only scans masks and issues copies.
+// The statistics: per-thread counters and sums, a block tree, per-CTA
+// partials and a last-CTA fold in CTA order (deterministic).
 // Rows past the end of the index list get row id n_rows: the gathers fill
 // them with zeros and the scatters drop them (out of the tensor's bounds).
 // A skipped (bad) row is left unchanged in the stage, so its scatter writes
